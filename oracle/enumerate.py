@@ -1,0 +1,178 @@
+"""Brute-force row-dependency enumerator -- TEST INFRASTRUCTURE ONLY.
+
+Explicit row SETS (no closed forms) for the band/halo structure of
+row-centric training.  It is the reference the planner's interval rule
+ must match bit-exactly.
+
+Definitions (PAPER.md:150 "Receptive Field", :153 row split, :287 2PS,
+:330 OverL):
+  * rf(op, rows_out)  = set of rows of each input read by output rows rows_out
+                        (row y reads y*s-p+ky, ky<k, inside [0,H_in); padding rows are
+                        not data).
+  * need_r(t)          = rows of t transitively needed by the segment output rows [0, E_r).
+  * 2PS band r computes rows [e_{r-1}(t), e_r(t)) of t with e_r(t) = max(need_r(t))+1
+    (the interval hull from row 0), e_N(t) = H_t; its band buffer also holds the
+    cached rows [lo_r(t), e_{r-1}(t)) where lo_r(t) = min(rows of t read while
+    computing band r's rows of every consumer, e_{r-1}(t)).
+  * OverL band r computes the hull [lo, hi) of rows transitively needed by
+    the owned output rows [E_{r-1}, E_r).
+Segments (2PS-H / OverL-H): a seg_end op's output is a
+checkpoint; each segment is enumerated from its own input.
+"""
+from oracle.column import out_hw
+
+
+def segments(net):
+    """List of (in_tid, [op ids], out_tid); boundaries after ops with seg_end."""
+    segs, cur, seg_in = [], [], 0
+    ops = net["ops"]
+    for i, op in enumerate(ops):
+        cur.append(i)
+        if op.get("seg_end") or i == len(ops) - 1:
+            segs.append((seg_in, cur, i + 1))
+            seg_in, cur = i + 1, []
+    for seg_in, ids, out in segs:
+        inside = {seg_in} | {i + 1 for i in ids}
+        for i in ids:
+            for key in ("src", "res"):
+                t = ops[i].get(key, -1)
+                if t is not None and t >= 0 and t not in inside:
+                    raise ValueError("op %d reads tensor %d across a checkpoint boundary" % (i, t))
+    return segs
+
+
+def band_ends(h_out, band_rows=None, n_bands=None):
+    """Band ends E_1<..<E_N=h_out at a segment output.
+    band_rows: every band owns band_rows rows, the remainder goes to the last band.
+    n_bands: near-equal split, the earliest bands take one extra row."""
+    if band_rows is not None:
+        E = list(range(band_rows, h_out, band_rows)) + [h_out]
+        return E
+    n = min(n_bands, h_out)
+    q, rem = divmod(h_out, n)
+    E, acc = [], 0
+    for r in range(n):
+        acc += q + (1 if r < rem else 0)
+        E.append(acc)
+    return E
+
+
+def _inputs(op):
+    ins = [op["src"]]
+    if op.get("res", -1) is not None and op.get("res", -1) >= 0:
+        ins.append(op["res"])
+    return ins
+
+
+def rf(op, rows_out, h_in):
+    """Rows of an input read by the given output rows (explicit set enumeration)."""
+    if op["kind"] == "add":
+        return {y for y in rows_out if 0 <= y < h_in}
+    k, s, p = op["k"], op["s"], op["p"]
+    got = set()
+    for y in rows_out:
+        for ky in range(k):
+            r = y * s - p + ky
+            if 0 <= r < h_in:
+                got.add(r)
+    return got
+
+
+def rf_of(op, tin, rows_out, h_in):
+    """RF rows of input tensor tin for op (residual inputs are read 1:1)."""
+    if op["kind"] == "conv" and tin == op.get("res", -1) and tin != op["src"]:
+        return {y for y in rows_out if 0 <= y < h_in}
+    return rf(op, rows_out, h_in)
+
+
+def need_sets(net, shp, seg, out_rows):
+    """Rows of every tensor of the segment transitively needed by out_rows of its output."""
+    seg_in, ids, out = seg
+    need = {out: set(out_rows)}
+    for i in reversed(ids):
+        op = net["ops"][i]
+        rows = need.get(i + 1, set())
+        for tin in set(_inputs(op)):
+            need.setdefault(tin, set())
+            need[tin] |= rf_of(op, tin, rows, shp[tin][1])
+    return need
+
+
+def enumerate_2ps(net, seg, E, shp=None):
+    """Per band r and tensor t of the segment: (lo, a, b) with computed rows [a, b)
+    and buffer rows [lo, b) (cache rows [lo, a)).  The segment input is full width."""
+    shp = shp or out_hw(net)
+    seg_in, ids, out = seg
+    tensors = [i + 1 for i in ids]
+    N = len(E)
+    ends = []
+    for r in range(N):
+        need = need_sets(net, shp, seg, range(0, E[r]))
+        e = {}
+        for t in tensors:
+            nt = need.get(t, set())
+            e[t] = (max(nt) + 1) if nt else 0
+            if r == N - 1:
+                e[t] = shp[t][1]
+        ends.append(e)
+    res = []
+    for r in range(N):
+        band = {}
+        for t in tensors:
+            a = ends[r - 1][t] if r > 0 else 0
+            band[t] = [a, a, ends[r][t]]
+        # rows of each tensor read while computing band r's rows of its consumers
+        for i in ids:
+            op = net["ops"][i]
+            _, a, b = band[i + 1]
+            for tin in set(_inputs(op)):
+                if tin == seg_in:
+                    continue
+                got = rf_of(op, tin, range(a, b), shp[tin][1])
+                if got:
+                    band[tin][0] = min(band[tin][0], min(got))
+        res.append({t: tuple(v) for t, v in band.items()})
+    return res
+
+
+def enumerate_overl(net, seg, E, shp=None):
+    """Per band r and tensor t: (lo, hi) hull of rows needed by owned output rows [E_{r-1}, E_r)."""
+    shp = shp or out_hw(net)
+    seg_in, ids, out = seg
+    res = []
+    for r in range(len(E)):
+        a = E[r - 1] if r > 0 else 0
+        need = need_sets(net, shp, seg, range(a, E[r]))
+        band = {}
+        for t in [seg_in] + [i + 1 for i in ids]:
+            nt = need.get(t, set())
+            band[t] = (min(nt), max(nt) + 1) if nt else (0, 0)
+        res.append(band)
+    return res
+
+
+def forward_split(chain, h0, in_ends):
+    """Input-specified ("skewed initial partitioning") mode for a chain of convs, PAPER.md:287,
+    Fig. 4: given input band ends, each band computes every output row whose RF lies in the rows
+    available so far (2PS shares the earlier rows).  Returns per-layer band sizes."""
+    sizes = []
+    h = h0
+    ends = list(in_ends)
+    sizes.append([ends[0]] + [ends[i] - ends[i - 1] for i in range(1, len(ends))])
+    for (k, s, p) in chain:
+        h_out = (h + 2 * p - k) // s + 1
+        new = []
+        for r, e in enumerate(ends):
+            if r == len(ends) - 1:
+                new.append(h_out)
+                continue
+            # output rows y with all RF rows < e (rows >= h are padding only at the very end)
+            cnt = 0
+            for y in range(h_out):
+                rows = [y * s - p + ky for ky in range(k)]
+                if all(rr < e for rr in rows):
+                    cnt = y + 1
+            new.append(cnt)
+        ends, h = new, h_out
+        sizes.append([ends[0]] + [ends[i] - ends[i - 1] for i in range(1, len(ends))])
+    return sizes
