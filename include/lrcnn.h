@@ -1,0 +1,213 @@
+/*
+ * lrcnn.h -- C-ABI of the B200-native LR-CNN hot path (arXiv 2401.11471).
+ *
+ * Row-centric training of a stack (DAG) of convolution layers: the forward
+ * pass (FP) sweeps horizontal bands of rows through every layer of a segment
+ * (Alg. 1 l.5-10, Eq. (4)); the backward
+ * pass (BP) walks the bands in reverse, recomputes each band (Alg. 1 l.17)
+ * and produces dgrad and wgrad with wgrad accumulated across bands
+ * (Eq. (5), Alg. 1 l.18-20).  Both of the paper's answers to
+ * the inter-row weak dependency are provided: two-phase sharing (2PS, cache the
+ * halo rows) and overlapping partitioning (OverL, recompute
+ * the overlap); "seg_end" checkpoints give the -H hybrids
+ * (PAPER.md:322, 394).
+ *
+ * Conventions for every entry point
+ *   - Plain C types and pointers only; no exceptions cross the ABI.
+ *   - Every function returns an lrcnn_status; LRCNN_OK == 0.  On error a
+ *     message is available from lrcnn_last_error() (thread-local, valid until
+ *     the next call on the same thread).
+ *   - Shape/feasibility errors are reported synchronously by lrcnn_plan.
+ *   - Device work is enqueued asynchronously on the caller's stream (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream).  Launch
+ *     errors are reported as LRCNN_E_CUDA by the call that enqueued them;
+ *     asynchronous faults surface at the caller's next synchronisation.
+ *   - The caller owns every device buffer (allocated e.g. by PyTorch).  The
+ *     library owns only the host-side plan.  Nothing is allocated on the device
+ *     inside forward/backward/step, so the peak HBM is the caller's
+ *     allocations (visible to torch.cuda.max_memory_allocated).
+ *
+ * Device data layouts (all row-major, C-contiguous)
+ *   - Activations: NHWC, channels padded to Cp = round_up(C, 8) (16-byte
+ *     rows for the tensor-core path).  Padded channels must be zero.
+ *   - Element type: float (LRCNN_FP32) or bfloat16 (LRCNN_BF16) -- "act_t".
+ *   - Parameters: one flat array laid out by the plan (lrcnn_plan_param):
+ *     per conv op w[C_out][k][k][Cp_in] (OHWI), then bias[C_out] (EPI_BIAS) or
+ *     gamma[C_out], beta[C_out] (EPI_AFFINE); then the head fc_w[classes][C_L],
+ *     fc_b[classes].  Device copies in act_t ("params"), an fp32 master copy
+ *     ("master") and fp32 gradients ("grads") share these offsets.
+ */
+#ifndef LRCNN_H
+#define LRCNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LRCNN_API __attribute__((visibility("default")))
+#else
+#define LRCNN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LRCNN_OK = 0,
+    LRCNN_E_ARG = 1,          /* NULL pointer, out-of-range index or enum           */
+    LRCNN_E_SHAPE = 2,        /* invalid shape, kernel exceeds input  */
+    LRCNN_E_INFEASIBLE = 3,   /* OverL N > H/o^0                  */
+    LRCNN_E_DEGENERATE = 4,   /* band ends not strictly increasing at a segment out  */
+    LRCNN_E_STATE = 5,        /* backward without forward, plan/buffer mismatch      */
+    LRCNN_E_WORKSPACE = 6,    /* workspace NULL or too small                         */
+    LRCNN_E_CUDA = 7,         /* a CUDA runtime/driver call failed                   */
+    LRCNN_E_NCCL = 8,         /* reserved for the multi-GPU exchange                 */
+    LRCNN_E_UNSUPPORTED = 9   /* valid request this build does not implement        */
+} lrcnn_status;
+
+typedef enum { LRCNN_COLUMN = 0, LRCNN_2PS = 1, LRCNN_OVERL = 2 } lrcnn_mode;
+typedef enum { LRCNN_FP32 = 0, LRCNN_BF16 = 1 } lrcnn_precision;
+enum { LRCNN_OP_CONV = 0, LRCNN_OP_MAXPOOL = 1, LRCNN_OP_ADD = 2 };
+enum { LRCNN_EPI_NONE = 0, LRCNN_EPI_BIAS = 1, LRCNN_EPI_AFFINE = 2 };
+
+/* One op of the DAG.  Tensor ids: 0 = the image, op i produces tensor i+1.
+ *   CONV:    t = relu?( epi(Conv_{k,s,p}(t_src)) + t_res )      (Eq. (1))
+ *            epi: BIAS  -> + b[co];  AFFINE -> gamma[co]*c + beta[co] (frozen-statistics BN)
+ *   MAXPOOL: t = max over k x k windows, stride s, pad p (pads never win, ties -> lowest index)
+ *   ADD:     t = relu?( t_src + t_res )
+ * seg_end != 0 stores the op's output as a full-width checkpoint (segment boundary). */
+typedef struct {
+    int kind;
+    int src;
+    int res;          /* residual/second input tensor id, -1 = none */
+    int c_out;        /* CONV only */
+    int k, s, p;      /* CONV / MAXPOOL */
+    int epi;          /* CONV only */
+    int relu;
+    int seg_end;
+} lrcnn_op;
+
+typedef struct {
+    int n_ops;
+    const lrcnn_op *ops;
+    int B, C, H, W;   /* batch and image shape (C = real channels, padded to Cp on device) */
+    int n_classes;    /* head: GAP -> FC(C_L -> n_classes) -> softmax-CE (mean over B) */
+} lrcnn_net_desc;
+
+typedef struct {
+    int mode;         /* lrcnn_mode.  COLUMN = layer-wise baseline: one segment, one band,
+                         every feature map kept, no recompute */
+    int prec;         /* lrcnn_precision */
+    int band_rows;    /* >0: owned rows of each segment output per band, remainder to the
+                         last band (reading R15) */
+    int n_bands;      /* used when band_rows <= 0: near-equal split, earliest bands +1 row */
+    int rank, world;  /* row sharding across GPUs (world == 1 in this build) */
+    int flags;        /* LRCNN_FLAG_* */
+} lrcnn_plan_opts;
+
+#define LRCNN_FLAG_ALLOW_OVERLAP_EXHAUSTION 1  /* OverL: do not reject N > H/o^0 */
+#define LRCNN_FLAG_NO_TCGEN05 2                /* bf16: use the SIMT kernels only (tests)     */
+
+typedef struct lrcnn_plan_t lrcnn_plan_t;
+
+/* Predicted memory of a plan, in bytes (host-side accounting). */
+typedef struct {
+    size_t omega;          /* Eq. (3): sum over all op outputs of B*H*W*C*elem (layer-wise)  */
+    size_t band_act;       /* band activation buffers (Eq. (8) working set)                  */
+    size_t band_delta;     /* band delta buffers                                             */
+    size_t halo_cache;     /* 2PS cache, B(N-1) sum c(t) W C elem (reading R9)  */
+    size_t carry;          /* 2PS delta carry buffers                                        */
+    size_t checkpoints;    /* full-width segment boundary maps           */
+    size_t delta_full;     /* full-width delta ping-pong for segment boundaries              */
+    size_t other;          /* head scratch, transposed weights, counters                      */
+    size_t workspace;      /* total workspace bytes (everything above but omega)              */
+    double tau_flops;      /* PAPER.md:375 tau for the whole batch                           */
+    double fwd_flops;      /* conv FLOPs one forward sweep executes (tau + iota for OverL)    */
+    double step_flops;     /* conv FLOPs one lrcnn_step executes (FP + recompute + 2 BP GEMMs)*/
+} lrcnn_memory_report;
+
+/* Build a plan (host only, synchronous, no device calls).  Validates the DAG
+ * (topological order, channel/shape propagation by floor((H+2p-k)/s)+1,
+ * SURVEY R1), splits segments, applies the interval rule for 2PS / the
+ * extended-range rule for OverL (R3/R4) and lays out the workspace.
+ * *out receives a plan owned by the caller, released with lrcnn_plan_free. */
+LRCNN_API lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, lrcnn_plan_t **out);
+LRCNN_API lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan);
+
+/* Sizes the caller must allocate: workspace bytes, number of parameters (flat
+ * element count of params/master/grads), z^L elements (B*H_L*W_L*Cp_L). */
+LRCNN_API lrcnn_status lrcnn_plan_sizes(const lrcnn_plan_t *plan, size_t *workspace_bytes, size_t *n_params,
+                              size_t *zl_elems);
+
+/* Shape of tensor `tid`: channels, padded channels, height, width. */
+LRCNN_API lrcnn_status lrcnn_plan_tensor(const lrcnn_plan_t *plan, int tid, int *C, int *Cp, int *H, int *W);
+
+/* Offset/count (elements) of a parameter block in the flat layout.
+ * op in [0, n_ops): which 0 = w, 1 = bias or gamma, 2 = beta.
+ * op == n_ops (head): which 0 = fc_w, 1 = fc_b.  count = 0 if absent. */
+LRCNN_API lrcnn_status lrcnn_plan_param(const lrcnn_plan_t *plan, int op, int which, size_t *offset, size_t *count);
+
+/* Segment structure: number of segments; per segment its input/output tensor ids and bands. */
+LRCNN_API lrcnn_status lrcnn_plan_nsegs(const lrcnn_plan_t *plan, int *n_segs);
+LRCNN_API lrcnn_status lrcnn_plan_seg(const lrcnn_plan_t *plan, int seg, int *in_tid, int *out_tid, int *n_bands);
+
+/* Rows of tensor `tid` in band `band` of segment `seg` (bit-exact contract, R3/R4):
+ * the band computes rows [*a, *b) and its buffer holds rows [*lo, *b); rows [*lo, *a) are
+ * 2PS cache rows (lo == a for OverL / COLUMN).  LRCNN_E_ARG if tid is not in the segment. */
+LRCNN_API lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int band, int tid, int *lo, int *a, int *b);
+
+LRCNN_API lrcnn_status lrcnn_plan_memory(const lrcnn_plan_t *plan, lrcnn_memory_report *rep);
+
+/* FP (Alg. 1 l.5-11): computes z^L [B][H_L][W_L][Cp_L] (act_t) from x [B][H][W][Cp] (act_t)
+ * and params (act_t, plan layout).  Leaves the 2PS halo cache and the checkpoints in ws for
+ * a following lrcnn_backward_rows with the same params/x (two-phase sharing). */
+LRCNN_API lrcnn_status lrcnn_forward_rows(lrcnn_plan_t *plan, const void *params, const void *x, void *zl,
+                                void *ws, size_t ws_bytes, void *stream);
+
+/* BP (Alg. 1 l.15-23): from dz^L (act_t, z^L layout) ACCUMULATES the gradient of every
+ * parameter into grads (fp32, plan layout; head entries untouched).  zl is the z^L the
+ * matching forward produced (read for the last op's ReLU gate and affine gradient).
+ * Requires a preceding lrcnn_forward_rows on the same plan, params, x and ws (else
+ * LRCNN_E_STATE): the 2PS halo cache and checkpoints it left in ws are consumed. */
+LRCNN_API lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const void *x, const void *zl,
+                                 const void *dzl, float *grads, void *ws, size_t ws_bytes, void *stream);
+
+/* One training iteration (Alg. 1 l.5-24): FP, head (GAP->FC->softmax-CE mean),
+ * BP, then SGD theta <- theta - lr*g on master (fp32), refresh params (act_t) from master and
+ * zero grads.  grads must be zero on entry.  labels: int32 [B] on device.
+ * loss_dev: one float on device receiving the mean loss of this iteration. */
+LRCNN_API lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
+                        const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes,
+                        void *stream);
+
+/* The two halves of lrcnn_step, for data-parallel training where the caller reduces the
+ * gradients across ranks in between (e.g. an NCCL all-reduce of `grads`, PAPER.md:577 DP):
+ *   lrcnn_step_grads: FP + head + BP; grads (zero on entry) receive this rank's gradient,
+ *                     loss_dev this rank's mean loss.
+ *   lrcnn_sgd:        master -= lr * grads; params = act_t(master); grads = 0. */
+LRCNN_API lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *grads, const void *x,
+                                        const int32_t *labels, float *loss_dev, void *ws, size_t ws_bytes,
+                                        void *stream);
+LRCNN_API lrcnn_status lrcnn_sgd(lrcnn_plan_t *plan, float *master, void *params, float *grads, float lr,
+                                 void *stream);
+
+/* Kernel timing for the roofline (bench.py): when enabled, every conv-class launch is
+ * bracketed by CUDA events on the launching stream.  lrcnn_profile_read synchronises the
+ * stream and returns, for kernel class `cls` (0 = tensor-core conv FP/dgrad, 1 = wgrad,
+ * 2 = other), total milliseconds, launch count and algorithmic FLOPs since the last reset. */
+LRCNN_API lrcnn_status lrcnn_profile_enable(lrcnn_plan_t *plan, int enable);
+LRCNN_API lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long long *launches,
+                                double *flops, void *stream);
+LRCNN_API lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan);
+
+/* Number of kernel launches the last forward/backward/step enqueued. */
+LRCNN_API lrcnn_status lrcnn_last_launch_count(const lrcnn_plan_t *plan, long long *launches);
+
+LRCNN_API const char *lrcnn_last_error(void);
+LRCNN_API const char *lrcnn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRCNN_H */

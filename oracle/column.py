@@ -75,8 +75,30 @@ def conv_op_bwd(op, prm, x, c, t, dt, pads, in_hw):
     return dx, dres, g
 
 
-def forward(net, params, x):
-    """Column FP: returns (tensors list [t0..tL], aux) with every feature map kept."""
+def bf16_store(a):
+    """Round to the nearest bfloat16 (round-to-nearest-even), kept as float64.
+
+    Storage-precision model for bf16 parity (reading R17b): the kernel
+    stores every feature map in bf16 and takes its integer decisions (ReLU
+    masks, max-pool argmax) on the stored values; the oracle takes them in the
+    same precision by storing its fp64 results rounded the same way.  All
+    arithmetic stays fp64."""
+    f = np.ascontiguousarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64).reshape(np.shape(a))
+
+
+def fp32_store(a):
+    """Round to float32, kept as float64: the storage model for the fp32 parity mode
+    (max-pool argmax on near-ties and ReLU masks decided on fp32 values, R17b)."""
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def forward(net, params, x, store=None):
+    """Column FP: returns (tensors list [t0..tL], aux) with every feature map kept.
+    store: optional storage-rounding function applied to every op output (bf16 parity)."""
+    st = store or (lambda a: a)
     ts = [np.asarray(x, dtype=np.float64)]
     aux = []
     for i, op in enumerate(net["ops"]):
@@ -94,7 +116,7 @@ def forward(net, params, x):
             a = src + ts[op["res"]]
             t = np.maximum(a, 0.0) if op["relu"] else a
             aux.append(None)
-        ts.append(t)
+        ts.append(st(t))
     return ts, aux
 
 

@@ -1,0 +1,593 @@
+// engine.cu -- the band loops of Algorithm 1 and the C-ABI entry points.
+//
+// FP  (Alg. 1 l.5-11): per segment, bands r = 1..N; each op
+//     computes its band rows from the band buffers; 2PS restores the cached halo
+//     rows of band r-1 at the top of each buffer before the band and saves the
+//     rows band r+1 will read after it.
+// BP  (Alg. 1 l.15-23): per segment in reverse, bands
+//     r = N..1: recompute the band (l.17), then per op in reverse: bias/affine
+//     reduction, wgrad (+= into fp32 grads, l.20), dgrad into the input's band
+//     delta; 2PS carries the delta of cached rows to band r-1 (R6).
+// Every device operation is enqueued on the caller's stream; nothing is
+// allocated on the device.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+#include "tc.hpp"
+
+struct lrcnn_plan_t {
+    lrcnn::Plan P;
+};
+
+namespace lrcnn {
+
+static thread_local std::string g_err;
+static lrcnn_status fail(lrcnn_status s, const std::string &m) { g_err = m; return s; }
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess) return fail(LRCNN_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct Run {
+    Plan &P;
+    char *ws;
+    const char *params;
+    const void *x;
+    void *zl;
+    float *grads;
+    cudaStream_t st;
+    int prec;
+    size_t E;   // element bytes
+};
+
+static View full_view(void *p, const TensorInfo &t) {
+    View v;
+    v.p = p; v.base = 0; v.rows = t.H; v.H = t.H; v.W = t.W; v.Cp = t.Cp;
+    v.bs = (long long)t.H * t.W * t.Cp;
+    return v;
+}
+
+static View band_view(char *base_ptr, const TensorInfo &t, int lo, int b) {
+    View v;
+    v.p = base_ptr; v.base = lo; v.rows = b - lo; v.H = t.H; v.W = t.W; v.Cp = t.Cp;
+    v.bs = (long long)t.cap * t.W * t.Cp;
+    return v;
+}
+
+// restrict a view to rows [a, b) (rows outside read as zero / are not data)
+static View sub_rows(const View &v, int a, int b, size_t E) {
+    View s = v;
+    s.p = (char *)v.p + (size_t)(a - v.base) * v.W * v.Cp * E;
+    s.base = a; s.rows = b - a;
+    return s;
+}
+
+static void *ckpt_ptr(Run &R, int t) {
+    const TensorInfo &ti = R.P.t[t];
+    if (t == 0) return (void *)R.x;
+    if (ti.is_zl) return R.zl;
+    return R.ws + ti.ckpt_off;
+}
+
+// activation view of tensor t in band r of segment s
+static View act_view(Run &R, const Segment &S, int r, int t) {
+    const TensorInfo &ti = R.P.t[t];
+    if (t == S.in_t || t == S.out_t) return full_view(ckpt_ptr(R, t), ti);
+    return band_view(R.ws + ti.act_off, ti, S.lo[r][t], S.b[r][t]);
+}
+
+static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
+    const TensorInfo &ti = R.P.t[t];
+    int nseg = (int)R.P.seg.size();
+    if (t == S.out_t) return full_view(R.ws + R.P.dfull_off[s & 1], ti);
+    if (t == S.in_t) return full_view(t == 0 ? nullptr : R.ws + R.P.dfull_off[(s + 1) & 1], ti);
+    (void)nseg;
+    return band_view(R.ws + ti.dlt_off, ti, S.lo[r][t], S.b[r][t]);
+}
+
+static const void *prm(Run &R, size_t off) { return off == (size_t)-1 ? nullptr : R.params + off * R.E; }
+
+// ------------------------------------------------------------------ profiling
+struct ProfScope {
+    Run &R;
+    int cls;
+    double flops;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ProfScope(Run &r, int c, double f) : R(r), cls(c), flops(f) {
+        if (R.P.profiling) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, R.st);
+        }
+    }
+    ~ProfScope() {
+        if (R.P.profiling) {
+            cudaEventRecord(e1, R.st);
+            R.P.pending_events[cls].push_back({(void *)e0, (void *)e1});
+            R.P.pending_flops[cls].push_back(flops);
+        }
+    }
+};
+
+static double conv_flops(Plan &P, const OpInfo &o, int rows) {
+    return 2.0 * o.d.k * o.d.k * P.net.B * P.t[o.in_t].C * P.t[o.out_t].C * (double)rows * P.t[o.out_t].W;
+}
+
+// ------------------------------------------------------------------ op forward on band rows [a, b)
+static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
+    Plan &P = R.P;
+    const OpInfo &o = P.op[i];
+    const int t = o.out_t;
+    const int a = S.a[r][t], b = S.b[r][t];
+    if (b <= a) return LRCNN_OK;
+    View out = act_view(R, S, r, t);
+    View in = act_view(R, S, r, o.in_t);
+    if (o.d.kind == LRCNN_OP_CONV) {
+        ConvFwdArgs A;
+        A.in = in; A.out = out;
+        if (o.d.res >= 0) A.res = act_view(R, S, r, o.d.res);
+        A.w = prm(R, o.w_off);
+        A.b = o.b_cnt ? prm(R, o.b_off) : nullptr;
+        A.beta = o.beta_cnt ? prm(R, o.beta_off) : nullptr;
+        A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.epi = o.d.epi; A.relu = o.d.relu;
+        A.a = a; A.b_ = b; A.B = P.net.B;
+        ProfScope ps(R, 0, conv_flops(P, o, b - a));
+        ++P.launches;
+        if (P.use_tc && tc_conv_fwd(A, R.st)) { CK(cudaGetLastError()); return LRCNN_OK; }
+        CK(simt_conv_fwd(R.prec, A, R.st));
+    } else if (o.d.kind == LRCNN_OP_MAXPOOL) {
+        PoolArgs A;
+        A.in = in; A.out = out; A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.a = a; A.b = b; A.B = P.net.B;
+        ++P.launches;
+        ProfScope ps(R, 2, 0);
+        CK(simt_pool_fwd(R.prec, A, R.st));
+    } else {
+        EltArgs A;
+        A.x0 = in; A.x1 = act_view(R, S, r, o.d.res); A.out = out; A.relu = o.d.relu; A.a = a; A.b = b; A.B = P.net.B;
+        ++P.launches;
+        ProfScope ps(R, 2, 0);
+        CK(simt_add_fwd(R.prec, A, R.st));
+    }
+    return LRCNN_OK;
+}
+
+// copy rows between two views of the same tensor (B planes, pitched)
+static lrcnn_status copy_rows(Run &R, const TensorInfo &ti, void *dst, size_t dst_pitch_rows, const void *src,
+                              size_t src_pitch_rows, int rows) {
+    if (rows <= 0) return LRCNN_OK;
+    size_t rb = (size_t)ti.W * ti.Cp * R.E;
+    CK(cudaMemcpy2DAsync(dst, dst_pitch_rows * rb, src, src_pitch_rows * rb, rows * rb, R.P.net.B,
+                         cudaMemcpyDeviceToDevice, R.st));
+    return LRCNN_OK;
+}
+
+static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cache, bool skip_out) {
+    Plan &P = R.P;
+    lrcnn_status st;
+    // 2PS: restore the cached rows [lo_r, a_r) of every band tensor (saved by band r-1)
+    if (P.opts.mode == LRCNN_2PS && r > 0) {
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            const TensorInfo &ti = P.t[t];
+            int rows = S.a[r][t] - S.lo[r][t];
+            if (rows <= 0) continue;
+            // cache[r-1] holds rows [lo_r, b_{r-1}) == [lo_r, a_r)
+            if ((st = copy_rows(R, ti, R.ws + ti.act_off, ti.cap, R.ws + ti.cache_off[r - 1], ti.cache_rows[r - 1],
+                                rows)) != LRCNN_OK) return st;
+        }
+    }
+    for (int i : S.ops) {
+        if (skip_out && i + 1 == S.out_t) continue;
+        if ((st = op_forward(R, S, r, i)) != LRCNN_OK) return st;
+    }
+    if (save_cache && P.opts.mode == LRCNN_2PS && r + 1 < (int)S.E.size()) {
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            const TensorInfo &ti = P.t[t];
+            int rows = ti.cache_rows[r];
+            if (rows <= 0) continue;
+            size_t rb = (size_t)ti.W * ti.Cp * R.E;
+            const char *src = R.ws + ti.act_off + (size_t)(ti.cache_lo[r] - S.lo[r][t]) * rb;
+            if ((st = copy_rows(R, ti, R.ws + ti.cache_off[r], rows, src, ti.cap, rows)) != LRCNN_OK) return st;
+        }
+    }
+    return LRCNN_OK;
+}
+
+static lrcnn_status run_forward(Run &R) {
+    lrcnn_status st;
+    for (const Segment &S : R.P.seg)
+        for (int r = 0; r < (int)S.E.size(); ++r)
+            if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) return st;
+    return LRCNN_OK;
+}
+
+// ------------------------------------------------------------------ op backward on band rows [a, b)
+static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
+    Plan &P = R.P;
+    const OpInfo &o = P.op[i];
+    const int t = o.out_t;
+    const int a = S.a[r][t], b = S.b[r][t];
+    if (b <= a) return LRCNN_OK;
+    const int B = P.net.B;
+    View dy = sub_rows(dlt_view(R, S, s, r, t), a, b, R.E);      // complete, gated delta rows
+    const TensorInfo &tin = P.t[o.in_t];
+    const bool need_dx = o.in_t != 0;
+    if (o.d.kind == LRCNN_OP_CONV) {
+        float *g = R.grads;
+        if (o.d.epi != LRCNN_EPI_NONE) {
+            ParamGradArgs A;
+            A.dy = dy; A.t = act_view(R, S, r, t);
+            if (o.d.res >= 0) A.res = act_view(R, S, r, o.d.res);
+            A.gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
+            A.beta = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.beta_off) : nullptr;
+            A.db = g + o.b_off;
+            A.dbeta = o.d.epi == LRCNN_EPI_AFFINE ? g + o.beta_off : nullptr;
+            A.epi = o.d.epi; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
+            ++P.launches;
+            ProfScope ps(R, 2, 0);
+            CK(simt_param_grad(R.prec, A, R.st));
+        }
+        const void *gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
+        {
+            WgradArgs A;
+            A.dy = dy; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
+            A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
+            ++P.launches;
+            ProfScope ps(R, 1, conv_flops(P, o, b - a));
+            if (!(P.use_tc && tc_conv_wgrad(A, R.st))) CK(simt_conv_wgrad(R.prec, A, R.st));
+            CK(cudaGetLastError());
+        }
+        if (need_dx) {
+            DgradArgs A;
+            A.dy = dy; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);
+            A.gate = tin.relu; A.w = prm(R, o.w_off); A.wt = R.ws + o.wt_off; A.gamma = gamma;
+            A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.B = B;
+            A.ra = std::max(0, a * o.d.s - o.d.p);
+            A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
+            ++P.launches;
+            ProfScope ps(R, 0, conv_flops(P, o, b - a));
+            if (!(P.use_tc && tc_conv_dgrad(A, R.st))) CK(simt_conv_dgrad(R.prec, A, R.st));
+            CK(cudaGetLastError());
+        }
+        if (o.d.res >= 0) {
+            const TensorInfo &tr = P.t[o.d.res];
+            EltArgs A;
+            A.dy = dy; A.dx = dlt_view(R, S, s, r, o.d.res); A.act = act_view(R, S, r, o.d.res);
+            A.gate = tr.relu; A.a = a; A.b = b; A.B = B;
+            if (o.d.res != 0) {
+                ++P.launches;
+                ProfScope ps(R, 2, 0);
+                CK(simt_acc_gate(R.prec, A, R.st));
+            }
+        }
+    } else if (o.d.kind == LRCNN_OP_MAXPOOL) {
+        if (need_dx) {
+            PoolArgs A;
+            A.dy = dy; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);
+            A.gate = tin.relu; A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.a = a; A.b = b; A.B = B;
+            A.ra = std::max(0, a * o.d.s - o.d.p);
+            A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
+            ++P.launches;
+            ProfScope ps(R, 2, 0);
+            CK(simt_pool_bwd(R.prec, A, R.st));
+        }
+    } else {
+        for (int which = 0; which < 2; ++which) {
+            int tid = which ? o.d.res : o.in_t;
+            if (tid == 0) continue;
+            EltArgs A;
+            A.dy = dy; A.dx = dlt_view(R, S, s, r, tid); A.act = act_view(R, S, r, tid);
+            A.gate = P.t[tid].relu; A.a = a; A.b = b; A.B = B;
+            ++P.launches;
+            ProfScope ps(R, 2, 0);
+            CK(simt_acc_gate(R.prec, A, R.st));
+        }
+    }
+    return LRCNN_OK;
+}
+
+static lrcnn_status run_backward(Run &R) {
+    Plan &P = R.P;
+    lrcnn_status st;
+    const bool recompute = !(P.seg.size() == 1 && P.seg[0].E.size() == 1);
+    // transposed weights for the tensor-core dgrad (gamma folded in)
+    if (P.use_tc) {
+        for (const OpInfo &o : P.op) {
+            if (o.d.kind != LRCNN_OP_CONV || o.in_t == 0) continue;
+            CK(transpose_weights(R.prec, prm(R, o.w_off), o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr,
+                                 R.ws + o.wt_off, o.d.c_out, P.t[o.out_t].Cp, o.d.k, P.t[o.in_t].Cp, R.st));
+            ++P.launches;
+        }
+    }
+    for (int s = (int)P.seg.size() - 1; s >= 0; --s) {
+        const Segment &S = P.seg[s];
+        if (S.in_t != 0) {
+            const TensorInfo &ti = P.t[S.in_t];
+            CK(cudaMemsetAsync(R.ws + P.dfull_off[(s + 1) & 1], 0, (size_t)P.net.B * ti.H * ti.W * ti.Cp * R.E, R.st));
+        }
+        const int N = (int)S.E.size();
+        for (int r = N - 1; r >= 0; --r) {
+            if (recompute && (st = band_forward(R, S, r, false, true)) != LRCNN_OK) return st;
+            // band delta buffers: zero, then the carry of band r+1 (R6)
+            for (int t : S.tensors) {
+                if (t == S.out_t) continue;
+                const TensorInfo &ti = P.t[t];
+                size_t rb = (size_t)ti.W * ti.Cp * R.E;
+                int rows = S.b[r][t] - S.lo[r][t];
+                if (rows > 0)
+                    CK(cudaMemset2DAsync(R.ws + ti.dlt_off, ti.cap * rb, 0, rows * rb, P.net.B, R.st));
+                if (P.opts.mode == LRCNN_2PS && r + 1 < N) {
+                    int clo = S.lo[r + 1][t], chi = S.a[r + 1][t];
+                    if (chi > clo) {
+                        if ((st = copy_rows(R, ti, R.ws + ti.dlt_off + (size_t)(clo - S.lo[r][t]) * rb, ti.cap,
+                                            R.ws + ti.carry_off, ti.carry_cap, chi - clo)) != LRCNN_OK) return st;
+                    }
+                }
+            }
+            for (auto it = S.ops.rbegin(); it != S.ops.rend(); ++it)
+                if ((st = op_backward(R, S, s, r, *it)) != LRCNN_OK) return st;
+            if (P.opts.mode == LRCNN_2PS && r > 0) {
+                for (int t : S.tensors) {
+                    if (t == S.out_t) continue;
+                    const TensorInfo &ti = P.t[t];
+                    int rows = S.a[r][t] - S.lo[r][t];
+                    if (rows > 0 && (st = copy_rows(R, ti, R.ws + ti.carry_off, ti.carry_cap, R.ws + ti.dlt_off, ti.cap,
+                                                    rows)) != LRCNN_OK) return st;
+                }
+            }
+        }
+    }
+    return LRCNN_OK;
+}
+
+static lrcnn_status check_ws(Plan &P, void *ws, size_t ws_bytes) {
+    if (!ws) return fail(LRCNN_E_WORKSPACE, "workspace is NULL");
+    if (ws_bytes < P.ws_bytes) return fail(LRCNN_E_WORKSPACE, "workspace too small: need " + std::to_string(P.ws_bytes));
+    return LRCNN_OK;
+}
+
+}  // namespace lrcnn
+
+using namespace lrcnn;
+
+extern "C" {
+
+const char *lrcnn_last_error(void) { return g_err.c_str(); }
+const char *lrcnn_version(void) { return "lrcnn-b200 0.1 (sm_100a)"; }
+
+lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, lrcnn_plan_t **out) {
+    if (!out) return fail(LRCNN_E_ARG, "out is NULL");
+    *out = nullptr;
+    lrcnn_plan_t *p = new lrcnn_plan_t();
+    std::string err;
+    lrcnn_status st = build_plan(net, opts, p->P, err);
+    if (st != LRCNN_OK) { delete p; return fail(st, err); }
+    p->P.use_tc = p->P.opts.prec == LRCNN_BF16 && !(p->P.opts.flags & LRCNN_FLAG_NO_TCGEN05) && tc_available();
+    *out = p;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
+    if (plan) {
+        for (int c = 0; c < 3; ++c)
+            for (auto &e : plan->P.pending_events[c]) {
+                cudaEventDestroy((cudaEvent_t)e.first);
+                cudaEventDestroy((cudaEvent_t)e.second);
+            }
+        delete plan;
+    }
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_sizes(const lrcnn_plan_t *plan, size_t *ws, size_t *n_params, size_t *zl_elems) {
+    if (!plan) return fail(LRCNN_E_ARG, "plan is NULL");
+    const Plan &P = plan->P;
+    const TensorInfo &z = P.t[P.net.n_ops];
+    if (ws) *ws = P.ws_bytes;
+    if (n_params) *n_params = P.n_params;
+    if (zl_elems) *zl_elems = (size_t)P.net.B * z.H * z.W * z.Cp;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_tensor(const lrcnn_plan_t *plan, int tid, int *C, int *Cp, int *H, int *W) {
+    if (!plan || tid < 0 || tid > plan->P.net.n_ops) return fail(LRCNN_E_ARG, "bad plan or tensor id");
+    const TensorInfo &t = plan->P.t[tid];
+    if (C) *C = t.C;
+    if (Cp) *Cp = t.Cp;
+    if (H) *H = t.H;
+    if (W) *W = t.W;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_param(const lrcnn_plan_t *plan, int op, int which, size_t *offset, size_t *count) {
+    if (!plan || !offset || !count || op < 0 || op > plan->P.net.n_ops) return fail(LRCNN_E_ARG, "bad args");
+    const Plan &P = plan->P;
+    *offset = 0; *count = 0;
+    if (op == P.net.n_ops) {
+        if (which == 0) { *offset = P.head_w_off; *count = P.head_w_cnt; }
+        else if (which == 1) { *offset = P.head_b_off; *count = P.head_b_cnt; }
+        else return fail(LRCNN_E_ARG, "bad which");
+        return LRCNN_OK;
+    }
+    const OpInfo &o = P.op[op];
+    if (which == 0) { *offset = o.w_off; *count = o.w_cnt; }
+    else if (which == 1) { *offset = o.b_off; *count = o.b_cnt; }
+    else if (which == 2) { *offset = o.beta_off; *count = o.beta_cnt; }
+    else return fail(LRCNN_E_ARG, "bad which");
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_nsegs(const lrcnn_plan_t *plan, int *n) {
+    if (!plan || !n) return fail(LRCNN_E_ARG, "bad args");
+    *n = (int)plan->P.seg.size();
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_seg(const lrcnn_plan_t *plan, int seg, int *in_tid, int *out_tid, int *n_bands) {
+    if (!plan || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad segment");
+    const Segment &S = plan->P.seg[seg];
+    if (in_tid) *in_tid = S.in_t;
+    if (out_tid) *out_tid = S.out_t;
+    if (n_bands) *n_bands = (int)S.E.size();
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int band, int tid, int *lo, int *a, int *b) {
+    if (!plan || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad segment");
+    const Segment &S = plan->P.seg[seg];
+    if (band < 0 || band >= (int)S.E.size()) return fail(LRCNN_E_ARG, "bad band");
+    bool in = tid == S.in_t;
+    for (int t : S.tensors) in = in || t == tid;
+    if (!in) return fail(LRCNN_E_ARG, "tensor not in segment");
+    if (lo) *lo = S.lo[band][tid];
+    if (a) *a = S.a[band][tid];
+    if (b) *b = S.b[band][tid];
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_memory(const lrcnn_plan_t *plan, lrcnn_memory_report *rep) {
+    if (!plan || !rep) return fail(LRCNN_E_ARG, "bad args");
+    *rep = plan->P.mem;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_forward_rows(lrcnn_plan_t *plan, const void *params, const void *x, void *zl, void *ws,
+                                size_t ws_bytes, void *stream) {
+    if (!plan || !params || !x || !zl) return fail(LRCNN_E_ARG, "NULL argument");
+    Plan &P = plan->P;
+    lrcnn_status st = check_ws(P, ws, ws_bytes);
+    if (st != LRCNN_OK) return st;
+    P.launches = 0;
+    Run R{P, (char *)ws, (const char *)params, x, zl, nullptr, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    P.fwd_done = false;
+    st = run_forward(R);
+    if (st != LRCNN_OK) return st;
+    P.fwd_done = true; P.fwd_params = params; P.fwd_x = x; P.fwd_ws = ws;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const void *x, const void *zl,
+                                 const void *dzl, float *grads, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !params || !x || !zl || !dzl || !grads) return fail(LRCNN_E_ARG, "NULL argument");
+    Plan &P = plan->P;
+    lrcnn_status st = check_ws(P, ws, ws_bytes);
+    if (st != LRCNN_OK) return st;
+    if (!P.fwd_done || P.fwd_ws != ws || P.fwd_params != params || P.fwd_x != x)
+        return fail(LRCNN_E_STATE, "backward_rows needs a matching forward_rows (same params, x, ws)");
+    P.launches = 0;
+    Run R{P, (char *)ws, (const char *)params, x, (void *)zl, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    const int L = P.net.n_ops;
+    const TensorInfo &z = P.t[L];
+    // delta^L, gated by the last op's ReLU (gate on write), into the last segment's delta buffer
+    int slast = (int)P.seg.size() - 1;
+    CK(gate_copy(P.opts.prec, dzl, zl, R.ws + P.dfull_off[slast & 1], (long long)P.net.B * z.H * z.W * z.Cp, z.relu,
+                 R.st));
+    ++P.launches;
+    st = run_backward(R);
+    P.fwd_done = false;
+    return st;
+}
+
+lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *grads, const void *x,
+                              const int32_t *labels, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
+    Plan &P = plan->P;
+    lrcnn_status st = check_ws(P, ws, ws_bytes);
+    if (st != LRCNN_OK) return st;
+    P.launches = 0;
+    char *w = (char *)ws;
+    Run R{P, w, (const char *)params, x, w + P.zl_off, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    if ((st = run_forward(R)) != LRCNN_OK) return st;
+    const int L = P.net.n_ops;
+    const TensorInfo &z = P.t[L];
+    int slast = (int)P.seg.size() - 1;
+    CK(head_forward_backward(P.opts.prec, R.zl, P.net.B, z.H * z.W, z.Cp, z.C, P.net.n_classes,
+                             R.params + P.head_w_off * R.E, R.params + P.head_b_off * R.E, labels,
+                             (float *)(w + P.head_off), loss_dev, grads + P.head_w_off, grads + P.head_b_off,
+                             w + P.dfull_off[slast & 1], z.relu, R.st));
+    P.launches += 3;
+    st = run_backward(R);
+    P.fwd_done = false;
+    return st;
+}
+
+lrcnn_status lrcnn_sgd(lrcnn_plan_t *plan, float *master, void *params, float *grads, float lr, void *stream) {
+    if (!plan || !master || !params || !grads) return fail(LRCNN_E_ARG, "NULL argument");
+    Plan &P = plan->P;
+    CK(sgd_update(P.opts.prec, master, params, grads, (long long)P.n_params, lr, (cudaStream_t)stream));
+    ++P.launches;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
+                        const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !master || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
+    lrcnn_status st = lrcnn_step_grads(plan, params, grads, x, labels, loss_dev, ws, ws_bytes, stream);
+    if (st != LRCNN_OK) return st;
+    long long n = plan->P.launches;
+    st = lrcnn_sgd(plan, master, params, grads, lr, stream);
+    plan->P.launches += n;
+    return st;
+}
+
+
+lrcnn_status lrcnn_profile_enable(lrcnn_plan_t *plan, int enable) {
+    if (!plan) return fail(LRCNN_E_ARG, "plan is NULL");
+    plan->P.profiling = enable != 0;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan) {
+    if (!plan) return fail(LRCNN_E_ARG, "plan is NULL");
+    for (int c = 0; c < 3; ++c) {
+        for (auto &e : plan->P.pending_events[c]) {
+            cudaEventDestroy((cudaEvent_t)e.first);
+            cudaEventDestroy((cudaEvent_t)e.second);
+        }
+        plan->P.pending_events[c].clear();
+        plan->P.pending_flops[c].clear();
+        plan->P.prof[c] = ProfileSlot();
+    }
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long long *launches, double *flops,
+                                void *stream) {
+    if (!plan || cls < 0 || cls > 2) return fail(LRCNN_E_ARG, "bad args");
+    Plan &P = plan->P;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int c = 0; c < 3; ++c) {
+        for (size_t i = 0; i < P.pending_events[c].size(); ++i) {
+            float t = 0;
+            auto &e = P.pending_events[c][i];
+            CK(cudaEventElapsedTime(&t, (cudaEvent_t)e.first, (cudaEvent_t)e.second));
+            P.prof[c].ms += t;
+            P.prof[c].flops += P.pending_flops[c][i];
+            P.prof[c].launches += 1;
+            cudaEventDestroy((cudaEvent_t)e.first);
+            cudaEventDestroy((cudaEvent_t)e.second);
+        }
+        P.pending_events[c].clear();
+        P.pending_flops[c].clear();
+    }
+    if (ms) *ms = P.prof[cls].ms;
+    if (launches) *launches = P.prof[cls].launches;
+    if (flops) *flops = P.prof[cls].flops;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_last_launch_count(const lrcnn_plan_t *plan, long long *launches) {
+    if (!plan || !launches) return fail(LRCNN_E_ARG, "bad args");
+    *launches = plan->P.launches;
+    return LRCNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// kernels.hpp -- launcher interfaces of the device kernels (internal).
+//
+// A View describes the rows of one NHWC tensor that a buffer holds:
+//   element (b, g, x, c) lives at p + b*bs + ((g - base)*W + x)*Cp + c
+//   and is DATA iff 0 <= g < H and base <= g < base + rows.
+// Rows g < 0 or g >= H are the zero padding of the semi-closed padding rule
+// (PAPER.md:235): the global top/bottom only -- a band cut never pads.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lrcnn {
+
+struct View {
+    void *p = nullptr;
+    int base = 0, rows = 0, H = 0, W = 0, Cp = 0;
+    long long bs = 0;   // batch stride in elements
+};
+
+struct ConvFwdArgs {
+    View in, out, res;         // res.p == nullptr: no residual
+    const void *w = nullptr;   // [Cout][k][k][Cin_p], act_t
+    const void *b = nullptr;   // bias or gamma [c_out], act_t
+    const void *beta = nullptr;
+    int k, s, p, c_out, epi, relu;
+    int a, b_;                 // output rows [a, b_)
+    int B;
+};
+
+struct DgradArgs {
+    View dy;                   // delta_pre of the conv output: rows [a, b) only (others = 0)
+    View dx, act;              // delta of the conv input (accumulated), its activation (gate)
+    int gate;                  // producer of the input applies ReLU
+    const void *w = nullptr;   // [Cout][k][k][Cin_p]
+    const void *wt = nullptr;  // transposed [Cin_p][k][k][Cout_p] (tensor-core path), gamma folded
+    const void *gamma = nullptr;
+    int k, s, p, c_out;
+    int ra, rb;                // input rows to produce
+    int B;
+};
+
+struct WgradArgs {
+    View dy, x;
+    float *dw = nullptr;       // [Cout][k][k][Cin_p] fp32, accumulated
+    const void *gamma = nullptr;
+    int k, s, p, c_out;
+    int a, b;                  // output rows contributing
+    int B;
+};
+
+struct ParamGradArgs {
+    View dy, t, res;
+    const void *gamma = nullptr, *beta = nullptr;
+    float *db = nullptr, *dbeta = nullptr;  // BIAS: db; AFFINE: db = dgamma, dbeta
+    int epi, c_out, a, b, B;
+};
+
+struct PoolArgs {
+    View in, out;              // fwd: out rows [a, b)
+    View dy, dx, act;          // bwd: dy rows [a, b) of the pool output, dx rows [ra, rb)
+    int gate, k, s, p, a, b, ra, rb, B;
+};
+
+struct EltArgs {
+    View x0, x1, out;          // add fwd: out = relu?(x0 + x1) on rows [a, b)
+    View dy, dx, act;          // res/add bwd: dx = gate(act) * (dx + dy) on rows [a, b)
+    int relu, gate, a, b, B;
+};
+
+// SIMT kernels (fp32 parity mode and the general fallback for shapes the tensor-core
+// kernels do not take); prec: 0 = fp32, 1 = bf16 storage (fp32 accumulate).
+cudaError_t simt_conv_fwd(int prec, const ConvFwdArgs &a, cudaStream_t st);
+cudaError_t simt_conv_dgrad(int prec, const DgradArgs &a, cudaStream_t st);
+cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st);
+cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st);
+cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st);
+cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st);
+cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st);
+cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st);
+
+// head (Alg. 1 l.12-14) and update (l.24)
+cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int Cp, int C, int classes,
+                                  const void *fc_w, const void *fc_b, const int32_t *labels, float *scratch,
+                                  float *loss, float *g_fc_w, float *g_fc_b, void *dzl, int gate,
+                                  cudaStream_t st);
+cudaError_t gate_copy(int prec, const void *src, const void *act, void *dst, long long n, int gate,
+                      cudaStream_t st);
+cudaError_t sgd_update(int prec, float *master, void *params, float *grads, long long n, float lr,
+                       cudaStream_t st);
+cudaError_t transpose_weights(int prec, const void *w, const void *gamma, void *wt, int cout, int coutp,
+                              int k, int cinp, cudaStream_t st);
+
+}  // namespace lrcnn

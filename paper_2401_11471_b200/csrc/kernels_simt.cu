@@ -1,0 +1,499 @@
+// kernels_simt.cu -- CUDA-core kernels of the row-centric path.
+//
+// These serve the fp32 parity mode (the tensor-core formats cannot meet the
+// 1e-5 bar), the small ops around the convolutions (max-pool,
+// residual add, bias/affine reductions, head, SGD) and the shapes the
+// tcgen05 kernels do not take.  Every kernel works on band Views
+// (kernels.hpp) so the semi-closed padding rule is a bounds
+// test on the GLOBAL row index, never on the band edge.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace lrcnn {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ float ldf(const float *p) { return *p; }
+__device__ __forceinline__ float ldf(const bf16 *p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void stf(float *p, float v) { *p = v; }
+__device__ __forceinline__ void stf(bf16 *p, float v) { *p = __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ bool vhas(const View &v, int g) {
+    return g >= 0 && g < v.H && g >= v.base && g < v.base + v.rows;
+}
+__device__ __forceinline__ long long voff(const View &v, int b, int g, int x) {
+    return (long long)b * v.bs + ((long long)(g - v.base) * v.W + x) * v.Cp;
+}
+
+// ------------------------------------------------------------------ conv forward
+template <typename T>
+__global__ void k_conv_fwd(ConvFwdArgs A) {
+    const int Cpo = A.out.Cp, Wo = A.out.W, rows = A.b_ - A.a, Cin = A.in.Cp;
+    long long n = (long long)A.B * rows * Wo * Cpo;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int co = idx % Cpo;
+        long long r = idx / Cpo;
+        int x = r % Wo; r /= Wo;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float acc = 0.f;
+        if (co < A.c_out) {
+            const T *in = (const T *)A.in.p;
+            const T *w = (const T *)A.w;
+            for (int ky = 0; ky < A.k; ++ky) {
+                int g = y * A.s - A.p + ky;
+                if (!vhas(A.in, g)) continue;
+                for (int kx = 0; kx < A.k; ++kx) {
+                    int xi = x * A.s - A.p + kx;
+                    if (xi < 0 || xi >= A.in.W) continue;
+                    const T *ip = in + voff(A.in, b, g, xi);
+                    const T *wp = w + ((long long)(co * A.k + ky) * A.k + kx) * Cin;
+                    for (int ci = 0; ci < Cin; ++ci) acc += ldf(wp + ci) * ldf(ip + ci);
+                }
+            }
+            if (A.epi == 1) acc += ldf((const T *)A.b + co);
+            else if (A.epi == 2) acc = ldf((const T *)A.b + co) * acc + ldf((const T *)A.beta + co);
+            if (A.res.p) acc += ldf((const T *)A.res.p + voff(A.res, b, y, x) + co);
+            if (A.relu) acc = fmaxf(acc, 0.f);
+        }
+        stf((T *)A.out.p + voff(A.out, b, y, x) + co, acc);
+    }
+}
+
+// ------------------------------------------------------------------ conv dgrad
+// dx[b,g,xi,ci] = gate(act) * (dx + sum_{co,ky,kx} w[co,ky,kx,ci] * gamma[co] * dy[b,y,x,co]),
+// y*s - p + ky = g.  Gating on write is idempotent (mask in {0,1}), so partial sums
+// (2PS carry rows, several consumers) may be gated more than once.
+template <typename T>
+__global__ void k_conv_dgrad(DgradArgs A) {
+    const int Cin = A.dx.Cp, Wi = A.dx.W, rows = A.rb - A.ra, Wo = A.dy.W, Cpo = A.dy.Cp;
+    long long n = (long long)A.B * rows * Wi * Cin;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int ci = idx % Cin;
+        long long r = idx / Cin;
+        int xi = r % Wi; r /= Wi;
+        int g = A.ra + (int)(r % rows);
+        int b = (int)(r / rows);
+        const T *w = (const T *)A.w;
+        const T *dy = (const T *)A.dy.p;
+        float acc = 0.f;
+        for (int ky = 0; ky < A.k; ++ky) {
+            int num = g + A.p - ky;
+            if (num < 0 || num % A.s) continue;
+            int y = num / A.s;
+            if (!vhas(A.dy, y)) continue;
+            for (int kx = 0; kx < A.k; ++kx) {
+                int nx = xi + A.p - kx;
+                if (nx < 0 || nx % A.s) continue;
+                int x = nx / A.s;
+                if (x >= Wo) continue;
+                const T *dp = dy + voff(A.dy, b, y, x);
+                const T *wp = w + ((long long)ky * A.k + kx) * Cin + ci;
+                const long long wstride = (long long)A.k * A.k * Cin;
+                for (int co = 0; co < A.c_out; ++co) {
+                    float d = ldf(dp + co);
+                    if (A.gamma) d *= ldf((const T *)A.gamma + co);
+                    acc += ldf(wp + co * wstride) * d;
+                }
+            }
+        }
+        (void)Cpo;
+        T *dx = (T *)A.dx.p + voff(A.dx, b, g, xi) + ci;
+        float v = ldf(dx) + acc;
+        if (A.gate && ldf((const T *)A.act.p + voff(A.act, b, g, xi) + ci) <= 0.f) v = 0.f;
+        stf(dx, v);
+    }
+}
+
+// ------------------------------------------------------------------ conv wgrad
+// dw[co,ky,kx,ci] += gamma[co] * sum_{b, y in [a,b), x} dy[b,y,x,co] * x[b, y*s-p+ky, x*s-p+kx, ci]
+// one block per (co, ky, kx), threads over ci x pixel slices, block reduction.
+template <typename T>
+__global__ void k_conv_wgrad(WgradArgs A) {
+    const int Cin = A.x.Cp, Wo = A.dy.W, rows = A.b - A.a;
+    const int co = blockIdx.x / (A.k * A.k), kk = blockIdx.x % (A.k * A.k);
+    const int ky = kk / A.k, kx = kk % A.k;
+    const int ci = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int lane_grp = threadIdx.x >> 5, ngrp = blockDim.x >> 5;
+    __shared__ float red[32][33];
+    float acc = 0.f;
+    if (ci < Cin) {
+        long long npix = (long long)A.B * rows * Wo;
+        for (long long q = lane_grp; q < npix; q += ngrp) {
+            int x = q % Wo;
+            long long r = q / Wo;
+            int y = A.a + (int)(r % rows);
+            int b = (int)(r / rows);
+            int g = y * A.s - A.p + ky, xi = x * A.s - A.p + kx;
+            if (!vhas(A.x, g) || xi < 0 || xi >= A.x.W) continue;
+            float d = ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + co);
+            acc += d * ldf((const T *)A.x.p + voff(A.x, b, g, xi) + ci);
+        }
+    }
+    red[lane_grp][threadIdx.x & 31] = acc;
+    __syncthreads();
+    if (lane_grp == 0 && ci < Cin) {
+        float s = 0.f;
+        for (int j = 0; j < ngrp; ++j) s += red[j][threadIdx.x & 31];
+        if (A.gamma) s *= ldf((const T *)A.gamma + co);
+        A.dw[((long long)(co * A.k + ky) * A.k + kx) * Cin + ci] += s;
+    }
+}
+
+// ------------------------------------------------------------------ bias / affine grads
+template <typename T>
+__global__ void k_param_grad(ParamGradArgs A) {
+    const int co = blockIdx.x, rows = A.b - A.a, W = A.dy.W;
+    long long npix = (long long)A.B * rows * W;
+    float s0 = 0.f, s1 = 0.f;
+    float gam = A.epi == 2 ? ldf((const T *)A.gamma + co) : 1.f;
+    float bet = A.epi == 2 ? ldf((const T *)A.beta + co) : 0.f;
+    for (long long q = threadIdx.x; q < npix; q += blockDim.x) {
+        int x = q % W;
+        long long r = q / W;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float d = ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + co);
+        s0 += d;
+        if (A.epi == 2 && d != 0.f) {
+            float t = ldf((const T *)A.t.p + voff(A.t, b, y, x) + co);
+            if (A.res.p) t -= ldf((const T *)A.res.p + voff(A.res, b, y, x) + co);
+            s1 += d * (t - bet) / gam;   // raw conv output c = (t - beta - res)/gamma
+        }
+    }
+    __shared__ float r0[32], r1[32];
+    for (int o = 16; o; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if ((threadIdx.x & 31) == 0) { r0[threadIdx.x >> 5] = s0; r1[threadIdx.x >> 5] = s1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float a0 = 0.f, a1 = 0.f;
+        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) { a0 += r0[j]; a1 += r1[j]; }
+        if (A.epi == 1) A.db[co] += a0;
+        else { A.db[co] += a1; A.dbeta[co] += a0; }
+    }
+}
+
+// ------------------------------------------------------------------ max-pool
+template <typename T>
+__device__ __forceinline__ void pool_window(const View &in, int b, int y, int x, int c, int k, int s, int p,
+                                            float &best, int &bg, int &bx) {
+    best = 0.f; bg = -1; bx = -1;
+    for (int ky = 0; ky < k; ++ky) {
+        int g = y * s - p + ky;
+        if (!vhas(in, g)) continue;
+        for (int kx = 0; kx < k; ++kx) {
+            int xi = x * s - p + kx;
+            if (xi < 0 || xi >= in.W) continue;
+            float v = ldf((const T *)in.p + voff(in, b, g, xi) + c);
+            if (bg < 0 || v > best) { best = v; bg = g; bx = xi; }
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_pool_fwd(PoolArgs A) {
+    const int Cp = A.out.Cp, Wo = A.out.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * Wo * Cp;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int c = idx % Cp;
+        long long r = idx / Cp;
+        int x = r % Wo; r /= Wo;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float best; int bg, bx;
+        pool_window<T>(A.in, b, y, x, c, A.k, A.s, A.p, best, bg, bx);
+        stf((T *)A.out.p + voff(A.out, b, y, x) + c, bg < 0 ? 0.f : best);
+    }
+}
+
+template <typename T>
+__global__ void k_pool_bwd(PoolArgs A) {
+    const int Cp = A.dx.Cp, Wi = A.dx.W, rows = A.rb - A.ra, Wo = A.dy.W;
+    long long n = (long long)A.B * rows * Wi * Cp;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int c = idx % Cp;
+        long long r = idx / Cp;
+        int xi = r % Wi; r /= Wi;
+        int g = A.ra + (int)(r % rows);
+        int b = (int)(r / rows);
+        float acc = 0.f;
+        for (int ky = 0; ky < A.k; ++ky) {
+            int num = g + A.p - ky;
+            if (num < 0 || num % A.s) continue;
+            int y = num / A.s;
+            if (!vhas(A.dy, y)) continue;
+            for (int kx = 0; kx < A.k; ++kx) {
+                int nx = xi + A.p - kx;
+                if (nx < 0 || nx % A.s) continue;
+                int x = nx / A.s;
+                if (x >= Wo) continue;
+                float best; int bg, bx;
+                pool_window<T>(A.act, b, y, x, c, A.k, A.s, A.p, best, bg, bx);
+                if (bg == g && bx == xi) acc += ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + c);
+            }
+        }
+        T *dx = (T *)A.dx.p + voff(A.dx, b, g, xi) + c;
+        float v = ldf(dx) + acc;
+        if (A.gate && ldf((const T *)A.act.p + voff(A.act, b, g, xi) + c) <= 0.f) v = 0.f;
+        stf(dx, v);
+    }
+}
+
+// ------------------------------------------------------------------ residual add, gated accumulate
+template <typename T>
+__global__ void k_add_fwd(EltArgs A) {
+    const int Cp = A.out.Cp, W = A.out.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * W * Cp;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int c = idx % Cp;
+        long long r = idx / Cp;
+        int x = r % W; r /= W;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float v = ldf((const T *)A.x0.p + voff(A.x0, b, y, x) + c) + ldf((const T *)A.x1.p + voff(A.x1, b, y, x) + c);
+        if (A.relu) v = fmaxf(v, 0.f);
+        stf((T *)A.out.p + voff(A.out, b, y, x) + c, v);
+    }
+}
+
+template <typename T>
+__global__ void k_acc_gate(EltArgs A) {
+    const int Cp = A.dx.Cp, W = A.dx.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * W * Cp;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int c = idx % Cp;
+        long long r = idx / Cp;
+        int x = r % W; r /= W;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        T *dx = (T *)A.dx.p + voff(A.dx, b, y, x) + c;
+        float v = ldf(dx) + ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + c);
+        if (A.gate && ldf((const T *)A.act.p + voff(A.act, b, y, x) + c) <= 0.f) v = 0.f;
+        stf(dx, v);
+    }
+}
+
+// ------------------------------------------------------------------ head
+template <typename T>
+__global__ void k_gap(const T *zl, int HW, int Cp, float *gap) {
+    int b = blockIdx.x, c = blockIdx.y * blockDim.x + threadIdx.x;
+    if (c >= Cp) return;
+    const T *z = zl + (long long)b * HW * Cp + c;
+    float s = 0.f;
+    for (int i = 0; i < HW; ++i) s += ldf(z + (long long)i * Cp);
+    gap[(long long)b * Cp + c] = s / HW;
+}
+
+template <typename T>
+__global__ void k_fc_ce(const float *gap, int B, int Cp, int C, int classes, const T *fw, const T *fb,
+                        const int32_t *labels, float *dlog, float *loss, float *gw, float *gb) {
+    extern __shared__ float sh[];   // logits [B*classes]
+    for (int i = threadIdx.x; i < B * classes; i += blockDim.x) {
+        int b = i / classes, j = i % classes;
+        float s = ldf(fb + j);
+        for (int c = 0; c < C; ++c) s += gap[(long long)b * Cp + c] * ldf(fw + (long long)j * Cp + c);
+        sh[i] = s;
+    }
+    __syncthreads();
+    __shared__ float lsum;
+    if (threadIdx.x == 0) lsum = 0.f;
+    __syncthreads();
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        float m = -INFINITY;
+        for (int j = 0; j < classes; ++j) m = fmaxf(m, sh[b * classes + j]);
+        float se = 0.f;
+        for (int j = 0; j < classes; ++j) se += expf(sh[b * classes + j] - m);
+        int lab = labels[b];
+        atomicAdd(&lsum, (m + logf(se)) - sh[b * classes + lab]);
+        for (int j = 0; j < classes; ++j)
+            dlog[b * classes + j] = (expf(sh[b * classes + j] - m) / se - (j == lab ? 1.f : 0.f)) / B;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *loss = lsum / B;
+    for (int i = threadIdx.x; i < classes * C; i += blockDim.x) {
+        int j = i / C, c = i % C;
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s += dlog[b * classes + j] * gap[(long long)b * Cp + c];
+        gw[(long long)j * Cp + c] += s;
+    }
+    for (int j = threadIdx.x; j < classes; j += blockDim.x) {
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s += dlog[b * classes + j];
+        gb[j] += s;
+    }
+}
+
+template <typename T>
+__global__ void k_dzl(const T *zl, const float *dlog, const T *fw, int B, int HW, int Cp, int C, int classes,
+                      T *dzl, int gate) {
+    long long n = (long long)B * HW * Cp;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int c = idx % Cp;
+        int b = (int)(idx / ((long long)HW * Cp));
+        float v = 0.f;
+        if (c < C) {
+            for (int j = 0; j < classes; ++j) v += dlog[b * classes + j] * ldf(fw + (long long)j * Cp + c);
+            v /= HW;
+        }
+        if (gate && ldf(zl + idx) <= 0.f) v = 0.f;
+        stf(dzl + idx, v);
+    }
+}
+
+template <typename T>
+__global__ void k_gate_copy(const T *src, const T *act, T *dst, long long n, int gate) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        float v = ldf(src + i);
+        if (gate && ldf(act + i) <= 0.f) v = 0.f;
+        stf(dst + i, v);
+    }
+}
+
+template <typename T>
+__global__ void k_sgd(float *master, T *params, float *grads, long long n, float lr) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        float m = master[i] - lr * grads[i];
+        master[i] = m;
+        stf(params + i, m);
+        grads[i] = 0.f;
+    }
+}
+
+template <typename T>
+__global__ void k_transpose_w(const T *w, const T *gamma, T *wt, int cout, int coutp, int k, int cinp) {
+    long long n = (long long)cinp * k * k * coutp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int co = i % coutp;
+        long long r = i / coutp;
+        int kx2 = r % k; r /= k;
+        int ky2 = r % k;
+        int ci = (int)(r / k);
+        float v = 0.f;
+        if (co < cout) {
+            int ky = k - 1 - ky2, kx = k - 1 - kx2;
+            v = ldf(w + ((long long)(co * k + ky) * k + kx) * cinp + ci);
+            if (gamma) v *= ldf(gamma + co);
+        }
+        stf(wt + i, v);
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+static const int kT = 256;
+static unsigned grid_for(long long n) {
+    long long g = (n + kT - 1) / kT;
+    if (g > 148LL * 64) g = 148LL * 64;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+#define DISPATCH(prec, KER, ...)                                        \
+    do {                                                                \
+        if (prec) KER<bf16><<<__VA_ARGS__>>>; else KER<float><<<__VA_ARGS__>>>; \
+    } while (0)
+
+cudaError_t simt_conv_fwd(int prec, const ConvFwdArgs &a, cudaStream_t st) {
+    long long n = (long long)a.B * (a.b_ - a.a) * a.out.W * a.out.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_conv_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_conv_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_conv_dgrad(int prec, const DgradArgs &a, cudaStream_t st) {
+    long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_conv_dgrad<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_conv_dgrad<float><<<grid_for(n), kT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st) {
+    if (a.b <= a.a) return cudaSuccess;
+    dim3 g(a.c_out * a.k * a.k, (a.x.Cp + 31) / 32);
+    if (prec) k_conv_wgrad<bf16><<<g, 256, 0, st>>>(a); else k_conv_wgrad<float><<<g, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
+    if (a.b <= a.a || a.epi == 0) return cudaSuccess;
+    if (prec) k_param_grad<bf16><<<a.c_out, 256, 0, st>>>(a); else k_param_grad<float><<<a.c_out, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
+    long long n = (long long)a.B * (a.b - a.a) * a.out.W * a.out.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_pool_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
+    long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_pool_bwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st) {
+    long long n = (long long)a.B * (a.b - a.a) * a.out.W * a.out.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_add_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_add_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
+    long long n = (long long)a.B * (a.b - a.a) * a.dx.W * a.dx.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_acc_gate<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate<float><<<grid_for(n), kT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int Cp, int C, int classes,
+                                  const void *fc_w, const void *fc_b, const int32_t *labels, float *scratch,
+                                  float *loss, float *g_fc_w, float *g_fc_b, void *dzl, int gate,
+                                  cudaStream_t st) {
+    float *gap = scratch, *dlog = scratch + (long long)B * Cp;
+    dim3 g1(B, (Cp + 127) / 128);
+    size_t shm = sizeof(float) * B * classes;
+    long long n = (long long)B * HW * Cp;
+    if (prec) {
+        k_gap<bf16><<<g1, 128, 0, st>>>((const bf16 *)zl, HW, Cp, gap);
+        k_fc_ce<bf16><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
+                                            dlog, loss, g_fc_w, g_fc_b);
+        k_dzl<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
+                                               (bf16 *)dzl, gate);
+    } else {
+        k_gap<float><<<g1, 128, 0, st>>>((const float *)zl, HW, Cp, gap);
+        k_fc_ce<float><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const float *)fc_w, (const float *)fc_b, labels,
+                                             dlog, loss, g_fc_w, g_fc_b);
+        k_dzl<float><<<grid_for(n), kT, 0, st>>>((const float *)zl, dlog, (const float *)fc_w, B, HW, Cp, C, classes,
+                                                (float *)dzl, gate);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t gate_copy(int prec, const void *src, const void *act, void *dst, long long n, int gate, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_gate_copy<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)src, (const bf16 *)act, (bf16 *)dst, n, gate);
+    else k_gate_copy<float><<<grid_for(n), kT, 0, st>>>((const float *)src, (const float *)act, (float *)dst, n, gate);
+    return cudaGetLastError();
+}
+
+cudaError_t sgd_update(int prec, float *master, void *params, float *grads, long long n, float lr, cudaStream_t st) {
+    if (prec) k_sgd<bf16><<<grid_for(n), kT, 0, st>>>(master, (bf16 *)params, grads, n, lr);
+    else k_sgd<float><<<grid_for(n), kT, 0, st>>>(master, (float *)params, grads, n, lr);
+    return cudaGetLastError();
+}
+
+cudaError_t transpose_weights(int prec, const void *w, const void *gamma, void *wt, int cout, int coutp, int k,
+                              int cinp, cudaStream_t st) {
+    long long n = (long long)cinp * k * k * coutp;
+    if (prec) k_transpose_w<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)w, (const bf16 *)gamma, (bf16 *)wt, cout, coutp, k, cinp);
+    else k_transpose_w<float><<<grid_for(n), kT, 0, st>>>((const float *)w, (const float *)gamma, (float *)wt, cout, coutp, k, cinp);
+    return cudaGetLastError();
+}
+
+}  // namespace lrcnn

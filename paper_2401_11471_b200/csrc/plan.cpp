@@ -1,0 +1,345 @@
+// plan.cpp -- the row-centric planner (host, integer only).
+//
+// Interval rule (R3; reproduces PAPER.md Eqs. (11), (13), (14) on
+// divisible chains):
+//   band ends E_1 < ... < E_N = H_out at the segment output; for every other
+//   tensor t of the segment, in reverse production order,
+//     e_r(t) = max over consumers u with e_r(u) > 0 of
+//                min(H_t, (e_r(u)-1)*s - p + k)   (window consumer)
+//                e_r(u)                           (1:1 consumer: residual / ADD)
+//     e_N(t) = H_t
+//   band r computes rows [e_{r-1}(t), e_r(t)); its buffer also holds the 2PS
+//   cache rows [lo_r(t), e_{r-1}(t)),
+//     lo_r(t) = min(e_{r-1}(t), min over consumers computing rows [a,b) in band r of
+//               max(0, a*s - p)  (window) | a (1:1)).
+// OverL extended ranges (R4): the backward image of
+// the owned output rows [E_{r-1}, E_r):
+//     lo = min_u max(0, lo_u*s - p),  hi = max_u min(H_t, (hi_u-1)*s - p + k).
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "plan.hpp"
+
+namespace lrcnn {
+
+static const size_t kAlign = 256;
+static size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+static std::vector<int> make_band_ends(int h_out, int band_rows, int n_bands) {
+    std::vector<int> E;
+    if (band_rows > 0) {
+        for (int e = band_rows; e < h_out; e += band_rows) E.push_back(e);
+        E.push_back(h_out);
+        return E;
+    }
+    int n = std::max(1, std::min(n_bands, h_out));
+    int q = h_out / n, rem = h_out % n, acc = 0;
+    for (int r = 0; r < n; ++r) {
+        acc += q + (r < rem ? 1 : 0);
+        E.push_back(acc);
+    }
+    return E;
+}
+
+static bool window_role(const OpInfo &o, int role) {
+    return role == 0 && o.d.kind != LRCNN_OP_ADD;
+}
+
+lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, Plan &P, std::string &err) {
+    if (!net || !opts || !net->ops || net->n_ops < 1) { err = "null net/opts or no ops"; return LRCNN_E_ARG; }
+    if (net->B < 1 || net->C < 1 || net->H < 1 || net->W < 1 || net->n_classes < 1) {
+        err = "batch/image/classes must be >= 1"; return LRCNN_E_SHAPE;
+    }
+    if (opts->mode < LRCNN_COLUMN || opts->mode > LRCNN_OVERL) { err = "bad mode"; return LRCNN_E_ARG; }
+    if (opts->prec != LRCNN_FP32 && opts->prec != LRCNN_BF16) { err = "bad precision"; return LRCNN_E_ARG; }
+    if (opts->world > 1) { err = "row sharding across GPUs (world > 1) is not in this build"; return LRCNN_E_UNSUPPORTED; }
+    if (opts->mode != LRCNN_COLUMN && opts->band_rows <= 0 && opts->n_bands <= 0) {
+        err = "band_rows or n_bands must be > 0"; return LRCNN_E_ARG;
+    }
+    P.net = *net;
+    P.ops_copy.assign(net->ops, net->ops + net->n_ops);
+    P.net.ops = P.ops_copy.data();
+    P.opts = *opts;
+    P.elem = opts->prec == LRCNN_BF16 ? 2 : 4;
+    const int n_ops = net->n_ops, T = n_ops + 1;
+    P.t.assign(T, TensorInfo());
+    P.op.assign(n_ops, OpInfo());
+    P.t[0].C = net->C; P.t[0].Cp = round_up(net->C, 8); P.t[0].H = net->H; P.t[0].W = net->W;
+    P.t[0].seg_in = true;
+
+    // ---------------------------------------------------------------- shapes
+    for (int i = 0; i < n_ops; ++i) {
+        const lrcnn_op &d = P.ops_copy[i];
+        OpInfo &o = P.op[i];
+        o.d = d; o.in_t = d.src; o.out_t = i + 1;
+        if (d.src < 0 || d.src > i) { err = "op " + std::to_string(i) + ": src must be an earlier tensor"; return LRCNN_E_ARG; }
+        if (d.res > i || d.res < -1) { err = "op " + std::to_string(i) + ": bad res"; return LRCNN_E_ARG; }
+        const TensorInfo &in = P.t[d.src];
+        TensorInfo &out = P.t[i + 1];
+        out.producer = i;
+        if (d.kind == LRCNN_OP_CONV || d.kind == LRCNN_OP_MAXPOOL) {
+            if (d.k < 1 || d.s < 1 || d.p < 0 || d.p >= d.k) { err = "op " + std::to_string(i) + ": need k>=1, s>=1, 0<=p<k"; return LRCNN_E_SHAPE; }
+            int ho = out_dim(in.H, d.k, d.s, d.p), wo = out_dim(in.W, d.k, d.s, d.p);
+            if (ho < 1 || wo < 1) { err = "op " + std::to_string(i) + ": kernel exceeds input (PAPER.md:218)"; return LRCNN_E_SHAPE; }
+            out.H = ho; out.W = wo;
+            if (d.kind == LRCNN_OP_CONV) {
+                if (d.c_out < 1) { err = "conv c_out < 1"; return LRCNN_E_SHAPE; }
+                if (d.epi < LRCNN_EPI_NONE || d.epi > LRCNN_EPI_AFFINE) { err = "bad epi"; return LRCNN_E_ARG; }
+                out.C = d.c_out;
+                out.relu = d.relu ? 1 : 0;
+                if (d.res >= 0) {
+                    const TensorInfo &r = P.t[d.res];
+                    if (r.C != out.C || r.H != out.H || r.W != out.W) { err = "conv residual shape mismatch"; return LRCNN_E_SHAPE; }
+                }
+            } else {
+                if (d.res >= 0) { err = "maxpool has no residual"; return LRCNN_E_ARG; }
+                out.C = in.C; out.relu = 0;
+            }
+        } else if (d.kind == LRCNN_OP_ADD) {
+            if (d.res < 0) { err = "add needs res"; return LRCNN_E_ARG; }
+            const TensorInfo &r = P.t[d.res];
+            if (r.C != in.C || r.H != in.H || r.W != in.W) { err = "add shape mismatch"; return LRCNN_E_SHAPE; }
+            out.C = in.C; out.H = in.H; out.W = in.W; out.relu = d.relu ? 1 : 0;
+        } else { err = "bad op kind"; return LRCNN_E_ARG; }
+        out.Cp = round_up(out.C, 8);
+        P.t[d.src].cons.push_back({i, 0});
+        if (d.res >= 0) P.t[d.res].cons.push_back({i, 1});
+    }
+    P.t[n_ops].is_zl = true;
+
+    // ---------------------------------------------------------------- segments
+    {
+        Segment cur; cur.in_t = 0;
+        for (int i = 0; i < n_ops; ++i) {
+            cur.ops.push_back(i);
+            bool end = (i == n_ops - 1) || (opts->mode != LRCNN_COLUMN && P.ops_copy[i].seg_end);
+            if (end) { cur.out_t = i + 1; P.seg.push_back(cur); cur = Segment(); cur.in_t = i + 1; }
+        }
+    }
+    for (size_t s = 0; s < P.seg.size(); ++s) {
+        Segment &S = P.seg[s];
+        std::vector<char> inside(T, 0);
+        inside[S.in_t] = 1;
+        for (int i : S.ops) inside[i + 1] = 1;
+        for (int i : S.ops) {
+            const lrcnn_op &d = P.ops_copy[i];
+            if (!inside[d.src] || (d.res >= 0 && !inside[d.res])) {
+                err = "op " + std::to_string(i) + " reads a tensor across a checkpoint boundary"; return LRCNN_E_ARG;
+            }
+            P.t[i + 1].seg = (int)s;
+            S.tensors.push_back(i + 1);
+        }
+        P.t[S.out_t].seg_out = true;
+        P.t[S.in_t].seg_in = true;
+        // every internal tensor needs a consumer inside the segment
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            bool has = false;
+            for (auto &c : P.t[t].cons) if (inside[c.op + 1]) has = true;
+            if (!has) { err = "tensor " + std::to_string(t) + " has no consumer in its segment"; return LRCNN_E_ARG; }
+            for (auto &c : P.t[t].cons)
+                if (!inside[c.op + 1]) { err = "tensor " + std::to_string(t) + " is read across a checkpoint"; return LRCNN_E_ARG; }
+        }
+    }
+
+    // ---------------------------------------------------------------- bands
+    for (Segment &S : P.seg) {
+        const int h_out = P.t[S.out_t].H;
+        if (opts->mode == LRCNN_COLUMN) S.E = {h_out};
+        else S.E = make_band_ends(h_out, opts->band_rows, opts->n_bands);
+        for (size_t r = 1; r < S.E.size(); ++r)
+            if (S.E[r] <= S.E[r - 1]) { err = "band ends not strictly increasing"; return LRCNN_E_DEGENERATE; }
+        const int N = (int)S.E.size();
+        S.lo.assign(N, std::vector<int>(T, 0));
+        S.a = S.lo; S.b = S.lo;
+        std::vector<char> inside(T, 0);
+        for (int i : S.ops) inside[i + 1] = 1;
+        if (opts->mode == LRCNN_OVERL) {
+            for (int r = 0; r < N; ++r) {
+                int e0 = r ? S.E[r - 1] : 0;
+                S.lo[r][S.out_t] = S.a[r][S.out_t] = e0; S.b[r][S.out_t] = S.E[r];
+                // internal tensors and the segment input, reverse production order
+                std::vector<int> order(S.tensors.rbegin(), S.tensors.rend());
+                order.push_back(S.in_t);
+                for (int t : order) {
+                    if (t == S.out_t) continue;
+                    int lo = INT_MAX, hi = 0;
+                    for (auto &c : P.t[t].cons) {
+                        if (!inside[c.op + 1]) continue;
+                        const OpInfo &o = P.op[c.op];
+                        int lu = S.lo[r][c.op + 1], hu = S.b[r][c.op + 1];
+                        if (hu <= lu) continue;
+                        int l, h;
+                        if (window_role(o, c.role)) {
+                            l = std::max(0, lu * o.d.s - o.d.p);
+                            h = std::min(P.t[t].H, (hu - 1) * o.d.s - o.d.p + o.d.k);
+                        } else { l = lu; h = hu; }
+                        lo = std::min(lo, l); hi = std::max(hi, h);
+                    }
+                    if (hi <= 0 || lo == INT_MAX) { lo = 0; hi = 0; }
+                    S.lo[r][t] = S.a[r][t] = lo; S.b[r][t] = hi;
+                }
+            }
+            int ov = 0;
+            for (int r = 0; r + 1 < N; ++r) ov = std::max(ov, S.b[r][S.in_t] - S.lo[r + 1][S.in_t]);
+            S.overlap_in = ov;
+            if (N > 1 && ov > 0 && (long)N * ov > P.t[S.in_t].H && !(opts->flags & LRCNN_FLAG_ALLOW_OVERLAP_EXHAUSTION)) {
+                err = "OverL: N > H/o^0 at a segment input (PAPER.md:391-392)"; return LRCNN_E_INFEASIBLE;
+            }
+        } else {
+            for (int r = 0; r < N; ++r) {
+                S.b[r][S.out_t] = S.E[r];
+                for (auto it = S.tensors.rbegin(); it != S.tensors.rend(); ++it) {
+                    int t = *it;
+                    if (t == S.out_t) continue;
+                    int e = 0;
+                    if (r == N - 1) e = P.t[t].H;
+                    else {
+                        for (auto &c : P.t[t].cons) {
+                            const OpInfo &o = P.op[c.op];
+                            int eu = S.b[r][c.op + 1];
+                            if (eu <= 0) continue;
+                            int need = window_role(o, c.role) ? (eu - 1) * o.d.s - o.d.p + o.d.k : eu;
+                            e = std::max(e, std::min(P.t[t].H, need));
+                        }
+                    }
+                    S.b[r][t] = e;
+                }
+                for (int t : S.tensors) S.a[r][t] = r ? S.b[r - 1][t] : 0;
+                for (int t : S.tensors) {
+                    int lo = S.a[r][t];
+                    if (t != S.out_t) {
+                        for (auto &c : P.t[t].cons) {
+                            const OpInfo &o = P.op[c.op];
+                            int au = S.a[r][c.op + 1], bu = S.b[r][c.op + 1];
+                            if (bu <= au) continue;
+                            int first = window_role(o, c.role) ? std::max(0, au * o.d.s - o.d.p) : au;
+                            if (first < P.t[t].H) lo = std::min(lo, first);
+                        }
+                    }
+                    S.lo[r][t] = lo;
+                }
+                for (int t : S.tensors)
+                    if (S.b[r][t] < S.a[r][t]) { err = "non-monotone band ends"; return LRCNN_E_DEGENERATE; }
+            }
+        }
+    }
+
+    // ---------------------------------------------------------------- parameters
+    size_t off = 0;
+    auto take = [&](size_t n) { size_t o = off; off += (n + 7) / 8 * 8; return o; };
+    for (int i = 0; i < n_ops; ++i) {
+        OpInfo &o = P.op[i];
+        if (o.d.kind != LRCNN_OP_CONV) continue;
+        o.w_cnt = (size_t)o.d.c_out * o.d.k * o.d.k * P.t[o.in_t].Cp;
+        o.w_off = take(o.w_cnt);
+        if (o.d.epi == LRCNN_EPI_BIAS) { o.b_cnt = o.d.c_out; o.b_off = take(o.b_cnt); }
+        if (o.d.epi == LRCNN_EPI_AFFINE) {
+            o.b_cnt = o.d.c_out; o.b_off = take(o.b_cnt);
+            o.beta_cnt = o.d.c_out; o.beta_off = take(o.beta_cnt);
+        }
+    }
+    const TensorInfo &zl = P.t[n_ops];
+    P.head_w_cnt = (size_t)net->n_classes * zl.Cp; P.head_w_off = take(P.head_w_cnt);
+    P.head_b_cnt = net->n_classes; P.head_b_off = take(P.head_b_cnt);
+    P.n_params = off;
+
+    // ---------------------------------------------------------------- workspace
+    const size_t B = net->B, E = P.elem;
+    auto rowbytes = [&](int t) { return (size_t)P.t[t].W * P.t[t].Cp * E; };
+    size_t ws = 0;
+    auto alloc = [&](size_t bytes) { size_t o = ws; ws = align_up(ws + bytes); return o; };
+    lrcnn_memory_report &M = P.mem;
+    std::memset(&M, 0, sizeof(M));
+    for (int t = 1; t < T; ++t) M.omega += B * P.t[t].H * P.t[t].W * P.t[t].C * E;
+    // persistent: checkpoints, 2PS caches, delta ping-pong, head scratch, transposed weights
+    for (const Segment &S : P.seg) {
+        if (!P.t[S.out_t].is_zl) {
+            P.t[S.out_t].ckpt_off = alloc(B * P.t[S.out_t].H * rowbytes(S.out_t));
+            M.checkpoints += B * P.t[S.out_t].H * rowbytes(S.out_t);
+        }
+        const int N = (int)S.E.size();
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            TensorInfo &ti = P.t[t];
+            ti.cache_lo.assign(std::max(0, N - 1), 0);
+            ti.cache_rows.assign(std::max(0, N - 1), 0);
+            ti.cache_off.assign(std::max(0, N - 1), 0);
+            if (opts->mode != LRCNN_2PS) continue;
+            for (int r = 0; r + 1 < N; ++r) {
+                int nlo = S.lo[r + 1][t], e = S.b[r][t];
+                ti.cache_lo[r] = nlo;
+                ti.cache_rows[r] = std::max(0, e - nlo);
+                if (ti.cache_rows[r] > 0) {
+                    ti.cache_off[r] = alloc(B * ti.cache_rows[r] * rowbytes(t));
+                    M.halo_cache += B * ti.cache_rows[r] * rowbytes(t);
+                }
+            }
+        }
+    }
+    size_t dmax = 0;
+    for (const Segment &S : P.seg) dmax = std::max(dmax, B * P.t[S.out_t].H * rowbytes(S.out_t));
+    P.dfull_bytes = dmax;
+    P.dfull_off[0] = alloc(dmax);
+    P.dfull_off[1] = P.seg.size() > 1 ? alloc(dmax) : P.dfull_off[0];
+    M.delta_full = dmax * (P.seg.size() > 1 ? 2 : 1);
+    P.zl_off = alloc(B * zl.H * rowbytes(n_ops));
+    M.checkpoints += B * zl.H * rowbytes(n_ops);
+    P.head_off = alloc(sizeof(float) * (B * zl.Cp + B * net->n_classes + 64));
+    P.flag_off = alloc(256);
+    M.other += ws - (P.head_off);
+    {
+        size_t o0 = ws;
+        for (OpInfo &o : P.op)
+            if (o.d.kind == LRCNN_OP_CONV) o.wt_off = alloc(o.w_cnt * E);
+        M.other += ws - o0;
+    }
+    // per-segment arena (band act/delta/carry), overlaid across segments
+    size_t arena0 = ws, arena_max = 0;
+    for (const Segment &S : P.seg) {
+        size_t a = 0, act = 0, dl = 0, car = 0;
+        auto sub = [&](size_t bytes) { size_t o = a; a = align_up(a + bytes); return arena0 + o; };
+        const int N = (int)S.E.size();
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            TensorInfo &ti = P.t[t];
+            int cap = 0, ccap = 0;
+            for (int r = 0; r < N; ++r) {
+                cap = std::max(cap, S.b[r][t] - S.lo[r][t]);
+                ccap = std::max(ccap, S.a[r][t] - S.lo[r][t]);
+            }
+            ti.cap = std::max(cap, 1);
+            ti.act_off = sub(B * ti.cap * rowbytes(t)); act += B * ti.cap * rowbytes(t);
+            ti.dlt_off = sub(B * ti.cap * rowbytes(t)); dl += B * ti.cap * rowbytes(t);
+            ti.carry_cap = ccap;
+            if (ccap > 0 && opts->mode == LRCNN_2PS) { ti.carry_off = sub(B * ccap * rowbytes(t)); car += B * ccap * rowbytes(t); }
+        }
+        if (a > arena_max) { arena_max = a; M.band_act = act; M.band_delta = dl; M.carry = car; }
+    }
+    ws = align_up(arena0 + arena_max);
+    P.ws_bytes = ws;
+    M.workspace = ws;
+
+    // ---------------------------------------------------------------- FLOPs
+    double tau = 0, fwd = 0, bwd = 0;
+    for (int i = 0; i < n_ops; ++i) {
+        const OpInfo &o = P.op[i];
+        if (o.d.kind != LRCNN_OP_CONV) continue;
+        double per_row = 2.0 * o.d.k * o.d.k * B * P.t[o.in_t].C * P.t[o.out_t].C * P.t[o.out_t].W;
+        tau += per_row * P.t[o.out_t].H;
+        const Segment &S = P.seg[P.t[o.out_t].seg];
+        for (size_t r = 0; r < S.E.size(); ++r) {
+            double rows = S.b[r][o.out_t] - S.a[r][o.out_t];
+            fwd += per_row * rows;
+            bwd += per_row * rows * (o.in_t == 0 ? 1 : 2);
+        }
+    }
+    bool recompute = !(P.seg.size() == 1 && P.seg[0].E.size() == 1);
+    M.tau_flops = tau;
+    M.fwd_flops = fwd;
+    M.step_flops = fwd * (recompute ? 2 : 1) + bwd;
+    return LRCNN_OK;
+}
+
+}  // namespace lrcnn

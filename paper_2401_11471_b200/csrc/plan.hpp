@@ -1,0 +1,100 @@
+// plan.hpp -- host-side plan of the row-centric hot path (internal, not part of the ABI).
+//
+// A plan fixes, per segment and band, the rows every tensor computes and holds
+// (the interval rule, R3 / R4), the halo-cache and carry sizes, and
+// the byte layout of the caller-provided workspace.  Pure integer host code.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/lrcnn.h"
+
+namespace lrcnn {
+
+struct Consumer {
+    int op;    // consuming op index
+    int role;  // 0 = read through the op's window (src of CONV/MAXPOOL), 1 = read 1:1 (res, ADD)
+};
+
+struct TensorInfo {
+    int C = 0, Cp = 0, H = 0, W = 0;
+    int producer = -1;        // op index, -1 for the image
+    int relu = 0;             // producer applies ReLU (delta gate on write)
+    int seg = -1;             // segment that produces it (-1 image)
+    bool seg_in = false;      // image or checkpoint: full-width map
+    bool seg_out = false;     // output of its segment (checkpoint or z^L)
+    bool is_zl = false;
+    std::vector<Consumer> cons;
+    // workspace placement (bytes)
+    int cap = 0;              // band buffer rows (internal tensors)
+    size_t act_off = 0, dlt_off = 0;
+    int carry_cap = 0;
+    size_t carry_off = 0;
+    std::vector<int> cache_lo, cache_rows;   // per band boundary r (0..N-2): rows [lo_{r+1}, b_r)
+    std::vector<size_t> cache_off;
+    size_t ckpt_off = 0;      // checkpoint (seg_out && !is_zl)
+    size_t wt_off = 0;        // unused for tensors
+};
+
+struct OpInfo {
+    lrcnn_op d;
+    int in_t, out_t;
+    size_t w_off = 0, w_cnt = 0, b_off = 0, b_cnt = 0, beta_off = 0, beta_cnt = 0;
+    size_t wt_off = 0;        // transposed (dgrad) weights in workspace (bf16 tensor-core path)
+};
+
+struct Segment {
+    int in_t = 0, out_t = 0;
+    std::vector<int> ops;                    // topological order
+    std::vector<int> tensors;                // internal tensors + out (ids), production order
+    std::vector<int> E;                      // band ends at the segment output
+    // per band r, per global tensor id: lo (buffer start), a (first computed), b (end)
+    std::vector<std::vector<int>> lo, a, b;
+    int overlap_in = 0;                      // OverL: max overlap of consecutive bands at the input
+};
+
+struct ProfileSlot {
+    double ms = 0, flops = 0;
+    long long launches = 0;
+};
+
+struct Plan {
+    lrcnn_net_desc net{};
+    std::vector<lrcnn_op> ops_copy;
+    lrcnn_plan_opts opts{};
+    int elem = 4;                            // bytes per activation element
+    std::vector<TensorInfo> t;
+    std::vector<OpInfo> op;
+    std::vector<Segment> seg;
+    size_t n_params = 0;
+    size_t head_w_off = 0, head_w_cnt = 0, head_b_off = 0, head_b_cnt = 0;
+    size_t ws_bytes = 0;
+    size_t dfull_off[2] = {0, 0}, dfull_bytes = 0;
+    size_t head_off = 0;                     // head scratch (fp32)
+    size_t zl_off = 0;                       // z^L buffer used by lrcnn_step
+    size_t flag_off = 0;                     // small device scratch
+    bool use_tc = false;                     // tensor-core kernels enabled
+    lrcnn_memory_report mem{};
+    // run state
+    bool fwd_done = false;
+    const void *fwd_params = nullptr, *fwd_x = nullptr;
+    void *fwd_ws = nullptr;
+    long long launches = 0;
+    bool profiling = false;
+    ProfileSlot prof[3];
+    std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t
+    std::vector<double> pending_flops[3];
+};
+
+// Builds the plan; returns status and fills err on failure.
+lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, Plan &P, std::string &err);
+
+inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+inline int out_dim(int h, int k, int s, int p) {
+    int span = h + 2 * p - k;
+    return span < 0 ? -1 : span / s + 1;
+}
+
+}  // namespace lrcnn

@@ -1,0 +1,12 @@
+// tc.hpp -- tensor-core (tcgen05 / TMEM / TMA) kernels for sm_100a (internal).
+// Each launcher returns true when it took the op (shape supported) and enqueued
+// the kernel; false means the caller runs the SIMT kernel instead.
+#pragma once
+#include "kernels.hpp"
+
+namespace lrcnn {
+bool tc_available();
+bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st);
+bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st);
+bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st);
+}  // namespace lrcnn

@@ -1,0 +1,354 @@
+"""Thin Python binding of liblrcnn.so (include/lrcnn.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+packs arguments (ctypes structs, device pointers from torch tensors, the
+caller's CUDA stream) and converts the parameter layout.  PyTorch is used for
+device memory and streams.  If the shared library is missing the import fails
+loudly: there is no CPU or PyTorch fallback for any compute.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblrcnn.so")
+
+OP_CONV, OP_MAXPOOL, OP_ADD = 0, 1, 2
+EPI = {"none": 0, "bias": 1, "affine": 2}
+MODES = {"column": 0, "2ps": 1, "overl": 2}
+PRECS = {"fp32": 0, "bf16": 1}
+FLAG_ALLOW_OVERLAP_EXHAUSTION = 1
+FLAG_NO_TCGEN05 = 2
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
+          6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
+
+
+class LrcnnError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("lrcnn %s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Op(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("src", ctypes.c_int), ("res", ctypes.c_int), ("c_out", ctypes.c_int),
+                ("k", ctypes.c_int), ("s", ctypes.c_int), ("p", ctypes.c_int), ("epi", ctypes.c_int),
+                ("relu", ctypes.c_int), ("seg_end", ctypes.c_int)]
+
+
+class NetDesc(ctypes.Structure):
+    _fields_ = [("n_ops", ctypes.c_int), ("ops", ctypes.POINTER(Op)), ("B", ctypes.c_int), ("C", ctypes.c_int),
+                ("H", ctypes.c_int), ("W", ctypes.c_int), ("n_classes", ctypes.c_int)]
+
+
+class PlanOpts(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("prec", ctypes.c_int), ("band_rows", ctypes.c_int),
+                ("n_bands", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("flags", ctypes.c_int)]
+
+
+class MemoryReport(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_size_t) for n in ("omega", "band_act", "band_delta", "halo_cache", "carry",
+                                                "checkpoints", "delta_full", "other", "workspace")] + \
+               [(n, ctypes.c_double) for n in ("tau_flops", "fwd_flops", "step_flops")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+EXPORTS = ["lrcnn_plan", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
+           "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
+           "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
+           "lrcnn_profile_reset", "lrcnn_last_launch_count", "lrcnn_last_error", "lrcnn_version"]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("liblrcnn.so not built (%s); run `python -m paper_2401_11471_b200.build` "
+                          "-- there is no fallback path" % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    vp, sz, i, ip = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_int)
+    szp = ctypes.POINTER(ctypes.c_size_t)
+    L.lrcnn_plan.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), ctypes.POINTER(vp)]
+    L.lrcnn_plan_free.argtypes = [vp]
+    L.lrcnn_plan_sizes.argtypes = [vp, szp, szp, szp]
+    L.lrcnn_plan_tensor.argtypes = [vp, i, ip, ip, ip, ip]
+    L.lrcnn_plan_param.argtypes = [vp, i, i, szp, szp]
+    L.lrcnn_plan_nsegs.argtypes = [vp, ip]
+    L.lrcnn_plan_seg.argtypes = [vp, i, ip, ip, ip]
+    L.lrcnn_plan_rows.argtypes = [vp, i, i, i, ip, ip, ip]
+    L.lrcnn_plan_memory.argtypes = [vp, ctypes.POINTER(MemoryReport)]
+    L.lrcnn_forward_rows.argtypes = [vp, vp, vp, vp, vp, sz, vp]
+    L.lrcnn_backward_rows.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lrcnn_step.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, sz, vp]
+    L.lrcnn_step_grads.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lrcnn_sgd.argtypes = [vp, vp, vp, vp, ctypes.c_float, vp]
+    L.lrcnn_profile_enable.argtypes = [vp, i]
+    L.lrcnn_profile_read.argtypes = [vp, i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong),
+                                     ctypes.POINTER(ctypes.c_double), vp]
+    L.lrcnn_profile_reset.argtypes = [vp]
+    L.lrcnn_last_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+    L.lrcnn_last_error.restype = ctypes.c_char_p
+    L.lrcnn_version.restype = ctypes.c_char_p
+    for n in EXPORTS:
+        if n not in ("lrcnn_last_error", "lrcnn_version"):
+            getattr(L, n).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(st):
+    if st != 0:
+        raise LrcnnError(st, lib().lrcnn_last_error().decode())
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor (or an int address)."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return ctypes.c_void_p(t)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def net_ops(net):
+    """Marshal a workloads-style net dict into the C op array."""
+    ops = (Op * len(net["ops"]))()
+    for i, o in enumerate(net["ops"]):
+        kind = {"conv": OP_CONV, "maxpool": OP_MAXPOOL, "add": OP_ADD}[o["kind"]]
+        ops[i] = Op(kind, o["src"], o.get("res", -1) if o.get("res", -1) is not None else -1, o.get("cout", 0),
+                    o.get("k", 1), o.get("s", 1), o.get("p", 0), EPI[o.get("epi", "none")] if kind == OP_CONV else 0,
+                    1 if o.get("relu", False) else 0, 1 if o.get("seg_end", False) else 0)
+    return ops
+
+
+class Plan:
+    """lrcnn_plan wrapper.  mode: column | 2ps | overl; prec: fp32 | bf16."""
+
+    def __init__(self, net, B, mode="2ps", prec="bf16", band_rows=None, n_bands=None, flags=0, rank=0, world=1):
+        L = lib()
+        self.net, self.B, self.mode, self.prec = net, B, mode, prec
+        self._ops = net_ops(net)
+        self._desc = NetDesc(len(net["ops"]), self._ops, B, net["C"], net["H"], net["W"], net["classes"])
+        self._opts = PlanOpts(MODES[mode], PRECS[prec], band_rows or 0, n_bands or 0, rank, world, flags)
+        h = ctypes.c_void_p()
+        _check(L.lrcnn_plan(ctypes.byref(self._desc), ctypes.byref(self._opts), ctypes.byref(h)))
+        self.h = h
+        ws, npar, zl = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        _check(L.lrcnn_plan_sizes(self.h, ctypes.byref(ws), ctypes.byref(npar), ctypes.byref(zl)))
+        self.ws_bytes, self.n_params, self.zl_elems = ws.value, npar.value, zl.value
+        self.elem = 2 if prec == "bf16" else 4
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().lrcnn_plan_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ plan queries
+    def tensor(self, tid):
+        c, cp, h, w = (ctypes.c_int() for _ in range(4))
+        _check(lib().lrcnn_plan_tensor(self.h, tid, ctypes.byref(c), ctypes.byref(cp), ctypes.byref(h), ctypes.byref(w)))
+        return c.value, cp.value, h.value, w.value
+
+    def param(self, op, which):
+        o, n = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(lib().lrcnn_plan_param(self.h, op, which, ctypes.byref(o), ctypes.byref(n)))
+        return o.value, n.value
+
+    def nsegs(self):
+        n = ctypes.c_int()
+        _check(lib().lrcnn_plan_nsegs(self.h, ctypes.byref(n)))
+        return n.value
+
+    def seg(self, s):
+        a, b, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().lrcnn_plan_seg(self.h, s, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+        return a.value, b.value, n.value
+
+    def rows(self, seg, band, tid):
+        lo, a, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().lrcnn_plan_rows(self.h, seg, band, tid, ctypes.byref(lo), ctypes.byref(a), ctypes.byref(b)))
+        return lo.value, a.value, b.value
+
+    def memory(self):
+        m = MemoryReport()
+        _check(lib().lrcnn_plan_memory(self.h, ctypes.byref(m)))
+        return m.as_dict()
+
+    # ------------------------------------------------------------ layouts (marshalling)
+    def pack_params(self, params):
+        """Canonical params (OIHW float arrays, workloads.make_params) -> flat plan layout (float32 numpy)."""
+        flat = np.zeros(self.n_params, dtype=np.float32)
+        for i, op in enumerate(self.net["ops"]):
+            p = params["convs"][i]
+            if p is None:
+                continue
+            off, n = self.param(i, 0)
+            w = np.asarray(p["w"], dtype=np.float64)
+            co, ci, k, _ = w.shape
+            cinp = self.tensor(op["src"])[1]
+            ohwi = np.zeros((co, k, k, cinp))
+            ohwi[..., :ci] = w.transpose(0, 2, 3, 1)
+            assert ohwi.size == n
+            flat[off:off + n] = ohwi.ravel()
+            if op["epi"] == "bias":
+                off, n = self.param(i, 1)
+                flat[off:off + n] = p["b"]
+            elif op["epi"] == "affine":
+                off, n = self.param(i, 1)
+                flat[off:off + n] = p["gamma"]
+                off, n = self.param(i, 2)
+                flat[off:off + n] = p["beta"]
+        L = len(self.net["ops"])
+        cl, clp = self.tensor(L)[0], self.tensor(L)[1]
+        off, n = self.param(L, 0)
+        fw = np.zeros((self.net["classes"], clp))
+        fw[:, :cl] = params["head"]["fc_w"]
+        flat[off:off + n] = fw.ravel()
+        off, n = self.param(L, 1)
+        flat[off:off + n] = params["head"]["fc_b"]
+        return flat
+
+    def unpack_grads(self, flat):
+        """Flat fp32 gradients -> per-op dicts in the canonical (OIHW) layout."""
+        flat = np.asarray(flat, dtype=np.float64)
+        out = []
+        for i, op in enumerate(self.net["ops"]):
+            if op["kind"] != "conv":
+                out.append(None)
+                continue
+            off, n = self.param(i, 0)
+            cin = self.tensor(op["src"])[0]
+            cinp = self.tensor(op["src"])[1]
+            k = op["k"]
+            w = flat[off:off + n].reshape(op["cout"], k, k, cinp)[..., :cin].transpose(0, 3, 1, 2)
+            g = {"w": w}
+            if op["epi"] == "bias":
+                off, n = self.param(i, 1)
+                g["b"] = flat[off:off + n]
+            elif op["epi"] == "affine":
+                off, n = self.param(i, 1)
+                g["gamma"] = flat[off:off + n]
+                off, n = self.param(i, 2)
+                g["beta"] = flat[off:off + n]
+            out.append(g)
+        L = len(self.net["ops"])
+        cl = self.tensor(L)[0]
+        clp = self.tensor(L)[1]
+        off, n = self.param(L, 0)
+        head = {"fc_w": flat[off:off + n].reshape(self.net["classes"], clp)[:, :cl]}
+        off, n = self.param(L, 1)
+        head["fc_b"] = flat[off:off + n]
+        return out, head
+
+    def to_nhwc(self, x_nchw, tid=0):
+        """NCHW float array -> NHWC with channels padded to Cp (float32 numpy)."""
+        c, cp, h, w = self.tensor(tid)
+        x = np.asarray(x_nchw, dtype=np.float64)
+        out = np.zeros((x.shape[0], h, w, cp), dtype=np.float32)
+        out[..., :c] = x.transpose(0, 2, 3, 1)
+        return out
+
+    def from_nhwc(self, y, tid):
+        c, cp, h, w = self.tensor(tid)
+        y = np.asarray(y, dtype=np.float64).reshape(self.B, h, w, cp)
+        return y[..., :c].transpose(0, 3, 1, 2)
+
+    # ------------------------------------------------------------ device calls
+    def forward_rows(self, params, x, zl, ws, stream=None):
+        _check(lib().lrcnn_forward_rows(self.h, _ptr(params), _ptr(x), _ptr(zl), _ptr(ws), self.ws_bytes,
+                                        _stream(stream)))
+
+    def backward_rows(self, params, x, zl, dzl, grads, ws, stream=None):
+        _check(lib().lrcnn_backward_rows(self.h, _ptr(params), _ptr(x), _ptr(zl), _ptr(dzl), _ptr(grads), _ptr(ws),
+                                         self.ws_bytes, _stream(stream)))
+
+    def step(self, master, params, grads, x, labels, lr, loss, ws, stream=None):
+        _check(lib().lrcnn_step(self.h, _ptr(master), _ptr(params), _ptr(grads), _ptr(x), _ptr(labels),
+                                ctypes.c_float(lr), _ptr(loss), _ptr(ws), self.ws_bytes, _stream(stream)))
+
+    def step_grads(self, params, grads, x, labels, loss, ws, stream=None):
+        _check(lib().lrcnn_step_grads(self.h, _ptr(params), _ptr(grads), _ptr(x), _ptr(labels), _ptr(loss),
+                                      _ptr(ws), self.ws_bytes, _stream(stream)))
+
+    def sgd(self, master, params, grads, lr, stream=None):
+        _check(lib().lrcnn_sgd(self.h, _ptr(master), _ptr(params), _ptr(grads), ctypes.c_float(lr),
+                               _stream(stream)))
+
+    def profile(self, enable=True):
+        _check(lib().lrcnn_profile_enable(self.h, 1 if enable else 0))
+
+    def profile_reset(self):
+        _check(lib().lrcnn_profile_reset(self.h))
+
+    def profile_read(self, cls, stream=None):
+        ms, n, fl = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
+        _check(lib().lrcnn_profile_read(self.h, cls, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl),
+                                        _stream(stream)))
+        return ms.value, n.value, fl.value
+
+    def last_launches(self):
+        n = ctypes.c_longlong()
+        _check(lib().lrcnn_last_launch_count(self.h, ctypes.byref(n)))
+        return n.value
+
+
+class DeviceState:
+    """Device buffers for one plan, allocated with torch (the caller owns all device memory)."""
+
+    def __init__(self, plan, device="cuda"):
+        import torch
+        self.plan = plan
+        dt = torch.bfloat16 if plan.prec == "bf16" else torch.float32
+        self.dtype = dt
+        self.ws = torch.empty(plan.ws_bytes, dtype=torch.uint8, device=device)
+        self.params = torch.zeros(plan.n_params, dtype=dt, device=device)
+        self.master = torch.zeros(plan.n_params, dtype=torch.float32, device=device)
+        self.grads = torch.zeros(plan.n_params, dtype=torch.float32, device=device)
+        c, cp, h, w = plan.tensor(0)
+        self.x = torch.zeros((plan.B, h, w, cp), dtype=dt, device=device)
+        cL, cpL, hL, wL = plan.tensor(len(plan.net["ops"]))
+        self.zl = torch.zeros((plan.B, hL, wL, cpL), dtype=dt, device=device)
+        self.dzl = torch.zeros_like(self.zl)
+        self.labels = torch.zeros(plan.B, dtype=torch.int32, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=device)
+
+    def load(self, params=None, x=None, labels=None, dzl=None):
+        import torch
+        if params is not None:
+            flat = torch.from_numpy(self.plan.pack_params(params))
+            self.master.copy_(flat)
+            self.params.copy_(flat.to(self.dtype))
+        if x is not None:
+            self.x.copy_(torch.from_numpy(self.plan.to_nhwc(x)).to(self.dtype))
+        if labels is not None:
+            self.labels.copy_(torch.from_numpy(np.asarray(labels, dtype=np.int32)))
+        if dzl is not None:
+            self.dzl.copy_(torch.from_numpy(self.plan.to_nhwc(dzl, len(self.plan.net["ops"]))).to(self.dtype))
+
+    def forward(self, stream=None):
+        self.plan.forward_rows(self.params, self.x, self.zl, self.ws, stream)
+
+    def backward(self, stream=None):
+        self.plan.backward_rows(self.params, self.x, self.zl, self.dzl, self.grads, self.ws, stream)
+
+    def step(self, lr, stream=None):
+        self.plan.step(self.master, self.params, self.grads, self.x, self.labels, lr, self.loss, self.ws, stream)

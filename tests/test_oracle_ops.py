@@ -303,3 +303,13 @@ def test_sgd_closed_forms():
     lr = 0.1
     new, _, grads, hg, _ = C.step(net, prm, x, lab, lr)
     assert np.allclose(new["convs"][0]["w"], prm["convs"][0]["w"] - lr * grads[0]["w"], rtol=0, atol=0)
+
+
+def test_bf16_store_matches_torch():
+    """The oracle's bf16 storage model equals PyTorch's float32->bfloat16 RNE conversion (library routine)."""
+    torch = pytest.importorskip("torch")
+    a = np.concatenate([R.standard_normal(5000) * 10.0 ** R.integers(-6, 6, 5000),
+                        [0.0, -0.0, 1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -9, 65504.0]])
+    ref = torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(C.bf16_store(a), ref)
+    assert np.array_equal(WL.round_bf16(a), ref)

@@ -1,0 +1,213 @@
+"""Host-side tests of the C-ABI library (no GPU): the library loads and exports
+every symbol include/lrcnn.h declares; the planner's band/halo rows are
+bit-exact against the oracle's brute-force enumerator; errors; memory/FLOP
+accounting against the paper's formulas (oracle/memmodel)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as WL
+from oracle import column as C
+from oracle import enumerate as EN
+from oracle import memmodel as MM
+from oracle import rowcentric as RC
+from paper_2401_11471_b200 import lrcnn as LB
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_header_symbols():
+    hdr = open(os.path.join(ROOT, "include", "lrcnn.h")).read()
+    names = set(re.findall(r"LRCNN_API\s+[\w\s\*]*?\b(lrcnn_\w+)\s*\(", hdr))
+    assert len(names) >= 18
+    L = LB.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(LB.EXPORTS) == names
+    assert b"sm_100a" in L.lrcnn_version()
+
+
+def random_net(rng, allow_res=True):
+    """Random DAG: chains of conv/maxpool with strides, optional residual blocks and checkpoints."""
+    H = int(rng.integers(12, 40))
+    W = int(rng.integers(3, 9))
+    C0 = int(rng.integers(1, 4))
+    ops = []
+    t = 0
+    h, w = H, W
+    n = int(rng.integers(1, 7))
+    for _ in range(n):
+        kind = rng.random()
+        if allow_res and kind < 0.25 and h >= 3:
+            # bottleneck-ish block: a = conv(t); b = conv(a); out = relu(conv1x1(b) + t or proj(t))
+            s = int(rng.integers(1, 3)) if h >= 6 else 1
+            ops.append(WL.conv(t, 3, 1, 1, 0, epi="affine"))
+            a = len(ops)
+            ops.append(WL.conv(a, 3, 3, s, 1, epi="affine"))
+            b = len(ops)
+            if s == 1:
+                ops.append(WL.conv(b, 4, 1, 1, 0, epi="affine", relu=False))
+                c = len(ops)
+                ops.append(WL.conv(t, 4, 1, 1, 0, epi="affine", relu=False))
+                d = len(ops)
+                ops.append(WL.add(c, d, relu=True))
+            else:
+                ops.append(WL.conv(t, 4, 1, 2, 0, epi="affine", relu=False))
+                d = len(ops)
+                ops.append(WL.conv(b, 4, 1, 1, 0, epi="affine", res=d))
+            t = len(ops)
+            h = (h - 1) // s + 1
+            w = (w - 1) // s + 1
+        elif kind < 0.45 and h >= 4 and w >= 2:
+            k = int(rng.choice([2, 3]))
+            s = 2
+            p = int(rng.integers(0, 2)) if k == 3 else 0
+            if (h + 2 * p - k) // s + 1 < 2 or (w + 2 * p - k) // s + 1 < 1:
+                continue
+            ops.append(WL.maxpool(t, k, s, p))
+            t = len(ops)
+            h, w = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        else:
+            k = int(rng.choice([1, 2, 3, 5, 7]))
+            s = int(rng.choice([1, 1, 2]))
+            p = int(rng.integers(0, (k - 1) // 2 + 1))
+            ho, wo = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+            if ho < 2 or wo < 1:
+                continue
+            ops.append(WL.conv(t, int(rng.integers(1, 5)), k, s, p, epi=str(rng.choice(["bias", "affine", "none"])),
+                               relu=bool(rng.random() < 0.8)))
+            t = len(ops)
+            h, w = ho, wo
+        if rng.random() < 0.25:
+            ops[-1]["seg_end"] = True
+    if not ops:
+        ops.append(WL.conv(0, 2, 3, 1, 1))
+    ops[-1]["seg_end"] = False
+    return {"C": C0, "H": H, "W": W, "classes": 3, "ops": ops}
+
+
+def _check_plan_vs_enum(net, mode, band_rows=None, n_bands=None, B=2):
+    plan = LB.Plan(net, B, mode=mode, prec="fp32", band_rows=band_rows, n_bands=n_bands,
+                   flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
+    shp = C.out_hw(net)
+    segs = EN.segments(net)
+    assert plan.nsegs() == len(segs)
+    for s, seg in enumerate(segs):
+        seg_in, ids, out = seg
+        E = EN.band_ends(shp[out][1], band_rows=band_rows, n_bands=n_bands if band_rows is None else None)
+        pin, pout, nb = plan.seg(s)
+        assert (pin, pout, nb) == (seg_in, out, len(E))
+        if mode == "overl":
+            en = EN.enumerate_overl(net, seg, E, shp)
+            for r in range(len(E)):
+                for t in [seg_in] + [i + 1 for i in ids]:
+                    lo, a, b = plan.rows(s, r, t)
+                    elo, ehi = en[r][t]
+                    if t == out:
+                        elo, ehi = (E[r - 1] if r else 0), E[r]
+                    assert (lo, a, b) == (elo, elo, ehi), (net, mode, s, r, t)
+        else:
+            en = EN.enumerate_2ps(net, seg, E, shp)
+            for r in range(len(E)):
+                for t in [i + 1 for i in ids]:
+                    assert plan.rows(s, r, t) == en[r][t], (net, mode, s, r, t, plan.rows(s, r, t), en[r][t])
+    return plan
+
+
+def test_plan_c1_table():
+    net = WL.tiny3(p=1)
+    plan = _check_plan_vs_enum(net, "2ps", band_rows=4, B=1)
+    assert [plan.rows(0, r, 1)[1:] for r in range(8)] == [(0, 6)] + [(6 + 4 * i, 10 + 4 * i) for i in range(6)] + [(30, 32)]
+    _check_plan_vs_enum(net, "overl", band_rows=4, B=1)
+
+
+@pytest.mark.parametrize("mode", ["2ps", "overl"])
+def test_plan_bit_exact_random(mode):
+    """Interval rule == brute-force enumeration on >= 100 random DAG configurations (SURVEY 8(c) pin 7)."""
+    rng = np.random.default_rng(2024 if mode == "2ps" else 77)
+    done = 0
+    while done < 120:
+        net = random_net(rng)
+        try:
+            shp = C.out_hw(net)
+        except ValueError:
+            continue
+        hout = min(shp[s[2]][1] for s in EN.segments(net))
+        if rng.random() < 0.5:
+            kw = {"band_rows": int(rng.integers(1, max(2, hout)))}
+        else:
+            kw = {"n_bands": int(rng.integers(1, 9))}
+        _check_plan_vs_enum(net, mode, **kw)
+        done += 1
+
+
+def test_plan_vgg_and_resnet_like():
+    for segs in ("none", "pool"):
+        net = WL.vgg16(H=224, W=224, segments=segs)
+        for kw in ({"band_rows": 1}, {"n_bands": 4}, {"n_bands": 7}):
+            _check_plan_vs_enum(net, "2ps", **kw)
+            _check_plan_vs_enum(net, "overl", **kw)
+
+
+def test_plan_errors():
+    net = {"C": 1, "H": 4, "W": 4, "classes": 2, "ops": [WL.conv(0, 2, 5, 1, 0)]}
+    with pytest.raises(LB.LrcnnError) as e:
+        LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=2)
+    assert e.value.name == "E_SHAPE"
+    # OverL infeasible: N > H / o^0
+    net = WL.tiny3(p=1, H=16, W=8)
+    with pytest.raises(LB.LrcnnError) as e:
+        LB.Plan(net, 1, mode="overl", prec="fp32", band_rows=1)
+    assert e.value.name == "E_INFEASIBLE"
+    LB.Plan(net, 1, mode="overl", prec="fp32", band_rows=1, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
+    # reading across a checkpoint boundary
+    bad = {"C": 2, "H": 8, "W": 8, "classes": 2,
+           "ops": [WL.conv(0, 2, 3, 1, 1, seg_end=True), WL.conv(1, 2, 3, 1, 1), WL.add(2, 0)]}
+    with pytest.raises(LB.LrcnnError) as e:
+        LB.Plan(bad, 1, mode="2ps", prec="fp32", n_bands=2)
+    assert e.value.name == "E_ARG"
+    with pytest.raises(LB.LrcnnError) as e:
+        LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=2, world=2)
+    assert e.value.name == "E_UNSUPPORTED"
+
+
+def test_memory_and_flops_accounting():
+    for net, B, kw in [(WL.tiny3(p=1), 1, {"band_rows": 4}), (WL.vgg16(H=64, W=64), 2, {"n_bands": 4}),
+                       (WL.vgg16(H=64, W=64, segments="pool"), 2, {"n_bands": 3})]:
+        for mode in ("2ps", "overl", "column"):
+            plan = LB.Plan(net, B, mode=mode, prec="bf16", flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION,
+                           **({} if mode == "column" else kw))
+            m = plan.memory()
+            assert m["omega"] == MM.omega(net, B) * 2                        # Eq. (3)
+            assert m["tau_flops"] == MM.tau(net, B)
+            if mode == "column":     # one segment, one band: the layer-wise dataflow
+                flat = dict(net, ops=[dict(o, seg_end=False) for o in net["ops"]])
+                rp = RC.Plan(flat, "2ps", n_bands=1)
+            else:
+                rp = RC.Plan(net, mode, **kw)
+            assert m["fwd_flops"] == MM.executed_fwd_flops(rp, B)
+            if mode == "2ps":
+                # 2PS cache = B * sum over boundaries and tensors of cached rows * W * Cp * 2 bytes
+                exp = 0
+                for s, (E, bands) in enumerate(rp.bands):
+                    seg_in, ids, out = rp.segs[s]
+                    for r in range(1, len(bands)):
+                        for i in ids:
+                            t = i + 1
+                            if t == out:
+                                continue
+                            lo, a, b = bands[r][t]
+                            _, cp, _, w = plan.tensor(t)
+                            exp += B * (a - lo) * w * cp * 2
+                assert m["halo_cache"] == exp
+            if mode == "column":
+                assert m["halo_cache"] == 0
+
+
+def test_c1_cache_is_k_minus_s():
+    """C1: 2 cached rows per tensor per boundary (k - s = 2)."""
+    plan = LB.Plan(WL.tiny3(p=1), 1, mode="2ps", prec="fp32", band_rows=4)
+    m = plan.memory()
+    assert m["halo_cache"] == 1 * 7 * 2 * (32 * 8) * 4 * 2    # B * (N-1) * c * W*Cp * 4B * 2 tensors
