@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py -- row-centric VGG-16 training throughput on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one lrcnn_step (Alg. 1 l.5-24: row-centric FP, head, row-centric BP with
+recompute, SGD) over one batch of synthetic input; workload C2: VGG-16 conv stack,
+224x224x3, batch 32 per GPU, bf16, 2PS-H (2PS bands inside per-pool checkpoint
+segments).  N>1: one process per GPU (torchrun), each rank trains its own batch
+(weak scaling) and the fp32 gradients are all-reduced with NCCL before SGD.
+Prints ONE JSON line (rank 0).  --impl reference times the fp64 CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as WL  # noqa: E402
+
+METRIC = "train images/s (VGG-16 conv stack, 224x224x3, row-centric 2PS-H, bf16)"
+UNIT = "images/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--hw", type=int, default=224)
+    ap.add_argument("--mode", default="2ps", choices=["2ps", "overl", "column"])
+    ap.add_argument("--segments", default="pool", choices=["pool", "none"])
+    ap.add_argument("--n-bands", type=int, default=4)
+    ap.add_argument("--band-rows", type=int, default=0)
+    ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
+    ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index):
+        super().__init__(daemon=True)
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def run(self):
+        while self.nv is not None and not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def result(self):
+        self.stop_ev.set()
+        self.join(timeout=1)
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_net(a):
+    return WL.vgg16(H=a.hw, W=a.hw, segments=a.segments)
+
+
+def cpu_baseline(a, steps=1):
+    """The fp64 oracle (column dataflow, as it stands) on a bounded sample: one image of the
+    workload at full 224x224, one training step (FP, head, BP, SGD), all host cores."""
+    import oracle
+    from oracle import column as C
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    net = make_net(a)
+    params = WL.make_params(net, seed=2)
+    x = WL.make_input(net, 1, seed=0)
+    lab = WL.make_labels(net, 1)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        params, loss, _, _, _ = C.step(net, params, x, lab, 0.01)
+        times.append(time.perf_counter() - t0)
+    return {"value": 1.0 / statistics.mean(times), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "1 image of the C2 batch at 224x224x3, one fp64 column step (FP+head+BP+SGD), "
+                      "OpenMP over (b, c_out), mean of %d" % steps,
+            "s_per_image": statistics.mean(times)}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_baseline(a, steps=1)             # warm-up/first measurement
+    import oracle
+    from oracle import column as C
+    net = make_net(a)
+    params = WL.make_params(net, seed=2)
+    x = WL.make_input(net, 1, seed=0)
+    lab = WL.make_labels(net, 1)
+    for _ in range(max(0, a.warmup - 1)):
+        params, _, _, _, _ = C.step(net, params, x, lab, 0.01)
+    times = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        params, _, _, _, _ = C.step(net, params, x, lab, 0.01)
+        times.append(time.perf_counter() - t0)
+    ms = 1000.0 * statistics.mean(times)
+    v = 1000.0 / ms
+    cb = dict(cb, value=v, sample=cb["sample"].replace("mean of 1", "mean of %d" % a.steps))
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+                      "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": "C2 VGG-16 224x224x3 (1-image bounded sample per step)",
+                                 "global_batch": 1, "parallelism": "cpu"},
+                      "cpu_baseline": cb,
+                      "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2401_11471_b200 import lrcnn as LB
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    net = make_net(a)
+    B = a.batch
+    flags = LB.FLAG_NO_TCGEN05 if a.simt else 0
+    kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}
+    if a.mode == "column":
+        kw = {}
+    plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
+    mem = plan.memory()
+
+    torch.cuda.reset_peak_memory_stats(dev)
+    ds = LB.DeviceState(plan, device=dev)
+    params = WL.make_params(net, seed=2)
+    x_np = WL.make_input(net, B, seed=1000 + rank)
+    lab_np = WL.make_labels(net, B, seed=1 + rank)
+    ds.load(params=params, x=x_np, labels=lab_np)
+    xi_bytes = ds.x.numel() * ds.x.element_size()
+    lab_bytes = ds.labels.numel() * 4
+    lr = 1e-3
+
+    def one_step():
+        if world > 1:
+            plan.step_grads(ds.params, ds.grads, ds.x, ds.labels, ds.loss, ds.ws, stream)
+            dist.all_reduce(ds.grads)          # wgrad all-reduce (NCCL, fp32, sum)
+            ds.grads.mul_(1.0 / world)
+            plan.sgd(ds.master, ds.params, ds.grads, lr, stream)
+        else:
+            plan.step(ds.master, ds.params, ds.grads, ds.x, ds.labels, lr, ds.loss, ds.ws, stream)
+
+    for _ in range(a.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated(dev)
+    xi = ds.params.numel() * ds.params.element_size() + (ds.master.numel() + ds.grads.numel()) * 4
+    launches_per_step = plan.last_launches()
+
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region (device)
+    sampler = ClockSampler(local)
+    sampler.start()
+    times = []
+    barrier()
+    for _ in range(a.steps):
+        flush.zero_()                               # L2 flushed between timed steps (untimed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one_step()
+        e1.record(stream)
+        times.append((e0, e1))
+    barrier()
+    clocks = sampler.result()
+    ms = [s.elapsed_time(e) for s, e in times]
+    ms_step = sum(ms) / len(ms)
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t)
+    value = B * world / (ms_step / 1000.0)
+
+    # ---------------------------------------------------------------- end-to-end through the public API
+    x_host = ds.x.cpu().pin_memory()
+    lab_host = ds.labels.cpu().pin_memory()
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    e2e = []
+    barrier()
+    for _ in range(a.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ds.x.copy_(x_host, non_blocking=True)
+        ds.labels.copy_(lab_host, non_blocking=True)
+        one_step()
+        loss_host.copy_(ds.loss, non_blocking=True)
+        e1.record(stream)
+        e2e.append((e0, e1))
+    barrier()
+    ms_e2e = sum(s.elapsed_time(e) for s, e in e2e) / len(e2e)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t)
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    plan.profile(True)
+    plan.profile_reset()
+    for _ in range(max(2, min(a.steps, 5))):
+        flush.zero_()
+        one_step()
+    tc_ms, tc_n, tc_fl = plan.profile_read(0, stream)
+    wg_ms, wg_n, wg_fl = plan.profile_read(1, stream)
+    ot_ms, ot_n, _ = plan.profile_read(2, stream)
+    plan.profile(False)
+    peaks, peak_src = measured_peaks()
+    achieved = tc_fl / (tc_ms / 1000.0) / 1e12 if tc_ms > 0 else 0.0
+    peak_tf = peaks.get("bf16_tflops_sustained", 1385.7)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get("conv_fwd_dgrad_bytes_per_launch")
+    except Exception:
+        pass
+    prof_steps = max(2, min(a.steps, 5))
+    roofline = {"bound": "tensor", "kernel": "conv FP + dgrad (implicit GEMM)", "achieved": achieved,
+                "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf if peak_tf else None,
+                "traffic": traffic, "peak_source": "%s bf16_tflops_sustained" % peak_src,
+                "launches_per_step": tc_n / prof_steps, "ms_per_step": tc_ms / prof_steps,
+                "share_of_step": (tc_ms / prof_steps) / ms_step,
+                "wgrad": {"achieved": wg_fl / (wg_ms / 1000.0) / 1e12 if wg_ms else 0.0, "ms_per_step": wg_ms / prof_steps},
+                "other_ms_per_step": ot_ms / prof_steps}
+
+    # ---------------------------------------------------------------- memory vs layer-wise (COLUMN)
+    mem_rep = {"peak_allocated_bytes": peak, "xi_bytes": xi, "feature_map_bytes": peak - xi,
+               "plan": {k: mem[k] for k in ("omega", "band_act", "band_delta", "halo_cache", "carry",
+                                            "checkpoints", "delta_full", "workspace")}}
+    cpu = None
+    if not a.no_baselines and rank == 0 and a.mode != "column":
+        del ds, flush
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(dev)
+        cplan = LB.Plan(net, B, mode="column", prec="bf16", flags=flags)
+        cds = LB.DeviceState(cplan, device=dev)
+        cds.load(params=params, x=x_np, labels=lab_np)
+        cplan.step(cds.master, cds.params, cds.grads, cds.x, cds.labels, lr, cds.loss, cds.ws, stream)
+        torch.cuda.synchronize()
+        cpeak = torch.cuda.max_memory_allocated(dev)
+        mem_rep["layerwise_peak_allocated_bytes"] = cpeak
+        mem_rep["layerwise_feature_map_bytes"] = cpeak - xi
+        mem_rep["reduction_x"] = (cpeak - xi) / max(1, peak - xi)
+        del cds
+        cpu = cpu_baseline(a)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+               "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[0,1) images, U{0..9} labels)",
+               "config": {"workload": "C2: VGG-16 conv stack 224x224x3, batch %d per GPU, bf16" % B,
+                          "global_batch": B * world, "seq_len": None,
+                          "parallelism": "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU",
+                          "mode": a.mode, "segments": a.segments, "bands": kw,
+                          "l2": "flushed (512 MB write) between timed steps"},
+               "clocks": clocks,
+               "e2e": {"value": B * world / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": xi_bytes + lab_bytes,
+                       "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e},
+               "gpu_launches": launches_per_step * a.steps,
+               "roofline": roofline, "memory": mem_rep, "cpu_baseline": cpu,
+               "tensor_core_kernels": (not a.simt)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
