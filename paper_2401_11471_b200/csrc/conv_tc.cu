@@ -1,8 +1,554 @@
-// conv_tc.cu -- tcgen05 implicit-GEMM convolution kernels (sm_100a).  Placeholder.
+// conv_tc.cu -- tcgen05 implicit-GEMM convolution kernels for sm_100a.
+//
+// The per-band convolutions of the row-centric sweep (Eq. (4)/(5))
+// are dense contractions and run on the 5th-generation tensor cores:
+//
+//   FP    D[pixel, co] = sum_{ky,kx,ci} X[y-p+ky, x-p+kx, ci] W[co,ky,kx,ci]   (+ fused epilogue)
+//   dgrad the same kernel on the band delta with the flipped, transposed weights
+//         W'[ci,ky',kx',co] = gamma[co] W[co,k-1-ky',k-1-kx',ci] and padding k-1-p;
+//         epilogue: delta_in = gate(act_in) * (delta_in + acc)  (gate-on-write)
+//   wgrad dW[co,ky,kx,ci] += sum_pixels dY[pixel,co] X[pixel+off,ci]  (K = band pixels)
+//
+// Structure (one CTA per SM, persistent over tiles, warp-specialised, 192 threads):
+//   warp 0      TMA producer: a 128-pixel rectangle (TW x TH of one image) x 64 channels
+//               of the band input per stage, SWIZZLE_128B; the rows of the band are
+//               addressed with band-relative coordinates so TMA's out-of-bounds zero
+//               fill IS the semi-closed padding: rows < 0 or >= H and
+//               rows outside the band's valid range read as zero.
+//   warp 1      TMEM allocation + single-thread tcgen05.mma issue (M=128, N=BN, K=16),
+//               tcgen05.commit releases smem stages and hands accumulators to the epilogue.
+//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns), bias/affine, residual, ReLU,
+//               bf16 pack, 16-byte stores (FP) or the gated delta accumulate (dgrad);
+//               wgrad: gamma scale and fp32 red.add into the flat gradient.
+// Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps the MMAs
+// of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
 #include "tc.hpp"
+#include "tc_ptx.cuh"
+
 namespace lrcnn {
-bool tc_available() { return false; }
-bool tc_conv_fwd(const ConvFwdArgs &, cudaStream_t) { return false; }
-bool tc_conv_dgrad(const DgradArgs &, cudaStream_t) { return false; }
-bool tc_conv_wgrad(const WgradArgs &, cudaStream_t) { return false; }
+
+typedef __nv_bfloat16 bf16;
+
+struct TcConv {
+    View out, res, act;
+    const bf16 *bias, *beta;
+    int mode;              // 0 = forward epilogue, 1 = dgrad (gated accumulate)
+    int epi, relu, gate, has_res, c_real, n_out;
+    int out_a, out_b, Wo, B;
+    int TW, TH, tiles_x, tiles_y, m_tiles, n_tiles;
+    int k, pad, in_base, cin_chunks, k_steps;
+};
+
+struct TcWgrad {
+    float *dw;
+    const bf16 *gamma;
+    int k, pad, c_out, cin_p;
+    int TW, TH, tiles_x, tiles_y, pix_tiles, per_split, splits;
+    int co_tiles, ci_tiles, items;
+    int out_a, dy_base, x_base;
+};
+
+static constexpr int kThreads = 192;
+static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
+
+template <int BN>
+struct ConvCfg {
+    static constexpr int kStageBytes = kABytes + BN * 128;
+    static constexpr int kStages = (192 * 1024) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr uint32_t kTmemCols = 2 * BN;
+};
+
+__device__ __forceinline__ float bf2f(uint16_t u) { return __uint_as_float(((uint32_t)u) << 16); }
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+// ------------------------------------------------------------------ conv FP / dgrad
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcConv P) {
+    using Cfg = ConvCfg<BN>;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + S * kABytes;
+    uint64_t *full = (uint64_t *)(sB + S * BN * 128);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tslot = (uint32_t *)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, Cfg::kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int num_tiles = P.m_tiles * P.n_tiles;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
+                const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                const int y0 = P.out_a + ty * P.TH, x0 = tx * P.TW, n0 = nt * BN;
+                for (int ks = 0; ks < P.k_steps; ++ks) {
+                    const int tap = ks / P.cin_chunks, c = ks - tap * P.cin_chunks;
+                    const int ky = tap / P.k, kx = tap - ky * P.k;
+                    ptx::mbar_wait(empty + stage, phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(full + stage, kABytes + BN * 128);
+                    ptx::tma_load_4d(sA + stage * kABytes, &tmA, full + stage, c * 64, x0 - P.pad + kx,
+                                     y0 - P.pad + ky - P.in_base, b);
+                    ptx::tma_load_2d(sB + stage * BN * 128, &tmB, full + stage, (tap * P.cin_chunks + c) * 64, n0);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int ks = 0; ks < P.k_steps; ++ks) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * kABytes);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * BN * 128);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        uint64_t ad = ptx::smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                        uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 32, 16, 1024);
+                        ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
+                    }
+                    ptx::umma_commit(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(tfull + acc);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        const int ew = warp & 3;                  // TMEM lane quarter this warp may access
+        const int m = ew * 32 + lane;             // accumulator row = pixel in the tile
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
+            const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+            const int y = P.out_a + ty * P.TH + m / P.TW, x = tx * P.TW + m % P.TW, n0 = nt * BN;
+            const bool valid = y < P.out_b && x < P.Wo;
+            const long long pix = valid ? (long long)b * P.out.bs + ((long long)(y - P.out.base) * P.out.W + x) * P.out.Cp : 0;
+            ptx::mbar_wait(tfull + acc, aphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
+                ptx::tmem_ld_wait();
+                if (!valid) continue;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int n = n0 + c * 32 + g * 8;
+                    if (n >= P.n_out) break;
+                    float f[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[g * 8 + j]);
+                    bf16 *dst = (bf16 *)P.out.p + pix + n;
+                    if (P.mode == 0) {
+                        if (P.epi != 0) {
+                            uint4 bb = *reinterpret_cast<const uint4 *>(P.bias + n);
+                            const uint16_t *bh = reinterpret_cast<const uint16_t *>(&bb);
+                            uint4 be = P.epi == 2 ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
+                            const uint16_t *beh = reinterpret_cast<const uint16_t *>(&be);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                float bj = n + j < P.c_real ? bf2f(bh[j]) : 0.f;
+                                if (P.epi == 1) f[j] += bj;
+                                else f[j] = n + j < P.c_real ? bj * f[j] + bf2f(beh[j]) : 0.f;
+                            }
+                        }
+                        if (P.has_res) {
+                            uint4 rr = *reinterpret_cast<const uint4 *>(
+                                (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                                ((long long)(y - P.res.base) * P.res.W + x) * P.res.Cp + n);
+                            const uint16_t *rh = reinterpret_cast<const uint16_t *>(&rr);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) f[j] += bf2f(rh[j]);
+                        }
+                        if (P.relu) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
+                        }
+                    } else {
+                        uint4 od = *reinterpret_cast<const uint4 *>(dst);
+                        const uint16_t *oh = reinterpret_cast<const uint16_t *>(&od);
+                        uint4 ac = make_uint4(0, 0, 0, 0);
+                        if (P.gate)
+                            ac = *reinterpret_cast<const uint4 *>(
+                                (const bf16 *)P.act.p + (long long)b * P.act.bs +
+                                ((long long)(y - P.act.base) * P.act.W + x) * P.act.Cp + n);
+                        const uint16_t *ah = reinterpret_cast<const uint16_t *>(&ac);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            f[j] += bf2f(oh[j]);
+                            if (P.gate && !(bf2f(ah[j]) > 0.f)) f[j] = 0.f;
+                        }
+                    }
+                    uint4 o;
+                    o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
+                    *reinterpret_cast<uint4 *>(dst) = o;
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty + acc);
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ wgrad
+// M = 128 output channels (two 64-channel MN-major boxes of the band delta),
+// N = BN input channels (BN/64 MN-major boxes of the shifted band input),
+// K = 128 band pixels per stage (8 MMAs of K=16).  Work item = (co tile, tap, ci tile,
+// pixel split); fp32 partial sums are added with red.global into the flat gradient.
+static constexpr int kWgA = 2 * kABytes;
+template <int BN>
+struct WgCfg {
+    static constexpr int kStageBytes = kWgA + (BN / 64) * kABytes;
+    static constexpr int kStages = (192 * 1024) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr uint32_t kTmemCols = 2 * BN;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad_tc(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
+    using Cfg = WgCfg<BN>;
+    constexpr int S = Cfg::kStages;
+    constexpr int SB = Cfg::kStageBytes;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + S * SB);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tslot = (uint32_t *)(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmD);
+        ptx::prefetch_tmap(&tmX);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, Cfg::kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int taps = P.k * P.k;
+
+    auto decode = [&](int item, int &cot, int &tap, int &cit, int &split) {
+        split = item % P.splits;
+        int r = item / P.splits;
+        cit = r % P.ci_tiles; r /= P.ci_tiles;
+        tap = r % taps;
+        cot = r / taps;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                int cot, tap, cit, split;
+                decode(item, cot, tap, cit, split);
+                const int ky = tap / P.k, kx = tap - ky * P.k;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                for (int pt = p0; pt < p1; ++pt) {
+                    const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                    const int y0 = P.out_a + ty * P.TH, x0 = tx * P.TW;
+                    ptx::mbar_wait(empty + stage, phase ^ 1);
+                    uint8_t *st = smem + stage * SB;
+                    ptx::mbar_arrive_expect_tx(full + stage, SB);
+                    ptx::tma_load_4d(st, &tmD, full + stage, cot * 128, x0, y0 - P.dy_base, b);
+                    ptx::tma_load_4d(st + kABytes, &tmD, full + stage, cot * 128 + 64, x0, y0 - P.dy_base, b);
+#pragma unroll
+                    for (int h = 0; h < BN / 64; ++h)
+                        ptx::tma_load_4d(st + kWgA + h * kABytes, &tmX, full + stage, cit * BN + h * 64,
+                                         x0 - P.pad + kx, y0 - P.pad + ky - P.x_base, b);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                int cot, tap, cit, split;
+                decode(item, cot, tap, cit, split);
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(smem + stage * SB);
+                    const uint32_t b0 = a0 + kWgA;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        // MN-major SW128: 64-element MN chunks LBO = 16 KB apart, 8-row K groups SBO = 1 KB
+                        uint64_t ad = ptx::smem_desc_sw128(a0 + kk * 2048, kABytes, 1024);
+                        uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 2048, kABytes, 1024);
+                        ptx::umma_bf16(d, ad, bd, idesc, (pt != p0 || kk != 0) ? 1u : 0u);
+                    }
+                    ptx::umma_commit(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(tfull + acc);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        const int ew = warp & 3;
+        const int m = ew * 32 + lane;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int cot, tap, cit, split;
+            decode(item, cot, tap, cit, split);
+            const int co = cot * 128 + m;
+            const float gsc = (P.gamma && co < P.c_out) ? __bfloat162float(P.gamma[co]) : 1.f;
+            float *dst = P.dw + ((long long)co * taps + tap) * P.cin_p;
+            ptx::mbar_wait(tfull + acc, aphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
+                ptx::tmem_ld_wait();
+                if (co >= P.c_out) continue;
+                const int ci0 = cit * BN + c * 32;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (ci0 + j < P.cin_p) atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty + acc);
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    });
+    return fn;
+}
+
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// 4D map over a band View: dims (Cp, W, rows, B); box (64, TW, TH, 1); 128B swizzle.
+static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH) {
+    auto fn = encode_fn();
+    if (!fn || v.rows <= 0) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)v.Cp, (cuuint64_t)v.W, (cuuint64_t)v.rows, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)v.Cp * 2, (cuuint64_t)v.W * v.Cp * 2, (cuuint64_t)v.bs * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)TW, (cuuint32_t)TH, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+static bool encode_w(CUtensorMap *m, const void *w, int rows, int K, int BN) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)BN};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(w), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// choose a 128-pixel rectangle TW x TH (TW*TH = 128) minimising padded pixels
+static void pick_tile(int rows, int W, int &TW, int &TH) {
+    long best = -1;
+    for (int tw = 128; tw >= 4; tw >>= 1) {
+        int th = 128 / tw;
+        long cost = (long)((W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+        if (best < 0 || cost < best) { best = cost; TW = tw; TH = th; }
+    }
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+bool tc_available() { return true; }
+
+template <int BN>
+static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, int tiles, cudaStream_t st) {
+    using Cfg = ConvCfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    k_conv_tc<BN><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, P);
+    return true;
+}
+
+static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, int cin_p, int k, int pad,
+                        cudaStream_t st) {
+    if (in.Cp % 64 || cin_p % 64 || P.n_out < 64 || P.n_out % 16) return false;
+    if (!aligned16(in.p) || !aligned16(w) || !aligned16(P.out.p)) return false;
+    int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
+    const int rows = P.out_b - P.out_a;
+    if (rows <= 0) return true;
+    pick_tile(rows, P.Wo, P.TW, P.TH);
+    P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    P.n_tiles = (P.n_out + BN - 1) / BN;
+    P.k = k; P.pad = pad; P.in_base = in.base;
+    P.cin_chunks = cin_p / 64;
+    P.k_steps = k * k * P.cin_chunks;
+    CUtensorMap A, Bm;
+    if (!encode_view(&A, in, P.B, P.TW, P.TH)) return false;
+    if (!encode_w(&Bm, w, w_rows, k * k * cin_p, BN)) return false;
+    int tiles = P.m_tiles * P.n_tiles;
+    if (BN == 64) return launch_conv<64>(P, A, Bm, tiles, st);
+    if (BN == 128) return launch_conv<128>(P, A, Bm, tiles, st);
+    return launch_conv<256>(P, A, Bm, tiles, st);
+}
+
+bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
+    if (a.s != 1) return false;
+    TcConv P{};
+    P.out = a.out; P.res = a.res; P.has_res = a.res.p != nullptr;
+    P.bias = (const bf16 *)a.b; P.beta = (const bf16 *)a.beta;
+    P.mode = 0; P.epi = a.epi; P.relu = a.relu; P.gate = 0; P.c_real = a.c_out; P.n_out = a.out.Cp;
+    P.out_a = a.a; P.out_b = a.b_; P.Wo = a.out.W; P.B = a.B;
+    if (P.epi != 0 && !aligned16(P.bias)) return false;
+    if (P.has_res && (a.res.Cp % 8 || !aligned16(a.res.p))) return false;
+    return conv_common(P, a.in, a.w, a.c_out, a.in.Cp, a.k, a.p, st);
+}
+
+bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
+    if (a.s != 1 || !a.wt) return false;
+    TcConv P{};
+    P.out = a.dx; P.act = a.act;
+    P.mode = 1; P.epi = 0; P.relu = 0; P.gate = a.gate; P.c_real = a.dx.Cp; P.n_out = a.dx.Cp;
+    P.out_a = a.ra; P.out_b = a.rb; P.Wo = a.dx.W; P.B = a.B;
+    if (a.gate && (!aligned16(a.act.p) || a.act.Cp != a.dx.Cp)) return false;
+    // input = the band delta rows [a, b) (view already restricted), weights W'[Cin_p][k][k][Cout_p]
+    return conv_common(P, a.dy, a.wt, a.dx.Cp, a.dy.Cp, a.k, a.k - 1 - a.p, st);
+}
+
+template <int BN>
+static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorMap &X, cudaStream_t st) {
+    using Cfg = WgCfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_wgrad_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    int grid = P.items < num_sms() ? P.items : num_sms();
+    k_wgrad_tc<BN><<<grid, kThreads, Cfg::kSmem, st>>>(D, X, P);
+    return true;
+}
+
+bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
+    if (a.s != 1) return false;
+    const View &dy = a.dy, &x = a.x;
+    if (dy.Cp % 64 || x.Cp % 64 || !aligned16(dy.p) || !aligned16(x.p)) return false;
+    const int rows = a.b - a.a;
+    if (rows <= 0) return true;
+    TcWgrad P{};
+    P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
+    pick_tile(rows, dy.W, P.TW, P.TH);
+    P.tiles_x = (dy.W + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
+    const int BN = x.Cp >= 128 ? 128 : 64;
+    P.co_tiles = (dy.Cp + 127) / 128;
+    P.ci_tiles = (x.Cp + BN - 1) / BN;
+    const int base_items = P.co_tiles * a.k * a.k * P.ci_tiles;
+    int splits = (2 * num_sms() + base_items - 1) / base_items;
+    if (splits > P.pix_tiles) splits = P.pix_tiles;
+    if (splits < 1) splits = 1;
+    P.per_split = (P.pix_tiles + splits - 1) / splits;
+    P.splits = (P.pix_tiles + P.per_split - 1) / P.per_split;
+    P.items = base_items * P.splits;
+    P.out_a = a.a; P.dy_base = dy.base; P.x_base = x.base;
+    CUtensorMap D, X;
+    if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
+    if (!encode_view(&X, x, a.B, P.TW, P.TH)) return false;
+    if (BN == 64) return launch_wgrad<64>(P, D, X, st);
+    return launch_wgrad<128>(P, D, X, st);
+}
+
 }  // namespace lrcnn
