@@ -203,6 +203,8 @@ LRCNN_API lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan);
 
 /* Number of kernel launches the last forward/backward/step enqueued. */
 LRCNN_API lrcnn_status lrcnn_last_launch_count(const lrcnn_plan_t *plan, long long *launches);
+/* Of those, how many were tcgen05 tensor-core convolution kernels (FP, dgrad, wgrad). */
+LRCNN_API lrcnn_status lrcnn_last_tc_launch_count(const lrcnn_plan_t *plan, long long *launches);
 
 LRCNN_API const char *lrcnn_last_error(void);
 LRCNN_API const char *lrcnn_version(void);

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_arrive_expect_tx(full + stage, kABytes + BN * 128);
                     ptx::tma_load_4d(sA + stage * kABytes, &tmA, full + stage, c * 64, x0 - P.pad + kx,
                                      y0 - P.pad + ky - P.in_base, b);
-                    ptx::tma_load_2d(sB + stage * BN * 128, &tmB, full + stage, (tap * P.cin_chunks + c) * 64, n0);
+                    ptx::tma_load_3d(sB + stage * BN * 128, &tmB, full + stage, c * 64, tap, n0);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -419,14 +419,16 @@ static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH) {
     return r == CUDA_SUCCESS;
 }
 
-static bool encode_w(CUtensorMap *m, const void *w, int rows, int K, int BN) {
+// 3D map over OHWI weights [rows][taps][cin_p]: box (64 channels, 1 tap, BN rows); channels
+// beyond cin_p (small-channel layers, e.g. the padded RGB input) are zero-filled by TMA.
+static bool encode_w(CUtensorMap *m, const void *w, int rows, int taps, int cin_p, int BN) {
     auto fn = encode_fn();
     if (!fn) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)BN};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(w), dims, strides, box, es,
+    cuuint64_t dims[3] = {(cuuint64_t)cin_p, (cuuint64_t)taps, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)cin_p * 2, (cuuint64_t)taps * cin_p * 2};
+    cuuint32_t box[3] = {64, 1, (cuuint32_t)BN};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(w), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -462,7 +464,7 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
 
 static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, int cin_p, int k, int pad,
                         cudaStream_t st) {
-    if (in.Cp % 64 || cin_p % 64 || P.n_out < 64 || P.n_out % 16) return false;
+    if (in.Cp % 8 || cin_p != in.Cp || P.n_out < 8 || P.n_out % 8) return false;
     if (!aligned16(in.p) || !aligned16(w) || !aligned16(P.out.p)) return false;
     int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
     const int rows = P.out_b - P.out_a;
@@ -473,11 +475,11 @@ static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, in
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
     P.n_tiles = (P.n_out + BN - 1) / BN;
     P.k = k; P.pad = pad; P.in_base = in.base;
-    P.cin_chunks = cin_p / 64;
+    P.cin_chunks = (cin_p + 63) / 64;
     P.k_steps = k * k * P.cin_chunks;
     CUtensorMap A, Bm;
     if (!encode_view(&A, in, P.B, P.TW, P.TH)) return false;
-    if (!encode_w(&Bm, w, w_rows, k * k * cin_p, BN)) return false;
+    if (!encode_w(&Bm, w, w_rows, k * k, cin_p, BN)) return false;
     int tiles = P.m_tiles * P.n_tiles;
     if (BN == 64) return launch_conv<64>(P, A, Bm, tiles, st);
     if (BN == 128) return launch_conv<128>(P, A, Bm, tiles, st);
@@ -524,7 +526,7 @@ static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorM
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     if (a.s != 1) return false;
     const View &dy = a.dy, &x = a.x;
-    if (dy.Cp % 64 || x.Cp % 64 || !aligned16(dy.p) || !aligned16(x.p)) return false;
+    if (dy.Cp % 8 || x.Cp % 8 || !aligned16(dy.p) || !aligned16(x.p)) return false;
     const int rows = a.b - a.a;
     if (rows <= 0) return true;
     TcWgrad P{};

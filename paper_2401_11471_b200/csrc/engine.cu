@@ -140,7 +140,7 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
         A.a = a; A.b_ = b; A.B = P.net.B;
         ProfScope ps(R, 0, conv_flops(P, o, b - a));
         ++P.launches;
-        if (P.use_tc && tc_conv_fwd(A, R.st)) { CK(cudaGetLastError()); return LRCNN_OK; }
+        if (P.use_tc && tc_conv_fwd(A, R.st)) { ++P.tc_launches; CK(cudaGetLastError()); return LRCNN_OK; }
         CK(simt_conv_fwd(R.prec, A, R.st));
     } else if (o.d.kind == LRCNN_OP_MAXPOOL) {
         PoolArgs A;
@@ -242,7 +242,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
             ++P.launches;
             ProfScope ps(R, 1, conv_flops(P, o, b - a));
-            if (!(P.use_tc && tc_conv_wgrad(A, R.st))) CK(simt_conv_wgrad(R.prec, A, R.st));
+            if (P.use_tc && tc_conv_wgrad(A, R.st)) ++P.tc_launches;
+            else CK(simt_conv_wgrad(R.prec, A, R.st));
             CK(cudaGetLastError());
         }
         if (need_dx) {
@@ -254,7 +255,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
             ++P.launches;
             ProfScope ps(R, 0, conv_flops(P, o, b - a));
-            if (!(P.use_tc && tc_conv_dgrad(A, R.st))) CK(simt_conv_dgrad(R.prec, A, R.st));
+            if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
+            else CK(simt_conv_dgrad(R.prec, A, R.st));
             CK(cudaGetLastError());
         }
         if (o.d.res >= 0) {
@@ -465,7 +467,7 @@ lrcnn_status lrcnn_forward_rows(lrcnn_plan_t *plan, const void *params, const vo
     Plan &P = plan->P;
     lrcnn_status st = check_ws(P, ws, ws_bytes);
     if (st != LRCNN_OK) return st;
-    P.launches = 0;
+    P.launches = 0; P.tc_launches = 0;
     Run R{P, (char *)ws, (const char *)params, x, zl, nullptr, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     P.fwd_done = false;
     st = run_forward(R);
@@ -482,7 +484,7 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
     if (st != LRCNN_OK) return st;
     if (!P.fwd_done || P.fwd_ws != ws || P.fwd_params != params || P.fwd_x != x)
         return fail(LRCNN_E_STATE, "backward_rows needs a matching forward_rows (same params, x, ws)");
-    P.launches = 0;
+    P.launches = 0; P.tc_launches = 0;
     Run R{P, (char *)ws, (const char *)params, x, (void *)zl, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     const int L = P.net.n_ops;
     const TensorInfo &z = P.t[L];
@@ -502,7 +504,7 @@ lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *gra
     Plan &P = plan->P;
     lrcnn_status st = check_ws(P, ws, ws_bytes);
     if (st != LRCNN_OK) return st;
-    P.launches = 0;
+    P.launches = 0; P.tc_launches = 0;
     char *w = (char *)ws;
     Run R{P, w, (const char *)params, x, w + P.zl_off, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     if ((st = run_forward(R)) != LRCNN_OK) return st;
@@ -532,10 +534,7 @@ lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *
     if (!plan || !master || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
     lrcnn_status st = lrcnn_step_grads(plan, params, grads, x, labels, loss_dev, ws, ws_bytes, stream);
     if (st != LRCNN_OK) return st;
-    long long n = plan->P.launches;
-    st = lrcnn_sgd(plan, master, params, grads, lr, stream);
-    plan->P.launches += n;
-    return st;
+    return lrcnn_sgd(plan, master, params, grads, lr, stream);   // adds its own launch
 }
 
 
@@ -581,6 +580,12 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
     if (ms) *ms = P.prof[cls].ms;
     if (launches) *launches = P.prof[cls].launches;
     if (flops) *flops = P.prof[cls].flops;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_last_tc_launch_count(const lrcnn_plan_t *plan, long long *launches) {
+    if (!plan || !launches) return fail(LRCNN_E_ARG, "bad args");
+    *launches = plan->P.tc_launches;
     return LRCNN_OK;
 }
 

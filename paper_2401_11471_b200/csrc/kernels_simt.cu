@@ -145,38 +145,142 @@ __global__ void k_conv_wgrad(WgradArgs A) {
 }
 
 // ------------------------------------------------------------------ bias / affine grads
+// db[c] += sum_pixels dy[p, c]  (BIAS);  AFFINE: dbeta[c] += sum dy, dgamma[c] += sum dy * c_raw
+// with c_raw = (t - beta - res)/gamma.  Block = (channel vectors of 8) x (pixel lanes);
+// coalesced 8-channel loads, per-thread partial sums, smem reduction over pixel lanes,
+// one fp32 atomicAdd per channel per block.
 template <typename T>
 __global__ void k_param_grad(ParamGradArgs A) {
-    const int co = blockIdx.x, rows = A.b - A.a, W = A.dy.W;
-    long long npix = (long long)A.B * rows * W;
-    float s0 = 0.f, s1 = 0.f;
-    float gam = A.epi == 2 ? ldf((const T *)A.gamma + co) : 1.f;
-    float bet = A.epi == 2 ? ldf((const T *)A.beta + co) : 0.f;
-    for (long long q = threadIdx.x; q < npix; q += blockDim.x) {
+    const int CV = blockDim.x, cv = threadIdx.x, py = threadIdx.y, PY = blockDim.y;
+    const int rows = A.b - A.a, W = A.dy.W, c0 = cv * 8;
+    const long long npix = (long long)A.B * rows * W;
+    float s0[8], s1[8], gam[8], bet[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        s0[j] = 0.f; s1[j] = 0.f;
+        const bool in = A.epi == 2 && c0 + j < A.c_out;
+        gam[j] = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
+        bet[j] = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
+    }
+    for (long long q = (long long)blockIdx.x * PY + py; q < npix; q += (long long)gridDim.x * PY) {
         int x = q % W;
         long long r = q / W;
         int y = A.a + (int)(r % rows);
         int b = (int)(r / rows);
-        float d = ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + co);
-        s0 += d;
-        if (A.epi == 2 && d != 0.f) {
-            float t = ldf((const T *)A.t.p + voff(A.t, b, y, x) + co);
-            if (A.res.p) t -= ldf((const T *)A.res.p + voff(A.res, b, y, x) + co);
-            s1 += d * (t - bet) / gam;   // raw conv output c = (t - beta - res)/gamma
+        const T *dp = (const T *)A.dy.p + voff(A.dy, b, y, x) + c0;
+        float d[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { d[j] = ldf(dp + j); s0[j] += d[j]; }
+        if (A.epi == 2) {
+            const T *tp = (const T *)A.t.p + voff(A.t, b, y, x) + c0;
+            const T *rp = A.res.p ? (const T *)A.res.p + voff(A.res, b, y, x) + c0 : nullptr;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float t = ldf(tp + j) - (rp ? ldf(rp + j) : 0.f);
+                s1[j] += d[j] * (t - bet[j]) / gam[j];
+            }
         }
     }
-    __shared__ float r0[32], r1[32];
-    for (int o = 16; o; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    if ((threadIdx.x & 31) == 0) { r0[threadIdx.x >> 5] = s0; r1[threadIdx.x >> 5] = s1; }
+    extern __shared__ float red[];   // [PY][CV*8] x 2
+    float *r0 = red, *r1 = red + PY * CV * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { r0[py * CV * 8 + c0 + j] = s0[j]; r1[py * CV * 8 + c0 + j] = s1[j]; }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    for (int c = py * CV + cv; c < CV * 8; c += PY * CV) {
         float a0 = 0.f, a1 = 0.f;
-        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) { a0 += r0[j]; a1 += r1[j]; }
-        if (A.epi == 1) A.db[co] += a0;
-        else { A.db[co] += a1; A.dbeta[co] += a0; }
+        for (int k = 0; k < PY; ++k) { a0 += r0[k * CV * 8 + c]; a1 += r1[k * CV * 8 + c]; }
+        if (c < A.c_out) {
+            if (A.epi == 1) atomicAdd(A.db + c, a0);
+            else { atomicAdd(A.db + c, a1); atomicAdd(A.dbeta + c, a0); }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 2x2/s2 max-pool (VGG), 8 channels per thread
+template <typename T>
+__device__ __forceinline__ void ld8(const T *p, float (&v)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = ldf(p + j);
+}
+__device__ __forceinline__ void ld8(const bf16 *p, float (&v)[8]) {
+    uint4 u = *reinterpret_cast<const uint4 *>(p);
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { float2 f = __bfloat1622float2(h[j]); v[2 * j] = f.x; v[2 * j + 1] = f.y; }
+}
+template <typename T>
+__device__ __forceinline__ void st8(T *p, const float (&v)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) stf(p + j, v[j]);
+}
+__device__ __forceinline__ void st8(bf16 *p, const float (&v)[8]) {
+    uint4 u;
+    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4 *>(p) = u;
+}
+
+// window order (0,0),(0,1),(1,0),(1,1) = raster order; strict '>' keeps the first maximum
+template <typename T>
+__global__ void k_pool2_fwd(PoolArgs A) {
+    const int CV = A.out.Cp / 8, Wo = A.out.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * Wo * CV;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int cv = idx % CV;
+        long long r = idx / CV;
+        int x = r % Wo; r /= Wo;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float best[8], v[8];
+        ld8((const T *)A.in.p + voff(A.in, b, 2 * y, 2 * x) + cv * 8, best);
+        const int dy[3] = {0, 1, 1}, dx[3] = {1, 0, 1};
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+            ld8((const T *)A.in.p + voff(A.in, b, 2 * y + dy[w], 2 * x + dx[w]) + cv * 8, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) best[j] = v[j] > best[j] ? v[j] : best[j];
+        }
+        st8((T *)A.out.p + voff(A.out, b, y, x) + cv * 8, best);
+    }
+}
+
+template <typename T>
+__global__ void k_pool2_bwd(PoolArgs A) {
+    const int CV = A.dy.Cp / 8, Wo = A.dy.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * Wo * CV;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int cv = idx % CV;
+        long long r = idx / CV;
+        int x = r % Wo; r /= Wo;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float d[8], v[4][8], best[8];
+        int arg[8];
+        ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) ld8((const T *)A.act.p + voff(A.act, b, 2 * y + (w >> 1), 2 * x + (w & 1)) + cv * 8, v[w]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            best[j] = v[0][j]; arg[j] = 0;
+#pragma unroll
+            for (int w = 1; w < 4; ++w)
+                if (v[w][j] > best[j]) { best[j] = v[w][j]; arg[j] = w; }
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            T *dp = (T *)A.dx.p + voff(A.dx, b, 2 * y + (w >> 1), 2 * x + (w & 1)) + cv * 8;
+            float o[8];
+            ld8(dp, o);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                o[j] += arg[j] == w ? d[j] : 0.f;
+                if (A.gate && !(v[w][j] > 0.f)) o[j] = 0.f;
+            }
+            st8(dp, o);
+        }
     }
 }
 
@@ -423,19 +527,38 @@ cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st) {
 }
 cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     if (a.b <= a.a || a.epi == 0) return cudaSuccess;
-    if (prec) k_param_grad<bf16><<<a.c_out, 256, 0, st>>>(a); else k_param_grad<float><<<a.c_out, 256, 0, st>>>(a);
+    const int CV = a.dy.Cp / 8;
+    if (CV < 1 || CV > 128 || a.dy.Cp % 8) return cudaErrorInvalidValue;
+    dim3 blk(CV, CV >= 64 ? 4 : 256 / CV);
+    long long npix = (long long)a.B * (a.b - a.a) * a.dy.W;
+    long long g = (npix + blk.y * 16 - 1) / (blk.y * 16);        // ~16 pixels per thread
+    if (g > 148 * 8) g = 148 * 8;
+    if (g < 1) g = 1;
+    size_t shm = 2 * sizeof(float) * blk.y * CV * 8;
+    if (prec) k_param_grad<bf16><<<(unsigned)g, blk, shm, st>>>(a); else k_param_grad<float><<<(unsigned)g, blk, shm, st>>>(a);
     return cudaGetLastError();
 }
+static bool pool2(const PoolArgs &a, const View &v) { return a.k == 2 && a.s == 2 && a.p == 0 && v.Cp % 8 == 0; }
 cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b - a.a) * a.out.W * a.out.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_pool_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    if (pool2(a, a.out)) {
+        n /= 8;
+        if (prec) k_pool2_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool2_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    } else {
+        if (prec) k_pool_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    }
     return cudaGetLastError();
 }
 cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_pool_bwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    if (pool2(a, a.dy)) {
+        long long m = (long long)a.B * (a.b - a.a) * a.dy.W * (a.dy.Cp / 8);
+        if (prec) k_pool2_bwd<bf16><<<grid_for(m), kT, 0, st>>>(a); else k_pool2_bwd<float><<<grid_for(m), kT, 0, st>>>(a);
+    } else {
+        if (prec) k_pool_bwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    }
     return cudaGetLastError();
 }
 cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st) {

@@ -81,7 +81,7 @@ struct Plan {
     bool fwd_done = false;
     const void *fwd_params = nullptr, *fwd_x = nullptr;
     void *fwd_ws = nullptr;
-    long long launches = 0;
+    long long launches = 0, tc_launches = 0;
     bool profiling = false;
     ProfileSlot prof[3];
     std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t

@@ -60,7 +60,7 @@ class MemoryReport(ctypes.Structure):
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
-           "lrcnn_profile_reset", "lrcnn_last_launch_count", "lrcnn_last_error", "lrcnn_version"]
+           "lrcnn_profile_reset", "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
 
 _lib = None
 
@@ -94,6 +94,7 @@ def lib():
                                      ctypes.POINTER(ctypes.c_double), vp]
     L.lrcnn_profile_reset.argtypes = [vp]
     L.lrcnn_last_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+    L.lrcnn_last_tc_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
     L.lrcnn_last_error.restype = ctypes.c_char_p
     L.lrcnn_version.restype = ctypes.c_char_p
     for n in EXPORTS:
@@ -308,6 +309,11 @@ class Plan:
     def last_launches(self):
         n = ctypes.c_longlong()
         _check(lib().lrcnn_last_launch_count(self.h, ctypes.byref(n)))
+        return n.value
+
+    def last_tc_launches(self):
+        n = ctypes.c_longlong()
+        _check(lib().lrcnn_last_tc_launch_count(self.h, ctypes.byref(n)))
         return n.value
 
 

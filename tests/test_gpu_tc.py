@@ -27,6 +27,8 @@ def run(net, B, mode, params, x, dzl, flags=0, **kw):
     zl = plan.from_nhwc(ds.zl.float().cpu().numpy(), len(net["ops"]))
     ds.backward()
     torch.cuda.synchronize()
+    if not flags & LB.FLAG_NO_TCGEN05:
+        assert plan.last_tc_launches() > 0          # the tcgen05 kernels ran
     g, _ = plan.unpack_grads(ds.grads.cpu().numpy())
     return zl, g
 
@@ -55,8 +57,11 @@ def test_two_conv_layers_vs_oracle(cin, cout, H, W, k, p):
 
 
 def test_tc_matches_simt():
-    """Tensor-core and SIMT kernels on the same bf16 inputs (same storage rounding points)."""
-    net = WL.vgg16(H=64, W=48, width_div=2, cfg=[64, 64, "M", 128, 128, "M", 256, "M"])
+    """Tensor-core and SIMT kernels on the same bf16 inputs (same storage rounding points).
+    No max-pool: argmax near-ties would make the comparison ill-conditioned (R17c)."""
+    net = {"C": 3, "H": 40, "W": 48, "classes": 10,
+           "ops": [WL.conv(0, 64, 3, 1, 1), WL.conv(1, 128, 3, 1, 1), WL.conv(2, 64, 1, 1, 0),
+                   WL.conv(3, 256, 3, 1, 1)]}
     B = 2
     params = WL.make_params(net, seed=2, bias_scale=0.05, bf16=True)
     x = WL.make_input(net, B, seed=0, bf16=True)
