@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "tc.hpp"
@@ -45,6 +46,8 @@ struct TcConv {
     int out_a, out_b, Wo, B;
     int TW, TH, tiles_x, tiles_y, m_tiles, n_tiles;
     int k, pad, in_base, cin_chunks, k_steps;
+    int boff;              // halo kernel: 1 = set the descriptor base-offset field from the address
+    int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
 };
 
 struct TcWgrad {
@@ -72,6 +75,90 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
 }
+
+// Epilogue warps (4 warps = 128 TMEM lanes = 128 pixels of the tile): tcgen05.ld the
+// accumulator in 32-column chunks, apply the fused epilogue, 16-byte bf16 stores.
+template <int BN>
+__device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
+                                              int warp, int lane) {
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    const int ew = warp & 3;                  // TMEM lane quarter this warp may access
+    const int m = ew * 32 + lane;             // accumulator row = pixel in the tile
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
+        const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+        const int y = P.out_a + ty * P.TH + m / P.TW, x = tx * P.TW + m % P.TW, n0 = nt * BN;
+        const bool valid = y < P.out_b && x < P.Wo;
+        const long long pix = valid ? (long long)b * P.out.bs + ((long long)(y - P.out.base) * P.out.W + x) * P.out.Cp : 0;
+        ptx::mbar_wait(tfull + acc, aphase);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+            uint32_t v[32];
+            ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
+            ptx::tmem_ld_wait();
+            if (!valid || (P.dbg & 1)) continue;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const int n = n0 + c * 32 + g * 8;
+                if (n >= P.n_out) break;
+                float f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[g * 8 + j]);
+                bf16 *dst = (bf16 *)P.out.p + pix + n;
+                if (P.mode == 0) {
+                    if (P.epi != 0) {
+                        uint4 bb = *reinterpret_cast<const uint4 *>(P.bias + n);
+                        const uint16_t *bh = reinterpret_cast<const uint16_t *>(&bb);
+                        uint4 be = P.epi == 2 ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
+                        const uint16_t *beh = reinterpret_cast<const uint16_t *>(&be);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            float bj = n + j < P.c_real ? bf2f(bh[j]) : 0.f;
+                            if (P.epi == 1) f[j] += bj;
+                            else f[j] = n + j < P.c_real ? bj * f[j] + bf2f(beh[j]) : 0.f;
+                        }
+                    }
+                    if (P.has_res) {
+                        uint4 rr = *reinterpret_cast<const uint4 *>(
+                            (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                            ((long long)(y - P.res.base) * P.res.W + x) * P.res.Cp + n);
+                        const uint16_t *rh = reinterpret_cast<const uint16_t *>(&rr);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] += bf2f(rh[j]);
+                    }
+                    if (P.relu) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
+                    }
+                } else {
+                    uint4 od = *reinterpret_cast<const uint4 *>(dst);
+                    const uint16_t *oh = reinterpret_cast<const uint16_t *>(&od);
+                    uint4 ac = make_uint4(0, 0, 0, 0);
+                    if (P.gate)
+                        ac = *reinterpret_cast<const uint4 *>(
+                            (const bf16 *)P.act.p + (long long)b * P.act.bs +
+                            ((long long)(y - P.act.base) * P.act.W + x) * P.act.Cp + n);
+                    const uint16_t *ah = reinterpret_cast<const uint16_t *>(&ac);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        f[j] += bf2f(oh[j]);
+                        if (P.gate && !(bf2f(ah[j]) > 0.f)) f[j] = 0.f;
+                    }
+                }
+                uint4 o;
+                o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
+                *reinterpret_cast<uint4 *>(dst) = o;
+            }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    }
 
 // ------------------------------------------------------------------ conv FP / dgrad
 template <int BN>
@@ -142,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < 4; ++kk) {
                         uint64_t ad = ptx::smem_desc_sw128(a0 + kk * 32, 16, 1024);
                         uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 32, 16, 1024);
-                        ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
+                        if (!(P.dbg & 2)) ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
                     }
                     ptx::umma_commit(empty + stage);
                     if (++stage == S) { stage = 0; phase ^= 1; }
@@ -152,82 +239,131 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        const int ew = warp & 3;                  // TMEM lane quarter this warp may access
-        const int m = ew * 32 + lane;             // accumulator row = pixel in the tile
-        int acc = 0;
-        uint32_t aphase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
-            const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
-            const int y = P.out_a + ty * P.TH + m / P.TW, x = tx * P.TW + m % P.TW, n0 = nt * BN;
-            const bool valid = y < P.out_b && x < P.Wo;
-            const long long pix = valid ? (long long)b * P.out.bs + ((long long)(y - P.out.base) * P.out.W + x) * P.out.Cp : 0;
-            ptx::mbar_wait(tfull + acc, aphase);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
-                ptx::tmem_ld_wait();
-                if (!valid) continue;
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const int n = n0 + c * 32 + g * 8;
-                    if (n >= P.n_out) break;
-                    float f[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[g * 8 + j]);
-                    bf16 *dst = (bf16 *)P.out.p + pix + n;
-                    if (P.mode == 0) {
-                        if (P.epi != 0) {
-                            uint4 bb = *reinterpret_cast<const uint4 *>(P.bias + n);
-                            const uint16_t *bh = reinterpret_cast<const uint16_t *>(&bb);
-                            uint4 be = P.epi == 2 ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
-                            const uint16_t *beh = reinterpret_cast<const uint16_t *>(&be);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                float bj = n + j < P.c_real ? bf2f(bh[j]) : 0.f;
-                                if (P.epi == 1) f[j] += bj;
-                                else f[j] = n + j < P.c_real ? bj * f[j] + bf2f(beh[j]) : 0.f;
-                            }
-                        }
-                        if (P.has_res) {
-                            uint4 rr = *reinterpret_cast<const uint4 *>(
-                                (const bf16 *)P.res.p + (long long)b * P.res.bs +
-                                ((long long)(y - P.res.base) * P.res.W + x) * P.res.Cp + n);
-                            const uint16_t *rh = reinterpret_cast<const uint16_t *>(&rr);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) f[j] += bf2f(rh[j]);
-                        }
-                        if (P.relu) {
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
-                        }
-                    } else {
-                        uint4 od = *reinterpret_cast<const uint4 *>(dst);
-                        const uint16_t *oh = reinterpret_cast<const uint16_t *>(&od);
-                        uint4 ac = make_uint4(0, 0, 0, 0);
-                        if (P.gate)
-                            ac = *reinterpret_cast<const uint4 *>(
-                                (const bf16 *)P.act.p + (long long)b * P.act.bs +
-                                ((long long)(y - P.act.base) * P.act.W + x) * P.act.Cp + n);
-                        const uint16_t *ah = reinterpret_cast<const uint16_t *>(&ac);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            f[j] += bf2f(oh[j]);
-                            if (P.gate && !(bf2f(ah[j]) > 0.f)) f[j] = 0.f;
-                        }
+        conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ conv FP / dgrad, halo reuse
+// Stride-1 k x k convolutions: the output tile is 8 columns x 16 rows.  One TMA box of
+// 16 x (16+k-1) input pixels x 64 channels (the tile plus its halo, row pitch 16 pixels =
+// 2 KB) is loaded once per input-channel chunk and serves all k*k taps: the A operand of
+// tap (ky, kx) is the same smem box at a start offset of (16*ky + kx) pixel rows, with
+// 8-pixel core-matrix groups 2 KB apart (SBO = 2048).  A traffic drops from k*k boxes
+// of 128 rows to one box of 16*(15+k) rows per chunk.  Weights stream per tap.
+static constexpr int kHaloPitch = 16;
+template <int BN, int KH>
+struct HaloCfg {
+    static constexpr int kABytes = kHaloPitch * (16 + KH - 1) * 128;
+    static constexpr int kBBytes = BN * 128;
+    static constexpr int kSA = 2;
+    static constexpr int kSB = (220 * 1024 - kSA * kABytes) / kBBytes;
+    static constexpr int kSmem = kSA * kABytes + kSB * kBBytes + 1024 + 512;
+    static constexpr uint32_t kTmemCols = 2 * BN;
+};
+
+template <int BN, int KH>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_conv_tc_halo(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcConv P) {
+    using Cfg = HaloCfg<BN, KH>;
+    constexpr int SA = Cfg::kSA, SB = Cfg::kSB;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + SA * Cfg::kABytes;
+    uint64_t *fullA = (uint64_t *)(sB + SB * Cfg::kBBytes);
+    uint64_t *emptyA = fullA + SA;
+    uint64_t *fullB = emptyA + SA;
+    uint64_t *emptyB = fullB + SB;
+    uint64_t *tfull = emptyB + SB;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tslot = (uint32_t *)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
+        for (int i = 0; i < SB; ++i) { ptx::mbar_init(fullB + i, 1); ptx::mbar_init(emptyB + i, 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, Cfg::kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    constexpr int taps = KH * KH;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int sa = 0, sb = 0;
+            uint32_t pa = 0, pb = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
+                const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                const int y0 = P.out_a + ty * 16, x0 = tx * 8, n0 = nt * BN;
+                for (int c = 0; c < P.cin_chunks; ++c) {
+                    ptx::mbar_wait(emptyA + sa, pa ^ 1);
+                    ptx::mbar_arrive_expect_tx(fullA + sa, Cfg::kABytes);
+                    ptx::tma_load_4d(sA + sa * Cfg::kABytes, &tmA, fullA + sa, c * 64, x0 - P.pad,
+                                     y0 - P.pad - P.in_base, b);
+                    if (++sa == SA) { sa = 0; pa ^= 1; }
+                    for (int tap = 0; tap < taps; ++tap) {
+                        ptx::mbar_wait(emptyB + sb, pb ^ 1);
+                        ptx::mbar_arrive_expect_tx(fullB + sb, Cfg::kBBytes);
+                        ptx::tma_load_3d(sB + sb * Cfg::kBBytes, &tmB, fullB + sb, c * 64, tap, n0);
+                        if (++sb == SB) { sb = 0; pb ^= 1; }
                     }
-                    uint4 o;
-                    o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
-                    *reinterpret_cast<uint4 *>(dst) = o;
                 }
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty + acc);
-            if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            int sa = 0, sb = 0, acc = 0;
+            uint32_t pa = 0, pb = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                int first = 1;
+                for (int c = 0; c < P.cin_chunks; ++c) {
+                    ptx::mbar_wait(fullA + sa, pa);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + sa * Cfg::kABytes);
+                    for (int tap = 0; tap < taps; ++tap) {
+                        const int ky = tap / KH, kx = tap - ky * KH;
+                        ptx::mbar_wait(fullB + sb, pb);
+                        ptx::tc_fence_after();
+                        const uint32_t at = a0 + (uint32_t)(ky * kHaloPitch + kx) * 128;
+                        const uint32_t b0 = ptx::smem_u32(sB + sb * Cfg::kBBytes);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint32_t aa = at + kk * 32;
+                            uint64_t ad = ptx::smem_desc_sw128_bo(aa, 16, kHaloPitch * 128, P.boff ? (aa >> 7) & 7 : 0);
+                            uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 32, 16, 1024);
+                            ptx::umma_bf16(d, ad, bd, idesc, first ? 0u : 1u);
+                            first = 0;
+                        }
+                        ptx::umma_commit(emptyB + sb);
+                        if (++sb == SB) { sb = 0; pb ^= 1; }
+                    }
+                    ptx::umma_commit(emptyA + sa);
+                    if (++sa == SA) { sa = 0; pa ^= 1; }
+                }
+                ptx::umma_commit(tfull + acc);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -462,6 +598,26 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
     return true;
 }
 
+template <int BN>
+static bool launch_conv_halo(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, int tiles, cudaStream_t st) {
+    using Cfg = HaloCfg<BN, 3>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_conv_tc_halo<BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+            cudaSuccess)
+            return false;
+        attr = true;
+    }
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    k_conv_tc_halo<BN, 3><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, P);
+    return true;
+}
+
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
 static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, int cin_p, int k, int pad,
                         cudaStream_t st) {
     if (in.Cp % 8 || cin_p != in.Cp || P.n_out < 8 || P.n_out % 8) return false;
@@ -469,6 +625,26 @@ static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, in
     int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
     const int rows = P.out_b - P.out_a;
     if (rows <= 0) return true;
+    static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
+    static const int dbg = env_int("LRCNN_TC_DBG", 0);
+    P.dbg = dbg;
+    if (halo_on && k == 3) {
+        P.TW = 8; P.TH = 16;
+        P.tiles_x = (P.Wo + 7) / 8;
+        P.tiles_y = (rows + 15) / 16;
+        P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+        P.n_tiles = (P.n_out + BN - 1) / BN;
+        P.k = k; P.pad = pad; P.in_base = in.base; P.boff = boff;
+        P.cin_chunks = (cin_p + 63) / 64;
+        P.k_steps = k * k * P.cin_chunks;
+        CUtensorMap A, Bm;
+        if (!encode_view(&A, in, P.B, kHaloPitch, 16 + k - 1)) return false;
+        if (!encode_w(&Bm, w, w_rows, k * k, cin_p, BN)) return false;
+        int tiles = P.m_tiles * P.n_tiles;
+        if (BN == 64) return launch_conv_halo<64>(P, A, Bm, tiles, st);
+        if (BN == 128) return launch_conv_halo<128>(P, A, Bm, tiles, st);
+        return launch_conv_halo<256>(P, A, Bm, tiles, st);
+    }
     pick_tile(rows, P.Wo, P.TW, P.TH);
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;

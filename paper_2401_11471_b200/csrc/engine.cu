@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -379,6 +380,7 @@ lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
 
 lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
     if (plan) {
+        if (plan->P.graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)plan->P.graph_exec);
         for (int c = 0; c < 3; ++c)
             for (auto &e : plan->P.pending_events[c]) {
                 cudaEventDestroy((cudaEvent_t)e.first);
@@ -529,12 +531,60 @@ lrcnn_status lrcnn_sgd(lrcnn_plan_t *plan, float *master, void *params, float *g
     return LRCNN_OK;
 }
 
-lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
-                        const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
-    if (!plan || !master || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
+static lrcnn_status step_eager(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
+                               const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes,
+                               void *stream) {
     lrcnn_status st = lrcnn_step_grads(plan, params, grads, x, labels, loss_dev, ws, ws_bytes, stream);
     if (st != LRCNN_OK) return st;
     return lrcnn_sgd(plan, master, params, grads, lr, stream);   // adds its own launch
+}
+
+// One training iteration.  The band x op sweep is hundreds of launches; from the second call
+// with unchanged arguments on a non-default stream the whole step is captured once into a CUDA
+// graph and replayed (tensor maps and launch parameters are baked in by value).
+lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
+                        const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !master || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
+    Plan &P = plan->P;
+    static const int graphs = getenv("LRCNN_GRAPH") ? atoi(getenv("LRCNN_GRAPH")) : 1;
+    float lr_copy = lr;
+    uint32_t lr_bits;
+    std::memcpy(&lr_bits, &lr_copy, 4);
+    const uintptr_t key[9] = {(uintptr_t)master, (uintptr_t)params, (uintptr_t)grads, (uintptr_t)x,
+                              (uintptr_t)labels, (uintptr_t)loss_dev, (uintptr_t)ws, (uintptr_t)stream, lr_bits};
+    if (!graphs || stream == nullptr || P.profiling) {
+        P.graph_calls = 0;
+        return step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
+    }
+    const bool same = std::memcmp(key, P.graph_key, sizeof(key)) == 0;
+    if (same && P.graph_exec) {
+        CK(cudaGraphLaunch((cudaGraphExec_t)P.graph_exec, (cudaStream_t)stream));
+        P.launches = P.graph_launches;
+        P.tc_launches = P.graph_tc_launches;
+        P.fwd_done = false;
+        return LRCNN_OK;
+    }
+    P.graph_calls = same ? P.graph_calls + 1 : 1;
+    std::memcpy(P.graph_key, key, sizeof(key));
+    if (P.graph_exec) { cudaGraphExecDestroy((cudaGraphExec_t)P.graph_exec); P.graph_exec = nullptr; }
+    if (P.graph_calls < 2)   // first call with these arguments: eager (warms caches, function attributes)
+        return step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
+    cudaStream_t cs = (cudaStream_t)stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    lrcnn_status st = step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    if (st != LRCNN_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (ce != cudaSuccess) return fail(LRCNN_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t ge = nullptr;
+    ce = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(LRCNN_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
+    P.graph_exec = ge;
+    P.graph_launches = P.launches;
+    P.graph_tc_launches = P.tc_launches;
+    CK(cudaGraphLaunch(ge, cs));
+    return LRCNN_OK;
 }
 
 

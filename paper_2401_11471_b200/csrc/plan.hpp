@@ -86,6 +86,11 @@ struct Plan {
     ProfileSlot prof[3];
     std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t
     std::vector<double> pending_flops[3];
+    // CUDA graph of one lrcnn_step, replayed while its arguments are unchanged
+    void *graph_exec = nullptr;                  // cudaGraphExec_t
+    uintptr_t graph_key[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int graph_calls = 0;                         // consecutive calls with the same key
+    long long graph_launches = 0, graph_tc_launches = 0;
 };
 
 // Builds the plan; returns status and fills err on failure.

@@ -116,6 +116,12 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
+// Same with the 3-bit "matrix base offset" field [49,52) (start address not aligned to the
+// 1024-byte repeat of the 128B swizzle pattern).
+__device__ __forceinline__ uint64_t smem_desc_sw128_bo(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                                       uint32_t base_off) {
+    return smem_desc_sw128(saddr, lbo_bytes, sbo_bytes) | ((uint64_t)(base_off & 7) << 49);
+}
 // Instruction descriptor, kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // A major [15], B major [16] (0 = K-major, 1 = MN-major), N>>3 [17,23), M>>4 [24,29).
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {

@@ -226,3 +226,30 @@ def test_state_and_workspace_errors():
                                      plan.ws_bytes, LB._stream(None))
     assert LB.STATUS[st] == "E_WORKSPACE"
     del ctypes
+
+
+def test_step_graph_replay_matches_eager():
+    """lrcnn_step captured into a CUDA graph (non-default stream) == eager steps on the default stream."""
+    net = WL.vgg16(H=32, W=32, width_div=4, cfg=[64, 64, "M", 128, "M"])
+    B = 2
+    params = WL.make_params(net, seed=2, bias_scale=0.05)
+    x = WL.make_input(net, B)
+    lab = WL.make_labels(net, B)
+    out = []
+    for use_stream in (False, True):
+        plan = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=3)
+        ds = LB.DeviceState(plan)
+        ds.load(params=params, x=x, labels=lab)
+        st = torch.cuda.Stream() if use_stream else None
+        losses = []
+        for _ in range(5):
+            if st is None:
+                ds.step(0.05)
+            else:
+                with torch.cuda.stream(st):
+                    ds.step(0.05, stream=st)
+            torch.cuda.synchronize()
+            losses.append(float(ds.loss.cpu()))
+        out.append((losses, ds.master.cpu().numpy()))
+    assert np.allclose(out[0][0], out[1][0], rtol=1e-5)
+    assert rel(out[1][1], out[0][1]) <= 1e-4
