@@ -47,6 +47,11 @@ struct TcConv {
     int TW, TH, tiles_x, tiles_y, m_tiles, n_tiles;
     int k, pad, in_base, cin_chunks, k_steps;
     int boff;              // halo kernel: 1 = set the descriptor base-offset field from the address
+    // generalised taps (stride-s FP, parity classes of strided dgrad): the A box of tap t starts at
+    // (grid_col*a_mul + tap_ox[t], grid_row*a_mul + tap_oy[t]) of the input view (TMA element
+    // stride a_mul), weights tap index tap_w[t]; output pixel = (o_row0 + o_stride*grid_row, ...)
+    int a_mul, ntaps, o_row0, o_col0, o_stride, halo_ok;
+    int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
 };
 
@@ -57,6 +62,7 @@ struct TcWgrad {
     int TW, TH, tiles_x, tiles_y, pix_tiles, per_split, splits;
     int co_tiles, ci_tiles, items;
     int out_a, dy_base, x_base;
+    int s;                 // conv stride (TMA element stride of the input box)
 };
 
 static constexpr int kThreads = 192;
@@ -89,8 +95,9 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
         const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
-        const int y = P.out_a + ty * P.TH + m / P.TW, x = tx * P.TW + m % P.TW, n0 = nt * BN;
-        const bool valid = y < P.out_b && x < P.Wo;
+        const int yg = P.out_a + ty * P.TH + m / P.TW, xg = tx * P.TW + m % P.TW, n0 = nt * BN;
+        const bool valid = yg < P.out_b && xg < P.Wo;
+        const int y = P.o_row0 + P.o_stride * yg, x = P.o_col0 + P.o_stride * xg;
         const long long pix = valid ? (long long)b * P.out.bs + ((long long)(y - P.out.base) * P.out.W + x) * P.out.Cp : 0;
         ptx::mbar_wait(tfull + acc, aphase);
         ptx::tc_fence_after();
@@ -198,15 +205,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
                 const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
-                const int y0 = P.out_a + ty * P.TH, x0 = tx * P.TW, n0 = nt * BN;
+                const int y0 = (P.out_a + ty * P.TH) * P.a_mul, x0 = tx * P.TW * P.a_mul, n0 = nt * BN;
                 for (int ks = 0; ks < P.k_steps; ++ks) {
                     const int tap = ks / P.cin_chunks, c = ks - tap * P.cin_chunks;
-                    const int ky = tap / P.k, kx = tap - ky * P.k;
                     ptx::mbar_wait(empty + stage, phase ^ 1);
                     ptx::mbar_arrive_expect_tx(full + stage, kABytes + BN * 128);
-                    ptx::tma_load_4d(sA + stage * kABytes, &tmA, full + stage, c * 64, x0 - P.pad + kx,
-                                     y0 - P.pad + ky - P.in_base, b);
-                    ptx::tma_load_3d(sB + stage * BN * 128, &tmB, full + stage, c * 64, tap, n0);
+                    ptx::tma_load_4d(sA + stage * kABytes, &tmA, full + stage, c * 64, x0 + P.tap_ox[tap],
+                                     y0 + P.tap_oy[tap] - P.in_base, b);
+                    ptx::tma_load_3d(sB + stage * BN * 128, &tmB, full + stage, c * 64, P.tap_w[tap], n0);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int h = 0; h < BN / 64; ++h)
                         ptx::tma_load_4d(st + kWgA + h * kABytes, &tmX, full + stage, cit * BN + h * 64,
-                                         x0 - P.pad + kx, y0 - P.pad + ky - P.x_base, b);
+                                         x0 * P.s - P.pad + kx, y0 * P.s - P.pad + ky - P.x_base, b);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -542,15 +548,16 @@ static int num_sms() {
     return n;
 }
 
-// 4D map over a band View: dims (Cp, W, rows, B); box (64, TW, TH, 1); 128B swizzle.
-static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH) {
+// 4D map over a band View: dims (Cp, W, rows, B); box (64, TW*es, TH*es, 1) with TMA element
+// stride es along W and H (es = conv stride: the box then holds TW x TH strided pixels); 128B swizzle.
+static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH, int es = 1) {
     auto fn = encode_fn();
-    if (!fn || v.rows <= 0) return false;
+    if (!fn || v.rows <= 0 || TW * es > 256 || TH * es > 256) return false;
     cuuint64_t dims[4] = {(cuuint64_t)v.Cp, (cuuint64_t)v.W, (cuuint64_t)v.rows, (cuuint64_t)B};
     cuuint64_t strides[3] = {(cuuint64_t)v.Cp * 2, (cuuint64_t)v.W * v.Cp * 2, (cuuint64_t)v.bs * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)TW, (cuuint32_t)TH, 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint32_t box[4] = {64, (cuuint32_t)(TW * es), (cuuint32_t)(TH * es), 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)es, (cuuint32_t)es, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -570,11 +577,12 @@ static bool encode_w(CUtensorMap *m, const void *w, int rows, int taps, int cin_
     return r == CUDA_SUCCESS;
 }
 
-// choose a 128-pixel rectangle TW x TH (TW*TH = 128) minimising padded pixels
-static void pick_tile(int rows, int W, int &TW, int &TH) {
+// choose a 128-pixel rectangle TW x TH (TW*TH = 128, TW*s <= 256) minimising padded pixels
+static void pick_tile(int rows, int W, int s, int &TW, int &TH) {
     long best = -1;
     for (int tw = 128; tw >= 4; tw >>= 1) {
         int th = 128 / tw;
+        if (tw * s > 256 || th * s > 256) continue;
         long cost = (long)((W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
         if (best < 0 || cost < best) { best = cost; TW = tw; TH = th; }
     }
@@ -618,44 +626,41 @@ static int env_int(const char *name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
-static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, int cin_p, int k, int pad,
+// Launch one implicit-GEMM conv over the output grid rows [P.out_a, P.out_b) x cols [0, P.Wo).
+// Caller sets the epilogue fields, the output mapping (o_*), a_mul and the tap table.
+static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, int w_taps, int cin_p,
                         cudaStream_t st) {
-    if (in.Cp % 8 || cin_p != in.Cp || P.n_out < 8 || P.n_out % 8) return false;
+    if (in.Cp % 8 || cin_p != in.Cp || P.n_out < 8 || P.n_out % 8 || P.ntaps < 1 || P.ntaps > 49) return false;
     if (!aligned16(in.p) || !aligned16(w) || !aligned16(P.out.p)) return false;
-    int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
+    const int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
     const int rows = P.out_b - P.out_a;
-    if (rows <= 0) return true;
-    static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
+    if (rows <= 0 || P.Wo <= 0) return true;
     static const int dbg = env_int("LRCNN_TC_DBG", 0);
     P.dbg = dbg;
-    if (halo_on && k == 3) {
+    P.in_base = in.base;
+    P.cin_chunks = (cin_p + 63) / 64;
+    P.k_steps = P.ntaps * P.cin_chunks;
+    P.n_tiles = (P.n_out + BN - 1) / BN;
+    CUtensorMap A, Bm;
+    if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN)) return false;
+    static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
+    if (halo_on && P.halo_ok) {
         P.TW = 8; P.TH = 16;
         P.tiles_x = (P.Wo + 7) / 8;
         P.tiles_y = (rows + 15) / 16;
         P.m_tiles = P.B * P.tiles_x * P.tiles_y;
-        P.n_tiles = (P.n_out + BN - 1) / BN;
-        P.k = k; P.pad = pad; P.in_base = in.base; P.boff = boff;
-        P.cin_chunks = (cin_p + 63) / 64;
-        P.k_steps = k * k * P.cin_chunks;
-        CUtensorMap A, Bm;
-        if (!encode_view(&A, in, P.B, kHaloPitch, 16 + k - 1)) return false;
-        if (!encode_w(&Bm, w, w_rows, k * k, cin_p, BN)) return false;
+        P.boff = boff;
+        if (!encode_view(&A, in, P.B, kHaloPitch, 16 + P.k - 1)) return false;
         int tiles = P.m_tiles * P.n_tiles;
         if (BN == 64) return launch_conv_halo<64>(P, A, Bm, tiles, st);
         if (BN == 128) return launch_conv_halo<128>(P, A, Bm, tiles, st);
         return launch_conv_halo<256>(P, A, Bm, tiles, st);
     }
-    pick_tile(rows, P.Wo, P.TW, P.TH);
+    pick_tile(rows, P.Wo, P.a_mul, P.TW, P.TH);
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
-    P.n_tiles = (P.n_out + BN - 1) / BN;
-    P.k = k; P.pad = pad; P.in_base = in.base;
-    P.cin_chunks = (cin_p + 63) / 64;
-    P.k_steps = k * k * P.cin_chunks;
-    CUtensorMap A, Bm;
-    if (!encode_view(&A, in, P.B, P.TW, P.TH)) return false;
-    if (!encode_w(&Bm, w, w_rows, k * k, cin_p, BN)) return false;
+    if (!encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul)) return false;
     int tiles = P.m_tiles * P.n_tiles;
     if (BN == 64) return launch_conv<64>(P, A, Bm, tiles, st);
     if (BN == 128) return launch_conv<128>(P, A, Bm, tiles, st);
@@ -663,7 +668,7 @@ static bool conv_common(TcConv &P, const View &in, const void *w, int w_rows, in
 }
 
 bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
-    if (a.s != 1) return false;
+    if (a.s < 1 || a.s > 2) return false;
     TcConv P{};
     P.out = a.out; P.res = a.res; P.has_res = a.res.p != nullptr;
     P.bias = (const bf16 *)a.b; P.beta = (const bf16 *)a.beta;
@@ -671,18 +676,55 @@ bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
     P.out_a = a.a; P.out_b = a.b_; P.Wo = a.out.W; P.B = a.B;
     if (P.epi != 0 && !aligned16(P.bias)) return false;
     if (P.has_res && (a.res.Cp % 8 || !aligned16(a.res.p))) return false;
-    return conv_common(P, a.in, a.w, a.c_out, a.in.Cp, a.k, a.p, st);
+    if (a.k * a.k > 49) return false;
+    P.a_mul = a.s; P.o_row0 = 0; P.o_col0 = 0; P.o_stride = 1;
+    P.ntaps = a.k * a.k;
+    for (int ky = 0; ky < a.k; ++ky)
+        for (int kx = 0; kx < a.k; ++kx) {
+            const int t = ky * a.k + kx;
+            P.tap_oy[t] = ky - a.p; P.tap_ox[t] = kx - a.p; P.tap_w[t] = t;
+        }
+    P.k = a.k; P.pad = a.p; P.halo_ok = a.s == 1 && a.k == 3;
+    return conv_launch(P, a.in, a.w, a.c_out, a.k * a.k, a.in.Cp, st);
 }
 
+// dgrad: delta_in[g] += sum_{ky: (g+p-ky) = s*y} W[ky] delta[y].  The input grid is split in
+// s x s parity classes (ry, rx); each class is a stride-1 implicit GEMM over the band delta
+// with the class's taps of the flipped/transposed weights W' and output stride s.
 bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
-    if (a.s != 1 || !a.wt) return false;
-    TcConv P{};
-    P.out = a.dx; P.act = a.act;
-    P.mode = 1; P.epi = 0; P.relu = 0; P.gate = a.gate; P.c_real = a.dx.Cp; P.n_out = a.dx.Cp;
-    P.out_a = a.ra; P.out_b = a.rb; P.Wo = a.dx.W; P.B = a.B;
+    if (!a.wt || a.s < 1 || a.s > 2 || a.k * a.k > 49) return false;
     if (a.gate && (!aligned16(a.act.p) || a.act.Cp != a.dx.Cp)) return false;
-    // input = the band delta rows [a, b) (view already restricted), weights W'[Cin_p][k][k][Cout_p]
-    return conv_common(P, a.dy, a.wt, a.dx.Cp, a.dy.Cp, a.k, a.k - 1 - a.p, st);
+    const int s = a.s, k = a.k, p = a.p;
+    for (int ry = 0; ry < s; ++ry)
+        for (int rx = 0; rx < s; ++rx) {
+            TcConv P{};
+            P.out = a.dx; P.act = a.act;
+            P.mode = 1; P.epi = 0; P.relu = 0; P.gate = a.gate; P.c_real = a.dx.Cp; P.n_out = a.dx.Cp;
+            P.B = a.B; P.a_mul = 1; P.o_row0 = ry; P.o_col0 = rx; P.o_stride = s;
+            // class grid: rows j with ra <= ry + s*j < rb, cols i with rx + s*i < W_in
+            P.out_a = (a.ra - ry + s - 1) / s;
+            P.out_b = (a.rb - ry + s - 1) / s;
+            P.Wo = (a.dx.W - rx + s - 1) / s;
+            if (a.ra - ry < 0) P.out_a = 0;
+            int n = 0;
+            for (int ky = 0; ky < k; ++ky) {
+                const int dy = ry + p - ky;
+                if (((dy % s) + s) % s) continue;
+                for (int kx = 0; kx < k; ++kx) {
+                    const int dx = rx + p - kx;
+                    if (((dx % s) + s) % s) continue;
+                    P.tap_oy[n] = dy >= 0 ? dy / s : -((-dy) / s);
+                    P.tap_ox[n] = dx >= 0 ? dx / s : -((-dx) / s);
+                    P.tap_w[n] = (k - 1 - ky) * k + (k - 1 - kx);
+                    ++n;
+                }
+            }
+            P.ntaps = n;
+            if (n == 0 || P.out_b <= P.out_a || P.Wo <= 0) continue;
+            P.k = k; P.pad = k - 1 - p; P.halo_ok = 0;
+            if (!conv_launch(P, a.dy, a.wt, a.dx.Cp, k * k, a.dy.Cp, st)) return false;
+        }
+    return true;
 }
 
 template <int BN>
@@ -700,14 +742,15 @@ static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorM
 }
 
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
-    if (a.s != 1) return false;
+    if (a.s < 1 || a.s > 2) return false;
     const View &dy = a.dy, &x = a.x;
     if (dy.Cp % 8 || x.Cp % 8 || !aligned16(dy.p) || !aligned16(x.p)) return false;
     const int rows = a.b - a.a;
     if (rows <= 0) return true;
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
-    pick_tile(rows, dy.W, P.TW, P.TH);
+    P.s = a.s;
+    pick_tile(rows, dy.W, a.s, P.TW, P.TH);
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
@@ -724,7 +767,7 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.out_a = a.a; P.dy_base = dy.base; P.x_base = x.base;
     CUtensorMap D, X;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
-    if (!encode_view(&X, x, a.B, P.TW, P.TH)) return false;
+    if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s)) return false;
     if (BN == 64) return launch_wgrad<64>(P, D, X, st);
     return launch_wgrad<128>(P, D, X, st);
 }

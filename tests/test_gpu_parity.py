@@ -140,6 +140,17 @@ def test_dag_fp32_and_bf16():
               flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
 
 
+def test_resnet50_reduced():
+    """ResNet-50 v1.5 topology (stem 7x7/s2, max-pool 3x3/s2/p1, bottlenecks with stride-2 3x3,
+    projection shortcuts, fused residual add), one block per stage, reduced width, per-stage
+    checkpoint segments: fp32 (1e-5) and bf16 (2e-2, training-workload delta^L) vs the oracle."""
+    net = WL.resnet50(H=64, W=48, width_div=8, blocks=(1, 1, 1, 1))
+    check(net, 2, "fp32", ["column", "2ps", "overl"], [{"n_bands": 3}, {"band_rows": 1}], bias=0.1,
+          gspread=0.2, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION, cond_gap=1e-5)
+    check(net, 2, "bf16", ["column", "2ps", "overl"], [{"n_bands": 3}], bias=0.1, gspread=0.2,
+          flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION, dzl_kind="head")
+
+
 def test_vgg_reduced_fp32():
     """VGG-16 topology (13 conv + 5 pool), reduced channels/size, fp32: every mode <= 1e-5."""
     net = WL.vgg16(H=64, W=64, width_div=8)

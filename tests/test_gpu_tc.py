@@ -56,6 +56,30 @@ def test_two_conv_layers_vs_oracle(cin, cout, H, W, k, p):
                 assert e <= TOL, (mode, kw, i, key, e)
 
 
+@pytest.mark.parametrize("cin,cout,H,W,k,s,p", [(64, 64, 21, 35, 3, 2, 1), (64, 128, 16, 18, 1, 2, 0),
+                                                (8, 64, 37, 45, 7, 2, 3), (128, 64, 9, 30, 3, 2, 1),
+                                                (64, 256, 11, 13, 3, 2, 0)])
+def test_strided_layers_vs_oracle(cin, cout, H, W, k, s, p):
+    """Strided convs on tcgen05: FP with TMA element strides, wgrad with a strided input box,
+    dgrad as s x s parity classes of the flipped weights (stride-2 convs of ResNet-50:
+    3x3/s2/p1, 1x1/s2 projection, 7x7/s2/p3 stem)."""
+    net = {"C": 3, "H": H, "W": W, "classes": 10,
+           "ops": [WL.conv(0, cin, 3, 1, 1), WL.conv(1, cout, k, s, p, epi="affine"), WL.conv(2, 64, 3, 1, 1)]}
+    B = 2
+    params = WL.make_params(net, seed=7, bias_scale=0.1, gamma_spread=0.2, bf16=True)
+    x = WL.make_input(net, B, seed=4, bf16=True)
+    ts, aux = C.forward(net, params, x, store=C.bf16_store)
+    dzl = WL.make_dzl(ts[-1].shape, bf16=True)
+    g_ref, _ = C.backward(net, params, ts, aux, dzl, need_dx=False)
+    for mode, kw in (("column", {}), ("2ps", {"band_rows": 2}), ("overl", {"n_bands": 2})):
+        zl, g = run(net, B, mode, params, x, dzl, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION, **kw)
+        assert rel(zl, ts[-1]) <= TOL, (mode, "zl", rel(zl, ts[-1]))
+        for i in range(3):
+            for key in g_ref[i]:
+                e = rel(g[i][key], g_ref[i][key])
+                assert e <= TOL, (mode, kw, i, key, e)
+
+
 def test_tc_matches_simt():
     """Tensor-core and SIMT kernels on the same bf16 inputs (same storage rounding points).
     No max-pool: argmax near-ties would make the comparison ill-conditioned (R17c)."""

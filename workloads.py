@@ -67,6 +67,38 @@ def vgg16(H=224, W=224, C=3, classes=10, segments="none", width_div=1, cfg=None)
     return {"C": C, "H": H, "W": W, "classes": classes, "ops": ops, "name": "vgg16"}
 
 
+def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, blocks=(3, 4, 6, 3)):
+    """ResNet-50 v1.5 (torchvision topology: stride on the 3x3 of the first block of stages 2-4,
+    1x1 projection shortcut on every stage's first block), frozen-statistics BN folded into
+    per-channel affine convs (R11, R14).  Bottleneck:
+        a = relu(aff(conv1x1(x)));  b = relu(aff(conv3x3/s(a)));  sc = aff(conv1x1/s(x)) or x
+        out = relu(aff(conv1x1(b)) + sc)      (the residual add is fused into the last conv)
+    segments: "stage" checkpoints after the stem max-pool and after every stage but the last
+    (2PS-H / OverL-H), "none" = whole-net row-centric."""
+    d = lambda c: max(8, c // width_div)
+    ops = [conv(0, d(64), 7, 2, 3, epi="affine"), maxpool(1, 3, 2, 1, seg_end=(segments == "stage"))]
+    t, cin = 2, d(64)
+    for si, (nb, w) in enumerate(zip(blocks, (64, 128, 256, 512))):
+        for bi in range(nb):
+            s = 2 if (bi == 0 and si > 0) else 1
+            x = t
+            ops.append(conv(x, d(w), 1, 1, 0, epi="affine"))
+            a = len(ops)
+            ops.append(conv(a, d(w), 3, s, 1, epi="affine"))
+            b = len(ops)
+            if bi == 0:
+                ops.append(conv(x, d(4 * w), 1, s, 0, epi="affine", relu=False))
+                sc = len(ops)
+            else:
+                sc = x
+            ops.append(conv(b, d(4 * w), 1, 1, 0, epi="affine", relu=True, res=sc))
+            t = len(ops)
+        if segments == "stage" and si < len(blocks) - 1:
+            ops[-1]["seg_end"] = True
+    ops[-1]["seg_end"] = False
+    return {"C": C, "H": H, "W": W, "classes": classes, "ops": ops, "name": "resnet50"}
+
+
 # ---------------------------------------------------------------- inputs
 def _rng(seed):
     return np.random.Generator(np.random.PCG64(seed))
