@@ -26,7 +26,7 @@ sys.path.insert(0, ROOT)
 
 import workloads as WL  # noqa: E402
 
-METRIC = "train images/s (VGG-16 conv stack, 224x224x3, row-centric 2PS-H, bf16)"
+METRIC = "train images/s (row-centric 2PS-H, bf16)"
 UNIT = "images/s"
 
 
@@ -36,14 +36,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=32)
-    ap.add_argument("--hw", type=int, default=224)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+                    help="BASELINE.json configs: c2 VGG-16 224^2 B32 (default), c3 ResNet-50 224^2 B256, "
+                         "c4 ResNet-50 3600x2400 B8, c5 VGG-16 2048^2 B16")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--hw", type=int, default=0)
     ap.add_argument("--mode", default="2ps", choices=["2ps", "overl", "column"])
     ap.add_argument("--segments", default="pool", choices=["pool", "none"])
     ap.add_argument("--n-bands", type=int, default=4)
     ap.add_argument("--band-rows", type=int, default=0)
     ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
+    ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
     return ap.parse_args()
 
 
@@ -95,8 +99,21 @@ class ClockSampler(threading.Thread):
                 "samples": len(self.samples)}
 
 
+CONFIGS = {   # (model, H, W, batch, description)
+    "c2": ("vgg16", 224, 224, 32, "C2: VGG-16 conv stack 224x224x3"),
+    "c3": ("resnet50", 224, 224, 256, "C3: ResNet-50 v1.5 224x224x3"),
+    "c4": ("resnet50", 3600, 2400, 8, "C4: ResNet-50 v1.5 3600x2400x3 (climate-scale)"),
+    "c5": ("vgg16", 2048, 2048, 16, "C5: VGG-16 conv stack 2048x2048x3"),
+}
+
+
 def make_net(a):
-    return WL.vgg16(H=a.hw, W=a.hw, segments=a.segments)
+    model, H, W, _, _ = CONFIGS[a.config]
+    if a.hw:
+        H = W = a.hw
+    if model == "vgg16":
+        return WL.vgg16(H=H, W=W, segments=a.segments)
+    return WL.resnet50(H=H, W=W, segments="stage" if a.segments == "pool" else "none")
 
 
 def cpu_baseline(a, steps=1):
@@ -106,7 +123,7 @@ def cpu_baseline(a, steps=1):
     from oracle import column as C
     cores = os.cpu_count() or 1
     oracle.set_threads(cores)
-    net = make_net(a)
+    net, scale, what = oracle_sample(a)
     params = WL.make_params(net, seed=2)
     x = WL.make_input(net, 1, seed=0)
     lab = WL.make_labels(net, 1)
@@ -115,10 +132,22 @@ def cpu_baseline(a, steps=1):
         t0 = time.perf_counter()
         params, loss, _, _, _ = C.step(net, params, x, lab, 0.01)
         times.append(time.perf_counter() - t0)
-    return {"value": 1.0 / statistics.mean(times), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "1 image of the C2 batch at 224x224x3, one fp64 column step (FP+head+BP+SGD), "
-                      "OpenMP over (b, c_out), mean of %d" % steps,
-            "s_per_image": statistics.mean(times)}
+    return {"value": scale / statistics.mean(times), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "%s, one fp64 column step (FP+head+BP+SGD), OpenMP over (b, c_out), mean of %d"
+                      % (what, steps),
+            "s_per_image": statistics.mean(times) / scale}
+
+
+def oracle_sample(a):
+    """Bounded CPU sample of the workload: one full image for C2/C3; for the climate-scale
+    configs one full-width strip of 224 image rows (images/s extrapolated by strip/H)."""
+    net = make_net(a)
+    if net["H"] * net["W"] <= 512 * 512:
+        return net, 1.0, "1 image of the %s batch" % a.config.upper()
+    strip = 224
+    sub = dict(net, H=strip)
+    return sub, strip / net["H"], ("1 image strip of %d rows x full width %d of %s (extrapolated x%d/%d)"
+                                   % (strip, net["W"], a.config.upper(), strip, net["H"]))
 
 
 def run_reference(a):
@@ -128,7 +157,7 @@ def run_reference(a):
     cb = cpu_baseline(a, steps=1)             # warm-up/first measurement
     import oracle
     from oracle import column as C
-    net = make_net(a)
+    net, scale, what = oracle_sample(a)
     params = WL.make_params(net, seed=2)
     x = WL.make_input(net, 1, seed=0)
     lab = WL.make_labels(net, 1)
@@ -139,13 +168,13 @@ def run_reference(a):
         t0 = time.perf_counter()
         params, _, _, _, _ = C.step(net, params, x, lab, 0.01)
         times.append(time.perf_counter() - t0)
-    ms = 1000.0 * statistics.mean(times)
+    ms = 1000.0 * statistics.mean(times) / scale
     v = 1000.0 / ms
     cb = dict(cb, value=v, sample=cb["sample"].replace("mean of 1", "mean of %d" % a.steps))
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
                       "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
                       "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                      "config": {"workload": "C2 VGG-16 224x224x3 (1-image bounded sample per step)",
+                      "config": {"workload": "%s (bounded sample per step: %s)" % (CONFIGS[a.config][4], what),
                                  "global_batch": 1, "parallelism": "cpu"},
                       "cpu_baseline": cb,
                       "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
@@ -172,7 +201,7 @@ def main():
     torch.cuda.set_stream(stream)
 
     net = make_net(a)
-    B = a.batch
+    B = a.batch or CONFIGS[a.config][3]
     flags = LB.FLAG_NO_TCGEN05 if a.simt else 0
     kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}
     if a.mode == "column":
@@ -270,6 +299,8 @@ def main():
     tc_ms, tc_n, tc_fl = plan.profile_read(0, stream)
     wg_ms, wg_n, wg_fl = plan.profile_read(1, stream)
     ot_ms, ot_n, _ = plan.profile_read(2, stream)
+    if a.per_op_csv:
+        plan.profile_dump(a.per_op_csv, stream)
     plan.profile(False)
     peaks, peak_src = measured_peaks()
     achieved = tc_fl / (tc_ms / 1000.0) / 1e12 if tc_ms > 0 else 0.0
@@ -314,7 +345,7 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[0,1) images, U{0..9} labels)",
-               "config": {"workload": "C2: VGG-16 conv stack 224x224x3, batch %d per GPU, bf16" % B,
+               "config": {"workload": "%s, batch %d per GPU, bf16" % (CONFIGS[a.config][4], B),
                           "global_batch": B * world, "seq_len": None,
                           "parallelism": "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU",
                           "mode": a.mode, "segments": a.segments, "bands": kw,

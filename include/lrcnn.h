@@ -200,6 +200,9 @@ LRCNN_API lrcnn_status lrcnn_profile_enable(lrcnn_plan_t *plan, int enable);
 LRCNN_API lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long long *launches,
                                 double *flops, void *stream);
 LRCNN_API lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan);
+/* Per-op profile since the last reset (synchronises the stream): CSV with one line per
+ * (op, kind in fwd|dgrad|wgrad|param_grad|pool_fwd|pool_bwd|elt_fwd|elt_bwd): launches, ms, FLOPs. */
+LRCNN_API lrcnn_status lrcnn_profile_dump(lrcnn_plan_t *plan, const char *path, void *stream);
 
 /* Number of kernel launches the last forward/backward/step enqueued. */
 LRCNN_API lrcnn_status lrcnn_last_launch_count(const lrcnn_plan_t *plan, long long *launches);

@@ -51,6 +51,7 @@ struct TcConv {
     // (grid_col*a_mul + tap_ox[t], grid_row*a_mul + tap_oy[t]) of the input view (TMA element
     // stride a_mul), weights tap index tap_w[t]; output pixel = (o_row0 + o_stride*grid_row, ...)
     int a_mul, ntaps, o_row0, o_col0, o_stride, halo_ok;
+    int tma_out;           // FP: stage the output tile in smem and TMA-store it
     int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
 };
@@ -68,11 +69,14 @@ struct TcWgrad {
 static constexpr int kThreads = 192;
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
-template <int BN>
+static constexpr int kStageBudget = 192 * 1024;
+static constexpr int kOutStage = 128 * 128;       // epilogue staging: 128 pixels x 64 channels bf16
+template <int BN, int KC = 64>
 struct ConvCfg {
-    static constexpr int kStageBytes = kABytes + BN * 128;
-    static constexpr int kStages = (192 * 1024) / kStageBytes;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kA = 128 * KC * 2, kB = BN * KC * 2;
+    static constexpr int kStageBytes = kA + kB;
+    static constexpr int kStages = kStageBudget / kStageBytes > 16 ? 16 : kStageBudget / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 2 * kOutStage + 1024 + 256;
     static constexpr uint32_t kTmemCols = 2 * BN;
 };
 
@@ -80,6 +84,105 @@ __device__ __forceinline__ float bf2f(uint16_t u) { return __uint_as_float(((uin
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *m, const void *src, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// FP epilogue with coalesced TMA stores: per 64-channel group the 4 epilogue warps write the
+// bf16 tile (128 pixels x 128 B, 128B-swizzled: conflict-free 16-byte smem stores) into one of
+// two staging buffers, then one thread issues a TMA tensor store of the TW x TH pixel
+// rectangle; the output map's row extent ends at the band's last computed row, so pixels
+// outside the band / image are clipped by TMA.
+template <int BN>
+__device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
+                                                  uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
+                                                  int lane) {
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    const int ew = warp & 3;
+    const int m = ew * 32 + lane;
+    const bool leader = (warp == 2 && lane == 0);
+    int acc = 0, sbuf = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
+        const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
+        const int yg = yg0 + m / P.TW, xg = xg0 + m % P.TW;
+        const bool valid = yg < P.out_b && xg < P.Wo;
+        ptx::mbar_wait(tfull + acc, aphase);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int grp = 0; grp < BN / 64; ++grp) {
+            const int nb = n0 + grp * 64;
+            if (nb >= P.n_out) break;
+            uint32_t v[64];
+            ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+            ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + grp * 64 + 32,
+                           *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            ptx::tmem_ld_wait();
+            if (leader) bulk_wait_read1();             // the store that last used this buffer has read it
+            epi_bar();
+            uint8_t *buf = stage_out + sbuf * kOutStage + m * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int n = nb + c * 8;
+                float f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c * 8 + j]);
+                if (valid && n < P.n_out) {
+                    if (P.epi != 0) {
+                        uint4 bb = *reinterpret_cast<const uint4 *>(P.bias + n);
+                        const uint16_t *bh = reinterpret_cast<const uint16_t *>(&bb);
+                        uint4 be = P.epi == 2 ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
+                        const uint16_t *beh = reinterpret_cast<const uint16_t *>(&be);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            float bj = n + j < P.c_real ? bf2f(bh[j]) : 0.f;
+                            if (P.epi == 1) f[j] += bj;
+                            else f[j] = n + j < P.c_real ? bj * f[j] + bf2f(beh[j]) : 0.f;
+                        }
+                    }
+                    if (P.has_res) {
+                        uint4 rr = *reinterpret_cast<const uint4 *>(
+                            (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                            ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp + n);
+                        const uint16_t *rh = reinterpret_cast<const uint16_t *>(&rr);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] += bf2f(rh[j]);
+                    }
+                    if (P.relu) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
+                    }
+                }
+                uint4 o;
+                o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
+                *reinterpret_cast<uint4 *>(buf + ((c ^ (m & 7)) << 4)) = o;
+            }
+            fence_async_smem();
+            epi_bar();
+            if (leader) {
+                tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, xg0, yg0 - P.out.base, b);
+                bulk_commit();
+            }
+            sbuf ^= 1;
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (leader) bulk_wait_all();
 }
 
 // Epilogue warps (4 warps = 128 TMEM lanes = 128 pixels of the tile): tcgen05.ld the
@@ -168,16 +271,24 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
     }
 
 // ------------------------------------------------------------------ conv FP / dgrad
-template <int BN>
+// KC = input channels per pipeline stage: 64 (128-byte rows, SWIZZLE_128B, 4 MMAs of K=16) for
+// regular layers, 16 (32-byte rows, SWIZZLE_32B, 1 MMA) for small-channel layers (padded RGB
+// input of conv1_1 / the 7x7 stem), which would otherwise waste 8x tensor work on zero channels.
+template <int BN, int KC>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcConv P) {
-    using Cfg = ConvCfg<BN>;
+    k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmO, const TcConv P) {
+    using Cfg = ConvCfg<BN, KC>;
     constexpr int S = Cfg::kStages;
+    constexpr int ABYTES = Cfg::kA, BBYTES = Cfg::kB;
+    constexpr uint32_t SBO = 8 * KC * 2;             // 8-row core-matrix groups
+    constexpr uint32_t LAYOUT = KC == 64 ? 2u : 6u;  // SWIZZLE_128B : SWIZZLE_32B
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
-    uint8_t *sB = smem + S * kABytes;
-    uint64_t *full = (uint64_t *)(sB + S * BN * 128);
+    uint8_t *sB = smem + S * ABYTES;
+    uint8_t *sO = sB + S * BBYTES;                   // 2 x 16 KB epilogue staging (1024-aligned)
+    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
@@ -209,10 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ks = 0; ks < P.k_steps; ++ks) {
                     const int tap = ks / P.cin_chunks, c = ks - tap * P.cin_chunks;
                     ptx::mbar_wait(empty + stage, phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(full + stage, kABytes + BN * 128);
-                    ptx::tma_load_4d(sA + stage * kABytes, &tmA, full + stage, c * 64, x0 + P.tap_ox[tap],
+                    ptx::mbar_arrive_expect_tx(full + stage, ABYTES + BBYTES);
+                    ptx::tma_load_4d(sA + stage * ABYTES, &tmA, full + stage, c * KC, x0 + P.tap_ox[tap],
                                      y0 + P.tap_oy[tap] - P.in_base, b);
-                    ptx::tma_load_3d(sB + stage * BN * 128, &tmB, full + stage, c * 64, P.tap_w[tap], n0);
+                    ptx::tma_load_3d(sB + stage * BBYTES, &tmB, full + stage, c * KC, P.tap_w[tap], n0);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -229,12 +340,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ks = 0; ks < P.k_steps; ++ks) {
                     ptx::mbar_wait(full + stage, phase);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + stage * kABytes);
-                    const uint32_t b0 = ptx::smem_u32(sB + stage * BN * 128);
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * ABYTES);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * BBYTES);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        uint64_t ad = ptx::smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                        uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 32, 16, 1024);
+                    for (int kk = 0; kk < KC / 16; ++kk) {
+                        uint64_t ad = ptx::smem_desc(a0 + kk * 32, 16, SBO, LAYOUT);
+                        uint64_t bd = ptx::smem_desc(b0 + kk * 32, 16, SBO, LAYOUT);
                         if (!(P.dbg & 2)) ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
                     }
                     ptx::umma_commit(empty + stage);
@@ -245,7 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
+        if (P.tma_out) conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
+        else conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -387,8 +499,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 static constexpr int kWgA = 2 * kABytes;
 template <int BN>
 struct WgCfg {
-    static constexpr int kStageBytes = kWgA + (BN / 64) * kABytes;
-    static constexpr int kStages = (192 * 1024) / kStageBytes;
+    // B operand (shifted band input): BN/KB boxes of KB channels (KB = 64, SWIZZLE_128B; or
+    // KB = BN = 16, SWIZZLE_32B for small-channel inputs)
+    static constexpr int KB = BN < 64 ? BN : 64;
+    static constexpr int kBBox = 128 * KB * 2;
+    static constexpr int kStageBytes = kWgA + (BN / KB) * kBBox;
+    static constexpr int kStages = (192 * 1024) / kStageBytes > 12 ? 12 : (192 * 1024) / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
     static constexpr uint32_t kTmemCols = 2 * BN;
 };
@@ -447,8 +563,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tma_load_4d(st, &tmD, full + stage, cot * 128, x0, y0 - P.dy_base, b);
                     ptx::tma_load_4d(st + kABytes, &tmD, full + stage, cot * 128 + 64, x0, y0 - P.dy_base, b);
 #pragma unroll
-                    for (int h = 0; h < BN / 64; ++h)
-                        ptx::tma_load_4d(st + kWgA + h * kABytes, &tmX, full + stage, cit * BN + h * 64,
+                    for (int h = 0; h < BN / Cfg::KB; ++h)
+                        ptx::tma_load_4d(st + kWgA + h * Cfg::kBBox, &tmX, full + stage, cit * BN + h * Cfg::KB,
                                          x0 * P.s - P.pad + kx, y0 * P.s - P.pad + ky - P.x_base, b);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -475,7 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < 8; ++kk) {
                         // MN-major SW128: 64-element MN chunks LBO = 16 KB apart, 8-row K groups SBO = 1 KB
                         uint64_t ad = ptx::smem_desc_sw128(a0 + kk * 2048, kABytes, 1024);
-                        uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 2048, kABytes, 1024);
+                        uint64_t bd = Cfg::KB == 64 ? ptx::smem_desc_sw128(b0 + kk * 2048, kABytes, 1024)
+                                                    : ptx::smem_desc(b0 + kk * 16 * Cfg::KB * 2, 4096, 8 * Cfg::KB * 2, 6);
                         ptx::umma_bf16(d, ad, bd, idesc, (pt != p0 || kk != 0) ? 1u : 0u);
                     }
                     ptx::umma_commit(empty + stage);
@@ -498,16 +615,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             float *dst = P.dw + ((long long)co * taps + tap) * P.cin_p;
             ptx::mbar_wait(tfull + acc, aphase);
             ptx::tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
+            if constexpr (BN < 32) {
+                uint32_t v[16];
+                ptx::tmem_ld16(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN, v);
                 ptx::tmem_ld_wait();
-                if (co >= P.c_out) continue;
-                const int ci0 = cit * BN + c * 32;
+                if (co < P.c_out) {
+                    const int ci0 = cit * BN;
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (ci0 + j < P.cin_p) atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                    for (int j = 0; j < 16; ++j)
+                        if (ci0 + j < P.cin_p) atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                }
+            } else {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (co >= P.c_out) continue;
+                    const int ci0 = cit * BN + c * 32;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (ci0 + j < P.cin_p) atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -550,29 +679,34 @@ static int num_sms() {
 
 // 4D map over a band View: dims (Cp, W, rows, B); box (64, TW*es, TH*es, 1) with TMA element
 // stride es along W and H (es = conv stride: the box then holds TW x TH strided pixels); 128B swizzle.
-static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH, int es = 1) {
+static CUtensorMapSwizzle swz_for(int kc) {
+    return kc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : (kc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// kc = channels per box (64 -> 128B rows / SWIZZLE_128B, 16 -> 32B rows / SWIZZLE_32B).
+static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH, int es = 1, int kc = 64) {
     auto fn = encode_fn();
     if (!fn || v.rows <= 0 || TW * es > 256 || TH * es > 256) return false;
     cuuint64_t dims[4] = {(cuuint64_t)v.Cp, (cuuint64_t)v.W, (cuuint64_t)v.rows, (cuuint64_t)B};
     cuuint64_t strides[3] = {(cuuint64_t)v.Cp * 2, (cuuint64_t)v.W * v.Cp * 2, (cuuint64_t)v.bs * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)(TW * es), (cuuint32_t)(TH * es), 1};
+    cuuint32_t box[4] = {(cuuint32_t)kc, (cuuint32_t)(TW * es), (cuuint32_t)(TH * es), 1};
     cuuint32_t estr[4] = {1, (cuuint32_t)es, (cuuint32_t)es, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    swz_for(kc), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-// 3D map over OHWI weights [rows][taps][cin_p]: box (64 channels, 1 tap, BN rows); channels
+// 3D map over OHWI weights [rows][taps][cin_p]: box (kc channels, 1 tap, BN rows); channels
 // beyond cin_p (small-channel layers, e.g. the padded RGB input) are zero-filled by TMA.
-static bool encode_w(CUtensorMap *m, const void *w, int rows, int taps, int cin_p, int BN) {
+static bool encode_w(CUtensorMap *m, const void *w, int rows, int taps, int cin_p, int BN, int kc = 64) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {(cuuint64_t)cin_p, (cuuint64_t)taps, (cuuint64_t)rows};
     cuuint64_t strides[2] = {(cuuint64_t)cin_p * 2, (cuuint64_t)taps * cin_p * 2};
-    cuuint32_t box[3] = {64, 1, (cuuint32_t)BN};
+    cuuint32_t box[3] = {(cuuint32_t)kc, 1, (cuuint32_t)BN};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(w), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz_for(kc), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -592,17 +726,18 @@ static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 bool tc_available() { return true; }
 
-template <int BN>
-static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, int tiles, cudaStream_t st) {
-    using Cfg = ConvCfg<BN>;
+template <int BN, int KC>
+static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O, int tiles,
+                        cudaStream_t st) {
+    using Cfg = ConvCfg<BN, KC>;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_conv_tc<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
             return false;
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_tc<BN><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, P);
+    k_conv_tc<BN, KC><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, O, P);
     return true;
 }
 
@@ -638,12 +773,13 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     static const int dbg = env_int("LRCNN_TC_DBG", 0);
     P.dbg = dbg;
     P.in_base = in.base;
-    P.cin_chunks = (cin_p + 63) / 64;
+    static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
+    const int KC = (cin_p <= 16 && !(halo_on && P.halo_ok)) ? 16 : 64;   // small-channel layers: 16-ch chunks
+    P.cin_chunks = (cin_p + KC - 1) / KC;
     P.k_steps = P.ntaps * P.cin_chunks;
     P.n_tiles = (P.n_out + BN - 1) / BN;
     CUtensorMap A, Bm;
-    if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN)) return false;
-    static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
+    if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN, KC)) return false;
     if (halo_on && P.halo_ok) {
         P.TW = 8; P.TH = 16;
         P.tiles_x = (P.Wo + 7) / 8;
@@ -660,11 +796,25 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
-    if (!encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul)) return false;
+    if (!encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC)) return false;
+    // output map for the TMA-store epilogue (FP, unit output stride): rows end at out_b
+    static const int tma_out = env_int("LRCNN_TMA_OUT", 1);
+    CUtensorMap O = A;
+    P.tma_out = 0;
+    if (tma_out && P.mode == 0 && P.o_stride == 1 && P.out.Cp % 8 == 0) {
+        View ov = P.out;
+        ov.rows = P.out_b - P.out.base;
+        if (encode_view(&O, ov, P.B, P.TW, P.TH)) P.tma_out = 1;
+    }
     int tiles = P.m_tiles * P.n_tiles;
-    if (BN == 64) return launch_conv<64>(P, A, Bm, tiles, st);
-    if (BN == 128) return launch_conv<128>(P, A, Bm, tiles, st);
-    return launch_conv<256>(P, A, Bm, tiles, st);
+    if (KC == 16) {
+        if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, tiles, st);
+        if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, tiles, st);
+        return launch_conv<256, 16>(P, A, Bm, O, tiles, st);
+    }
+    if (BN == 64) return launch_conv<64, 64>(P, A, Bm, O, tiles, st);
+    if (BN == 128) return launch_conv<128, 64>(P, A, Bm, O, tiles, st);
+    return launch_conv<256, 64>(P, A, Bm, O, tiles, st);
 }
 
 bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
@@ -754,7 +904,7 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
-    const int BN = x.Cp >= 128 ? 128 : 64;
+    const int BN = x.Cp >= 128 ? 128 : (x.Cp <= 16 ? 16 : 64);
     P.co_tiles = (dy.Cp + 127) / 128;
     P.ci_tiles = (x.Cp + BN - 1) / BN;
     const int base_items = P.co_tiles * a.k * a.k * P.ci_tiles;
@@ -767,7 +917,8 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.out_a = a.a; P.dy_base = dy.base; P.x_base = x.base;
     CUtensorMap D, X;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
-    if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s)) return false;
+    if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s, BN < 64 ? BN : 64)) return false;
+    if (BN == 16) return launch_wgrad<16>(P, D, X, st);
     if (BN == 64) return launch_wgrad<64>(P, D, X, st);
     return launch_wgrad<128>(P, D, X, st);
 }

@@ -46,7 +46,25 @@ struct Run {
     cudaStream_t st;
     int prec;
     size_t E;   // element bytes
+    cudaStream_t side = nullptr;   // wgrad / param-grad stream (nullptr: everything on st)
+    bool side_busy = false;
 };
+
+// Fork: side stream waits for everything enqueued so far on the main stream.
+static cudaError_t fork_side(Run &R) {
+    cudaError_t e = cudaEventRecord((cudaEvent_t)R.P.ev_fork, R.st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(R.side, (cudaEvent_t)R.P.ev_fork, 0);
+    R.side_busy = true;
+    return e;
+}
+// Join: main stream waits for the side stream (before buffers it reads are overwritten).
+static cudaError_t join_side(Run &R) {
+    if (!R.side || !R.side_busy) return cudaSuccess;
+    cudaError_t e = cudaEventRecord((cudaEvent_t)R.P.ev_join, R.side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(R.st, (cudaEvent_t)R.P.ev_join, 0);
+    R.side_busy = false;
+    return e;
+}
 
 static View full_view(void *p, const TensorInfo &t) {
     View v;
@@ -100,8 +118,9 @@ struct ProfScope {
     Run &R;
     int cls;
     double flops;
+    int tag;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    ProfScope(Run &r, int c, double f) : R(r), cls(c), flops(f) {
+    ProfScope(Run &r, int c, double f, int t = -1) : R(r), cls(c), flops(f), tag(t) {
         if (R.P.profiling) {
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
@@ -113,6 +132,7 @@ struct ProfScope {
             cudaEventRecord(e1, R.st);
             R.P.pending_events[cls].push_back({(void *)e0, (void *)e1});
             R.P.pending_flops[cls].push_back(flops);
+            R.P.pending_tags[cls].push_back(tag);
         }
     }
 };
@@ -139,7 +159,7 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
         A.beta = o.beta_cnt ? prm(R, o.beta_off) : nullptr;
         A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.epi = o.d.epi; A.relu = o.d.relu;
         A.a = a; A.b_ = b; A.B = P.net.B;
-        ProfScope ps(R, 0, conv_flops(P, o, b - a));
+        ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 0);
         ++P.launches;
         if (P.use_tc && tc_conv_fwd(A, R.st)) { ++P.tc_launches; CK(cudaGetLastError()); return LRCNN_OK; }
         CK(simt_conv_fwd(R.prec, A, R.st));
@@ -147,13 +167,13 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
         PoolArgs A;
         A.in = in; A.out = out; A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.a = a; A.b = b; A.B = P.net.B;
         ++P.launches;
-        ProfScope ps(R, 2, 0);
+        ProfScope ps(R, 2, 0, i * 8 + 4);
         CK(simt_pool_fwd(R.prec, A, R.st));
     } else {
         EltArgs A;
         A.x0 = in; A.x1 = act_view(R, S, r, o.d.res); A.out = out; A.relu = o.d.relu; A.a = a; A.b = b; A.B = P.net.B;
         ++P.launches;
-        ProfScope ps(R, 2, 0);
+        ProfScope ps(R, 2, 0, i * 8 + 6);
         CK(simt_add_fwd(R.prec, A, R.st));
     }
     return LRCNN_OK;
@@ -223,6 +243,10 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     const bool need_dx = o.in_t != 0;
     if (o.d.kind == LRCNN_OP_CONV) {
         float *g = R.grads;
+        // wgrad and the bias/affine reduction only read complete data of this band: run them on
+        // the side stream so they overlap the dgrad chain (joined at the end of the band)
+        cudaStream_t gst = R.st;
+        if (R.side) { CK(fork_side(R)); gst = R.side; }
         if (o.d.epi != LRCNN_EPI_NONE) {
             ParamGradArgs A;
             A.dy = dy; A.t = act_view(R, S, r, t);
@@ -233,8 +257,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.dbeta = o.d.epi == LRCNN_EPI_AFFINE ? g + o.beta_off : nullptr;
             A.epi = o.d.epi; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
             ++P.launches;
-            ProfScope ps(R, 2, 0);
-            CK(simt_param_grad(R.prec, A, R.st));
+            ProfScope ps(R, 2, 0, i * 8 + 3);
+            CK(simt_param_grad(R.prec, A, gst));
         }
         const void *gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
         {
@@ -242,9 +266,9 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.dy = dy; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
             A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
             ++P.launches;
-            ProfScope ps(R, 1, conv_flops(P, o, b - a));
-            if (P.use_tc && tc_conv_wgrad(A, R.st)) ++P.tc_launches;
-            else CK(simt_conv_wgrad(R.prec, A, R.st));
+            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2);
+            if (P.use_tc && tc_conv_wgrad(A, gst)) ++P.tc_launches;
+            else CK(simt_conv_wgrad(R.prec, A, gst));
             CK(cudaGetLastError());
         }
         if (need_dx) {
@@ -255,7 +279,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.ra = std::max(0, a * o.d.s - o.d.p);
             A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
             ++P.launches;
-            ProfScope ps(R, 0, conv_flops(P, o, b - a));
+            ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1);
             if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
             else CK(simt_conv_dgrad(R.prec, A, R.st));
             CK(cudaGetLastError());
@@ -267,7 +291,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.gate = tr.relu; A.a = a; A.b = b; A.B = B;
             if (o.d.res != 0) {
                 ++P.launches;
-                ProfScope ps(R, 2, 0);
+                ProfScope ps(R, 2, 0, i * 8 + 7);
                 CK(simt_acc_gate(R.prec, A, R.st));
             }
         }
@@ -279,7 +303,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.ra = std::max(0, a * o.d.s - o.d.p);
             A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
             ++P.launches;
-            ProfScope ps(R, 2, 0);
+            ProfScope ps(R, 2, 0, i * 8 + 5);
             CK(simt_pool_bwd(R.prec, A, R.st));
         }
     } else {
@@ -290,7 +314,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.dy = dy; A.dx = dlt_view(R, S, s, r, tid); A.act = act_view(R, S, r, tid);
             A.gate = P.t[tid].relu; A.a = a; A.b = b; A.B = B;
             ++P.launches;
-            ProfScope ps(R, 2, 0);
+            ProfScope ps(R, 2, 0, i * 8 + 7);
             CK(simt_acc_gate(R.prec, A, R.st));
         }
     }
@@ -301,6 +325,18 @@ static lrcnn_status run_backward(Run &R) {
     Plan &P = R.P;
     lrcnn_status st;
     const bool recompute = !(P.seg.size() == 1 && P.seg[0].E.size() == 1);
+    static const int side_on = getenv("LRCNN_SIDE") ? atoi(getenv("LRCNN_SIDE")) : 1;
+    if (side_on && !P.profiling) {
+        if (!P.side_stream) {   // created on the first (eager) call, before any graph capture
+            cudaStream_t ss;
+            cudaEvent_t e0, e1;
+            CK(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+            P.side_stream = ss; P.ev_fork = e0; P.ev_join = e1;
+        }
+        R.side = (cudaStream_t)P.side_stream;
+    }
     // transposed weights for the tensor-core dgrad (gamma folded in)
     if (P.use_tc) {
         for (const OpInfo &o : P.op) {
@@ -337,6 +373,7 @@ static lrcnn_status run_backward(Run &R) {
             }
             for (auto it = S.ops.rbegin(); it != S.ops.rend(); ++it)
                 if ((st = op_backward(R, S, s, r, *it)) != LRCNN_OK) return st;
+            CK(join_side(R));
             if (P.opts.mode == LRCNN_2PS && r > 0) {
                 for (int t : S.tensors) {
                     if (t == S.out_t) continue;
@@ -381,6 +418,12 @@ lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
 lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
     if (plan) {
         if (plan->P.graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)plan->P.graph_exec);
+        if (plan->P.side_stream) {
+            cudaStreamSynchronize((cudaStream_t)plan->P.side_stream);
+            cudaStreamDestroy((cudaStream_t)plan->P.side_stream);
+            cudaEventDestroy((cudaEvent_t)plan->P.ev_fork);
+            cudaEventDestroy((cudaEvent_t)plan->P.ev_join);
+        }
         for (int c = 0; c < 3; ++c)
             for (auto &e : plan->P.pending_events[c]) {
                 cudaEventDestroy((cudaEvent_t)e.first);
@@ -603,8 +646,10 @@ lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan) {
         }
         plan->P.pending_events[c].clear();
         plan->P.pending_flops[c].clear();
+        plan->P.pending_tags[c].clear();
         plan->P.prof[c] = ProfileSlot();
     }
+    plan->P.per_tag.clear();
     return LRCNN_OK;
 }
 
@@ -621,15 +666,48 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
             P.prof[c].ms += t;
             P.prof[c].flops += P.pending_flops[c][i];
             P.prof[c].launches += 1;
+            const int tag = P.pending_tags[c][i];
+            if (tag >= 0) {
+                auto it = std::find_if(P.per_tag.begin(), P.per_tag.end(),
+                                       [tag](const std::pair<int, ProfileSlot> &q) { return q.first == tag; });
+                if (it == P.per_tag.end()) { P.per_tag.push_back({tag, ProfileSlot()}); it = P.per_tag.end() - 1; }
+                it->second.ms += t;
+                it->second.flops += P.pending_flops[c][i];
+                it->second.launches += 1;
+            }
             cudaEventDestroy((cudaEvent_t)e.first);
             cudaEventDestroy((cudaEvent_t)e.second);
         }
         P.pending_events[c].clear();
         P.pending_flops[c].clear();
+        P.pending_tags[c].clear();
     }
     if (ms) *ms = P.prof[cls].ms;
     if (launches) *launches = P.prof[cls].launches;
     if (flops) *flops = P.prof[cls].flops;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_profile_dump(lrcnn_plan_t *plan, const char *path, void *stream) {
+    if (!plan || !path) return fail(LRCNN_E_ARG, "bad args");
+    lrcnn_status st = lrcnn_profile_read(plan, 0, nullptr, nullptr, nullptr, stream);
+    if (st != LRCNN_OK) return st;
+    FILE *f = fopen(path, "w");
+    if (!f) return fail(LRCNN_E_ARG, std::string("cannot open ") + path);
+    static const char *kinds[8] = {"fwd", "dgrad", "wgrad", "param_grad", "pool_fwd", "pool_bwd", "elt_fwd", "elt_bwd"};
+    fprintf(f, "op,kind,k,s,c_in,c_out,h_out,w_out,launches,ms,flops\n");
+    auto v = plan->P.per_tag;
+    std::sort(v.begin(), v.end(), [](const std::pair<int, ProfileSlot> &a, const std::pair<int, ProfileSlot> &b) {
+        return a.first < b.first;
+    });
+    for (auto &e : v) {
+        const int op = e.first / 8, kind = e.first % 8;
+        const OpInfo &o = plan->P.op[op];
+        const TensorInfo &ti = plan->P.t[o.in_t], &to = plan->P.t[o.out_t];
+        fprintf(f, "%d,%s,%d,%d,%d,%d,%d,%d,%lld,%.6f,%.6e\n", op, kinds[kind], o.d.k, o.d.s, ti.C, to.C, to.H, to.W,
+                e.second.launches, e.second.ms, e.second.flops);
+    }
+    fclose(f);
     return LRCNN_OK;
 }
 

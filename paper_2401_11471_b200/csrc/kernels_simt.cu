@@ -151,8 +151,10 @@ __global__ void k_conv_wgrad(WgradArgs A) {
 // one fp32 atomicAdd per channel per block.
 template <typename T>
 __global__ void k_param_grad(ParamGradArgs A) {
+    // blockDim.x channel vectors (8 channels each) of group blockIdx.y; blockDim.y pixel lanes
     const int CV = blockDim.x, cv = threadIdx.x, py = threadIdx.y, PY = blockDim.y;
-    const int rows = A.b - A.a, W = A.dy.W, c0 = cv * 8;
+    const int rows = A.b - A.a, W = A.dy.W, c0 = (blockIdx.y * CV + cv) * 8;
+    const bool live = c0 < A.dy.Cp;
     const long long npix = (long long)A.B * rows * W;
     float s0[8], s1[8], gam[8], bet[8];
 #pragma unroll
@@ -162,7 +164,7 @@ __global__ void k_param_grad(ParamGradArgs A) {
         gam[j] = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
         bet[j] = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
     }
-    for (long long q = (long long)blockIdx.x * PY + py; q < npix; q += (long long)gridDim.x * PY) {
+    for (long long q = (long long)blockIdx.x * PY + py; live && q < npix; q += (long long)gridDim.x * PY) {
         int x = q % W;
         long long r = q / W;
         int y = A.a + (int)(r % rows);
@@ -184,14 +186,15 @@ __global__ void k_param_grad(ParamGradArgs A) {
     extern __shared__ float red[];   // [PY][CV*8] x 2
     float *r0 = red, *r1 = red + PY * CV * 8;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { r0[py * CV * 8 + c0 + j] = s0[j]; r1[py * CV * 8 + c0 + j] = s1[j]; }
+    for (int j = 0; j < 8; ++j) { r0[py * CV * 8 + cv * 8 + j] = s0[j]; r1[py * CV * 8 + cv * 8 + j] = s1[j]; }
     __syncthreads();
     for (int c = py * CV + cv; c < CV * 8; c += PY * CV) {
         float a0 = 0.f, a1 = 0.f;
         for (int k = 0; k < PY; ++k) { a0 += r0[k * CV * 8 + c]; a1 += r1[k * CV * 8 + c]; }
-        if (c < A.c_out) {
-            if (A.epi == 1) atomicAdd(A.db + c, a0);
-            else { atomicAdd(A.db + c, a1); atomicAdd(A.dbeta + c, a0); }
+        const int ch = blockIdx.y * CV * 8 + c;
+        if (ch < A.c_out) {
+            if (A.epi == 1) atomicAdd(A.db + ch, a0);
+            else { atomicAdd(A.db + ch, a1); atomicAdd(A.dbeta + ch, a0); }
         }
     }
 }
@@ -494,6 +497,142 @@ __global__ void k_transpose_w(const T *w, const T *gamma, T *wt, int cout, int c
     }
 }
 
+// ------------------------------------------------------------------ 8-channel vector versions (Cp % 8 == 0)
+// general k x k / stride s / pad p max-pool: padded cells never win, ties -> first in raster order
+template <typename T>
+__device__ __forceinline__ void pool_window8(const View &in, int b, int y, int x, int c0, int k, int s, int p,
+                                             float (&best)[8], int (&arg)[8]) {
+    bool first = true;
+    for (int ky = 0; ky < k; ++ky) {
+        int g = y * s - p + ky;
+        if (!vhas(in, g)) continue;
+        for (int kx = 0; kx < k; ++kx) {
+            int xi = x * s - p + kx;
+            if (xi < 0 || xi >= in.W) continue;
+            float v[8];
+            ld8((const T *)in.p + voff(in, b, g, xi) + c0, v);
+            const int code = ky * k + kx;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (first || v[j] > best[j]) { best[j] = v[j]; arg[j] = code; }
+            first = false;
+        }
+    }
+    if (first) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { best[j] = 0.f; arg[j] = -1; }
+    }
+}
+
+template <typename T>
+__global__ void k_pool_fwd8(PoolArgs A) {
+    const int CV = A.out.Cp / 8, Wo = A.out.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * Wo * CV;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int cv = idx % CV;
+        long long r = idx / CV;
+        int x = r % Wo; r /= Wo;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float best[8];
+        int arg[8];
+        pool_window8<T>(A.in, b, y, x, cv * 8, A.k, A.s, A.p, best, arg);
+        st8((T *)A.out.p + voff(A.out, b, y, x) + cv * 8, best);
+    }
+}
+
+// gather: every input pixel checks the (at most ceil(k/s)^2) windows that contain it
+template <typename T>
+__global__ void k_pool_bwd8(PoolArgs A) {
+    const int CV = A.dx.Cp / 8, Wi = A.dx.W, rows = A.rb - A.ra, Wo = A.dy.W;
+    long long n = (long long)A.B * rows * Wi * CV;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int cv = idx % CV;
+        long long r = idx / CV;
+        int xi = r % Wi; r /= Wi;
+        int g = A.ra + (int)(r % rows);
+        int b = (int)(r / rows);
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int ky = 0; ky < A.k; ++ky) {
+            int num = g + A.p - ky;
+            if (num < 0 || num % A.s) continue;
+            int y = num / A.s;
+            if (!vhas(A.dy, y)) continue;
+            for (int kx = 0; kx < A.k; ++kx) {
+                int nx = xi + A.p - kx;
+                if (nx < 0 || nx % A.s) continue;
+                int x = nx / A.s;
+                if (x >= Wo) continue;
+                float best[8], d[8];
+                int arg[8];
+                pool_window8<T>(A.act, b, y, x, cv * 8, A.k, A.s, A.p, best, arg);
+                ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
+                const int code = ky * A.k + kx;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (arg[j] == code) acc[j] += d[j];
+            }
+        }
+        T *dp = (T *)A.dx.p + voff(A.dx, b, g, xi) + cv * 8;
+        float o[8], a[8];
+        ld8(dp, o);
+        if (A.gate) ld8((const T *)A.act.p + voff(A.act, b, g, xi) + cv * 8, a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            o[j] += acc[j];
+            if (A.gate && !(a[j] > 0.f)) o[j] = 0.f;
+        }
+        st8(dp, o);
+    }
+}
+
+template <typename T>
+__global__ void k_acc_gate8(EltArgs A) {
+    const int CV = A.dx.Cp / 8, W = A.dx.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * W * CV;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int cv = idx % CV;
+        long long r = idx / CV;
+        int x = r % W; r /= W;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        T *dp = (T *)A.dx.p + voff(A.dx, b, y, x) + cv * 8;
+        float o[8], d[8], a[8];
+        ld8(dp, o);
+        ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
+        if (A.gate) ld8((const T *)A.act.p + voff(A.act, b, y, x) + cv * 8, a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            o[j] += d[j];
+            if (A.gate && !(a[j] > 0.f)) o[j] = 0.f;
+        }
+        st8(dp, o);
+    }
+}
+
+template <typename T>
+__global__ void k_add_fwd8(EltArgs A) {
+    const int CV = A.out.Cp / 8, W = A.out.W, rows = A.b - A.a;
+    long long n = (long long)A.B * rows * W * CV;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int cv = idx % CV;
+        long long r = idx / CV;
+        int x = r % W; r /= W;
+        int y = A.a + (int)(r % rows);
+        int b = (int)(r / rows);
+        float u[8], v[8];
+        ld8((const T *)A.x0.p + voff(A.x0, b, y, x) + cv * 8, u);
+        ld8((const T *)A.x1.p + voff(A.x1, b, y, x) + cv * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { u[j] += v[j]; if (A.relu) u[j] = fmaxf(u[j], 0.f); }
+        st8((T *)A.out.p + voff(A.out, b, y, x) + cv * 8, u);
+    }
+}
+
 // ------------------------------------------------------------------ launchers
 static const int kT = 256;
 static unsigned grid_for(long long n) {
@@ -527,15 +666,18 @@ cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st) {
 }
 cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     if (a.b <= a.a || a.epi == 0) return cudaSuccess;
-    const int CV = a.dy.Cp / 8;
-    if (CV < 1 || CV > 128 || a.dy.Cp % 8) return cudaErrorInvalidValue;
+    const int CVall = a.dy.Cp / 8;
+    if (CVall < 1 || a.dy.Cp % 8) return cudaErrorInvalidValue;
+    const int CV = CVall < 64 ? CVall : 64, groups = (CVall + CV - 1) / CV;
     dim3 blk(CV, CV >= 64 ? 4 : 256 / CV);
     long long npix = (long long)a.B * (a.b - a.a) * a.dy.W;
     long long g = (npix + blk.y * 16 - 1) / (blk.y * 16);        // ~16 pixels per thread
-    if (g > 148 * 8) g = 148 * 8;
+    long long cap = 148 * 8 / groups + 1;
+    if (g > cap) g = cap;
     if (g < 1) g = 1;
+    dim3 grid((unsigned)g, groups);
     size_t shm = 2 * sizeof(float) * blk.y * CV * 8;
-    if (prec) k_param_grad<bf16><<<(unsigned)g, blk, shm, st>>>(a); else k_param_grad<float><<<(unsigned)g, blk, shm, st>>>(a);
+    if (prec) k_param_grad<bf16><<<grid, blk, shm, st>>>(a); else k_param_grad<float><<<grid, blk, shm, st>>>(a);
     return cudaGetLastError();
 }
 static bool pool2(const PoolArgs &a, const View &v) { return a.k == 2 && a.s == 2 && a.p == 0 && v.Cp % 8 == 0; }
@@ -545,6 +687,9 @@ cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     if (pool2(a, a.out)) {
         n /= 8;
         if (prec) k_pool2_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool2_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    } else if (a.out.Cp % 8 == 0) {
+        n /= 8;
+        if (prec) k_pool_fwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd8<float><<<grid_for(n), kT, 0, st>>>(a);
     } else {
         if (prec) k_pool_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
     }
@@ -556,6 +701,9 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     if (pool2(a, a.dy)) {
         long long m = (long long)a.B * (a.b - a.a) * a.dy.W * (a.dy.Cp / 8);
         if (prec) k_pool2_bwd<bf16><<<grid_for(m), kT, 0, st>>>(a); else k_pool2_bwd<float><<<grid_for(m), kT, 0, st>>>(a);
+    } else if (a.dx.Cp % 8 == 0) {
+        n /= 8;
+        if (prec) k_pool_bwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd8<float><<<grid_for(n), kT, 0, st>>>(a);
     } else {
         if (prec) k_pool_bwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd<float><<<grid_for(n), kT, 0, st>>>(a);
     }
@@ -564,13 +712,19 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
 cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b - a.a) * a.out.W * a.out.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_add_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_add_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    if (a.out.Cp % 8 == 0) {
+        n /= 8;
+        if (prec) k_add_fwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_add_fwd8<float><<<grid_for(n), kT, 0, st>>>(a);
+    } else if (prec) k_add_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_add_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
     return cudaGetLastError();
 }
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b - a.a) * a.dx.W * a.dx.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_acc_gate<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate<float><<<grid_for(n), kT, 0, st>>>(a);
+    if (a.dx.Cp % 8 == 0) {
+        n /= 8;
+        if (prec) k_acc_gate8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate8<float><<<grid_for(n), kT, 0, st>>>(a);
+    } else if (prec) k_acc_gate<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate<float><<<grid_for(n), kT, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -86,8 +86,12 @@ struct Plan {
     ProfileSlot prof[3];
     std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t
     std::vector<double> pending_flops[3];
+    std::vector<int> pending_tags[3];             // op*8 + kind (profile dump)
+    std::vector<std::pair<int, ProfileSlot>> per_tag;
     // CUDA graph of one lrcnn_step, replayed while its arguments are unchanged
     void *graph_exec = nullptr;                  // cudaGraphExec_t
+    // side stream for wgrad / parameter reductions (overlap with the dgrad chain) and its events
+    void *side_stream = nullptr, *ev_fork = nullptr, *ev_join = nullptr;
     uintptr_t graph_key[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int graph_calls = 0;                         // consecutive calls with the same key
     long long graph_launches = 0, graph_tc_launches = 0;

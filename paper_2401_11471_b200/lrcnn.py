@@ -60,7 +60,7 @@ class MemoryReport(ctypes.Structure):
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
-           "lrcnn_profile_reset", "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
+           "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
 
 _lib = None
 
@@ -93,6 +93,7 @@ def lib():
     L.lrcnn_profile_read.argtypes = [vp, i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong),
                                      ctypes.POINTER(ctypes.c_double), vp]
     L.lrcnn_profile_reset.argtypes = [vp]
+    L.lrcnn_profile_dump.argtypes = [vp, ctypes.c_char_p, vp]
     L.lrcnn_last_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
     L.lrcnn_last_tc_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
     L.lrcnn_last_error.restype = ctypes.c_char_p
@@ -305,6 +306,9 @@ class Plan:
         _check(lib().lrcnn_profile_read(self.h, cls, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl),
                                         _stream(stream)))
         return ms.value, n.value, fl.value
+
+    def profile_dump(self, path, stream=None):
+        _check(lib().lrcnn_profile_dump(self.h, path.encode(), _stream(stream)))
 
     def last_launches(self):
         n = ctypes.c_longlong()
