@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
+    ap.add_argument("--parallel", default="dp", choices=["dp", "rows"],
+                    help="N>1: dp = each rank its own batch, wgrad all-reduce (weak scaling); rows = the "
+                         "same batch row-sharded across ranks with halo exchange (strong scaling, SURVEY 8(e))")
     return ap.parse_args()
 
 
@@ -206,21 +209,29 @@ def main():
     kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}
     if a.mode == "column":
         kw = {}
-    plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
+    rows = world > 1 and a.parallel == "rows"
+    if rows:
+        plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, world=world, rank=rank, **kw)
+        uid = [LB.Comm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = LB.Comm.nccl(uid[0], rank, world)
+        plan.set_comm(comm)
+    else:
+        plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
     mem = plan.memory()
 
     torch.cuda.reset_peak_memory_stats(dev)
     ds = LB.DeviceState(plan, device=dev)
     params = WL.make_params(net, seed=2)
-    x_np = WL.make_input(net, B, seed=1000 + rank)
-    lab_np = WL.make_labels(net, B, seed=1 + rank)
+    x_np = WL.make_input(net, B, seed=1000 + (0 if rows else rank))   # rows: every rank sees the same batch
+    lab_np = WL.make_labels(net, B, seed=1 + (0 if rows else rank))
     ds.load(params=params, x=x_np, labels=lab_np)
     xi_bytes = ds.x.numel() * ds.x.element_size()
     lab_bytes = ds.labels.numel() * 4
     lr = 1e-3
 
     def one_step():
-        if world > 1:
+        if world > 1 and not rows:
             plan.step_grads(ds.params, ds.grads, ds.x, ds.labels, ds.loss, ds.ws, stream)
             dist.all_reduce(ds.grads)          # wgrad all-reduce (NCCL, fp32, sum)
             ds.grads.mul_(1.0 / world)
@@ -265,7 +276,8 @@ def main():
         t = torch.tensor([ms_step], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t)
-    value = B * world / (ms_step / 1000.0)
+    gb = B if rows else B * world        # images per step of the whole job
+    value = gb / (ms_step / 1000.0)
 
     # ---------------------------------------------------------------- end-to-end through the public API
     x_host = ds.x.cpu().pin_memory()
@@ -325,7 +337,7 @@ def main():
                "plan": {k: mem[k] for k in ("omega", "band_act", "band_delta", "halo_cache", "carry",
                                             "checkpoints", "delta_full", "workspace")}}
     cpu = None
-    if not a.no_baselines and rank == 0 and a.mode != "column":
+    if not a.no_baselines and rank == 0 and a.mode != "column" and not rows:
         del ds, flush
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats(dev)
@@ -343,21 +355,26 @@ def main():
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-               "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+               "scaling": "strong" if rows else "weak",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[0,1) images, U{0..9} labels)",
                "config": {"workload": "%s, batch %d per GPU, bf16" % (CONFIGS[a.config][4], B),
-                          "global_batch": B * world, "seq_len": None,
-                          "parallelism": "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU",
+                          "global_batch": gb, "seq_len": None,
+                          "parallelism": ("rows%d (row sharding, NCCL halo exchange + all-reduce)" % world if rows
+                                          else "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU"),
                           "mode": a.mode, "segments": a.segments, "bands": kw,
                           "l2": "flushed (512 MB write) between timed steps"},
                "clocks": clocks,
-               "e2e": {"value": B * world / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": xi_bytes + lab_bytes,
+               "e2e": {"value": gb / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": xi_bytes + lab_bytes,
                        "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e},
                "gpu_launches": launches_per_step * a.steps,
                "host_enqueue_ms_per_step": 1000.0 * host_s / a.steps,
                "roofline": roofline, "memory": mem_rep, "cpu_baseline": cpu,
                "tensor_core_kernels": (not a.simt)}
         print(json.dumps(out), flush=True)
+    if rows:
+        plan.set_comm(None)
+        comm.free()
     if world > 1:
         dist.destroy_process_group()
 

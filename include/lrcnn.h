@@ -159,6 +159,34 @@ LRCNN_API lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int ba
 
 LRCNN_API lrcnn_status lrcnn_plan_memory(const lrcnn_plan_t *plan, lrcnn_memory_report *rep);
 
+/* Row sharding (opts.world > 1): this rank owns rows [*own_lo, *own_hi) of the
+ * segment output and computes tensor `tid` of the segment over [*lo, *hi) (the OverL backward
+ * image of the owned rows, so ranks overlap by the receptive-field halo). */
+LRCNN_API lrcnn_status lrcnn_plan_shard(const lrcnn_plan_t *plan, int seg, int tid, int *own_lo, int *own_hi,
+                                        int *lo, int *hi);
+/* Halo transfers of segment `seg`'s input tensor (empty for world == 1 and for the image):
+ * up to max entries (peer rank, send flag, rows [r0, r1)); *n receives the count.  In FP the
+ * send entries carry this rank's activation rows to the peer and the receive entries fill this
+ * rank's halo; in BP the same entries run reversed and the received delta rows are added. */
+LRCNN_API lrcnn_status lrcnn_plan_xfers(const lrcnn_plan_t *plan, int seg, int max, int *n, int *peer, int *send,
+                                        int *r0, int *r1);
+
+/* ---- communicators for row sharding (world > 1) --------------------------------------
+ * NCCL: rank 0 calls lrcnn_comm_nccl_unique_id (128 bytes), the caller broadcasts it (e.g. with
+ * torch.distributed), every rank calls lrcnn_comm_init_nccl.  libnccl.so.2 is opened at run time.
+ * Loopback: `world` ranks as host threads of one process on one GPU (tests): one group, one
+ * communicator per rank; graph capture is disabled for loopback ranks.
+ * A plan with world > 1 needs lrcnn_plan_set_comm before forward/backward/step (else
+ * LRCNN_E_STATE).  The communicator is owned by the caller and must outlive the plan's use. */
+typedef struct lrcnn_comm lrcnn_comm;
+LRCNN_API lrcnn_status lrcnn_comm_nccl_unique_id(void *id128);
+LRCNN_API lrcnn_status lrcnn_comm_init_nccl(const void *id128, int rank, int world, lrcnn_comm **out);
+LRCNN_API lrcnn_status lrcnn_comm_loopback_group(int world, void **group);
+LRCNN_API lrcnn_status lrcnn_comm_loopback_group_free(void *group);
+LRCNN_API lrcnn_status lrcnn_comm_init_loopback(void *group, int rank, lrcnn_comm **out);
+LRCNN_API lrcnn_status lrcnn_comm_free(lrcnn_comm *comm);
+LRCNN_API lrcnn_status lrcnn_plan_set_comm(lrcnn_plan_t *plan, lrcnn_comm *comm);
+
 /* FP (Alg. 1 l.5-11): computes z^L [B][H_L][W_L][Cp_L] (act_t) from x [B][H][W][Cp] (act_t)
  * and params (act_t, plan layout).  Leaves the 2PS halo cache and the checkpoints in ws for
  * a following lrcnn_backward_rows with the same params/x (two-phase sharing). */

@@ -151,6 +151,66 @@ def enumerate_overl(net, seg, E, shp=None):
     return res
 
 
+def rank_rows(h, world, g):
+    """Contiguous near-equal split of h rows over `world` ranks, earliest ranks one extra row."""
+    q, rem = divmod(h, world)
+    lo = g * q + min(g, rem)
+    return lo, lo + q + (1 if g < rem else 0)
+
+
+def enumerate_rank(net, seg, world, g, band_rows=None, n_bands=None, shp=None):
+    """Row sharding across ranks, enumerated with explicit row sets.
+
+    Rank g owns rows [ol, oh) of the segment output (rank_rows).  Every tensor t of the segment
+    is computed over the hull [LO, HI) of the rows transitively needed by the owned rows
+    (the last rank also computes the trailing rows nobody reads, as the single-rank 2PS does).
+    Inside the rank, 2PS bands over the owned rows: band r computes [e_{r-1}, e_r) with e_r the
+    hull end of the rows needed by [ol, E_r), e_0 = LO, e_N = HI.  Returns
+    ({t: (LO, HI)}, [{t: (lo, a, b)} per band], (ol, oh))."""
+    shp = shp or out_hw(net)
+    seg_in, ids, out = seg
+    ol, oh = rank_rows(shp[out][1], world, g)
+    need = need_sets(net, shp, seg, range(ol, oh))
+    ext = {}
+    for t in [seg_in] + [i + 1 for i in ids]:
+        nt = need.get(t, set())
+        ext[t] = (min(nt), max(nt) + 1) if nt else (0, 0)
+    for i in ids:
+        t = i + 1
+        if t != out and (world == 1 or g == world - 1):
+            ext[t] = (ext[t][0] if world > 1 else 0, shp[t][1])
+    E = [ol + e for e in band_ends(oh - ol, band_rows=band_rows, n_bands=n_bands if band_rows is None else None)]
+    tensors = [i + 1 for i in ids]
+    ends = []
+    for r in range(len(E)):
+        nd = need_sets(net, shp, seg, range(ol, E[r]))
+        e = {}
+        for t in tensors:
+            nt = nd.get(t, set())
+            e[t] = (max(nt) + 1) if nt else ext[t][0]
+            e[t] = max(e[t], ext[t][0])
+            if r == len(E) - 1:
+                e[t] = ext[t][1]
+        ends.append(e)
+    bands = []
+    for r in range(len(E)):
+        band = {}
+        for t in tensors:
+            a = ends[r - 1][t] if r > 0 else ext[t][0]
+            band[t] = [a, a, ends[r][t]]
+        for i in ids:
+            op = net["ops"][i]
+            _, a, b = band[i + 1]
+            for tin in set(_inputs(op)):
+                if tin == seg_in:
+                    continue
+                got = rf_of(op, tin, range(a, b), shp[tin][1])
+                if got:
+                    band[tin][0] = min(band[tin][0], min(got))
+        bands.append({t: tuple(v) for t, v in band.items()})
+    return ext, bands, (ol, oh)
+
+
 def forward_split(chain, h0, in_ends):
     """Input-specified ("skewed initial partitioning") mode for a chain of convs, PAPER.md:287,
     Fig. 4: given input band ends, each band computes every output row whose RF lies in the rows

@@ -16,8 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["plan.cpp", "kernels_simt.cu", "conv_tc.cu", "engine.cu"]
-HEADERS = ["plan.hpp", "kernels.hpp", "tc.hpp", "tc_ptx.cuh"]
+SOURCES = ["plan.cpp", "kernels_simt.cu", "conv_tc.cu", "comm.cu", "engine.cu"]
+HEADERS = ["plan.hpp", "kernels.hpp", "tc.hpp", "tc_ptx.cuh", "comm.hpp"]
 
 
 def _newer(src, dst):
@@ -41,7 +41,7 @@ def build(force=False, verbose=False):
             print(" ".join(cmd), flush=True)
             subprocess.check_call(cmd)
     if force or not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-cudart", "static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-cudart", "static", "-ldl"]
         print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
     return OUT

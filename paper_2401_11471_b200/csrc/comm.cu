@@ -1,0 +1,250 @@
+// comm.cu -- NCCL (run-time loaded) and in-process loopback backends of comm.hpp, and the
+// comm entry points of the C-ABI.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lrcnn.h"
+#include "comm.hpp"
+
+// NCCL declarations (types only; the library is opened with dlopen so liblrcnn.so has no
+// link-time dependency and shares the libnccl.so.2 PyTorch already loaded)
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclUint8 = 1, kNcclFloat32 = 7 };
+enum { kNcclSum = 0 };
+
+namespace lrcnn {
+void set_last_error(const std::string &m);
+
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi *nccl_api(std::string &err) {
+    static NcclApi api;
+    static bool tried = false;
+    static std::mutex m;
+    std::lock_guard<std::mutex> g(m);
+    if (!tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.h = h;
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+        }
+    }
+    if (!api.h || !api.CommInitRank || !api.Send || !api.AllReduce) {
+        err = "libnccl.so.2 not available";
+        return nullptr;
+    }
+    return &api;
+}
+
+// ------------------------------------------------------------------ loopback group
+struct LoopGroup {
+    int world;
+    std::mutex m;
+    std::condition_variable cv;
+    int count = 0;
+    long gen = 0;
+    std::vector<std::vector<XferBuf>> pub;
+    std::vector<cudaEvent_t> ready, done;
+    std::vector<float *> ar;
+    explicit LoopGroup(int w) : world(w), pub(w), ready(w), done(w), ar(w, nullptr) {
+        for (int i = 0; i < w; ++i) {
+            cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+        }
+    }
+    ~LoopGroup() {
+        for (int i = 0; i < world; ++i) { cudaEventDestroy(ready[i]); cudaEventDestroy(done[i]); }
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> l(m);
+        long g = gen;
+        if (++count == world) { count = 0; ++gen; cv.notify_all(); }
+        else cv.wait(l, [&] { return gen != g; });
+    }
+};
+
+struct Comm {
+    int kind;       // 0 = NCCL, 1 = loopback
+    int rank, world;
+    ncclComm_t nccl = nullptr;
+    LoopGroup *group = nullptr;
+};
+
+int comm_rank(const Comm *c) { return c->rank; }
+int comm_world(const Comm *c) { return c->world; }
+bool comm_graph_safe(const Comm *c) { return c->kind == 0; }
+
+__global__ void k_add_f32(float *dst, const float *src, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+
+int comm_exchange(Comm *c, const std::vector<XferBuf> &xs, cudaStream_t st, const char **err) {
+    static thread_local std::string e;
+    if (c->kind == 0) {
+        NcclApi *api = nccl_api(e);
+        if (!api) { *err = e.c_str(); return 1; }
+        api->GroupStart();
+        for (const XferBuf &x : xs) {
+            ncclResult_t r = x.send ? api->Send(x.ptr, x.bytes, kNcclUint8, x.peer, c->nccl, st)
+                                    : api->Recv(x.ptr, x.bytes, kNcclUint8, x.peer, c->nccl, st);
+            if (r) { api->GroupEnd(); e = "ncclSend/Recv failed"; *err = e.c_str(); return 1; }
+        }
+        if (api->GroupEnd()) { e = "ncclGroupEnd failed"; *err = e.c_str(); return 1; }
+        return 0;
+    }
+    LoopGroup &G = *c->group;
+    const int r = c->rank;
+    cudaEventRecord(G.ready[r], st);
+    G.pub[r] = xs;
+    G.barrier();
+    for (const XferBuf &x : xs) {
+        if (x.send) continue;
+        const XferBuf *src = nullptr;
+        for (const XferBuf &y : G.pub[x.peer])
+            if (y.send && y.peer == r) src = &y;
+        if (!src || src->bytes != x.bytes) { e = "loopback: unmatched transfer"; *err = e.c_str(); return 1; }
+        cudaStreamWaitEvent(st, G.ready[x.peer], 0);
+        cudaMemcpyAsync(x.ptr, src->ptr, x.bytes, cudaMemcpyDeviceToDevice, st);
+    }
+    cudaEventRecord(G.done[r], st);
+    G.barrier();
+    for (const XferBuf &x : xs)
+        if (x.send) cudaStreamWaitEvent(st, G.done[x.peer], 0);
+    G.barrier();
+    return cudaGetLastError() == cudaSuccess ? 0 : (e = "loopback copy failed", *err = e.c_str(), 1);
+}
+
+int comm_allreduce_f32(Comm *c, float *buf, size_t n, cudaStream_t st, const char **err) {
+    static thread_local std::string e;
+    if (c->world == 1 || n == 0) return 0;
+    if (c->kind == 0) {
+        NcclApi *api = nccl_api(e);
+        if (!api) { *err = e.c_str(); return 1; }
+        if (api->AllReduce(buf, buf, n, kNcclFloat32, kNcclSum, c->nccl, st)) {
+            e = "ncclAllReduce failed"; *err = e.c_str(); return 1;
+        }
+        return 0;
+    }
+    LoopGroup &G = *c->group;
+    const int r = c->rank;
+    cudaEventRecord(G.ready[r], st);
+    G.ar[r] = buf;
+    G.barrier();
+    if (r == 0) {
+        for (int p = 1; p < G.world; ++p) {
+            cudaStreamWaitEvent(st, G.ready[p], 0);
+            k_add_f32<<<592, 256, 0, st>>>(buf, G.ar[p], n);
+        }
+        cudaEventRecord(G.done[0], st);
+    }
+    G.barrier();
+    if (r != 0) {
+        cudaStreamWaitEvent(st, G.done[0], 0);
+        cudaMemcpyAsync(buf, G.ar[0], n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+        cudaEventRecord(G.done[r], st);
+    }
+    G.barrier();
+    if (r == 0)
+        for (int p = 1; p < G.world; ++p) cudaStreamWaitEvent(st, G.done[p], 0);
+    G.barrier();
+    return cudaGetLastError() == cudaSuccess ? 0 : (e = "loopback allreduce failed", *err = e.c_str(), 1);
+}
+
+}  // namespace lrcnn
+
+using namespace lrcnn;
+
+struct lrcnn_comm : Comm {};
+
+extern "C" {
+
+lrcnn_status lrcnn_comm_nccl_unique_id(void *id128) {
+    std::string e;
+    NcclApi *api = nccl_api(e);
+    if (!id128) { set_last_error("NULL id"); return LRCNN_E_ARG; }
+    if (!api || !api->GetUniqueId) { set_last_error(e); return LRCNN_E_NCCL; }
+    if (api->GetUniqueId((ncclUniqueId *)id128)) { set_last_error("ncclGetUniqueId failed"); return LRCNN_E_NCCL; }
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_comm_init_nccl(const void *id128, int rank, int world, lrcnn_comm **out) {
+    if (!id128 || !out || world < 1 || rank < 0 || rank >= world) { set_last_error("bad args"); return LRCNN_E_ARG; }
+    std::string e;
+    NcclApi *api = nccl_api(e);
+    if (!api) { set_last_error(e); return LRCNN_E_NCCL; }
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    lrcnn_comm *c = new lrcnn_comm();
+    c->kind = 0; c->rank = rank; c->world = world;
+    ncclResult_t r = api->CommInitRank(&c->nccl, world, id, rank);
+    if (r) {
+        set_last_error(std::string("ncclCommInitRank: ") + (api->GetErrorString ? api->GetErrorString(r) : "error"));
+        delete c;
+        return LRCNN_E_NCCL;
+    }
+    *out = c;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_comm_loopback_group(int world, void **group) {
+    if (!group || world < 1) { set_last_error("bad args"); return LRCNN_E_ARG; }
+    *group = new LoopGroup(world);
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_comm_loopback_group_free(void *group) {
+    delete (LoopGroup *)group;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_comm_init_loopback(void *group, int rank, lrcnn_comm **out) {
+    LoopGroup *G = (LoopGroup *)group;
+    if (!G || !out || rank < 0 || rank >= G->world) { set_last_error("bad args"); return LRCNN_E_ARG; }
+    lrcnn_comm *c = new lrcnn_comm();
+    c->kind = 1; c->rank = rank; c->world = G->world; c->group = G;
+    *out = c;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_comm_free(lrcnn_comm *c) {
+    if (c && c->kind == 0 && c->nccl) {
+        std::string e;
+        NcclApi *api = nccl_api(e);
+        if (api && api->CommDestroy) api->CommDestroy(c->nccl);
+    }
+    delete c;
+    return LRCNN_OK;
+}
+
+}  // extern "C"

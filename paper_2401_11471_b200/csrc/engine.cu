@@ -19,6 +19,7 @@
 
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "comm.hpp"
 #include "tc.hpp"
 
 struct lrcnn_plan_t {
@@ -66,12 +67,22 @@ static cudaError_t join_side(Run &R) {
     return e;
 }
 
+// a boundary map (image, checkpoint, z^L) on this rank: rows [ck_lo, ck_lo + ck_rows)
 static View full_view(void *p, const TensorInfo &t) {
     View v;
-    v.p = p; v.base = 0; v.rows = t.H; v.H = t.H; v.W = t.W; v.Cp = t.Cp;
-    v.bs = (long long)t.H * t.W * t.Cp;
+    v.p = p; v.base = t.ck_lo; v.rows = t.ck_rows; v.H = t.H; v.W = t.W; v.Cp = t.Cp;
+    v.bs = (long long)t.ck_rows * t.W * t.Cp;
     return v;
 }
+// the boundary delta buffer of a segment input/output: rows [dl_lo, dl_lo + dl_rows)
+static View dfull_view(void *p, const TensorInfo &t) {
+    View v;
+    v.p = p; v.base = t.dl_lo; v.rows = t.dl_rows; v.H = t.H; v.W = t.W; v.Cp = t.Cp;
+    v.bs = (long long)t.dl_rows * t.W * t.Cp;
+    return v;
+}
+
+void set_last_error(const std::string &m) { g_err = m; }
 
 static View band_view(char *base_ptr, const TensorInfo &t, int lo, int b) {
     View v;
@@ -105,8 +116,8 @@ static View act_view(Run &R, const Segment &S, int r, int t) {
 static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
     const TensorInfo &ti = R.P.t[t];
     int nseg = (int)R.P.seg.size();
-    if (t == S.out_t) return full_view(R.ws + R.P.dfull_off[s & 1], ti);
-    if (t == S.in_t) return full_view(t == 0 ? nullptr : R.ws + R.P.dfull_off[(s + 1) & 1], ti);
+    if (t == S.out_t) return dfull_view(R.ws + R.P.dfull_off[s & 1], ti);
+    if (t == S.in_t) return dfull_view(t == 0 ? nullptr : R.ws + R.P.dfull_off[(s + 1) & 1], ti);
     (void)nseg;
     return band_view(R.ws + ti.dlt_off, ti, S.lo[r][t], S.b[r][t]);
 }
@@ -222,11 +233,62 @@ static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cach
     return LRCNN_OK;
 }
 
+// ------------------------------------------------------------------ halo exchange between ranks
+// FP: before a segment runs, the rows of its input that neighbouring ranks own are received
+// into this rank's checkpoint (and this rank's rows they need are sent).  BP: after a segment's
+// backward, the delta this rank accumulated on the neighbours' rows is sent back and the
+// neighbours' delta on this rank's rows is added (the OverL overlap sum at rank cuts).
+static lrcnn_status pack_rows(Run &R, const View &v, int r0, int r1, void *dst, bool unpack) {
+    const size_t rb = (size_t)v.W * v.Cp * R.E;
+    char *p = (char *)v.p + (size_t)(r0 - v.base) * rb;
+    if (unpack)
+        CK(cudaMemcpy2DAsync(p, v.bs * R.E, dst, (r1 - r0) * rb, (r1 - r0) * rb, R.P.net.B, cudaMemcpyDeviceToDevice, R.st));
+    else
+        CK(cudaMemcpy2DAsync(dst, (r1 - r0) * rb, p, v.bs * R.E, (r1 - r0) * rb, R.P.net.B, cudaMemcpyDeviceToDevice, R.st));
+    return LRCNN_OK;
+}
+
+static lrcnn_status exchange(Run &R, const Segment &S, const View &v, bool bp) {
+    Plan &P = R.P;
+    const TensorInfo &ti = P.t[S.in_t];
+    const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+    char *sendb = R.ws + P.xstage_off[0], *recvb = R.ws + P.xstage_off[1];
+    const int rank = P.opts.rank;
+    std::vector<XferBuf> xs;
+    std::vector<std::pair<const Xfer *, char *>> incoming;
+    lrcnn_status st;
+    for (const Xfer &x : S.in_xfers) {
+        const int slot = x.peer < rank ? 0 : 1;
+        const size_t bytes = (size_t)P.net.B * (x.r1 - x.r0) * rb;
+        const bool out = bp ? !x.send : x.send;          // BP runs the FP schedule reversed
+        if (out) {
+            char *buf = sendb + slot * P.xstage_bytes;
+            if ((st = pack_rows(R, v, x.r0, x.r1, buf, false)) != LRCNN_OK) return st;
+            xs.push_back({x.peer, 1, buf, bytes});
+        } else {
+            char *buf = recvb + slot * P.xstage_bytes;
+            xs.push_back({x.peer, 0, buf, bytes});
+            incoming.push_back({&x, buf});
+        }
+    }
+    const char *err = nullptr;
+    if (comm_exchange((Comm *)P.comm, xs, R.st, &err)) return fail(LRCNN_E_NCCL, err ? err : "exchange failed");
+    for (auto &in : incoming) {
+        if (bp) CK(add_rows(R.prec, v, in.first->r0, in.first->r1, in.second, P.net.B, R.st));
+        else if ((st = pack_rows(R, v, in.first->r0, in.first->r1, in.second, true)) != LRCNN_OK) return st;
+    }
+    return LRCNN_OK;
+}
+
 static lrcnn_status run_forward(Run &R) {
     lrcnn_status st;
-    for (const Segment &S : R.P.seg)
+    const bool sharded = R.P.opts.world > 1;
+    for (const Segment &S : R.P.seg) {
+        if (sharded && S.in_t != 0 && !S.in_xfers.empty())
+            if ((st = exchange(R, S, full_view(ckpt_ptr(R, S.in_t), R.P.t[S.in_t]), false)) != LRCNN_OK) return st;
         for (int r = 0; r < (int)S.E.size(); ++r)
             if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) return st;
+    }
     return LRCNN_OK;
 }
 
@@ -350,7 +412,8 @@ static lrcnn_status run_backward(Run &R) {
         const Segment &S = P.seg[s];
         if (S.in_t != 0) {
             const TensorInfo &ti = P.t[S.in_t];
-            CK(cudaMemsetAsync(R.ws + P.dfull_off[(s + 1) & 1], 0, (size_t)P.net.B * ti.H * ti.W * ti.Cp * R.E, R.st));
+            CK(cudaMemsetAsync(R.ws + P.dfull_off[(s + 1) & 1], 0, (size_t)P.net.B * ti.dl_rows * ti.W * ti.Cp * R.E,
+                               R.st));
         }
         const int N = (int)S.E.size();
         for (int r = N - 1; r >= 0; --r) {
@@ -384,6 +447,9 @@ static lrcnn_status run_backward(Run &R) {
                 }
             }
         }
+        if (P.opts.world > 1 && S.in_t != 0 && !S.in_xfers.empty())
+            if ((st = exchange(R, S, dfull_view(R.ws + P.dfull_off[(s + 1) & 1], P.t[S.in_t]), true)) != LRCNN_OK)
+                return st;
     }
     return LRCNN_OK;
 }
@@ -500,6 +566,32 @@ lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int band, int ti
     return LRCNN_OK;
 }
 
+lrcnn_status lrcnn_plan_shard(const lrcnn_plan_t *plan, int seg, int tid, int *own_lo, int *own_hi, int *lo,
+                              int *hi) {
+    if (!plan || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad segment");
+    const Segment &S = plan->P.seg[seg];
+    if (tid < 0 || tid > plan->P.net.n_ops) return fail(LRCNN_E_ARG, "bad tensor");
+    if (own_lo) *own_lo = S.own_lo;
+    if (own_hi) *own_hi = S.own_hi;
+    if (lo) *lo = S.LO[tid];
+    if (hi) *hi = S.HI[tid];
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_xfers(const lrcnn_plan_t *plan, int seg, int max, int *n, int *peer, int *send, int *r0,
+                              int *r1) {
+    if (!plan || !n || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad args");
+    const Segment &S = plan->P.seg[seg];
+    *n = (int)S.in_xfers.size();
+    for (int i = 0; i < *n && i < max; ++i) {
+        if (peer) peer[i] = S.in_xfers[i].peer;
+        if (send) send[i] = S.in_xfers[i].send;
+        if (r0) r0[i] = S.in_xfers[i].r0;
+        if (r1) r1[i] = S.in_xfers[i].r1;
+    }
+    return LRCNN_OK;
+}
+
 lrcnn_status lrcnn_plan_memory(const lrcnn_plan_t *plan, lrcnn_memory_report *rep) {
     if (!plan || !rep) return fail(LRCNN_E_ARG, "bad args");
     *rep = plan->P.mem;
@@ -515,6 +607,7 @@ lrcnn_status lrcnn_forward_rows(lrcnn_plan_t *plan, const void *params, const vo
     P.launches = 0; P.tc_launches = 0;
     Run R{P, (char *)ws, (const char *)params, x, zl, nullptr, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     P.fwd_done = false;
+    if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     st = run_forward(R);
     if (st != LRCNN_OK) return st;
     P.fwd_done = true; P.fwd_params = params; P.fwd_x = x; P.fwd_ws = ws;
@@ -535,10 +628,16 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
     const TensorInfo &z = P.t[L];
     // delta^L, gated by the last op's ReLU (gate on write), into the last segment's delta buffer
     int slast = (int)P.seg.size() - 1;
-    CK(gate_copy(P.opts.prec, dzl, zl, R.ws + P.dfull_off[slast & 1], (long long)P.net.B * z.H * z.W * z.Cp, z.relu,
-                 R.st));
+    CK(gate_copy(P.opts.prec, dzl, zl, R.ws + P.dfull_off[slast & 1], (long long)P.net.B * z.ck_rows * z.W * z.Cp,
+                 z.relu, R.st));
     ++P.launches;
+    if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     st = run_backward(R);
+    if (st == LRCNN_OK && P.opts.world > 1) {
+        const char *err = nullptr;
+        if (comm_allreduce_f32((Comm *)P.comm, grads, P.head_w_off, R.st, &err))
+            return fail(LRCNN_E_NCCL, err ? err : "allreduce failed");
+    }
     P.fwd_done = false;
     return st;
 }
@@ -552,18 +651,40 @@ lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *gra
     P.launches = 0; P.tc_launches = 0;
     char *w = (char *)ws;
     Run R{P, w, (const char *)params, x, w + P.zl_off, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     if ((st = run_forward(R)) != LRCNN_OK) return st;
     const int L = P.net.n_ops;
     const TensorInfo &z = P.t[L];
     int slast = (int)P.seg.size() - 1;
-    CK(head_forward_backward(P.opts.prec, R.zl, P.net.B, z.H * z.W, z.Cp, z.C, P.net.n_classes,
-                             R.params + P.head_w_off * R.E, R.params + P.head_b_off * R.E, labels,
-                             (float *)(w + P.head_off), loss_dev, grads + P.head_w_off, grads + P.head_b_off,
-                             w + P.dfull_off[slast & 1], z.relu, R.st));
+    // head on the pooled z^L: each rank pools its own rows, the partial sums are all-reduced
+    const float hw = (float)z.H * z.W;
+    float *scratch = (float *)(w + P.head_off);
+    CK(head_gap(P.opts.prec, R.zl, P.net.B, z.ck_rows * z.W, z.Cp, hw, scratch, R.st));
+    if (P.opts.world > 1) {
+        const char *err = nullptr;
+        if (comm_allreduce_f32((Comm *)P.comm, scratch, (size_t)P.net.B * z.Cp, R.st, &err))
+            return fail(LRCNN_E_NCCL, err ? err : "allreduce failed");
+    }
+    CK(head_tail(P.opts.prec, R.zl, P.net.B, z.ck_rows * z.W, z.Cp, z.C, P.net.n_classes,
+                 R.params + P.head_w_off * R.E, R.params + P.head_b_off * R.E, labels, scratch, loss_dev,
+                 grads + P.head_w_off, grads + P.head_b_off, w + P.dfull_off[slast & 1], z.relu, hw, R.st));
     P.launches += 3;
     st = run_backward(R);
+    if (st == LRCNN_OK && P.opts.world > 1) {   // wgrad all-reduce (the conv parameters precede the head)
+        const char *err = nullptr;
+        if (comm_allreduce_f32((Comm *)P.comm, grads, P.head_w_off, R.st, &err))
+            return fail(LRCNN_E_NCCL, err ? err : "allreduce failed");
+    }
     P.fwd_done = false;
     return st;
+}
+
+lrcnn_status lrcnn_plan_set_comm(lrcnn_plan_t *plan, lrcnn_comm *comm) {
+    if (!plan) return fail(LRCNN_E_ARG, "plan is NULL");
+    if (comm && (comm_world((Comm *)comm) != plan->P.opts.world || comm_rank((Comm *)comm) != plan->P.opts.rank))
+        return fail(LRCNN_E_ARG, "communicator rank/world differ from the plan's");
+    plan->P.comm = comm;
+    return LRCNN_OK;
 }
 
 lrcnn_status lrcnn_sgd(lrcnn_plan_t *plan, float *master, void *params, float *grads, float lr, void *stream) {
@@ -595,7 +716,7 @@ lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *
     std::memcpy(&lr_bits, &lr_copy, 4);
     const uintptr_t key[9] = {(uintptr_t)master, (uintptr_t)params, (uintptr_t)grads, (uintptr_t)x,
                               (uintptr_t)labels, (uintptr_t)loss_dev, (uintptr_t)ws, (uintptr_t)stream, lr_bits};
-    if (!graphs || stream == nullptr || P.profiling) {
+    if (!graphs || stream == nullptr || P.profiling || (P.comm && !comm_graph_safe((Comm *)P.comm))) {
         P.graph_calls = 0;
         return step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
     }

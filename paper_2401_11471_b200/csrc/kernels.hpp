@@ -83,6 +83,11 @@ cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int C
                                   const void *fc_w, const void *fc_b, const int32_t *labels, float *scratch,
                                   float *loss, float *g_fc_w, float *g_fc_b, void *dzl, int gate,
                                   cudaStream_t st);
+cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st);
+cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, int classes, const void *fc_w,
+                      const void *fc_b, const int32_t *labels, float *scratch, float *loss, float *g_fc_w,
+                      float *g_fc_b, void *dzl, int gate, float hw_div, cudaStream_t st);
+cudaError_t add_rows(int prec, const View &dst, int r0, int r1, const void *src, int B, cudaStream_t st);
 cudaError_t gate_copy(int prec, const void *src, const void *act, void *dst, long long n, int gate,
                       cudaStream_t st);
 cudaError_t sgd_update(int prec, float *master, void *params, float *grads, long long n, float lr,

@@ -393,13 +393,13 @@ __global__ void k_acc_gate(EltArgs A) {
 
 // ------------------------------------------------------------------ head
 template <typename T>
-__global__ void k_gap(const T *zl, int HW, int Cp, float *gap) {
+__global__ void k_gap(const T *zl, int HW, int Cp, float *gap, float hw_div) {
     int b = blockIdx.x, c = blockIdx.y * blockDim.x + threadIdx.x;
     if (c >= Cp) return;
     const T *z = zl + (long long)b * HW * Cp + c;
     float s = 0.f;
     for (int i = 0; i < HW; ++i) s += ldf(z + (long long)i * Cp);
-    gap[(long long)b * Cp + c] = s / HW;
+    gap[(long long)b * Cp + c] = s / hw_div;
 }
 
 template <typename T>
@@ -443,7 +443,7 @@ __global__ void k_fc_ce(const float *gap, int B, int Cp, int C, int classes, con
 
 template <typename T>
 __global__ void k_dzl(const T *zl, const float *dlog, const T *fw, int B, int HW, int Cp, int C, int classes,
-                      T *dzl, int gate) {
+                      T *dzl, int gate, float hw_div) {
     long long n = (long long)B * HW * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -452,7 +452,7 @@ __global__ void k_dzl(const T *zl, const float *dlog, const T *fw, int B, int HW
         float v = 0.f;
         if (c < C) {
             for (int j = 0; j < classes; ++j) v += dlog[b * classes + j] * ldf(fw + (long long)j * Cp + c);
-            v /= HW;
+            v /= hw_div;
         }
         if (gate && ldf(zl + idx) <= 0.f) v = 0.f;
         stf(dzl + idx, v);
@@ -728,27 +728,69 @@ cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// GAP over the z^L rows this rank holds (HW pixels per image), divided by the global H_L*W_L
+cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st) {
+    dim3 g1(B, (Cp + 127) / 128);
+    if (prec) k_gap<bf16><<<g1, 128, 0, st>>>((const bf16 *)zl, HW, Cp, scratch, hw_div);
+    else k_gap<float><<<g1, 128, 0, st>>>((const float *)zl, HW, Cp, scratch, hw_div);
+    return cudaGetLastError();
+}
+
+// FC -> softmax-CE -> d logits -> FC grads -> delta^L (gated by the last op's ReLU) on this rank's rows
+cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, int classes, const void *fc_w,
+                      const void *fc_b, const int32_t *labels, float *scratch, float *loss, float *g_fc_w,
+                      float *g_fc_b, void *dzl, int gate, float hw_div, cudaStream_t st) {
+    float *gap = scratch, *dlog = scratch + (long long)B * Cp;
+    size_t shm = sizeof(float) * B * classes;
+    long long n = (long long)B * HW * Cp;
+    if (prec) {
+        k_fc_ce<bf16><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
+                                            dlog, loss, g_fc_w, g_fc_b);
+        if (n > 0)
+            k_dzl<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
+                                                   (bf16 *)dzl, gate, hw_div);
+    } else {
+        k_fc_ce<float><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const float *)fc_w, (const float *)fc_b,
+                                             labels, dlog, loss, g_fc_w, g_fc_b);
+        if (n > 0)
+            k_dzl<float><<<grid_for(n), kT, 0, st>>>((const float *)zl, dlog, (const float *)fc_w, B, HW, Cp, C,
+                                                    classes, (float *)dzl, gate, hw_div);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int Cp, int C, int classes,
                                   const void *fc_w, const void *fc_b, const int32_t *labels, float *scratch,
                                   float *loss, float *g_fc_w, float *g_fc_b, void *dzl, int gate,
                                   cudaStream_t st) {
-    float *gap = scratch, *dlog = scratch + (long long)B * Cp;
-    dim3 g1(B, (Cp + 127) / 128);
-    size_t shm = sizeof(float) * B * classes;
-    long long n = (long long)B * HW * Cp;
-    if (prec) {
-        k_gap<bf16><<<g1, 128, 0, st>>>((const bf16 *)zl, HW, Cp, gap);
-        k_fc_ce<bf16><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
-                                            dlog, loss, g_fc_w, g_fc_b);
-        k_dzl<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
-                                               (bf16 *)dzl, gate);
-    } else {
-        k_gap<float><<<g1, 128, 0, st>>>((const float *)zl, HW, Cp, gap);
-        k_fc_ce<float><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const float *)fc_w, (const float *)fc_b, labels,
-                                             dlog, loss, g_fc_w, g_fc_b);
-        k_dzl<float><<<grid_for(n), kT, 0, st>>>((const float *)zl, dlog, (const float *)fc_w, B, HW, Cp, C, classes,
-                                                (float *)dzl, gate);
+    cudaError_t e = head_gap(prec, zl, B, HW, Cp, (float)HW, scratch, st);
+    if (e != cudaSuccess) return e;
+    return head_tail(prec, zl, B, HW, Cp, C, classes, fc_w, fc_b, labels, scratch, loss, g_fc_w, g_fc_b, dzl, gate,
+                     (float)HW, st);
+}
+
+// dst rows [r0, r1) += src (contiguous [B][r1-r0][W][Cp]): received halo delta of a neighbour rank
+template <typename T>
+__global__ void k_add_rows(View dst, int r0, int r1, const T *src, int B) {
+    const int rows = r1 - r0, W = dst.W, Cp = dst.Cp;
+    long long n = (long long)B * rows * W * Cp;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int c = idx % Cp;
+        long long r = idx / Cp;
+        int x = r % W; r /= W;
+        int g = r0 + (int)(r % rows);
+        int b = (int)(r / rows);
+        T *d = (T *)dst.p + voff(dst, b, g, x) + c;
+        stf(d, ldf(d) + ldf(src + idx));
     }
+}
+
+cudaError_t add_rows(int prec, const View &dst, int r0, int r1, const void *src, int B, cudaStream_t st) {
+    long long n = (long long)B * (r1 - r0) * dst.W * dst.Cp;
+    if (n <= 0) return cudaSuccess;
+    if (prec) k_add_rows<bf16><<<grid_for(n), kT, 0, st>>>(dst, r0, r1, (const bf16 *)src, B);
+    else k_add_rows<float><<<grid_for(n), kT, 0, st>>>(dst, r0, r1, (const float *)src, B);
     return cudaGetLastError();
 }
 

@@ -53,7 +53,6 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     }
     if (opts->mode < LRCNN_COLUMN || opts->mode > LRCNN_OVERL) { err = "bad mode"; return LRCNN_E_ARG; }
     if (opts->prec != LRCNN_FP32 && opts->prec != LRCNN_BF16) { err = "bad precision"; return LRCNN_E_ARG; }
-    if (opts->world > 1) { err = "row sharding across GPUs (world > 1) is not in this build"; return LRCNN_E_UNSUPPORTED; }
     if (opts->mode != LRCNN_COLUMN && opts->band_rows <= 0 && opts->n_bands <= 0) {
         err = "band_rows or n_bands must be > 0"; return LRCNN_E_ARG;
     }
@@ -143,11 +142,90 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         }
     }
 
+    // ---------------------------------------------------------------- rank shards
+    // Row sharding across `world` ranks (SURVEY 8(e) "per-stage segments, OverL at rank cuts,
+    // 2PS bands inside each rank"): each segment output is split into near-equal contiguous row
+    // ranges (earliest ranks +1); a rank computes every tensor of the segment over the backward
+    // image [LO, HI) of its owned output rows (the OverL extended range, R4), so its only
+    // dependency on other ranks is the halo of the segment input, exchanged once per segment.
+    const int world = std::max(1, opts->world), rank = opts->rank;
+    if (rank < 0 || rank >= world) { err = "rank out of range"; return LRCNN_E_ARG; }
+    auto split = [&](int h, int g, int &lo, int &hi) {
+        int q = h / world, rem = h % world;
+        lo = g * q + std::min(g, rem);
+        hi = lo + q + (g < rem ? 1 : 0);
+    };
+    // extended ranges of every tensor of segment S for owned output rows [ol, oh)
+    auto ext = [&](const Segment &S, int ol, int oh, std::vector<int> &LO, std::vector<int> &HI) {
+        LO.assign(T, 0); HI.assign(T, 0);
+        std::vector<char> inside(T, 0);
+        for (int i : S.ops) inside[i + 1] = 1;
+        LO[S.out_t] = ol; HI[S.out_t] = oh;
+        std::vector<int> order(S.tensors.rbegin(), S.tensors.rend());
+        order.push_back(S.in_t);
+        for (int t : order) {
+            if (t == S.out_t) continue;
+            int lo = INT_MAX, hi = 0;
+            for (auto &c : P.t[t].cons) {
+                if (!inside[c.op + 1]) continue;
+                const OpInfo &o = P.op[c.op];
+                int lu = LO[c.op + 1], hu = HI[c.op + 1];
+                if (hu <= lu) continue;
+                int l, h;
+                if (window_role(o, c.role)) {
+                    l = std::max(0, lu * o.d.s - o.d.p);
+                    h = std::min(P.t[t].H, (hu - 1) * o.d.s - o.d.p + o.d.k);
+                } else { l = lu; h = hu; }
+                lo = std::min(lo, l); hi = std::max(hi, h);
+            }
+            if (hi <= 0 || lo == INT_MAX) { lo = 0; hi = 0; }
+            LO[t] = lo; HI[t] = hi;
+        }
+    };
+    for (size_t si = 0; si < P.seg.size(); ++si) {
+        Segment &S = P.seg[si];
+        if (P.t[S.out_t].H < world) { err = "fewer segment-output rows than ranks"; return LRCNN_E_INFEASIBLE; }
+        split(P.t[S.out_t].H, rank, S.own_lo, S.own_hi);
+        split(P.t[S.in_t].H, rank, S.in_own_lo, S.in_own_hi);
+        if (si > 0) { S.in_own_lo = P.seg[si - 1].own_lo; S.in_own_hi = P.seg[si - 1].own_hi; }
+        ext(S, S.own_lo, S.own_hi, S.LO, S.HI);
+        if (world > 1 && rank == world - 1)
+            for (int t : S.tensors) if (t != S.out_t) S.HI[t] = P.t[t].H;   // last rank: all trailing rows
+        if (world == 1)
+            for (int t : S.tensors) if (t != S.out_t) { S.LO[t] = 0; S.HI[t] = P.t[t].H; }
+        if (world > 1 && S.in_t != 0) {
+            // halo of the segment input from the neighbours; must come from adjacent ranks only
+            for (int d = -1; d <= 1; d += 2) {
+                const int g = rank + d;
+                if (g < 0 || g >= world) continue;
+                int gol, goh;
+                split(P.t[S.out_t].H, g, gol, goh);
+                std::vector<int> LOg, HIg;
+                ext(S, gol, goh, LOg, HIg);
+                int pl, ph;   // rows of the input tensor rank g owns (its previous-segment output split)
+                split(P.t[S.in_t].H, g, pl, ph);
+                // FP: what I need from g / what g needs from me
+                if (d < 0) {
+                    if (S.LO[S.in_t] < S.in_own_lo) S.in_xfers.push_back({g, 0, S.LO[S.in_t], S.in_own_lo});
+                    if (HIg[S.in_t] > S.in_own_lo) S.in_xfers.push_back({g, 1, S.in_own_lo, HIg[S.in_t]});
+                    if (S.LO[S.in_t] < pl) { err = "halo wider than a neighbour's shard"; return LRCNN_E_INFEASIBLE; }
+                } else {
+                    if (S.HI[S.in_t] > S.in_own_hi) S.in_xfers.push_back({g, 0, S.in_own_hi, S.HI[S.in_t]});
+                    if (LOg[S.in_t] < S.in_own_hi) S.in_xfers.push_back({g, 1, LOg[S.in_t], S.in_own_hi});
+                    if (S.HI[S.in_t] > ph) { err = "halo wider than a neighbour's shard"; return LRCNN_E_INFEASIBLE; }
+                }
+            }
+        }
+    }
+
     // ---------------------------------------------------------------- bands
     for (Segment &S : P.seg) {
-        const int h_out = P.t[S.out_t].H;
-        if (opts->mode == LRCNN_COLUMN) S.E = {h_out};
-        else S.E = make_band_ends(h_out, opts->band_rows, opts->n_bands);
+        const int own = S.own_hi - S.own_lo;
+        if (opts->mode == LRCNN_COLUMN) S.E = {S.own_hi};
+        else {
+            S.E = make_band_ends(own, opts->band_rows, opts->n_bands);
+            for (int &e : S.E) e += S.own_lo;
+        }
         for (size_t r = 1; r < S.E.size(); ++r)
             if (S.E[r] <= S.E[r - 1]) { err = "band ends not strictly increasing"; return LRCNN_E_DEGENERATE; }
         const int N = (int)S.E.size();
@@ -157,7 +235,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         for (int i : S.ops) inside[i + 1] = 1;
         if (opts->mode == LRCNN_OVERL) {
             for (int r = 0; r < N; ++r) {
-                int e0 = r ? S.E[r - 1] : 0;
+                int e0 = r ? S.E[r - 1] : S.own_lo;
                 S.lo[r][S.out_t] = S.a[r][S.out_t] = e0; S.b[r][S.out_t] = S.E[r];
                 // internal tensors and the segment input, reverse production order
                 std::vector<int> order(S.tensors.rbegin(), S.tensors.rend());
@@ -193,20 +271,20 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
                 for (auto it = S.tensors.rbegin(); it != S.tensors.rend(); ++it) {
                     int t = *it;
                     if (t == S.out_t) continue;
-                    int e = 0;
-                    if (r == N - 1) e = P.t[t].H;
+                    int e = S.LO[t];
+                    if (r == N - 1) e = S.HI[t];
                     else {
                         for (auto &c : P.t[t].cons) {
                             const OpInfo &o = P.op[c.op];
                             int eu = S.b[r][c.op + 1];
-                            if (eu <= 0) continue;
+                            if (eu <= S.LO[c.op + 1]) continue;   // consumer computed nothing yet
                             int need = window_role(o, c.role) ? (eu - 1) * o.d.s - o.d.p + o.d.k : eu;
-                            e = std::max(e, std::min(P.t[t].H, need));
+                            e = std::max(e, std::min(S.HI[t], need));
                         }
                     }
                     S.b[r][t] = e;
                 }
-                for (int t : S.tensors) S.a[r][t] = r ? S.b[r - 1][t] : 0;
+                for (int t : S.tensors) S.a[r][t] = r ? S.b[r - 1][t] : S.LO[t];
                 for (int t : S.tensors) {
                     int lo = S.a[r][t];
                     if (t != S.out_t) {
@@ -253,11 +331,25 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     lrcnn_memory_report &M = P.mem;
     std::memset(&M, 0, sizeof(M));
     for (int t = 1; t < T; ++t) M.omega += B * P.t[t].H * P.t[t].W * P.t[t].C * E;
+    // rows every full-width (boundary) map holds on this rank: image = all rows (caller's x);
+    // a checkpoint = its owned rows plus the next segment's halo; z^L = owned rows
+    P.t[0].ck_lo = 0; P.t[0].ck_rows = P.t[0].H;
+    for (size_t si = 0; si < P.seg.size(); ++si) {
+        const Segment &S = P.seg[si];
+        TensorInfo &to = P.t[S.out_t];
+        int lo = S.own_lo, hi = S.own_hi;
+        if (si + 1 < P.seg.size()) {
+            lo = std::min(lo, P.seg[si + 1].LO[S.out_t]);
+            hi = std::max(hi, P.seg[si + 1].HI[S.out_t]);
+        }
+        to.ck_lo = lo; to.ck_rows = hi - lo;
+        to.dl_lo = lo; to.dl_rows = hi - lo;
+    }
     // persistent: checkpoints, 2PS caches, delta ping-pong, head scratch, transposed weights
     for (const Segment &S : P.seg) {
         if (!P.t[S.out_t].is_zl) {
-            P.t[S.out_t].ckpt_off = alloc(B * P.t[S.out_t].H * rowbytes(S.out_t));
-            M.checkpoints += B * P.t[S.out_t].H * rowbytes(S.out_t);
+            P.t[S.out_t].ckpt_off = alloc(B * P.t[S.out_t].ck_rows * rowbytes(S.out_t));
+            M.checkpoints += B * P.t[S.out_t].ck_rows * rowbytes(S.out_t);
         }
         const int N = (int)S.E.size();
         for (int t : S.tensors) {
@@ -278,14 +370,23 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             }
         }
     }
-    size_t dmax = 0;
-    for (const Segment &S : P.seg) dmax = std::max(dmax, B * P.t[S.out_t].H * rowbytes(S.out_t));
+    size_t dmax = 0, xmax = 0;
+    for (const Segment &S : P.seg) {
+        dmax = std::max(dmax, B * P.t[S.out_t].dl_rows * rowbytes(S.out_t));
+        for (const Xfer &x : S.in_xfers) xmax = std::max(xmax, B * (size_t)(x.r1 - x.r0) * rowbytes(S.in_t));
+    }
     P.dfull_bytes = dmax;
     P.dfull_off[0] = alloc(dmax);
     P.dfull_off[1] = P.seg.size() > 1 ? alloc(dmax) : P.dfull_off[0];
     M.delta_full = dmax * (P.seg.size() > 1 ? 2 : 1);
-    P.zl_off = alloc(B * zl.H * rowbytes(n_ops));
-    M.checkpoints += B * zl.H * rowbytes(n_ops);
+    P.zl_off = alloc(B * zl.ck_rows * rowbytes(n_ops));
+    M.checkpoints += B * zl.ck_rows * rowbytes(n_ops);
+    if (xmax) {   // two send and two receive staging slots (one per neighbour)
+        P.xstage_bytes = xmax;
+        P.xstage_off[0] = alloc(4 * xmax);
+        P.xstage_off[1] = P.xstage_off[0] + 2 * xmax;
+        M.other += 4 * xmax;
+    }
     P.head_off = alloc(sizeof(float) * (B * zl.Cp + B * net->n_classes + 64));
     P.flag_off = alloc(256);
     M.other += ws - (P.head_off);

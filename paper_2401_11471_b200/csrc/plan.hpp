@@ -35,6 +35,8 @@ struct TensorInfo {
     std::vector<int> cache_lo, cache_rows;   // per band boundary r (0..N-2): rows [lo_{r+1}, b_r)
     std::vector<size_t> cache_off;
     size_t ckpt_off = 0;      // checkpoint (seg_out && !is_zl)
+    int ck_lo = 0, ck_rows = 0;   // rows a full-width map (image, checkpoint, z^L) holds on this rank
+    int dl_lo = 0, dl_rows = 0;   // rows of the boundary delta buffer (segment in/out) on this rank
     size_t wt_off = 0;        // unused for tensors
 };
 
@@ -45,10 +47,23 @@ struct OpInfo {
     size_t wt_off = 0;        // transposed (dgrad) weights in workspace (bf16 tensor-core path)
 };
 
+// One halo transfer of a boundary tensor between this rank and a neighbour (rows [r0, r1)).
+struct Xfer {
+    int peer;      // rank
+    int send;      // 1 = send (FP: my rows to the neighbour; BP: the neighbour's delta rows I hold)
+    int r0, r1;
+};
+
 struct Segment {
     int in_t = 0, out_t = 0;
     std::vector<int> ops;                    // topological order
     std::vector<int> tensors;                // internal tensors + out (ids), production order
+    // row sharding across ranks (world > 1): this rank owns output rows [own_lo, own_hi) and
+    // computes every tensor t over its extended range [LO[t], HI[t]) (OverL at rank cuts);
+    // in_own_lo/hi = rows of the segment input this rank owns (previous segment's split)
+    int own_lo = 0, own_hi = 0, in_own_lo = 0, in_own_hi = 0;
+    std::vector<int> LO, HI;
+    std::vector<Xfer> in_xfers;              // FP halo of the segment input (BP: reversed, added)
     std::vector<int> E;                      // band ends at the segment output
     // per band r, per global tensor id: lo (buffer start), a (first computed), b (end)
     std::vector<std::vector<int>> lo, a, b;
@@ -72,6 +87,8 @@ struct Plan {
     size_t head_w_off = 0, head_w_cnt = 0, head_b_off = 0, head_b_cnt = 0;
     size_t ws_bytes = 0;
     size_t dfull_off[2] = {0, 0}, dfull_bytes = 0;
+    size_t xstage_off[2] = {0, 0}, xstage_bytes = 0;   // halo exchange staging (send, recv)
+    void *comm = nullptr;                    // lrcnn_comm* (world > 1)
     size_t head_off = 0;                     // head scratch (fp32)
     size_t zl_off = 0;                       // z^L buffer used by lrcnn_step
     size_t flag_off = 0;                     // small device scratch

@@ -60,7 +60,10 @@ class MemoryReport(ctypes.Structure):
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
-           "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
+           "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_plan_shard", "lrcnn_plan_xfers",
+           "lrcnn_comm_nccl_unique_id", "lrcnn_comm_init_nccl", "lrcnn_comm_loopback_group",
+           "lrcnn_comm_loopback_group_free", "lrcnn_comm_init_loopback", "lrcnn_comm_free", "lrcnn_plan_set_comm",
+           "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
 
 _lib = None
 
@@ -95,6 +98,15 @@ def lib():
     L.lrcnn_profile_reset.argtypes = [vp]
     L.lrcnn_profile_dump.argtypes = [vp, ctypes.c_char_p, vp]
     L.lrcnn_last_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+    L.lrcnn_plan_shard.argtypes = [vp, i, i, ip, ip, ip, ip]
+    L.lrcnn_plan_xfers.argtypes = [vp, i, i, ip, ip, ip, ip, ip]
+    L.lrcnn_comm_nccl_unique_id.argtypes = [vp]
+    L.lrcnn_comm_init_nccl.argtypes = [vp, i, i, ctypes.POINTER(vp)]
+    L.lrcnn_comm_loopback_group.argtypes = [i, ctypes.POINTER(vp)]
+    L.lrcnn_comm_loopback_group_free.argtypes = [vp]
+    L.lrcnn_comm_init_loopback.argtypes = [vp, i, ctypes.POINTER(vp)]
+    L.lrcnn_comm_free.argtypes = [vp]
+    L.lrcnn_plan_set_comm.argtypes = [vp, vp]
     L.lrcnn_last_tc_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
     L.lrcnn_last_error.restype = ctypes.c_char_p
     L.lrcnn_version.restype = ctypes.c_char_p
@@ -189,6 +201,23 @@ class Plan:
         lo, a, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _check(lib().lrcnn_plan_rows(self.h, seg, band, tid, ctypes.byref(lo), ctypes.byref(a), ctypes.byref(b)))
         return lo.value, a.value, b.value
+
+    def shard(self, seg, tid):
+        """(own_lo, own_hi, lo, hi): owned segment-output rows and tensor tid's extended range."""
+        v = [ctypes.c_int() for _ in range(4)]
+        _check(lib().lrcnn_plan_shard(self.h, seg, tid, *[ctypes.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def xfers(self, seg):
+        """Halo transfers of segment seg's input: list of (peer, send, r0, r1)."""
+        n = ctypes.c_int()
+        arrs = [(ctypes.c_int * 16)() for _ in range(4)]
+        _check(lib().lrcnn_plan_xfers(self.h, seg, 16, ctypes.byref(n), *arrs))
+        return [tuple(a[i] for a in arrs) for i in range(n.value)]
+
+    def set_comm(self, comm):
+        _check(lib().lrcnn_plan_set_comm(self.h, comm.h if comm is not None else None))
+        self._comm = comm
 
     def memory(self):
         m = MemoryReport()
@@ -321,6 +350,43 @@ class Plan:
         return n.value
 
 
+class Comm:
+    """Communicator for row sharding: NCCL (one process per GPU) or in-process loopback."""
+
+    def __init__(self, h, group=None):
+        self.h, self.group = h, group
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = (ctypes.c_char * 128)()
+        _check(lib().lrcnn_comm_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(unique_id, rank, world):
+        h = ctypes.c_void_p()
+        buf = (ctypes.c_char * 128).from_buffer_copy(unique_id)
+        _check(lib().lrcnn_comm_init_nccl(buf, rank, world, ctypes.byref(h)))
+        return Comm(h)
+
+    @staticmethod
+    def loopback(world):
+        """One communicator per rank of an in-process group (ranks = host threads, one GPU)."""
+        g = ctypes.c_void_p()
+        _check(lib().lrcnn_comm_loopback_group(world, ctypes.byref(g)))
+        out = []
+        for r in range(world):
+            h = ctypes.c_void_p()
+            _check(lib().lrcnn_comm_init_loopback(g, r, ctypes.byref(h)))
+            out.append(Comm(h, g))
+        return out
+
+    def free(self):
+        if self.h:
+            lib().lrcnn_comm_free(self.h)
+            self.h = None
+
+
 class DeviceState:
     """Device buffers for one plan, allocated with torch (the caller owns all device memory)."""
 
@@ -359,6 +425,9 @@ class DeviceState:
 
     def backward(self, stream=None):
         self.plan.backward_rows(self.params, self.x, self.zl, self.dzl, self.grads, self.ws, stream)
+
+    def step_grads(self, stream=None):
+        self.plan.step_grads(self.params, self.grads, self.x, self.labels, self.loss, self.ws, stream)
 
     def step(self, lr, stream=None):
         self.plan.step(self.master, self.params, self.grads, self.x, self.labels, lr, self.loss, self.ws, stream)

@@ -168,9 +168,13 @@ def test_plan_errors():
     with pytest.raises(LB.LrcnnError) as e:
         LB.Plan(bad, 1, mode="2ps", prec="fp32", n_bands=2)
     assert e.value.name == "E_ARG"
-    with pytest.raises(LB.LrcnnError) as e:
-        LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=2, world=2)
-    assert e.value.name == "E_UNSUPPORTED"
+    LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=2, world=2, rank=1)
+    with pytest.raises(LB.LrcnnError) as e:      # more ranks than segment-output rows
+        LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=2, world=32, rank=0)
+    assert e.value.name == "E_INFEASIBLE"
+    with pytest.raises(LB.LrcnnError) as e:      # halo wider than a neighbour's shard
+        LB.Plan(WL.vgg16(H=64, W=32, width_div=8), 1, mode="2ps", prec="fp32", n_bands=1, world=8, rank=3)
+    assert e.value.name == "E_INFEASIBLE"
 
 
 def test_memory_and_flops_accounting():
