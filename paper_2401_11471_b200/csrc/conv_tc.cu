@@ -40,6 +40,7 @@ typedef __nv_bfloat16 bf16;
 
 struct TcConv {
     View out, res, act;
+    View in;               // im2col kernel: the band input it gathers from
     const bf16 *bias, *beta;
     int mode;              // 0 = forward epilogue, 1 = dgrad (gated accumulate)
     int epi, relu, gate, has_res, c_real, n_out;
@@ -92,25 +93,36 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap *m, const void *s
                  "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                  : "memory");
 }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// FP epilogue with coalesced TMA stores: per 64-channel group the 4 epilogue warps write the
+// FP epilogue with coalesced TMA stores: per 64-channel group the NE epilogue warps write the
 // bf16 tile (128 pixels x 128 B, 128B-swizzled: conflict-free 16-byte smem stores) into one of
 // two staging buffers, then one thread issues a TMA tensor store of the TW x TH pixel
 // rectangle; the output map's row extent ends at the band's last computed row, so pixels
-// outside the band / image are clipped by TMA.
-template <int BN>
+// outside the band / image are clipped by TMA.  NE = 4: a warp per TMEM lane quarter (32
+// pixels) x 64 channels; NE = 8: two warps per quarter, 32 channels each (half the serial
+// per-thread work per tile).  Warps lead_warp .. lead_warp+NE-1; TMEM quarter = warp % 4.
+template <int NE>
+__device__ __forceinline__ void epi_bar_n() { asm volatile("bar.sync 1, %0;" ::"n"(NE * 32) : "memory"); }
+
+template <int BN, int NE = 4>
 __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
                                                   uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
-                                                  int lane) {
+                                                  int lane, int lead_warp = 2) {
+    constexpr int CH = 64 * 4 / NE;   // channels of a 64-channel group handled per thread
     const int num_tiles = P.m_tiles * P.n_tiles;
-    const int ew = warp & 3;
-    const int m = ew * 32 + lane;
-    const bool leader = (warp == 2 && lane == 0);
+    const int q = warp & 3, hh = (warp - lead_warp) >> 2;
+    const int m = q * 32 + lane;
+    const bool leader = (warp == lead_warp && lane == 0);
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     int acc = 0, sbuf = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -119,58 +131,57 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
         const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
         const int yg = yg0 + m / P.TW, xg = xg0 + m % P.TW;
         const bool valid = yg < P.out_b && xg < P.Wo;
+        const bf16 *resp = P.has_res && valid ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                                                    ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp
+                                              : nullptr;
         ptx::mbar_wait(tfull + acc, aphase);
         ptx::tc_fence_after();
 #pragma unroll 1
         for (int grp = 0; grp < BN / 64; ++grp) {
             const int nb = n0 + grp * 64;
             if (nb >= P.n_out) break;
-            uint32_t v[64];
-            ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-            ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + grp * 64 + 32,
-                           *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            const int cb = nb + hh * CH;              // this thread's first channel
+            uint32_t v[CH];
+#pragma unroll
+            for (int h = 0; h < CH / 32; ++h)
+                ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+            // per-channel epilogue parameters (identical for every pixel) and the residual
+            uint4 pb[CH / 8], pe[CH / 8], pr[CH / 8];
+#pragma unroll
+            for (int c = 0; c < CH / 8; ++c) {
+                const int n = cb + c * 8;
+                const bool in = n < P.n_out;
+                pb[c] = P.epi != 0 && in ? *reinterpret_cast<const uint4 *>(P.bias + n) : make_uint4(0, 0, 0, 0);
+                pe[c] = P.epi == 2 && in ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
+                pr[c] = resp && in ? *reinterpret_cast<const uint4 *>(resp + n) : make_uint4(0, 0, 0, 0);
+            }
+            const bool ragged = cb + CH > P.c_real;   // channels >= c_real get 0 (affine) / no bias
             ptx::tmem_ld_wait();
             if (leader) bulk_wait_read1();             // the store that last used this buffer has read it
-            epi_bar();
-            uint8_t *buf = stage_out + sbuf * kOutStage + m * 128;
+            epi_bar_n<NE>();
+            const uint32_t buf = ptx::smem_u32(stage_out + sbuf * kOutStage + m * 128);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int n = nb + c * 8;
+            for (int c = 0; c < CH / 8; ++c) {
+                const int n = cb + c * 8;
+                const uint16_t *bh = reinterpret_cast<const uint16_t *>(&pb[c]);
+                const uint16_t *eh = reinterpret_cast<const uint16_t *>(&pe[c]);
+                const uint16_t *rh = reinterpret_cast<const uint16_t *>(&pr[c]);
                 float f[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c * 8 + j]);
-                if (valid && n < P.n_out) {
-                    if (P.epi != 0) {
-                        uint4 bb = *reinterpret_cast<const uint4 *>(P.bias + n);
-                        const uint16_t *bh = reinterpret_cast<const uint16_t *>(&bb);
-                        uint4 be = P.epi == 2 ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
-                        const uint16_t *beh = reinterpret_cast<const uint16_t *>(&be);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            float bj = n + j < P.c_real ? bf2f(bh[j]) : 0.f;
-                            if (P.epi == 1) f[j] += bj;
-                            else f[j] = n + j < P.c_real ? bj * f[j] + bf2f(beh[j]) : 0.f;
-                        }
-                    }
-                    if (P.has_res) {
-                        uint4 rr = *reinterpret_cast<const uint4 *>(
-                            (const bf16 *)P.res.p + (long long)b * P.res.bs +
-                            ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp + n);
-                        const uint16_t *rh = reinterpret_cast<const uint16_t *>(&rr);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) f[j] += bf2f(rh[j]);
-                    }
-                    if (P.relu) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
-                    }
+                for (int j = 0; j < 8; ++j) {
+                    float x = __uint_as_float(v[c * 8 + j]);
+                    const bool live = !ragged || n + j < P.c_real;
+                    if (P.epi == 1) x += live ? bf2f(bh[j]) : 0.f;
+                    else if (P.epi == 2) x = live ? bf2f(bh[j]) * x + bf2f(eh[j]) : 0.f;
+                    x += bf2f(rh[j]);
+                    f[j] = P.relu ? fmaxf(x, 0.f) : x;
                 }
                 uint4 o;
                 o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
-                *reinterpret_cast<uint4 *>(buf + ((c ^ (m & 7)) << 4)) = o;
+                st_shared_v4(buf + (((hh * (CH / 8) + c) ^ (m & 7)) << 4), o);
             }
             fence_async_smem();
-            epi_bar();
+            epi_bar_n<NE>();
             if (leader) {
                 tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, xg0, yg0 - P.out.base, b);
                 bulk_commit();
@@ -364,6 +375,143 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ small-channel conv FP (im2col in smem)
+// Layers whose input has cin_p = 8 channels (the padded RGB image: conv1_1 of VGG-16, the 7x7/s2
+// stem of ResNet-50).  The contraction index is K = tap x 8 channels; one pipeline stage holds
+// 8 taps: row m of the 16 KB stage (SWIZZLE_128B, K-major) is output pixel m's 8 taps x 16 bytes,
+// gathered by 4 producer warps with coalesced 16-byte loads (zeros for padding rows/columns, rows
+// outside the band and taps >= k*k).  The weights viewed as [cout][k*k*8] are TMA-loaded once per
+// CTA and stay resident.  Per 128-pixel tile this is ceil(k*k/2) MMAs of K=16 (5 for 3x3) instead
+// of k*k TMA boxes with half of every box zero-filled channels.
+// Warps 0-7 gather (pixel x half of the stage's taps), warp 8 TMEM + MMA issue, warps 9-16 the
+// TMA-store epilogue.
+static constexpr int kI2cGather = 8;                          // gather warps (2 per 32-pixel quarter)
+static constexpr int kI2cMmaWarp = kI2cGather;
+static constexpr int kI2cEpi = 8;
+static constexpr int kI2cThreads = (kI2cGather + 1 + kI2cEpi) * 32;
+static constexpr int kI2cStages = 6;
+static constexpr int kI2cStage = 128 * 128;
+static constexpr int kI2cBMax = 64 * 1024;
+static constexpr int kI2cSmem = kI2cStages * kI2cStage + kI2cBMax + 2 * kOutStage + 1024 + 256;
+
+template <int BN>
+__global__ void __launch_bounds__(kI2cThreads, 1)
+    k_conv_im2col(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmO, const TcConv P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = sA + kI2cStages * kI2cStage;
+    uint8_t *sO = sB + kI2cBMax;
+    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
+    uint64_t *empty = full + kI2cStages;
+    uint64_t *tfull = empty + kI2cStages;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *bfull = tempty + 2;
+    uint32_t *tslot = (uint32_t *)(bfull + 1);
+    const int KS = (P.ntaps + 7) / 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kI2cStages; ++i) {
+            ptx::mbar_init(full + i, kI2cGather * 32);
+            ptx::mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, kI2cEpi); }
+        ptx::mbar_init(bfull, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmO);
+    }
+    if (warp == kI2cMmaWarp) ptx::tmem_alloc(tslot, 2 * BN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int num_tiles = P.m_tiles * P.n_tiles;
+
+    if (warp < kI2cGather) {
+        if (threadIdx.x == 0) {   // resident weights: n_tiles x KS boxes of BN rows x 64 K
+            ptx::mbar_arrive_expect_tx(bfull, P.n_tiles * KS * BN * 128);
+            for (int nt = 0; nt < P.n_tiles; ++nt)
+                for (int ks = 0; ks < KS; ++ks)
+                    ptx::tma_load_2d(sB + (nt * KS + ks) * BN * 128, &tmB, bfull, ks * 64, nt * BN);
+        }
+        // thread = (pixel m of the tile, half h of the stage's 8 taps)
+        const int m = threadIdx.x & 127, h = threadIdx.x >> 7;
+        const View &in = P.in;
+        const int W = in.W;
+        const int ylo = max(0, in.base), yhi = min(in.H, in.base + in.rows);
+        const uint4 *src = (const uint4 *)in.p;   // 8 bf16 channels = one 16-byte pixel
+        const uint32_t a_base = ptx::smem_u32(sA) + m * 128;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int mt = tile / P.n_tiles;
+            const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+            const int yo = P.out_a + ty * P.TH + m / P.TW, xo = tx * P.TW + m % P.TW;
+            const bool valid = yo < P.out_b && xo < P.Wo;
+            const int yi = yo * P.a_mul, xi = xo * P.a_mul;
+            const uint4 *pp = src + (long long)b * (in.bs >> 3) + (long long)(yi - in.base) * W + xi;
+            for (int ks = 0; ks < KS; ++ks) {
+                uint4 v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tap = ks * 8 + h * 4 + j;
+                    v[j] = make_uint4(0, 0, 0, 0);
+                    if (valid && tap < P.ntaps) {
+                        const int dy = P.tap_oy[tap], dx = P.tap_ox[tap];
+                        const int iy = yi + dy, ix = xi + dx;
+                        if (iy >= ylo && iy < yhi && ix >= 0 && ix < W) v[j] = __ldg(pp + dy * W + dx);
+                    }
+                }
+                ptx::mbar_wait(empty + stage, phase ^ 1);
+                const uint32_t row = a_base + stage * kI2cStage;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) st_shared_v4(row + (((h * 4 + j) ^ (m & 7)) << 4), v[j]);
+                fence_async_smem();
+                ptx::mbar_arrive(full + stage);
+                if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == kI2cMmaWarp) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            ptx::mbar_wait(bfull, 0);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int nt = tile % P.n_tiles;
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int ks = 0; ks < KS; ++ks) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * kI2cStage);
+                    const uint32_t b0 = ptx::smem_u32(sB + (nt * KS + ks) * BN * 128);
+                    const int nk = min(8, P.ntaps - ks * 8);   // real taps in this stage
+                    for (int kk = 0; kk < (nk + 1) / 2; ++kk) {
+                        uint64_t ad = ptx::smem_desc(a0 + kk * 32, 16, 1024, 2);
+                        uint64_t bd = ptx::smem_desc(b0 + kk * 32, 16, 1024, 2);
+                        ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
+                    }
+                    ptx::umma_commit(empty + stage);
+                    if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(tfull + acc);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        conv_epilogue_tma<BN, kI2cEpi>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, kI2cMmaWarp + 1);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kI2cMmaWarp) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 2 * BN);
     }
 }
 
@@ -817,6 +965,64 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     return launch_conv<256, 64>(P, A, Bm, O, tiles, st);
 }
 
+// weights [rows][K] (K = taps * 8, the OHWI layout of an 8-channel input) as a 2D map with
+// 64-element boxes (SWIZZLE_128B); K beyond taps*8 and rows beyond `rows` read as zero.
+static bool encode_w2d(CUtensorMap *m, const void *w, int rows, int K, int BN) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)BN};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(w), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensorMap &O, int tiles, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_conv_im2col<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI2cSmem) !=
+            cudaSuccess)
+            return false;
+        attr = true;
+    }
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    k_conv_im2col<BN><<<grid, kI2cThreads, kI2cSmem, st>>>(Bm, O, P);
+    return true;
+}
+
+// FP of an 8-channel-input conv through the im2col kernel; false = shape not taken.
+static bool conv_im2col(TcConv &P, const View &in, const void *w, int w_rows, cudaStream_t st) {
+    if (in.Cp != 8 || P.mode != 0 || P.o_stride != 1 || P.n_out % 8 || P.out.Cp % 8) return false;
+    if (!aligned16(in.p) || !aligned16(w) || !aligned16(P.out.p) || (in.bs & 7)) return false;
+    static const int on = env_int("LRCNN_IM2COL", 1);
+    if (!on) return false;
+    const int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
+    const int KS = (P.ntaps + 7) / 8;
+    P.n_tiles = (P.n_out + BN - 1) / BN;
+    if ((long)P.n_tiles * KS * BN * 128 > kI2cBMax) return false;
+    const int rows = P.out_b - P.out_a;
+    if (rows <= 0 || P.Wo <= 0) return true;
+    P.in = in;
+    P.in_base = in.base;
+    pick_tile(rows, P.Wo, 1, P.TW, P.TH);
+    P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    CUtensorMap Bm, O;
+    if (!encode_w2d(&Bm, w, w_rows, P.ntaps * 8, BN)) return false;
+    View ov = P.out;
+    ov.rows = P.out_b - P.out.base;
+    if (!encode_view(&O, ov, P.B, P.TW, P.TH)) return false;
+    P.tma_out = 1;
+    const int tiles = P.m_tiles * P.n_tiles;
+    if (BN == 64) return launch_im2col<64>(P, Bm, O, tiles, st);
+    if (BN == 128) return launch_im2col<128>(P, Bm, O, tiles, st);
+    return launch_im2col<256>(P, Bm, O, tiles, st);
+}
+
 bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
     if (a.s < 1 || a.s > 2) return false;
     TcConv P{};
@@ -835,6 +1041,7 @@ bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
             P.tap_oy[t] = ky - a.p; P.tap_ox[t] = kx - a.p; P.tap_w[t] = t;
         }
     P.k = a.k; P.pad = a.p; P.halo_ok = a.s == 1 && a.k == 3;
+    if (a.in.Cp == 8 && conv_im2col(P, a.in, a.w, a.c_out, st)) return true;
     return conv_launch(P, a.in, a.w, a.c_out, a.k * a.k, a.in.Cp, st);
 }
 
