@@ -55,7 +55,36 @@ struct TcConv {
     int tma_out;           // FP: stage the output tile in smem and TMA-store it
     int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
+    int tw_log2;           // TW = 1 << tw_log2
+    uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
+    // tile index -> (n tile, tile column, tile row, image); n tiles vary fastest
+    __device__ __forceinline__ void decode(int tile, int &nt, int &tx, int &ty, int &b) const {
+        const int mt = fdiv(tile, fd_nt), r = fdiv(mt, fd_tx);
+        nt = tile - mt * n_tiles;
+        tx = mt - r * tiles_x;
+        b = fdiv(r, fd_ty);
+        ty = r - b * tiles_y;
+    }
+    __device__ __forceinline__ static int fdiv(int n, const uint32_t (&f)[2]) {
+        return (int)((__umulhi((uint32_t)n, f[0]) + (uint32_t)n) >> f[1]);
+    }
 };
+
+// n / d for 0 <= n < 2^31 as (umulhi(n, mul) + n) >> shift (round-up reciprocal)
+static inline void fastdiv_init(uint32_t (&f)[2], int d) {
+    uint32_t l = 0;
+    while ((1ull << l) < (unsigned long long)d) ++l;
+    f[0] = (uint32_t)(((1ull << 32) * ((1ull << l) - (unsigned long long)d)) / (unsigned long long)d + 1);
+    f[1] = l;
+}
+static inline void tile_div_init(TcConv &P) {
+    fastdiv_init(P.fd_nt, P.n_tiles);
+    fastdiv_init(P.fd_tx, P.tiles_x);
+    fastdiv_init(P.fd_ty, P.tiles_y);
+    int l = 0;
+    while ((1 << l) < P.TW) ++l;
+    P.tw_log2 = l;
+}
 
 struct TcWgrad {
     float *dw;
@@ -113,6 +142,34 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 template <int NE>
 __device__ __forceinline__ void epi_bar_n() { asm volatile("bar.sync 1, %0;" ::"n"(NE * 32) : "memory"); }
 
+// bf16 pair (one 32-bit word) -> two floats
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Fast path of the FP epilogue for CH channels starting at cb (all < c_real): EPI 0 none,
+// 1 bias, 2 affine; RES adds the residual; lo = 0 (ReLU) or -inf.  Parameters / residual
+// were loaded into pb/pe/pr before the accumulator wait.
+template <int CH, int EPI, bool RES>
+__device__ __forceinline__ void epi_fast(const uint32_t (&v)[CH], const uint4 (&pb)[CH / 8], const uint4 (&pe)[CH / 8],
+                                         const uint4 (&pr)[CH / 8], float lo, uint32_t buf, int chunk0, int m) {
+#pragma unroll
+    for (int c = 0; c < CH / 8; ++c) {
+        const uint32_t bw[4] = {pb[c].x, pb[c].y, pb[c].z, pb[c].w};
+        const uint32_t ew[4] = {pe[c].x, pe[c].y, pe[c].z, pe[c].w};
+        const uint32_t rw[4] = {pr[c].x, pr[c].y, pr[c].z, pr[c].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            float x0 = __uint_as_float(v[c * 8 + 2 * h]), x1 = __uint_as_float(v[c * 8 + 2 * h + 1]);
+            if (EPI == 1) { x0 += bf_lo(bw[h]); x1 += bf_hi(bw[h]); }
+            if (EPI == 2) { x0 = fmaf(x0, bf_lo(bw[h]), bf_lo(ew[h])); x1 = fmaf(x1, bf_hi(bw[h]), bf_hi(ew[h])); }
+            if (RES) { x0 += bf_lo(rw[h]); x1 += bf_hi(rw[h]); }
+            o[h] = pack2(fmaxf(x0, lo), fmaxf(x1, lo));
+        }
+        st_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4), make_uint4(o[0], o[1], o[2], o[3]));
+    }
+}
+
 template <int BN, int NE = 4>
 __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
                                                   uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
@@ -123,17 +180,21 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
     const int m = q * 32 + lane;
     const bool leader = (warp == lead_warp && lane == 0);
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    const float lo = P.relu ? 0.f : -INFINITY;
+    const int my = m >> P.tw_log2, mx = m & ((1 << P.tw_log2) - 1);
     int acc = 0, sbuf = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
-        const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
         const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
-        const int yg = yg0 + m / P.TW, xg = xg0 + m % P.TW;
+        const int yg = yg0 + my, xg = xg0 + mx;
         const bool valid = yg < P.out_b && xg < P.Wo;
-        const bf16 *resp = P.has_res && valid ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
-                                                    ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp
-                                              : nullptr;
+        // invalid pixels (clipped by the TMA store) read the residual's first pixel instead
+        const bf16 *resp = !P.has_res ? nullptr
+                           : valid    ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                                         ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp
+                                      : (const bf16 *)P.res.p;
         ptx::mbar_wait(tfull + acc, aphase);
         ptx::tc_fence_after();
 #pragma unroll 1
@@ -160,29 +221,36 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             if (leader) bulk_wait_read1();             // the store that last used this buffer has read it
             epi_bar_n<NE>();
             const uint32_t buf = ptx::smem_u32(stage_out + sbuf * kOutStage + m * 128);
+            const int chunk0 = hh * (CH / 8);
+            if (!ragged && P.epi == 1 && !P.has_res) epi_fast<CH, 1, false>(v, pb, pe, pr, lo, buf, chunk0, m);
+            else if (!ragged && P.epi == 2 && !P.has_res) epi_fast<CH, 2, false>(v, pb, pe, pr, lo, buf, chunk0, m);
+            else if (!ragged && P.epi == 2 && P.has_res) epi_fast<CH, 2, true>(v, pb, pe, pr, lo, buf, chunk0, m);
+            else if (!ragged && P.epi == 0 && !P.has_res) epi_fast<CH, 0, false>(v, pb, pe, pr, lo, buf, chunk0, m);
+            else {
 #pragma unroll
-            for (int c = 0; c < CH / 8; ++c) {
-                const int n = cb + c * 8;
-                const uint16_t *bh = reinterpret_cast<const uint16_t *>(&pb[c]);
-                const uint16_t *eh = reinterpret_cast<const uint16_t *>(&pe[c]);
-                const uint16_t *rh = reinterpret_cast<const uint16_t *>(&pr[c]);
-                float f[8];
+                for (int c = 0; c < CH / 8; ++c) {
+                    const int n = cb + c * 8;
+                    const uint16_t *bh = reinterpret_cast<const uint16_t *>(&pb[c]);
+                    const uint16_t *eh = reinterpret_cast<const uint16_t *>(&pe[c]);
+                    const uint16_t *rh = reinterpret_cast<const uint16_t *>(&pr[c]);
+                    float f[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    float x = __uint_as_float(v[c * 8 + j]);
-                    const bool live = !ragged || n + j < P.c_real;
-                    if (P.epi == 1) x += live ? bf2f(bh[j]) : 0.f;
-                    else if (P.epi == 2) x = live ? bf2f(bh[j]) * x + bf2f(eh[j]) : 0.f;
-                    x += bf2f(rh[j]);
-                    f[j] = P.relu ? fmaxf(x, 0.f) : x;
+                    for (int j = 0; j < 8; ++j) {
+                        float x = __uint_as_float(v[c * 8 + j]);
+                        const bool live = !ragged || n + j < P.c_real;
+                        if (P.epi == 1) x += live ? bf2f(bh[j]) : 0.f;
+                        else if (P.epi == 2) x = live ? bf2f(bh[j]) * x + bf2f(eh[j]) : 0.f;
+                        x += bf2f(rh[j]);
+                        f[j] = fmaxf(x, lo);
+                    }
+                    uint4 o;
+                    o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
+                    st_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4), o);
                 }
-                uint4 o;
-                o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
-                st_shared_v4(buf + (((hh * (CH / 8) + c) ^ (m & 7)) << 4), o);
             }
             fence_async_smem();
             epi_bar_n<NE>();
-            if (leader) {
+            if (leader && !(P.dbg & 1)) {
                 tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, xg0, yg0 - P.out.base, b);
                 bulk_commit();
             }
@@ -342,6 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            const uint64_t dA = ptx::smem_desc(ptx::smem_u32(sA), 16, SBO, LAYOUT);
+            const uint64_t dB = ptx::smem_desc(ptx::smem_u32(sB), 16, SBO, LAYOUT);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -351,14 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ks = 0; ks < P.k_steps; ++ks) {
                     ptx::mbar_wait(full + stage, phase);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + stage * ABYTES);
-                    const uint32_t b0 = ptx::smem_u32(sB + stage * BBYTES);
+                    const uint32_t a0 = (uint32_t)dA + stage * (ABYTES >> 4);
+                    const uint32_t b0 = (uint32_t)dB + stage * (BBYTES >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < KC / 16; ++kk) {
-                        uint64_t ad = ptx::smem_desc(a0 + kk * 32, 16, SBO, LAYOUT);
-                        uint64_t bd = ptx::smem_desc(b0 + kk * 32, 16, SBO, LAYOUT);
-                        if (!(P.dbg & 2)) ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
-                    }
+                    for (int kk = 0; kk < KC / 16; ++kk)
+                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
                     ptx::umma_commit(empty + stage);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -438,38 +506,49 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
                 for (int ks = 0; ks < KS; ++ks)
                     ptx::tma_load_2d(sB + (nt * KS + ks) * BN * 128, &tmB, bfull, ks * 64, nt * BN);
         }
-        // thread = (pixel m of the tile, half h of the stage's 8 taps)
-        const int m = threadIdx.x & 127, h = threadIdx.x >> 7;
+        // thread = (tap slot c of the stage, pixels pg + 32 i): the tap's offsets are per-stage
+        // constants, each pixel is decoded once per tile
+        const int c = threadIdx.x & 7, pg = threadIdx.x >> 3;
         const View &in = P.in;
         const int W = in.W;
         const int ylo = max(0, in.base), yhi = min(in.H, in.base + in.rows);
         const uint4 *src = (const uint4 *)in.p;   // 8 bf16 channels = one 16-byte pixel
-        const uint32_t a_base = ptx::smem_u32(sA) + m * 128;
+        const uint32_t a_base = ptx::smem_u32(sA);
+        const int twm = (1 << P.tw_log2) - 1;
         int stage = 0;
         uint32_t phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int mt = tile / P.n_tiles;
-            const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
-            const int yo = P.out_a + ty * P.TH + m / P.TW, xo = tx * P.TW + m % P.TW;
-            const bool valid = yo < P.out_b && xo < P.Wo;
-            const int yi = yo * P.a_mul, xi = xo * P.a_mul;
-            const uint4 *pp = src + (long long)b * (in.bs >> 3) + (long long)(yi - in.base) * W + xi;
+            int nt, tx, ty, b;
+            P.decode(tile, nt, tx, ty, b);
+            int yi[4], xi[4];
+            const uint4 *pp[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int m = pg + 32 * i;
+                const int yo = P.out_a + ty * P.TH + (m >> P.tw_log2), xo = tx * P.TW + (m & twm);
+                const bool valid = yo < P.out_b && xo < P.Wo;
+                yi[i] = valid ? yo * P.a_mul : -(1 << 20);     // invalid pixel: every tap out of range
+                xi[i] = xo * P.a_mul;
+                pp[i] = src + (long long)b * (in.bs >> 3) + (long long)(yi[i] - in.base) * W + xi[i];
+            }
             for (int ks = 0; ks < KS; ++ks) {
+                const int tap = ks * 8 + c;
+                const bool tv = tap < P.ntaps && !(P.dbg & 4);
+                const int dy = tv ? P.tap_oy[tap] : 0, dx = tv ? P.tap_ox[tap] : 0;
                 uint4 v[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int tap = ks * 8 + h * 4 + j;
-                    v[j] = make_uint4(0, 0, 0, 0);
-                    if (valid && tap < P.ntaps) {
-                        const int dy = P.tap_oy[tap], dx = P.tap_ox[tap];
-                        const int iy = yi + dy, ix = xi + dx;
-                        if (iy >= ylo && iy < yhi && ix >= 0 && ix < W) v[j] = __ldg(pp + dy * W + dx);
-                    }
+                for (int i = 0; i < 4; ++i) {
+                    const int iy = yi[i] + dy, ix = xi[i] + dx;
+                    v[i] = make_uint4(0, 0, 0, 0);
+                    if (tv && iy >= ylo && iy < yhi && ix >= 0 && ix < W) v[i] = __ldg(pp[i] + dy * W + dx);
                 }
                 ptx::mbar_wait(empty + stage, phase ^ 1);
-                const uint32_t row = a_base + stage * kI2cStage;
+                const uint32_t sa = a_base + stage * kI2cStage;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) st_shared_v4(row + (((h * 4 + j) ^ (m & 7)) << 4), v[j]);
+                for (int i = 0; i < 4; ++i) {
+                    const int m = pg + 32 * i;
+                    st_shared_v4(sa + m * 128 + ((c ^ (m & 7)) << 4), v[i]);
+                }
                 fence_async_smem();
                 ptx::mbar_arrive(full + stage);
                 if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
@@ -478,6 +557,9 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
     } else if (warp == kI2cMmaWarp) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            const uint64_t dA = ptx::smem_desc(ptx::smem_u32(sA), 16, 1024, 2);
+            const uint64_t dB = ptx::smem_desc(ptx::smem_u32(sB), 16, 1024, 2);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
             ptx::mbar_wait(bfull, 0);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
@@ -489,14 +571,11 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
                 for (int ks = 0; ks < KS; ++ks) {
                     ptx::mbar_wait(full + stage, phase);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + stage * kI2cStage);
-                    const uint32_t b0 = ptx::smem_u32(sB + (nt * KS + ks) * BN * 128);
+                    const uint32_t a0 = (uint32_t)dA + stage * (kI2cStage >> 4);
+                    const uint32_t b0 = (uint32_t)dB + (nt * KS + ks) * (BN * 128 >> 4);
                     const int nk = min(8, P.ntaps - ks * 8);   // real taps in this stage
-                    for (int kk = 0; kk < (nk + 1) / 2; ++kk) {
-                        uint64_t ad = ptx::smem_desc(a0 + kk * 32, 16, 1024, 2);
-                        uint64_t bd = ptx::smem_desc(b0 + kk * 32, 16, 1024, 2);
-                        ptx::umma_bf16(d, ad, bd, idesc, (ks | kk) != 0);
-                    }
+                    for (int kk = 0; kk < (nk + 1) / 2; ++kk)
+                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
                     ptx::umma_commit(empty + stage);
                     if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
                 }
@@ -517,32 +596,43 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
 
 // ------------------------------------------------------------------ conv FP / dgrad, halo reuse
 // Stride-1 k x k convolutions: the output tile is 8 columns x 16 rows.  One TMA box of
-// 16 x (16+k-1) input pixels x 64 channels (the tile plus its halo, row pitch 16 pixels =
-// 2 KB) is loaded once per input-channel chunk and serves all k*k taps: the A operand of
-// tap (ky, kx) is the same smem box at a start offset of (16*ky + kx) pixel rows, with
-// 8-pixel core-matrix groups 2 KB apart (SBO = 2048).  A traffic drops from k*k boxes
-// of 128 rows to one box of 16*(15+k) rows per chunk.  Weights stream per tap.
-static constexpr int kHaloPitch = 16;
+// (8+k-1) x (16+k-1) input pixels x 64 channels (the tile plus its halo; row pitch 8+k-1
+// pixels) is loaded once per input-channel chunk and serves all k*k taps: the A operand of
+// tap (ky, kx) is the same smem box at a start offset of (pitch*ky + kx) pixel rows, with the
+// 8-pixel core-matrix groups (tile rows) pitch*128 B apart (SBO).  The SWIZZLE_128B pattern is
+// a function of the absolute smem address bits [7,10) on both the TMA write and the UMMA read,
+// so a start at any 128-byte row (descriptor base offset 0) addresses the box consistently.
+// A traffic drops from k*k boxes of 128 rows to one box of (7+k)(15+k) rows per chunk;
+// weights stream per (chunk, tap).
+template <int KH>
+struct HaloGeom {
+    static constexpr int kPitch = 8 + KH - 1, kRows = 16 + KH - 1;
+    static constexpr int kABytes = ((kPitch * kRows * 128 + 1023) / 1024) * 1024;
+};
 template <int BN, int KH>
 struct HaloCfg {
-    static constexpr int kABytes = kHaloPitch * (16 + KH - 1) * 128;
+    static constexpr int kABytes = HaloGeom<KH>::kABytes;
     static constexpr int kBBytes = BN * 128;
-    static constexpr int kSA = 2;
-    static constexpr int kSB = (220 * 1024 - kSA * kABytes) / kBBytes;
-    static constexpr int kSmem = kSA * kABytes + kSB * kBBytes + 1024 + 512;
+    static constexpr int kSA = 4;
+    static constexpr int kSB = (232448 - kSA * kABytes - 2 * kOutStage - 2048) / kBBytes > 16
+                                   ? 16 : (232448 - kSA * kABytes - 2 * kOutStage - 2048) / kBBytes;
+    static constexpr int kSmem = kSA * kABytes + kSB * kBBytes + 2 * kOutStage + 1024 + 512;
     static constexpr uint32_t kTmemCols = 2 * BN;
 };
 
 template <int BN, int KH>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_conv_tc_halo(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcConv P) {
+    k_conv_tc_halo(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO, const TcConv P) {
     using Cfg = HaloCfg<BN, KH>;
     constexpr int SA = Cfg::kSA, SB = Cfg::kSB;
+    constexpr int HP = HaloGeom<KH>::kPitch;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
     uint8_t *sB = smem + SA * Cfg::kABytes;
-    uint64_t *fullA = (uint64_t *)(sB + SB * Cfg::kBBytes);
+    uint8_t *sO = sB + SB * Cfg::kBBytes;
+    uint64_t *fullA = (uint64_t *)(sO + 2 * kOutStage);
     uint64_t *emptyA = fullA + SA;
     uint64_t *fullB = emptyA + SA;
     uint64_t *emptyB = fullB + SB;
@@ -572,12 +662,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             int sa = 0, sb = 0;
             uint32_t pa = 0, pb = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
-                const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                int nt, tx, ty, b;
+                P.decode(tile, nt, tx, ty, b);
                 const int y0 = P.out_a + ty * 16, x0 = tx * 8, n0 = nt * BN;
                 for (int c = 0; c < P.cin_chunks; ++c) {
                     ptx::mbar_wait(emptyA + sa, pa ^ 1);
-                    ptx::mbar_arrive_expect_tx(fullA + sa, Cfg::kABytes);
+                    ptx::mbar_arrive_expect_tx(fullA + sa, HP * HaloGeom<KH>::kRows * 128);
                     ptx::tma_load_4d(sA + sa * Cfg::kABytes, &tmA, fullA + sa, c * 64, x0 - P.pad,
                                      y0 - P.pad - P.in_base, b);
                     if (++sa == SA) { sa = 0; pa ^= 1; }
@@ -593,6 +683,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            const uint64_t dA = ptx::smem_desc_sw128_bo(ptx::smem_u32(sA), 16, HP * 128, 0);
+            const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(sB), 16, 1024);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
             int sa = 0, sb = 0, acc = 0;
             uint32_t pa = 0, pb = 0, aphase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -603,19 +696,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < P.cin_chunks; ++c) {
                     ptx::mbar_wait(fullA + sa, pa);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + sa * Cfg::kABytes);
+                    const uint32_t a0 = (uint32_t)dA + sa * (Cfg::kABytes >> 4);
+#pragma unroll
                     for (int tap = 0; tap < taps; ++tap) {
                         const int ky = tap / KH, kx = tap - ky * KH;
                         ptx::mbar_wait(fullB + sb, pb);
                         ptx::tc_fence_after();
-                        const uint32_t at = a0 + (uint32_t)(ky * kHaloPitch + kx) * 128;
-                        const uint32_t b0 = ptx::smem_u32(sB + sb * Cfg::kBBytes);
+                        const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
+                        const uint32_t b0 = (uint32_t)dB + sb * (Cfg::kBBytes >> 4);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            const uint32_t aa = at + kk * 32;
-                            uint64_t ad = ptx::smem_desc_sw128_bo(aa, 16, kHaloPitch * 128, P.boff ? (aa >> 7) & 7 : 0);
-                            uint64_t bd = ptx::smem_desc_sw128(b0 + kk * 32, 16, 1024);
-                            ptx::umma_bf16(d, ad, bd, idesc, first ? 0u : 1u);
+                            if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
                             first = 0;
                         }
                         ptx::umma_commit(emptyB + sb);
@@ -628,6 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
+    } else if (P.tma_out) {
+        conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
     } else {
         conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
     }
@@ -721,6 +814,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
+            const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), kABytes, 1024);
+            const uint64_t dB = Cfg::KB == 64 ? ptx::smem_desc_sw128(ptx::smem_u32(smem + kWgA), kABytes, 1024)
+                                              : ptx::smem_desc(ptx::smem_u32(smem + kWgA), 4096, 8 * Cfg::KB * 2, 6);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
             for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
@@ -733,16 +830,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int pt = p0; pt < p1; ++pt) {
                     ptx::mbar_wait(full + stage, phase);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(smem + stage * SB);
-                    const uint32_t b0 = a0 + kWgA;
+                    // MN-major SW128: 64-element MN chunks LBO = 16 KB apart, 8-row K groups SBO = 1 KB
+                    const uint32_t a0 = (uint32_t)dA + stage * (SB >> 4);
+                    const uint32_t b0 = (uint32_t)dB + stage * (SB >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        // MN-major SW128: 64-element MN chunks LBO = 16 KB apart, 8-row K groups SBO = 1 KB
-                        uint64_t ad = ptx::smem_desc_sw128(a0 + kk * 2048, kABytes, 1024);
-                        uint64_t bd = Cfg::KB == 64 ? ptx::smem_desc_sw128(b0 + kk * 2048, kABytes, 1024)
-                                                    : ptx::smem_desc(b0 + kk * 16 * Cfg::KB * 2, 4096, 8 * Cfg::KB * 2, 6);
-                        ptx::umma_bf16(d, ad, bd, idesc, (pt != p0 || kk != 0) ? 1u : 0u);
-                    }
+                    for (int kk = 0; kk < 8; ++kk)
+                        ptx::umma_bf16_lh(d, a0 + kk * 128, hiA, b0 + kk * (Cfg::KB == 64 ? 128 : 2 * Cfg::KB), hiB, idesc,
+                                          (pt != p0 || kk != 0) ? 1u : 0u);
                     ptx::umma_commit(empty + stage);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -890,7 +984,8 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
 }
 
 template <int BN>
-static bool launch_conv_halo(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, int tiles, cudaStream_t st) {
+static bool launch_conv_halo(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
+                             int tiles, cudaStream_t st) {
     using Cfg = HaloCfg<BN, 3>;
     static bool attr = false;
     if (!attr) {
@@ -900,7 +995,7 @@ static bool launch_conv_halo(const TcConv &P, const CUtensorMap &A, const CUtens
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_tc_halo<BN, 3><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, P);
+    k_conv_tc_halo<BN, 3><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, O, P);
     return true;
 }
 
@@ -922,28 +1017,37 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     P.dbg = dbg;
     P.in_base = in.base;
     static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
-    const int KC = (cin_p <= 16 && !(halo_on && P.halo_ok)) ? 16 : 64;   // small-channel layers: 16-ch chunks
+    const int KC = cin_p <= 16 ? 16 : 64;   // small-channel layers: 16-ch chunks
     P.cin_chunks = (cin_p + KC - 1) / KC;
     P.k_steps = P.ntaps * P.cin_chunks;
     P.n_tiles = (P.n_out + BN - 1) / BN;
     CUtensorMap A, Bm;
     if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN, KC)) return false;
-    if (halo_on && P.halo_ok) {
+    if (halo_on && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1) {
         P.TW = 8; P.TH = 16;
         P.tiles_x = (P.Wo + 7) / 8;
         P.tiles_y = (rows + 15) / 16;
         P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+        tile_div_init(P);
         P.boff = boff;
-        if (!encode_view(&A, in, P.B, kHaloPitch, 16 + P.k - 1)) return false;
+        if (!encode_view(&A, in, P.B, HaloGeom<3>::kPitch, HaloGeom<3>::kRows)) return false;
+        CUtensorMap O = A;
+        P.tma_out = 0;
+        if (P.mode == 0 && P.o_stride == 1 && P.out.Cp % 8 == 0) {
+            View ov = P.out;
+            ov.rows = P.out_b - P.out.base;
+            if (encode_view(&O, ov, P.B, 8, 16)) P.tma_out = 1;
+        }
         int tiles = P.m_tiles * P.n_tiles;
-        if (BN == 64) return launch_conv_halo<64>(P, A, Bm, tiles, st);
-        if (BN == 128) return launch_conv_halo<128>(P, A, Bm, tiles, st);
-        return launch_conv_halo<256>(P, A, Bm, tiles, st);
+        if (BN == 64) return launch_conv_halo<64>(P, A, Bm, O, tiles, st);
+        if (BN == 128) return launch_conv_halo<128>(P, A, Bm, O, tiles, st);
+        return launch_conv_halo<256>(P, A, Bm, O, tiles, st);
     }
     pick_tile(rows, P.Wo, P.a_mul, P.TW, P.TH);
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    tile_div_init(P);
     if (!encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC)) return false;
     // output map for the TMA-store epilogue (FP, unit output stride): rows end at out_b
     static const int tma_out = env_int("LRCNN_TMA_OUT", 1);
@@ -1007,10 +1111,12 @@ static bool conv_im2col(TcConv &P, const View &in, const void *w, int w_rows, cu
     if (rows <= 0 || P.Wo <= 0) return true;
     P.in = in;
     P.in_base = in.base;
+    P.dbg = env_int("LRCNN_TC_DBG", 0);
     pick_tile(rows, P.Wo, 1, P.TW, P.TH);
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    tile_div_init(P);
     CUtensorMap Bm, O;
     if (!encode_w2d(&Bm, w, w_rows, P.ntaps * 8, BN)) return false;
     View ov = P.out;
@@ -1078,7 +1184,7 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
             }
             P.ntaps = n;
             if (n == 0 || P.out_b <= P.out_a || P.Wo <= 0) continue;
-            P.k = k; P.pad = k - 1 - p; P.halo_ok = 0;
+            P.k = k; P.pad = k - 1 - p; P.halo_ok = s == 1 && k == 3;
             if (!conv_launch(P, a.dy, a.wt, a.dx.Cp, k * k, a.dy.Cp, st)) return false;
         }
     return true;

@@ -364,6 +364,11 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.gate = tin.relu; A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.a = a; A.b = b; A.B = B;
             A.ra = std::max(0, a * o.d.s - o.d.p);
             A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
+            // a non-overlapping pool whose input is band-internal with this pool as its only
+            // consumer and no delta carried in from band r+1 is the only writer of those rows
+            const int N = (int)S.E.size();
+            const bool carry_in = P.opts.mode == LRCNN_2PS && r + 1 < N && S.lo[r + 1][o.in_t] < S.a[r + 1][o.in_t];
+            A.acc = !(o.d.k == o.d.s && o.d.p == 0 && o.in_t != S.in_t && tin.cons.size() == 1 && !carry_in);
             ++P.launches;
             ProfScope ps(R, 2, 0, i * 8 + 5);
             CK(simt_pool_bwd(R.prec, A, R.st));

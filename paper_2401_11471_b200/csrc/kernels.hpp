@@ -59,6 +59,7 @@ struct PoolArgs {
     View in, out;              // fwd: out rows [a, b)
     View dy, dx, act;          // bwd: dy rows [a, b) of the pool output, dx rows [ra, rb)
     int gate, k, s, p, a, b, ra, rb, B;
+    int acc = 1;               // bwd: 1 = dx += ..., 0 = dx rows [ra, rb) are written, not read (single writer)
 };
 
 struct EltArgs {

@@ -144,62 +144,6 @@ __global__ void k_conv_wgrad(WgradArgs A) {
     }
 }
 
-// ------------------------------------------------------------------ bias / affine grads
-// db[c] += sum_pixels dy[p, c]  (BIAS);  AFFINE: dbeta[c] += sum dy, dgamma[c] += sum dy * c_raw
-// with c_raw = (t - beta - res)/gamma.  Block = (channel vectors of 8) x (pixel lanes);
-// coalesced 8-channel loads, per-thread partial sums, smem reduction over pixel lanes,
-// one fp32 atomicAdd per channel per block.
-template <typename T>
-__global__ void k_param_grad(ParamGradArgs A) {
-    // blockDim.x channel vectors (8 channels each) of group blockIdx.y; blockDim.y pixel lanes
-    const int CV = blockDim.x, cv = threadIdx.x, py = threadIdx.y, PY = blockDim.y;
-    const int rows = A.b - A.a, W = A.dy.W, c0 = (blockIdx.y * CV + cv) * 8;
-    const bool live = c0 < A.dy.Cp;
-    const long long npix = (long long)A.B * rows * W;
-    float s0[8], s1[8], gam[8], bet[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        s0[j] = 0.f; s1[j] = 0.f;
-        const bool in = A.epi == 2 && c0 + j < A.c_out;
-        gam[j] = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
-        bet[j] = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
-    }
-    for (long long q = (long long)blockIdx.x * PY + py; live && q < npix; q += (long long)gridDim.x * PY) {
-        int x = q % W;
-        long long r = q / W;
-        int y = A.a + (int)(r % rows);
-        int b = (int)(r / rows);
-        const T *dp = (const T *)A.dy.p + voff(A.dy, b, y, x) + c0;
-        float d[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { d[j] = ldf(dp + j); s0[j] += d[j]; }
-        if (A.epi == 2) {
-            const T *tp = (const T *)A.t.p + voff(A.t, b, y, x) + c0;
-            const T *rp = A.res.p ? (const T *)A.res.p + voff(A.res, b, y, x) + c0 : nullptr;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float t = ldf(tp + j) - (rp ? ldf(rp + j) : 0.f);
-                s1[j] += d[j] * (t - bet[j]) / gam[j];
-            }
-        }
-    }
-    extern __shared__ float red[];   // [PY][CV*8] x 2
-    float *r0 = red, *r1 = red + PY * CV * 8;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) { r0[py * CV * 8 + cv * 8 + j] = s0[j]; r1[py * CV * 8 + cv * 8 + j] = s1[j]; }
-    __syncthreads();
-    for (int c = py * CV + cv; c < CV * 8; c += PY * CV) {
-        float a0 = 0.f, a1 = 0.f;
-        for (int k = 0; k < PY; ++k) { a0 += r0[k * CV * 8 + c]; a1 += r1[k * CV * 8 + c]; }
-        const int ch = blockIdx.y * CV * 8 + c;
-        if (ch < A.c_out) {
-            if (A.epi == 1) atomicAdd(A.db + ch, a0);
-            else { atomicAdd(A.db + ch, a1); atomicAdd(A.dbeta + ch, a0); }
-        }
-    }
-}
-
-// ------------------------------------------------------------------ 2x2/s2 max-pool (VGG), 8 channels per thread
 template <typename T>
 __device__ __forceinline__ void ld8(const T *p, float (&v)[8]) {
 #pragma unroll
@@ -224,66 +168,139 @@ __device__ __forceinline__ void st8(bf16 *p, const float (&v)[8]) {
     *reinterpret_cast<uint4 *>(p) = u;
 }
 
+// ------------------------------------------------------------------ bias / affine grads
+// db[c] += sum_pixels dy[p, c]  (BIAS);  AFFINE: dbeta[c] += sum dy, dgamma[c] += sum dy * c_raw
+// with c_raw = (t - beta - res)/gamma.  Block = (channel vectors of 8) x (pixel lanes);
+// coalesced 8-channel loads, per-thread partial sums, smem reduction over pixel lanes,
+// one fp32 atomicAdd per channel per block.
+template <typename T>
+__global__ void k_param_grad(ParamGradArgs A) {
+    // blockDim.x channel vectors (8 channels each) of group blockIdx.y; blockDim.y pixel lanes
+    const int CV = blockDim.x, cv = threadIdx.x, py = threadIdx.y, PY = blockDim.y;
+    const int rows = A.b - A.a, W = A.dy.W, c0 = (blockIdx.y * CV + cv) * 8;
+    const bool live = c0 < A.dy.Cp;
+    const int RW = rows * W;                        // band pixels per image (contiguous rows)
+    float s0[8], s1[8], gam[8], bet[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        s0[j] = 0.f; s1[j] = 0.f;
+        const bool in = A.epi == 2 && c0 + j < A.c_out;
+        gam[j] = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
+        bet[j] = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
+    }
+    // pixel q = b * RW + p walks with stride S; (b, p) updated without division
+    const int S = gridDim.x * PY;
+    const int q0 = blockIdx.x * PY + py;
+    int b = q0 / RW, p = q0 - b * RW;
+    const T *dbase = (const T *)A.dy.p + voff(A.dy, 0, A.a, 0) + c0;
+    const T *tbase = A.epi == 2 ? (const T *)A.t.p + voff(A.t, 0, A.a, 0) + c0 : nullptr;
+    const T *rbase = A.epi == 2 && A.res.p ? (const T *)A.res.p + voff(A.res, 0, A.a, 0) + c0 : nullptr;
+    while (live && b < A.B) {
+        // up to 4 independent pixels per iteration (loads in flight)
+        long long po[4], pt[4], pr[4];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (b < A.B) {
+                po[u] = (long long)b * A.dy.bs + (long long)p * A.dy.Cp;
+                pt[u] = (long long)b * A.t.bs + (long long)p * A.t.Cp;
+                pr[u] = (long long)b * A.res.bs + (long long)p * A.res.Cp;
+                ++cnt;
+                p += S;
+                while (p >= RW) { p -= RW; ++b; }
+            }
+        }
+        float d[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (u < cnt) ld8(dbase + po[u], d[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (u >= cnt) break;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s0[j] += d[u][j];
+            if (A.epi == 2) {
+                float t[8], rr[8];
+                ld8(tbase + pt[u], t);
+                if (rbase) ld8(rbase + pr[u], rr);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s1[j] += d[u][j] * ((t[j] - (rbase ? rr[j] : 0.f)) - bet[j]) / gam[j];
+            }
+        }
+    }
+    extern __shared__ float red[];   // [PY][CV*8] x 2
+    float *r0 = red, *r1 = red + PY * CV * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { r0[py * CV * 8 + cv * 8 + j] = s0[j]; r1[py * CV * 8 + cv * 8 + j] = s1[j]; }
+    __syncthreads();
+    for (int c = py * CV + cv; c < CV * 8; c += PY * CV) {
+        float a0 = 0.f, a1 = 0.f;
+        for (int k = 0; k < PY; ++k) { a0 += r0[k * CV * 8 + c]; a1 += r1[k * CV * 8 + c]; }
+        const int ch = blockIdx.y * CV * 8 + c;
+        if (ch < A.c_out) {
+            if (A.epi == 1) atomicAdd(A.db + ch, a0);
+            else { atomicAdd(A.db + ch, a1); atomicAdd(A.dbeta + ch, a0); }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 2x2/s2 max-pool (VGG), 8 channels per thread
 // window order (0,0),(0,1),(1,0),(1,1) = raster order; strict '>' keeps the first maximum
+// grid: x = (output column, channel vector) chunks of one output row, y = (image, row) of the band
 template <typename T>
 __global__ void k_pool2_fwd(PoolArgs A) {
     const int CV = A.out.Cp / 8, Wo = A.out.W, rows = A.b - A.a;
-    long long n = (long long)A.B * rows * Wo * CV;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
-         idx += (long long)gridDim.x * blockDim.x) {
-        int cv = idx % CV;
-        long long r = idx / CV;
-        int x = r % Wo; r /= Wo;
-        int y = A.a + (int)(r % rows);
-        int b = (int)(r / rows);
-        float best[8], v[8];
-        ld8((const T *)A.in.p + voff(A.in, b, 2 * y, 2 * x) + cv * 8, best);
-        const int dy[3] = {0, 1, 1}, dx[3] = {1, 0, 1};
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Wo * CV) return;
+    const int x = i / CV, cv = i - x * CV;
+    const int b = blockIdx.y / rows, y = A.a + (int)(blockIdx.y - b * rows);
+    const T *ip = (const T *)A.in.p + voff(A.in, b, 2 * y, 2 * x) + cv * 8;
+    const long long rs = (long long)A.in.W * A.in.Cp;
+    float best[8], v[8];
+    ld8(ip, best);
+    const long long off[3] = {A.in.Cp, rs, rs + A.in.Cp};
 #pragma unroll
-        for (int w = 0; w < 3; ++w) {
-            ld8((const T *)A.in.p + voff(A.in, b, 2 * y + dy[w], 2 * x + dx[w]) + cv * 8, v);
+    for (int w = 0; w < 3; ++w) {
+        ld8(ip + off[w], v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) best[j] = v[j] > best[j] ? v[j] : best[j];
-        }
-        st8((T *)A.out.p + voff(A.out, b, y, x) + cv * 8, best);
+        for (int j = 0; j < 8; ++j) best[j] = v[j] > best[j] ? v[j] : best[j];
     }
+    st8((T *)A.out.p + voff(A.out, b, y, x) + cv * 8, best);
 }
 
 template <typename T>
 __global__ void k_pool2_bwd(PoolArgs A) {
     const int CV = A.dy.Cp / 8, Wo = A.dy.W, rows = A.b - A.a;
-    long long n = (long long)A.B * rows * Wo * CV;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
-         idx += (long long)gridDim.x * blockDim.x) {
-        int cv = idx % CV;
-        long long r = idx / CV;
-        int x = r % Wo; r /= Wo;
-        int y = A.a + (int)(r % rows);
-        int b = (int)(r / rows);
-        float d[8], v[4][8], best[8];
-        int arg[8];
-        ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Wo * CV) return;
+    const int x = i / CV, cv = i - x * CV;
+    const int b = blockIdx.y / rows, y = A.a + (int)(blockIdx.y - b * rows);
+    float d[8], v[4][8], best[8];
+    int arg[8];
+    ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
+    const T *ap = (const T *)A.act.p + voff(A.act, b, 2 * y, 2 * x) + cv * 8;
+    T *dp0 = (T *)A.dx.p + voff(A.dx, b, 2 * y, 2 * x) + cv * 8;
+    const long long ars = (long long)A.act.W * A.act.Cp, drs = (long long)A.dx.W * A.dx.Cp;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) ld8((const T *)A.act.p + voff(A.act, b, 2 * y + (w >> 1), 2 * x + (w & 1)) + cv * 8, v[w]);
+    for (int w = 0; w < 4; ++w) ld8(ap + (w >> 1) * ars + (w & 1) * A.act.Cp, v[w]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        best[j] = v[0][j]; arg[j] = 0;
+#pragma unroll
+        for (int w = 1; w < 4; ++w)
+            if (v[w][j] > best[j]) { best[j] = v[w][j]; arg[j] = w; }
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        T *dp = dp0 + (w >> 1) * drs + (w & 1) * A.dx.Cp;
+        float o[8];
+        if (A.acc) ld8(dp, o);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            best[j] = v[0][j]; arg[j] = 0;
-#pragma unroll
-            for (int w = 1; w < 4; ++w)
-                if (v[w][j] > best[j]) { best[j] = v[w][j]; arg[j] = w; }
+            o[j] = (A.acc ? o[j] : 0.f) + (arg[j] == w ? d[j] : 0.f);
+            if (A.gate && !(v[w][j] > 0.f)) o[j] = 0.f;
         }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            T *dp = (T *)A.dx.p + voff(A.dx, b, 2 * y + (w >> 1), 2 * x + (w & 1)) + cv * 8;
-            float o[8];
-            ld8(dp, o);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                o[j] += arg[j] == w ? d[j] : 0.f;
-                if (A.gate && !(v[w][j] > 0.f)) o[j] = 0.f;
-            }
-            st8(dp, o);
-        }
+        st8(dp, o);
     }
 }
 
@@ -680,13 +697,16 @@ cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     if (prec) k_param_grad<bf16><<<grid, blk, shm, st>>>(a); else k_param_grad<float><<<grid, blk, shm, st>>>(a);
     return cudaGetLastError();
 }
-static bool pool2(const PoolArgs &a, const View &v) { return a.k == 2 && a.s == 2 && a.p == 0 && v.Cp % 8 == 0; }
+static bool pool2(const PoolArgs &a, const View &v) {
+    return a.k == 2 && a.s == 2 && a.p == 0 && v.Cp % 8 == 0 && (long long)a.B * (a.b - a.a) <= 65535;
+}
 cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b - a.a) * a.out.W * a.out.Cp;
     if (n <= 0) return cudaSuccess;
     if (pool2(a, a.out)) {
-        n /= 8;
-        if (prec) k_pool2_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool2_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+        const int rowv = a.out.W * (a.out.Cp / 8);
+        dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
+        if (prec) k_pool2_fwd<bf16><<<g, kT, 0, st>>>(a); else k_pool2_fwd<float><<<g, kT, 0, st>>>(a);
     } else if (a.out.Cp % 8 == 0) {
         n /= 8;
         if (prec) k_pool_fwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd8<float><<<grid_for(n), kT, 0, st>>>(a);
@@ -699,8 +719,10 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
     if (n <= 0) return cudaSuccess;
     if (pool2(a, a.dy)) {
-        long long m = (long long)a.B * (a.b - a.a) * a.dy.W * (a.dy.Cp / 8);
-        if (prec) k_pool2_bwd<bf16><<<grid_for(m), kT, 0, st>>>(a); else k_pool2_bwd<float><<<grid_for(m), kT, 0, st>>>(a);
+        if (a.b <= a.a) return cudaSuccess;
+        const int rowv = a.dy.W * (a.dy.Cp / 8);
+        dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
+        if (prec) k_pool2_bwd<bf16><<<g, kT, 0, st>>>(a); else k_pool2_bwd<float><<<g, kT, 0, st>>>(a);
     } else if (a.dx.Cp % 8 == 0) {
         n /= 8;
         if (prec) k_pool_bwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd8<float><<<grid_for(n), kT, 0, st>>>(a);
