@@ -894,6 +894,176 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ wgrad, row halo (stride 1)
+// One work item = (co tile of 128, filter row ky, ci tile of BN, pixel split); its k taps
+// kx = 0..k-1 accumulate in k TMEM accumulators (k * BN columns).  Per pixel tile (TW x TH
+// output pixels, TW a multiple of 16) the band delta is loaded once (two 64-channel MN-major
+// boxes, K = pixels in raster order) and the input once as a halo box of (TW+k-1) x TH pixels
+// (row pitch TW+k-1) per 64-channel chunk.  The B operand of K-step j (16 pixels = output
+// row r, columns c..c+15) for tap kx starts at box row r*(TW+k-1) + c + kx: every MMA gets its
+// own start, so one box serves all k taps (the absolute-address SWIZZLE_128B pattern makes an
+// arbitrary 128-byte row start valid).  Traffic per pixel tile: 32 KB delta + (BN/64) boxes of
+// (TW+k-1)*TH*128 B, for 8k MMAs; the per-tap kernel loads 32 KB + BN*256 B for 8 MMAs.
+struct WgHaloCfg {
+    static constexpr int kBoxMax = ((144 * 128 + 1023) / 1024) * 1024;   // (TW+k-1)*TH <= 144 rows (k = 3)
+};
+template <int BN, int KW>
+struct WgHCfg {
+    static constexpr int kXBox = WgHaloCfg::kBoxMax;
+    static constexpr int kStageBytes = kWgA + (BN / 64) * kXBox;
+    static constexpr int kStages = (224 * 1024) / kStageBytes > 8 ? 8 : (224 * 1024) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr uint32_t kTmemCols = KW * BN <= 32 ? 32 : KW * BN <= 64 ? 64 : KW * BN <= 128 ? 128 : KW * BN <= 256 ? 256 : 512;
+};
+
+__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+template <int BN, int KW>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad_halo(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
+    using Cfg = WgHCfg<BN, KW>;
+    constexpr int S = Cfg::kStages;
+    constexpr int SB = Cfg::kStageBytes;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + S * SB);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = (uint32_t *)(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        ptx::mbar_init(tfull, 1);
+        ptx::mbar_init(tempty, 4);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmD);
+        ptx::prefetch_tmap(&tmX);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, Cfg::kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int XP = P.TW + KW - 1;                  // halo box row pitch (pixels)
+    const uint32_t xbytes = (uint32_t)XP * P.TH * 128;
+
+    auto decode = [&](int item, int &cot, int &ky, int &cit, int &split) {
+        split = item % P.splits;
+        int r = item / P.splits;
+        cit = r % P.ci_tiles; r /= P.ci_tiles;
+        ky = r % KW;
+        cot = r / KW;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                int cot, ky, cit, split;
+                decode(item, cot, ky, cit, split);
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                for (int pt = p0; pt < p1; ++pt) {
+                    const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                    const int y0 = P.out_a + ty * P.TH, x0 = tx * P.TW;
+                    ptx::mbar_wait(empty + stage, phase ^ 1);
+                    uint8_t *st = smem + stage * SB;
+                    ptx::mbar_arrive_expect_tx(full + stage, kWgA + (BN / 64) * xbytes);
+                    ptx::tma_load_4d(st, &tmD, full + stage, cot * 128, x0, y0 - P.dy_base, b);
+                    ptx::tma_load_4d(st + kABytes, &tmD, full + stage, cot * 128 + 64, x0, y0 - P.dy_base, b);
+#pragma unroll
+                    for (int h = 0; h < BN / 64; ++h)
+                        ptx::tma_load_4d(st + kWgA + h * Cfg::kXBox, &tmX, full + stage, cit * BN + h * 64, x0 - P.pad,
+                                         y0 - P.pad + ky - P.x_base, b);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
+            const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), kABytes, 1024);
+            const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(smem + kWgA), Cfg::kXBox, 1024);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            // B start (in 16-byte units) of K-step j relative to the box: row r*XP + c
+            uint32_t joff[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int px = 16 * j, r = px / P.TW, c = px - r * P.TW;
+                joff[j] = (uint32_t)(r * XP + c) * 8;
+            }
+            int stage = 0;
+            uint32_t phase = 0, tphase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                int cot, ky, cit, split;
+                decode(item, cot, ky, cit, split);
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                ptx::mbar_wait(tempty, tphase ^ 1);
+                ptx::tc_fence_after();
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = (uint32_t)dA + stage * (SB >> 4);
+                    const uint32_t b0 = (uint32_t)dB + stage * (SB >> 4);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+#pragma unroll
+                        for (int kx = 0; kx < KW; ++kx)
+                            ptx::umma_bf16_lh(tmem + kx * BN, a0 + j * 128, hiA, b0 + joff[j] + kx * 8, hiB, idesc,
+                                              (pt != p0 || j != 0) ? 1u : 0u);
+                    ptx::umma_commit(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(tfull);
+                tphase ^= 1;
+            }
+        }
+    } else {
+        const int ew = warp & 3;
+        const int m = ew * 32 + lane;
+        const int taps = KW * KW;
+        uint32_t tphase = 0;
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int cot, ky, cit, split;
+            decode(item, cot, ky, cit, split);
+            const int co = cot * 128 + m;
+            const float gsc = (P.gamma && co < P.c_out) ? __bfloat162float(P.gamma[co]) : 1.f;
+            ptx::mbar_wait(tfull, tphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int kx = 0; kx < KW; ++kx) {
+                float *dst = P.dw + ((long long)co * taps + ky * KW + kx) * P.cin_p + cit * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + kx * BN + c * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (co >= P.c_out) continue;
+                    const int ci0 = cit * BN + c * 32;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        if (ci0 + j < P.cin_p)
+                            red_add_v4(dst + c * 32 + j, __uint_as_float(v[j]) * gsc, __uint_as_float(v[j + 1]) * gsc,
+                                       __uint_as_float(v[j + 2]) * gsc, __uint_as_float(v[j + 3]) * gsc);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty);
+            tphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1204,12 +1374,66 @@ static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorM
     return true;
 }
 
+template <int BN, int KW>
+static bool launch_wgrad_halo(const TcWgrad &P, const CUtensorMap &D, const CUtensorMap &X, cudaStream_t st) {
+    using Cfg = WgHCfg<BN, KW>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_wgrad_halo<BN, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+            cudaSuccess)
+            return false;
+        attr = true;
+    }
+    int grid = P.items < num_sms() ? P.items : num_sms();
+    k_wgrad_halo<BN, KW><<<grid, kThreads, Cfg::kSmem, st>>>(D, X, P);
+    return true;
+}
+
+// stride-1 3x3 wgrad with input channels in 64-multiples through the row-halo kernel
+static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
+    static const int on = env_int("LRCNN_WG_HALO", 1);
+    const View &dy = a.dy, &x = a.x;
+    if (!on || a.s != 1 || a.k != 3 || x.Cp % 64) return false;
+    const int rows = a.b - a.a;
+    TcWgrad P{};
+    P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
+    P.s = 1;
+    // 128-pixel tile, TW a multiple of 16 (one K-step = 16 pixels of one output row)
+    long best = -1;
+    for (int tw = 128; tw >= 16; tw >>= 1) {
+        const int th = 128 / tw;
+        long cost = (long)((dy.W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+        if (best < 0 || cost < best) { best = cost; P.TW = tw; P.TH = th; }
+    }
+    if ((P.TW + a.k - 1) * P.TH > 144) return false;
+    P.tiles_x = (dy.W + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
+    const int BN = x.Cp >= 128 ? 128 : 64;
+    P.co_tiles = (dy.Cp + 127) / 128;
+    P.ci_tiles = (x.Cp + BN - 1) / BN;
+    const int base_items = P.co_tiles * a.k * P.ci_tiles;
+    int splits = (num_sms() + base_items - 1) / base_items;
+    if (splits > P.pix_tiles) splits = P.pix_tiles;
+    if (splits < 1) splits = 1;
+    P.per_split = (P.pix_tiles + splits - 1) / splits;
+    P.splits = (P.pix_tiles + P.per_split - 1) / P.per_split;
+    P.items = base_items * P.splits;
+    P.out_a = a.a; P.dy_base = dy.base; P.x_base = x.base;
+    CUtensorMap D, X;
+    if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
+    if (!encode_view(&X, x, a.B, P.TW + a.k - 1, P.TH)) return false;
+    if (BN == 64) return launch_wgrad_halo<64, 3>(P, D, X, st);
+    return launch_wgrad_halo<128, 3>(P, D, X, st);
+}
+
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     if (a.s < 1 || a.s > 2) return false;
     const View &dy = a.dy, &x = a.x;
     if (dy.Cp % 8 || x.Cp % 8 || !aligned16(dy.p) || !aligned16(x.p)) return false;
     const int rows = a.b - a.a;
     if (rows <= 0) return true;
+    if (wgrad_halo(a, st)) return true;
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = a.s;
