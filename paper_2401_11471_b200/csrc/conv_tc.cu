@@ -53,6 +53,7 @@ struct TcConv {
     // stride a_mul), weights tap index tap_w[t]; output pixel = (o_row0 + o_stride*grid_row, ...)
     int a_mul, ntaps, o_row0, o_col0, o_stride, halo_ok;
     int tma_out;           // FP: stage the output tile in smem and TMA-store it
+    int tma_dg;            // dgrad: TMA-load delta (+ activation), combine in smem, TMA-store
     int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
     int tw_log2;           // TW = 1 << tw_log2
@@ -106,7 +107,7 @@ struct ConvCfg {
     static constexpr int kA = 128 * KC * 2, kB = BN * KC * 2;
     static constexpr int kStageBytes = kA + kB;
     static constexpr int kStages = kStageBudget / kStageBytes > 16 ? 16 : kStageBudget / kStageBytes;
-    static constexpr int kSmem = kStages * kStageBytes + 2 * kOutStage + 1024 + 256;
+    static constexpr int kSmem = kStages * kStageBytes + 2 * kOutStage + 1024 + 512;
     static constexpr uint32_t kTmemCols = 2 * BN;
 };
 
@@ -126,6 +127,13 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -264,6 +272,85 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
     if (leader) bulk_wait_all();
 }
 
+// dgrad epilogue through TMA (unit output stride): per 64-channel group the delta tile of the
+// conv input (and, when its producer applies ReLU, the activation tile) is TMA-loaded into
+// smem, combined with the accumulator (gate-on-write: delta = gate(act) * (delta + acc)) in
+// place and TMA-stored back; rows >= out_b / columns >= W are clipped by the maps.
+template <int BN>
+__device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
+                                                     uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
+                                                     uint8_t *stage_out, uint64_t *ebar, int warp, int lane) {
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    const int q = warp & 3, m = q * 32 + lane;
+    const bool leader = (warp == 2 && lane == 0);
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    uint8_t *bufD = stage_out, *bufG = stage_out + kOutStage;
+    const uint32_t rowD = ptx::smem_u32(bufD) + m * 128, rowG = ptx::smem_u32(bufG) + m * 128;
+    const uint32_t ebytes = P.gate ? 2 * kOutStage : kOutStage;
+    int acc = 0;
+    uint32_t aphase = 0, ephase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
+        const int ngrp = min(BN / 64, (P.n_out - n0 + 63) / 64);
+        if (leader) {
+            bulk_wait_read0();
+            ptx::mbar_arrive_expect_tx(ebar, ebytes);
+            ptx::tma_load_4d(bufD, tmO, ebar, n0, xg0, yg0 - P.out.base, b);
+            if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, n0, xg0, yg0 - P.act.base, b);
+        }
+        ptx::mbar_wait(tfull + acc, aphase);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int grp = 0; grp < ngrp; ++grp) {
+            const int nb = n0 + grp * 64;
+            uint32_t v[64];
+            ptx::tmem_ld32(tq + acc * BN + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+            ptx::tmem_ld32(tq + acc * BN + grp * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            ptx::tmem_ld_wait();
+            ptx::mbar_wait(ebar, ephase);
+            ephase ^= 1;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
+                const uint4 dd = ld_shared_v4(rowD + off);
+                const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
+                const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    float x0 = __uint_as_float(v[c * 8 + 2 * h]) + bf_lo(dw[h]);
+                    float x1 = __uint_as_float(v[c * 8 + 2 * h + 1]) + bf_hi(dw[h]);
+                    if (P.gate) {
+                        if (!(bf_lo(gw[h]) > 0.f)) x0 = 0.f;
+                        if (!(bf_hi(gw[h]) > 0.f)) x1 = 0.f;
+                    }
+                    o[h] = pack2(x0, x1);
+                }
+                st_shared_v4(rowD + off, make_uint4(o[0], o[1], o[2], o[3]));
+            }
+            fence_async_smem();
+            epi_bar();
+            if (leader) {
+                tma_store_4d(tmO, bufD, nb, xg0, yg0 - P.out.base, b);
+                bulk_commit();
+                if (grp + 1 < ngrp) {   // next group: wait until the store has read bufD, then reload
+                    bulk_wait_read0();
+                    ptx::mbar_arrive_expect_tx(ebar, ebytes);
+                    ptx::tma_load_4d(bufD, tmO, ebar, nb + 64, xg0, yg0 - P.out.base, b);
+                    if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, nb + 64, xg0, yg0 - P.act.base, b);
+                }
+            }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (leader) bulk_wait_all();
+}
+
 // Epilogue warps (4 warps = 128 TMEM lanes = 128 pixels of the tile): tcgen05.ld the
 // accumulator in 32-column chunks, apply the fused epilogue, 16-byte bf16 stores.
 template <int BN>
@@ -356,7 +443,7 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
 template <int BN, int KC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmO, const TcConv P) {
+              const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
     using Cfg = ConvCfg<BN, KC>;
     constexpr int S = Cfg::kStages;
     constexpr int ABYTES = Cfg::kA, BBYTES = Cfg::kB;
@@ -371,12 +458,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tslot = (uint32_t *)(tempty + 2);
+    uint64_t *ebar = tempty + 2;
+    uint32_t *tslot = (uint32_t *)(ebar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
+        ptx::mbar_init(ebar, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -436,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         if (P.tma_out) conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
+        else if (P.tma_dg) conv_epilogue_tma_dg<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
     }
     ptx::tc_fence_before();
@@ -1139,8 +1229,8 @@ static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 bool tc_available() { return true; }
 
 template <int BN, int KC>
-static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O, int tiles,
-                        cudaStream_t st) {
+static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
+                        const CUtensorMap &G, int tiles, cudaStream_t st) {
     using Cfg = ConvCfg<BN, KC>;
     static bool attr = false;
     if (!attr) {
@@ -1149,7 +1239,7 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_tc<BN, KC><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, O, P);
+    k_conv_tc<BN, KC><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, O, G, P);
     return true;
 }
 
@@ -1180,9 +1270,16 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
                         cudaStream_t st) {
     if (in.Cp % 8 || cin_p != in.Cp || P.n_out < 8 || P.n_out % 8 || P.ntaps < 1 || P.ntaps > 49) return false;
     if (!aligned16(in.p) || !aligned16(w) || !aligned16(P.out.p)) return false;
-    const int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
+    int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
     const int rows = P.out_b - P.out_a;
     if (rows <= 0 || P.Wo <= 0) return true;
+    {   // small launches (deep layers, thin bands): narrower N tiles so that every SM gets work
+        static const int adapt = env_int("LRCNN_BN_ADAPT", 0);
+        int tw = 8, th = 16;
+        if (!(env_int("LRCNN_HALO", 0) && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1)) pick_tile(rows, P.Wo, P.a_mul, tw, th);
+        const long mt = (long)P.B * ((P.Wo + tw - 1) / tw) * ((rows + th - 1) / th);
+        while (adapt && BN > 64 && mt * ((P.n_out + BN - 1) / BN) < num_sms()) BN >>= 1;
+    }
     static const int dbg = env_int("LRCNN_TC_DBG", 0);
     P.dbg = dbg;
     P.in_base = in.base;
@@ -1228,15 +1325,25 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         ov.rows = P.out_b - P.out.base;
         if (encode_view(&O, ov, P.B, P.TW, P.TH)) P.tma_out = 1;
     }
+    // dgrad with unit output stride: TMA load / combine / store of the delta tile
+    static const int tma_dg = env_int("LRCNN_TMA_DG", 1);
+    CUtensorMap G = A;
+    P.tma_dg = 0;
+    if (tma_dg && P.mode == 1 && P.o_stride == 1 && P.out.Cp % 64 == 0 && P.n_out == P.out.Cp &&
+        (!P.gate || (P.act.Cp == P.out.Cp && aligned16(P.act.p)))) {
+        View ov = P.out;
+        ov.rows = P.out_b - P.out.base;
+        if (encode_view(&O, ov, P.B, P.TW, P.TH) && (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH))) P.tma_dg = 1;
+    }
     int tiles = P.m_tiles * P.n_tiles;
     if (KC == 16) {
-        if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, tiles, st);
-        if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, tiles, st);
-        return launch_conv<256, 16>(P, A, Bm, O, tiles, st);
+        if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, G, tiles, st);
+        if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, G, tiles, st);
+        return launch_conv<256, 16>(P, A, Bm, O, G, tiles, st);
     }
-    if (BN == 64) return launch_conv<64, 64>(P, A, Bm, O, tiles, st);
-    if (BN == 128) return launch_conv<128, 64>(P, A, Bm, O, tiles, st);
-    return launch_conv<256, 64>(P, A, Bm, O, tiles, st);
+    if (BN == 64) return launch_conv<64, 64>(P, A, Bm, O, G, tiles, st);
+    if (BN == 128) return launch_conv<128, 64>(P, A, Bm, O, G, tiles, st);
+    return launch_conv<256, 64>(P, A, Bm, O, G, tiles, st);
 }
 
 // weights [rows][K] (K = taps * 8, the OHWI layout of an 8-channel input) as a 2D map with
