@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--band-rows", type=int, default=0)
     ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
+    ap.add_argument("--no-balanced", action="store_true",
+                    help="same band count in every segment (default: balanced bands, LRCNN_FLAG_BALANCED_BANDS)")
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
     ap.add_argument("--parallel", default="dp", choices=["dp", "rows"],
                     help="N>1: dp = each rank its own batch, wgrad all-reduce (weak scaling); rows = the "
@@ -205,7 +207,7 @@ def main():
 
     net = make_net(a)
     B = a.batch or CONFIGS[a.config][3]
-    flags = LB.FLAG_NO_TCGEN05 if a.simt else 0
+    flags = (LB.FLAG_NO_TCGEN05 if a.simt else 0) | (0 if a.no_balanced else LB.FLAG_BALANCED_BANDS)
     kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}
     if a.mode == "column":
         kw = {}
@@ -363,6 +365,7 @@ def main():
                           "parallelism": ("rows%d (row sharding, NCCL halo exchange + all-reduce)" % world if rows
                                           else "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU"),
                           "mode": a.mode, "segments": a.segments, "bands": kw,
+                          "bands_per_segment": [plan.seg(si)[2] for si in range(plan.nsegs())],
                           "l2": "flushed (512 MB write) between timed steps"},
                "clocks": clocks,
                "e2e": {"value": gb / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": xi_bytes + lab_bytes,

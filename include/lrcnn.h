@@ -108,6 +108,12 @@ typedef struct {
 
 #define LRCNN_FLAG_ALLOW_OVERLAP_EXHAUSTION 1  /* OverL: do not reject N > H/o^0 */
 #define LRCNN_FLAG_NO_TCGEN05 2                /* bf16: use the SIMT kernels only (tests)     */
+/* Balanced bands (budget-driven N per segment; "max H^L then
+ * min N"): n_bands / band_rows fixes the band working set of the segment that needs the most;
+ * every other segment uses the smallest band count whose working set (activation + delta +
+ * carry buffers, overlaid across segments) fits in that same budget.  Peak memory is unchanged,
+ * thin deep segments get fewer, larger bands (fewer halo rows, larger kernel launches). */
+#define LRCNN_FLAG_BALANCED_BANDS 4
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 

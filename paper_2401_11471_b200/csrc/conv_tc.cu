@@ -1154,6 +1154,175 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ wgrad of 8-channel-input convs (im2col)
+// dW[co][tap][ci] = sum_pixels dY[p][co] X[p + off(tap)][ci] for the padded RGB layer:
+// D[m = (tap - 16*mt)*8 + ci][co] (M = 128 = 16 taps x 8 channels, N = c_out) accumulates over
+// K = output pixels.  Per 128-pixel tile the A operand (M-major: per pixel 16 taps x 16 bytes in
+// two 64-element chunks, SWIZZLE_128B) is gathered by 8 warps with 16-byte loads exactly as the
+// FP im2col kernel does; the band delta is one TMA box per tile (MN-major B).
+struct TcWgI2c {
+    View in;
+    float *dw;
+    const bf16 *gamma;
+    int ntaps, mtiles, a_mul, c_out;
+    int tap_oy[49], tap_ox[49];
+    int TW, TH, tw_log2, tiles_x, tiles_y, pix_tiles, per_split, splits, items;
+    int out_a, out_b, Wo, dy_base;
+};
+static constexpr int kWiStages = 4;
+static constexpr int kWiStage = 2 * 16384 + 16384;                 // A: 2 chunks x 16 KB, B: 16 KB
+static constexpr int kWiSmem = kWiStages * kWiStage + 1024 + 256;
+
+template <int BN>
+__global__ void __launch_bounds__(kI2cThreads - 4 * 32, 1)
+    k_wgrad_im2col(const __grid_constant__ CUtensorMap tmD, const TcWgI2c P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + kWiStages * kWiStage);
+    uint64_t *empty = full + kWiStages;
+    uint64_t *tfull = empty + kWiStages;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = (uint32_t *)(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kMma = kI2cGather;                  // warp 8; epilogue warps 9..12
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kWiStages; ++i) { ptx::mbar_init(full + i, kI2cGather * 32 + 1); ptx::mbar_init(empty + i, 1); }
+        ptx::mbar_init(tfull, 1);
+        ptx::mbar_init(tempty, 4);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmD);
+    }
+    if (warp == kMma) ptx::tmem_alloc(tslot, BN < 32 ? 32 : BN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int twm = (1 << P.tw_log2) - 1;
+
+    if (warp < kI2cGather) {
+        const int c = threadIdx.x & 7, pg = threadIdx.x >> 3;
+        const View &in = P.in;
+        const int W = in.W;
+        const int ylo = max(0, in.base), yhi = min(in.H, in.base + in.rows);
+        const uint4 *src = (const uint4 *)in.p;
+        const uint32_t a_base = ptx::smem_u32(smem);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            const int split = item % P.splits, mt = item / P.splits;
+            const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+            // this thread's two taps of the m tile (chunk h = taps 16 mt + 8 h .. + 8)
+            int dy2[2], dx2[2];
+            bool tv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int tap = mt * 16 + h * 8 + c;
+                tv[h] = tap < P.ntaps;
+                dy2[h] = tv[h] ? P.tap_oy[tap] : 0;
+                dx2[h] = tv[h] ? P.tap_ox[tap] : 0;
+            }
+            for (int pt = p0; pt < p1; ++pt) {
+                const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                uint4 v[2][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int m = pg + 32 * i;
+                    const int yo = P.out_a + ty * P.TH + (m >> P.tw_log2), xo = tx * P.TW + (m & twm);
+                    const bool valid = yo < P.out_b && xo < P.Wo;
+                    const int yi = yo * P.a_mul, xi = xo * P.a_mul;
+                    const uint4 *pp = src + (long long)b * (in.bs >> 3) + (long long)(yi - in.base) * W + xi;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int iy = yi + dy2[h], ix = xi + dx2[h];
+                        v[h][i] = make_uint4(0, 0, 0, 0);
+                        if (valid && tv[h] && iy >= ylo && iy < yhi && ix >= 0 && ix < W)
+                            v[h][i] = __ldg(pp + dy2[h] * W + dx2[h]);
+                    }
+                }
+                ptx::mbar_wait(empty + stage, phase ^ 1);
+                uint8_t *st = smem + stage * kWiStage;
+                if (threadIdx.x == 0) {
+                    ptx::mbar_arrive_expect_tx(full + stage, 16384);
+                    ptx::tma_load_4d(st + 2 * 16384, &tmD, full + stage, 0, tx * P.TW, P.out_a + ty * P.TH - P.dy_base, b);
+                }
+                const uint32_t sa = a_base + stage * kWiStage;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int m = pg + 32 * i;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) st_shared_v4(sa + h * 16384 + m * 128 + ((c ^ (m & 7)) << 4), v[h][i]);
+                }
+                fence_async_smem();
+                ptx::mbar_arrive(full + stage);
+                if (++stage == kWiStages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == kMma) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
+            const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), 16384, 1024);
+            const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(smem + 2 * 16384), 16384, 1024);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            int stage = 0;
+            uint32_t phase = 0, tphase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                const int split = item % P.splits;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                ptx::mbar_wait(tempty, tphase ^ 1);
+                ptx::tc_fence_after();
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = (uint32_t)dA + stage * (kWiStage >> 4);
+                    const uint32_t b0 = (uint32_t)dB + stage * (kWiStage >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        ptx::umma_bf16_lh(tmem, a0 + kk * 128, hiA, b0 + kk * 128, hiB, idesc, (pt != p0 || kk != 0) ? 1u : 0u);
+                    ptx::umma_commit(empty + stage);
+                    if (++stage == kWiStages) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(tfull);
+                tphase ^= 1;
+            }
+        }
+    } else {
+        const int ew = warp & 3;
+        const int m = ew * 32 + lane;                 // accumulator row = (tap - 16 mt) * 8 + ci
+        uint32_t tphase = 0;
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            const int mt = item / P.splits;
+            const int tap = mt * 16 + (m >> 3), ci = m & 7;
+            ptx::mbar_wait(tfull, tphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + c * 32, v);
+                ptx::tmem_ld_wait();
+                if (tap >= P.ntaps) continue;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int co = c * 32 + j;
+                    if (co < P.c_out) {
+                        const float g = P.gamma ? __bfloat162float(P.gamma[co]) : 1.f;
+                        atomicAdd(P.dw + ((long long)co * P.ntaps + tap) * 8 + ci, __uint_as_float(v[j]) * g);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty);
+            tphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMma) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+    }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1534,6 +1703,49 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     return launch_wgrad_halo<128, 3>(P, D, X, st);
 }
 
+template <int BN>
+static bool launch_wgrad_im2col(const TcWgI2c &P, const CUtensorMap &D, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_wgrad_im2col<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWiSmem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    int grid = P.items < num_sms() ? P.items : num_sms();
+    k_wgrad_im2col<BN><<<grid, kI2cThreads - 4 * 32, kWiSmem, st>>>(D, P);
+    return true;
+}
+
+// wgrad of a conv whose input has 8 (padded) channels; N = c_out padded to 64 / 128 / 256
+static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
+    static const int on = env_int("LRCNN_IM2COL", 1);
+    const View &dy = a.dy, &x = a.x;
+    if (!on || x.Cp != 8 || (x.bs & 7) || !aligned16(x.p) || dy.Cp % 64 || dy.Cp > 64 || a.k * a.k > 49) return false;
+    const int rows = a.b - a.a;
+    TcWgI2c P{};
+    P.in = x; P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.ntaps = a.k * a.k; P.mtiles = (P.ntaps + 15) / 16;
+    P.a_mul = a.s; P.c_out = a.c_out;
+    for (int ky = 0; ky < a.k; ++ky)
+        for (int kx = 0; kx < a.k; ++kx) { P.tap_oy[ky * a.k + kx] = ky - a.p; P.tap_ox[ky * a.k + kx] = kx - a.p; }
+    pick_tile(rows, dy.W, 1, P.TW, P.TH);
+    int l = 0;
+    while ((1 << l) < P.TW) ++l;
+    P.tw_log2 = l;
+    P.tiles_x = (dy.W + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
+    int splits = (num_sms() + P.mtiles - 1) / P.mtiles;
+    if (splits > P.pix_tiles) splits = P.pix_tiles;
+    if (splits < 1) splits = 1;
+    P.per_split = (P.pix_tiles + splits - 1) / splits;
+    P.splits = (P.pix_tiles + P.per_split - 1) / P.per_split;
+    P.items = P.mtiles * P.splits;
+    P.out_a = a.a; P.out_b = a.b; P.Wo = dy.W; P.dy_base = dy.base;
+    CUtensorMap D;
+    if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
+    return launch_wgrad_im2col<64>(P, D, st);
+}
+
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     if (a.s < 1 || a.s > 2) return false;
     const View &dy = a.dy, &x = a.x;
@@ -1541,6 +1753,7 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     const int rows = a.b - a.a;
     if (rows <= 0) return true;
     if (wgrad_halo(a, st)) return true;
+    if (wgrad_im2col(a, st)) return true;
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = a.s;

@@ -423,11 +423,14 @@ template <typename T>
 __global__ void k_fc_ce(const float *gap, int B, int Cp, int C, int classes, const T *fw, const T *fb,
                         const int32_t *labels, float *dlog, float *loss, float *gw, float *gb) {
     extern __shared__ float sh[];   // logits [B*classes]
-    for (int i = threadIdx.x; i < B * classes; i += blockDim.x) {
-        int b = i / classes, j = i % classes;
-        float s = ldf(fb + j);
-        for (int c = 0; c < C; ++c) s += gap[(long long)b * Cp + c] * ldf(fw + (long long)j * Cp + c);
-        sh[i] = s;
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x >> 5; i < B * classes; i += nw) {   // one warp per (image, class)
+        const int b = i / classes, j = i % classes;
+        float s = 0.f;
+        for (int c = lane; c < C; c += 32) s += gap[(long long)b * Cp + c] * ldf(fw + (long long)j * Cp + c);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sh[i] = s + ldf(fb + j);
     }
     __syncthreads();
     __shared__ float lsum;
@@ -496,21 +499,27 @@ __global__ void k_sgd(float *master, T *params, float *grads, long long n, float
 }
 
 template <typename T>
+// wt[ci][k-1-ky][k-1-kx][co] = gamma[co] * w[co][ky][kx][ci] (0 for co >= cout): per tap a 32 x 32
+// tile transpose through shared memory, coalesced along ci on the read and co on the write.
 __global__ void k_transpose_w(const T *w, const T *gamma, T *wt, int cout, int coutp, int k, int cinp) {
-    long long n = (long long)cinp * k * k * coutp;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        int co = i % coutp;
-        long long r = i / coutp;
-        int kx2 = r % k; r /= k;
-        int ky2 = r % k;
-        int ci = (int)(r / k);
+    __shared__ float tile[32][33];
+    const int taps = k * k, tap = blockIdx.z;
+    const int ci0 = blockIdx.x * 32, co0 = blockIdx.y * 32;
+    const int ky = tap / k, kx = tap - ky * k;
+    const int tap2 = (k - 1 - ky) * k + (k - 1 - kx);
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int co = co0 + r, ci = ci0 + threadIdx.x;
         float v = 0.f;
-        if (co < cout) {
-            int ky = k - 1 - ky2, kx = k - 1 - kx2;
-            v = ldf(w + ((long long)(co * k + ky) * k + kx) * cinp + ci);
+        if (co < cout && ci < cinp) {
+            v = ldf(w + ((long long)co * taps + tap) * cinp + ci);
             if (gamma) v *= ldf(gamma + co);
         }
-        stf(wt + i, v);
+        tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int ci = ci0 + r, co = co0 + threadIdx.x;
+        if (ci < cinp && co < coutp) stf(wt + ((long long)ci * taps + tap2) * coutp + co, tile[threadIdx.x][r]);
     }
 }
 
@@ -688,8 +697,8 @@ cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     const int CV = CVall < 64 ? CVall : 64, groups = (CVall + CV - 1) / CV;
     dim3 blk(CV, CV >= 64 ? 4 : 256 / CV);
     long long npix = (long long)a.B * (a.b - a.a) * a.dy.W;
-    long long g = (npix + blk.y * 16 - 1) / (blk.y * 16);        // ~16 pixels per thread
-    long long cap = 148 * 8 / groups + 1;
+    long long g = (npix + blk.y * 4 - 1) / (blk.y * 4);          // ~4 pixels per thread
+    long long cap = 148 * 4 / groups + 1;
     if (g > cap) g = cap;
     if (g < 1) g = 1;
     dim3 grid((unsigned)g, groups);
@@ -831,9 +840,9 @@ cudaError_t sgd_update(int prec, float *master, void *params, float *grads, long
 
 cudaError_t transpose_weights(int prec, const void *w, const void *gamma, void *wt, int cout, int coutp, int k,
                               int cinp, cudaStream_t st) {
-    long long n = (long long)cinp * k * k * coutp;
-    if (prec) k_transpose_w<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)w, (const bf16 *)gamma, (bf16 *)wt, cout, coutp, k, cinp);
-    else k_transpose_w<float><<<grid_for(n), kT, 0, st>>>((const float *)w, (const float *)gamma, (float *)wt, cout, coutp, k, cinp);
+    dim3 g((cinp + 31) / 32, (coutp + 31) / 32, k * k), blk(32, 8);
+    if (prec) k_transpose_w<bf16><<<g, blk, 0, st>>>((const bf16 *)w, (const bf16 *)gamma, (bf16 *)wt, cout, coutp, k, cinp);
+    else k_transpose_w<float><<<g, blk, 0, st>>>((const float *)w, (const float *)gamma, (float *)wt, cout, coutp, k, cinp);
     return cudaGetLastError();
 }
 

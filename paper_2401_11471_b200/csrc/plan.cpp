@@ -219,11 +219,12 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     }
 
     // ---------------------------------------------------------------- bands
-    for (Segment &S : P.seg) {
+    // rows of every tensor of segment S for its band ends (nb > 0: nb near-equal bands)
+    auto make_bands = [&](Segment &S, int nb) -> lrcnn_status {
         const int own = S.own_hi - S.own_lo;
         if (opts->mode == LRCNN_COLUMN) S.E = {S.own_hi};
         else {
-            S.E = make_band_ends(own, opts->band_rows, opts->n_bands);
+            S.E = nb > 0 ? make_band_ends(own, 0, nb) : make_band_ends(own, opts->band_rows, opts->n_bands);
             for (int &e : S.E) e += S.own_lo;
         }
         for (size_t r = 1; r < S.E.size(); ++r)
@@ -300,6 +301,41 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
                 }
                 for (int t : S.tensors)
                     if (S.b[r][t] < S.a[r][t]) { err = "non-monotone band ends"; return LRCNN_E_DEGENERATE; }
+            }
+        }
+        return LRCNN_OK;
+    };
+    const size_t Bsz = net->B, Esz = P.elem;
+    // band working set of a segment: act + delta buffers of its internal tensors + 2PS carries
+    auto seg_arena = [&](const Segment &S) {
+        size_t a = 0;
+        const int N = (int)S.E.size();
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            int cap = 0, ccap = 0;
+            for (int r = 0; r < N; ++r) {
+                cap = std::max(cap, S.b[r][t] - S.lo[r][t]);
+                ccap = std::max(ccap, S.a[r][t] - S.lo[r][t]);
+            }
+            const size_t rb = (size_t)P.t[t].W * P.t[t].Cp * Esz;
+            a += 2 * align_up(Bsz * std::max(cap, 1) * rb);
+            if (ccap > 0 && opts->mode == LRCNN_2PS) a += align_up(Bsz * ccap * rb);
+        }
+        return a;
+    };
+    for (Segment &S : P.seg) {
+        lrcnn_status st = make_bands(S, 0);
+        if (st != LRCNN_OK) return st;
+    }
+    if ((opts->flags & LRCNN_FLAG_BALANCED_BANDS) && opts->mode != LRCNN_COLUMN) {
+        size_t budget = 0;
+        for (const Segment &S : P.seg) budget = std::max(budget, seg_arena(S));
+        for (Segment &S : P.seg) {
+            const int n0 = (int)S.E.size();
+            for (int nb = 1; nb < n0; ++nb) {
+                Segment T2 = S;
+                if (make_bands(T2, nb) != LRCNN_OK) continue;
+                if (seg_arena(T2) <= budget) { S = T2; break; }
             }
         }
     }

@@ -1,9 +1,12 @@
-"""Microbenchmark (GPU): one conv layer, forward + backward through the C-ABI (bf16, column
-mode), per-kernel-class times from the library's profiler (class 0 = conv FP/dgrad,
-1 = wgrad, 2 = other).  Usage: python scripts/microbench_layer.py cin,cout,H,W[,k,s] ...
-"""
+"""Microbenchmark (GPU): one conv layer (after a cheap 1x1 producer, so its dgrad runs too),
+forward + backward through the C-ABI (bf16, column mode); per-kind kernel times of the measured
+layer from the library's per-op profile.  Usage:
+    python scripts/microbench_layer.py cin,cout,H,W[,k,s] ...
+cin = 3 measures the first layer (no producer, no dgrad)."""
+import csv
 import os
 import sys
+import tempfile
 
 import torch
 
@@ -12,12 +15,18 @@ import workloads as WL  # noqa: E402
 from paper_2401_11471_b200 import lrcnn as LB  # noqa: E402
 
 B = int(os.environ.get("B", "32"))
-shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]] or [(3, 64, 56, 224)]
+shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]] or [(64, 64, 56, 224)]
 for sh in shapes:
     cin, cout, H, W = sh[:4]
     k = sh[4] if len(sh) > 4 else 3
     s = sh[5] if len(sh) > 5 else 1
-    net = {"C": cin, "H": H, "W": W, "classes": 10, "ops": [WL.conv(0, cout, k, s, k // 2)]}
+    if cin <= 8:
+        net = {"C": cin, "H": H, "W": W, "classes": 10, "ops": [WL.conv(0, cout, k, s, k // 2)]}
+        op = 0
+    else:
+        net = {"C": 8, "H": H, "W": W, "classes": 10,
+               "ops": [WL.conv(0, cin, 1, 1, 0), WL.conv(1, cout, k, s, k // 2)]}
+        op = 1
     plan = LB.Plan(net, B, mode="column", prec="bf16")
     ds = LB.DeviceState(plan)
     ds.params.uniform_(-0.1, 0.1)
@@ -34,12 +43,12 @@ for sh in shapes:
         ds.forward()
         ds.backward()
     torch.cuda.synchronize()
-    c0 = plan.profile_read(0)
-    c1 = plan.profile_read(1)
-    c2 = plan.profile_read(2)
+    path = os.path.join(tempfile.gettempdir(), "mb_layer.csv")
+    plan.profile_dump(path)
     plan.profile(False)
-    fl = 2 * k * k * cin * cout * (H // s) * (W // s) * B
-    print("cin %4d cout %4d %4dx%4d k%d s%d B%d | convFP+dgrad %.3f ms/iter (%d launches) %.1f TF/s | "
-          "wgrad %.3f ms %.1f TF/s | other %.3f ms | tc=%d" %
-          (cin, cout, H, W, k, s, B, c0[0] / n, c0[1] // n, c0[2] / max(c0[0], 1e-9) / 1e9,
-           c1[0] / n, c1[2] / max(c1[0], 1e-9) / 1e9, c2[0] / n, plan.last_tc_launches()), flush=True)
+    out = {}
+    for r in csv.DictReader(open(path)):
+        if int(r["op"]) == op:
+            out[r["kind"]] = (float(r["ms"]) / n, float(r["flops"]) / max(float(r["ms"]), 1e-9) / 1e9)
+    txt = " | ".join("%s %.3f ms %.0f TF/s" % (kd, v[0], v[1]) for kd, v in sorted(out.items()))
+    print("cin %4d cout %4d %4dx%4d k%d s%d B%d | %s" % (cin, cout, H, W, k, s, B, txt), flush=True)

@@ -215,3 +215,73 @@ def test_c1_cache_is_k_minus_s():
     plan = LB.Plan(WL.tiny3(p=1), 1, mode="2ps", prec="fp32", band_rows=4)
     m = plan.memory()
     assert m["halo_cache"] == 1 * 7 * 2 * (32 * 8) * 4 * 2    # B * (N-1) * c * W*Cp * 4B * 2 tensors
+
+
+# ---------------------------------------------------------------- balanced bands
+def _arena_bytes(net, seg, bands, shp, B, E, cps):
+    """Band working set of one segment from the oracle enumerator's rows: act + delta buffers
+    (rows [lo, b) of every internal tensor, max over bands) plus the 2PS carry rows [lo, a)."""
+    seg_in, ids, out = seg
+    align = lambda v: (v + 255) // 256 * 256
+    tot = 0
+    for t in [i + 1 for i in ids]:
+        if t == out:
+            continue
+        cap = max(max(b[t][2] - b[t][0] for b in bands), 1)
+        ccap = max(b[t][1] - b[t][0] for b in bands)
+        rb = shp[t][2] * cps[t] * E
+        tot += 2 * align(B * cap * rb)
+        if ccap > 0:
+            tot += align(B * ccap * rb)
+    return tot
+
+
+@pytest.mark.parametrize("which", ["vgg", "resnet", "random"])
+def test_balanced_bands_minimal_and_exact(which):
+    """FLAG_BALANCED_BANDS: every segment's rows equal the enumerator at that segment's band
+    count; that count is the smallest whose working set fits the largest segment's (the budget),
+    and the workspace does not grow."""
+    rng = np.random.default_rng(5)
+    if which == "vgg":
+        nets = [(WL.vgg16(H=224, W=224, segments="pool"), 4), (WL.vgg16(H=96, W=40, segments="pool"), 6)]
+    elif which == "resnet":
+        nets = [(WL.resnet50(H=224, W=224), 4), (WL.resnet50(H=256, W=64), 7)]
+    else:
+        nets = []
+        while len(nets) < 25:
+            net = random_net(rng)
+            try:
+                C.out_hw(net)
+                EN.segments(net)
+            except ValueError:
+                continue
+            nets.append((net, int(rng.integers(2, 6))))
+    for net, nb in nets:
+        B = 2
+        try:
+            p0 = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb)
+        except LB.LrcnnError:
+            continue
+        p1 = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb, flags=LB.FLAG_BALANCED_BANDS)
+        shp = C.out_hw(net)
+        cps = {t: p1.tensor(t)[1] for t in range(len(net["ops"]) + 1)}
+        segs = EN.segments(net)
+        arenas = []
+        for s, seg in enumerate(segs):
+            h = shp[seg[2]][1]
+            bands = EN.enumerate_2ps(net, seg, EN.band_ends(h, n_bands=nb), shp)
+            arenas.append(_arena_bytes(net, seg, bands, shp, B, 2, cps))
+        budget = max(arenas)
+        for s, seg in enumerate(segs):
+            n = p1.seg(s)[2]
+            h = shp[seg[2]][1]
+            assert 1 <= n <= min(nb, h)
+            bands = EN.enumerate_2ps(net, seg, EN.band_ends(h, n_bands=n), shp)
+            for r, band in enumerate(bands):
+                for t in [i + 1 for i in seg[1]]:
+                    assert p1.rows(s, r, t) == band[t]
+            assert _arena_bytes(net, seg, bands, shp, B, 2, cps) <= budget
+            if n > 1:   # minimal: one band fewer would not fit
+                fewer = EN.enumerate_2ps(net, seg, EN.band_ends(h, n_bands=n - 1), shp)
+                assert _arena_bytes(net, seg, fewer, shp, B, 2, cps) > budget
+        assert p1.ws_bytes <= p0.ws_bytes
