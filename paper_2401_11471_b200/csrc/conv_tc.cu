@@ -1323,6 +1323,110 @@ __global__ void __launch_bounds__(kI2cThreads - 4 * 32, 1)
     }
 }
 
+// ------------------------------------------------------------------ conv FP / dgrad: halo + resident weights
+// 64-channel 3x3 stride-1 layers (VGG conv1_2, ResNet stage-1 3x3) are load-bound in the per-tap
+// kernel (a 16 KB A box + an 8 KB weight box per 136 tensor cycles).  Here the whole weight
+// tensor (9 taps x 64 x 64, 72 KB) is TMA-loaded once per CTA and stays in smem, and the A
+// operand of all 9 taps comes from one (8+2) x (16+2) halo box per tile (HaloGeom): per tile
+// 23 KB of loads for 36 MMAs.  Epilogue: TMA store (FP) or TMA load/combine/store (dgrad).
+static constexpr int kRbSA = 3;
+static constexpr int kRbB = 9 * 64 * 128;                                    // 72 KB
+static constexpr int kRbSmem = kRbSA * HaloGeom<3>::kABytes + kRbB + 2 * kOutStage + 1024 + 512;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_conv_halo_rb(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
+    constexpr int BN = 64, KH = 3, taps = 9, SA = kRbSA;
+    constexpr int HP = HaloGeom<KH>::kPitch, AB = HaloGeom<KH>::kABytes;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + SA * AB;
+    uint8_t *sO = sB + kRbB;
+    uint64_t *fullA = (uint64_t *)(sO + 2 * kOutStage);
+    uint64_t *emptyA = fullA + SA;
+    uint64_t *bfull = emptyA + SA;
+    uint64_t *tfull = bfull + 1;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *ebar = tempty + 2;
+    uint32_t *tslot = (uint32_t *)(ebar + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
+        ptx::mbar_init(bfull, 1);
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
+        ptx::mbar_init(ebar, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, 2 * BN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int num_tiles = P.m_tiles;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(bfull, kRbB);
+            for (int tap = 0; tap < taps; ++tap) ptx::tma_load_3d(sB + tap * BN * 128, &tmB, bfull, 0, tap, 0);
+            int sa = 0;
+            uint32_t pa = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int nt, tx, ty, b;
+                P.decode(tile, nt, tx, ty, b);
+                const int y0 = P.out_a + ty * 16, x0 = tx * 8;
+                ptx::mbar_wait(emptyA + sa, pa ^ 1);
+                ptx::mbar_arrive_expect_tx(fullA + sa, HP * HaloGeom<KH>::kRows * 128);
+                ptx::tma_load_4d(sA + sa * AB, &tmA, fullA + sa, 0, x0 - P.pad, y0 - P.pad - P.in_base, b);
+                if (++sa == SA) { sa = 0; pa ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            const uint64_t dA = ptx::smem_desc_sw128_bo(ptx::smem_u32(sA), 16, HP * 128, 0);
+            const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(sB), 16, 1024);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            ptx::mbar_wait(bfull, 0);
+            int sa = 0, acc = 0;
+            uint32_t pa = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                ptx::mbar_wait(fullA + sa, pa);
+                ptx::tc_fence_after();
+                const uint32_t a0 = (uint32_t)dA + sa * (AB >> 4);
+#pragma unroll
+                for (int tap = 0; tap < taps; ++tap) {
+                    const int ky = tap / KH, kx = tap - ky * KH;
+                    const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
+                    const uint32_t b0 = (uint32_t)dB + tap * (BN * 128 >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        ptx::umma_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (tap | kk) != 0);
+                }
+                ptx::umma_commit(emptyA + sa);
+                if (++sa == SA) { sa = 0; pa ^= 1; }
+                ptx::umma_commit(tfull + acc);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else if (P.mode == 0) {
+        conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
+    } else {
+        conv_epilogue_tma_dg<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 2 * BN);
+    }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1433,6 +1537,41 @@ static int env_int(const char *name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
+// 64 -> 64 channel 3x3 stride-1 FP / dgrad (unit output stride) through k_conv_halo_rb
+static bool conv_halo_rb(TcConv &P, const View &in, const void *w, int w_rows, int cin_p, cudaStream_t st) {
+    static const int on = env_int("LRCNN_HALO_RB", 1);
+    if (!on || cin_p != 64 || P.n_out != 64 || P.ntaps != 9 || P.k != 3 || P.o_stride != 1 || P.a_mul != 1) return false;
+    if (P.mode == 1 && (P.out.Cp != 64 || (P.gate && (P.act.Cp != 64 || !aligned16(P.act.p))))) return false;
+    if (P.mode == 0 && P.out.Cp % 8) return false;
+    const int rows = P.out_b - P.out_a;
+    P.in_base = in.base;
+    P.n_tiles = 1;
+    P.TW = 8; P.TH = 16;
+    P.tiles_x = (P.Wo + 7) / 8;
+    P.tiles_y = (rows + 15) / 16;
+    P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    tile_div_init(P);
+    CUtensorMap A, Bm, O, G;
+    if (!encode_w(&Bm, w, w_rows, 9, cin_p, 64, 64)) return false;
+    if (!encode_view(&A, in, P.B, HaloGeom<3>::kPitch, HaloGeom<3>::kRows)) return false;
+    View ov = P.out;
+    ov.rows = P.out_b - P.out.base;
+    if (!encode_view(&O, ov, P.B, 8, 16)) return false;
+    G = O;
+    if (P.mode == 1 && P.gate && !encode_view(&G, P.act, P.B, 8, 16)) return false;
+    P.tma_out = P.mode == 0;
+    P.tma_dg = P.mode == 1;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_conv_halo_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, kRbSmem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
+    k_conv_halo_rb<<<grid, kThreads, kRbSmem, st>>>(A, Bm, O, G, P);
+    return true;
+}
+
 // Launch one implicit-GEMM conv over the output grid rows [P.out_a, P.out_b) x cols [0, P.Wo).
 // Caller sets the epilogue fields, the output mapping (o_*), a_mul and the tap table.
 static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, int w_taps, int cin_p,
@@ -1442,6 +1581,7 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     int BN = P.n_out <= 64 ? 64 : (P.n_out <= 128 ? 128 : 256);
     const int rows = P.out_b - P.out_a;
     if (rows <= 0 || P.Wo <= 0) return true;
+    if (P.halo_ok && conv_halo_rb(P, in, w, w_rows, cin_p, st)) return true;
     {   // small launches (deep layers, thin bands): narrower N tiles so that every SM gets work
         static const int adapt = env_int("LRCNN_BN_ADAPT", 0);
         int tw = 8, th = 16;
