@@ -90,6 +90,7 @@ static inline void tile_div_init(TcConv &P) {
 struct TcWgrad {
     float *dw;
     const bf16 *gamma;
+    float *db;             // row-halo kernel: fused bias gradient (items with ky == 0, ci tile 0)
     int k, pad, c_out, cin_p;
     int TW, TH, tiles_x, tiles_y, pix_tiles, per_split, splits;
     int co_tiles, ci_tiles, items;
@@ -1025,7 +1026,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *tslot = (uint32_t *)(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        // empty: the MMA commit + (fused bias gradient) the 4 epilogue warps, which read every delta tile
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, P.db ? 5 : 1); }
         ptx::mbar_init(tfull, 1);
         ptx::mbar_init(tempty, 4);
         ptx::fence_barrier_init();
@@ -1116,11 +1118,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m = ew * 32 + lane;
         const int taps = KW * KW;
         uint32_t tphase = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        // fused bias gradient: thread m sums delta column (co tile row) m of every pixel tile
+        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             int cot, ky, cit, split;
             decode(item, cot, ky, cit, split);
             const int co = cot * 128 + m;
             const float gsc = (P.gamma && co < P.c_out) ? __bfloat162float(P.gamma[co]) : 1.f;
+            if (P.db) {
+                const bool want = ky == 0 && cit == 0;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float sum = 0.f;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    if (want) {
+                        const uint32_t base = ptx::smem_u32(smem + stage * SB);
+#pragma unroll 8
+                        for (int r = 0; r < 128; ++r) {
+                            const uint32_t a = base + r * 128 + (col ^ ((r & 7) << 4));
+                            unsigned short h;
+                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+                            sum += __uint_as_float((uint32_t)h << 16);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
+            }
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -1814,6 +1842,8 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = 1;
+    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
+    P.db = fuse_db ? a.db : nullptr;
     // 128-pixel tile, TW a multiple of 16 (one K-step = 16 pixels of one output row)
     long best = -1;
     for (int tw = 128; tw >= 16; tw >>= 1) {
@@ -1839,8 +1869,9 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     CUtensorMap D, X;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
     if (!encode_view(&X, x, a.B, P.TW + a.k - 1, P.TH)) return false;
-    if (BN == 64) return launch_wgrad_halo<64, 3>(P, D, X, st);
-    return launch_wgrad_halo<128, 3>(P, D, X, st);
+    const bool ok = BN == 64 ? launch_wgrad_halo<64, 3>(P, D, X, st) : launch_wgrad_halo<128, 3>(P, D, X, st);
+    if (ok && P.db) a.db_done = true;
+    return ok;
 }
 
 template <int BN>

@@ -309,7 +309,22 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
         // the side stream so they overlap the dgrad chain (joined at the end of the band)
         cudaStream_t gst = R.st;
         if (R.side) { CK(fork_side(R)); gst = R.side; }
-        if (o.d.epi != LRCNN_EPI_NONE) {
+        bool db_done = false;
+        const void *gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
+        {
+            WgradArgs A;
+            A.dy = dy; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
+            A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
+            // VGG bias gradient fused into the row-halo wgrad kernel when it takes the op
+            if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
+            ++P.launches;
+            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2);
+            if (P.use_tc && tc_conv_wgrad(A, gst)) ++P.tc_launches;
+            else CK(simt_conv_wgrad(R.prec, A, gst));
+            CK(cudaGetLastError());
+            db_done = A.db_done;
+        }
+        if (o.d.epi != LRCNN_EPI_NONE && !db_done) {
             ParamGradArgs A;
             A.dy = dy; A.t = act_view(R, S, r, t);
             if (o.d.res >= 0) A.res = act_view(R, S, r, o.d.res);
@@ -322,17 +337,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             ProfScope ps(R, 2, 0, i * 8 + 3);
             CK(simt_param_grad(R.prec, A, gst));
         }
-        const void *gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
-        {
-            WgradArgs A;
-            A.dy = dy; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
-            A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
-            ++P.launches;
-            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2);
-            if (P.use_tc && tc_conv_wgrad(A, gst)) ++P.tc_launches;
-            else CK(simt_conv_wgrad(R.prec, A, gst));
-            CK(cudaGetLastError());
-        }
+
         if (need_dx) {
             DgradArgs A;
             A.dy = dy; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);

@@ -43,6 +43,8 @@ struct WgradArgs {
     View dy, x;
     float *dw = nullptr;       // [Cout][k][k][Cin_p] fp32, accumulated
     const void *gamma = nullptr;
+    float *db = nullptr;       // optional: bias gradient sum_pixels dy[., co] fused into the kernel
+    mutable bool db_done = false;   // set by a launcher that accumulated db
     int k, s, p, c_out;
     int a, b;                  // output rows contributing
     int B;
