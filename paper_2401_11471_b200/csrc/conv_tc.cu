@@ -1859,7 +1859,8 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     P.co_tiles = (dy.Cp + 127) / 128;
     P.ci_tiles = (x.Cp + BN - 1) / BN;
     const int base_items = P.co_tiles * a.k * P.ci_tiles;
-    int splits = (num_sms() + base_items - 1) / base_items;
+    // one wave: at most num_sms items (a second partial wave would double the kernel time)
+    int splits = num_sms() / base_items;
     if (splits > P.pix_tiles) splits = P.pix_tiles;
     if (splits < 1) splits = 1;
     P.per_split = (P.pix_tiles + splits - 1) / splits;
@@ -1905,7 +1906,7 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
-    int splits = (num_sms() + P.mtiles - 1) / P.mtiles;
+    int splits = num_sms() / P.mtiles;
     if (splits > P.pix_tiles) splits = P.pix_tiles;
     if (splits < 1) splits = 1;
     P.per_split = (P.pix_tiles + splits - 1) / splits;
@@ -1936,7 +1937,7 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.co_tiles = (dy.Cp + 127) / 128;
     P.ci_tiles = (x.Cp + BN - 1) / BN;
     const int base_items = P.co_tiles * a.k * a.k * P.ci_tiles;
-    int splits = (2 * num_sms() + base_items - 1) / base_items;
+    int splits = 2 * num_sms() / base_items;
     if (splits > P.pix_tiles) splits = P.pix_tiles;
     if (splits < 1) splits = 1;
     P.per_split = (P.pix_tiles + splits - 1) / splits;
