@@ -374,7 +374,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             const int N = (int)S.E.size();
             const bool carry_in = P.opts.mode == LRCNN_2PS && r + 1 < N && S.lo[r + 1][o.in_t] < S.a[r + 1][o.in_t];
             A.acc = !(o.d.k == o.d.s && o.d.p == 0 && o.in_t != S.in_t && tin.cons.size() == 1 && !carry_in);
-            ++P.launches;
+            P.launches += simt_pool_bwd_launches(A);
             ProfScope ps(R, 2, 0, i * 8 + 5);
             CK(simt_pool_bwd(R.prec, A, R.st));
         }

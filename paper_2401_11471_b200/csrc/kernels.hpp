@@ -78,6 +78,7 @@ cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st);
 cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st);
 cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st);
 cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st);
+int simt_pool_bwd_launches(const PoolArgs &a);   // kernels simt_pool_bwd enqueues
 cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st);
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st);
 

@@ -195,8 +195,9 @@ __global__ void k_param_grad(ParamGradArgs A) {
     const T *dbase = (const T *)A.dy.p + voff(A.dy, 0, A.a, 0) + c0;
     const T *tbase = A.epi == 2 ? (const T *)A.t.p + voff(A.t, 0, A.a, 0) + c0 : nullptr;
     const T *rbase = A.epi == 2 && A.res.p ? (const T *)A.res.p + voff(A.res, 0, A.a, 0) + c0 : nullptr;
+    // AFFINE: dgamma = sum d (t - res - beta) / gamma = (sum d (t - res) - beta sum d) / gamma
     while (live && b < A.B) {
-        // up to 4 independent pixels per iteration (loads in flight)
+        // up to 4 independent pixels per iteration, all loads issued before the arithmetic
         long long po[4], pt[4], pr[4];
         int cnt = 0;
 #pragma unroll
@@ -210,23 +211,28 @@ __global__ void k_param_grad(ParamGradArgs A) {
                 while (p >= RW) { p -= RW; ++b; }
             }
         }
-        float d[4][8];
+        float d[4][8], t[4][8], rr[4][8];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (u < cnt) ld8(dbase + po[u], d[u]);
+            if (u < cnt) {
+                ld8(dbase + po[u], d[u]);
+                if (A.epi == 2) ld8(tbase + pt[u], t[u]);
+                if (rbase) ld8(rbase + pr[u], rr[u]);
+            }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (u >= cnt) break;
 #pragma unroll
             for (int j = 0; j < 8; ++j) s0[j] += d[u][j];
             if (A.epi == 2) {
-                float t[8], rr[8];
-                ld8(tbase + pt[u], t);
-                if (rbase) ld8(rbase + pr[u], rr);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) s1[j] += d[u][j] * ((t[j] - (rbase ? rr[j] : 0.f)) - bet[j]) / gam[j];
+                for (int j = 0; j < 8; ++j) s1[j] += d[u][j] * (t[u][j] - (rbase ? rr[u][j] : 0.f));
             }
         }
+    }
+    if (A.epi == 2) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s1[j] = (s1[j] - bet[j] * s0[j]) / gam[j];
     }
     extern __shared__ float red[];   // [PY][CV*8] x 2
     float *r0 = red, *r1 = red + PY * CV * 8;
@@ -614,6 +620,56 @@ __global__ void k_pool_bwd8(PoolArgs A) {
     }
 }
 
+// Overlapping max-pool backward (s < k <= 2s, e.g. ResNet's 3x3/s2/p1) as a scatter in 4 parity
+// phases: output pixels (y, x) with y = py, x = px (mod 2) have disjoint windows, so each phase
+// recomputes every window's argmax once and adds dy into dx at the argmax (gate-on-write) without
+// write conflicts.  Traffic per output pixel: k*k input vectors + the dy vector + one dx RMW per
+// distinct argmax position (the gather form re-reads every window once per input pixel in it).
+template <typename T>
+__global__ void k_pool_bwd_scatter8(PoolArgs A, int py, int px) {
+    const int CV = A.dy.Cp / 8, Wo = A.dy.W, rows = A.b - A.a;
+    const int wx = (Wo - px + 1) / 2;                      // output columns of this parity
+    const int y0 = A.a + ((py - A.a) % 2 + 2) % 2;         // first band row of this parity
+    const int ry = y0 < A.b ? (A.b - y0 + 1) / 2 : 0;
+    const long long n = (long long)A.B * ry * wx * CV;
+    (void)rows;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int cv = (int)(idx % CV);
+        long long r = idx / CV;
+        const int x = px + 2 * (int)(r % wx); r /= wx;
+        const int y = y0 + 2 * (int)(r % ry);
+        const int b = (int)(r / ry);
+        float best[8], d[8];
+        int arg[8];
+        pool_window8<T>(A.act, b, y, x, cv * 8, A.k, A.s, A.p, best, arg);
+        ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
+        for (int ky = 0; ky < A.k; ++ky) {
+            const int g = y * A.s - A.p + ky;
+            if (!vhas(A.dx, g)) continue;
+            for (int kx = 0; kx < A.k; ++kx) {
+                const int xi = x * A.s - A.p + kx;
+                if (xi < 0 || xi >= A.dx.W) continue;
+                const int code = ky * A.k + kx;
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) any |= arg[j] == code;
+                if (!any) continue;
+                T *dp = (T *)A.dx.p + voff(A.dx, b, g, xi) + cv * 8;
+                float o[8];
+                ld8(dp, o);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (arg[j] != code) continue;
+                    o[j] += d[j];
+                    if (A.gate && !(best[j] > 0.f)) o[j] = 0.f;    // best = act at the argmax
+                }
+                st8(dp, o);
+            }
+        }
+    }
+}
+
 template <typename T>
 __global__ void k_acc_gate8(EltArgs A) {
     const int CV = A.dx.Cp / 8, W = A.dx.W, rows = A.b - A.a;
@@ -698,7 +754,7 @@ cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     dim3 blk(CV, CV >= 64 ? 4 : 256 / CV);
     long long npix = (long long)a.B * (a.b - a.a) * a.dy.W;
     long long g = (npix + blk.y * 4 - 1) / (blk.y * 4);          // ~4 pixels per thread
-    long long cap = 148 * 4 / groups + 1;
+    long long cap = 148 * 8 / groups + 1;
     if (g > cap) g = cap;
     if (g < 1) g = 1;
     dim3 grid((unsigned)g, groups);
@@ -724,6 +780,11 @@ cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     }
     return cudaGetLastError();
 }
+int simt_pool_bwd_launches(const PoolArgs &a) {
+    if ((long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp <= 0) return 0;
+    if (pool2(a, a.dy)) return a.b > a.a ? 1 : 0;
+    return a.dx.Cp % 8 == 0 && a.k > a.s && a.k <= 2 * a.s ? 4 : 1;
+}
 cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
     if (n <= 0) return cudaSuccess;
@@ -732,6 +793,12 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
         const int rowv = a.dy.W * (a.dy.Cp / 8);
         dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
         if (prec) k_pool2_bwd<bf16><<<g, kT, 0, st>>>(a); else k_pool2_bwd<float><<<g, kT, 0, st>>>(a);
+    } else if (a.dx.Cp % 8 == 0 && a.k > a.s && a.k <= 2 * a.s) {
+        const long long m = (long long)a.B * (a.b - a.a) * a.dy.W * (a.dy.Cp / 8) / 4 + 1;
+        for (int ph = 0; ph < 4; ++ph) {
+            if (prec) k_pool_bwd_scatter8<bf16><<<grid_for(m), kT, 0, st>>>(a, ph >> 1, ph & 1);
+            else k_pool_bwd_scatter8<float><<<grid_for(m), kT, 0, st>>>(a, ph >> 1, ph & 1);
+        }
     } else if (a.dx.Cp % 8 == 0) {
         n /= 8;
         if (prec) k_pool_bwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd8<float><<<grid_for(n), kT, 0, st>>>(a);
