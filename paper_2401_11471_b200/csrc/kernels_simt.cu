@@ -174,20 +174,34 @@ __device__ __forceinline__ void st8(bf16 *p, const float (&v)[8]) {
 // coalesced 8-channel loads, per-thread partial sums, smem reduction over pixel lanes,
 // one fp32 atomicAdd per channel per block.
 template <typename T>
-__global__ void k_param_grad(ParamGradArgs A) {
+__device__ __forceinline__ void acc8(const uint4 &u, float (&s)[8]) {
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { float2 f = __bfloat1622float2(h[j]); s[2 * j] += f.x; s[2 * j + 1] += f.y; }
+}
+// s += d * (t - r)  (bf16 vectors of 8)
+__device__ __forceinline__ void accdot8(const uint4 &d, const uint4 &t, const uint4 &r, float (&s)[8]) {
+    const __nv_bfloat162 *dh = reinterpret_cast<const __nv_bfloat162 *>(&d);
+    const __nv_bfloat162 *th = reinterpret_cast<const __nv_bfloat162 *>(&t);
+    const __nv_bfloat162 *rh = reinterpret_cast<const __nv_bfloat162 *>(&r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float2 fd = __bfloat1622float2(dh[j]), ft = __bfloat1622float2(th[j]), fr = __bfloat1622float2(rh[j]);
+        s[2 * j] += fd.x * (ft.x - fr.x);
+        s[2 * j + 1] += fd.y * (ft.y - fr.y);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
     // blockDim.x channel vectors (8 channels each) of group blockIdx.y; blockDim.y pixel lanes
     const int CV = blockDim.x, cv = threadIdx.x, py = threadIdx.y, PY = blockDim.y;
     const int rows = A.b - A.a, W = A.dy.W, c0 = (blockIdx.y * CV + cv) * 8;
     const bool live = c0 < A.dy.Cp;
     const int RW = rows * W;                        // band pixels per image (contiguous rows)
-    float s0[8], s1[8], gam[8], bet[8];
+    float s0[8], s1[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        s0[j] = 0.f; s1[j] = 0.f;
-        const bool in = A.epi == 2 && c0 + j < A.c_out;
-        gam[j] = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
-        bet[j] = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
-    }
+    for (int j = 0; j < 8; ++j) { s0[j] = 0.f; s1[j] = 0.f; }
     // pixel q = b * RW + p walks with stride S; (b, p) updated without division
     const int S = gridDim.x * PY;
     const int q0 = blockIdx.x * PY + py;
@@ -195,44 +209,55 @@ __global__ void k_param_grad(ParamGradArgs A) {
     const T *dbase = (const T *)A.dy.p + voff(A.dy, 0, A.a, 0) + c0;
     const T *tbase = A.epi == 2 ? (const T *)A.t.p + voff(A.t, 0, A.a, 0) + c0 : nullptr;
     const T *rbase = A.epi == 2 && A.res.p ? (const T *)A.res.p + voff(A.res, 0, A.a, 0) + c0 : nullptr;
-    // AFFINE: dgamma = sum d (t - res - beta) / gamma = (sum d (t - res) - beta sum d) / gamma
-    while (live && b < A.B) {
-        // up to 4 independent pixels per iteration, all loads issued before the arithmetic
-        long long po[4], pt[4], pr[4];
-        int cnt = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (b < A.B) {
-                po[u] = (long long)b * A.dy.bs + (long long)p * A.dy.Cp;
-                pt[u] = (long long)b * A.t.bs + (long long)p * A.t.Cp;
-                pr[u] = (long long)b * A.res.bs + (long long)p * A.res.Cp;
-                ++cnt;
-                p += S;
-                while (p >= RW) { p -= RW; ++b; }
-            }
-        }
-        float d[4][8], t[4][8], rr[4][8];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (u < cnt) {
-                ld8(dbase + po[u], d[u]);
-                if (A.epi == 2) ld8(tbase + pt[u], t[u]);
-                if (rbase) ld8(rbase + pr[u], rr[u]);
-            }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (u >= cnt) break;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s0[j] += d[u][j];
+    if constexpr (sizeof(T) == 2) {
+        // bf16: raw 16-byte vectors, two pixels in flight per thread; AFFINE accumulates
+        // sum d (t - res) and dgamma = (sum d (t - res) - beta sum d) / gamma at the end
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        while (live && b < A.B) {
+            const int b0 = b, p0 = p;
+            p += S;
+            while (p >= RW) { p -= RW; ++b; }
+            const bool two = b < A.B;
+            const int b1 = b, p1 = p;
+            if (two) { p += S; while (p >= RW) { p -= RW; ++b; } }
+            const uint4 d0 = *reinterpret_cast<const uint4 *>(dbase + (long long)b0 * A.dy.bs + (long long)p0 * A.dy.Cp);
+            const uint4 d1 = two ? *reinterpret_cast<const uint4 *>(dbase + (long long)b1 * A.dy.bs + (long long)p1 * A.dy.Cp) : z;
             if (A.epi == 2) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) s1[j] += d[u][j] * (t[u][j] - (rbase ? rr[u][j] : 0.f));
+                const uint4 t0 = *reinterpret_cast<const uint4 *>(tbase + (long long)b0 * A.t.bs + (long long)p0 * A.t.Cp);
+                const uint4 t1 = two ? *reinterpret_cast<const uint4 *>(tbase + (long long)b1 * A.t.bs + (long long)p1 * A.t.Cp) : z;
+                const uint4 r0 = rbase ? *reinterpret_cast<const uint4 *>(rbase + (long long)b0 * A.res.bs + (long long)p0 * A.res.Cp) : z;
+                const uint4 r1 = rbase && two ? *reinterpret_cast<const uint4 *>(rbase + (long long)b1 * A.res.bs + (long long)p1 * A.res.Cp) : z;
+                accdot8(d0, t0, r0, s1);
+                accdot8(d1, t1, r1, s1);
             }
+            acc8<T>(d0, s0);
+            acc8<T>(d1, s0);
+        }
+    } else {
+        while (live && b < A.B) {
+            float d[8], t[8], rr[8];
+            ld8(dbase + (long long)b * A.dy.bs + (long long)p * A.dy.Cp, d);
+            if (A.epi == 2) {
+                ld8(tbase + (long long)b * A.t.bs + (long long)p * A.t.Cp, t);
+                if (rbase) ld8(rbase + (long long)b * A.res.bs + (long long)p * A.res.Cp, rr);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                s0[j] += d[j];
+                if (A.epi == 2) s1[j] += d[j] * (t[j] - (rbase ? rr[j] : 0.f));
+            }
+            p += S;
+            while (p >= RW) { p -= RW; ++b; }
         }
     }
     if (A.epi == 2) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s1[j] = (s1[j] - bet[j] * s0[j]) / gam[j];
+        for (int j = 0; j < 8; ++j) {
+            const bool in = c0 + j < A.c_out;
+            const float g = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
+            const float be = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
+            s1[j] = (s1[j] - be * s0[j]) / g;
+        }
     }
     extern __shared__ float red[];   // [PY][CV*8] x 2
     float *r0 = red, *r1 = red + PY * CV * 8;
@@ -695,6 +720,29 @@ __global__ void k_acc_gate8(EltArgs A) {
     }
 }
 
+// dx = gate(act) * (dx + dy) on rows [a, b): grid y = (image, row), x = row vectors; each row of
+// one image is contiguous in all three views (W * Cp elements)
+template <typename T>
+__global__ void k_acc_gate_rows(EltArgs A) {
+    const int rows = A.b - A.a, nv = A.dx.W * A.dx.Cp / 8;
+    const int b = blockIdx.y / rows, y = A.a + (int)(blockIdx.y - b * rows);
+    T *dx = (T *)A.dx.p + voff(A.dx, b, y, 0);
+    const T *dy = (const T *)A.dy.p + voff(A.dy, b, y, 0);
+    const T *ac = A.gate ? (const T *)A.act.p + voff(A.act, b, y, 0) : nullptr;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+        float o[8], d[8], g[8];
+        ld8(dx + i * 8, o);
+        ld8(dy + i * 8, d);
+        if (ac) ld8(ac + i * 8, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            o[j] += d[j];
+            if (ac && !(g[j] > 0.f)) o[j] = 0.f;
+        }
+        st8(dx + i * 8, o);
+    }
+}
+
 template <typename T>
 __global__ void k_add_fwd8(EltArgs A) {
     const int CV = A.out.Cp / 8, W = A.out.W, rows = A.b - A.a;
@@ -819,7 +867,12 @@ cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st) {
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b - a.a) * a.dx.W * a.dx.Cp;
     if (n <= 0) return cudaSuccess;
-    if (a.dx.Cp % 8 == 0) {
+    const long long gy = (long long)a.B * (a.b - a.a);
+    if (a.dx.Cp % 8 == 0 && a.dx.Cp == a.dy.Cp && (!a.gate || a.act.Cp == a.dx.Cp) && gy <= 65535) {
+        const int nv = a.dx.W * a.dx.Cp / 8;
+        dim3 g((nv + kT - 1) / kT, (unsigned)gy);
+        if (prec) k_acc_gate_rows<bf16><<<g, kT, 0, st>>>(a); else k_acc_gate_rows<float><<<g, kT, 0, st>>>(a);
+    } else if (a.dx.Cp % 8 == 0) {
         n /= 8;
         if (prec) k_acc_gate8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate8<float><<<grid_for(n), kT, 0, st>>>(a);
     } else if (prec) k_acc_gate<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate<float><<<grid_for(n), kT, 0, st>>>(a);
