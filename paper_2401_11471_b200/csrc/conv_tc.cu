@@ -54,6 +54,7 @@ struct TcConv {
     int a_mul, ntaps, o_row0, o_col0, o_stride, halo_ok;
     int tma_out;           // FP: stage the output tile in smem and TMA-store it
     int tma_dg;            // dgrad: TMA-load delta (+ activation), combine in smem, TMA-store
+    int tma_res;           // FP: the residual tile is TMA-loaded into the staging buffer
     int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
     int tw_log2;           // TW = 1 << tw_log2
@@ -182,7 +183,8 @@ __device__ __forceinline__ void epi_fast(const uint32_t (&v)[CH], const uint4 (&
 template <int BN, int NE = 4>
 __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
                                                   uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
-                                                  int lane, int lead_warp = 2) {
+                                                  int lane, int lead_warp = 2, const CUtensorMap *tmR = nullptr,
+                                                  uint64_t *rbar = nullptr) {
     constexpr int CH = 64 * 4 / NE;   // channels of a 64-channel group handled per thread
     const int num_tiles = P.m_tiles * P.n_tiles;
     const int q = warp & 3, hh = (warp - lead_warp) >> 2;
@@ -191,6 +193,19 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     const float lo = P.relu ? 0.f : -INFINITY;
     const int my = m >> P.tw_log2, mx = m & ((1 << P.tw_log2) - 1);
+    // residual through TMA: the tile of group g is loaded into the staging buffer the group's
+    // output will use (issued one group ahead, tracked by rbar); each thread adds its row
+    const bool rt = P.has_res && P.tma_res && tmR;
+    uint32_t rphase = 0;
+    auto res_load = [&](int tile2, int grp2, int buf2) {
+        int nt2, tx2, ty2, b2;
+        P.decode(tile2, nt2, tx2, ty2, b2);
+        bulk_wait_read1();                       // the store that last used buf2 has read it
+        ptx::mbar_arrive_expect_tx(rbar, kOutStage);
+        ptx::tma_load_4d(stage_out + buf2 * kOutStage, tmR, rbar, nt2 * BN + grp2 * 64, tx2 * P.TW,
+                         P.out_a + ty2 * P.TH - P.res.base, b2);
+    };
+    if (rt && leader && (int)blockIdx.x < num_tiles) res_load(blockIdx.x, 0, 0);
     int acc = 0, sbuf = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -200,10 +215,10 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
         const int yg = yg0 + my, xg = xg0 + mx;
         const bool valid = yg < P.out_b && xg < P.Wo;
         // invalid pixels (clipped by the TMA store) read the residual's first pixel instead
-        const bf16 *resp = !P.has_res ? nullptr
-                           : valid    ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
-                                         ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp
-                                      : (const bf16 *)P.res.p;
+        const bf16 *resp = !P.has_res || rt ? nullptr
+                           : valid          ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                                               ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp
+                                            : (const bf16 *)P.res.p;
         ptx::mbar_wait(tfull + acc, aphase);
         ptx::tc_fence_after();
 #pragma unroll 1
@@ -227,13 +242,22 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             }
             const bool ragged = cb + CH > P.c_real;   // channels >= c_real get 0 (affine) / no bias
             ptx::tmem_ld_wait();
-            if (leader) bulk_wait_read1();             // the store that last used this buffer has read it
-            epi_bar_n<NE>();
             const uint32_t buf = ptx::smem_u32(stage_out + sbuf * kOutStage + m * 128);
             const int chunk0 = hh * (CH / 8);
+            if (rt) {
+                ptx::mbar_wait(rbar, rphase);          // residual tile of this group in buf
+                rphase ^= 1;
+#pragma unroll
+                for (int c = 0; c < CH / 8; ++c) pr[c] = ld_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4));
+                epi_bar_n<NE>();                       // every thread has read its residual row
+            } else {
+                if (leader) bulk_wait_read1();         // the store that last used this buffer has read it
+                epi_bar_n<NE>();
+            }
             if (!ragged && P.epi == 1 && !P.has_res) epi_fast<CH, 1, false>(v, pb, pe, pr, lo, buf, chunk0, m);
             else if (!ragged && P.epi == 2 && !P.has_res) epi_fast<CH, 2, false>(v, pb, pe, pr, lo, buf, chunk0, m);
             else if (!ragged && P.epi == 2 && P.has_res) epi_fast<CH, 2, true>(v, pb, pe, pr, lo, buf, chunk0, m);
+            else if (!ragged && P.epi == 1 && P.has_res) epi_fast<CH, 1, true>(v, pb, pe, pr, lo, buf, chunk0, m);
             else if (!ragged && P.epi == 0 && !P.has_res) epi_fast<CH, 0, false>(v, pb, pe, pr, lo, buf, chunk0, m);
             else {
 #pragma unroll
@@ -262,6 +286,10 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             if (leader && !(P.dbg & 1)) {
                 tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, xg0, yg0 - P.out.base, b);
                 bulk_commit();
+            }
+            if (rt && leader) {   // prefetch the next group's residual into the other buffer
+                if (grp + 1 < BN / 64 && nb + 64 < P.n_out) res_load(tile, grp + 1, sbuf ^ 1);
+                else if (tile + (int)gridDim.x < num_tiles) res_load(tile + gridDim.x, 0, sbuf ^ 1);
             }
             sbuf ^= 1;
         }
@@ -525,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
+        if (P.tma_out) conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
     }
@@ -1666,6 +1694,11 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     static const int tma_dg = env_int("LRCNN_TMA_DG", 1);
     CUtensorMap G = A;
     P.tma_dg = 0;
+    P.tma_res = 0;
+    static const int tma_res = env_int("LRCNN_TMA_RES", 1);
+    if (tma_res && P.tma_out && P.has_res && P.res.Cp == P.out.Cp && P.n_out % 64 == 0 && aligned16(P.res.p) &&
+        encode_view(&G, P.res, P.B, P.TW, P.TH))
+        P.tma_res = 1;
     if (tma_dg && P.mode == 1 && P.o_stride == 1 && P.out.Cp % 64 == 0 && P.n_out == P.out.Cp &&
         (!P.gate || (P.act.Cp == P.out.Cp && aligned16(P.act.p)))) {
         View ov = P.out;
