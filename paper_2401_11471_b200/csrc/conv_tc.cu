@@ -100,6 +100,7 @@ struct TcWgrad {
 };
 
 static constexpr int kThreads = 192;
+static constexpr int kConvThreads = 320;      // k_conv_tc: producer, MMA, 8 epilogue warps
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
 static constexpr int kStageBudget = 192 * 1024;
@@ -305,12 +306,13 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
 // conv input (and, when its producer applies ReLU, the activation tile) is TMA-loaded into
 // smem, combined with the accumulator (gate-on-write: delta = gate(act) * (delta + acc)) in
 // place and TMA-stored back; rows >= out_b / columns >= W are clipped by the maps.
-template <int BN>
+template <int BN, int NE = 4>
 __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
                                                      uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
                                                      uint8_t *stage_out, uint64_t *ebar, int warp, int lane) {
+    constexpr int CH = 64 * 4 / NE;           // channels of a 64-channel group per thread
     const int num_tiles = P.m_tiles * P.n_tiles;
-    const int q = warp & 3, m = q * 32 + lane;
+    const int q = warp & 3, m = q * 32 + lane, hh = (warp - 2) >> 2;
     const bool leader = (warp == 2 && lane == 0);
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     uint8_t *bufD = stage_out, *bufG = stage_out + kOutStage;
@@ -334,14 +336,16 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
 #pragma unroll 1
         for (int grp = 0; grp < ngrp; ++grp) {
             const int nb = n0 + grp * 64;
-            uint32_t v[64];
-            ptx::tmem_ld32(tq + acc * BN + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-            ptx::tmem_ld32(tq + acc * BN + grp * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            uint32_t v[CH];
+#pragma unroll
+            for (int h = 0; h < CH / 32; ++h)
+                ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
             ptx::tmem_ld_wait();
             ptx::mbar_wait(ebar, ephase);
             ephase ^= 1;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int cc = 0; cc < CH / 8; ++cc) {
+                const int c = hh * (CH / 8) + cc;
                 const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
                 const uint4 dd = ld_shared_v4(rowD + off);
                 const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
@@ -349,8 +353,8 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
                 uint32_t o[4];
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    float x0 = __uint_as_float(v[c * 8 + 2 * h]) + bf_lo(dw[h]);
-                    float x1 = __uint_as_float(v[c * 8 + 2 * h + 1]) + bf_hi(dw[h]);
+                    float x0 = __uint_as_float(v[cc * 8 + 2 * h]) + bf_lo(dw[h]);
+                    float x1 = __uint_as_float(v[cc * 8 + 2 * h + 1]) + bf_hi(dw[h]);
                     if (P.gate) {
                         if (!(bf_lo(gw[h]) > 0.f)) x0 = 0.f;
                         if (!(bf_hi(gw[h]) > 0.f)) x1 = 0.f;
@@ -360,7 +364,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
                 st_shared_v4(rowD + off, make_uint4(o[0], o[1], o[2], o[3]));
             }
             fence_async_smem();
-            epi_bar();
+            epi_bar_n<NE>();
             if (leader) {
                 tma_store_4d(tmO, bufD, nb, xg0, yg0 - P.out.base, b);
                 bulk_commit();
@@ -382,12 +386,13 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
 
 // Epilogue warps (4 warps = 128 TMEM lanes = 128 pixels of the tile): tcgen05.ld the
 // accumulator in 32-column chunks, apply the fused epilogue, 16-byte bf16 stores.
-template <int BN>
+template <int BN, int NE = 4>
 __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
                                               int warp, int lane) {
     const int num_tiles = P.m_tiles * P.n_tiles;
     const int ew = warp & 3;                  // TMEM lane quarter this warp may access
     const int m = ew * 32 + lane;             // accumulator row = pixel in the tile
+    const int hh = (warp - 2) >> 2;           // NE = 8: two warps per quarter split the 32-column chunks
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -400,7 +405,7 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
         ptx::mbar_wait(tfull + acc, aphase);
         ptx::tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = NE == 8 ? hh : 0; c < BN / 32; c += NE / 4) {
             uint32_t v[32];
             ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
             ptx::tmem_ld_wait();
@@ -470,7 +475,7 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
 // regular layers, 16 (32-byte rows, SWIZZLE_32B, 1 MMA) for small-channel layers (padded RGB
 // input of conv1_1 / the 7x7 stem), which would otherwise waste 8x tensor work on zero channels.
 template <int BN, int KC>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
     using Cfg = ConvCfg<BN, KC>;
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
-        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
         ptx::mbar_init(ebar, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
@@ -553,9 +558,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
-        else if (P.tma_dg) conv_epilogue_tma_dg<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
-        else conv_epilogue<BN>(P, tmem, tfull, tempty, warp, lane);
+        if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -1568,7 +1573,7 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_tc<BN, KC><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, O, G, P);
+    k_conv_tc<BN, KC><<<grid, kConvThreads, Cfg::kSmem, st>>>(A, Bm, O, G, P);
     return true;
 }
 
