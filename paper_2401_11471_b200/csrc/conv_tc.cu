@@ -91,7 +91,9 @@ static inline void tile_div_init(TcConv &P) {
 struct TcWgrad {
     float *dw;
     const bf16 *gamma;
-    float *db;             // row-halo kernel: fused bias gradient (items with ky == 0, ci tile 0)
+    float *db;             // fused bias / beta gradient (items with ky == 0 / tap == 0 and ci tile 0)
+    float *dg;             // fused gamma gradient: dgamma[co] = sum_{tap,ci} W[co][tap][ci] * (sum_p dy x)
+    const bf16 *w;
     int k, pad, c_out, cin_p;
     int TW, TH, tiles_x, tiles_y, pix_tiles, per_split, splits;
     int co_tiles, ci_tiles, items;
@@ -889,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *tslot = (uint32_t *)(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, P.db ? 5 : 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmD);
@@ -973,12 +975,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m = ew * 32 + lane;
         int acc = 0;
         uint32_t aphase = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             int cot, tap, cit, split;
             decode(item, cot, tap, cit, split);
             const int co = cot * 128 + m;
             const float gsc = (P.gamma && co < P.c_out) ? __bfloat162float(P.gamma[co]) : 1.f;
             float *dst = P.dw + ((long long)co * taps + tap) * P.cin_p;
+            const bf16 *wrow = P.w + ((long long)co * taps + tap) * P.cin_p;
+            float gdot = 0.f;
+            if (P.db) {   // fused bias / beta gradient: sum the delta column m of every pixel tile
+                const bool want = tap == 0 && cit == 0;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float sum = 0.f;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    if (want) {
+                        const uint32_t base = ptx::smem_u32(smem + stage * SB);
+#pragma unroll 8
+                        for (int r = 0; r < 128; ++r) {
+                            unsigned short h;
+                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + r * 128 + (col ^ ((r & 7) << 4))));
+                            sum += __uint_as_float((uint32_t)h << 16);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
+            }
             ptx::mbar_wait(tfull + acc, aphase);
             ptx::tc_fence_after();
             if constexpr (BN < 32) {
@@ -989,7 +1017,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int ci0 = cit * BN;
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (ci0 + j < P.cin_p) atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                        if (ci0 + j < P.cin_p) {
+                            atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                            if (P.dg) gdot += __uint_as_float(v[j]) * __bfloat162float(wrow[ci0 + j]);
+                        }
                 }
             } else {
 #pragma unroll 1
@@ -1001,9 +1032,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int ci0 = cit * BN + c * 32;
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (ci0 + j < P.cin_p) atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                        if (ci0 + j < P.cin_p) {
+                            atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
+                            if (P.dg) gdot += __uint_as_float(v[j]) * __bfloat162float(wrow[ci0 + j]);
+                        }
                 }
             }
+            if (P.dg && co < P.c_out) atomicAdd(P.dg + co, gdot);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty + acc);
@@ -1184,9 +1219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
+            float gdot = 0.f;
 #pragma unroll 1
             for (int kx = 0; kx < KW; ++kx) {
                 float *dst = P.dw + ((long long)co * taps + ky * KW + kx) * P.cin_p + cit * BN;
+                const bf16 *wrow = P.w + ((long long)co * taps + ky * KW + kx) * P.cin_p + cit * BN;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
@@ -1196,11 +1233,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int ci0 = cit * BN + c * 32;
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
-                        if (ci0 + j < P.cin_p)
+                        if (ci0 + j < P.cin_p) {
                             red_add_v4(dst + c * 32 + j, __uint_as_float(v[j]) * gsc, __uint_as_float(v[j + 1]) * gsc,
                                        __uint_as_float(v[j + 2]) * gsc, __uint_as_float(v[j + 3]) * gsc);
+                            if (P.dg) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    gdot += __uint_as_float(v[j + q]) * __bfloat162float(wrow[c * 32 + j + q]);
+                            }
+                        }
                 }
             }
+            if (P.dg && co < P.c_out) atomicAdd(P.dg + co, gdot);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty);
@@ -1882,6 +1926,9 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     P.s = 1;
     static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
     P.db = fuse_db ? a.db : nullptr;
+    P.dg = fuse_db && a.db ? a.dg : nullptr;
+    P.w = (const bf16 *)a.w;
+    if (P.dg && !P.w) P.db = P.dg = nullptr;
     // 128-pixel tile, TW a multiple of 16 (one K-step = 16 pixels of one output row)
     long best = -1;
     for (int tw = 128; tw >= 16; tw >>= 1) {
@@ -1967,6 +2014,11 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = a.s;
+    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
+    P.db = fuse_db ? a.db : nullptr;
+    P.dg = fuse_db && a.db ? a.dg : nullptr;
+    P.w = (const bf16 *)a.w;
+    if (P.dg && !P.w) P.db = P.dg = nullptr;
     pick_tile(rows, dy.W, a.s, P.TW, P.TH);
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
@@ -1985,9 +2037,10 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     CUtensorMap D, X;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
     if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s, BN < 64 ? BN : 64)) return false;
-    if (BN == 16) return launch_wgrad<16>(P, D, X, st);
-    if (BN == 64) return launch_wgrad<64>(P, D, X, st);
-    return launch_wgrad<128>(P, D, X, st);
+    const bool ok = BN == 16 ? launch_wgrad<16>(P, D, X, st)
+                  : BN == 64 ? launch_wgrad<64>(P, D, X, st) : launch_wgrad<128>(P, D, X, st);
+    if (ok && P.db) a.db_done = true;
+    return ok;
 }
 
 }  // namespace lrcnn

@@ -315,8 +315,10 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             WgradArgs A;
             A.dy = dy; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
             A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
-            // VGG bias gradient fused into the row-halo wgrad kernel when it takes the op
+            // bias (VGG) or affine (ResNet) parameter gradients fused into the tensor-core wgrad:
+            // db / dbeta = sum dy, dgamma = sum_{tap,ci} W * (sum_p dy x)
             if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
+            if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
             ++P.launches;
             ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2);
             if (P.use_tc && tc_conv_wgrad(A, gst)) ++P.tc_launches;

@@ -43,8 +43,10 @@ struct WgradArgs {
     View dy, x;
     float *dw = nullptr;       // [Cout][k][k][Cin_p] fp32, accumulated
     const void *gamma = nullptr;
-    float *db = nullptr;       // optional: bias gradient sum_pixels dy[., co] fused into the kernel
-    mutable bool db_done = false;   // set by a launcher that accumulated db
+    float *db = nullptr;       // optional: bias (or affine beta) gradient sum_pixels dy[., co], fused
+    float *dg = nullptr;       // optional: affine gamma gradient, fused as sum_{tap,ci} W * (sum_p dy x)
+    const void *w = nullptr;   // weights [Cout][k][k][Cin_p] (for dg)
+    mutable bool db_done = false;   // set by a launcher that accumulated db (and dg when requested)
     int k, s, p, c_out;
     int a, b;                  // output rows contributing
     int B;
