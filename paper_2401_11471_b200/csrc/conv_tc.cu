@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -58,6 +59,7 @@ struct TcConv {
     int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
     int tw_log2;           // TW = 1 << tw_log2
+    int pat_w, pat_h, pat_ox, pat_oy;   // im2col kernel: input patch per tile (pixels) and its offset
     uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
     // tile index -> (n tile, tile column, tile row, image); n tiles vary fastest
     __device__ __forceinline__ void decode(int tile, int &nt, int &tx, int &ty, int &b) const {
@@ -575,36 +577,44 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // ------------------------------------------------------------------ small-channel conv FP (im2col in smem)
 // Layers whose input has cin_p = 8 channels (the padded RGB image: conv1_1 of VGG-16, the 7x7/s2
 // stem of ResNet-50).  The contraction index is K = tap x 8 channels; one pipeline stage holds
-// 8 taps: row m of the 16 KB stage (SWIZZLE_128B, K-major) is output pixel m's 8 taps x 16 bytes,
-// gathered by 4 producer warps with coalesced 16-byte loads (zeros for padding rows/columns, rows
-// outside the band and taps >= k*k).  The weights viewed as [cout][k*k*8] are TMA-loaded once per
-// CTA and stay resident.  Per 128-pixel tile this is ceil(k*k/2) MMAs of K=16 (5 for 3x3) instead
-// of k*k TMA boxes with half of every box zero-filled channels.
-// Warps 0-7 gather (pixel x half of the stage's taps), warp 8 TMEM + MMA issue, warps 9-16 the
+// 8 taps: row m of the 16 KB stage (SWIZZLE_128B, K-major) is output pixel m's 8 taps x 16 bytes.
+// The input patch a tile reads ((TW-1)s+k x (TH-1)s+k pixels x 16 bytes, at most 16 KB) is ONE
+// TMA box per tile (double-buffered; out-of-bounds rows/columns = the semi-closed zero padding,
+// PAPER.md:235), and the 8 gather warps build the im2col stages from it with shared-memory
+// copies (a quarter-warp moves 8 consecutive pixels of one tap: conflict-free 16-byte accesses).
+// The weights viewed as [cout][k*k*8] are TMA-loaded once per CTA and stay resident.  Per
+// 128-pixel tile this is ceil(k*k/2) MMAs of K=16 (5 for 3x3).
+// Warps 0-7 gather, warp 8 TMEM + MMA issue, warp 9 patch TMA producer, warps 10-17 the
 // TMA-store epilogue.
-static constexpr int kI2cGather = 8;                          // gather warps (2 per 32-pixel quarter)
+static constexpr int kI2cGather = 8;                          // gather warps
 static constexpr int kI2cMmaWarp = kI2cGather;
+static constexpr int kI2cPatchWarp = kI2cGather + 1;
 static constexpr int kI2cEpi = 8;
-static constexpr int kI2cThreads = (kI2cGather + 1 + kI2cEpi) * 32;
-static constexpr int kI2cStages = 6;
+static constexpr int kI2pThreads = (kI2cGather + 2 + kI2cEpi) * 32;        // k_conv_im2col
+static constexpr int kI2cStages = 4;
 static constexpr int kI2cStage = 128 * 128;
 static constexpr int kI2cBMax = 64 * 1024;
-static constexpr int kI2cSmem = kI2cStages * kI2cStage + kI2cBMax + 2 * kOutStage + 1024 + 256;
+static constexpr int kI2cPatch = 16 * 1024;                   // one input patch buffer (<= 1024 pixels)
+static constexpr int kI2cSmem = kI2cStages * kI2cStage + kI2cBMax + 2 * kOutStage + 2 * kI2cPatch + 1024 + 256;
 
 template <int BN>
-__global__ void __launch_bounds__(kI2cThreads, 1)
-    k_conv_im2col(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmO, const TcConv P) {
+__global__ void __launch_bounds__(kI2pThreads, 1)
+    k_conv_im2col(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmO,
+                  const __grid_constant__ CUtensorMap tmP, const TcConv P) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
     uint8_t *sB = sA + kI2cStages * kI2cStage;
     uint8_t *sO = sB + kI2cBMax;
-    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
+    uint8_t *sP = sO + 2 * kOutStage;
+    uint64_t *full = (uint64_t *)(sP + 2 * kI2cPatch);
     uint64_t *empty = full + kI2cStages;
     uint64_t *tfull = empty + kI2cStages;
     uint64_t *tempty = tfull + 2;
     uint64_t *bfull = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(bfull + 1);
+    uint64_t *pfull = bfull + 1;
+    uint64_t *pempty = pfull + 2;
+    uint32_t *tslot = (uint32_t *)(pempty + 2);
     const int KS = (P.ntaps + 7) / 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -613,10 +623,12 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
             ptx::mbar_init(empty + i, 1);
         }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, kI2cEpi); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(pfull + i, 1); ptx::mbar_init(pempty + i, kI2cGather * 32); }
         ptx::mbar_init(bfull, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmB);
         ptx::prefetch_tmap(&tmO);
+        ptx::prefetch_tmap(&tmP);
     }
     if (warp == kI2cMmaWarp) ptx::tmem_alloc(tslot, 2 * BN);
     ptx::tc_fence_before();
@@ -632,52 +644,57 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
                 for (int ks = 0; ks < KS; ++ks)
                     ptx::tma_load_2d(sB + (nt * KS + ks) * BN * 128, &tmB, bfull, ks * 64, nt * BN);
         }
-        // thread = (tap slot c of the stage, pixels pg + 32 i): the tap's offsets are per-stage
-        // constants, each pixel is decoded once per tile
-        const int c = threadIdx.x & 7, pg = threadIdx.x >> 3;
-        const View &in = P.in;
-        const int W = in.W;
-        const int ylo = max(0, in.base), yhi = min(in.H, in.base + in.rows);
-        const uint4 *src = (const uint4 *)in.p;   // 8 bf16 channels = one 16-byte pixel
-        const uint32_t a_base = ptx::smem_u32(sA);
+        // thread = (tap slot c, pixels m0 + 32 i): a quarter-warp covers 8 consecutive pixels of
+        // one tap, so both the patch reads and the swizzled stage writes are conflict-free
+        const int c = (threadIdx.x >> 3) & 7, m0 = (threadIdx.x & 7) + 8 * (threadIdx.x >> 6);
         const int twm = (1 << P.tw_log2) - 1;
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            int nt, tx, ty, b;
-            P.decode(tile, nt, tx, ty, b);
-            int yi[4], xi[4];
-            const uint4 *pp[4];
+        int poff[4];   // patch pixel index of this thread's 4 output pixels (tap (0,0) of the patch)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int m = pg + 32 * i;
-                const int yo = P.out_a + ty * P.TH + (m >> P.tw_log2), xo = tx * P.TW + (m & twm);
-                const bool valid = yo < P.out_b && xo < P.Wo;
-                yi[i] = valid ? yo * P.a_mul : -(1 << 20);     // invalid pixel: every tap out of range
-                xi[i] = xo * P.a_mul;
-                pp[i] = src + (long long)b * (in.bs >> 3) + (long long)(yi[i] - in.base) * W + xi[i];
-            }
+        for (int i = 0; i < 4; ++i) {
+            const int m = m0 + 32 * i;
+            poff[i] = (m >> P.tw_log2) * P.a_mul * P.pat_w + (m & twm) * P.a_mul;
+        }
+        const uint32_t a_base = ptx::smem_u32(sA), p_base = ptx::smem_u32(sP);
+        int stage = 0, pb = 0;
+        uint32_t phase = 0, pphase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            ptx::mbar_wait(pfull + pb, pphase);
+            const uint32_t pbase = p_base + pb * kI2cPatch;
             for (int ks = 0; ks < KS; ++ks) {
                 const int tap = ks * 8 + c;
                 const bool tv = tap < P.ntaps && !(P.dbg & 4);
-                const int dy = tv ? P.tap_oy[tap] : 0, dx = tv ? P.tap_ox[tap] : 0;
+                const int toff = tv ? (P.tap_oy[tap] - P.pat_oy) * P.pat_w + P.tap_ox[tap] - P.pat_ox : 0;
                 uint4 v[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int iy = yi[i] + dy, ix = xi[i] + dx;
-                    v[i] = make_uint4(0, 0, 0, 0);
-                    if (tv && iy >= ylo && iy < yhi && ix >= 0 && ix < W) v[i] = __ldg(pp[i] + dy * W + dx);
-                }
+                for (int i = 0; i < 4; ++i)
+                    v[i] = tv ? ld_shared_v4(pbase + (uint32_t)(poff[i] + toff) * 16u) : make_uint4(0, 0, 0, 0);
                 ptx::mbar_wait(empty + stage, phase ^ 1);
                 const uint32_t sa = a_base + stage * kI2cStage;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int m = pg + 32 * i;
+                    const int m = m0 + 32 * i;
                     st_shared_v4(sa + m * 128 + ((c ^ (m & 7)) << 4), v[i]);
                 }
                 fence_async_smem();
                 ptx::mbar_arrive(full + stage);
                 if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
+            }
+            ptx::mbar_arrive(pempty + pb);          // this thread is done with the patch
+            if (++pb == 2) { pb = 0; pphase ^= 1; }
+        }
+    } else if (warp == kI2cPatchWarp) {
+        if (lane == 0) {
+            const uint32_t pbytes = (uint32_t)P.pat_w * P.pat_h * 16;
+            int pb = 0;
+            uint32_t pphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int nt, tx, ty, b;
+                P.decode(tile, nt, tx, ty, b);
+                ptx::mbar_wait(pempty + pb, pphase ^ 1);
+                ptx::mbar_arrive_expect_tx(pfull + pb, pbytes);
+                ptx::tma_load_4d(sP + pb * kI2cPatch, &tmP, pfull + pb, 0, tx * P.TW * P.a_mul + P.pat_ox,
+                                 (P.out_a + ty * P.TH) * P.a_mul + P.pat_oy - P.in_base, b);
+                if (++pb == 2) { pb = 0; pphase ^= 1; }
             }
         }
     } else if (warp == kI2cMmaWarp) {
@@ -710,11 +727,133 @@ __global__ void __launch_bounds__(kI2cThreads, 1)
             }
         }
     } else {
-        conv_epilogue_tma<BN, kI2cEpi>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, kI2cMmaWarp + 1);
+        conv_epilogue_tma<BN, kI2cEpi>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, kI2cPatchWarp + 1);
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == kI2cMmaWarp) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 2 * BN);
+    }
+}
+
+// ------------------------------------------------------------------ small-channel conv FP: tap pairs
+// 8-channel inputs (the padded RGB image) without any im2col copy.  An input pixel is 8 bf16 =
+// 16 bytes = one K-chunk of a K-major no-swizzle UMMA operand, whose core matrix is 8 rows x 16 B
+// at a 16 B row stride.  The tile is 8 output columns x 16 output rows; its input patch is TMA-
+// loaded into smem as dense [row][pixel] planes, and the A operand of a K=16 MMA is the pair of
+// taps (ky, kx) and (ky, kx+1), read straight out of the patch by a descriptor:
+//   stride 1: one plane; tap kx of output column i is pixel i+kx, so the 8 output columns are 8
+//             consecutive 16 B pixels (a core matrix) and the second tap of the pair is the same
+//             matrix one pixel on (LBO = 16 B; the core matrices of the two K-halves overlap);
+//   stride 2: two planes, the even- and odd-offset columns of the patch (two TMA loads with element
+//             stride 2); tap kx = 2j (+1) of output column i is plane A (B) pixel i+j, so LBO =
+//             plane B - plane A.
+// Consecutive output rows (8-row core-matrix groups) are s patch rows apart (SBO).  Per tile:
+// ceil(k/2)*k MMAs (6 for 3x3, 28 for the 7x7 stem; the odd tap of the last pair has zero
+// weights), one patch box of at most 16 KB, no register traffic for the operand at all.  The
+// weights [c_out][k][k][8] are TMA-loaded once per CTA as 1 KB chunks (64 rows x 16 B), the
+// chunk of a pair's odd tap kx = k reads as zero (out-of-bounds).
+static constexpr int kPrStages = 4;
+static constexpr int kPrPatch = 16 * 1024;
+static constexpr int kPrBMax = 7 * 4 * 2048;          // 7 rows x 4 pairs x 2 chunks x 1 KB
+static constexpr int kPrSmem = kPrStages * kPrPatch + kPrBMax + 2 * kOutStage + 1024 + 256;
+
+__global__ void __launch_bounds__(kConvThreads, 1)
+    k_conv_pair(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
+                const __grid_constant__ CUtensorMap tmO, const TcConv P) {
+    constexpr int BN = 64;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sP = smem;
+    uint8_t *sB = sP + kPrStages * kPrPatch;
+    uint8_t *sO = sB + kPrBMax;
+    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
+    uint64_t *empty = full + kPrStages;
+    uint64_t *tfull = empty + kPrStages;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *bfull = tempty + 2;
+    uint32_t *tslot = (uint32_t *)(bfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KY = P.k, NPR = (P.k + 1) / 2, s = P.a_mul;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPrStages; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
+        ptx::mbar_init(bfull, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmP);
+        ptx::prefetch_tmap(&tmW);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, 2 * BN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int num_tiles = P.m_tiles;
+    const uint32_t plane = (uint32_t)P.pat_w * P.pat_h * 16;   // bytes of one plane
+    const uint32_t pstride = (plane + 127) & ~127u;             // plane B offset (TMA: 128 B aligned)
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // weights: chunk (ky, pair j, half h) = tap (ky, 2j+h) for all 64 rows, 1 KB each
+            ptx::mbar_arrive_expect_tx(bfull, KY * NPR * 2 * 1024);
+            for (int ky = 0; ky < KY; ++ky)
+                for (int j = 0; j < NPR; ++j)
+                    for (int h = 0; h < 2; ++h)
+                        ptx::tma_load_4d(sB + ((ky * NPR + j) * 2 + h) * 1024, &tmW, bfull, 0, 2 * j + h, ky, 0);
+            int st = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int nt, tx, ty, b;
+                P.decode(tile, nt, tx, ty, b);
+                const int xs = tx * 8 * s + P.pat_ox, ys = (P.out_a + ty * 16) * s + P.pat_oy - P.in_base;
+                ptx::mbar_wait(empty + st, ph ^ 1);
+                ptx::mbar_arrive_expect_tx(full + st, s * plane);
+                ptx::tma_load_4d(sP + st * kPrPatch, &tmP, full + st, 0, xs, ys, b);
+                if (s == 2) ptx::tma_load_4d(sP + st * kPrPatch + pstride, &tmP, full + st, 0, xs + 1, ys, b);
+                if (++st == kPrStages) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+            const uint32_t row = (uint32_t)P.pat_w * 16;                 // bytes per patch row (one plane)
+            const uint32_t lbo = s == 1 ? 16u : pstride;
+            const bool sw = P.dbg & 8;   // debug: exchange the LBO / SBO roles
+            const uint64_t dA = sw ? ptx::smem_desc(ptx::smem_u32(sP), s * row, lbo, 0)
+                                   : ptx::smem_desc(ptx::smem_u32(sP), lbo, s * row, 0);
+            const uint64_t dB = sw ? ptx::smem_desc(ptx::smem_u32(sB), 128, 1024, 0)
+                                   : ptx::smem_desc(ptx::smem_u32(sB), 1024, 128, 0);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            ptx::mbar_wait(bfull, 0);
+            int st = 0, acc = 0;
+            uint32_t ph = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                ptx::mbar_wait(full + st, ph);
+                ptx::tc_fence_after();
+                const uint32_t a0 = (uint32_t)dA + st * (kPrPatch >> 4);
+                for (int ky = 0; ky < KY; ++ky)
+                    for (int j = 0; j < NPR; ++j) {
+                        // first K-half: tap kx = 2j -> plane A pixel i + (s == 1 ? 2j : j)
+                        const uint32_t at = a0 + (ky * row + (uint32_t)(s == 1 ? 2 * j : j) * 16) / 16;
+                        const uint32_t bt = (uint32_t)dB + (ky * NPR + j) * (2048 >> 4);
+                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, at, hiA, bt, hiB, idesc, (ky | j) != 0);
+                    }
+                ptx::umma_commit(empty + st);
+                if (++st == kPrStages) { st = 0; ph ^= 1; }
+                ptx::umma_commit(tfull + acc);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 2 * BN);
     }
@@ -1263,8 +1402,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // dW[co][tap][ci] = sum_pixels dY[p][co] X[p + off(tap)][ci] for the padded RGB layer:
 // D[m = (tap - 16*mt)*8 + ci][co] (M = 128 = 16 taps x 8 channels, N = c_out) accumulates over
 // K = output pixels.  Per 128-pixel tile the A operand (M-major: per pixel 16 taps x 16 bytes in
-// two 64-element chunks, SWIZZLE_128B) is gathered by 8 warps with 16-byte loads exactly as the
-// FP im2col kernel does; the band delta is one TMA box per tile (MN-major B).
+// two 64-element chunks, SWIZZLE_128B) is copied by 8 gather warps out of the tile's input patch,
+// which one producer warp TMA-loads (double-buffered, as in k_conv_im2col); pixels outside the
+// band contribute zero.  The band delta is one TMA box per tile (MN-major B).
 struct TcWgI2c {
     View in;
     float *dw;
@@ -1273,29 +1413,38 @@ struct TcWgI2c {
     int tap_oy[49], tap_ox[49];
     int TW, TH, tw_log2, tiles_x, tiles_y, pix_tiles, per_split, splits, items;
     int out_a, out_b, Wo, dy_base;
+    int pat_w, pat_h, pat_ox, pat_oy, in_base;
 };
 static constexpr int kWiStages = 4;
 static constexpr int kWiStage = 2 * 16384 + 16384;                 // A: 2 chunks x 16 KB, B: 16 KB
-static constexpr int kWiSmem = kWiStages * kWiStage + 1024 + 256;
+static constexpr int kWiThreads = (kI2cGather + 1 + 4 + 1) * 32;   // gather, MMA, 4 epilogue, patch
+static constexpr int kWiPatchWarp = kI2cGather + 5;
+static constexpr int kWiSmem = kWiStages * kWiStage + 2 * kI2cPatch + 1024 + 256;
 
 template <int BN>
-__global__ void __launch_bounds__(kI2cThreads - 4 * 32, 1)
-    k_wgrad_im2col(const __grid_constant__ CUtensorMap tmD, const TcWgI2c P) {
+__global__ void __launch_bounds__(kWiThreads, 1)
+    k_wgrad_im2col(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP,
+                   const TcWgI2c P) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *full = (uint64_t *)(smem + kWiStages * kWiStage);
+    uint8_t *sP = smem + kWiStages * kWiStage;
+    uint64_t *full = (uint64_t *)(sP + 2 * kI2cPatch);
     uint64_t *empty = full + kWiStages;
     uint64_t *tfull = empty + kWiStages;
     uint64_t *tempty = tfull + 1;
-    uint32_t *tslot = (uint32_t *)(tempty + 1);
+    uint64_t *pfull = tempty + 1;
+    uint64_t *pempty = pfull + 2;
+    uint32_t *tslot = (uint32_t *)(pempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int kMma = kI2cGather;                  // warp 8; epilogue warps 9..12
+    constexpr int kMma = kI2cGather;                  // warp 8; epilogue warps 9..12; patch warp 13
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWiStages; ++i) { ptx::mbar_init(full + i, kI2cGather * 32 + 1); ptx::mbar_init(empty + i, 1); }
         ptx::mbar_init(tfull, 1);
         ptx::mbar_init(tempty, 4);
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(pfull + i, 1); ptx::mbar_init(pempty + i, kI2cGather * 32); }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmD);
+        ptx::prefetch_tmap(&tmP);
     }
     if (warp == kMma) ptx::tmem_alloc(tslot, BN < 32 ? 32 : BN);
     ptx::tc_fence_before();
@@ -1305,61 +1454,80 @@ __global__ void __launch_bounds__(kI2cThreads - 4 * 32, 1)
     const int twm = (1 << P.tw_log2) - 1;
 
     if (warp < kI2cGather) {
-        const int c = threadIdx.x & 7, pg = threadIdx.x >> 3;
-        const View &in = P.in;
-        const int W = in.W;
-        const int ylo = max(0, in.base), yhi = min(in.H, in.base + in.rows);
-        const uint4 *src = (const uint4 *)in.p;
-        const uint32_t a_base = ptx::smem_u32(smem);
-        int stage = 0;
-        uint32_t phase = 0;
+        // thread = (tap slot c, pixels m0 + 32 i): a quarter-warp moves 8 consecutive pixels of one tap
+        const int c = (threadIdx.x >> 3) & 7, m0 = (threadIdx.x & 7) + 8 * (threadIdx.x >> 6);
+        int poff[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int m = m0 + 32 * i;
+            poff[i] = (m >> P.tw_log2) * P.a_mul * P.pat_w + (m & twm) * P.a_mul;
+        }
+        const uint32_t a_base = ptx::smem_u32(smem), p_base = ptx::smem_u32(sP);
+        int stage = 0, pb = 0;
+        uint32_t phase = 0, pphase = 0;
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             const int split = item % P.splits, mt = item / P.splits;
             const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
             // this thread's two taps of the m tile (chunk h = taps 16 mt + 8 h .. + 8)
-            int dy2[2], dx2[2];
+            int toff[2];
             bool tv[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int tap = mt * 16 + h * 8 + c;
                 tv[h] = tap < P.ntaps;
-                dy2[h] = tv[h] ? P.tap_oy[tap] : 0;
-                dx2[h] = tv[h] ? P.tap_ox[tap] : 0;
+                toff[h] = tv[h] ? (P.tap_oy[tap] - P.pat_oy) * P.pat_w + P.tap_ox[tap] - P.pat_ox : 0;
             }
             for (int pt = p0; pt < p1; ++pt) {
-                const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y;
+                ptx::mbar_wait(pfull + pb, pphase);
+                const uint32_t pbase = p_base + pb * kI2cPatch;
                 uint4 v[2][4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int m = pg + 32 * i;
-                    const int yo = P.out_a + ty * P.TH + (m >> P.tw_log2), xo = tx * P.TW + (m & twm);
-                    const bool valid = yo < P.out_b && xo < P.Wo;
-                    const int yi = yo * P.a_mul, xi = xo * P.a_mul;
-                    const uint4 *pp = src + (long long)b * (in.bs >> 3) + (long long)(yi - in.base) * W + xi;
+                    const int m = m0 + 32 * i;
+                    const bool valid = P.out_a + ty * P.TH + (m >> P.tw_log2) < P.out_b && tx * P.TW + (m & twm) < P.Wo;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int iy = yi + dy2[h], ix = xi + dx2[h];
-                        v[h][i] = make_uint4(0, 0, 0, 0);
-                        if (valid && tv[h] && iy >= ylo && iy < yhi && ix >= 0 && ix < W)
-                            v[h][i] = __ldg(pp + dy2[h] * W + dx2[h]);
-                    }
+                    for (int h = 0; h < 2; ++h)
+                        v[h][i] = valid && tv[h] ? ld_shared_v4(pbase + (uint32_t)(poff[i] + toff[h]) * 16u)
+                                                 : make_uint4(0, 0, 0, 0);
                 }
+                ptx::mbar_arrive(pempty + pb);
+                if (++pb == 2) { pb = 0; pphase ^= 1; }
                 ptx::mbar_wait(empty + stage, phase ^ 1);
                 uint8_t *st = smem + stage * kWiStage;
                 if (threadIdx.x == 0) {
+                    const int b = r / P.tiles_y;
                     ptx::mbar_arrive_expect_tx(full + stage, 16384);
                     ptx::tma_load_4d(st + 2 * 16384, &tmD, full + stage, 0, tx * P.TW, P.out_a + ty * P.TH - P.dy_base, b);
                 }
                 const uint32_t sa = a_base + stage * kWiStage;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int m = pg + 32 * i;
+                    const int m = m0 + 32 * i;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) st_shared_v4(sa + h * 16384 + m * 128 + ((c ^ (m & 7)) << 4), v[h][i]);
                 }
                 fence_async_smem();
                 ptx::mbar_arrive(full + stage);
                 if (++stage == kWiStages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == kWiPatchWarp) {
+        if (lane == 0) {
+            const uint32_t pbytes = (uint32_t)P.pat_w * P.pat_h * 16;
+            int pb = 0;
+            uint32_t pphase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                const int split = item % P.splits;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                for (int pt = p0; pt < p1; ++pt) {
+                    const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                    ptx::mbar_wait(pempty + pb, pphase ^ 1);
+                    ptx::mbar_arrive_expect_tx(pfull + pb, pbytes);
+                    ptx::tma_load_4d(sP + pb * kI2cPatch, &tmP, pfull + pb, 0, tx * P.TW * P.a_mul + P.pat_ox,
+                                     (P.out_a + ty * P.TH) * P.a_mul + P.pat_oy - P.in_base, b);
+                    if (++pb == 2) { pb = 0; pphase ^= 1; }
+                }
             }
         }
     } else if (warp == kMma) {
@@ -1780,7 +1948,8 @@ static bool encode_w2d(CUtensorMap *m, const void *w, int rows, int K, int BN) {
 }
 
 template <int BN>
-static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensorMap &O, int tiles, cudaStream_t st) {
+static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensorMap &O, const CUtensorMap &Pm,
+                          int tiles, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_conv_im2col<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI2cSmem) !=
@@ -1789,7 +1958,75 @@ static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensor
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_im2col<BN><<<grid, kI2cThreads, kI2cSmem, st>>>(Bm, O, P);
+    k_conv_im2col<BN><<<grid, kI2pThreads, kI2cSmem, st>>>(Bm, O, Pm, P);
+    return true;
+}
+
+// 4D map over an 8-channel band View with a (8, pw, ph, 1) box, no swizzle (16-byte pixels packed
+// densely in smem); rows outside the band's valid range [base, min(base+rows, H)) read as zero.
+static bool encode_patch(CUtensorMap *m, const View &v, int B, int pw, int ph, int es_w = 1) {
+    auto fn = encode_fn();
+    const int rows = v.rows < v.H - v.base ? v.rows : v.H - v.base;
+    if (!fn || rows <= 0 || pw * es_w > 256 || ph > 256) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)v.Cp, (cuuint64_t)v.W, (cuuint64_t)rows, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)v.Cp * 2, (cuuint64_t)v.W * v.Cp * 2, (cuuint64_t)v.bs * 2};
+    cuuint32_t box[4] = {(cuuint32_t)v.Cp, (cuuint32_t)(pw * es_w), (cuuint32_t)ph, 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)es_w, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// FP of an 8-channel-input k x k conv (stride 1 or 2, c_out <= 64) through k_conv_pair.
+static bool conv_pair(TcConv &P, const View &in, const void *w, int w_rows, cudaStream_t st) {
+    static const int on = env_int("LRCNN_PAIR", 1);
+    const int s = P.a_mul, k = P.k;
+    if (!on || in.Cp != 8 || P.mode != 0 || P.o_stride != 1 || P.n_out != 64 || P.out.Cp % 8 || w_rows > 64) return false;
+    if (k > 7 || s < 1 || s > 2 || P.ntaps != k * k || !aligned16(in.p) || !aligned16(w) || !aligned16(P.out.p) ||
+        (in.bs & 7))
+        return false;
+    const int rows = P.out_b - P.out_a;
+    if (rows <= 0 || P.Wo <= 0) return true;
+    const int npr = (k + 1) / 2;
+    P.in = in;
+    P.in_base = in.base;
+    P.dbg = env_int("LRCNN_TC_DBG", 0);
+    P.pat_w = s == 1 ? 7 + 2 * npr : 7 + npr;
+    P.pat_h = 15 * s + k;
+    P.pat_ox = -P.pad; P.pat_oy = -P.pad;
+    if (((P.pat_w * P.pat_h * 16 + 127) & ~127) * s > kPrPatch) return false;
+    P.n_tiles = 1;
+    P.TW = 8; P.TH = 16;
+    P.tiles_x = (P.Wo + 7) / 8;
+    P.tiles_y = (rows + 15) / 16;
+    P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    tile_div_init(P);
+    CUtensorMap Pm, Wm, O;
+    if (!encode_patch(&Pm, in, P.B, P.pat_w, P.pat_h, s)) return false;
+    {   // weights [w_rows][k][k][8] as (8, kx, ky, rows), box (8, 1, 1, 64): rows / kx >= k read as zero
+        auto fn = encode_fn();
+        if (!fn) return false;
+        cuuint64_t dims[4] = {8, (cuuint64_t)k, (cuuint64_t)k, (cuuint64_t)w_rows};
+        cuuint64_t strides[3] = {16, (cuuint64_t)k * 16, (cuuint64_t)k * k * 16};
+        cuuint32_t box[4] = {8, 1, 1, 64};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (fn(&Wm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(w), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    View ov = P.out;
+    ov.rows = P.out_b - P.out.base;
+    if (!encode_view(&O, ov, P.B, 8, 16)) return false;
+    P.tma_out = 1;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_conv_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrSmem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
+    k_conv_pair<<<grid, kConvThreads, kPrSmem, st>>>(Pm, Wm, O, P);
     return true;
 }
 
@@ -1808,21 +2045,39 @@ static bool conv_im2col(TcConv &P, const View &in, const void *w, int w_rows, cu
     P.in = in;
     P.in_base = in.base;
     P.dbg = env_int("LRCNN_TC_DBG", 0);
-    pick_tile(rows, P.Wo, 1, P.TW, P.TH);
+    // tap offset hull -> patch geometry; tile = the 128-pixel rectangle with the fewest padded
+    // pixels whose patch fits one 16 KB buffer
+    int oy0 = 1 << 20, oy1 = -(1 << 20), ox0 = 1 << 20, ox1 = -(1 << 20);
+    for (int t = 0; t < P.ntaps; ++t) {
+        oy0 = std::min(oy0, P.tap_oy[t]); oy1 = std::max(oy1, P.tap_oy[t]);
+        ox0 = std::min(ox0, P.tap_ox[t]); ox1 = std::max(ox1, P.tap_ox[t]);
+    }
+    const int s = P.a_mul;
+    long best = -1;
+    for (int tw = 128; tw >= 4; tw >>= 1) {
+        const int th = 128 / tw;
+        const int pw = (tw - 1) * s + ox1 - ox0 + 1, ph = (th - 1) * s + oy1 - oy0 + 1;
+        if (pw > 256 || ph > 256 || pw * ph * 16 > kI2cPatch) continue;
+        long cost = (long)((P.Wo + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+        if (best < 0 || cost < best) { best = cost; P.TW = tw; P.TH = th; P.pat_w = pw; P.pat_h = ph; }
+    }
+    if (best < 0) return false;
+    P.pat_ox = ox0; P.pat_oy = oy0;
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
     tile_div_init(P);
-    CUtensorMap Bm, O;
+    CUtensorMap Bm, O, Pm;
     if (!encode_w2d(&Bm, w, w_rows, P.ntaps * 8, BN)) return false;
+    if (!encode_patch(&Pm, in, P.B, P.pat_w, P.pat_h)) return false;
     View ov = P.out;
     ov.rows = P.out_b - P.out.base;
     if (!encode_view(&O, ov, P.B, P.TW, P.TH)) return false;
     P.tma_out = 1;
     const int tiles = P.m_tiles * P.n_tiles;
-    if (BN == 64) return launch_im2col<64>(P, Bm, O, tiles, st);
-    if (BN == 128) return launch_im2col<128>(P, Bm, O, tiles, st);
-    return launch_im2col<256>(P, Bm, O, tiles, st);
+    if (BN == 64) return launch_im2col<64>(P, Bm, O, Pm, tiles, st);
+    if (BN == 128) return launch_im2col<128>(P, Bm, O, Pm, tiles, st);
+    return launch_im2col<256>(P, Bm, O, Pm, tiles, st);
 }
 
 bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
@@ -1843,6 +2098,7 @@ bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st) {
             P.tap_oy[t] = ky - a.p; P.tap_ox[t] = kx - a.p; P.tap_w[t] = t;
         }
     P.k = a.k; P.pad = a.p; P.halo_ok = a.s == 1 && a.k == 3;
+    if (a.in.Cp == 8 && conv_pair(P, a.in, a.w, a.c_out, st)) return true;
     if (a.in.Cp == 8 && conv_im2col(P, a.in, a.w, a.c_out, st)) return true;
     return conv_launch(P, a.in, a.w, a.c_out, a.k * a.k, a.in.Cp, st);
 }
@@ -1961,7 +2217,7 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
 }
 
 template <int BN>
-static bool launch_wgrad_im2col(const TcWgI2c &P, const CUtensorMap &D, cudaStream_t st) {
+static bool launch_wgrad_im2col(const TcWgI2c &P, const CUtensorMap &D, const CUtensorMap &Pm, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_wgrad_im2col<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWiSmem) != cudaSuccess)
@@ -1969,7 +2225,7 @@ static bool launch_wgrad_im2col(const TcWgI2c &P, const CUtensorMap &D, cudaStre
         attr = true;
     }
     int grid = P.items < num_sms() ? P.items : num_sms();
-    k_wgrad_im2col<BN><<<grid, kI2cThreads - 4 * 32, kWiSmem, st>>>(D, P);
+    k_wgrad_im2col<BN><<<grid, kWiThreads, kWiSmem, st>>>(D, Pm, P);
     return true;
 }
 
@@ -1984,7 +2240,21 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     P.a_mul = a.s; P.c_out = a.c_out;
     for (int ky = 0; ky < a.k; ++ky)
         for (int kx = 0; kx < a.k; ++kx) { P.tap_oy[ky * a.k + kx] = ky - a.p; P.tap_ox[ky * a.k + kx] = kx - a.p; }
-    pick_tile(rows, dy.W, 1, P.TW, P.TH);
+    int oy0 = 1 << 20, oy1 = -(1 << 20), ox0 = 1 << 20, ox1 = -(1 << 20);
+    for (int t = 0; t < P.ntaps; ++t) {
+        oy0 = std::min(oy0, P.tap_oy[t]); oy1 = std::max(oy1, P.tap_oy[t]);
+        ox0 = std::min(ox0, P.tap_ox[t]); ox1 = std::max(ox1, P.tap_ox[t]);
+    }
+    long best = -1;
+    for (int tw = 128; tw >= 4; tw >>= 1) {
+        const int th = 128 / tw;
+        const int pw = (tw - 1) * a.s + ox1 - ox0 + 1, ph = (th - 1) * a.s + oy1 - oy0 + 1;
+        if (pw > 256 || ph > 256 || pw * ph * 16 > kI2cPatch) continue;
+        long cost = (long)((dy.W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+        if (best < 0 || cost < best) { best = cost; P.TW = tw; P.TH = th; P.pat_w = pw; P.pat_h = ph; }
+    }
+    if (best < 0) return false;
+    P.pat_ox = ox0; P.pat_oy = oy0; P.in_base = x.base;
     int l = 0;
     while ((1 << l) < P.TW) ++l;
     P.tw_log2 = l;
@@ -1998,9 +2268,10 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     P.splits = (P.pix_tiles + P.per_split - 1) / P.per_split;
     P.items = P.mtiles * P.splits;
     P.out_a = a.a; P.out_b = a.b; P.Wo = dy.W; P.dy_base = dy.base;
-    CUtensorMap D;
+    CUtensorMap D, Pm;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
-    return launch_wgrad_im2col<64>(P, D, st);
+    if (!encode_patch(&Pm, x, a.B, P.pat_w, P.pat_h)) return false;
+    return launch_wgrad_im2col<64>(P, D, Pm, st);
 }
 
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {

@@ -100,3 +100,25 @@ def test_tc_matches_simt():
         if b is not None:
             for key in b:
                 assert rel(a[key], b[key]) <= TOL, key
+
+
+@pytest.mark.parametrize("k,s,p,H,W", [(3, 1, 1, 37, 45), (7, 2, 3, 41, 53), (3, 2, 1, 30, 34), (5, 1, 2, 19, 70)])
+def test_image_layer_vs_oracle(k, s, p, H, W):
+    """The RGB input layer (8 padded channels -> 64): FP through the tap-pair kernel (k_conv_pair,
+    stride 1 and 2, descriptors straight into the TMA-loaded patch), wgrad through the patch-gather
+    im2col kernel; several bands, ragged rows and columns."""
+    net = {"C": 3, "H": H, "W": W, "classes": 10,
+           "ops": [WL.conv(0, 64, k, s, p), WL.conv(1, 64, 3, 1, 1)]}
+    B = 3
+    params = WL.make_params(net, seed=11, bias_scale=0.1, bf16=True)
+    x = WL.make_input(net, B, seed=6, bf16=True)
+    ts, aux = C.forward(net, params, x, store=C.bf16_store)
+    dzl = WL.make_dzl(ts[-1].shape, bf16=True)
+    g_ref, _ = C.backward(net, params, ts, aux, dzl, need_dx=False)
+    for mode, kw in (("column", {}), ("2ps", {"band_rows": 5}), ("overl", {"n_bands": 3})):
+        zl, g = run(net, B, mode, params, x, dzl, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION, **kw)
+        assert rel(zl, ts[-1]) <= TOL, (mode, "zl", rel(zl, ts[-1]))
+        for i in range(2):
+            for key in g_ref[i]:
+                e = rel(g[i][key], g_ref[i][key])
+                assert e <= TOL, (mode, kw, i, key, e)
