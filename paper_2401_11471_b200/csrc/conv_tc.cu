@@ -161,12 +161,40 @@ __device__ __forceinline__ void epi_bar_n() { asm volatile("bar.sync 1, %0;" ::"
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
+// fp32 + bf16 -> fp32 with one rounding (sm_100 mixed-precision add, no unpacking of the bf16
+// half: FHADD.BF16 reads the register half directly)
+__device__ __forceinline__ float hadd_lo(uint32_t w, float x) {
+    float r;
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(r) : "h"((unsigned short)(w & 0xffffu)), "f"(x));
+    return r;
+}
+__device__ __forceinline__ float hadd_hi(uint32_t w, float x) {
+    float r;
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(r) : "h"((unsigned short)(w >> 16)), "f"(x));
+    return r;
+}
+// two fp32 -> bf16x2 (RNE), optionally with ReLU folded into the conversion (F2FP.RELU)
+template <bool RELU>
+__device__ __forceinline__ uint32_t pack2_act(float lo, float hi) {
+    uint32_t d;
+    if (RELU) asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    else asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    return d;
+}
+// per-half mask 0xffff where the bf16 activation is > 0 (ReLU'(0) = 0), packed compare
+__device__ __forceinline__ uint32_t relu_mask2(uint32_t act) {
+    uint32_t m;
+    asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(act), "r"(0u));
+    return m;
+}
+
 // Fast path of the FP epilogue for CH channels starting at cb (all < c_real): EPI 0 none,
-// 1 bias, 2 affine; RES adds the residual; lo = 0 (ReLU) or -inf.  Parameters / residual
-// were loaded into pb/pe/pr before the accumulator wait.
-template <int CH, int EPI, bool RES>
+// 1 bias, 2 affine; RES adds the residual; RELU.  Parameters / residual were loaded into
+// pb/pe/pr before the accumulator wait.  Bias and residual are added with mixed-precision
+// FHADD.BF16, ReLU is folded into the bf16 conversion: 1.5-3 instructions per element.
+template <int CH, int EPI, bool RES, bool RELU>
 __device__ __forceinline__ void epi_fast(const uint32_t (&v)[CH], const uint4 (&pb)[CH / 8], const uint4 (&pe)[CH / 8],
-                                         const uint4 (&pr)[CH / 8], float lo, uint32_t buf, int chunk0, int m) {
+                                         const uint4 (&pr)[CH / 8], uint32_t buf, int chunk0, int m) {
 #pragma unroll
     for (int c = 0; c < CH / 8; ++c) {
         const uint32_t bw[4] = {pb[c].x, pb[c].y, pb[c].z, pb[c].w};
@@ -176,13 +204,20 @@ __device__ __forceinline__ void epi_fast(const uint32_t (&v)[CH], const uint4 (&
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             float x0 = __uint_as_float(v[c * 8 + 2 * h]), x1 = __uint_as_float(v[c * 8 + 2 * h + 1]);
-            if (EPI == 1) { x0 += bf_lo(bw[h]); x1 += bf_hi(bw[h]); }
+            if (EPI == 1) { x0 = hadd_lo(bw[h], x0); x1 = hadd_hi(bw[h], x1); }
             if (EPI == 2) { x0 = fmaf(x0, bf_lo(bw[h]), bf_lo(ew[h])); x1 = fmaf(x1, bf_hi(bw[h]), bf_hi(ew[h])); }
-            if (RES) { x0 += bf_lo(rw[h]); x1 += bf_hi(rw[h]); }
-            o[h] = pack2(fmaxf(x0, lo), fmaxf(x1, lo));
+            if (RES) { x0 = hadd_lo(rw[h], x0); x1 = hadd_hi(rw[h], x1); }
+            o[h] = pack2_act<RELU>(x0, x1);
         }
         st_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4), make_uint4(o[0], o[1], o[2], o[3]));
     }
+}
+template <int CH, int EPI, bool RES>
+__device__ __forceinline__ void epi_fast_r(bool relu, const uint32_t (&v)[CH], const uint4 (&pb)[CH / 8],
+                                           const uint4 (&pe)[CH / 8], const uint4 (&pr)[CH / 8], uint32_t buf,
+                                           int chunk0, int m) {
+    if (relu) epi_fast<CH, EPI, RES, true>(v, pb, pe, pr, buf, chunk0, m);
+    else epi_fast<CH, EPI, RES, false>(v, pb, pe, pr, buf, chunk0, m);
 }
 
 template <int BN, int NE = 4>
@@ -259,11 +294,11 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                 if (leader) bulk_wait_read1();         // the store that last used this buffer has read it
                 epi_bar_n<NE>();
             }
-            if (!ragged && P.epi == 1 && !P.has_res) epi_fast<CH, 1, false>(v, pb, pe, pr, lo, buf, chunk0, m);
-            else if (!ragged && P.epi == 2 && !P.has_res) epi_fast<CH, 2, false>(v, pb, pe, pr, lo, buf, chunk0, m);
-            else if (!ragged && P.epi == 2 && P.has_res) epi_fast<CH, 2, true>(v, pb, pe, pr, lo, buf, chunk0, m);
-            else if (!ragged && P.epi == 1 && P.has_res) epi_fast<CH, 1, true>(v, pb, pe, pr, lo, buf, chunk0, m);
-            else if (!ragged && P.epi == 0 && !P.has_res) epi_fast<CH, 0, false>(v, pb, pe, pr, lo, buf, chunk0, m);
+            if (!ragged && P.epi == 1 && !P.has_res) epi_fast_r<CH, 1, false>(P.relu, v, pb, pe, pr, buf, chunk0, m);
+            else if (!ragged && P.epi == 2 && !P.has_res) epi_fast_r<CH, 2, false>(P.relu, v, pb, pe, pr, buf, chunk0, m);
+            else if (!ragged && P.epi == 2 && P.has_res) epi_fast_r<CH, 2, true>(P.relu, v, pb, pe, pr, buf, chunk0, m);
+            else if (!ragged && P.epi == 1 && P.has_res) epi_fast_r<CH, 1, true>(P.relu, v, pb, pe, pr, buf, chunk0, m);
+            else if (!ragged && P.epi == 0 && !P.has_res) epi_fast_r<CH, 0, false>(P.relu, v, pb, pe, pr, buf, chunk0, m);
             else {
 #pragma unroll
                 for (int c = 0; c < CH / 8; ++c) {
@@ -357,13 +392,10 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
                 uint32_t o[4];
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    float x0 = __uint_as_float(v[cc * 8 + 2 * h]) + bf_lo(dw[h]);
-                    float x1 = __uint_as_float(v[cc * 8 + 2 * h + 1]) + bf_hi(dw[h]);
-                    if (P.gate) {
-                        if (!(bf_lo(gw[h]) > 0.f)) x0 = 0.f;
-                        if (!(bf_hi(gw[h]) > 0.f)) x1 = 0.f;
-                    }
-                    o[h] = pack2(x0, x1);
+                    const float x0 = hadd_lo(dw[h], __uint_as_float(v[cc * 8 + 2 * h]));
+                    const float x1 = hadd_hi(dw[h], __uint_as_float(v[cc * 8 + 2 * h + 1]));
+                    o[h] = pack2_act<false>(x0, x1);
+                    if (P.gate) o[h] &= relu_mask2(gw[h]);   // gate-on-write: delta = [act > 0] (delta + acc)
                 }
                 st_shared_v4(rowD + off, make_uint4(o[0], o[1], o[2], o[3]));
             }
