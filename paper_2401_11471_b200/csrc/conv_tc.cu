@@ -113,8 +113,11 @@ template <int BN, int KC = 64>
 struct ConvCfg {
     static constexpr int kA = 128 * KC * 2, kB = BN * KC * 2;
     static constexpr int kStageBytes = kA + kB;
-    static constexpr int kStages = kStageBudget / kStageBytes > 16 ? 16 : kStageBudget / kStageBytes;
-    static constexpr int kSmem = kStages * kStageBytes + 2 * kOutStage + 1024 + 512;
+    // BN <= 128: two (delta, activation) staging pairs (double-buffered dgrad epilogue)
+    static constexpr int kOutBufs = BN <= 128 ? 4 : 2;
+    static constexpr int kBudget = BN <= 128 ? 232448 - kOutBufs * kOutStage - 2048 : kStageBudget;
+    static constexpr int kStages = kBudget / kStageBytes > 16 ? 16 : kBudget / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + kOutBufs * kOutStage + 1024 + 512;
     static constexpr uint32_t kTmemCols = 2 * BN;
 };
 
@@ -143,6 +146,8 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_n() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -220,7 +225,7 @@ __device__ __forceinline__ void epi_fast_r(bool relu, const uint32_t (&v)[CH], c
     else epi_fast<CH, EPI, RES, false>(v, pb, pe, pr, buf, chunk0, m);
 }
 
-template <int BN, int NE = 4>
+template <int BN, int NE = 4, int NB = 2>
 __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
                                                   uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
                                                   int lane, int lead_warp = 2, const CUtensorMap *tmR = nullptr,
@@ -291,7 +296,7 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                 for (int c = 0; c < CH / 8; ++c) pr[c] = ld_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4));
                 epi_bar_n<NE>();                       // every thread has read its residual row
             } else {
-                if (leader) bulk_wait_read1();         // the store that last used this buffer has read it
+                if (leader) bulk_wait_read_n<NB - 1>();   // the store that last used this buffer has read it
                 epi_bar_n<NE>();
             }
             if (!ragged && P.epi == 1 && !P.has_res) epi_fast_r<CH, 1, false>(P.relu, v, pb, pe, pr, buf, chunk0, m);
@@ -331,7 +336,7 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                 if (grp + 1 < BN / 64 && nb + 64 < P.n_out) res_load(tile, grp + 1, sbuf ^ 1);
                 else if (tile + (int)gridDim.x < num_tiles) res_load(tile + gridDim.x, 0, sbuf ^ 1);
             }
-            sbuf ^= 1;
+            sbuf = rt ? sbuf ^ 1 : (sbuf + 1 == NB ? 0 : sbuf + 1);
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -411,6 +416,95 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
                     if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, nb + 64, xg0, yg0 - P.act.base, b);
                 }
             }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (leader) bulk_wait_all();
+}
+
+// dgrad epilogue, double-buffered: two (delta, activation) staging pairs and two mbarriers.  The
+// work items are the (tile, 64-channel group)s of this CTA in order; item k uses pair k % 2, and the
+// TMA loads of item k+1 are issued before item k's combine (once item k-1's store has read that
+// pair), so the HBM latency of the delta / activation tiles overlaps the current item instead of
+// being exposed once per tile (small-K layers: a 64-channel 3x3 dgrad tile is ~1200 MMA cycles).
+template <int BN, int NE = 4>
+__device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
+                                                      uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
+                                                      uint8_t *stage_out, uint64_t *ebar, int warp, int lane,
+                                                      int lead_warp = 2) {
+    constexpr int CH = 64 * 4 / NE;           // channels of a 64-channel group per thread
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    const int q = warp & 3, m = q * 32 + lane, hh = (warp - lead_warp) >> 2;
+    const bool leader = (warp == lead_warp && lane == 0);
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t ebytes = P.gate ? 2 * kOutStage : kOutStage;
+    // pair i: delta buffer stage_out + 2i*16K, activation buffer stage_out + (2i+1)*16K
+    auto issue = [&](int tile, int grp, int pi) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        const int nb = nt * BN + grp * 64, xg0 = tx * P.TW, yg0 = P.out_a + ty * P.TH;
+        uint8_t *bd = stage_out + (2 * pi) * kOutStage;
+        ptx::mbar_arrive_expect_tx(ebar + pi, ebytes);
+        ptx::tma_load_4d(bd, tmO, ebar + pi, nb, xg0, yg0 - P.out.base, b);
+        if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, xg0, yg0 - P.act.base, b);
+    };
+    auto ngroups = [&](int tile) { const int nt = tile % P.n_tiles; return min(BN / 64, (P.n_out - nt * BN + 63) / 64); };
+    if (leader && (int)blockIdx.x < num_tiles) issue(blockIdx.x, 0, 0);
+    int acc = 0, pi = 0;
+    uint32_t aphase = 0, ephase[2] = {0, 0};
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
+        const int ngrp = ngroups(tile);
+        ptx::mbar_wait(tfull + acc, aphase);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int grp = 0; grp < ngrp; ++grp) {
+            const int nb = n0 + grp * 64;
+            uint32_t v[CH];
+#pragma unroll
+            for (int h = 0; h < CH / 32; ++h)
+                ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+            if (leader) {   // prefetch the next item into the other pair (its last store has been read)
+                const int t2 = grp + 1 < ngrp ? tile : tile + (int)gridDim.x, g2 = grp + 1 < ngrp ? grp + 1 : 0;
+                if (t2 < num_tiles) {
+                    bulk_wait_read0();
+                    issue(t2, g2, pi ^ 1);
+                }
+            }
+            ptx::tmem_ld_wait();
+            ptx::mbar_wait(ebar + pi, ephase[pi]);
+            ephase[pi] ^= 1;
+            const uint32_t rowD = ptx::smem_u32(stage_out + (2 * pi) * kOutStage) + m * 128;
+            const uint32_t rowG = rowD + kOutStage;
+#pragma unroll
+            for (int cc = 0; cc < CH / 8; ++cc) {
+                const int c = hh * (CH / 8) + cc;
+                const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
+                const uint4 dd = ld_shared_v4(rowD + off);
+                const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
+                const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const float x0 = hadd_lo(dw[h], __uint_as_float(v[cc * 8 + 2 * h]));
+                    const float x1 = hadd_hi(dw[h], __uint_as_float(v[cc * 8 + 2 * h + 1]));
+                    o[h] = pack2_act<false>(x0, x1);
+                    if (P.gate) o[h] &= relu_mask2(gw[h]);   // gate-on-write: delta = [act > 0] (delta + acc)
+                }
+                st_shared_v4(rowD + off, make_uint4(o[0], o[1], o[2], o[3]));
+            }
+            fence_async_smem();
+            epi_bar_n<NE>();
+            if (leader) {
+                tma_store_4d(tmO, stage_out + (2 * pi) * kOutStage, nb, xg0, yg0 - P.out.base, b);
+                bulk_commit();
+            }
+            pi ^= 1;
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -523,19 +617,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
     uint8_t *sB = smem + S * ABYTES;
-    uint8_t *sO = sB + S * BBYTES;                   // 2 x 16 KB epilogue staging (1024-aligned)
-    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
+    uint8_t *sO = sB + S * BBYTES;                   // kOutBufs x 16 KB epilogue staging (1024-aligned)
+    uint64_t *full = (uint64_t *)(sO + Cfg::kOutBufs * kOutStage);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
-    uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 1);
+    uint64_t *ebar = tempty + 2;                     // 2 dgrad staging barriers
+    uint32_t *tslot = (uint32_t *)(ebar + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
         ptx::mbar_init(ebar, 1);
+        ptx::mbar_init(ebar + 1, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -567,7 +662,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
             const uint64_t dA = ptx::smem_desc(ptx::smem_u32(sA), 16, SBO, LAYOUT);
             const uint64_t dB = ptx::smem_desc(ptx::smem_u32(sB), 16, SBO, LAYOUT);
@@ -595,6 +690,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
     } else {
         if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        else if (P.tma_dg && Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
     }
@@ -730,7 +826,7 @@ __global__ void __launch_bounds__(kI2pThreads, 1)
             }
         }
     } else if (warp == kI2cMmaWarp) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
             const uint64_t dA = ptx::smem_desc(ptx::smem_u32(sA), 16, 1024, 2);
             const uint64_t dB = ptx::smem_desc(ptx::smem_u32(sB), 16, 1024, 2);
@@ -789,7 +885,8 @@ __global__ void __launch_bounds__(kI2pThreads, 1)
 static constexpr int kPrStages = 4;
 static constexpr int kPrPatch = 16 * 1024;
 static constexpr int kPrBMax = 7 * 4 * 2048;          // 7 rows x 4 pairs x 2 chunks x 1 KB
-static constexpr int kPrSmem = kPrStages * kPrPatch + kPrBMax + 2 * kOutStage + 1024 + 256;
+static constexpr int kPrOutBufs = 6;
+static constexpr int kPrSmem = kPrStages * kPrPatch + kPrBMax + kPrOutBufs * kOutStage + 1024 + 256;
 
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_pair(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
@@ -800,7 +897,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint8_t *sP = smem;
     uint8_t *sB = sP + kPrStages * kPrPatch;
     uint8_t *sO = sB + kPrBMax;
-    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
+    uint64_t *full = (uint64_t *)(sO + kPrOutBufs * kOutStage);
     uint64_t *empty = full + kPrStages;
     uint64_t *tfull = empty + kPrStages;
     uint64_t *tempty = tfull + 2;
@@ -847,7 +944,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
             const uint32_t row = (uint32_t)P.pat_w * 16;                 // bytes per patch row (one plane)
             const uint32_t lbo = s == 1 ? 16u : pstride;
@@ -881,7 +978,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
         }
     } else {
-        conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2);
+        conv_epilogue_tma<BN, 8, kPrOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -978,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
             const uint64_t dA = ptx::smem_desc_sw128_bo(ptx::smem_u32(sA), 16, HP * 128, 0);
             const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(sB), 16, 1024);
@@ -1109,7 +1206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
             const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), kABytes, 1024);
             const uint64_t dB = Cfg::KB == 64 ? ptx::smem_desc_sw128(ptx::smem_u32(smem + kWgA), kABytes, 1024)
@@ -1314,7 +1411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
             const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), kABytes, 1024);
             const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(smem + kWgA), Cfg::kXBox, 1024);
@@ -1563,7 +1660,7 @@ __global__ void __launch_bounds__(kWiThreads, 1)
             }
         }
     } else if (warp == kMma) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
             const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), 16384, 1024);
             const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(smem + 2 * 16384), 16384, 1024);
@@ -1636,7 +1733,7 @@ __global__ void __launch_bounds__(kWiThreads, 1)
 // 23 KB of loads for 36 MMAs.  Epilogue: TMA store (FP) or TMA load/combine/store (dgrad).
 static constexpr int kRbSA = 3;
 static constexpr int kRbB = 9 * 64 * 128;                                    // 72 KB
-static constexpr int kRbSmem = kRbSA * HaloGeom<3>::kABytes + kRbB + 2 * kOutStage + 1024 + 512;
+static constexpr int kRbSmem = kRbSA * HaloGeom<3>::kABytes + kRbB + 4 * kOutStage + 1024 + 512;
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_halo_rb(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1647,20 +1744,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
     uint8_t *sB = smem + SA * AB;
-    uint8_t *sO = sB + kRbB;
-    uint64_t *fullA = (uint64_t *)(sO + 2 * kOutStage);
+    uint8_t *sO = sB + kRbB;                         // 4 x 16 KB staging: two dgrad (delta, act) pairs
+    uint64_t *fullA = (uint64_t *)(sO + 4 * kOutStage);
     uint64_t *emptyA = fullA + SA;
     uint64_t *bfull = emptyA + SA;
     uint64_t *tfull = bfull + 1;
     uint64_t *tempty = tfull + 2;
     uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 1);
+    uint32_t *tslot = (uint32_t *)(ebar + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
         ptx::mbar_init(bfull, 1);
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
         ptx::mbar_init(ebar, 1);
+        ptx::mbar_init(ebar + 1, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -1689,7 +1787,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
             const uint64_t dA = ptx::smem_desc_sw128_bo(ptx::smem_u32(sA), 16, HP * 128, 0);
             const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(sB), 16, 1024);
@@ -1722,7 +1820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (P.mode == 0) {
         conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
     } else {
-        conv_epilogue_tma_dg<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        conv_epilogue_tma_dg2<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -1904,7 +2002,8 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     P.n_tiles = (P.n_out + BN - 1) / BN;
     CUtensorMap A, Bm;
     if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN, KC)) return false;
-    if (halo_on && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1) {
+    static const int halo_fp128 = env_int("LRCNN_HALO_FP128", 1);   // FP of 128-wide outputs: A traffic / 6
+    if ((halo_on || (halo_fp128 && P.mode == 0 && BN == 128)) && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1) {
         P.TW = 8; P.TH = 16;
         P.tiles_x = (P.Wo + 7) / 8;
         P.tiles_y = (rows + 15) / 16;

@@ -1,0 +1,7 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+B=32 timeout 300 python scripts/microbench_layer.py 3,64,224,224,3 64,64,224,224,3 256,256,56,56,3 512,512,28,28,3 2>&1 | tail -4
+B=8 timeout 300 python scripts/microbench_layer.py 3,64,900,2400,7,2 64,256,225,600,1 2>&1 | tail -2
+for cfg in "$@"; do
+  timeout 600 python bench.py --config $cfg --no-baselines > gpurun_out/q_$cfg.log 2>&1
+  tail -1 gpurun_out/q_$cfg.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$cfg', round(d['value'],2), 'img/s ms', round(d['ms_per_step'],3), 'frac', round(r['frac'],3), 'conv ms', round(r['ms_per_step'],3), 'wgrad', round(r['wgrad']['ms_per_step'],3), round(r['wgrad']['achieved'],1), 'other', round(r['other_ms_per_step'],3), d['clocks'])" || tail -5 gpurun_out/q_$cfg.log
+done
