@@ -1527,6 +1527,191 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ wgrad, 64 output channels: tap pairs on M
+// For c_out <= 64 (VGG conv1_2, the ResNet stage-1 3x3) the M = 128 output-channel tile of
+// k_wgrad_halo is half empty.  Here the roles are swapped: M = 128 = two filter taps x 64 input
+// channels, N = the 64 output channels, K = pixels.  A is the input halo box itself (MN-major,
+// SWIZZLE_128B, one 128-byte row per pixel): the first 64-element M chunk starts at the box row of
+// tap tA, the second at tap tB, and the descriptor's LBO is the row distance between the two taps,
+// so one (TW+2) x (TH+2) box per 64-channel chunk serves all 9 taps of the 3x3 filter as 5 MMAs per
+// 16-pixel K-step: (0,1) (2,3) (4,5) (6,7) (7,8) -- of the last pair only rows 64..127 (tap 8) are
+// kept.  B is the band delta (one 64-channel MN-major box).  9 taps cost 5 MMAs instead of the 9
+// half-empty ones of the (co, ky) x kx kernel.  Bias gradient fused as in k_wgrad_halo.
+template <int KW>
+struct WgPCfg {
+    static constexpr int kXBoxMax = ((272 * 128 + 1023) / 1024) * 1024;   // (TW+2)*(TH+2) <= 272 rows
+    static constexpr int kStageBytes = kABytes + kXBoxMax;
+    static constexpr int kStages = (220 * 1024) / kStageBytes > 6 ? 6 : (220 * 1024) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kPairs = (KW * KW + 1) / 2;
+};
+
+template <int KW>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad_pair(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
+    using Cfg = WgPCfg<KW>;
+    constexpr int S = Cfg::kStages, SB = Cfg::kStageBytes, NP = Cfg::kPairs, TAPS = KW * KW;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + S * SB);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = (uint32_t *)(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, P.db ? 5 : 1); }
+        ptx::mbar_init(tfull, 1);
+        ptx::mbar_init(tempty, 4);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmD);
+        ptx::prefetch_tmap(&tmX);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int XP = P.TW + KW - 1, XR = P.TH + KW - 1;   // halo box pitch / rows (pixels)
+    const uint32_t xbytes = (uint32_t)XP * XR * 128;
+    // pair p = taps (tA, tB): tA = 2p (last pair: TAPS-2), tB = tA + 1; box row offset of tap t
+    auto tap_off = [&](int t) { return (t / KW) * XP + t % KW; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                const int split = item % P.splits, cit = item / P.splits;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                for (int pt = p0; pt < p1; ++pt) {
+                    const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                    const int y0 = P.out_a + ty * P.TH, x0 = tx * P.TW;
+                    ptx::mbar_wait(empty + stage, phase ^ 1);
+                    uint8_t *st = smem + stage * SB;
+                    ptx::mbar_arrive_expect_tx(full + stage, kABytes + xbytes);
+                    ptx::tma_load_4d(st, &tmD, full + stage, 0, x0, y0 - P.dy_base, b);
+                    ptx::tma_load_4d(st + kABytes, &tmX, full + stage, cit * 64, x0 - P.pad, y0 - P.pad - P.x_base, b);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
+            constexpr uint32_t idesc = ptx::idesc_bf16(128, 64, 1, 1);
+            // descriptor words: low = start >> 4 | LBO >> 4 << 16, high = SBO | version | layout
+            const uint32_t hi = (uint32_t)(ptx::smem_desc_sw128(0, kABytes, 1024) >> 32);
+            uint32_t loA[NP];   // A (input box) of pair p at stage 0, K-step 0: start at tap tA, LBO = tB - tA rows
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const int tA = p == NP - 1 && TAPS % 2 ? TAPS - 2 : 2 * p;
+                const int lbo = (tap_off(tA + 1) - tap_off(tA)) * 128;
+                loA[p] = (uint32_t)ptx::smem_desc_sw128(ptx::smem_u32(smem + kABytes) + tap_off(tA) * 128, lbo, 1024);
+            }
+            uint32_t joff[8];   // K-step j (16 pixels): box row r*XP + c of its first pixel
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int px = 16 * j, r = px / P.TW, c = px - r * P.TW;
+                joff[j] = (uint32_t)(r * XP + c) * 8;
+            }
+            const uint32_t lo0 = (uint32_t)ptx::smem_desc_sw128(ptx::smem_u32(smem), kABytes, 1024);
+            int stage = 0;
+            uint32_t phase = 0, tphase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                const int split = item % P.splits;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                ptx::mbar_wait(tempty, tphase ^ 1);
+                ptx::tc_fence_after();
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t so = stage * (SB >> 4);
+                    const uint32_t b0 = lo0 + so;                      // delta box (B)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+#pragma unroll
+                        for (int p = 0; p < NP; ++p)
+                            ptx::umma_bf16_lh(tmem + p * 64, loA[p] + so + joff[j], hi, b0 + j * 128, hi, idesc,
+                                              (pt != p0 || j != 0) ? 1u : 0u);
+                    ptx::umma_commit(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(tfull);
+                tphase ^= 1;
+            }
+        }
+    } else {
+        const int ew = warp & 3;
+        const int m = ew * 32 + lane;             // accumulator row: (tap tA or tB, input channel m & 63)
+        uint32_t tphase = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t col = (uint32_t)(((m & 63) >> 3) * 16 + (m & 7) * 2);   // delta column m (m < 64)
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            const int split = item % P.splits, cit = item / P.splits;
+            if (P.db) {
+                const bool want = cit == 0 && m < 64;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float sum = 0.f;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    if (want) {
+                        const uint32_t base = ptx::smem_u32(smem + stage * SB);
+#pragma unroll 8
+                        for (int r = 0; r < 128; ++r) {
+                            const uint32_t a = base + r * 128 + (col ^ ((r & 7) << 4));
+                            unsigned short h;
+                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+                            sum += __uint_as_float((uint32_t)h << 16);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                if (want && m < P.c_out) atomicAdd(P.db + m, sum);
+            }
+            ptx::mbar_wait(tfull, tphase);
+            ptx::tc_fence_after();
+            const int ci = cit * 64 + (m & 63);
+#pragma unroll 1
+            for (int p = 0; p < NP; ++p) {
+                const int tA = p == NP - 1 && TAPS % 2 ? TAPS - 2 : 2 * p;
+                const int t = m < 64 ? tA : tA + 1;
+                const bool keep = !(p == NP - 1 && TAPS % 2 && m < 64) && ci < P.cin_p;
+                float *dst = P.dw + (long long)t * P.cin_p + ci;
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + p * 64 + c * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (!keep) continue;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int co = c * 32 + j;
+                        if (co < P.c_out) {
+                            const float g = P.gamma ? __bfloat162float(P.gamma[co]) : 1.f;
+                            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + (long long)co * TAPS * P.cin_p),
+                                         "f"(__uint_as_float(v[j]) * g)
+                                         : "memory");
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty);
+            tphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
 // ------------------------------------------------------------------ wgrad of 8-channel-input convs (im2col)
 // dW[co][tap][ci] = sum_pixels dY[p][co] X[p + off(tap)][ci] for the padded RGB layer:
 // D[m = (tap - 16*mt)*8 + ci][co] (M = 128 = 16 taps x 8 channels, N = c_out) accumulates over
@@ -2302,6 +2487,56 @@ static bool launch_wgrad_halo(const TcWgrad &P, const CUtensorMap &D, const CUte
     return true;
 }
 
+// stride-1 k x k wgrad with c_out <= 64 (one 64-channel delta box) and 64-multiple input channels
+// through the tap-pair kernel (M = two taps x 64 input channels)
+static bool wgrad_pair(const WgradArgs &a, cudaStream_t st) {
+    static const int on = env_int("LRCNN_WG_PAIR", 1);
+    const View &dy = a.dy, &x = a.x;
+    if (!on || a.s != 1 || a.k != 3 || x.Cp % 64 || dy.Cp != 64 || a.c_out > 64) return false;
+    const int rows = a.b - a.a;
+    TcWgrad P{};
+    P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
+    P.s = 1;
+    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
+    P.db = fuse_db && !a.dg ? a.db : nullptr;   // (dgamma is not fused here: param-grad kernel)
+    P.dg = nullptr;
+    P.w = (const bf16 *)a.w;
+    long best = -1;
+    for (int tw = 128; tw >= 16; tw >>= 1) {
+        const int th = 128 / tw;
+        if ((tw + a.k - 1) * (th + a.k - 1) > 272) continue;
+        long cost = (long)((dy.W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+        if (best < 0 || cost < best) { best = cost; P.TW = tw; P.TH = th; }
+    }
+    if (best < 0) return false;
+    P.tiles_x = (dy.W + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
+    P.co_tiles = 1;
+    P.ci_tiles = x.Cp / 64;
+    int splits = num_sms() / P.ci_tiles;
+    if (splits > P.pix_tiles) splits = P.pix_tiles;
+    if (splits < 1) splits = 1;
+    P.per_split = (P.pix_tiles + splits - 1) / splits;
+    P.splits = (P.pix_tiles + P.per_split - 1) / P.per_split;
+    P.items = P.ci_tiles * P.splits;
+    P.out_a = a.a; P.dy_base = dy.base; P.x_base = x.base;
+    CUtensorMap D, X;
+    if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
+    if (!encode_view(&X, x, a.B, P.TW + a.k - 1, P.TH + a.k - 1)) return false;
+    using Cfg = WgPCfg<3>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_wgrad_pair<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    const int grid = P.items < num_sms() ? P.items : num_sms();
+    k_wgrad_pair<3><<<grid, kThreads, Cfg::kSmem, st>>>(D, X, P);
+    if (P.db) a.db_done = true;
+    return true;
+}
+
 // stride-1 3x3 wgrad with input channels in 64-multiples through the row-halo kernel
 static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     static const int on = env_int("LRCNN_WG_HALO", 1);
@@ -2411,6 +2646,7 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     if (dy.Cp % 8 || x.Cp % 8 || !aligned16(dy.p) || !aligned16(x.p)) return false;
     const int rows = a.b - a.a;
     if (rows <= 0) return true;
+    if (wgrad_pair(a, st)) return true;
     if (wgrad_halo(a, st)) return true;
     if (wgrad_im2col(a, st)) return true;
     TcWgrad P{};
