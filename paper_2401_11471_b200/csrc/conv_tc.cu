@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <utility>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -640,6 +641,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int num_tiles = P.m_tiles * P.n_tiles;
 
     if (warp == 0) {
@@ -763,6 +766,8 @@ __global__ void __launch_bounds__(kI2pThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int num_tiles = P.m_tiles * P.n_tiles;
 
     if (warp < kI2cGather) {
@@ -918,6 +923,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int num_tiles = P.m_tiles;
     const uint32_t plane = (uint32_t)P.pat_w * P.pat_h * 16;   // bytes of one plane
     const uint32_t pstride = (plane + 127) & ~127u;             // plane B offset (TMA: 128 B aligned)
@@ -1048,6 +1055,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int num_tiles = P.m_tiles * P.n_tiles;
     constexpr int taps = KH * KH;
 
@@ -1170,6 +1179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int taps = P.k * P.k;
 
     auto decode = [&](int item, int &cot, int &tap, int &cit, int &split) {
@@ -1375,6 +1386,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int XP = P.TW + KW - 1;                  // halo box row pitch (pixels)
     const uint32_t xbytes = (uint32_t)XP * P.TH * 128;
 
@@ -1572,6 +1585,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int XP = P.TW + KW - 1, XR = P.TH + KW - 1;   // halo box pitch / rows (pixels)
     const uint32_t xbytes = (uint32_t)XP * XR * 128;
     // pair p = taps (tA, tB): tA = 2p (last pair: TAPS-2), tB = tA + 1; box row offset of tap t
@@ -1765,6 +1780,8 @@ __global__ void __launch_bounds__(kWiThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int twm = (1 << P.tw_log2) - 1;
 
     if (warp < kI2cGather) {
@@ -1953,6 +1970,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail; its results are visible now
+    ptx::griddep_launch();   // let the next kernel's CTAs start their own setup as SMs free up
     const int num_tiles = P.m_tiles;
 
     if (warp == 0) {
@@ -2016,6 +2035,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ host side
+// Launch with programmatic dependent launch (PDL): the kernel may start while the previous kernel
+// in the stream is still finishing; every tcgen05 kernel runs its barrier / TMEM / tensor-map setup
+// first and then waits (griddepcontrol.wait) before touching global memory.  Captured into the
+// step's CUDA graph as programmatic edges.  LRCNN_PDL=0 disables it.
+static int env_int(const char *name, int dflt);
+template <typename... KArgs, typename... Args>
+static bool launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args &&...args) {
+    static const int pdl = env_int("LRCNN_PDL", 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess;
+}
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -2100,8 +2139,7 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_tc<BN, KC><<<grid, kConvThreads, Cfg::kSmem, st>>>(A, Bm, O, G, P);
-    return true;
+    return launch_pdl(k_conv_tc<BN, KC>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P);
 }
 
 template <int BN>
@@ -2116,8 +2154,7 @@ static bool launch_conv_halo(const TcConv &P, const CUtensorMap &A, const CUtens
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_tc_halo<BN, 3><<<grid, kThreads, Cfg::kSmem, st>>>(A, Bm, O, P);
-    return true;
+    return launch_pdl(k_conv_tc_halo<BN, 3>, grid, kThreads, Cfg::kSmem, st, A, Bm, O, P);
 }
 
 static int env_int(const char *name, int dflt) {
@@ -2156,8 +2193,7 @@ static bool conv_halo_rb(TcConv &P, const View &in, const void *w, int w_rows, i
         attr = true;
     }
     const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
-    k_conv_halo_rb<<<grid, kThreads, kRbSmem, st>>>(A, Bm, O, G, P);
-    return true;
+    return launch_pdl(k_conv_halo_rb, grid, kThreads, kRbSmem, st, A, Bm, O, G, P);
 }
 
 // Launch one implicit-GEMM conv over the output grid rows [P.out_a, P.out_b) x cols [0, P.Wo).
@@ -2274,8 +2310,7 @@ static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensor
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_conv_im2col<BN><<<grid, kI2pThreads, kI2cSmem, st>>>(Bm, O, Pm, P);
-    return true;
+    return launch_pdl(k_conv_im2col<BN>, grid, kI2pThreads, kI2cSmem, st, Bm, O, Pm, P);
 }
 
 // 4D map over an 8-channel band View with a (8, pw, ph, 1) box, no swizzle (16-byte pixels packed
@@ -2342,8 +2377,7 @@ static bool conv_pair(TcConv &P, const View &in, const void *w, int w_rows, cuda
         attr = true;
     }
     const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
-    k_conv_pair<<<grid, kConvThreads, kPrSmem, st>>>(Pm, Wm, O, P);
-    return true;
+    return launch_pdl(k_conv_pair, grid, kConvThreads, kPrSmem, st, Pm, Wm, O, P);
 }
 
 // FP of an 8-channel-input conv through the im2col kernel; false = shape not taken.
@@ -2468,8 +2502,7 @@ static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorM
         attr = true;
     }
     int grid = P.items < num_sms() ? P.items : num_sms();
-    k_wgrad_tc<BN><<<grid, kThreads, Cfg::kSmem, st>>>(D, X, P);
-    return true;
+    return launch_pdl(k_wgrad_tc<BN>, grid, kThreads, Cfg::kSmem, st, D, X, P);
 }
 
 template <int BN, int KW>
@@ -2483,8 +2516,7 @@ static bool launch_wgrad_halo(const TcWgrad &P, const CUtensorMap &D, const CUte
         attr = true;
     }
     int grid = P.items < num_sms() ? P.items : num_sms();
-    k_wgrad_halo<BN, KW><<<grid, kThreads, Cfg::kSmem, st>>>(D, X, P);
-    return true;
+    return launch_pdl(k_wgrad_halo<BN, KW>, grid, kThreads, Cfg::kSmem, st, D, X, P);
 }
 
 // stride-1 k x k wgrad with c_out <= 64 (one 64-channel delta box) and 64-multiple input channels
@@ -2532,7 +2564,7 @@ static bool wgrad_pair(const WgradArgs &a, cudaStream_t st) {
         attr = true;
     }
     const int grid = P.items < num_sms() ? P.items : num_sms();
-    k_wgrad_pair<3><<<grid, kThreads, Cfg::kSmem, st>>>(D, X, P);
+    if (!launch_pdl(k_wgrad_pair<3>, grid, kThreads, Cfg::kSmem, st, D, X, P)) return false;
     if (P.db) a.db_done = true;
     return true;
 }
@@ -2591,8 +2623,7 @@ static bool launch_wgrad_im2col(const TcWgI2c &P, const CUtensorMap &D, const CU
         attr = true;
     }
     int grid = P.items < num_sms() ? P.items : num_sms();
-    k_wgrad_im2col<BN><<<grid, kWiThreads, kWiSmem, st>>>(D, Pm, P);
-    return true;
+    return launch_pdl(k_wgrad_im2col<BN>, grid, kWiThreads, kWiSmem, st, D, Pm, P);
 }
 
 // wgrad of a conv whose input has 8 (padded) channels; N = c_out padded to 64 / 128 / 256
