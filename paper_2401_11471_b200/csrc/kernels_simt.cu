@@ -9,9 +9,37 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "kernels.hpp"
 
 namespace lrcnn {
+
+// programmatic dependent launch (see conv_tc.cu launch_pdl): every kernel of this file waits for
+// the preceding grid at its first statement, so it may be launched while that grid drains.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+static int simt_pdl() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("LRCNN_PDL"); v = e && *e ? atoi(e) : 1; }
+    return v;
+}
+template <typename... KArgs, typename... Args>
+static void launch_simt(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = simt_pdl() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 
 typedef __nv_bfloat16 bf16;
 
@@ -30,6 +58,8 @@ __device__ __forceinline__ long long voff(const View &v, int b, int g, int x) {
 // ------------------------------------------------------------------ conv forward
 template <typename T>
 __global__ void k_conv_fwd(ConvFwdArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cpo = A.out.Cp, Wo = A.out.W, rows = A.b_ - A.a, Cin = A.in.Cp;
     long long n = (long long)A.B * rows * Wo * Cpo;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -69,6 +99,8 @@ __global__ void k_conv_fwd(ConvFwdArgs A) {
 // (2PS carry rows, several consumers) may be gated more than once.
 template <typename T>
 __global__ void k_conv_dgrad(DgradArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cin = A.dx.Cp, Wi = A.dx.W, rows = A.rb - A.ra, Wo = A.dy.W, Cpo = A.dy.Cp;
     long long n = (long long)A.B * rows * Wi * Cin;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -114,6 +146,8 @@ __global__ void k_conv_dgrad(DgradArgs A) {
 // one block per (co, ky, kx), threads over ci x pixel slices, block reduction.
 template <typename T>
 __global__ void k_conv_wgrad(WgradArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cin = A.x.Cp, Wo = A.dy.W, rows = A.b - A.a;
     const int co = blockIdx.x / (A.k * A.k), kk = blockIdx.x % (A.k * A.k);
     const int ky = kk / A.k, kx = kk % A.k;
@@ -194,6 +228,8 @@ __device__ __forceinline__ void accdot8(const uint4 &d, const uint4 &t, const ui
 
 template <typename T>
 __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     // blockDim.x channel vectors (8 channels each) of group blockIdx.y; blockDim.y pixel lanes
     const int CV = blockDim.x, cv = threadIdx.x, py = threadIdx.y, PY = blockDim.y;
     const int rows = A.b - A.a, W = A.dy.W, c0 = (blockIdx.y * CV + cv) * 8;
@@ -280,6 +316,8 @@ __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
 // grid: x = (output column, channel vector) chunks of one output row, y = (image, row) of the band
 template <typename T>
 __global__ void k_pool2_fwd(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.out.Cp / 8, Wo = A.out.W, rows = A.b - A.a;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= Wo * CV) return;
@@ -301,6 +339,8 @@ __global__ void k_pool2_fwd(PoolArgs A) {
 
 template <typename T>
 __global__ void k_pool2_bwd(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.dy.Cp / 8, Wo = A.dy.W, rows = A.b - A.a;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= Wo * CV) return;
@@ -354,6 +394,8 @@ __device__ __forceinline__ void pool_window(const View &in, int b, int y, int x,
 
 template <typename T>
 __global__ void k_pool_fwd(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cp = A.out.Cp, Wo = A.out.W, rows = A.b - A.a;
     long long n = (long long)A.B * rows * Wo * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -371,6 +413,8 @@ __global__ void k_pool_fwd(PoolArgs A) {
 
 template <typename T>
 __global__ void k_pool_bwd(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cp = A.dx.Cp, Wi = A.dx.W, rows = A.rb - A.ra, Wo = A.dy.W;
     long long n = (long long)A.B * rows * Wi * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -406,6 +450,8 @@ __global__ void k_pool_bwd(PoolArgs A) {
 // ------------------------------------------------------------------ residual add, gated accumulate
 template <typename T>
 __global__ void k_add_fwd(EltArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cp = A.out.Cp, W = A.out.W, rows = A.b - A.a;
     long long n = (long long)A.B * rows * W * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -423,6 +469,8 @@ __global__ void k_add_fwd(EltArgs A) {
 
 template <typename T>
 __global__ void k_acc_gate(EltArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int Cp = A.dx.Cp, W = A.dx.W, rows = A.b - A.a;
     long long n = (long long)A.B * rows * W * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -442,6 +490,8 @@ __global__ void k_acc_gate(EltArgs A) {
 // ------------------------------------------------------------------ head
 template <typename T>
 __global__ void k_gap(const T *zl, int HW, int Cp, float *gap, float hw_div) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     int b = blockIdx.x, c = blockIdx.y * blockDim.x + threadIdx.x;
     if (c >= Cp) return;
     const T *z = zl + (long long)b * HW * Cp + c;
@@ -453,6 +503,8 @@ __global__ void k_gap(const T *zl, int HW, int Cp, float *gap, float hw_div) {
 template <typename T>
 __global__ void k_fc_ce(const float *gap, int B, int Cp, int C, int classes, const T *fw, const T *fb,
                         const int32_t *labels, float *dlog, float *loss, float *gw, float *gb) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     extern __shared__ float sh[];   // logits [B*classes]
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int i = threadIdx.x >> 5; i < B * classes; i += nw) {   // one warp per (image, class)
@@ -495,6 +547,8 @@ __global__ void k_fc_ce(const float *gap, int B, int Cp, int C, int classes, con
 template <typename T>
 __global__ void k_dzl(const T *zl, const float *dlog, const T *fw, int B, int HW, int Cp, int C, int classes,
                       T *dzl, int gate, float hw_div) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     long long n = (long long)B * HW * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -512,6 +566,8 @@ __global__ void k_dzl(const T *zl, const float *dlog, const T *fw, int B, int HW
 
 template <typename T>
 __global__ void k_gate_copy(const T *src, const T *act, T *dst, long long n, int gate) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         float v = ldf(src + i);
         if (gate && ldf(act + i) <= 0.f) v = 0.f;
@@ -521,6 +577,8 @@ __global__ void k_gate_copy(const T *src, const T *act, T *dst, long long n, int
 
 template <typename T>
 __global__ void k_sgd(float *master, T *params, float *grads, long long n, float lr) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         float m = master[i] - lr * grads[i];
         master[i] = m;
@@ -533,6 +591,8 @@ template <typename T>
 // wt[ci][k-1-ky][k-1-kx][co] = gamma[co] * w[co][ky][kx][ci] (0 for co >= cout): per tap a 32 x 32
 // tile transpose through shared memory, coalesced along ci on the read and co on the write.
 __global__ void k_transpose_w(const T *w, const T *gamma, T *wt, int cout, int coutp, int k, int cinp) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     __shared__ float tile[32][33];
     const int taps = k * k, tap = blockIdx.z;
     const int ci0 = blockIdx.x * 32, co0 = blockIdx.y * 32;
@@ -583,6 +643,8 @@ __device__ __forceinline__ void pool_window8(const View &in, int b, int y, int x
 
 template <typename T>
 __global__ void k_pool_fwd8(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.out.Cp / 8, Wo = A.out.W, rows = A.b - A.a;
     long long n = (long long)A.B * rows * Wo * CV;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -602,6 +664,8 @@ __global__ void k_pool_fwd8(PoolArgs A) {
 // gather: every input pixel checks the (at most ceil(k/s)^2) windows that contain it
 template <typename T>
 __global__ void k_pool_bwd8(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.dx.Cp / 8, Wi = A.dx.W, rows = A.rb - A.ra, Wo = A.dy.W;
     long long n = (long long)A.B * rows * Wi * CV;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -652,6 +716,8 @@ __global__ void k_pool_bwd8(PoolArgs A) {
 // distinct argmax position (the gather form re-reads every window once per input pixel in it).
 template <typename T>
 __global__ void k_pool_bwd_scatter8(PoolArgs A, int py, int px) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.dy.Cp / 8, Wo = A.dy.W, rows = A.b - A.a;
     const int wx = (Wo - px + 1) / 2;                      // output columns of this parity
     const int y0 = A.a + ((py - A.a) % 2 + 2) % 2;         // first band row of this parity
@@ -697,6 +763,8 @@ __global__ void k_pool_bwd_scatter8(PoolArgs A, int py, int px) {
 
 template <typename T>
 __global__ void k_acc_gate8(EltArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.dx.Cp / 8, W = A.dx.W, rows = A.b - A.a;
     long long n = (long long)A.B * rows * W * CV;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -724,6 +792,8 @@ __global__ void k_acc_gate8(EltArgs A) {
 // one image is contiguous in all three views (W * Cp elements)
 template <typename T>
 __global__ void k_acc_gate_rows(EltArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int rows = A.b - A.a, nv = A.dx.W * A.dx.Cp / 8;
     const int b = blockIdx.y / rows, y = A.a + (int)(blockIdx.y - b * rows);
     T *dx = (T *)A.dx.p + voff(A.dx, b, y, 0);
@@ -745,6 +815,8 @@ __global__ void k_acc_gate_rows(EltArgs A) {
 
 template <typename T>
 __global__ void k_add_fwd8(EltArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int CV = A.out.Cp / 8, W = A.out.W, rows = A.b - A.a;
     long long n = (long long)A.B * rows * W * CV;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -771,27 +843,23 @@ static unsigned grid_for(long long n) {
     return (unsigned)(g < 1 ? 1 : g);
 }
 
-#define DISPATCH(prec, KER, ...)                                        \
-    do {                                                                \
-        if (prec) KER<bf16><<<__VA_ARGS__>>>; else KER<float><<<__VA_ARGS__>>>; \
-    } while (0)
 
 cudaError_t simt_conv_fwd(int prec, const ConvFwdArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b_ - a.a) * a.out.W * a.out.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_conv_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_conv_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+    if (prec) launch_simt(k_conv_fwd<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_conv_fwd<float>, grid_for(n), kT, 0, st, a);
     return cudaGetLastError();
 }
 cudaError_t simt_conv_dgrad(int prec, const DgradArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_conv_dgrad<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_conv_dgrad<float><<<grid_for(n), kT, 0, st>>>(a);
+    if (prec) launch_simt(k_conv_dgrad<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_conv_dgrad<float>, grid_for(n), kT, 0, st, a);
     return cudaGetLastError();
 }
 cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st) {
     if (a.b <= a.a) return cudaSuccess;
     dim3 g(a.c_out * a.k * a.k, (a.x.Cp + 31) / 32);
-    if (prec) k_conv_wgrad<bf16><<<g, 256, 0, st>>>(a); else k_conv_wgrad<float><<<g, 256, 0, st>>>(a);
+    if (prec) launch_simt(k_conv_wgrad<bf16>, g, 256, 0, st, a); else launch_simt(k_conv_wgrad<float>, g, 256, 0, st, a);
     return cudaGetLastError();
 }
 cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
@@ -807,7 +875,7 @@ cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     if (g < 1) g = 1;
     dim3 grid((unsigned)g, groups);
     size_t shm = 2 * sizeof(float) * blk.y * CV * 8;
-    if (prec) k_param_grad<bf16><<<grid, blk, shm, st>>>(a); else k_param_grad<float><<<grid, blk, shm, st>>>(a);
+    if (prec) launch_simt(k_param_grad<bf16>, grid, blk, shm, st, a); else launch_simt(k_param_grad<float>, grid, blk, shm, st, a);
     return cudaGetLastError();
 }
 static bool pool2(const PoolArgs &a, const View &v) {
@@ -819,12 +887,12 @@ cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     if (pool2(a, a.out)) {
         const int rowv = a.out.W * (a.out.Cp / 8);
         dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
-        if (prec) k_pool2_fwd<bf16><<<g, kT, 0, st>>>(a); else k_pool2_fwd<float><<<g, kT, 0, st>>>(a);
+        if (prec) launch_simt(k_pool2_fwd<bf16>, g, kT, 0, st, a); else launch_simt(k_pool2_fwd<float>, g, kT, 0, st, a);
     } else if (a.out.Cp % 8 == 0) {
         n /= 8;
-        if (prec) k_pool_fwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd8<float><<<grid_for(n), kT, 0, st>>>(a);
+        if (prec) launch_simt(k_pool_fwd8<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_fwd8<float>, grid_for(n), kT, 0, st, a);
     } else {
-        if (prec) k_pool_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+        if (prec) launch_simt(k_pool_fwd<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_fwd<float>, grid_for(n), kT, 0, st, a);
     }
     return cudaGetLastError();
 }
@@ -840,18 +908,18 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
         if (a.b <= a.a) return cudaSuccess;
         const int rowv = a.dy.W * (a.dy.Cp / 8);
         dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
-        if (prec) k_pool2_bwd<bf16><<<g, kT, 0, st>>>(a); else k_pool2_bwd<float><<<g, kT, 0, st>>>(a);
+        if (prec) launch_simt(k_pool2_bwd<bf16>, g, kT, 0, st, a); else launch_simt(k_pool2_bwd<float>, g, kT, 0, st, a);
     } else if (a.dx.Cp % 8 == 0 && a.k > a.s && a.k <= 2 * a.s) {
         const long long m = (long long)a.B * (a.b - a.a) * a.dy.W * (a.dy.Cp / 8) / 4 + 1;
         for (int ph = 0; ph < 4; ++ph) {
-            if (prec) k_pool_bwd_scatter8<bf16><<<grid_for(m), kT, 0, st>>>(a, ph >> 1, ph & 1);
-            else k_pool_bwd_scatter8<float><<<grid_for(m), kT, 0, st>>>(a, ph >> 1, ph & 1);
+            if (prec) launch_simt(k_pool_bwd_scatter8<bf16>, grid_for(m), kT, 0, st, a, ph >> 1, ph & 1);
+            else launch_simt(k_pool_bwd_scatter8<float>, grid_for(m), kT, 0, st, a, ph >> 1, ph & 1);
         }
     } else if (a.dx.Cp % 8 == 0) {
         n /= 8;
-        if (prec) k_pool_bwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd8<float><<<grid_for(n), kT, 0, st>>>(a);
+        if (prec) launch_simt(k_pool_bwd8<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_bwd8<float>, grid_for(n), kT, 0, st, a);
     } else {
-        if (prec) k_pool_bwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_pool_bwd<float><<<grid_for(n), kT, 0, st>>>(a);
+        if (prec) launch_simt(k_pool_bwd<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_bwd<float>, grid_for(n), kT, 0, st, a);
     }
     return cudaGetLastError();
 }
@@ -860,8 +928,8 @@ cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     if (a.out.Cp % 8 == 0) {
         n /= 8;
-        if (prec) k_add_fwd8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_add_fwd8<float><<<grid_for(n), kT, 0, st>>>(a);
-    } else if (prec) k_add_fwd<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_add_fwd<float><<<grid_for(n), kT, 0, st>>>(a);
+        if (prec) launch_simt(k_add_fwd8<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_add_fwd8<float>, grid_for(n), kT, 0, st, a);
+    } else if (prec) launch_simt(k_add_fwd<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_add_fwd<float>, grid_for(n), kT, 0, st, a);
     return cudaGetLastError();
 }
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
@@ -871,19 +939,19 @@ cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
     if (a.dx.Cp % 8 == 0 && a.dx.Cp == a.dy.Cp && (!a.gate || a.act.Cp == a.dx.Cp) && gy <= 65535) {
         const int nv = a.dx.W * a.dx.Cp / 8;
         dim3 g((nv + kT - 1) / kT, (unsigned)gy);
-        if (prec) k_acc_gate_rows<bf16><<<g, kT, 0, st>>>(a); else k_acc_gate_rows<float><<<g, kT, 0, st>>>(a);
+        if (prec) launch_simt(k_acc_gate_rows<bf16>, g, kT, 0, st, a); else launch_simt(k_acc_gate_rows<float>, g, kT, 0, st, a);
     } else if (a.dx.Cp % 8 == 0) {
         n /= 8;
-        if (prec) k_acc_gate8<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate8<float><<<grid_for(n), kT, 0, st>>>(a);
-    } else if (prec) k_acc_gate<bf16><<<grid_for(n), kT, 0, st>>>(a); else k_acc_gate<float><<<grid_for(n), kT, 0, st>>>(a);
+        if (prec) launch_simt(k_acc_gate8<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_acc_gate8<float>, grid_for(n), kT, 0, st, a);
+    } else if (prec) launch_simt(k_acc_gate<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_acc_gate<float>, grid_for(n), kT, 0, st, a);
     return cudaGetLastError();
 }
 
 // GAP over the z^L rows this rank holds (HW pixels per image), divided by the global H_L*W_L
 cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st) {
     dim3 g1(B, (Cp + 127) / 128);
-    if (prec) k_gap<bf16><<<g1, 128, 0, st>>>((const bf16 *)zl, HW, Cp, scratch, hw_div);
-    else k_gap<float><<<g1, 128, 0, st>>>((const float *)zl, HW, Cp, scratch, hw_div);
+    if (prec) launch_simt(k_gap<bf16>, g1, 128, 0, st, (const bf16 *)zl, HW, Cp, scratch, hw_div);
+    else launch_simt(k_gap<float>, g1, 128, 0, st, (const float *)zl, HW, Cp, scratch, hw_div);
     return cudaGetLastError();
 }
 
@@ -895,16 +963,16 @@ cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, in
     size_t shm = sizeof(float) * B * classes;
     long long n = (long long)B * HW * Cp;
     if (prec) {
-        k_fc_ce<bf16><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
+        launch_simt(k_fc_ce<bf16>, 1, 1024, shm, st, gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
                                             dlog, loss, g_fc_w, g_fc_b);
         if (n > 0)
-            k_dzl<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
+            launch_simt(k_dzl<bf16>, grid_for(n), kT, 0, st, (const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
                                                    (bf16 *)dzl, gate, hw_div);
     } else {
-        k_fc_ce<float><<<1, 1024, shm, st>>>(gap, B, Cp, C, classes, (const float *)fc_w, (const float *)fc_b,
+        launch_simt(k_fc_ce<float>, 1, 1024, shm, st, gap, B, Cp, C, classes, (const float *)fc_w, (const float *)fc_b,
                                              labels, dlog, loss, g_fc_w, g_fc_b);
         if (n > 0)
-            k_dzl<float><<<grid_for(n), kT, 0, st>>>((const float *)zl, dlog, (const float *)fc_w, B, HW, Cp, C,
+            launch_simt(k_dzl<float>, grid_for(n), kT, 0, st, (const float *)zl, dlog, (const float *)fc_w, B, HW, Cp, C,
                                                     classes, (float *)dzl, gate, hw_div);
     }
     return cudaGetLastError();
@@ -923,6 +991,8 @@ cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int C
 // dst rows [r0, r1) += src (contiguous [B][r1-r0][W][Cp]): received halo delta of a neighbour rank
 template <typename T>
 __global__ void k_add_rows(View dst, int r0, int r1, const T *src, int B) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
     const int rows = r1 - r0, W = dst.W, Cp = dst.Cp;
     long long n = (long long)B * rows * W * Cp;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -940,29 +1010,29 @@ __global__ void k_add_rows(View dst, int r0, int r1, const T *src, int B) {
 cudaError_t add_rows(int prec, const View &dst, int r0, int r1, const void *src, int B, cudaStream_t st) {
     long long n = (long long)B * (r1 - r0) * dst.W * dst.Cp;
     if (n <= 0) return cudaSuccess;
-    if (prec) k_add_rows<bf16><<<grid_for(n), kT, 0, st>>>(dst, r0, r1, (const bf16 *)src, B);
-    else k_add_rows<float><<<grid_for(n), kT, 0, st>>>(dst, r0, r1, (const float *)src, B);
+    if (prec) launch_simt(k_add_rows<bf16>, grid_for(n), kT, 0, st, dst, r0, r1, (const bf16 *)src, B);
+    else launch_simt(k_add_rows<float>, grid_for(n), kT, 0, st, dst, r0, r1, (const float *)src, B);
     return cudaGetLastError();
 }
 
 cudaError_t gate_copy(int prec, const void *src, const void *act, void *dst, long long n, int gate, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    if (prec) k_gate_copy<bf16><<<grid_for(n), kT, 0, st>>>((const bf16 *)src, (const bf16 *)act, (bf16 *)dst, n, gate);
-    else k_gate_copy<float><<<grid_for(n), kT, 0, st>>>((const float *)src, (const float *)act, (float *)dst, n, gate);
+    if (prec) launch_simt(k_gate_copy<bf16>, grid_for(n), kT, 0, st, (const bf16 *)src, (const bf16 *)act, (bf16 *)dst, n, gate);
+    else launch_simt(k_gate_copy<float>, grid_for(n), kT, 0, st, (const float *)src, (const float *)act, (float *)dst, n, gate);
     return cudaGetLastError();
 }
 
 cudaError_t sgd_update(int prec, float *master, void *params, float *grads, long long n, float lr, cudaStream_t st) {
-    if (prec) k_sgd<bf16><<<grid_for(n), kT, 0, st>>>(master, (bf16 *)params, grads, n, lr);
-    else k_sgd<float><<<grid_for(n), kT, 0, st>>>(master, (float *)params, grads, n, lr);
+    if (prec) launch_simt(k_sgd<bf16>, grid_for(n), kT, 0, st, master, (bf16 *)params, grads, n, lr);
+    else launch_simt(k_sgd<float>, grid_for(n), kT, 0, st, master, (float *)params, grads, n, lr);
     return cudaGetLastError();
 }
 
 cudaError_t transpose_weights(int prec, const void *w, const void *gamma, void *wt, int cout, int coutp, int k,
                               int cinp, cudaStream_t st) {
     dim3 g((cinp + 31) / 32, (coutp + 31) / 32, k * k), blk(32, 8);
-    if (prec) k_transpose_w<bf16><<<g, blk, 0, st>>>((const bf16 *)w, (const bf16 *)gamma, (bf16 *)wt, cout, coutp, k, cinp);
-    else k_transpose_w<float><<<g, blk, 0, st>>>((const float *)w, (const float *)gamma, (float *)wt, cout, coutp, k, cinp);
+    if (prec) launch_simt(k_transpose_w<bf16>, g, blk, 0, st, (const bf16 *)w, (const bf16 *)gamma, (bf16 *)wt, cout, coutp, k, cinp);
+    else launch_simt(k_transpose_w<float>, g, blk, 0, st, (const float *)w, (const float *)gamma, (float *)wt, cout, coutp, k, cinp);
     return cudaGetLastError();
 }
 
