@@ -62,13 +62,30 @@ struct TcConv {
     int tw_log2;           // TW = 1 << tw_log2
     int pat_w, pat_h, pat_ox, pat_oy;   // im2col kernel: input patch per tile (pixels) and its offset
     uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
-    // tile index -> (n tile, tile column, tile row, image); n tiles vary fastest
+    int cta2;              // 1: CTA-pair kernel (k_conv_tc2): tile = 2 * pair + CTA rank, m_tiles rounded up to even
+    // tile index -> (n tile, tile column, tile row, image); n tiles vary fastest.  CTA pairs: the two
+    // CTAs of a pair take consecutive pixel tiles of the same n tile (an odd last tile decodes to
+    // image B: fully out of bounds for every TMA load / store).
     __device__ __forceinline__ void decode(int tile, int &nt, int &tx, int &ty, int &b) const {
-        const int mt = fdiv(tile, fd_nt), r = fdiv(mt, fd_tx);
-        nt = tile - mt * n_tiles;
+        int mt;
+        if (cta2) {
+            const int pair = tile >> 1, mp = fdiv(pair, fd_nt);
+            nt = pair - mp * n_tiles;
+            mt = 2 * mp + (tile & 1);
+        } else {
+            mt = fdiv(tile, fd_nt);
+            nt = tile - mt * n_tiles;
+        }
+        const int r = fdiv(mt, fd_tx);
         tx = mt - r * tiles_x;
         b = fdiv(r, fd_ty);
         ty = r - b * tiles_y;
+    }
+    // the accumulator of this CTA's tile has been drained: arrive on the MMA issuer's tempty barrier
+    // (CTA pairs: the leader CTA's barrier, through the cluster window)
+    __device__ __forceinline__ void tempty_arrive(uint64_t *bar) const {
+        if (cta2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(bar), 0));
+        else ptx::mbar_arrive(bar);
     }
     __device__ __forceinline__ static int fdiv(int n, const uint32_t (&f)[2]) {
         return (int)((__umulhi((uint32_t)n, f[0]) + (uint32_t)n) >> f[1]);
@@ -259,7 +276,7 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
         P.decode(tile, nt, tx, ty, b);
         const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
         const int yg = yg0 + my, xg = xg0 + mx;
-        const bool valid = yg < P.out_b && xg < P.Wo;
+        const bool valid = yg < P.out_b && xg < P.Wo && b < P.B;
         // invalid pixels (clipped by the TMA store) read the residual's first pixel instead
         const bf16 *resp = !P.has_res || rt ? nullptr
                            : valid          ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
@@ -341,7 +358,7 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (lane == 0) P.tempty_arrive(tempty + acc);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     if (leader) bulk_wait_all();
@@ -420,7 +437,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (lane == 0) P.tempty_arrive(tempty + acc);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     if (leader) bulk_wait_all();
@@ -452,7 +469,11 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         ptx::tma_load_4d(bd, tmO, ebar + pi, nb, xg0, yg0 - P.out.base, b);
         if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, xg0, yg0 - P.act.base, b);
     };
-    auto ngroups = [&](int tile) { const int nt = tile % P.n_tiles; return min(BN / 64, (P.n_out - nt * BN + 63) / 64); };
+    auto ngroups = [&](int tile) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        return min(BN / 64, (P.n_out - nt * BN + 63) / 64);
+    };
     if (leader && (int)blockIdx.x < num_tiles) issue(blockIdx.x, 0, 0);
     int acc = 0, pi = 0;
     uint32_t aphase = 0, ephase[2] = {0, 0};
@@ -509,7 +530,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (lane == 0) P.tempty_arrive(tempty + acc);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     if (leader) bulk_wait_all();
@@ -596,7 +617,7 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(tempty + acc);
+        if (lane == 0) P.tempty_arrive(tempty + acc);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     }
@@ -702,6 +723,134 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ conv FP / dgrad on CTA pairs (cta_group::2)
+// The per-tap kernel above is bound by its TMA loads (48 KB per 64-channel K-step at BN = 256, one
+// 128-pixel A box + the BN x 64 weight box, for 512 tensor cycles).  Here two CTAs of a cluster
+// (one TPC) form one M = 256 x N = BN tcgen05.mma.cta_group::2: each CTA loads its own 128-pixel
+// A tile and HALF of the weight tile (BN/2 rows), the leader issues the MMA over both CTAs' smem and
+// each CTA's TMEM receives its own 128 accumulator rows.  Loads per CTA per K-step: 16 + BN/2 x 128 B
+// (32 KB at BN = 256), so more pipeline stages fit and the tensor pipe is fed from 2/3 of the bytes.
+//   full[s]   leader CTA only: expects both CTAs' bytes (the peer's TMA signals it through the
+//             cluster window, .cta_group::2);
+//   empty[s], tfull[a]: in both CTAs, arrived by the leader's multicast tcgen05.commit;
+//   tempty[a] leader CTA: 8 epilogue warps of each CTA arrive (the peer's remotely).
+template <int BN>
+struct Conv2Cfg {
+    static constexpr int kA = 128 * 128, kBh = (BN / 2) * 128;
+    static constexpr int kStageBytes = kA + kBh;
+    static constexpr int kOutBufs = BN <= 128 ? 4 : 2;
+    static constexpr int kAvail = 232448 - kOutBufs * kOutStage - 2048;
+    static constexpr int kStages = kAvail / kStageBytes > 10 ? 10 : kAvail / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + kOutBufs * kOutStage + 1024 + 512;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
+    k_conv_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
+    using Cfg = Conv2Cfg<BN>;
+    constexpr int S = Cfg::kStages;
+    constexpr int ABYTES = Cfg::kA, BBYTES = Cfg::kBh;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + S * ABYTES;
+    uint8_t *sO = sB + S * BBYTES;
+    uint64_t *full = (uint64_t *)(sO + Cfg::kOutBufs * kOutStage);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *ebar = tempty + 2;
+    uint32_t *tslot = (uint32_t *)(ebar + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 16); }
+        ptx::mbar_init(ebar, 1);
+        ptx::mbar_init(ebar + 1, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc2(tslot, 2 * BN);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();     // both CTAs' barriers initialised, TMEM allocated
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    ptx::griddep_wait();     // PDL: the setup above overlapped the previous kernel's tail
+    ptx::griddep_launch();
+    const int num_tiles = P.m_tiles * P.n_tiles;   // = 2 x pairs (m_tiles rounded up to even)
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t full0 = ptx::mapa(ptx::smem_u32(full), 0);   // leader's full[0] (cluster window)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int nt, tx, ty, b;
+                P.decode(tile, nt, tx, ty, b);
+                const int y0 = (P.out_a + ty * P.TH) * P.a_mul, x0 = tx * P.TW * P.a_mul;
+                const int n0 = nt * BN + (int)rank * (BN / 2);
+                for (int ks = 0; ks < P.k_steps; ++ks) {
+                    const int tap = ks / P.cin_chunks, c = ks - tap * P.cin_chunks;
+                    ptx::mbar_wait(empty + stage, phase ^ 1);
+                    if (rank == 0) {
+                        ptx::mbar_arrive_expect_tx(full + stage, 2 * (ABYTES + BBYTES));
+                        ptx::tma_load_4d(sA + stage * ABYTES, &tmA, full + stage, c * 64, x0 + P.tap_ox[tap],
+                                         y0 + P.tap_oy[tap] - P.in_base, b);
+                        ptx::tma_load_3d(sB + stage * BBYTES, &tmB, full + stage, c * 64, P.tap_w[tap], n0);
+                    } else {
+                        const uint32_t fb = full0 + stage * 8;
+                        ptx::tma_load_4d_2sm(sA + stage * ABYTES, &tmA, fb, c * 64, x0 + P.tap_ox[tap],
+                                             y0 + P.tap_oy[tap] - P.in_base, b);
+                        ptx::tma_load_3d_2sm(sB + stage * BBYTES, &tmB, fb, c * 64, P.tap_w[tap], n0);
+                    }
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {   // whole warp of the leader CTA: tcgen05.mma.cta_group::2 / commit, elect.sync-issued
+            constexpr uint32_t idesc = ptx::idesc_bf16(256, BN, 0, 0);
+            const uint64_t dA = ptx::smem_desc(ptx::smem_u32(sA), 16, 1024, 2);
+            const uint64_t dB = ptx::smem_desc(ptx::smem_u32(sB), 16, 1024, 2);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int ks = 0; ks < P.k_steps; ++ks) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = (uint32_t)dA + stage * (ABYTES >> 4);
+                    const uint32_t b0 = (uint32_t)dB + stage * (BBYTES >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        if (!(P.dbg & 2)) ptx::umma2_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                    ptx::umma2_commit_mc(empty + stage, 3);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma2_commit_mc(tfull + acc, 3);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();     // no CTA leaves while its peer may still signal its barriers
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc2(tmem, 2 * BN);
     }
 }
 
@@ -1132,6 +1281,150 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ conv FP / dgrad: CTA pairs + halo-reuse A
+// Stride-1 3x3 layers with >= 128 output channels.  Shared-memory traffic per SM decides the rate
+// here (TMA writes + UMMA operand reads share the 128 B/clk smem port): the CTA pair halves the
+// weight bytes per SM, and the halo box ((8+2) x (16+2) pixels x 64 channels, loaded once per
+// 64-channel chunk and read by all 9 taps at start offsets ky*10+kx, see k_conv_tc_halo) divides the
+// activation bytes by ~6.  Per CTA per tap: 16 KB of weights (BN = 256) + 1/9 of a 23 KB box.
+template <int BN>
+struct Conv2HCfg {
+    static constexpr int kABytes = HaloGeom<3>::kABytes;          // 23 KB halo box
+    static constexpr int kBh = (BN / 2) * 128;
+    static constexpr int kSA = 3;
+    static constexpr int kOutBufs = BN <= 128 ? 4 : 2;
+    static constexpr int kAvail = 232448 - kSA * kABytes - kOutBufs * kOutStage - 2048;
+    static constexpr int kSB = kAvail / kBh > 12 ? 12 : kAvail / kBh;
+    static constexpr int kSmem = kSA * kABytes + kSB * kBh + kOutBufs * kOutStage + 1024 + 512;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
+    k_conv_tc2h(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
+    using Cfg = Conv2HCfg<BN>;
+    constexpr int SA = Cfg::kSA, SB = Cfg::kSB, AB = Cfg::kABytes, BB = Cfg::kBh;
+    constexpr int KH = 3, HP = HaloGeom<KH>::kPitch, taps = 9;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = sA + SA * AB;
+    uint8_t *sO = sB + SB * BB;
+    uint64_t *fullA = (uint64_t *)(sO + Cfg::kOutBufs * kOutStage);
+    uint64_t *emptyA = fullA + SA;
+    uint64_t *fullB = emptyA + SA;
+    uint64_t *emptyB = fullB + SB;
+    uint64_t *tfull = emptyB + SB;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *ebar = tempty + 2;
+    uint32_t *tslot = (uint32_t *)(ebar + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
+        for (int i = 0; i < SB; ++i) { ptx::mbar_init(fullB + i, 1); ptx::mbar_init(emptyB + i, 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 16); }
+        ptx::mbar_init(ebar, 1);
+        ptx::mbar_init(ebar + 1, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc2(tslot, 2 * BN);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int num_tiles = P.m_tiles * P.n_tiles;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t fullA0 = ptx::mapa(ptx::smem_u32(fullA), 0), fullB0 = ptx::mapa(ptx::smem_u32(fullB), 0);
+            constexpr uint32_t abytes = HP * HaloGeom<KH>::kRows * 128;
+            int sa = 0, sb = 0;
+            uint32_t pa = 0, pb = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int nt, tx, ty, b;
+                P.decode(tile, nt, tx, ty, b);
+                const int y0 = P.out_a + ty * 16, x0 = tx * 8, n0 = nt * BN + (int)rank * (BN / 2);
+                for (int c = 0; c < P.cin_chunks; ++c) {
+                    ptx::mbar_wait(emptyA + sa, pa ^ 1);
+                    if (rank == 0) {
+                        ptx::mbar_arrive_expect_tx(fullA + sa, 2 * abytes);
+                        ptx::tma_load_4d(sA + sa * AB, &tmA, fullA + sa, c * 64, x0 - P.pad, y0 - P.pad - P.in_base, b);
+                    } else {
+                        ptx::tma_load_4d_2sm(sA + sa * AB, &tmA, fullA0 + sa * 8, c * 64, x0 - P.pad,
+                                             y0 - P.pad - P.in_base, b);
+                    }
+                    if (++sa == SA) { sa = 0; pa ^= 1; }
+                    for (int tap = 0; tap < taps; ++tap) {
+                        ptx::mbar_wait(emptyB + sb, pb ^ 1);
+                        if (rank == 0) {
+                            ptx::mbar_arrive_expect_tx(fullB + sb, 2 * BB);
+                            ptx::tma_load_3d(sB + sb * BB, &tmB, fullB + sb, c * 64, tap, n0);
+                        } else {
+                            ptx::tma_load_3d_2sm(sB + sb * BB, &tmB, fullB0 + sb * 8, c * 64, tap, n0);
+                        }
+                        if (++sb == SB) { sb = 0; pb ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(256, BN, 0, 0);
+            const uint64_t dA = ptx::smem_desc_sw128_bo(ptx::smem_u32(sA), 16, HP * 128, 0);
+            const uint64_t dB = ptx::smem_desc_sw128(ptx::smem_u32(sB), 16, 1024);
+            const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            int sa = 0, sb = 0, acc = 0;
+            uint32_t pa = 0, pb = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                int first = 1;
+                for (int c = 0; c < P.cin_chunks; ++c) {
+                    ptx::mbar_wait(fullA + sa, pa);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = (uint32_t)dA + sa * (AB >> 4);
+#pragma unroll
+                    for (int tap = 0; tap < taps; ++tap) {
+                        const int ky = tap / KH, kx = tap - ky * KH;
+                        ptx::mbar_wait(fullB + sb, pb);
+                        ptx::tc_fence_after();
+                        const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
+                        const uint32_t b0 = (uint32_t)dB + sb * (BB >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            if (!(P.dbg & 2)) ptx::umma2_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
+                            first = 0;
+                        }
+                        ptx::umma2_commit_mc(emptyB + sb, 3);
+                        if (++sb == SB) { sb = 0; pb ^= 1; }
+                    }
+                    ptx::umma2_commit_mc(emptyA + sa, 3);
+                    if (++sa == SA) { sa = 0; pa ^= 1; }
+                }
+                ptx::umma2_commit_mc(tfull + acc, 3);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc2(tmem, 2 * BN);
     }
 }
 
@@ -2224,7 +2517,18 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     CUtensorMap A, Bm;
     if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN, KC)) return false;
     static const int halo_fp128 = env_int("LRCNN_HALO_FP128", 1);   // FP of 128-wide outputs: A traffic / 6
-    if ((halo_on || (halo_fp128 && P.mode == 0 && BN == 128)) && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1) {
+    static const int cta2 = env_int("LRCNN_2CTA", 1);
+    // stride-1 3x3 with >= 128 outputs: CTA pairs + halo-reuse A (k_conv_tc2h)
+    bool try2h = cta2 && KC == 64 && BN >= 128 && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1;
+    if (try2h) {   // the fixed 8 x 16 halo tile must not pad small maps much more than pick_tile would
+        int tw = 8, th = 16;
+        pick_tile(rows, P.Wo, 1, tw, th);
+        const long best = (long)((P.Wo + tw - 1) / tw) * tw * ((rows + th - 1) / th) * th;
+        const long halo = (long)((P.Wo + 7) / 8) * 8 * ((rows + 15) / 16) * 16;
+        try2h = halo * 100 <= best * 108;
+    }
+    if (!try2h && (halo_on || (halo_fp128 && P.mode == 0 && BN == 128)) && P.halo_ok && cin_p % 64 == 0 &&
+        P.o_stride == 1) {
         P.TW = 8; P.TH = 16;
         P.tiles_x = (P.Wo + 7) / 8;
         P.tiles_y = (rows + 15) / 16;
@@ -2244,12 +2548,15 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         if (BN == 128) return launch_conv_halo<128>(P, A, Bm, O, tiles, st);
         return launch_conv_halo<256>(P, A, Bm, O, tiles, st);
     }
-    pick_tile(rows, P.Wo, P.a_mul, P.TW, P.TH);
+    if (try2h) { P.TW = 8; P.TH = 16; }
+    else pick_tile(rows, P.Wo, P.a_mul, P.TW, P.TH);
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.m_tiles = P.B * P.tiles_x * P.tiles_y;
     tile_div_init(P);
-    if (!encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC)) return false;
+    if (try2h ? !encode_view(&A, in, P.B, HaloGeom<3>::kPitch, HaloGeom<3>::kRows)
+              : !encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC))
+        return false;
     // output map for the TMA-store epilogue (FP, unit output stride): rows end at out_b
     static const int tma_out = env_int("LRCNN_TMA_OUT", 1);
     CUtensorMap O = A;
@@ -2275,6 +2582,61 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         if (encode_view(&O, ov, P.B, P.TW, P.TH) && (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH))) P.tma_dg = 1;
     }
     int tiles = P.m_tiles * P.n_tiles;
+    if (try2h && (P.tma_out || P.tma_dg) && P.m_tiles >= 2) {
+        P.cta2 = 1;
+        P.m_tiles += P.m_tiles & 1;
+        tiles = P.m_tiles * P.n_tiles;
+        if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN / 2, KC)) return false;
+        const int grid = tiles < num_sms() ? tiles : num_sms() & ~1;
+        if (BN == 256) {
+            static bool attr = false;
+            if (!attr) {
+                if (cudaFuncSetAttribute(k_conv_tc2h<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Conv2HCfg<256>::kSmem) != cudaSuccess)
+                    return false;
+                attr = true;
+            }
+            return launch_pdl(k_conv_tc2h<256>, grid, kConvThreads, Conv2HCfg<256>::kSmem, st, A, Bm, O, G, P);
+        }
+        static bool attr = false;
+        if (!attr) {
+            if (cudaFuncSetAttribute(k_conv_tc2h<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Conv2HCfg<128>::kSmem) != cudaSuccess)
+                return false;
+            attr = true;
+        }
+        return launch_pdl(k_conv_tc2h<128>, grid, kConvThreads, Conv2HCfg<128>::kSmem, st, A, Bm, O, G, P);
+    }
+    if (try2h) {   // no TMA epilogue for this shape: single-CTA halo kernel with the same box map
+        if (BN == 128) return launch_conv_halo<128>(P, A, Bm, O, tiles, st);
+        return launch_conv_halo<256>(P, A, Bm, O, tiles, st);
+    }
+    if (cta2 && KC == 64 && BN >= 128 && (P.tma_out || P.tma_dg) && P.m_tiles >= 2 && P.k_steps >= 8) {
+        // CTA pairs: M = 256 (two pixel tiles), each CTA loads half of the weight tile
+        P.cta2 = 1;
+        P.m_tiles += P.m_tiles & 1;
+        tiles = P.m_tiles * P.n_tiles;
+        if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN / 2, KC)) return false;
+        int grid = tiles < num_sms() ? tiles : num_sms() & ~1;
+        if (BN == 256) {
+            static bool attr = false;
+            if (!attr) {
+                if (cudaFuncSetAttribute(k_conv_tc2<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Conv2Cfg<256>::kSmem) != cudaSuccess)
+                    return false;
+                attr = true;
+            }
+            return launch_pdl(k_conv_tc2<256>, grid, kConvThreads, Conv2Cfg<256>::kSmem, st, A, Bm, O, G, P);
+        }
+        static bool attr = false;
+        if (!attr) {
+            if (cudaFuncSetAttribute(k_conv_tc2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Conv2Cfg<128>::kSmem) !=
+                cudaSuccess)
+                return false;
+            attr = true;
+        }
+        return launch_pdl(k_conv_tc2<128>, grid, kConvThreads, Conv2Cfg<128>::kSmem, st, A, Bm, O, G, P);
+    }
     if (KC == 16) {
         if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, G, tiles, st);
         if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, G, tiles, st);
