@@ -347,7 +347,7 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             fence_async_smem();
             epi_bar_n<NE>();
             if (leader && !(P.dbg & 1)) {
-                tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, xg0, yg0 - P.out.base, b);
+                tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
                 bulk_commit();
             }
             if (rt && leader) {   // prefetch the next group's residual into the other buffer
@@ -390,8 +390,8 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
         if (leader) {
             bulk_wait_read0();
             ptx::mbar_arrive_expect_tx(ebar, ebytes);
-            ptx::tma_load_4d(bufD, tmO, ebar, n0, xg0, yg0 - P.out.base, b);
-            if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, n0, xg0, yg0 - P.act.base, b);
+            ptx::tma_load_4d(bufD, tmO, ebar, n0, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+            if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, n0, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
         }
         ptx::mbar_wait(tfull + acc, aphase);
         ptx::tc_fence_after();
@@ -425,13 +425,13 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
             fence_async_smem();
             epi_bar_n<NE>();
             if (leader) {
-                tma_store_4d(tmO, bufD, nb, xg0, yg0 - P.out.base, b);
+                tma_store_4d(tmO, bufD, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
                 bulk_commit();
                 if (grp + 1 < ngrp) {   // next group: wait until the store has read bufD, then reload
                     bulk_wait_read0();
                     ptx::mbar_arrive_expect_tx(ebar, ebytes);
-                    ptx::tma_load_4d(bufD, tmO, ebar, nb + 64, xg0, yg0 - P.out.base, b);
-                    if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, nb + 64, xg0, yg0 - P.act.base, b);
+                    ptx::tma_load_4d(bufD, tmO, ebar, nb + 64, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+                    if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, nb + 64, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
                 }
             }
         }
@@ -466,8 +466,8 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         const int nb = nt * BN + grp * 64, xg0 = tx * P.TW, yg0 = P.out_a + ty * P.TH;
         uint8_t *bd = stage_out + (2 * pi) * kOutStage;
         ptx::mbar_arrive_expect_tx(ebar + pi, ebytes);
-        ptx::tma_load_4d(bd, tmO, ebar + pi, nb, xg0, yg0 - P.out.base, b);
-        if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, xg0, yg0 - P.act.base, b);
+        ptx::tma_load_4d(bd, tmO, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+        if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
     };
     auto ngroups = [&](int tile) {
         int nt, tx, ty, b;
@@ -523,7 +523,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
             fence_async_smem();
             epi_bar_n<NE>();
             if (leader) {
-                tma_store_4d(tmO, stage_out + (2 * pi) * kOutStage, nb, xg0, yg0 - P.out.base, b);
+                tma_store_4d(tmO, stage_out + (2 * pi) * kOutStage, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
                 bulk_commit();
             }
             pi ^= 1;
@@ -2575,11 +2575,15 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     if (tma_res && P.tma_out && P.has_res && P.res.Cp == P.out.Cp && P.n_out % 64 == 0 && aligned16(P.res.p) &&
         encode_view(&G, P.res, P.B, P.TW, P.TH))
         P.tma_res = 1;
-    if (tma_dg && P.mode == 1 && P.o_stride == 1 && P.out.Cp % 64 == 0 && P.n_out == P.out.Cp &&
+    // (strided convs: each parity class writes every o_stride-th row / column of delta_in, so the
+    // delta / activation boxes use TMA element strides o_stride; rows end at the class's last row)
+    if (tma_dg && P.mode == 1 && P.out.Cp % 64 == 0 && P.n_out == P.out.Cp &&
         (!P.gate || (P.act.Cp == P.out.Cp && aligned16(P.act.p)))) {
         View ov = P.out;
-        ov.rows = P.out_b - P.out.base;
-        if (encode_view(&O, ov, P.B, P.TW, P.TH) && (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH))) P.tma_dg = 1;
+        ov.rows = P.o_row0 + P.o_stride * (P.out_b - 1) + 1 - P.out.base;
+        if (encode_view(&O, ov, P.B, P.TW, P.TH, P.o_stride) &&
+            (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH, P.o_stride)))
+            P.tma_dg = 1;
     }
     int tiles = P.m_tiles * P.n_tiles;
     if (try2h && (P.tma_out || P.tma_dg) && P.m_tiles >= 2) {
