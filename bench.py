@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--segments", default="pool", choices=["pool", "none"])
     ap.add_argument("--n-bands", type=int, default=4)
     ap.add_argument("--band-rows", type=int, default=0)
+    ap.add_argument("--mem-budget-gb", type=float, default=0.0,
+                    help="budget-driven planning: the smallest band count whose workspace fits (lrcnn_plan_budget)")
     ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
     ap.add_argument("--no-balanced", action="store_true",
@@ -218,6 +220,10 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         comm = LB.Comm.nccl(uid[0], rank, world)
         plan.set_comm(comm)
+    elif a.mem_budget_gb > 0 and a.mode != "column":
+        plan = LB.Plan.for_budget(net, B, int(a.mem_budget_gb * 1e9), max_bands=64, mode=a.mode, prec="bf16",
+                                  flags=flags)
+        kw = {"n_bands": plan.n_bands, "mem_budget_gb": a.mem_budget_gb}
     else:
         plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
     mem = plan.memory()

@@ -141,6 +141,20 @@ typedef struct {
 LRCNN_API lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, lrcnn_plan_t **out);
 LRCNN_API lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan);
 
+/* Budget-driven planning (Eqs. (9)-(10): "M >= Omega_FP / N" -- choose N from the
+ * memory budget; the paper's greedy takes the largest bands that fit, i.e. the smallest N).  Tries
+ * n_bands = 1 .. max_bands with opts (band_rows ignored, mode 2PS or OverL, any flags) and returns
+ * in *out the first plan whose workspace (lrcnn_plan_sizes) is <= budget_bytes, its band count in
+ * *n_bands.  The memory model is the plan's exact workspace bytes (reading R10).
+ * Host only.  LRCNN_E_INFEASIBLE if no band count fits; LRCNN_E_ARG for COLUMN mode. */
+LRCNN_API lrcnn_status lrcnn_plan_budget(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, size_t budget_bytes,
+                                         int max_bands, lrcnn_plan_t **out, int *n_bands);
+/* The turning point: the n_bands in 1 .. max_bands with the smallest
+ * workspace -- past it the 2PS halo cache (growing with N) outweighs the shrinking band working
+ * set.  Ties go to the smaller N.  Host only. */
+LRCNN_API lrcnn_status lrcnn_plan_turning_point(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts,
+                                                int max_bands, int *n_star, size_t *ws_star);
+
 /* Sizes the caller must allocate: workspace bytes, number of parameters (flat
  * element count of params/master/grads), z^L elements (B*H_L*W_L*Cp_L). */
 LRCNN_API lrcnn_status lrcnn_plan_sizes(const lrcnn_plan_t *plan, size_t *workspace_bytes, size_t *n_params,

@@ -493,6 +493,60 @@ lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     return LRCNN_OK;
 }
 
+// Budget-driven planning (Eqs. (9)-(10): choose the band count
+// N from the memory budget M, the paper's greedy "the largest band that fits, i.e. the smallest N").
+// The memory model is the plan's exact workspace bytes (reading R10), not the garbled Eq. (12).
+lrcnn_status lrcnn_plan_budget(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, size_t budget_bytes,
+                               int max_bands, lrcnn_plan_t **out, int *n_bands) {
+    if (!out || !opts || !net) return fail(LRCNN_E_ARG, "net, opts or out is NULL");
+    *out = nullptr;
+    if (opts->mode == LRCNN_COLUMN) return fail(LRCNN_E_ARG, "budget planning needs a row-centric mode");
+    if (max_bands < 1) return fail(LRCNN_E_ARG, "max_bands must be >= 1");
+    size_t best_ws = (size_t)-1;
+    for (int n = 1; n <= max_bands; ++n) {
+        lrcnn_plan_opts o = *opts;
+        o.band_rows = 0;
+        o.n_bands = n;
+        lrcnn_plan_t *p = nullptr;
+        if (lrcnn_plan(net, &o, &p) != LRCNN_OK) continue;
+        const size_t ws = p->P.ws_bytes;
+        if (ws <= budget_bytes) {
+            *out = p;
+            if (n_bands) *n_bands = n;
+            return LRCNN_OK;
+        }
+        best_ws = std::min(best_ws, ws);
+        lrcnn_plan_free(p);
+    }
+    return fail(LRCNN_E_INFEASIBLE, "no band count <= " + std::to_string(max_bands) + " fits the budget of " +
+                                        std::to_string(budget_bytes) + " bytes (smallest workspace " +
+                                        std::to_string(best_ws) + ")");
+}
+
+// The paper's turning point: the band count whose workspace is the
+// smallest -- beyond it the 2PS halo cache, which grows with N, outweighs the shrinking band
+// working set.  Ties go to the smaller N (fewer, larger launches).
+lrcnn_status lrcnn_plan_turning_point(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, int max_bands,
+                                      int *n_star, size_t *ws_star) {
+    if (!opts || !net || max_bands < 1) return fail(LRCNN_E_ARG, "bad arguments");
+    if (opts->mode == LRCNN_COLUMN) return fail(LRCNN_E_ARG, "turning point needs a row-centric mode");
+    int bn = 0;
+    size_t bws = (size_t)-1;
+    for (int n = 1; n <= max_bands; ++n) {
+        lrcnn_plan_opts o = *opts;
+        o.band_rows = 0;
+        o.n_bands = n;
+        lrcnn_plan_t *p = nullptr;
+        if (lrcnn_plan(net, &o, &p) != LRCNN_OK) continue;
+        if (p->P.ws_bytes < bws) { bws = p->P.ws_bytes; bn = n; }
+        lrcnn_plan_free(p);
+    }
+    if (!bn) return fail(LRCNN_E_INFEASIBLE, "no feasible band count");
+    if (n_star) *n_star = bn;
+    if (ws_star) *ws_star = bws;
+    return LRCNN_OK;
+}
+
 lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
     if (plan) {
         if (plan->P.graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)plan->P.graph_exec);

@@ -58,7 +58,7 @@ class MemoryReport(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
-EXPORTS = ["lrcnn_plan", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
+EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
            "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_plan_shard", "lrcnn_plan_xfers",
@@ -81,6 +81,8 @@ def lib():
     szp = ctypes.POINTER(ctypes.c_size_t)
     L.lrcnn_plan.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), ctypes.POINTER(vp)]
     L.lrcnn_plan_free.argtypes = [vp]
+    L.lrcnn_plan_budget.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), sz, i, ctypes.POINTER(vp), ip]
+    L.lrcnn_plan_turning_point.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), i, ip, szp]
     L.lrcnn_plan_sizes.argtypes = [vp, szp, szp, szp]
     L.lrcnn_plan_tensor.argtypes = [vp, i, ip, ip, ip, ip]
     L.lrcnn_plan_param.argtypes = [vp, i, i, szp, szp]
@@ -168,6 +170,38 @@ class Plan:
         _check(L.lrcnn_plan_sizes(self.h, ctypes.byref(ws), ctypes.byref(npar), ctypes.byref(zl)))
         self.ws_bytes, self.n_params, self.zl_elems = ws.value, npar.value, zl.value
         self.elem = 2 if prec == "bf16" else 4
+
+    @classmethod
+    def for_budget(cls, net, B, budget_bytes, max_bands=64, mode="2ps", prec="bf16", flags=0):
+        """lrcnn_plan_budget: the smallest band count whose workspace fits budget_bytes."""
+        L = lib()
+        self = cls.__new__(cls)
+        self.net, self.B, self.mode, self.prec = net, B, mode, prec
+        self._ops = net_ops(net)
+        self._desc = NetDesc(len(net["ops"]), self._ops, B, net["C"], net["H"], net["W"], net["classes"])
+        self._opts = PlanOpts(MODES[mode], PRECS[prec], 0, 0, 0, 1, flags)
+        h, nb = ctypes.c_void_p(), ctypes.c_int()
+        _check(L.lrcnn_plan_budget(ctypes.byref(self._desc), ctypes.byref(self._opts), budget_bytes, max_bands,
+                                   ctypes.byref(h), ctypes.byref(nb)))
+        self.h = h
+        self.n_bands = nb.value
+        ws, npar, zl = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        _check(L.lrcnn_plan_sizes(self.h, ctypes.byref(ws), ctypes.byref(npar), ctypes.byref(zl)))
+        self.ws_bytes, self.n_params, self.zl_elems = ws.value, npar.value, zl.value
+        self.elem = 2 if prec == "bf16" else 4
+        return self
+
+    @staticmethod
+    def turning_point(net, B, max_bands=64, mode="2ps", prec="bf16", flags=0):
+        """lrcnn_plan_turning_point: (n*, workspace bytes at n*)."""
+        L = lib()
+        ops = net_ops(net)
+        desc = NetDesc(len(net["ops"]), ops, B, net["C"], net["H"], net["W"], net["classes"])
+        opts = PlanOpts(MODES[mode], PRECS[prec], 0, 0, 0, 1, flags)
+        n, ws = ctypes.c_int(), ctypes.c_size_t()
+        _check(L.lrcnn_plan_turning_point(ctypes.byref(desc), ctypes.byref(opts), max_bands, ctypes.byref(n),
+                                          ctypes.byref(ws)))
+        return n.value, ws.value
 
     def __del__(self):
         try:

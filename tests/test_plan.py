@@ -285,3 +285,44 @@ def test_balanced_bands_minimal_and_exact(which):
                 fewer = EN.enumerate_2ps(net, seg, EN.band_ends(h, n_bands=n - 1), shp)
                 assert _arena_bytes(net, seg, fewer, shp, B, 2, cps) > budget
         assert p1.ws_bytes <= p0.ws_bytes
+
+
+# ---------------------------------------------------------------- budget-driven planning (f2)
+def _ws(net, B, n, mode="2ps", flags=0):
+    return LB.Plan(net, B, mode=mode, prec="bf16", n_bands=n, flags=flags).ws_bytes
+
+
+@pytest.mark.parametrize("which", ["c2", "c4", "vgg_whole"])
+def test_plan_budget_is_smallest_fitting_n(which):
+    """lrcnn_plan_budget (the greedy 'largest band that fits'): the returned band
+    count is the smallest n whose workspace fits the budget, checked by brute force over plans."""
+    if which == "c2":
+        net, B, flags = WL.vgg16(H=224, W=224, segments="pool"), 32, LB.FLAG_BALANCED_BANDS
+    elif which == "c4":
+        net, B, flags = WL.resnet50(H=3600, W=2400), 8, LB.FLAG_BALANCED_BANDS
+    else:
+        net, B, flags = WL.vgg16(H=512, W=512, segments="none"), 4, 0
+    ws = {n: _ws(net, B, n, flags=flags) for n in range(1, 25)}
+    lo, hi = min(ws.values()), ws[1]
+    for budget in (hi, (lo + hi) // 2, lo + (hi - lo) // 5, lo):
+        p = LB.Plan.for_budget(net, B, budget, max_bands=24, flags=flags)
+        n = p.n_bands
+        assert p.ws_bytes == ws[n] <= budget
+        assert all(ws[m] > budget for m in range(1, n)), (which, budget, n)
+    with pytest.raises(LB.LrcnnError) as e:
+        LB.Plan.for_budget(net, B, lo - 1, max_bands=24, flags=flags)
+    assert e.value.status == 3            # LRCNN_E_INFEASIBLE
+
+
+def test_plan_turning_point():
+    """The paper's turning point: 2PS workspace first falls with N (smaller band
+    working set) and then rises (the halo cache grows with N); lrcnn_plan_turning_point returns the
+    brute-force argmin, strictly inside the range for a whole-net VGG-16 at 2048x2048 (C5's image
+    size; z^L has 64 rows, so 64 is the largest band count)."""
+    net, B = WL.vgg16(H=2048, W=2048, segments="none"), 2
+    ws = {n: _ws(net, B, n) for n in range(1, 65)}
+    n_star, w_star = LB.Plan.turning_point(net, B, max_bands=64)
+    assert w_star == min(ws.values()) and ws[n_star] == w_star
+    assert all(ws[m] > w_star for m in range(1, n_star))
+    assert 1 < n_star < 64
+    assert ws[64] > w_star and ws[1] > w_star
