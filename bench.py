@@ -58,6 +58,19 @@ def parse():
     return ap.parse_args()
 
 
+def demangle(name):
+    """lrcnn::k_conv_tc2h<256> from the mangled kernel name cudaFuncGetName returns."""
+    try:
+        import subprocess
+        out = subprocess.run(["c++filt", name], capture_output=True, text=True, timeout=5).stdout.strip()
+        if out:
+            name = out
+    except Exception:
+        pass
+    name = name.split("(")[0].replace("lrcnn::", "").replace("(int)", "")
+    return name[5:] if name.startswith("void ") else name
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -319,6 +332,7 @@ def main():
     tc_ms, tc_n, tc_fl = plan.profile_read(0, stream)
     wg_ms, wg_n, wg_fl = plan.profile_read(1, stream)
     ot_ms, ot_n, _ = plan.profile_read(2, stream)
+    kern = plan.profile_kernels(0, stream) + plan.profile_kernels(1, stream)
     if a.per_op_csv:
         plan.profile_dump(a.per_op_csv, stream)
     plan.profile(False)
@@ -326,19 +340,35 @@ def main():
     achieved = tc_fl / (tc_ms / 1000.0) / 1e12 if tc_ms > 0 else 0.0
     peak_tf = peaks.get("bf16_tflops_sustained", 1385.7)
     traffic = None
-    try:
+    try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get("conv_fwd_dgrad_bytes_per_launch")
+            tj = json.load(f)
+        for name, b in tj.get("per_kernel", {}).items():
+            if kern and name == max(kern, key=lambda k: k["ms"])["name"]:
+                traffic = b
     except Exception:
         pass
     prof_steps = max(2, min(a.steps, 5))
-    roofline = {"bound": "tensor", "kernel": "conv FP + dgrad (implicit GEMM)", "achieved": achieved,
-                "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf if peak_tf else None,
+    # the dominant kernel: the tcgen05 kernel with the largest share of the step (CUDA events around
+    # each of its launches); its achieved = algorithmic conv FLOPs of its launches / their time
+    kern = [dict(k, name=demangle(k["name"])) for k in kern]
+    dom = max(kern, key=lambda k: k["ms"]) if kern else None
+    def _tf(k):
+        return k["flops"] / (k["ms"] / 1000.0) / 1e12 if k["ms"] > 0 else 0.0
+    dom_tf = _tf(dom) if dom else 0.0
+    roofline = {"bound": "tensor", "kernel": dom["name"] if dom else None, "achieved": dom_tf,
+                "peak": peak_tf, "unit": "TFLOP/s", "frac": dom_tf / peak_tf if peak_tf else None,
                 "traffic": traffic, "peak_source": "%s bf16_tflops_sustained" % peak_src,
-                "launches_per_step": tc_n / prof_steps, "ms_per_step": tc_ms / prof_steps,
-                "share_of_step": (tc_ms / prof_steps) / ms_step,
+                "launches_per_step": dom["launches"] / prof_steps if dom else 0,
+                "ms_per_step": dom["ms"] / prof_steps if dom else 0,
+                "share_of_step": (dom["ms"] / prof_steps) / ms_step if dom else 0,
+                "all_conv_fp_dgrad": {"achieved": achieved, "frac": achieved / peak_tf if peak_tf else None,
+                                      "launches_per_step": tc_n / prof_steps, "ms_per_step": tc_ms / prof_steps},
                 "wgrad": {"achieved": wg_fl / (wg_ms / 1000.0) / 1e12 if wg_ms else 0.0, "ms_per_step": wg_ms / prof_steps},
-                "other_ms_per_step": ot_ms / prof_steps}
+                "other_ms_per_step": ot_ms / prof_steps,
+                "kernels": sorted([{"name": k["name"], "ms_per_step": k["ms"] / prof_steps,
+                                    "achieved": _tf(k), "frac": _tf(k) / peak_tf if peak_tf else None}
+                                   for k in kern], key=lambda k: -k["ms_per_step"])[:8]}
 
     # ---------------------------------------------------------------- memory vs layer-wise (COLUMN)
     mem_rep = {"peak_allocated_bytes": peak, "xi_bytes": xi, "feature_map_bytes": peak - xi,

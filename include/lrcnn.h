@@ -251,6 +251,10 @@ LRCNN_API lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan);
 /* Per-op profile since the last reset (synchronises the stream): CSV with one line per
  * (op, kind in fwd|dgrad|wgrad|param_grad|pool_fwd|pool_bwd|elt_fwd|elt_bwd): launches, ms, FLOPs. */
 LRCNN_API lrcnn_status lrcnn_profile_dump(lrcnn_plan_t *plan, const char *path, void *stream);
+/* Per-kernel profile of class cls (0 conv FP + dgrad, 1 wgrad, 2 other): one line per tcgen05
+ * kernel ("simt" for SIMT launches) "name,launches,ms,flops\n" written NUL-terminated into buf
+ * (len bytes; LRCNN_E_ARG if too small).  Synchronises `stream` (a cudaStream_t). */
+LRCNN_API lrcnn_status lrcnn_profile_kernels(lrcnn_plan_t *plan, int cls, char *buf, size_t len, void *stream);
 
 /* Number of kernel launches the last forward/backward/step enqueued. */
 LRCNN_API lrcnn_status lrcnn_last_launch_count(const lrcnn_plan_t *plan, long long *launches);

@@ -2333,6 +2333,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // first and then waits (griddepcontrol.wait) before touching global memory.  Captured into the
 // step's CUDA graph as programmatic edges.  LRCNN_PDL=0 disables it.
 static int env_int(const char *name, int dflt);
+static thread_local const char *g_last_kernel = nullptr;
+static void note_kernel(const void *fn) {
+    const char *nm = nullptr;
+    if (cudaFuncGetName(&nm, fn) == cudaSuccess) g_last_kernel = nm;
+}
+const char *tc_last_kernel() { return g_last_kernel; }
+void tc_clear_last_kernel() { g_last_kernel = nullptr; }
 template <typename... KArgs, typename... Args>
 static bool launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args &&...args) {
     static const int pdl = env_int("LRCNN_PDL", 1);
@@ -2346,7 +2353,9 @@ static bool launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
     at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess;
+    const bool ok = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess;
+    if (ok) note_kernel((const void *)kern);
+    return ok;
 }
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

@@ -136,6 +136,7 @@ struct ProfScope {
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             cudaEventRecord(e0, R.st);
+            tc_clear_last_kernel();
         }
     }
     ~ProfScope() {
@@ -144,6 +145,8 @@ struct ProfScope {
             R.P.pending_events[cls].push_back({(void *)e0, (void *)e1});
             R.P.pending_flops[cls].push_back(flops);
             R.P.pending_tags[cls].push_back(tag);
+            const char *k = tc_last_kernel();
+            R.P.pending_names[cls].push_back(k ? k : "");
         }
     }
 };
@@ -834,6 +837,8 @@ lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan) {
         plan->P.pending_events[c].clear();
         plan->P.pending_flops[c].clear();
         plan->P.pending_tags[c].clear();
+        plan->P.pending_names[c].clear();
+        plan->P.per_kernel[c].clear();
         plan->P.prof[c] = ProfileSlot();
     }
     plan->P.per_tag.clear();
@@ -853,6 +858,15 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
             P.prof[c].ms += t;
             P.prof[c].flops += P.pending_flops[c][i];
             P.prof[c].launches += 1;
+            {   // per tcgen05 kernel
+                const std::string &nm = P.pending_names[c][i];
+                auto it = std::find_if(P.per_kernel[c].begin(), P.per_kernel[c].end(),
+                                       [&nm](const std::pair<std::string, ProfileSlot> &q) { return q.first == nm; });
+                if (it == P.per_kernel[c].end()) { P.per_kernel[c].push_back({nm, ProfileSlot()}); it = P.per_kernel[c].end() - 1; }
+                it->second.ms += t;
+                it->second.flops += P.pending_flops[c][i];
+                it->second.launches += 1;
+            }
             const int tag = P.pending_tags[c][i];
             if (tag >= 0) {
                 auto it = std::find_if(P.per_tag.begin(), P.per_tag.end(),
@@ -868,10 +882,27 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
         P.pending_events[c].clear();
         P.pending_flops[c].clear();
         P.pending_tags[c].clear();
+        P.pending_names[c].clear();
     }
     if (ms) *ms = P.prof[cls].ms;
     if (launches) *launches = P.prof[cls].launches;
     if (flops) *flops = P.prof[cls].flops;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_profile_kernels(lrcnn_plan_t *plan, int cls, char *buf, size_t len, void *stream) {
+    if (!plan || cls < 0 || cls > 2 || !buf || !len) return fail(LRCNN_E_ARG, "bad args");
+    lrcnn_status st = lrcnn_profile_read(plan, cls, nullptr, nullptr, nullptr, stream);
+    if (st != LRCNN_OK) return st;
+    std::string out;
+    char line[512];
+    for (auto &e : plan->P.per_kernel[cls]) {
+        snprintf(line, sizeof line, "%s,%lld,%.6f,%.6e\n", e.first.empty() ? "simt" : e.first.c_str(),
+                 e.second.launches, e.second.ms, e.second.flops);
+        out += line;
+    }
+    if (out.size() + 1 > len) return fail(LRCNN_E_ARG, "buffer too small");
+    memcpy(buf, out.c_str(), out.size() + 1);
     return LRCNN_OK;
 }
 

@@ -104,6 +104,8 @@ struct Plan {
     std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t
     std::vector<double> pending_flops[3];
     std::vector<int> pending_tags[3];             // op*8 + kind (profile dump)
+    std::vector<std::string> pending_names[3];    // tcgen05 kernel launched inside the scope ("" = SIMT)
+    std::vector<std::pair<std::string, ProfileSlot>> per_kernel[3];
     std::vector<std::pair<int, ProfileSlot>> per_tag;
     // CUDA graph of one lrcnn_step, replayed while its arguments are unchanged
     void *graph_exec = nullptr;                  // cudaGraphExec_t

@@ -61,7 +61,7 @@ class MemoryReport(ctypes.Structure):
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
-           "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_plan_shard", "lrcnn_plan_xfers",
+           "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_profile_kernels", "lrcnn_plan_shard", "lrcnn_plan_xfers",
            "lrcnn_comm_nccl_unique_id", "lrcnn_comm_init_nccl", "lrcnn_comm_loopback_group",
            "lrcnn_comm_loopback_group_free", "lrcnn_comm_init_loopback", "lrcnn_comm_free", "lrcnn_plan_set_comm",
            "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
@@ -100,6 +100,7 @@ def lib():
                                      ctypes.POINTER(ctypes.c_double), vp]
     L.lrcnn_profile_reset.argtypes = [vp]
     L.lrcnn_profile_dump.argtypes = [vp, ctypes.c_char_p, vp]
+    L.lrcnn_profile_kernels.argtypes = [vp, i, ctypes.c_char_p, sz, vp]
     L.lrcnn_last_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
     L.lrcnn_plan_shard.argtypes = [vp, i, i, ip, ip, ip, ip]
     L.lrcnn_plan_xfers.argtypes = [vp, i, i, ip, ip, ip, ip, ip]
@@ -370,6 +371,16 @@ class Plan:
         _check(lib().lrcnn_profile_read(self.h, cls, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl),
                                         _stream(stream)))
         return ms.value, n.value, fl.value
+
+    def profile_kernels(self, cls, stream=None):
+        """Per-kernel totals of profile class cls: [{name, launches, ms, flops}] (lrcnn_profile_kernels)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(lib().lrcnn_profile_kernels(self.h, cls, buf, len(buf), _stream(stream)))
+        out = []
+        for line in buf.value.decode().splitlines():
+            name, n, ms, fl = line.rsplit(",", 3)
+            out.append({"name": name, "launches": int(n), "ms": float(ms), "flops": float(fl)})
+        return out
 
     def profile_dump(self, path, stream=None):
         _check(lib().lrcnn_profile_dump(self.h, path.encode(), _stream(stream)))
