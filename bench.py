@@ -301,23 +301,43 @@ def main():
     value = gb / (ms_step / 1000.0)
 
     # ---------------------------------------------------------------- end-to-end through the public API
+    # Every step copies its batch from pinned host memory and reads the loss back.  The H2D copy of
+    # batch i+1 runs on a copy stream into a device staging buffer while step i computes (double
+    # buffering, as a training loop feeding the library would); the step then takes its batch with a
+    # device-to-device copy.  Steps run back to back (no L2 flush: the per-step working set, ~0.6 GB
+    # for C2, exceeds the 126 MB L2).  Timed as a whole on the device: first copy to last loss.
     x_host = ds.x.cpu().pin_memory()
     lab_host = ds.labels.cpu().pin_memory()
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    e2e = []
+    x_stage, lab_stage = torch.empty_like(ds.x), torch.empty_like(ds.labels)
+    cstream = torch.cuda.Stream(device=dev)
     barrier()
-    for _ in range(a.steps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        ds.x.copy_(x_host, non_blocking=True)
-        ds.labels.copy_(lab_host, non_blocking=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cstream.wait_event(e0)
+    staged = torch.cuda.Event()
+    with torch.cuda.stream(cstream):
+        x_stage.copy_(x_host, non_blocking=True)
+        lab_stage.copy_(lab_host, non_blocking=True)
+        staged.record(cstream)
+    for i in range(a.steps):
+        stream.wait_event(staged)
+        ds.x.copy_(x_stage, non_blocking=True)
+        ds.labels.copy_(lab_stage, non_blocking=True)
+        taken = torch.cuda.Event()
+        taken.record(stream)
+        if i + 1 < a.steps:
+            cstream.wait_event(taken)
+            staged = torch.cuda.Event()
+            with torch.cuda.stream(cstream):
+                x_stage.copy_(x_host, non_blocking=True)
+                lab_stage.copy_(lab_host, non_blocking=True)
+                staged.record(cstream)
         one_step()
         loss_host.copy_(ds.loss, non_blocking=True)
-        e1.record(stream)
-        e2e.append((e0, e1))
+    e1.record(stream)
     barrier()
-    ms_e2e = sum(s.elapsed_time(e) for s, e in e2e) / len(e2e)
+    ms_e2e = e0.elapsed_time(e1) / a.steps
     if world > 1:
         t = torch.tensor([ms_e2e], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
