@@ -1110,6 +1110,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const uint64_t dB = sw ? ptx::smem_desc(ptx::smem_u32(sB), 128, 1024, 0)
                                    : ptx::smem_desc(ptx::smem_u32(sB), 1024, 128, 0);
             const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
+            const uint32_t row16 = row >> 4, jstep = s == 1 ? 2u : 1u;
             ptx::mbar_wait(bfull, 0);
             int st = 0, acc = 0;
             uint32_t ph = 0, aphase = 0;
@@ -1119,14 +1120,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 const uint32_t d = tmem + acc * BN;
                 ptx::mbar_wait(full + st, ph);
                 ptx::tc_fence_after();
-                const uint32_t a0 = (uint32_t)dA + st * (kPrPatch >> 4);
-                for (int ky = 0; ky < KY; ++ky)
-                    for (int j = 0; j < NPR; ++j) {
-                        // first K-half: tap kx = 2j -> plane A pixel i + (s == 1 ? 2j : j)
-                        const uint32_t at = a0 + (ky * row + (uint32_t)(s == 1 ? 2 * j : j) * 16) / 16;
-                        const uint32_t bt = (uint32_t)dB + (ky * NPR + j) * (2048 >> 4);
-                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, at, hiA, bt, hiB, idesc, (ky | j) != 0);
+                // descriptors advance incrementally: first K-half of pair (ky, j) is tap kx = 2j ->
+                // plane-A pixel i + (s == 1 ? 2j : j) of patch row ky; weights chunk pair (ky, j)
+                uint32_t aky = (uint32_t)dA + st * (kPrPatch >> 4), bt = (uint32_t)dB;
+                uint32_t acc_flag = 0;
+                for (int ky = 0; ky < KY; ++ky, aky += row16) {
+                    uint32_t at = aky;
+                    for (int j = 0; j < NPR; ++j, at += jstep, bt += 2048 >> 4) {
+                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, at, hiA, bt, hiB, idesc, acc_flag);
+                        acc_flag = 1;
                     }
+                }
                 ptx::umma_commit(empty + st);
                 if (++st == kPrStages) { st = 0; ph ^= 1; }
                 ptx::umma_commit(tfull + acc);
