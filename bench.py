@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-balanced", action="store_true",
                     help="same band count in every segment (default: balanced bands, LRCNN_FLAG_BALANCED_BANDS)")
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group backend; gloo only to exercise the N>1 code path on one GPU")
     ap.add_argument("--parallel", default="dp", choices=["dp", "rows"],
                     help="N>1: dp = each rank its own batch, wgrad all-reduce (weak scaling); rows = the "
                          "same batch row-sharded across ranks with halo exchange (strong scaling, SURVEY 8(e))")
@@ -213,9 +215,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.backend == "gloo":   # code-path check with several ranks sharing the visible GPUs (not a bench)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)     # non-default stream: lrcnn_step replays a CUDA graph
     torch.cuda.set_stream(stream)
@@ -395,7 +402,7 @@ def main():
                "plan": {k: mem[k] for k in ("omega", "band_act", "band_delta", "halo_cache", "carry",
                                             "checkpoints", "delta_full", "workspace")}}
     cpu = None
-    if not a.no_baselines and rank == 0 and a.mode != "column" and not rows:
+    if not a.no_baselines and world == 1 and a.mode != "column":   # layer-wise memory + cpu_baseline: N=1 only
         del ds, flush
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats(dev)
