@@ -2538,7 +2538,8 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         pick_tile(rows, P.Wo, 1, tw, th);
         const long best = (long)((P.Wo + tw - 1) / tw) * tw * ((rows + th - 1) / th) * th;
         const long halo = (long)((P.Wo + 7) / 8) * 8 * ((rows + 15) / 16) * 16;
-        try2h = halo * 100 <= best * 108;
+        // FP with 128 outputs would otherwise take the single-CTA halo kernel (same 8 x 16 tile)
+        try2h = halo * 100 <= best * 108 || (P.mode == 0 && BN == 128 && halo_fp128);
     }
     if (!try2h && (halo_on || (halo_fp128 && P.mode == 0 && BN == 128)) && P.halo_ok && cin_p % 64 == 0 &&
         P.o_stride == 1) {
