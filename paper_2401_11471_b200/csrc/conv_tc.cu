@@ -60,6 +60,8 @@ struct TcConv {
     int tap_oy[49], tap_ox[49], tap_w[49];
     int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
     int tw_log2;           // TW = 1 << tw_log2
+    int th_log2;           // TH = 1 << th_log2
+    int NBt;               // images per tile (small maps: a 128-pixel tile spans NBt images; 0/1 = one)
     int pat_w, pat_h, pat_ox, pat_oy;   // im2col kernel: input patch per tile (pixels) and its offset
     uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
     int cta2;              // 1: CTA-pair kernel (k_conv_tc2): tile = 2 * pair + CTA rank, m_tiles rounded up to even
@@ -80,6 +82,7 @@ struct TcConv {
         tx = mt - r * tiles_x;
         b = fdiv(r, fd_ty);
         ty = r - b * tiles_y;
+        if (NBt > 1) b *= NBt;   // first image of the tile
     }
     // the accumulator of this CTA's tile has been drained: arrive on the MMA issuer's tempty barrier
     // (CTA pairs: the leader CTA's barrier, through the cluster window)
@@ -106,6 +109,9 @@ static inline void tile_div_init(TcConv &P) {
     int l = 0;
     while ((1 << l) < P.TW) ++l;
     P.tw_log2 = l;
+    l = 0;
+    while ((1 << l) < P.TH) ++l;
+    P.th_log2 = l;
 }
 
 struct TcWgrad {
@@ -119,6 +125,7 @@ struct TcWgrad {
     int co_tiles, ci_tiles, items;
     int out_a, dy_base, x_base;
     int s;                 // conv stride (TMA element stride of the input box)
+    int NB;                // k_wgrad_tc: images per pixel tile (batch folding for small maps)
 };
 
 static constexpr int kThreads = 192;
@@ -255,7 +262,8 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
     const bool leader = (warp == lead_warp && lane == 0);
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     const float lo = P.relu ? 0.f : -INFINITY;
-    const int my = m >> P.tw_log2, mx = m & ((1 << P.tw_log2) - 1);
+    const int my = (m >> P.tw_log2) & ((1 << P.th_log2) - 1), mx = m & ((1 << P.tw_log2) - 1);
+    const int mb = P.NBt > 1 ? m >> (P.tw_log2 + P.th_log2) : 0;   // image within a batch-folded tile
     // residual through TMA: the tile of group g is loaded into the staging buffer the group's
     // output will use (issued one group ahead, tracked by rbar); each thread adds its row
     const bool rt = P.has_res && P.tma_res && tmR;
@@ -276,10 +284,10 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
         P.decode(tile, nt, tx, ty, b);
         const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
         const int yg = yg0 + my, xg = xg0 + mx;
-        const bool valid = yg < P.out_b && xg < P.Wo && b < P.B;
+        const bool valid = yg < P.out_b && xg < P.Wo && b + mb < P.B;
         // invalid pixels (clipped by the TMA store) read the residual's first pixel instead
         const bf16 *resp = !P.has_res || rt ? nullptr
-                           : valid          ? (const bf16 *)P.res.p + (long long)b * P.res.bs +
+                           : valid          ? (const bf16 *)P.res.p + (long long)(b + mb) * P.res.bs +
                                                ((long long)(yg - P.res.base) * P.res.W + xg) * P.res.Cp
                                             : (const bf16 *)P.res.p;
         ptx::mbar_wait(tfull + acc, aphase);
@@ -549,9 +557,10 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
-        const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
-        const int yg = P.out_a + ty * P.TH + m / P.TW, xg = tx * P.TW + m % P.TW, n0 = nt * BN;
-        const bool valid = yg < P.out_b && xg < P.Wo;
+        const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y;
+        const int b = (r / P.tiles_y) * (P.NBt > 1 ? P.NBt : 1) + m / (P.TW * P.TH);
+        const int yg = P.out_a + ty * P.TH + (m / P.TW) % P.TH, xg = tx * P.TW + m % P.TW, n0 = nt * BN;
+        const bool valid = yg < P.out_b && xg < P.Wo && b < P.B;
         const int y = P.o_row0 + P.o_stride * yg, x = P.o_col0 + P.o_stride * xg;
         const long long pix = valid ? (long long)b * P.out.bs + ((long long)(y - P.out.base) * P.out.W + x) * P.out.Cp : 0;
         ptx::mbar_wait(tfull + acc, aphase);
@@ -672,7 +681,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 const int nt = tile % P.n_tiles, mt = tile / P.n_tiles;
-                const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                const int tx = mt % P.tiles_x, r = mt / P.tiles_x, ty = r % P.tiles_y;
+                const int b = (r / P.tiles_y) * (P.NBt > 1 ? P.NBt : 1);
                 const int y0 = (P.out_a + ty * P.TH) * P.a_mul, x0 = tx * P.TW * P.a_mul, n0 = nt * BN;
                 for (int ks = 0; ks < P.k_steps; ++ks) {
                     const int tap = ks / P.cin_chunks, c = ks - tap * P.cin_chunks;
@@ -1498,7 +1508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int ky = tap / P.k, kx = tap - ky * P.k;
                 const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
                 for (int pt = p0; pt < p1; ++pt) {
-                    const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
+                    const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y;
+                    const int b = (r / P.tiles_y) * (P.NB > 1 ? P.NB : 1);
                     const int y0 = P.out_a + ty * P.TH, x0 = tx * P.TW;
                     ptx::mbar_wait(empty + stage, phase ^ 1);
                     uint8_t *st = smem + stage * SB;
@@ -2392,12 +2403,12 @@ static CUtensorMapSwizzle swz_for(int kc) {
 }
 
 // kc = channels per box (64 -> 128B rows / SWIZZLE_128B, 16 -> 32B rows / SWIZZLE_32B).
-static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH, int es = 1, int kc = 64) {
+static bool encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH, int es = 1, int kc = 64, int nb = 1) {
     auto fn = encode_fn();
-    if (!fn || v.rows <= 0 || TW * es > 256 || TH * es > 256) return false;
+    if (!fn || v.rows <= 0 || TW * es > 256 || TH * es > 256 || nb < 1 || nb > 256) return false;
     cuuint64_t dims[4] = {(cuuint64_t)v.Cp, (cuuint64_t)v.W, (cuuint64_t)v.rows, (cuuint64_t)B};
     cuuint64_t strides[3] = {(cuuint64_t)v.Cp * 2, (cuuint64_t)v.W * v.Cp * 2, (cuuint64_t)v.bs * 2};
-    cuuint32_t box[4] = {(cuuint32_t)kc, (cuuint32_t)(TW * es), (cuuint32_t)(TH * es), 1};
+    cuuint32_t box[4] = {(cuuint32_t)kc, (cuuint32_t)(TW * es), (cuuint32_t)(TH * es), (cuuint32_t)nb};
     cuuint32_t estr[4] = {1, (cuuint32_t)es, (cuuint32_t)es, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     swz_for(kc), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2428,6 +2439,19 @@ static void pick_tile(int rows, int W, int s, int &TW, int &TH) {
         long cost = (long)((W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
         if (best < 0 || cost < best) { best = cost; TW = tw; TH = th; }
     }
+}
+
+// the same with batch folding: a 128-pixel tile of TW x TH x NB (NB images of a small map), the
+// shape with the fewest padded pixel slots (small maps: 7x7 -> 8x8x2 instead of 8x16x1)
+static void pick_tile_nb(int rows, int W, int s, int B, int &TW, int &TH, int &NB) {
+    long best = -1;
+    for (int nb = 1; nb <= 16; nb <<= 1)
+        for (int tw = 128 / nb; tw >= 4; tw >>= 1) {
+            const int th = 128 / nb / tw;
+            if (th < 1 || tw * s > 256 || th * s > 256) continue;
+            const long cost = (long)((B + nb - 1) / nb) * nb * ((W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+            if (best < 0 || cost < best) { best = cost; TW = tw; TH = th; NB = nb; }
+        }
 }
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
@@ -2562,14 +2586,18 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         if (BN == 128) return launch_conv_halo<128>(P, A, Bm, O, tiles, st);
         return launch_conv_halo<256>(P, A, Bm, O, tiles, st);
     }
+    static const int fold = env_int("LRCNN_BATCH_FOLD", 1);
+    int NB = 1;
     if (try2h) { P.TW = 8; P.TH = 16; }
+    else if (fold) pick_tile_nb(rows, P.Wo, P.a_mul, P.B, P.TW, P.TH, NB);
     else pick_tile(rows, P.Wo, P.a_mul, P.TW, P.TH);
+    P.NBt = NB;
     P.tiles_x = (P.Wo + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
-    P.m_tiles = P.B * P.tiles_x * P.tiles_y;
+    P.m_tiles = (P.B + NB - 1) / NB * P.tiles_x * P.tiles_y;
     tile_div_init(P);
     if (try2h ? !encode_view(&A, in, P.B, HaloGeom<3>::kPitch, HaloGeom<3>::kRows)
-              : !encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC))
+              : !encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC, NB))
         return false;
     // output map for the TMA-store epilogue (FP, unit output stride): rows end at out_b
     static const int tma_out = env_int("LRCNN_TMA_OUT", 1);
@@ -2578,7 +2606,7 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     if (tma_out && P.mode == 0 && P.o_stride == 1 && P.out.Cp % 8 == 0) {
         View ov = P.out;
         ov.rows = P.out_b - P.out.base;
-        if (encode_view(&O, ov, P.B, P.TW, P.TH)) P.tma_out = 1;
+        if (encode_view(&O, ov, P.B, P.TW, P.TH, 1, 64, NB)) P.tma_out = 1;
     }
     // dgrad with unit output stride: TMA load / combine / store of the delta tile
     static const int tma_dg = env_int("LRCNN_TMA_DG", 1);
@@ -2587,7 +2615,7 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     P.tma_res = 0;
     static const int tma_res = env_int("LRCNN_TMA_RES", 1);
     if (tma_res && P.tma_out && P.has_res && P.res.Cp == P.out.Cp && P.n_out % 64 == 0 && aligned16(P.res.p) &&
-        encode_view(&G, P.res, P.B, P.TW, P.TH))
+        encode_view(&G, P.res, P.B, P.TW, P.TH, 1, 64, NB))
         P.tma_res = 1;
     // (strided convs: each parity class writes every o_stride-th row / column of delta_in, so the
     // delta / activation boxes use TMA element strides o_stride; rows end at the class's last row)
@@ -2595,8 +2623,8 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         (!P.gate || (P.act.Cp == P.out.Cp && aligned16(P.act.p)))) {
         View ov = P.out;
         ov.rows = P.o_row0 + P.o_stride * (P.out_b - 1) + 1 - P.out.base;
-        if (encode_view(&O, ov, P.B, P.TW, P.TH, P.o_stride) &&
-            (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH, P.o_stride)))
+        if (encode_view(&O, ov, P.B, P.TW, P.TH, P.o_stride, 64, NB) &&
+            (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH, P.o_stride, 64, NB)))
             P.tma_dg = 1;
     }
     int tiles = P.m_tiles * P.n_tiles;
@@ -2953,7 +2981,7 @@ static bool wgrad_pair(const WgradArgs &a, cudaStream_t st) {
 static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     static const int on = env_int("LRCNN_WG_HALO", 1);
     const View &dy = a.dy, &x = a.x;
-    if (!on || a.s != 1 || a.k != 3 || x.Cp % 64) return false;
+    if (!on || a.s != 1 || a.k != 3 || x.Cp % 64 || dy.W < 16) return false;
     const int rows = a.b - a.a;
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
@@ -3068,10 +3096,14 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.dg = fuse_db && a.db ? a.dg : nullptr;
     P.w = (const bf16 *)a.w;
     if (P.dg && !P.w) P.db = P.dg = nullptr;
-    pick_tile(rows, dy.W, a.s, P.TW, P.TH);
+    static const int fold = env_int("LRCNN_BATCH_FOLD", 1);
+    int NB = 1;
+    if (fold) pick_tile_nb(rows, dy.W, a.s, a.B, P.TW, P.TH, NB);
+    else pick_tile(rows, dy.W, a.s, P.TW, P.TH);
+    P.NB = NB;
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
-    P.pix_tiles = a.B * P.tiles_x * P.tiles_y;
+    P.pix_tiles = (a.B + NB - 1) / NB * P.tiles_x * P.tiles_y;
     const int BN = x.Cp >= 128 ? 128 : (x.Cp <= 16 ? 16 : 64);
     P.co_tiles = (dy.Cp + 127) / 128;
     P.ci_tiles = (x.Cp + BN - 1) / BN;
@@ -3084,8 +3116,8 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.items = base_items * P.splits;
     P.out_a = a.a; P.dy_base = dy.base; P.x_base = x.base;
     CUtensorMap D, X;
-    if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
-    if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s, BN < 64 ? BN : 64)) return false;
+    if (!encode_view(&D, dy, a.B, P.TW, P.TH, 1, 64, NB)) return false;
+    if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s, BN < 64 ? BN : 64, NB)) return false;
     const bool ok = BN == 16 ? launch_wgrad<16>(P, D, X, st)
                   : BN == 64 ? launch_wgrad<64>(P, D, X, st) : launch_wgrad<128>(P, D, X, st);
     if (ok && P.db) a.db_done = true;
