@@ -7,7 +7,7 @@ for cfg in c2 c4; do
   bash scripts/ncu_launches.sh gpurun_out/${tag}_launches_$cfg.csv $cfg > gpurun_out/${tag}_launches_$cfg.txt 2>&1
   timeout 600 python bench.py --config $cfg --no-baselines --steps 3 --per-op-csv gpurun_out/${tag}_perop_$cfg.csv > /dev/null 2>&1
 done
-for k in "k_conv_tc2h:6:4" "k_wgrad_halo:6:3" "k_conv_tc2<:2:2" "k_conv_halo_rb:6:2"; do
+for k in "k_conv_tc2h:6:4" "k_wgrad_halo:6:3" "k_conv_tc2:40:2" "k_conv_halo_rb:6:2"; do
   IFS=: read kre skip cnt <<< "$k"
   name=$(echo $kre | tr -dc 'a-z0-9_')
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$kre" -s $skip -c $cnt \
@@ -19,4 +19,6 @@ for k in "k_conv_tc2h:6:4" "k_wgrad_halo:6:3" "k_conv_tc2<:2:2" "k_conv_halo_rb:
 done
 timeout 900 python bench.py > gpurun_out/${tag}_bench_c2.json 2>gpurun_out/${tag}_bench_c2.err
 timeout 900 python bench.py --config c4 --n-bands 16 > gpurun_out/${tag}_bench_c4.json 2>gpurun_out/${tag}_bench_c4.err
+timeout 900 python bench.py --config c3 --no-baselines > gpurun_out/${tag}_bench_c3.json 2>gpurun_out/${tag}_bench_c3.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${tag}_bench_reference.json 2>&1
 tail -c 400 gpurun_out/${tag}_bench_c2.json; tail -c 300 gpurun_out/${tag}_bench_c4.json
