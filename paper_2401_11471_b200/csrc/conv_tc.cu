@@ -62,6 +62,7 @@ struct TcConv {
     int tw_log2;           // TW = 1 << tw_log2
     int th_log2;           // TH = 1 << th_log2
     int NBt;               // images per tile (small maps: a 128-pixel tile spans NBt images; 0/1 = one)
+    int dg_write;          // dgrad: overwrite delta_in (gate * acc) instead of accumulating into it
     int pat_w, pat_h, pat_ox, pat_oy;   // im2col kernel: input patch per tile (pixels) and its offset
     uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
     int cta2;              // 1: CTA-pair kernel (k_conv_tc2): tile = 2 * pair + CTA rank, m_tiles rounded up to even
@@ -387,7 +388,9 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     uint8_t *bufD = stage_out, *bufG = stage_out + kOutStage;
     const uint32_t rowD = ptx::smem_u32(bufD) + m * 128, rowG = ptx::smem_u32(bufG) + m * 128;
-    const uint32_t ebytes = P.gate ? 2 * kOutStage : kOutStage;
+    // bytes the leader TMA-loads per group: the delta tile (unless overwritten) and the activation tile
+    // (gate); 0 bytes is a plain arrive that still orders the staging buffer's reuse after the store
+    const uint32_t ebytes = (P.dg_write ? 0u : (uint32_t)kOutStage) + (P.gate ? (uint32_t)kOutStage : 0u);
     int acc = 0;
     uint32_t aphase = 0, ephase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -398,7 +401,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
         if (leader) {
             bulk_wait_read0();
             ptx::mbar_arrive_expect_tx(ebar, ebytes);
-            ptx::tma_load_4d(bufD, tmO, ebar, n0, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+            if (!P.dg_write) ptx::tma_load_4d(bufD, tmO, ebar, n0, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
             if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, n0, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
         }
         ptx::mbar_wait(tfull + acc, aphase);
@@ -417,7 +420,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
             for (int cc = 0; cc < CH / 8; ++cc) {
                 const int c = hh * (CH / 8) + cc;
                 const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
-                const uint4 dd = ld_shared_v4(rowD + off);
+                const uint4 dd = P.dg_write ? make_uint4(0, 0, 0, 0) : ld_shared_v4(rowD + off);
                 const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
                 const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
                 uint32_t o[4];
@@ -438,7 +441,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
                 if (grp + 1 < ngrp) {   // next group: wait until the store has read bufD, then reload
                     bulk_wait_read0();
                     ptx::mbar_arrive_expect_tx(ebar, ebytes);
-                    ptx::tma_load_4d(bufD, tmO, ebar, nb + 64, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+                    if (!P.dg_write) ptx::tma_load_4d(bufD, tmO, ebar, nb + 64, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
                     if (P.gate) ptx::tma_load_4d(bufG, tmG, ebar, nb + 64, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
                 }
             }
@@ -466,7 +469,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
     const int q = warp & 3, m = q * 32 + lane, hh = (warp - lead_warp) >> 2;
     const bool leader = (warp == lead_warp && lane == 0);
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t ebytes = P.gate ? 2 * kOutStage : kOutStage;
+    const uint32_t ebytes = (P.dg_write ? 0u : (uint32_t)kOutStage) + (P.gate ? (uint32_t)kOutStage : 0u);
     // pair i: delta buffer stage_out + 2i*16K, activation buffer stage_out + (2i+1)*16K
     auto issue = [&](int tile, int grp, int pi) {
         int nt, tx, ty, b;
@@ -474,7 +477,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         const int nb = nt * BN + grp * 64, xg0 = tx * P.TW, yg0 = P.out_a + ty * P.TH;
         uint8_t *bd = stage_out + (2 * pi) * kOutStage;
         ptx::mbar_arrive_expect_tx(ebar + pi, ebytes);
-        ptx::tma_load_4d(bd, tmO, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+        if (!P.dg_write) ptx::tma_load_4d(bd, tmO, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
         if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
     };
     auto ngroups = [&](int tile) {
@@ -515,7 +518,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
             for (int cc = 0; cc < CH / 8; ++cc) {
                 const int c = hh * (CH / 8) + cc;
                 const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
-                const uint4 dd = ld_shared_v4(rowD + off);
+                const uint4 dd = P.dg_write ? make_uint4(0, 0, 0, 0) : ld_shared_v4(rowD + off);
                 const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
                 const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
                 uint32_t o[4];
@@ -605,7 +608,7 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
                         for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
                     }
                 } else {
-                    uint4 od = *reinterpret_cast<const uint4 *>(dst);
+                    uint4 od = P.dg_write ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4 *>(dst);
                     const uint16_t *oh = reinterpret_cast<const uint16_t *>(&od);
                     uint4 ac = make_uint4(0, 0, 0, 0);
                     if (P.gate)
@@ -2872,6 +2875,7 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
         for (int rx = 0; rx < s; ++rx) {
             TcConv P{};
             P.out = a.dx; P.act = a.act;
+            P.dg_write = a.write && s == 1;
             P.mode = 1; P.epi = 0; P.relu = 0; P.gate = a.gate; P.c_real = a.dx.Cp; P.n_out = a.dx.Cp;
             P.B = a.B; P.a_mul = 1; P.o_row0 = ry; P.o_col0 = rx; P.o_stride = s;
             // class grid: rows j with ra <= ry + s*j < rb, cols i with rx + s*i < W_in

@@ -296,6 +296,19 @@ static lrcnn_status run_forward(Run &R) {
 }
 
 // ------------------------------------------------------------------ op backward on band rows [a, b)
+// A band-internal tensor whose only reader is a stride-1 convolution gets its delta rows from that
+// conv's dgrad alone, and the dgrad's input rows cover the tensor's band rows exactly (interval
+// rule): the dgrad overwrites them (gate * acc) instead of accumulating into a zeroed buffer, and
+// the 2PS carry of band r+1 is added (gated) right after it.  Saves the band-buffer memset and
+// the dgrad epilogue's delta load.
+static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
+    if (t == 0 || t == S.in_t || t == S.out_t) return false;
+    const TensorInfo &ti = P.t[t];
+    if (ti.cons.size() != 1 || ti.cons[0].role != 0) return false;
+    const OpInfo &u = P.op[ti.cons[0].op];
+    return u.d.kind == LRCNN_OP_CONV && u.d.s == 1;
+}
+
 static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     Plan &P = R.P;
     const OpInfo &o = P.op[i];
@@ -350,11 +363,28 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.B = B;
             A.ra = std::max(0, a * o.d.s - o.d.p);
             A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
-            ++P.launches;
-            ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1);
-            if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
-            else CK(simt_conv_dgrad(R.prec, A, R.st));
-            CK(cudaGetLastError());
+            A.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
+            {
+                ++P.launches;
+                ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1);
+                if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
+                else CK(simt_conv_dgrad(R.prec, A, R.st));
+                CK(cudaGetLastError());
+            }
+            const int N = (int)S.E.size();
+            if (A.write && P.opts.mode == LRCNN_2PS && r + 1 < N) {   // + the carry of band r+1, gated
+                const int t = o.in_t, clo = S.lo[r + 1][t], chi = S.a[r + 1][t];
+                if (chi > clo) {
+                    EltArgs E;
+                    E.dx = A.dx; E.act = A.act; E.gate = tin.relu;
+                    E.dy = View{R.ws + tin.carry_off, clo, chi - clo, tin.H, tin.W, tin.Cp,
+                                (long long)tin.carry_cap * tin.W * tin.Cp};
+                    E.a = clo; E.b = chi; E.B = B;
+                    ++P.launches;
+                    ProfScope ps(R, 2, 0, i * 8 + 7);
+                    CK(simt_acc_gate(R.prec, E, R.st));
+                }
+            }
         }
         if (o.d.res >= 0) {
             const TensorInfo &tr = P.t[o.d.res];
@@ -435,7 +465,7 @@ static lrcnn_status run_backward(Run &R) {
             if (recompute && (st = band_forward(R, S, r, false, true)) != LRCNN_OK) return st;
             // band delta buffers: zero, then the carry of band r+1 (R6)
             for (int t : S.tensors) {
-                if (t == S.out_t) continue;
+                if (t == S.out_t || delta_overwrite(P, S, t)) continue;   // overwritten by its dgrad
                 const TensorInfo &ti = P.t[t];
                 size_t rb = (size_t)ti.W * ti.Cp * R.E;
                 int rows = S.b[r][t] - S.lo[r][t];

@@ -37,6 +37,7 @@ struct DgradArgs {
     int k, s, p, c_out;
     int ra, rb;                // input rows to produce
     int B;
+    int write = 0;             // 1: delta_in rows [ra, rb) = gate(act) * acc, not accumulated (single writer)
 };
 
 struct WgradArgs {

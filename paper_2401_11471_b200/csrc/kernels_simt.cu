@@ -135,7 +135,7 @@ __global__ void k_conv_dgrad(DgradArgs A) {
         }
         (void)Cpo;
         T *dx = (T *)A.dx.p + voff(A.dx, b, g, xi) + ci;
-        float v = ldf(dx) + acc;
+        float v = (A.write ? 0.f : ldf(dx)) + acc;
         if (A.gate && ldf((const T *)A.act.p + voff(A.act, b, g, xi) + ci) <= 0.f) v = 0.f;
         stf(dx, v);
     }
