@@ -306,7 +306,11 @@ static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
     const TensorInfo &ti = P.t[t];
     if (ti.cons.size() != 1 || ti.cons[0].role != 0) return false;
     const OpInfo &u = P.op[ti.cons[0].op];
-    return u.d.kind == LRCNN_OP_CONV && u.d.s == 1;
+    if (u.d.kind == LRCNN_OP_CONV) return u.d.s == 1;
+    // a non-overlapping max-pool that tiles the map exactly writes every input position once
+    const TensorInfo &to = P.t[u.out_t];
+    return u.d.kind == LRCNN_OP_MAXPOOL && u.d.k == u.d.s && u.d.p == 0 && to.H * u.d.k == ti.H &&
+           to.W * u.d.k == ti.W;
 }
 
 static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
