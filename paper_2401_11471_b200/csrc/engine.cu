@@ -283,8 +283,32 @@ static lrcnn_status exchange(Run &R, const Segment &S, const View &v, bool bp) {
     return LRCNN_OK;
 }
 
+// transposed weights for the tensor-core dgrad (gamma folded in), on stream st
+static lrcnn_status launch_transposes(Run &R, cudaStream_t st) {
+    Plan &P = R.P;
+    for (const OpInfo &o : P.op) {
+        if (o.d.kind != LRCNN_OP_CONV || o.in_t == 0) continue;
+        CK(transpose_weights(R.prec, prm(R, o.w_off), o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr,
+                             R.ws + o.wt_off, o.d.c_out, P.t[o.out_t].Cp, o.d.k, P.t[o.in_t].Cp, st));
+        ++P.launches;
+    }
+    return LRCNN_OK;
+}
+
 static lrcnn_status run_forward(Run &R) {
     lrcnn_status st;
+    {   // the dgrad weight transposes depend only on this step's weights: overlap them with the FP
+        Plan &P = R.P;
+        P.wt_pending = false;
+        if (P.use_tc && P.side_stream && P.ev_wt && !P.profiling) {
+            cudaStream_t ss = (cudaStream_t)P.side_stream;
+            CK(cudaEventRecord((cudaEvent_t)P.ev_fork, R.st));
+            CK(cudaStreamWaitEvent(ss, (cudaEvent_t)P.ev_fork, 0));
+            if ((st = launch_transposes(R, ss)) != LRCNN_OK) return st;
+            CK(cudaEventRecord((cudaEvent_t)P.ev_wt, ss));
+            P.wt_pending = true;
+        }
+    }
     const bool sharded = R.P.opts.world > 1;
     for (const Segment &S : R.P.seg) {
         if (sharded && S.in_t != 0 && !S.in_xfers.empty())
@@ -445,17 +469,18 @@ static lrcnn_status run_backward(Run &R) {
             CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
             P.side_stream = ss; P.ev_fork = e0; P.ev_join = e1;
+            cudaEvent_t e2;
+            CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+            P.ev_wt = e2;
         }
         R.side = (cudaStream_t)P.side_stream;
     }
-    // transposed weights for the tensor-core dgrad (gamma folded in)
-    if (P.use_tc) {
-        for (const OpInfo &o : P.op) {
-            if (o.d.kind != LRCNN_OP_CONV || o.in_t == 0) continue;
-            CK(transpose_weights(R.prec, prm(R, o.w_off), o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr,
-                                 R.ws + o.wt_off, o.d.c_out, P.t[o.out_t].Cp, o.d.k, P.t[o.in_t].Cp, R.st));
-            ++P.launches;
-        }
+    // transposed weights for the tensor-core dgrad: launched on the side stream during the FP, or here
+    if (P.wt_pending) {
+        CK(cudaStreamWaitEvent(R.st, (cudaEvent_t)P.ev_wt, 0));
+        P.wt_pending = false;
+    } else if (P.use_tc) {
+        if ((st = launch_transposes(R, R.st)) != LRCNN_OK) return st;
     }
     for (int s = (int)P.seg.size() - 1; s >= 0; --s) {
         const Segment &S = P.seg[s];
@@ -592,6 +617,7 @@ lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
             cudaStreamDestroy((cudaStream_t)plan->P.side_stream);
             cudaEventDestroy((cudaEvent_t)plan->P.ev_fork);
             cudaEventDestroy((cudaEvent_t)plan->P.ev_join);
+            if (plan->P.ev_wt) cudaEventDestroy((cudaEvent_t)plan->P.ev_wt);
         }
         for (int c = 0; c < 3; ++c)
             for (auto &e : plan->P.pending_events[c]) {

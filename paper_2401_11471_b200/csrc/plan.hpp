@@ -101,6 +101,8 @@ struct Plan {
     long long launches = 0, tc_launches = 0;
     bool profiling = false;
     ProfileSlot prof[3];
+    void *ev_wt = nullptr;                   // transposed dgrad weights written (side stream, during FP)
+    bool wt_pending = false;                 // FP launched the transposes; BP waits on ev_wt
     std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t
     std::vector<double> pending_flops[3];
     std::vector<int> pending_tags[3];             // op*8 + kind (profile dump)
