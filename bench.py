@@ -366,36 +366,48 @@ def main():
     peaks, peak_src = measured_peaks()
     achieved = tc_fl / (tc_ms / 1000.0) / 1e12 if tc_ms > 0 else 0.0
     peak_tf = peaks.get("bf16_tflops_sustained", 1385.7)
+    prof_steps = max(2, min(a.steps, 5))
+    hbm_gbs = peaks.get("hbm_gbs", 6550.0)
+    ridge = peak_tf * 1e12 / (hbm_gbs * 1e9)          # FLOP/B where the two rooflines meet
+    # each kernel against the roofline its algorithmic intensity puts it under:
+    # tensor-bound: algorithmic conv FLOPs / time vs the bf16 tensor peak; HBM-bound: algorithmic
+    # bytes (every operand read once, every result written once) / time vs the measured copy bandwidth
+    def _rl(k):
+        sec = k["ms"] / 1000.0
+        if sec <= 0:
+            return {"bound": "tensor", "achieved": 0.0, "peak": peak_tf, "unit": "TFLOP/s", "frac": 0.0}
+        if k.get("bytes", 0) > 0 and k["flops"] / k["bytes"] < ridge:
+            gbs = k["bytes"] / sec / 1e9
+            return {"bound": "hbm", "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs}
+        tf = k["flops"] / sec / 1e12
+        return {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": tf / peak_tf}
+    # the dominant kernel: the tcgen05 kernel with the largest share of the step (CUDA events around
+    # each of its launches on the launching stream)
+    kern = [dict(k, name=demangle(k["name"])) for k in kern]
+    dom = max(kern, key=lambda k: k["ms"]) if kern else None
     traffic = None
     try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        for name, b in tj.get("per_kernel", {}).items():
-            if kern and name == max(kern, key=lambda k: k["ms"])["name"]:
-                traffic = b
+            traffic = json.load(f).get("per_kernel", {}).get(dom["name"]) if dom else None
     except Exception:
         pass
-    prof_steps = max(2, min(a.steps, 5))
-    # the dominant kernel: the tcgen05 kernel with the largest share of the step (CUDA events around
-    # each of its launches); its achieved = algorithmic conv FLOPs of its launches / their time
-    kern = [dict(k, name=demangle(k["name"])) for k in kern]
-    dom = max(kern, key=lambda k: k["ms"]) if kern else None
-    def _tf(k):
-        return k["flops"] / (k["ms"] / 1000.0) / 1e12 if k["ms"] > 0 else 0.0
-    dom_tf = _tf(dom) if dom else 0.0
-    roofline = {"bound": "tensor", "kernel": dom["name"] if dom else None, "achieved": dom_tf,
-                "peak": peak_tf, "unit": "TFLOP/s", "frac": dom_tf / peak_tf if peak_tf else None,
-                "traffic": traffic, "peak_source": "%s bf16_tflops_sustained" % peak_src,
-                "launches_per_step": dom["launches"] / prof_steps if dom else 0,
-                "ms_per_step": dom["ms"] / prof_steps if dom else 0,
-                "share_of_step": (dom["ms"] / prof_steps) / ms_step if dom else 0,
-                "all_conv_fp_dgrad": {"achieved": achieved, "frac": achieved / peak_tf if peak_tf else None,
-                                      "launches_per_step": tc_n / prof_steps, "ms_per_step": tc_ms / prof_steps},
-                "wgrad": {"achieved": wg_fl / (wg_ms / 1000.0) / 1e12 if wg_ms else 0.0, "ms_per_step": wg_ms / prof_steps},
-                "other_ms_per_step": ot_ms / prof_steps,
-                "kernels": sorted([{"name": k["name"], "ms_per_step": k["ms"] / prof_steps,
-                                    "achieved": _tf(k), "frac": _tf(k) / peak_tf if peak_tf else None}
-                                   for k in kern], key=lambda k: -k["ms_per_step"])[:8]}
+    drl = _rl(dom) if dom else _rl({"ms": 0, "flops": 0})
+    roofline = dict(drl, kernel=dom["name"] if dom else None, traffic=traffic,
+                    algorithmic_bytes_per_launch=dom["bytes"] / dom["launches"] if dom and dom["launches"] else None,
+                    peak_source="%s %s" % (peak_src, "bf16_tflops_sustained" if drl["bound"] == "tensor" else "hbm_gbs"),
+                    ridge_flop_per_byte=ridge,
+                    launches_per_step=dom["launches"] / prof_steps if dom else 0,
+                    ms_per_step=dom["ms"] / prof_steps if dom else 0,
+                    share_of_step=(dom["ms"] / prof_steps) / ms_step if dom else 0,
+                    all_conv_fp_dgrad={"achieved": achieved, "unit": "TFLOP/s",
+                                       "frac": achieved / peak_tf if peak_tf else None,
+                                       "launches_per_step": tc_n / prof_steps, "ms_per_step": tc_ms / prof_steps},
+                    wgrad={"achieved": wg_fl / (wg_ms / 1000.0) / 1e12 if wg_ms else 0.0, "unit": "TFLOP/s",
+                           "ms_per_step": wg_ms / prof_steps},
+                    other_ms_per_step=ot_ms / prof_steps,
+                    kernels=sorted([dict(_rl(k), name=k["name"], ms_per_step=k["ms"] / prof_steps,
+                                         tflops=k["flops"] / (k["ms"] / 1000.0) / 1e12 if k["ms"] > 0 else 0.0)
+                                    for k in kern], key=lambda k: -k["ms_per_step"])[:10])
 
     # ---------------------------------------------------------------- memory vs layer-wise (COLUMN)
     mem_rep = {"peak_allocated_bytes": peak, "xi_bytes": xi, "feature_map_bytes": peak - xi,

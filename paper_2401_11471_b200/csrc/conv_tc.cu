@@ -133,15 +133,16 @@ static constexpr int kThreads = 192;
 static constexpr int kConvThreads = 320;      // k_conv_tc: producer, MMA, 8 epilogue warps
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
-static constexpr int kStageBudget = 192 * 1024;
 static constexpr int kOutStage = 128 * 128;       // epilogue staging: 128 pixels x 64 channels bf16
 template <int BN, int KC = 64>
 struct ConvCfg {
     static constexpr int kA = 128 * KC * 2, kB = BN * KC * 2;
     static constexpr int kStageBytes = kA + kB;
     // BN <= 128: two (delta, activation) staging pairs (double-buffered dgrad epilogue)
-    static constexpr int kOutBufs = BN <= 128 ? 4 : 2;
-    static constexpr int kBudget = BN <= 128 ? 232448 - kOutBufs * kOutStage - 2048 : kStageBudget;
+    // four 16 KB staging buffers: FP stores / residual loads run up to three 64-channel groups
+    // ahead; dgrad: two (delta, activation) pairs (double-buffered epilogue)
+    static constexpr int kOutBufs = 4;
+    static constexpr int kBudget = 232448 - kOutBufs * kOutStage - 2048;
     static constexpr int kStages = kBudget / kStageBytes > 16 ? 16 : kBudget / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + kOutBufs * kOutStage + 1024 + 512;
     static constexpr uint32_t kTmemCols = 2 * BN;
@@ -265,21 +266,30 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
     const float lo = P.relu ? 0.f : -INFINITY;
     const int my = (m >> P.tw_log2) & ((1 << P.th_log2) - 1), mx = m & ((1 << P.tw_log2) - 1);
     const int mb = P.NBt > 1 ? m >> (P.tw_log2 + P.th_log2) : 0;   // image within a batch-folded tile
-    // residual through TMA: the tile of group g is loaded into the staging buffer the group's
-    // output will use (issued one group ahead, tracked by rbar); each thread adds its row
+    // residual through TMA: group q (64 channels of one tile, counted across this CTA's tiles) uses
+    // staging buffer q % NB; its residual tile is TMA-loaded into that buffer NB-1 groups ahead
+    // (barrier rbar[q % NB]), the output overwrites it in place and is TMA-stored from it.  Without
+    // a residual the NB buffers rotate with NB-1 stores in flight.
     const bool rt = P.has_res && P.tma_res && tmR;
-    uint32_t rphase = 0;
-    auto res_load = [&](int tile2, int grp2, int buf2) {
+    auto ngrp = [&](int tile2) {
         int nt2, tx2, ty2, b2;
         P.decode(tile2, nt2, tx2, ty2, b2);
-        bulk_wait_read1();                       // the store that last used buf2 has read it
-        ptx::mbar_arrive_expect_tx(rbar, kOutStage);
-        ptx::tma_load_4d(stage_out + buf2 * kOutStage, tmR, rbar, nt2 * BN + grp2 * 64, tx2 * P.TW,
-                         P.out_a + ty2 * P.TH - P.res.base, b2);
+        const int left = P.n_out - nt2 * BN;
+        return left >= BN ? BN / 64 : (left + 63) / 64;
     };
-    if (rt && leader && (int)blockIdx.x < num_tiles) res_load(blockIdx.x, 0, 0);
+    int lt = blockIdx.x, lg = 0;   // leader: next residual group to load
+    auto res_load = [&](int buf2) {
+        int nt2, tx2, ty2, b2;
+        P.decode(lt, nt2, tx2, ty2, b2);
+        ptx::mbar_arrive_expect_tx(rbar + buf2, kOutStage);
+        ptx::tma_load_4d(stage_out + buf2 * kOutStage, tmR, rbar + buf2, nt2 * BN + lg * 64, tx2 * P.TW,
+                         P.out_a + ty2 * P.TH - P.res.base, b2);
+        if (++lg == ngrp(lt)) { lg = 0; lt += gridDim.x; }
+    };
+    if (rt && leader)
+        for (int i = 0; i < NB - 1 && lt < num_tiles; ++i) res_load(i);
     int acc = 0, sbuf = 0;
-    uint32_t aphase = 0;
+    uint32_t aphase = 0, rphases = 0;   // bit i: parity of the next completion of rbar[i]
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int nt, tx, ty, b;
         P.decode(tile, nt, tx, ty, b);
@@ -317,8 +327,8 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             const uint32_t buf = ptx::smem_u32(stage_out + sbuf * kOutStage + m * 128);
             const int chunk0 = hh * (CH / 8);
             if (rt) {
-                ptx::mbar_wait(rbar, rphase);          // residual tile of this group in buf
-                rphase ^= 1;
+                ptx::mbar_wait(rbar + sbuf, (rphases >> sbuf) & 1);   // residual tile of this group in buf
+                rphases ^= 1u << sbuf;
 #pragma unroll
                 for (int c = 0; c < CH / 8; ++c) pr[c] = ld_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4));
                 epi_bar_n<NE>();                       // every thread has read its residual row
@@ -359,11 +369,11 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                 tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
                 bulk_commit();
             }
-            if (rt && leader) {   // prefetch the next group's residual into the other buffer
-                if (grp + 1 < BN / 64 && nb + 64 < P.n_out) res_load(tile, grp + 1, sbuf ^ 1);
-                else if (tile + (int)gridDim.x < num_tiles) res_load(tile + gridDim.x, 0, sbuf ^ 1);
+            if (rt && leader && lt < num_tiles) {   // residual NB-1 groups ahead, into the buffer group q-1 used
+                bulk_wait_read1();                     // ... once that group's store has read it
+                res_load(sbuf == 0 ? NB - 1 : sbuf - 1);
             }
-            sbuf = rt ? sbuf ^ 1 : (sbuf + 1 == NB ? 0 : sbuf + 1);
+            sbuf = sbuf + 1 == NB ? 0 : sbuf + 1;
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -657,14 +667,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
     uint64_t *ebar = tempty + 2;                     // 2 dgrad staging barriers
-    uint32_t *tslot = (uint32_t *)(ebar + 2);
+    uint32_t *tslot = (uint32_t *)(ebar + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
-        ptx::mbar_init(ebar, 1);
-        ptx::mbar_init(ebar + 1, 1);
+        for (int i = 0; i < 4; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -726,7 +735,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
         }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
         else if (P.tma_dg && Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
@@ -754,7 +763,7 @@ template <int BN>
 struct Conv2Cfg {
     static constexpr int kA = 128 * 128, kBh = (BN / 2) * 128;
     static constexpr int kStageBytes = kA + kBh;
-    static constexpr int kOutBufs = BN <= 128 ? 4 : 2;
+    static constexpr int kOutBufs = 4;
     static constexpr int kAvail = 232448 - kOutBufs * kOutStage - 2048;
     static constexpr int kStages = kAvail / kStageBytes > 10 ? 10 : kAvail / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + kOutBufs * kOutStage + 1024 + 512;
@@ -777,15 +786,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
     uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 2);
+    uint32_t *tslot = (uint32_t *)(ebar + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 16); }
-        ptx::mbar_init(ebar, 1);
-        ptx::mbar_init(ebar + 1, 1);
+        for (int i = 0; i < 4; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -855,7 +863,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
             }
         }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
         else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
     }
@@ -1337,7 +1345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
     uint64_t *tfull = emptyB + SB;
     uint64_t *tempty = tfull + 2;
     uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 2);
+    uint32_t *tslot = (uint32_t *)(ebar + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -1345,8 +1353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
         for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
         for (int i = 0; i < SB; ++i) { ptx::mbar_init(fullB + i, 1); ptx::mbar_init(emptyB + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 16); }
-        ptx::mbar_init(ebar, 1);
-        ptx::mbar_init(ebar + 1, 1);
+        for (int i = 0; i < 4; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -1433,7 +1440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
             }
         }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN, 8>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
         else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
     }

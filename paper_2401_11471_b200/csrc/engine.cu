@@ -130,8 +130,9 @@ struct ProfScope {
     int cls;
     double flops;
     int tag;
+    double bytes;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    ProfScope(Run &r, int c, double f, int t = -1) : R(r), cls(c), flops(f), tag(t) {
+    ProfScope(Run &r, int c, double f, int t = -1, double by = 0) : R(r), cls(c), flops(f), tag(t), bytes(by) {
         if (R.P.profiling) {
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
@@ -144,6 +145,7 @@ struct ProfScope {
             cudaEventRecord(e1, R.st);
             R.P.pending_events[cls].push_back({(void *)e0, (void *)e1});
             R.P.pending_flops[cls].push_back(flops);
+            R.P.pending_bytes[cls].push_back(bytes);
             R.P.pending_tags[cls].push_back(tag);
             const char *k = tc_last_kernel();
             R.P.pending_names[cls].push_back(k ? k : "");
@@ -153,6 +155,22 @@ struct ProfScope {
 
 static double conv_flops(Plan &P, const OpInfo &o, int rows) {
     return 2.0 * o.d.k * o.d.k * P.net.B * P.t[o.in_t].C * P.t[o.out_t].C * (double)rows * P.t[o.out_t].W;
+}
+
+// Algorithmic HBM bytes of one conv launch over output rows [a, b): every operand
+// read once, every result written once.  kind 0 FP: input rows [a*s-p, (b-1)*s-p+k) clipped + weights
+// + output (+ residual); kind 1 dgrad: dy + weights + dx and the gating activation (+ dx read when
+// it accumulates); kind 2 wgrad: dy + input rows + the fp32 gradient read-modify-write.
+static double conv_bytes(Plan &P, const OpInfo &o, int a, int b, int kind, int dx_accum = 0, int gate = 0) {
+    const TensorInfo &ti = P.t[o.in_t], &to = P.t[o.out_t];
+    const double E = P.opts.prec == LRCNN_FP32 ? 4.0 : 2.0, B = P.net.B;
+    const int ra = std::max(0, a * o.d.s - o.d.p), rb = std::min(ti.H, (b - 1) * o.d.s - o.d.p + o.d.k);
+    const double in = B * (double)(rb - ra) * ti.W * ti.Cp * E;
+    const double out = B * (double)(b - a) * to.W * to.Cp * E;
+    const double w = (double)o.d.k * o.d.k * ti.Cp * o.d.c_out;
+    if (kind == 0) return in + out + w * E + (o.d.res >= 0 ? out : 0.0);
+    if (kind == 1) return out + w * E + in * (1.0 + gate + dx_accum);
+    return out + in + w * 8.0;
 }
 
 // ------------------------------------------------------------------ op forward on band rows [a, b)
@@ -173,7 +191,7 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
         A.beta = o.beta_cnt ? prm(R, o.beta_off) : nullptr;
         A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.epi = o.d.epi; A.relu = o.d.relu;
         A.a = a; A.b_ = b; A.B = P.net.B;
-        ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 0);
+        ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 0, conv_bytes(P, o, a, b, 0));
         ++P.launches;
         if (P.use_tc && tc_conv_fwd(A, R.st)) { ++P.tc_launches; CK(cudaGetLastError()); return LRCNN_OK; }
         CK(simt_conv_fwd(R.prec, A, R.st));
@@ -333,8 +351,11 @@ static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
     if (u.d.kind == LRCNN_OP_CONV) return u.d.s == 1;
     // a non-overlapping max-pool that tiles the map exactly writes every input position once
     const TensorInfo &to = P.t[u.out_t];
-    return u.d.kind == LRCNN_OP_MAXPOOL && u.d.k == u.d.s && u.d.p == 0 && to.H * u.d.k == ti.H &&
-           to.W * u.d.k == ti.W;
+    if (u.d.kind != LRCNN_OP_MAXPOOL) return false;
+    if (u.d.k == u.d.s && u.d.p == 0 && to.H * u.d.k == ti.H && to.W * u.d.k == ti.W) return true;
+    // an overlapping max-pool backward in its tiled-gather form writes every input row it covers
+    // (all columns); the last window must reach the last row so the final band is covered too
+    return pool_tiled_shape(u.d.k, u.d.s, ti.Cp) && (to.H - 1) * u.d.s - u.d.p + u.d.k >= ti.H;
 }
 
 static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
@@ -364,7 +385,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
             if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
             ++P.launches;
-            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2);
+            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2, conv_bytes(P, o, a, b, 2));
             if (P.use_tc && tc_conv_wgrad(A, gst)) ++P.tc_launches;
             else CK(simt_conv_wgrad(R.prec, A, gst));
             CK(cudaGetLastError());
@@ -394,7 +415,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
             {
                 ++P.launches;
-                ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1);
+                ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0));
                 if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
                 else CK(simt_conv_dgrad(R.prec, A, R.st));
                 CK(cudaGetLastError());
@@ -436,10 +457,24 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             // consumer and no delta carried in from band r+1 is the only writer of those rows
             const int N = (int)S.E.size();
             const bool carry_in = P.opts.mode == LRCNN_2PS && r + 1 < N && S.lo[r + 1][o.in_t] < S.a[r + 1][o.in_t];
-            A.acc = !(o.d.k == o.d.s && o.d.p == 0 && o.in_t != S.in_t && tin.cons.size() == 1 && !carry_in);
-            P.launches += simt_pool_bwd_launches(A);
-            ProfScope ps(R, 2, 0, i * 8 + 5);
-            CK(simt_pool_bwd(R.prec, A, R.st));
+            const bool single = delta_overwrite(P, S, o.in_t);
+            A.acc = !(single || (o.d.k == o.d.s && o.d.p == 0 && o.in_t != S.in_t && tin.cons.size() == 1 && !carry_in));
+            {
+                P.launches += simt_pool_bwd_launches(A);
+                ProfScope ps(R, 2, 0, i * 8 + 5);
+                CK(simt_pool_bwd(R.prec, A, R.st));
+            }
+            if (single && carry_in) {   // + the carry of band r+1, gated (as after a single-writer dgrad)
+                const int t = o.in_t, clo = S.lo[r + 1][t], chi = S.a[r + 1][t];
+                EltArgs E;
+                E.dx = A.dx; E.act = A.act; E.gate = tin.relu;
+                E.dy = View{R.ws + tin.carry_off, clo, chi - clo, tin.H, tin.W, tin.Cp,
+                            (long long)tin.carry_cap * tin.W * tin.Cp};
+                E.a = clo; E.b = chi; E.B = B;
+                ++P.launches;
+                ProfScope ps(R, 2, 0, i * 8 + 7);
+                CK(simt_acc_gate(R.prec, E, R.st));
+            }
         }
     } else {
         for (int which = 0; which < 2; ++which) {
@@ -896,6 +931,7 @@ lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan) {
         }
         plan->P.pending_events[c].clear();
         plan->P.pending_flops[c].clear();
+        plan->P.pending_bytes[c].clear();
         plan->P.pending_tags[c].clear();
         plan->P.pending_names[c].clear();
         plan->P.per_kernel[c].clear();
@@ -925,6 +961,7 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
                 if (it == P.per_kernel[c].end()) { P.per_kernel[c].push_back({nm, ProfileSlot()}); it = P.per_kernel[c].end() - 1; }
                 it->second.ms += t;
                 it->second.flops += P.pending_flops[c][i];
+                it->second.bytes += P.pending_bytes[c][i];
                 it->second.launches += 1;
             }
             const int tag = P.pending_tags[c][i];
@@ -941,6 +978,7 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
         }
         P.pending_events[c].clear();
         P.pending_flops[c].clear();
+        P.pending_bytes[c].clear();
         P.pending_tags[c].clear();
         P.pending_names[c].clear();
     }
@@ -957,8 +995,8 @@ lrcnn_status lrcnn_profile_kernels(lrcnn_plan_t *plan, int cls, char *buf, size_
     std::string out;
     char line[512];
     for (auto &e : plan->P.per_kernel[cls]) {
-        snprintf(line, sizeof line, "%s,%lld,%.6f,%.6e\n", e.first.empty() ? "simt" : e.first.c_str(),
-                 e.second.launches, e.second.ms, e.second.flops);
+        snprintf(line, sizeof line, "%s,%lld,%.6f,%.6e,%.6e\n", e.first.empty() ? "simt" : e.first.c_str(),
+                 e.second.launches, e.second.ms, e.second.flops, e.second.bytes);
         out += line;
     }
     if (out.size() + 1 > len) return fail(LRCNN_E_ARG, "buffer too small");

@@ -82,6 +82,7 @@ cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st);
 cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st);
 cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st);
 int simt_pool_bwd_launches(const PoolArgs &a);   // kernels simt_pool_bwd enqueues
+bool pool_tiled_shape(int k, int s, int Cp);      // overlapping max-pool backward as a tiled gather (single writer)
 cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st);
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st);
 

@@ -709,54 +709,222 @@ __global__ void k_pool_bwd8(PoolArgs A) {
     }
 }
 
-// Overlapping max-pool backward (s < k <= 2s, e.g. ResNet's 3x3/s2/p1) as a scatter in 4 parity
-// phases: output pixels (y, x) with y = py, x = px (mod 2) have disjoint windows, so each phase
-// recomputes every window's argmax once and adds dy into dx at the argmax (gate-on-write) without
-// write conflicts.  Traffic per output pixel: k*k input vectors + the dy vector + one dx RMW per
-// distinct argmax position (the gather form re-reads every window once per input pixel in it).
+// Overlapping max-pool backward (s < k <= 2s, e.g. ResNet's 3x3/s2/p1) as a tiled gather.  A CTA
+// owns kPoolTR x kPoolTC input pixels (all channel vectors) of one image.  Phase 1 computes, once,
+// the argmax code and dy of every pooling window that touches them (output rows limited to the
+// band rows [a, b) whose dy is present) into shared memory; phase 2 gives every owned input pixel
+// the sum of dy over the windows whose argmax it is, applies the gate (act > 0) and stores dx once
+// (A.acc: dx += ..., else dx is written, single writer).  HBM traffic ~ act read once (+ window
+// halo, L1/L2 hits), dy once, dx written once: the scatter form paid a memset, 2.25 window reads
+// and a read-modify-write of dx per window position.
+constexpr int kPoolTR = 8, kPoolTC = 32;
+static inline int pool_tile_rows(int t, int k, int s) { return (t + k - 2) / s + 1; }   // windows per tile edge
+
 template <typename T>
-__global__ void k_pool_bwd_scatter8(PoolArgs A, int py, int px) {
+__global__ void __launch_bounds__(256) k_pool_bwd_tile8(PoolArgs A, int ny_max, int nx_max) {
     griddep_wait();   // PDL: previous kernel complete and visible
     griddep_launch();
-    const int CV = A.dy.Cp / 8, Wo = A.dy.W, rows = A.b - A.a;
-    const int wx = (Wo - px + 1) / 2;                      // output columns of this parity
-    const int y0 = A.a + ((py - A.a) % 2 + 2) % 2;         // first band row of this parity
-    const int ry = y0 < A.b ? (A.b - y0 + 1) / 2 : 0;
-    const long long n = (long long)A.B * ry * wx * CV;
-    (void)rows;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int cv = (int)(idx % CV);
-        long long r = idx / CV;
-        const int x = px + 2 * (int)(r % wx); r /= wx;
-        const int y = y0 + 2 * (int)(r % ry);
-        const int b = (int)(r / ry);
-        float best[8], d[8];
-        int arg[8];
-        pool_window8<T>(A.act, b, y, x, cv * 8, A.k, A.s, A.p, best, arg);
-        ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
-        for (int ky = 0; ky < A.k; ++ky) {
-            const int g = y * A.s - A.p + ky;
-            if (!vhas(A.dx, g)) continue;
-            for (int kx = 0; kx < A.k; ++kx) {
-                const int xi = x * A.s - A.p + kx;
-                if (xi < 0 || xi >= A.dx.W) continue;
-                const int code = ky * A.k + kx;
-                bool any = false;
+    extern __shared__ float pool_smem[];
+    const int CV = A.dy.Cp / 8, Wo = A.dy.W, Wi = A.dx.W;
+    const int k = A.k, s = A.s, p = A.p;
+    const int b = blockIdx.z;
+    const int g0 = A.ra + blockIdx.y * kPoolTR, g1 = min(g0 + kPoolTR, A.rb);
+    const int x0 = blockIdx.x * kPoolTC, x1 = min(x0 + kPoolTC, Wi);
+    // windows touching rows [g0, g1): y*s - p <= g1-1 and y*s - p + k - 1 >= g0
+    auto first_win = [&](int g) { int lo = g + p - k + 1; return lo <= 0 ? 0 : (lo + s - 1) / s; };
+    const int ylo = max(first_win(g0), A.a), yhi = min((g1 - 1 + p) / s, A.b - 1);
+    const int xlo = first_win(x0), xhi = min((x1 - 1 + p) / s, Wo - 1);
+    const int ny = yhi - ylo + 1, nx = xhi - xlo + 1;
+    // per window slot: dy as 8 raw T (one 16-byte vector for bf16: conflict-free LDS.128 across the
+    // warp's consecutive channel vectors) and the 8 argmax codes as int8 in one 8-byte word
+    T *sdy = (T *)pool_smem;                                                   // [ny_max*nx_max*CV][8]
+    uint2 *scode = (uint2 *)(sdy + (size_t)ny_max * nx_max * CV * 8);
+    if (ny > 0 && nx > 0) {
+        const int items = ny * nx * CV;
+        for (int i = threadIdx.x; i < items; i += blockDim.x) {
+            const int cv = i % CV, pix = i / CV;
+            const int oy = ylo + pix / nx, ox = xlo + pix % nx;
+            float best[8], d[8];
+            int arg[8];
+            pool_window8<T>(A.act, b, oy, ox, cv * 8, k, s, p, best, arg);
+            ld8((const T *)A.dy.p + voff(A.dy, b, oy, ox) + cv * 8, d);
+            const int slot = ((pix / nx) * nx_max + pix % nx) * CV + cv;
+            st8(sdy + (size_t)slot * 8, d);
+            uint2 c;
+            c.x = c.y = 0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) any |= arg[j] == code;
-                if (!any) continue;
-                T *dp = (T *)A.dx.p + voff(A.dx, b, g, xi) + cv * 8;
-                float o[8];
-                ld8(dp, o);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (arg[j] != code) continue;
-                    o[j] += d[j];
-                    if (A.gate && !(best[j] > 0.f)) o[j] = 0.f;    // best = act at the argmax
-                }
-                st8(dp, o);
+            for (int j = 0; j < 4; ++j) {
+                c.x |= (uint32_t)(arg[j] & 0xff) << (8 * j);
+                c.y |= (uint32_t)(arg[j + 4] & 0xff) << (8 * j);
             }
+            scode[slot] = c;
+        }
+    }
+    __syncthreads();
+    const int tw = x1 - x0, owned = (g1 - g0) * tw * CV;
+    for (int i = threadIdx.x; i < owned; i += blockDim.x) {
+        const int cv = i % CV, pix = i / CV;
+        const int g = g0 + pix / tw, xi = x0 + pix % tw;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int ya = max(first_win(g), ylo), yb = min((g + p) / s, yhi);
+        const int xa = max(first_win(xi), xlo), xb = min((xi + p) / s, xhi);
+        for (int y = ya; y <= yb; ++y)
+            for (int x = xa; x <= xb; ++x) {
+                const uint32_t code = (uint32_t)((g - (y * s - p)) * k + (xi - (x * s - p)));
+                const int slot = ((y - ylo) * nx_max + (x - xlo)) * CV + cv;
+                const uint2 c = scode[slot];
+                const uint32_t rep = code * 0x01010101u;
+                // bytes of c equal to code (per-byte compare via __vcmpeq4: 0xff where equal)
+                const uint32_t m0 = __vcmpeq4(c.x, rep), m1 = __vcmpeq4(c.y, rep);
+                if ((m0 | m1) == 0) continue;
+                float d[8];
+                ld8(sdy + (size_t)slot * 8, d);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (((j < 4 ? m0 : m1) >> (8 * (j & 3))) & 1) acc[j] += d[j];
+            }
+        T *dp = (T *)A.dx.p + voff(A.dx, b, g, xi) + cv * 8;
+        float o[8], a[8];
+        if (A.acc) {
+            ld8(dp, o);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] += acc[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = acc[j];
+        }
+        if (A.gate) {
+            ld8((const T *)A.act.p + voff(A.act, b, g, xi) + cv * 8, a);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (!(a[j] > 0.f)) o[j] = 0.f;
+        }
+        st8(dp, o);
+    }
+}
+
+// ResNet's 3x3 / stride 2 / pad 1 max-pool backward, bf16: the tiled gather above with the
+// window geometry fixed.  Input column pair (2x', 2x'+1) lies in windows x' (kx = 1, 2) and
+// x'+1 (kx = 0); input row g lies in window g/2 (ky = 1) if even, else (g-1)/2 (ky = 2) and
+// (g+1)/2 (ky = 0).  Phase 1 computes each window's max and first-in-raster argmax with packed
+// bf16x2 compares (set.gt / max / lop3: 3 instructions per channel pair and position) and keeps
+// 16-bit codes + dy in shared memory (invalid windows: code 0xffff); phase 2 gives a thread one
+// input row x column pair x 8 channels and masks dy with packed compares (vcmpeq2), no branches
+// on window validity.  A warp covers one input row, so the row-parity branch is warp-uniform.
+constexpr int kP3TR = 8, kP3TP = 16;   // input rows x column pairs per CTA
+__device__ __forceinline__ uint32_t bf2_gt_mask(uint32_t a, uint32_t b) {
+    uint32_t m;
+    asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(a), "r"(b));
+    return m;
+}
+__device__ __forceinline__ uint32_t bf2_max(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ void acc_masked(float (&acc)[8], const uint4 &d, const uint4 &c, uint32_t code2) {
+    const uint32_t dw[4] = {d.x, d.y, d.z, d.w}, cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const uint32_t u = dw[h] & __vcmpeq2(cw[h], code2);
+        acc[2 * h] += __uint_as_float(u << 16);
+        acc[2 * h + 1] += __uint_as_float(u & 0xffff0000u);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pool3s2_bwd(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
+    extern __shared__ uint4 p3_smem[];
+    const int CV = A.dy.Cp / 8, Wo = A.dy.W, Wi = A.dx.W;
+    const int b = blockIdx.z;
+    const int g0 = A.ra + blockIdx.y * kP3TR, g1 = min(g0 + kP3TR, A.rb);
+    const int xp0 = blockIdx.x * kP3TP;
+    // windows of this tile: rows [wy0, wy0 + NY), columns [xp0, xp0 + NX)
+    const int wy0 = g0 >> 1, NY = ((g1 - 1 + 1) >> 1) - wy0 + 1, NX = kP3TP + 1;
+    uint4 *scode = p3_smem, *sdy = p3_smem + (kP3TR / 2 + 2) * NX * CV;
+    const int items = NY * NX * CV;
+    for (int i = threadIdx.x; i < items; i += blockDim.x) {
+        const int cv = i % CV, pix = i / CV;
+        const int y = wy0 + pix / NX, x = xp0 + pix % NX;
+        uint4 code = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu), dyv = make_uint4(0, 0, 0, 0);
+        if (y >= A.a && y < A.b && x < Wo) {
+            uint32_t best[4] = {0, 0, 0, 0}, cw[4] = {0, 0, 0, 0};
+            bool have = false;
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                const int g = 2 * y - 1 + ky;
+                if (!vhas(A.act, g)) continue;
+                const bf16 *row = (const bf16 *)A.act.p + voff(A.act, b, g, 0) + cv * 8;
+#pragma unroll
+                for (int kx = 0; kx < 3; ++kx) {
+                    const int xi = 2 * x - 1 + kx;
+                    if (xi < 0 || xi >= Wi) continue;
+                    const uint4 v = *reinterpret_cast<const uint4 *>(row + (long long)xi * A.act.Cp);
+                    const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+                    const uint32_t pos = (uint32_t)(ky * 3 + kx) * 0x00010001u;
+                    if (!have) {
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) { best[h] = vw[h]; cw[h] = pos; }
+                        have = true;
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const uint32_t m = bf2_gt_mask(vw[h], best[h]);   // strictly greater: first wins ties
+                            best[h] = bf2_max(vw[h], best[h]);
+                            cw[h] = (cw[h] & ~m) | (pos & m);
+                        }
+                    }
+                }
+            }
+            if (have) {
+                code = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+                dyv = *reinterpret_cast<const uint4 *>((const bf16 *)A.dy.p + voff(A.dy, b, y, x) + cv * 8);
+            }
+        }
+        scode[pix * CV + cv] = code;
+        sdy[pix * CV + cv] = dyv;
+    }
+    __syncthreads();
+    const int owned = (g1 - g0) * kP3TP * CV;
+    for (int i = threadIdx.x; i < owned; i += blockDim.x) {
+        const int cv = i % CV, r = i / CV;
+        const int xp = xp0 + r % kP3TP, g = g0 + r / kP3TP;
+        const int xa = 2 * xp;
+        if (xa >= Wi) continue;
+        float accA[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, accB[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int c0 = (xp - xp0) * CV + cv;
+        auto window_row = [&](int y, int ky) {
+            const int sl = (y - wy0) * NX * CV + c0;
+            const uint4 cl = scode[sl], dl = sdy[sl], cr = scode[sl + CV], dr = sdy[sl + CV];
+            acc_masked(accA, dl, cl, (uint32_t)(ky * 3 + 1) * 0x00010001u);
+            acc_masked(accB, dl, cl, (uint32_t)(ky * 3 + 2) * 0x00010001u);
+            acc_masked(accB, dr, cr, (uint32_t)(ky * 3 + 0) * 0x00010001u);
+        };
+        if ((g & 1) == 0) window_row(g >> 1, 1);
+        else { window_row(g >> 1, 2); window_row((g >> 1) + 1, 0); }
+        bf16 *dp = (bf16 *)A.dx.p + voff(A.dx, b, g, xa) + cv * 8;
+        const bf16 *ap = (const bf16 *)A.act.p + voff(A.act, b, g, xa) + cv * 8;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            if (e == 1 && xa + 1 >= Wi) break;
+            float o[8], a[8];
+            const float (&acc)[8] = e ? accB : accA;
+            if (A.acc) {
+                ld8(dp + e * A.dx.Cp, o);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] += acc[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] = acc[j];
+            }
+            if (A.gate) {
+                ld8(ap + e * A.act.Cp, a);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (!(a[j] > 0.f)) o[j] = 0.f;
+            }
+            st8(dp + e * A.dx.Cp, o);
         }
     }
 }
@@ -896,10 +1064,18 @@ cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     }
     return cudaGetLastError();
 }
+// the tiled gather (k_pool_bwd_tile8) takes overlapping windows whose per-tile state fits in shared memory
+bool pool_tiled_shape(int k, int s, int Cp) {
+    const size_t shm = (size_t)pool_tile_rows(kPoolTR, k, s) * pool_tile_rows(kPoolTC, k, s) * (Cp / 8) * 40;
+    return Cp % 8 == 0 && k > s && k <= 2 * s && k <= 16 && shm <= 200 * 1024;
+}
+static bool pool_tiled(const PoolArgs &a) {
+    return a.dx.Cp == a.dy.Cp && pool_tiled_shape(a.k, a.s, a.dx.Cp) && a.B <= 65535;
+}
 int simt_pool_bwd_launches(const PoolArgs &a) {
     if ((long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp <= 0) return 0;
     if (pool2(a, a.dy)) return a.b > a.a ? 1 : 0;
-    return a.dx.Cp % 8 == 0 && a.k > a.s && a.k <= 2 * a.s ? 4 : 1;
+    return 1;
 }
 cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.rb - a.ra) * a.dx.W * a.dx.Cp;
@@ -909,11 +1085,21 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
         const int rowv = a.dy.W * (a.dy.Cp / 8);
         dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
         if (prec) launch_simt(k_pool2_bwd<bf16>, g, kT, 0, st, a); else launch_simt(k_pool2_bwd<float>, g, kT, 0, st, a);
-    } else if (a.dx.Cp % 8 == 0 && a.k > a.s && a.k <= 2 * a.s) {
-        const long long m = (long long)a.B * (a.b - a.a) * a.dy.W * (a.dy.Cp / 8) / 4 + 1;
-        for (int ph = 0; ph < 4; ++ph) {
-            if (prec) launch_simt(k_pool_bwd_scatter8<bf16>, grid_for(m), kT, 0, st, a, ph >> 1, ph & 1);
-            else launch_simt(k_pool_bwd_scatter8<float>, grid_for(m), kT, 0, st, a, ph >> 1, ph & 1);
+    } else if (prec && a.k == 3 && a.s == 2 && a.p == 1 && a.dx.Cp % 8 == 0 && a.dx.Cp == a.dy.Cp && a.B <= 65535) {
+        const size_t shm = (size_t)2 * (kP3TR / 2 + 2) * (kP3TP + 1) * (a.dy.Cp / 8) * 16;
+        dim3 g((a.dx.W + 2 * kP3TP - 1) / (2 * kP3TP), (a.rb - a.ra + kP3TR - 1) / kP3TR, a.B);
+        cudaFuncSetAttribute(k_pool3s2_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        launch_simt(k_pool3s2_bwd, g, kT, shm, st, a);
+    } else if (pool_tiled(a)) {
+        const int ny = pool_tile_rows(kPoolTR, a.k, a.s), nx = pool_tile_rows(kPoolTC, a.k, a.s);
+        const size_t shm = (size_t)ny * nx * (a.dy.Cp / 8) * (8 * (prec ? 2 : 4) + 8);
+        dim3 g((a.dx.W + kPoolTC - 1) / kPoolTC, (a.rb - a.ra + kPoolTR - 1) / kPoolTR, a.B);
+        if (prec) {
+            cudaFuncSetAttribute(k_pool_bwd_tile8<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+            launch_simt(k_pool_bwd_tile8<bf16>, g, kT, shm, st, a, ny, nx);
+        } else {
+            cudaFuncSetAttribute(k_pool_bwd_tile8<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+            launch_simt(k_pool_bwd_tile8<float>, g, kT, shm, st, a, ny, nx);
         }
     } else if (a.dx.Cp % 8 == 0) {
         n /= 8;

@@ -373,13 +373,14 @@ class Plan:
         return ms.value, n.value, fl.value
 
     def profile_kernels(self, cls, stream=None):
-        """Per-kernel totals of profile class cls: [{name, launches, ms, flops}] (lrcnn_profile_kernels)."""
+        """Per-kernel totals of profile class cls: [{name, launches, ms, flops, bytes}] (lrcnn_profile_kernels;
+        bytes = algorithmic HBM bytes of the launches)."""
         buf = ctypes.create_string_buffer(1 << 16)
         _check(lib().lrcnn_profile_kernels(self.h, cls, buf, len(buf), _stream(stream)))
         out = []
         for line in buf.value.decode().splitlines():
-            name, n, ms, fl = line.rsplit(",", 3)
-            out.append({"name": name, "launches": int(n), "ms": float(ms), "flops": float(fl)})
+            name, n, ms, fl, by = line.rsplit(",", 4)
+            out.append({"name": name, "launches": int(n), "ms": float(ms), "flops": float(fl), "bytes": float(by)})
         return out
 
     def profile_dump(self, path, stream=None):

@@ -4,7 +4,9 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+# several captured launches: keep the first kernel's block (up to the next "Kernel Name" line)
+end = next((i for i in range(2, len(rows)) if rows[i] and rows[i][0] == "Kernel Name"), len(rows))
+data = [dict(zip(hdr, r)) for r in rows[2:end] if len(r) == len(hdr)]
 tot = sum(int(d["Warp Stall Sampling (All Samples)"] or 0) for d in data)
 stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 agg = {h: sum(int(d[h] or 0) for d in data) for h in stall_cols}
