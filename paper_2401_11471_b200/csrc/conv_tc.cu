@@ -1458,6 +1458,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
 // K = 128 band pixels per stage (8 MMAs of K=16).  Work item = (co tile, tap, ci tile,
 // pixel split); fp32 partial sums are added with red.global into the flat gradient.
 static constexpr int kWgA = 2 * kABytes;
+__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 template <int BN>
 struct WgCfg {
     // B operand (shifted band input): BN/KB boxes of KB channels (KB = 64, SWIZZLE_128B; or
@@ -1620,6 +1624,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                 }
             } else {
+                // this thread's row co: 32 consecutive input channels per TMEM load, added with
+                // 16-byte vector reductions (cin_p % 8 == 0, so a 4-group is all in or all out)
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
@@ -1628,11 +1634,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (co >= P.c_out) continue;
                     const int ci0 = cit * BN + c * 32;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (ci0 + j < P.cin_p) {
-                            atomicAdd(dst + ci0 + j, __uint_as_float(v[j]) * gsc);
-                            if (P.dg) gdot += __uint_as_float(v[j]) * __bfloat162float(wrow[ci0 + j]);
+                    for (int j = 0; j < 32; j += 8) {
+                        if (ci0 + j >= P.cin_p) break;
+                        red_add_v4(dst + ci0 + j, __uint_as_float(v[j]) * gsc, __uint_as_float(v[j + 1]) * gsc,
+                                   __uint_as_float(v[j + 2]) * gsc, __uint_as_float(v[j + 3]) * gsc);
+                        red_add_v4(dst + ci0 + j + 4, __uint_as_float(v[j + 4]) * gsc, __uint_as_float(v[j + 5]) * gsc,
+                                   __uint_as_float(v[j + 6]) * gsc, __uint_as_float(v[j + 7]) * gsc);
+                        if (P.dg) {
+                            const uint4 wv = *reinterpret_cast<const uint4 *>(wrow + ci0 + j);
+                            const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+                                gdot += __uint_as_float(v[j + 2 * h]) * bf_lo(ww[h]) + __uint_as_float(v[j + 2 * h + 1]) * bf_hi(ww[h]);
                         }
+                    }
                 }
             }
             if (P.dg && co < P.c_out) atomicAdd(P.dg + co, gdot);
@@ -1672,9 +1687,6 @@ struct WgHCfg {
     static constexpr uint32_t kTmemCols = KW * BN <= 32 ? 32 : KW * BN <= 64 ? 64 : KW * BN <= 128 ? 128 : KW * BN <= 256 ? 256 : 512;
 };
 
-__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
 
 template <int BN, int KW>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -3119,7 +3131,8 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.co_tiles = (dy.Cp + 127) / 128;
     P.ci_tiles = (x.Cp + BN - 1) / BN;
     const int base_items = P.co_tiles * a.k * a.k * P.ci_tiles;
-    int splits = 2 * num_sms() / base_items;
+    static const int split_mul = env_int("LRCNN_WG_SPLIT_MUL", 1);
+    int splits = split_mul * num_sms() / base_items;
     if (splits > P.pix_tiles) splits = P.pix_tiles;
     if (splits < 1) splits = 1;
     P.per_split = (P.pix_tiles + splits - 1) / splits;
