@@ -114,6 +114,11 @@ typedef struct {
  * carry buffers, overlaid across segments) fits in that same budget.  Peak memory is unchanged,
  * thin deep segments get fewer, larger bands (fewer halo rows, larger kernel launches). */
 #define LRCNN_FLAG_BALANCED_BANDS 4
+/* Disable the fused residual gradient (bf16 tensor-core path): a block input read by a stride-1
+ * convolution and a residual add gets delta = gate * (dgrad + delta(block output)) from that
+ * convolution's dgrad epilogue (the block output's delta as a TMA-loaded addend) instead of a
+ * memset, an accumulating dgrad and a separate residual pass.  Set only to compare (tests). */
+#define LRCNN_FLAG_NO_FUSE_RES 8
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 

@@ -43,6 +43,7 @@ typedef __nv_bfloat16 bf16;
 struct TcConv {
     View out, res, act;
     View in;               // im2col kernel: the band input it gathers from
+    View add;              // dgrad addend (dg_add)
     const bf16 *bias, *beta;
     int mode;              // 0 = forward epilogue, 1 = dgrad (gated accumulate)
     int epi, relu, gate, has_res, c_real, n_out;
@@ -63,6 +64,8 @@ struct TcConv {
     int th_log2;           // TH = 1 << th_log2
     int NBt;               // images per tile (small maps: a 128-pixel tile spans NBt images; 0/1 = one)
     int dg_write;          // dgrad: overwrite delta_in (gate * acc) instead of accumulating into it
+    int dg_add;            // dgrad, with dg_write: delta_in = gate * (acc + addend tile, TMA-loaded from tmX)
+    int add_req;           // host: the caller asks for the addend (conv_launch sets dg_add if the kernel takes it)
     int pat_w, pat_h, pat_ox, pat_oy;   // im2col kernel: input patch per tile (pixels) and its offset
     uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
     int cta2;              // 1: CTA-pair kernel (k_conv_tc2): tile = 2 * pair + CTA rank, m_tiles rounded up to even
@@ -329,12 +332,9 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             if (rt) {
                 ptx::mbar_wait(rbar + sbuf, (rphases >> sbuf) & 1);   // residual tile of this group in buf
                 rphases ^= 1u << sbuf;
+                // each thread reads, then overwrites, only its own row's chunks: no barrier needed
 #pragma unroll
                 for (int c = 0; c < CH / 8; ++c) pr[c] = ld_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4));
-                epi_bar_n<NE>();                       // every thread has read its residual row
-            } else {
-                if (leader) bulk_wait_read_n<NB - 1>();   // the store that last used this buffer has read it
-                epi_bar_n<NE>();
             }
             if (!ragged && P.epi == 1 && !P.has_res) epi_fast_r<CH, 1, false>(P.relu, v, pb, pe, pr, buf, chunk0, m);
             else if (!ragged && P.epi == 2 && !P.has_res) epi_fast_r<CH, 2, false>(P.relu, v, pb, pe, pr, buf, chunk0, m);
@@ -364,6 +364,9 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                 }
             }
             fence_async_smem();
+            // without a residual: before this barrier the leader makes sure the NEXT group's buffer
+            // (last stored NB groups before it) has been read by its store
+            if (!rt && leader) bulk_wait_read_n<NB - 2>();
             epi_bar_n<NE>();
             if (leader && !(P.dbg & 1)) {
                 tma_store_4d(tmO, stage_out + sbuf * kOutStage, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
@@ -473,13 +476,16 @@ template <int BN, int NE = 4>
 __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
                                                       uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
                                                       uint8_t *stage_out, uint64_t *ebar, int warp, int lane,
-                                                      int lead_warp = 2) {
+                                                      int lead_warp = 2, const CUtensorMap *tmX = nullptr) {
     constexpr int CH = 64 * 4 / NE;           // channels of a 64-channel group per thread
     const int num_tiles = P.m_tiles * P.n_tiles;
     const int q = warp & 3, m = q * 32 + lane, hh = (warp - lead_warp) >> 2;
     const bool leader = (warp == lead_warp && lane == 0);
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t ebytes = (P.dg_write ? 0u : (uint32_t)kOutStage) + (P.gate ? (uint32_t)kOutStage : 0u);
+    // delta tile: the old delta (accumulate), the addend (dg_add, from tmX) or nothing (single writer)
+    const bool dload = !P.dg_write || (P.dg_add && tmX);
+    const CUtensorMap *tmD = P.dg_write ? tmX : tmO;
+    const uint32_t ebytes = (dload ? (uint32_t)kOutStage : 0u) + (P.gate ? (uint32_t)kOutStage : 0u);
     // pair i: delta buffer stage_out + 2i*16K, activation buffer stage_out + (2i+1)*16K
     auto issue = [&](int tile, int grp, int pi) {
         int nt, tx, ty, b;
@@ -487,7 +493,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         const int nb = nt * BN + grp * 64, xg0 = tx * P.TW, yg0 = P.out_a + ty * P.TH;
         uint8_t *bd = stage_out + (2 * pi) * kOutStage;
         ptx::mbar_arrive_expect_tx(ebar + pi, ebytes);
-        if (!P.dg_write) ptx::tma_load_4d(bd, tmO, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+        if (dload) ptx::tma_load_4d(bd, tmD, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - (P.dg_write ? P.add.base : P.out.base), b);
         if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
     };
     auto ngroups = [&](int tile) {
@@ -528,7 +534,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
             for (int cc = 0; cc < CH / 8; ++cc) {
                 const int c = hh * (CH / 8) + cc;
                 const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
-                const uint4 dd = P.dg_write ? make_uint4(0, 0, 0, 0) : ld_shared_v4(rowD + off);
+                const uint4 dd = dload ? ld_shared_v4(rowD + off) : make_uint4(0, 0, 0, 0);
                 const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
                 const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
                 uint32_t o[4];
@@ -651,7 +657,8 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
 template <int BN, int KC>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
+              const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P,
+              const __grid_constant__ CUtensorMap tmX) {
     using Cfg = ConvCfg<BN, KC>;
     constexpr int S = Cfg::kStages;
     constexpr int ABYTES = Cfg::kA, BBYTES = Cfg::kB;
@@ -736,7 +743,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
     } else {
         if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
-        else if (P.tma_dg && Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        else if (P.tma_dg && Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
     }
@@ -772,7 +779,8 @@ struct Conv2Cfg {
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
     k_conv_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P,
+               const __grid_constant__ CUtensorMap tmX) {
     using Cfg = Conv2Cfg<BN>;
     constexpr int S = Cfg::kStages;
     constexpr int ABYTES = Cfg::kA, BBYTES = Cfg::kBh;
@@ -864,7 +872,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
         }
     } else {
         if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
-        else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
         else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
     }
     ptx::tc_fence_before();
@@ -2482,7 +2490,7 @@ bool tc_available() { return true; }
 
 template <int BN, int KC>
 static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
-                        const CUtensorMap &G, int tiles, cudaStream_t st) {
+                        const CUtensorMap &G, const CUtensorMap &X, int tiles, cudaStream_t st) {
     using Cfg = ConvCfg<BN, KC>;
     static bool attr = false;
     if (!attr) {
@@ -2491,7 +2499,7 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
         attr = true;
     }
     int grid = tiles < num_sms() ? tiles : num_sms();
-    return launch_pdl(k_conv_tc<BN, KC>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P);
+    return launch_pdl(k_conv_tc<BN, KC>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P, X);
 }
 
 template <int BN>
@@ -2649,6 +2657,12 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
             (!P.gate || encode_view(&G, P.act, P.B, P.TW, P.TH, P.o_stride, 64, NB)))
             P.tma_dg = 1;
     }
+    // fused residual addend (write-mode dgrad with unit stride; k_conv_tc / k_conv_tc2 only)
+    CUtensorMap X = A;
+    P.dg_add = 0;
+    if (P.add_req && P.tma_dg && P.dg_write && !try2h && P.o_stride == 1 && P.add.Cp == P.out.Cp &&
+        aligned16(P.add.p) && P.add.rows > 0 && encode_view(&X, P.add, P.B, P.TW, P.TH, 1, 64, NB))
+        P.dg_add = 1;
     int tiles = P.m_tiles * P.n_tiles;
     if (try2h && (P.tma_out || P.tma_dg) && P.m_tiles >= 2) {
         P.cta2 = 1;
@@ -2694,7 +2708,7 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
                     return false;
                 attr = true;
             }
-            return launch_pdl(k_conv_tc2<256>, grid, kConvThreads, Conv2Cfg<256>::kSmem, st, A, Bm, O, G, P);
+            return launch_pdl(k_conv_tc2<256>, grid, kConvThreads, Conv2Cfg<256>::kSmem, st, A, Bm, O, G, P, X);
         }
         static bool attr = false;
         if (!attr) {
@@ -2703,16 +2717,16 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
                 return false;
             attr = true;
         }
-        return launch_pdl(k_conv_tc2<128>, grid, kConvThreads, Conv2Cfg<128>::kSmem, st, A, Bm, O, G, P);
+        return launch_pdl(k_conv_tc2<128>, grid, kConvThreads, Conv2Cfg<128>::kSmem, st, A, Bm, O, G, P, X);
     }
     if (KC == 16) {
-        if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, G, tiles, st);
-        if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, G, tiles, st);
-        return launch_conv<256, 16>(P, A, Bm, O, G, tiles, st);
+        if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, G, X, tiles, st);
+        if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, G, X, tiles, st);
+        return launch_conv<256, 16>(P, A, Bm, O, G, X, tiles, st);
     }
-    if (BN == 64) return launch_conv<64, 64>(P, A, Bm, O, G, tiles, st);
-    if (BN == 128) return launch_conv<128, 64>(P, A, Bm, O, G, tiles, st);
-    return launch_conv<256, 64>(P, A, Bm, O, G, tiles, st);
+    if (BN == 64) return launch_conv<64, 64>(P, A, Bm, O, G, X, tiles, st);
+    if (BN == 128) return launch_conv<128, 64>(P, A, Bm, O, G, X, tiles, st);
+    return launch_conv<256, 64>(P, A, Bm, O, G, X, tiles, st);
 }
 
 // weights [rows][K] (K = taps * 8, the OHWI layout of an 8-channel input) as a 2D map with
@@ -2918,7 +2932,9 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
             P.ntaps = n;
             if (n == 0 || P.out_b <= P.out_a || P.Wo <= 0) continue;
             P.k = k; P.pad = k - 1 - p; P.halo_ok = s == 1 && k == 3;
+            if (a.add_on && s == 1) { P.add = a.add; P.add_req = 1; }
             if (!conv_launch(P, a.dy, a.wt, a.dx.Cp, k * k, a.dy.Cp, st)) return false;
+            if (P.dg_add) a.add_done = true;
         }
     return true;
 }

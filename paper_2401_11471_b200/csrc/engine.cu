@@ -343,8 +343,45 @@ static lrcnn_status run_forward(Run &R) {
 // rule): the dgrad overwrites them (gate * acc) instead of accumulating into a zeroed buffer, and
 // the 2PS carry of band r+1 is added (gated) right after it.  Saves the band-buffer memset and
 // the dgrad epilogue's delta load.
+// Fused residual gradient.  A band-internal block input t read by exactly one stride-1 convolution
+// (role 0) and by one residual convolution u (role 1, same shape as its output) gets
+//   delta(t) = gate(t) * (dgrad + delta(out_u))
+// from the stride-1 conv's dgrad in write mode with delta(out_u) as a TMA-loaded addend, instead
+// of a memset, an accumulating dgrad and a separate residual pass.  Rows of t that only the
+// residual reads (the 2PS cache row below the dgrad's rows) are written gate * delta(out_u) by a
+// row kernel.  Every band row of t must be covered by one of the two row ranges.  Returns u, or -1.
+static int fused_res(const Plan &P, const Segment &S, int t) {
+    if (!P.use_tc || P.opts.mode == LRCNN_OVERL || t == 0 || t == S.in_t || t == S.out_t) return -1;
+    if (P.opts.flags & LRCNN_FLAG_NO_FUSE_RES) return -1;
+    const TensorInfo &ti = P.t[t];
+    if (ti.cons.size() != 2) return -1;
+    const Consumer &c0 = ti.cons[0].role == 0 ? ti.cons[0] : ti.cons[1];
+    const Consumer &c1 = ti.cons[0].role == 0 ? ti.cons[1] : ti.cons[0];
+    if (c0.role != 0 || c1.role != 1) return -1;
+    const OpInfo &v = P.op[c0.op], &u = P.op[c1.op];
+    if (v.d.kind != LRCNN_OP_CONV || v.d.s != 1 || u.d.kind != LRCNN_OP_CONV || u.d.res != t || c0.op >= c1.op)
+        return -1;
+    const TensorInfo &to = P.t[u.out_t];
+    if (to.Cp != ti.Cp || to.W != ti.W || to.H != ti.H || P.t[u.out_t].seg != ti.seg) return -1;
+    for (size_t r = 0; r < S.E.size(); ++r) {
+        const int lo = S.lo[r][t], hi = S.b[r][t];
+        const int va = S.a[r][v.out_t], vb = S.b[r][v.out_t];
+        const int ra = vb > va ? std::max(0, va - v.d.p) : 0, rb = vb > va ? std::min(ti.H, vb - 1 - v.d.p + v.d.k) : 0;
+        const int oa = S.a[r][u.out_t], ob = S.b[r][u.out_t];
+        // the union of [ra, rb) and [oa, ob) must be exactly the band rows [lo, hi)
+        int x0 = hi, x1 = lo;
+        if (rb > ra) { x0 = std::min(x0, ra); x1 = std::max(x1, rb); }
+        if (ob > oa) { x0 = std::min(x0, oa); x1 = std::max(x1, ob); }
+        if (hi <= lo) continue;
+        if (x0 != lo || x1 != hi) return -1;
+        if (rb > ra && ob > oa && (ob < ra || rb < oa)) return -1;   // a gap between the two ranges
+    }
+    return c1.op;
+}
+
 static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
     if (t == 0 || t == S.in_t || t == S.out_t) return false;
+    if (fused_res(P, S, t) >= 0) return true;
     const TensorInfo &ti = P.t[t];
     if (ti.cons.size() != 1 || ti.cons[0].role != 0) return false;
     const OpInfo &u = P.op[ti.cons[0].op];
@@ -358,12 +395,58 @@ static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
     return pool_tiled_shape(u.d.k, u.d.s, ti.Cp) && (to.H - 1) * u.d.s - u.d.p + u.d.k >= ti.H;
 }
 
+// Residual rows of a fused block input (see fused_res) that the dgrad of op i (input rows [ra, rb),
+// addend consumed or not) did not produce: rows outside [ra, rb) are written gate * delta(out_u),
+// rows inside are added when the dgrad kernel did not take the addend.  with_carry: also add the
+// 2PS carry of band r+1 (the dgrad, which normally does it, produced no rows in this band).
+static lrcnn_status fused_res_rows(Run &R, const Segment &S, int s, int r, int i, int ra, int rb, bool add_done,
+                                   bool with_carry) {
+    Plan &P = R.P;
+    const OpInfo &o = P.op[i];
+    const int fu = fused_res(P, S, o.in_t);
+    if (fu < 0) return LRCNN_OK;
+    const TensorInfo &tt = P.t[o.in_t];
+    const int tu = P.op[fu].out_t, oa = S.a[r][tu], ob = S.b[r][tu];
+    const View dx = dlt_view(R, S, s, r, o.in_t), act = act_view(R, S, r, o.in_t);
+    auto rows = [&](const View &src, int ya, int yb, int write) -> lrcnn_status {
+        if (yb <= ya) return LRCNN_OK;
+        EltArgs E;
+        E.dy = src; E.dx = dx; E.act = act; E.gate = tt.relu;
+        E.a = ya; E.b = yb; E.B = P.net.B; E.write = write;
+        ++P.launches;
+        ProfScope ps(R, 2, 0, i * 8 + 7);
+        CK(simt_acc_gate(R.prec, E, R.st));
+        return LRCNN_OK;
+    };
+    lrcnn_status st;
+    if (ob > oa) {
+        const View dres = sub_rows(dlt_view(R, S, s, r, tu), oa, ob, R.E);
+        if (rb <= ra) {
+            if ((st = rows(dres, oa, ob, 1)) != LRCNN_OK) return st;
+        } else {
+            if (!add_done && (st = rows(dres, std::max(oa, ra), std::min(ob, rb), 0)) != LRCNN_OK) return st;
+            if ((st = rows(dres, oa, std::min(ob, ra), 1)) != LRCNN_OK) return st;
+            if ((st = rows(dres, std::max(oa, rb), ob, 1)) != LRCNN_OK) return st;
+        }
+    }
+    const int N = (int)S.E.size();
+    if (with_carry && P.opts.mode == LRCNN_2PS && r + 1 < N) {
+        const int clo = S.lo[r + 1][o.in_t], chi = S.a[r + 1][o.in_t];
+        const View cv{R.ws + tt.carry_off, clo, chi - clo, tt.H, tt.W, tt.Cp, (long long)tt.carry_cap * tt.W * tt.Cp};
+        if ((st = rows(cv, clo, chi, 0)) != LRCNN_OK) return st;
+    }
+    return LRCNN_OK;
+}
+
 static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     Plan &P = R.P;
     const OpInfo &o = P.op[i];
     const int t = o.out_t;
     const int a = S.a[r][t], b = S.b[r][t];
-    if (b <= a) return LRCNN_OK;
+    if (b <= a) {   // no rows of this op in band r; a fused block input still gets its residual rows
+        if (o.d.kind == LRCNN_OP_CONV && o.in_t != 0) return fused_res_rows(R, S, s, r, i, 0, 0, false, true);
+        return LRCNN_OK;
+    }
     const int B = P.net.B;
     View dy = sub_rows(dlt_view(R, S, s, r, t), a, b, R.E);      // complete, gated delta rows
     const TensorInfo &tin = P.t[o.in_t];
@@ -413,12 +496,24 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             A.ra = std::max(0, a * o.d.s - o.d.p);
             A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
             A.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
+            const int fu = fused_res(P, S, o.in_t);   // residual conv whose output delta is the addend
+            if (fu >= 0) {
+                const int tu = P.op[fu].out_t, oa = S.a[r][tu], ob = S.b[r][tu];
+                if (ob > oa) {
+                    A.add = sub_rows(dlt_view(R, S, s, r, tu), oa, ob, R.E);
+                    A.add_on = 1;
+                }
+            }
             {
                 ++P.launches;
                 ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0));
                 if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
                 else CK(simt_conv_dgrad(R.prec, A, R.st));
                 CK(cudaGetLastError());
+            }
+            if (fu >= 0) {   // residual rows the dgrad did not take
+                lrcnn_status rs = fused_res_rows(R, S, s, r, i, A.ra, A.rb, A.add_done, false);
+                if (rs != LRCNN_OK) return rs;
             }
             const int N = (int)S.E.size();
             if (A.write && P.opts.mode == LRCNN_2PS && r + 1 < N) {   // + the carry of band r+1, gated
@@ -435,7 +530,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
                 }
             }
         }
-        if (o.d.res >= 0) {
+        if (o.d.res >= 0 && fused_res(P, S, o.d.res) != i) {   // (fused: added by the block input's dgrad)
             const TensorInfo &tr = P.t[o.d.res];
             EltArgs A;
             A.dy = dy; A.dx = dlt_view(R, S, s, r, o.d.res); A.act = act_view(R, S, r, o.d.res);

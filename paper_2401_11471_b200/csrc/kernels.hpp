@@ -38,6 +38,11 @@ struct DgradArgs {
     int ra, rb;                // input rows to produce
     int B;
     int write = 0;             // 1: delta_in rows [ra, rb) = gate(act) * acc, not accumulated (single writer)
+    // write mode with an addend (fused residual gradient): delta_in = gate(act) * (acc + add),
+    // add = the complete delta rows of the block output (rows outside add's view read as 0)
+    View add;
+    int add_on = 0;
+    mutable bool add_done = false;   // set by a launcher that consumed the addend
 };
 
 struct WgradArgs {
@@ -71,6 +76,7 @@ struct EltArgs {
     View x0, x1, out;          // add fwd: out = relu?(x0 + x1) on rows [a, b)
     View dy, dx, act;          // res/add bwd: dx = gate(act) * (dx + dy) on rows [a, b)
     int relu, gate, a, b, B;
+    int write = 0;             // res/add bwd: 1 = dx = gate(act) * dy (single writer), 0 = accumulate
 };
 
 // SIMT kernels (fp32 parity mode and the general fallback for shapes the tensor-core

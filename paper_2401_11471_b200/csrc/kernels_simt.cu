@@ -481,7 +481,7 @@ __global__ void k_acc_gate(EltArgs A) {
         int y = A.a + (int)(r % rows);
         int b = (int)(r / rows);
         T *dx = (T *)A.dx.p + voff(A.dx, b, y, x) + c;
-        float v = ldf(dx) + ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + c);
+        float v = (A.write ? 0.f : ldf(dx)) + ldf((const T *)A.dy.p + voff(A.dy, b, y, x) + c);
         if (A.gate && ldf((const T *)A.act.p + voff(A.act, b, y, x) + c) <= 0.f) v = 0.f;
         stf(dx, v);
     }
@@ -943,8 +943,8 @@ __global__ void k_acc_gate8(EltArgs A) {
         int y = A.a + (int)(r % rows);
         int b = (int)(r / rows);
         T *dp = (T *)A.dx.p + voff(A.dx, b, y, x) + cv * 8;
-        float o[8], d[8], a[8];
-        ld8(dp, o);
+        float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, d[8], a[8];
+        if (!A.write) ld8(dp, o);
         ld8((const T *)A.dy.p + voff(A.dy, b, y, x) + cv * 8, d);
         if (A.gate) ld8((const T *)A.act.p + voff(A.act, b, y, x) + cv * 8, a);
 #pragma unroll
@@ -968,8 +968,8 @@ __global__ void k_acc_gate_rows(EltArgs A) {
     const T *dy = (const T *)A.dy.p + voff(A.dy, b, y, 0);
     const T *ac = A.gate ? (const T *)A.act.p + voff(A.act, b, y, 0) : nullptr;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
-        float o[8], d[8], g[8];
-        ld8(dx + i * 8, o);
+        float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, d[8], g[8];
+        if (!A.write) ld8(dx + i * 8, o);
         ld8(dy + i * 8, d);
         if (ac) ld8(ac + i * 8, g);
 #pragma unroll

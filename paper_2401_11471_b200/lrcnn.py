@@ -21,6 +21,7 @@ PRECS = {"fp32": 0, "bf16": 1}
 FLAG_ALLOW_OVERLAP_EXHAUSTION = 1
 FLAG_NO_TCGEN05 = 2
 FLAG_BALANCED_BANDS = 4
+FLAG_NO_FUSE_RES = 8
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 

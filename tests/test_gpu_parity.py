@@ -151,6 +151,32 @@ def test_resnet50_reduced():
           flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION, dzl_kind="head")
 
 
+def test_resnet_identity_blocks_fused_residual():
+    """Identity bottlenecks whose block input has 64 / 128 channels: the tensor-core dgrad of conv1
+    takes the block output's delta as a TMA-loaded addend (fused residual gradient)
+    and the 2PS cache row of the block input is written by the residual row kernel.  The unfused
+    path (memset + accumulating dgrad + residual pass, LRCNN_FLAG_NO_FUSE_RES) is the one the
+    oracle tests above pin; here the fused gradients must equal it up to the one bf16 rounding of
+    delta it saves (same forward, same integer decisions), for COLUMN and 2PS (3 bands, 1-row
+    bands), and z^L must match the oracle."""
+    net = WL.resnet50(H=48, W=40, width_div=4, blocks=(3, 2, 1, 1))
+    B = 2
+    params = WL.make_params(net, seed=2, bias_scale=0.1, gamma_spread=0.2, bf16=True)
+    x = WL.make_input(net, B, seed=0, bf16=True)
+    ts, _ = C.forward(net, params, x, store=C.bf16_store)
+    _, dzl, _, _ = C.head_forward_backward(ts[-1], params["head"], WL.make_labels(net, B))
+    dzl = WL.round_bf16(dzl)
+    for mode, kw in (("column", {}), ("2ps", {"n_bands": 3}), ("2ps", {"band_rows": 1})):
+        _, zl, g_f = run_gpu(net, B, mode, "bf16", params, x, dzl, **kw)
+        _, _, g_u = run_gpu(net, B, mode, "bf16", params, x, dzl, flags=LB.FLAG_NO_FUSE_RES, **kw)
+        assert rel(zl, ts[-1]) <= TOL["bf16"], (mode, kw, "zL")
+        for i, (a, b) in enumerate(zip(g_f, g_u)):
+            if b is None:
+                continue
+            for k in b:
+                assert rel(a[k], b[k]) <= 1e-2, (mode, kw, "op", i, k, rel(a[k], b[k]))
+
+
 def test_vgg_reduced_fp32():
     """VGG-16 topology (13 conv + 5 pool), reduced channels/size, fp32: every mode <= 1e-5."""
     net = WL.vgg16(H=64, W=64, width_div=8)
