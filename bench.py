@@ -49,6 +49,8 @@ def parse():
                     help="budget-driven planning: the smallest band count whose workspace fits (lrcnn_plan_budget)")
     ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
+    ap.add_argument("--no-fp-merge", action="store_true",
+                    help="forward pass on the BP bands (default: merged FP bands, LRCNN_FLAG_FP_MERGE)")
     ap.add_argument("--no-balanced", action="store_true",
                     help="same band count in every segment (default: balanced bands, LRCNN_FLAG_BALANCED_BANDS)")
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
@@ -230,6 +232,8 @@ def main():
     net = make_net(a)
     B = a.batch or CONFIGS[a.config][3]
     flags = (LB.FLAG_NO_TCGEN05 if a.simt else 0) | (0 if a.no_balanced else LB.FLAG_BALANCED_BANDS)
+    if not a.no_fp_merge:   # decoupled FP bands (N_FP < N_BP, same peak memory)
+        flags |= LB.FLAG_FP_MERGE
     kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}
     if a.mode == "column":
         kw = {}
@@ -441,6 +445,7 @@ def main():
                                           else "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU"),
                           "mode": a.mode, "segments": a.segments, "bands": kw,
                           "bands_per_segment": [plan.seg(si)[2] for si in range(plan.nsegs())],
+                          "fp_bands_per_segment": [plan.fp_bands(si)[0] for si in range(plan.nsegs())],
                           "l2": "flushed (512 MB write) between timed steps"},
                "clocks": clocks,
                "e2e": {"value": gb / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": xi_bytes + lab_bytes,

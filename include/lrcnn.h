@@ -119,6 +119,13 @@ typedef struct {
  * convolution's dgrad epilogue (the block output's delta as a TMA-loaded addend) instead of a
  * memset, an accumulating dgrad and a separate residual pass.  Set only to compare (tests). */
 #define LRCNN_FLAG_NO_FUSE_RES 8
+/* Decoupled FP bands (2PS, the FP working set Omega_FP < Omega_BP, so
+ * N_FP <= N_BP): the forward pass runs each segment with the fewest bands -- merges of
+ * consecutive BP bands -- whose activation buffers fit in the band arena the BP needs anyway
+ * (the FP has no delta buffers), and saves the halo rows of every BP band boundary inside a
+ * merged band.  Peak memory is unchanged; results are identical (same kernels, same per-pixel
+ * accumulation order).  lrcnn_plan_fp_bands reports N_FP per segment. */
+#define LRCNN_FLAG_FP_MERGE 16
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 
@@ -183,6 +190,10 @@ LRCNN_API lrcnn_status lrcnn_plan_seg(const lrcnn_plan_t *plan, int seg, int *in
 LRCNN_API lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int band, int tid, int *lo, int *a, int *b);
 
 LRCNN_API lrcnn_status lrcnn_plan_memory(const lrcnn_plan_t *plan, lrcnn_memory_report *rep);
+
+/* Forward / backward band counts of segment `seg`: *n_bp = its bands; *n_fp = the bands the
+ * forward pass runs (< *n_bp with LRCNN_FLAG_FP_MERGE when merged bands fit, else == *n_bp). */
+LRCNN_API lrcnn_status lrcnn_plan_fp_bands(const lrcnn_plan_t *plan, int seg, int *n_fp, int *n_bp);
 
 /* Row sharding (opts.world > 1): this rank owns rows [*own_lo, *own_hi) of the
  * segment output and computes tensor `tid` of the segment over [*lo, *hi) (the OverL backward

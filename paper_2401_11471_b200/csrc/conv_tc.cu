@@ -1466,8 +1466,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
 // K = 128 band pixels per stage (8 MMAs of K=16).  Work item = (co tile, tap, ci tile,
 // pixel split); fp32 partial sums are added with red.global into the flat gradient.
 static constexpr int kWgA = 2 * kABytes;
+// fp32 gradient reduction (no "memory" clobber: the gradient buffer is only ever reduced into
+// here, so surrounding loads of weights / activations may be scheduled across it)
 __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
 }
 
 template <int BN>
@@ -1601,14 +1603,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float sum = 0.f;
                 for (int pt = p0; pt < p1; ++pt) {
                     ptx::mbar_wait(full + stage, phase);
-                    if (want) {
+                    if (want) {   // column m of the 128-pixel delta tile, four independent partial sums
                         const uint32_t base = ptx::smem_u32(smem + stage * SB);
+                        float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 8
                         for (int r = 0; r < 128; ++r) {
                             unsigned short h;
                             asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + r * 128 + (col ^ ((r & 7) << 4))));
-                            sum += __uint_as_float((uint32_t)h << 16);
+                            s4[r & 3] += __uint_as_float((uint32_t)h << 16);
                         }
+                        sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     }
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(empty + stage);
@@ -1638,9 +1642,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
+                    const int ci0 = cit * BN + c * 32;
+                    uint4 wq[4];   // dgamma: this row's 32 weights, loaded while the TMEM load completes
+                    if (P.dg && co < P.c_out) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            wq[j] = ci0 + 8 * j < P.cin_p ? *reinterpret_cast<const uint4 *>(wrow + ci0 + 8 * j)
+                                                          : make_uint4(0, 0, 0, 0);
+                    }
                     ptx::tmem_ld_wait();
                     if (co >= P.c_out) continue;
-                    const int ci0 = cit * BN + c * 32;
 #pragma unroll
                     for (int j = 0; j < 32; j += 8) {
                         if (ci0 + j >= P.cin_p) break;
@@ -1649,7 +1660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         red_add_v4(dst + ci0 + j + 4, __uint_as_float(v[j + 4]) * gsc, __uint_as_float(v[j + 5]) * gsc,
                                    __uint_as_float(v[j + 6]) * gsc, __uint_as_float(v[j + 7]) * gsc);
                         if (P.dg) {
-                            const uint4 wv = *reinterpret_cast<const uint4 *>(wrow + ci0 + j);
+                            const uint4 wv = wq[j / 8];
                             const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
                             for (int h = 0; h < 4; ++h)

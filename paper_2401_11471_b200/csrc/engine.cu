@@ -49,6 +49,7 @@ struct Run {
     size_t E;   // element bytes
     cudaStream_t side = nullptr;   // wgrad / param-grad stream (nullptr: everything on st)
     bool side_busy = false;
+    bool fp_merged = false;        // FP over merged bands: band tensors live in the FP buffers
 };
 
 // Fork: side stream waits for everything enqueued so far on the main stream.
@@ -110,6 +111,11 @@ static void *ckpt_ptr(Run &R, int t) {
 static View act_view(Run &R, const Segment &S, int r, int t) {
     const TensorInfo &ti = R.P.t[t];
     if (t == S.in_t || t == S.out_t) return full_view(ckpt_ptr(R, t), ti);
+    if (R.fp_merged) {   // S is the merged FP view of the segment (fp_lo / fp_b as lo / b)
+        View v = band_view(R.ws + ti.act_fp_off, ti, S.lo[r][t], S.b[r][t]);
+        v.bs = (long long)ti.cap_fp * ti.W * ti.Cp;
+        return v;
+    }
     return band_view(R.ws + ti.act_off, ti, S.lo[r][t], S.b[r][t]);
 }
 
@@ -218,6 +224,41 @@ static lrcnn_status copy_rows(Run &R, const TensorInfo &ti, void *dst, size_t ds
     size_t rb = (size_t)ti.W * ti.Cp * R.E;
     CK(cudaMemcpy2DAsync(dst, dst_pitch_rows * rb, src, src_pitch_rows * rb, rows * rb, R.P.net.B,
                          cudaMemcpyDeviceToDevice, R.st));
+    return LRCNN_OK;
+}
+
+// FP band k of a merged-band segment (LRCNN_FLAG_FP_MERGE): BP bands [r0, r1) computed as one band
+// in the FP buffers; restores the cache rows of BP boundary r0-1 and saves those of every BP
+// boundary r0 .. r1-1 (the BP recomputes band by band from them, R7).
+static lrcnn_status band_forward_merged(Run &R, const Segment &S, const Segment &F, int k) {
+    Plan &P = R.P;
+    lrcnn_status st;
+    const int N = (int)S.E.size(), r0 = S.fp_r0[k], r1 = k + 1 < (int)S.fp_r0.size() ? S.fp_r0[k + 1] : N;
+    if (r0 > 0) {
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            const TensorInfo &ti = P.t[t];
+            const int rows = F.a[k][t] - F.lo[k][t];
+            if (rows <= 0) continue;
+            if ((st = copy_rows(R, ti, R.ws + ti.act_fp_off, ti.cap_fp, R.ws + ti.cache_off[r0 - 1],
+                                ti.cache_rows[r0 - 1], rows)) != LRCNN_OK) return st;
+        }
+    }
+    R.fp_merged = true;
+    for (int i : S.ops)
+        if ((st = op_forward(R, F, k, i)) != LRCNN_OK) { R.fp_merged = false; return st; }
+    R.fp_merged = false;
+    for (int r = r0; r < r1 && r + 1 < N; ++r) {
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            const TensorInfo &ti = P.t[t];
+            const int rows = ti.cache_rows[r];
+            if (rows <= 0) continue;
+            const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+            const char *src = R.ws + ti.act_fp_off + (size_t)(ti.cache_lo[r] - F.lo[k][t]) * rb;
+            if ((st = copy_rows(R, ti, R.ws + ti.cache_off[r], rows, src, ti.cap_fp, rows)) != LRCNN_OK) return st;
+        }
+    }
     return LRCNN_OK;
 }
 
@@ -331,6 +372,16 @@ static lrcnn_status run_forward(Run &R) {
     for (const Segment &S : R.P.seg) {
         if (sharded && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, full_view(ckpt_ptr(R, S.in_t), R.P.t[S.in_t]), false)) != LRCNN_OK) return st;
+        if (!S.fp_r0.empty()) {   // decoupled FP bands (N_FP < N_BP)
+            Segment F = S;
+            F.lo = S.fp_lo; F.a = S.fp_a; F.b = S.fp_b;
+            F.E.clear();
+            for (size_t k = 0; k < S.fp_r0.size(); ++k)
+                F.E.push_back(S.E[k + 1 < S.fp_r0.size() ? S.fp_r0[k + 1] - 1 : S.E.size() - 1]);
+            for (int k = 0; k < (int)S.fp_r0.size(); ++k)
+                if ((st = band_forward_merged(R, S, F, k)) != LRCNN_OK) return st;
+            continue;
+        }
         for (int r = 0; r < (int)S.E.size(); ++r)
             if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) return st;
     }
@@ -822,6 +873,14 @@ lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int band, int ti
     if (lo) *lo = S.lo[band][tid];
     if (a) *a = S.a[band][tid];
     if (b) *b = S.b[band][tid];
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_fp_bands(const lrcnn_plan_t *plan, int seg, int *n_fp, int *n_bp) {
+    if (!plan || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad segment");
+    const Segment &S = plan->P.seg[seg];
+    if (n_bp) *n_bp = (int)S.E.size();
+    if (n_fp) *n_fp = S.fp_r0.empty() ? (int)S.E.size() : (int)S.fp_r0.size();
     return LRCNN_OK;
 }
 

@@ -454,6 +454,51 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         }
         if (a > arena_max) { arena_max = a; M.band_act = act; M.band_delta = dl; M.carry = car; }
     }
+    // decoupled FP bands (LRCNN_FLAG_FP_MERGE): per segment the largest merge
+    // factor m (FP band = m consecutive BP bands) whose FP activation buffers fit in the arena
+    // the BP needs anyway; the FP buffers alias that arena (FP and BP never overlap in time)
+    for (Segment &S : P.seg) {
+        S.fp_r0.clear(); S.fp_lo.clear(); S.fp_a.clear(); S.fp_b.clear();
+        const int N = (int)S.E.size();
+        if (!(opts->flags & LRCNN_FLAG_FP_MERGE) || opts->mode != LRCNN_2PS || N < 2) continue;
+        auto fp_arena = [&](int m, std::vector<int> *caps) {
+            size_t a = 0;
+            for (int t : S.tensors) {
+                if (t == S.out_t) continue;
+                int cap = 0;
+                for (int r0 = 0; r0 < N; r0 += m) {
+                    const int r1 = std::min(N, r0 + m);
+                    cap = std::max(cap, S.b[r1 - 1][t] - S.lo[r0][t]);
+                }
+                cap = std::max(cap, 1);
+                if (caps) caps->push_back(cap);
+                a += align_up(B * cap * rowbytes(t));
+            }
+            return a;
+        };
+        int best = 1;
+        for (int m = 2; m <= N; ++m)
+            if (fp_arena(m, nullptr) <= arena_max) best = m;
+        if (best < 2) continue;
+        std::vector<int> caps;
+        fp_arena(best, &caps);
+        size_t o = arena0;
+        int ci = 0;
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            TensorInfo &ti = P.t[t];
+            ti.cap_fp = caps[ci++];
+            ti.act_fp_off = o;
+            o = arena0 + align_up(o - arena0 + B * ti.cap_fp * rowbytes(t));
+        }
+        for (int r0 = 0; r0 < N; r0 += best) {
+            const int r1 = std::min(N, r0 + best);
+            S.fp_r0.push_back(r0);
+            std::vector<int> lo(T, 0), a(T, 0), b(T, 0);
+            for (int t = 0; t < T; ++t) { lo[t] = S.lo[r0][t]; a[t] = S.a[r0][t]; b[t] = S.b[r1 - 1][t]; }
+            S.fp_lo.push_back(lo); S.fp_a.push_back(a); S.fp_b.push_back(b);
+        }
+    }
     ws = align_up(arena0 + arena_max);
     P.ws_bytes = ws;
     M.workspace = ws;

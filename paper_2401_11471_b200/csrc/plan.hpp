@@ -38,6 +38,9 @@ struct TensorInfo {
     int ck_lo = 0, ck_rows = 0;   // rows a full-width map (image, checkpoint, z^L) holds on this rank
     int dl_lo = 0, dl_rows = 0;   // rows of the boundary delta buffer (segment in/out) on this rank
     size_t wt_off = 0;        // unused for tensors
+    // decoupled FP bands (LRCNN_FLAG_FP_MERGE): FP band buffer (aliases the band arena)
+    size_t act_fp_off = 0;
+    int cap_fp = 0;
 };
 
 struct OpInfo {
@@ -68,6 +71,10 @@ struct Segment {
     // per band r, per global tensor id: lo (buffer start), a (first computed), b (end)
     std::vector<std::vector<int>> lo, a, b;
     int overlap_in = 0;                      // OverL: max overlap of consecutive bands at the input
+    // decoupled FP bands (LRCNN_FLAG_FP_MERGE): FP band k = BP bands [fp_r0[k], fp_r0[k+1]); the
+    // merged per-band ranges live in fp_lo / fp_a / fp_b (empty: FP uses the BP bands)
+    std::vector<int> fp_r0;
+    std::vector<std::vector<int>> fp_lo, fp_a, fp_b;
 };
 
 struct ProfileSlot {

@@ -22,6 +22,7 @@ FLAG_ALLOW_OVERLAP_EXHAUSTION = 1
 FLAG_NO_TCGEN05 = 2
 FLAG_BALANCED_BANDS = 4
 FLAG_NO_FUSE_RES = 8
+FLAG_FP_MERGE = 16
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 
@@ -60,7 +61,7 @@ class MemoryReport(ctypes.Structure):
 
 
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
-           "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_memory", "lrcnn_forward_rows",
+           "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_fp_bands", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
            "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_profile_kernels", "lrcnn_plan_shard", "lrcnn_plan_xfers",
            "lrcnn_comm_nccl_unique_id", "lrcnn_comm_init_nccl", "lrcnn_comm_loopback_group",
@@ -89,6 +90,7 @@ def lib():
     L.lrcnn_plan_param.argtypes = [vp, i, i, szp, szp]
     L.lrcnn_plan_nsegs.argtypes = [vp, ip]
     L.lrcnn_plan_seg.argtypes = [vp, i, ip, ip, ip]
+    L.lrcnn_plan_fp_bands.argtypes = [vp, i, ip, ip]
     L.lrcnn_plan_rows.argtypes = [vp, i, i, i, ip, ip, ip]
     L.lrcnn_plan_memory.argtypes = [vp, ctypes.POINTER(MemoryReport)]
     L.lrcnn_forward_rows.argtypes = [vp, vp, vp, vp, vp, sz, vp]
@@ -233,6 +235,12 @@ class Plan:
         a, b, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _check(lib().lrcnn_plan_seg(self.h, s, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
         return a.value, b.value, n.value
+
+    def fp_bands(self, s):
+        """(N_FP, N_BP) of segment s (lrcnn_plan_fp_bands; N_FP < N_BP with FLAG_FP_MERGE)."""
+        nf, nb = ctypes.c_int(), ctypes.c_int()
+        _check(lib().lrcnn_plan_fp_bands(self.h, s, ctypes.byref(nf), ctypes.byref(nb)))
+        return nf.value, nb.value
 
     def rows(self, seg, band, tid):
         lo, a, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()

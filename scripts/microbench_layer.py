@@ -25,9 +25,10 @@ for sh in shapes:
         op = 0
     else:
         net = {"C": 8, "H": H, "W": W, "classes": 10,
-               "ops": [WL.conv(0, cin, 1, 1, 0), WL.conv(1, cout, k, s, k // 2)]}
+               "ops": [WL.conv(0, cin, 1, 1, 0), WL.conv(1, cout, k, s, k // 2, epi=os.environ.get("EPI", "bias"))]}
         op = 1
-    plan = LB.Plan(net, B, mode="column", prec="bf16")
+    nb = int(os.environ.get("NBANDS", "0"))
+    plan = LB.Plan(net, B, mode="2ps" if nb else "column", prec="bf16", **({"n_bands": nb} if nb else {}))
     ds = LB.DeviceState(plan)
     ds.params.uniform_(-0.1, 0.1)
     ds.x.uniform_()

@@ -290,3 +290,28 @@ def test_step_graph_replay_matches_eager():
         out.append((losses, ds.master.cpu().numpy()))
     assert np.allclose(out[0][0], out[1][0], rtol=1e-5)
     assert rel(out[1][1], out[0][1]) <= 1e-4
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_fp_merge_identical(prec):
+    """Decoupled FP bands (LRCNN_FLAG_FP_MERGE, N_FP < N_BP): the forward runs merged bands and
+    saves the halo rows of every BP boundary; same kernels and per-pixel accumulation order, so
+    z^L equals the unmerged run bit for bit and every gradient up to the order of its fp32
+    atomic reductions (1e-5); fp32 z^L also vs the oracle (1e-5)."""
+    for net, kw in ((WL.vgg16(H=64, W=48, width_div=8, segments="pool"), {"n_bands": 4}),
+                    (WL.resnet50(H=64, W=48, width_div=4, blocks=(2, 2, 1, 1)), {"n_bands": 6})):
+        bf = prec == "bf16"
+        params = WL.make_params(net, seed=2, bias_scale=0.05, bf16=bf)
+        x = WL.make_input(net, 2, seed=0, bf16=bf)
+        ts, _ = C.forward(net, params, x, store=C.bf16_store if bf else C.fp32_store)
+        dzl = WL.make_dzl(ts[-1].shape, bf16=bf)
+        p0, zl0, g0 = run_gpu(net, 2, "2ps", prec, params, x, dzl, **kw)
+        p1, zl1, g1 = run_gpu(net, 2, "2ps", prec, params, x, dzl, flags=LB.FLAG_FP_MERGE, **kw)
+        assert any(p1.fp_bands(s)[0] < p1.fp_bands(s)[1] for s in range(p1.nsegs()))
+        assert np.array_equal(zl0, zl1)
+        for a, b in zip(g0, g1):   # gradients: fp32 atomic reductions, order not fixed
+            if b is not None:
+                for k in b:
+                    assert rel(a[k], b[k]) <= 1e-5, (k, rel(a[k], b[k]))
+        if not bf:
+            assert rel(zl1, ts[-1]) <= TOL["fp32"]

@@ -326,3 +326,27 @@ def test_plan_turning_point():
     assert all(ws[m] > w_star for m in range(1, n_star))
     assert 1 < n_star < 64
     assert ws[64] > w_star and ws[1] > w_star
+
+
+@pytest.mark.parametrize("which", ["vgg", "resnet"])
+def test_fp_merge_bands(which):
+    """Decoupled FP bands (LRCNN_FLAG_FP_MERGE, R7): the FP of a segment merges
+    consecutive BP bands (N_FP < N_BP where the merged activation buffers fit in the band arena);
+    the BP bands, their rows and the workspace are unchanged (peak memory is the same)."""
+    net = WL.vgg16(H=224, W=224, segments="pool") if which == "vgg" else WL.resnet50(H=224, W=224)
+    B = 8
+    for nb in (2, 4, 8):
+        p0 = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb)
+        p1 = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb, flags=LB.FLAG_FP_MERGE)
+        assert p0.ws_bytes == p1.ws_bytes
+        merged = 0
+        for s in range(p1.nsegs()):
+            nf, nbp = p1.fp_bands(s)
+            assert nbp == p0.seg(s)[2] and 1 <= nf <= nbp
+            assert p0.fp_bands(s) == (nbp, nbp)
+            merged += nf < nbp
+            t_in, t_out, n = p1.seg(s)
+            for r in range(n):
+                for t in range(t_in + 1, t_out + 1):
+                    assert p0.rows(s, r, t) == p1.rows(s, r, t)
+        assert merged > 0, nb
