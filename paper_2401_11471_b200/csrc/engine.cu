@@ -119,7 +119,26 @@ static View act_view(Run &R, const Segment &S, int r, int t) {
     return band_view(R.ws + ti.act_off, ti, S.lo[r][t], S.b[r][t]);
 }
 
+// A band-internal tensor without ReLU whose only reader is the residual input of a convolution u
+// (ResNet's projection shortcut) has delta(t) == delta(out_u) on the same rows: the residual add
+// passes the gradient through and there is no gate.  Its delta is that buffer (no memset, no copy
+// pass).  Returns u's output tensor, or -1.
+static int alias_delta(const Plan &P, const Segment &S, int t) {
+    if (t == 0 || t == S.in_t || t == S.out_t) return -1;
+    const TensorInfo &ti = P.t[t];
+    if (ti.relu || ti.cons.size() != 1 || ti.cons[0].role != 1) return -1;
+    const OpInfo &u = P.op[ti.cons[0].op];
+    if (u.d.kind != LRCNN_OP_CONV || u.d.res != t) return -1;
+    const TensorInfo &to = P.t[u.out_t];
+    if (to.Cp != ti.Cp || to.W != ti.W || to.H != ti.H) return -1;
+    return u.out_t;
+}
+
 static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
+    {
+        const int al = alias_delta(R.P, S, t);
+        if (al >= 0) t = al;
+    }
     const TensorInfo &ti = R.P.t[t];
     int nseg = (int)R.P.seg.size();
     if (t == S.out_t) return dfull_view(R.ws + R.P.dfull_off[s & 1], ti);
@@ -581,7 +600,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
                 }
             }
         }
-        if (o.d.res >= 0 && fused_res(P, S, o.d.res) != i) {   // (fused: added by the block input's dgrad)
+        if (o.d.res >= 0 && fused_res(P, S, o.d.res) != i && alias_delta(P, S, o.d.res) < 0) {
+            // (fused: added by the block input's dgrad; aliased: the residual's delta IS dy)
             const TensorInfo &tr = P.t[o.d.res];
             EltArgs A;
             A.dy = dy; A.dx = dlt_view(R, S, s, r, o.d.res); A.act = act_view(R, S, r, o.d.res);
@@ -675,7 +695,7 @@ static lrcnn_status run_backward(Run &R) {
             if (recompute && (st = band_forward(R, S, r, false, true)) != LRCNN_OK) return st;
             // band delta buffers: zero, then the carry of band r+1 (R6)
             for (int t : S.tensors) {
-                if (t == S.out_t || delta_overwrite(P, S, t)) continue;   // overwritten by its dgrad
+                if (t == S.out_t || delta_overwrite(P, S, t) || alias_delta(P, S, t) >= 0) continue;
                 const TensorInfo &ti = P.t[t];
                 size_t rb = (size_t)ti.W * ti.Cp * R.E;
                 int rows = S.b[r][t] - S.lo[r][t];

@@ -1133,6 +1133,41 @@ cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// delta^L for bf16 maps with Cp % 8 == 0: grid (x: pixel chunks, y: image b).  The per-channel
+// value g[c] = (sum_j dlog[b][j] * fw[j][c]) / hw_div (the same order as k_dzl) is computed once per
+// block into shared memory; threads then stream 16-byte vectors of z^L (gate) and delta^L.
+__global__ void k_dzl8(const bf16 *zl, const float *dlog, const bf16 *fw, int HW, int Cp, int C, int classes,
+                       bf16 *dzl, int gate, float hw_div) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
+    extern __shared__ float dz_g[];
+    const int b = blockIdx.y;
+    for (int c = threadIdx.x; c < Cp; c += blockDim.x) {
+        float v = 0.f;
+        if (c < C) {
+            for (int j = 0; j < classes; ++j) v += dlog[b * classes + j] * __bfloat162float(fw[(long long)j * Cp + c]);
+            v /= hw_div;
+        }
+        dz_g[c] = v;
+    }
+    __syncthreads();
+    const int CV = Cp / 8;
+    const long long nv = (long long)HW * CV, base = (long long)b * HW * Cp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+        const int c0 = (int)(i % CV) * 8;
+        float o[8], z[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = dz_g[c0 + j];
+        if (gate) {
+            ld8(zl + base + i * 8, z);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (z[j] <= 0.f) o[j] = 0.f;
+        }
+        st8(dzl + base + i * 8, o);
+    }
+}
+
 // GAP over the z^L rows this rank holds (HW pixels per image), divided by the global H_L*W_L
 cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st) {
     dim3 g1(B, (Cp + 127) / 128);
@@ -1151,7 +1186,14 @@ cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, in
     if (prec) {
         launch_simt(k_fc_ce<bf16>, 1, 1024, shm, st, gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
                                             dlog, loss, g_fc_w, g_fc_b);
-        if (n > 0)
+        if (n > 0 && Cp % 8 == 0 && B <= 65535) {
+            const long long nv = (long long)HW * Cp / 8;
+            long long gx = (nv + kT * 4 - 1) / (kT * 4);
+            const long long cap = (148LL * 8 + B - 1) / B;
+            dim3 g((unsigned)(gx < 1 ? 1 : gx > cap ? cap : gx), B);
+            launch_simt(k_dzl8, g, kT, sizeof(float) * Cp, st, (const bf16 *)zl, dlog, (const bf16 *)fc_w, HW, Cp, C,
+                        classes, (bf16 *)dzl, gate, hw_div);
+        } else if (n > 0)
             launch_simt(k_dzl<bf16>, grid_for(n), kT, 0, st, (const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
                                                    (bf16 *)dzl, gate, hw_div);
     } else {
