@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--mode", default="2ps", choices=["2ps", "overl", "column"])
     ap.add_argument("--segments", default="pool", choices=["pool", "none"])
     ap.add_argument("--n-bands", type=int, default=None,
-                    help="bands of the largest segment (default: 4; 16 for the climate-scale C4 / C5, where "
+                    help="bands of the largest segment (default: 4; 8 for the climate-scale C4 / C5, where "
                          "it meets the north star's >= 5x feature-map reduction vs layer-wise)")
     ap.add_argument("--band-rows", type=int, default=0)
     ap.add_argument("--mem-budget-gb", type=float, default=0.0,
@@ -237,7 +237,7 @@ def main():
     if not a.no_fp_merge:   # decoupled FP bands (N_FP < N_BP, same peak memory)
         flags |= LB.FLAG_FP_MERGE
     if a.n_bands is None:
-        a.n_bands = 16 if a.config in ("c4", "c5") else 4
+        a.n_bands = 8 if a.config in ("c4", "c5") else 4
     kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}
     if a.mode == "column":
         kw = {}

@@ -406,15 +406,19 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             }
         }
     }
-    size_t dmax = 0, xmax = 0;
-    for (const Segment &S : P.seg) {
-        dmax = std::max(dmax, B * P.t[S.out_t].dl_rows * rowbytes(S.out_t));
+    // full-width delta of segment outputs, ping-pong: buffer p holds the outputs of the segments
+    // with index parity p (segment s reads its output delta from s & 1 and writes its input delta
+    // into the other), so each buffer is sized for its own parity's largest map only
+    size_t dmax[2] = {0, 0}, xmax = 0;
+    for (size_t si = 0; si < P.seg.size(); ++si) {
+        const Segment &S = P.seg[si];
+        dmax[si & 1] = std::max(dmax[si & 1], B * P.t[S.out_t].dl_rows * rowbytes(S.out_t));
         for (const Xfer &x : S.in_xfers) xmax = std::max(xmax, B * (size_t)(x.r1 - x.r0) * rowbytes(S.in_t));
     }
-    P.dfull_bytes = dmax;
-    P.dfull_off[0] = alloc(dmax);
-    P.dfull_off[1] = P.seg.size() > 1 ? alloc(dmax) : P.dfull_off[0];
-    M.delta_full = dmax * (P.seg.size() > 1 ? 2 : 1);
+    P.dfull_bytes = std::max(dmax[0], dmax[1]);
+    P.dfull_off[0] = alloc(dmax[0]);
+    P.dfull_off[1] = P.seg.size() > 1 ? alloc(dmax[1]) : P.dfull_off[0];
+    M.delta_full = dmax[0] + (P.seg.size() > 1 ? dmax[1] : 0);
     P.zl_off = alloc(B * zl.ck_rows * rowbytes(n_ops));
     M.checkpoints += B * zl.ck_rows * rowbytes(n_ops);
     if (xmax) {   // two send and two receive staging slots (one per neighbour)
