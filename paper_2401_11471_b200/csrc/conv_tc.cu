@@ -133,6 +133,7 @@ struct TcWgrad {
 };
 
 static constexpr int kThreads = 192;
+static constexpr int kWgThreads = 320;        // wgrad kernels: producer, MMA, 4 epilogue, 4 bias-sum warps
 static constexpr int kConvThreads = 320;      // k_conv_tc: producer, MMA, 8 epilogue warps
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
@@ -1472,6 +1473,22 @@ __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, 
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
 }
 
+// Fused bias / beta gradient: column m (one output channel) of a 128-pixel delta tile in smem
+// (SWIZZLE_128B rows of 128 B), rows r0, r0 + step, ...: the items of one pixel split share the
+// rows of every tile (step = items per split that see the tile), so no item carries the whole
+// column sum (it gated the pipeline of the items that did: 2x slower 3x3 wgrad launches).
+__device__ __forceinline__ float db_col_sum(uint32_t base, uint32_t col, int r0, int step) {
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    int i = 0;
+#pragma unroll 4
+    for (int r = r0; r < 128; r += step, ++i) {
+        unsigned short h;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + r * 128 + (col ^ ((r & 7) << 4))));
+        s4[i & 3] += __uint_as_float((uint32_t)h << 16);
+    }
+    return (s4[0] + s4[1]) + (s4[2] + s4[3]);
+}
+
 template <int BN>
 struct WgCfg {
     // B operand (shifted band input): BN/KB boxes of KB channels (KB = 64, SWIZZLE_128B; or
@@ -1485,7 +1502,7 @@ struct WgCfg {
 };
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad_tc(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
     using Cfg = WgCfg<BN>;
     constexpr int S = Cfg::kStages;
@@ -1581,14 +1598,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
-    } else {
+    } else if (warp < 6) {
         const int ew = warp & 3;
         const int m = ew * 32 + lane;
         int acc = 0;
         uint32_t aphase = 0;
-        int stage = 0;
-        uint32_t phase = 0;
-        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             int cot, tap, cit, split;
             decode(item, cot, tap, cit, split);
@@ -1597,29 +1611,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             float *dst = P.dw + ((long long)co * taps + tap) * P.cin_p;
             const bf16 *wrow = P.w + ((long long)co * taps + tap) * P.cin_p;
             float gdot = 0.f;
-            if (P.db) {   // fused bias / beta gradient: sum the delta column m of every pixel tile
-                const bool want = tap == 0 && cit == 0;
-                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
-                float sum = 0.f;
-                for (int pt = p0; pt < p1; ++pt) {
-                    ptx::mbar_wait(full + stage, phase);
-                    if (want) {   // column m of the 128-pixel delta tile, four independent partial sums
-                        const uint32_t base = ptx::smem_u32(smem + stage * SB);
-                        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-                        for (int r = 0; r < 128; ++r) {
-                            unsigned short h;
-                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + r * 128 + (col ^ ((r & 7) << 4))));
-                            s4[r & 3] += __uint_as_float((uint32_t)h << 16);
-                        }
-                        sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
-                    }
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty + stage);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
-            }
             ptx::mbar_wait(tfull + acc, aphase);
             ptx::tc_fence_after();
             if constexpr (BN < 32) {
@@ -1675,6 +1666,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) ptx::mbar_arrive(tempty + acc);
             if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
+    } else if (P.db) {
+        // warps 6..9: the fused bias / beta gradient (delta column sums) on their own warps, so the
+        // epilogue warps never gate the pipeline stages of the next item
+        const int m = (warp & 3) * 32 + lane;
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int cot, tap, cit, split;
+            decode(item, cot, tap, cit, split);
+            const int co = cot * 128 + m;
+            if (P.db) {   // fused bias / beta gradient: sum the delta column m of every pixel tile
+                const int nparts = taps * P.ci_tiles, part = tap * P.ci_tiles + cit;
+                const bool want = part < 128;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float sum = 0.f;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    if (want) sum += db_col_sum(ptx::smem_u32(smem + stage * SB), col, part, nparts);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
+            }
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -1708,7 +1725,7 @@ struct WgHCfg {
 
 
 template <int BN, int KW>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad_halo(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
     using Cfg = WgHCfg<BN, KW>;
     constexpr int S = Cfg::kStages;
@@ -1811,42 +1828,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tphase ^= 1;
             }
         }
-    } else {
+    } else if (warp < 6) {
         const int ew = warp & 3;
         const int m = ew * 32 + lane;
         const int taps = KW * KW;
         uint32_t tphase = 0;
-        int stage = 0;
-        uint32_t phase = 0;
-        // fused bias gradient: thread m sums delta column (co tile row) m of every pixel tile
-        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             int cot, ky, cit, split;
             decode(item, cot, ky, cit, split);
             const int co = cot * 128 + m;
             const float gsc = (P.gamma && co < P.c_out) ? __bfloat162float(P.gamma[co]) : 1.f;
-            if (P.db) {
-                const bool want = ky == 0 && cit == 0;
-                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
-                float sum = 0.f;
-                for (int pt = p0; pt < p1; ++pt) {
-                    ptx::mbar_wait(full + stage, phase);
-                    if (want) {
-                        const uint32_t base = ptx::smem_u32(smem + stage * SB);
-#pragma unroll 8
-                        for (int r = 0; r < 128; ++r) {
-                            const uint32_t a = base + r * 128 + (col ^ ((r & 7) << 4));
-                            unsigned short h;
-                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
-                            sum += __uint_as_float((uint32_t)h << 16);
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty + stage);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
-            }
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
             float gdot = 0.f;
@@ -1858,18 +1849,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + kx * BN + c * 32, v);
+                    const int ci0 = cit * BN + c * 32;
+                    uint4 wq[4];   // dgamma: this row's 32 weights (16-byte loads overlapping the TMEM load)
+                    if (P.dg && co < P.c_out) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            wq[q] = ci0 + 8 * q < P.cin_p ? *reinterpret_cast<const uint4 *>(wrow + c * 32 + 8 * q)
+                                                          : make_uint4(0, 0, 0, 0);
+                    }
                     ptx::tmem_ld_wait();
                     if (co >= P.c_out) continue;
-                    const int ci0 = cit * BN + c * 32;
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
                         if (ci0 + j < P.cin_p) {
                             red_add_v4(dst + c * 32 + j, __uint_as_float(v[j]) * gsc, __uint_as_float(v[j + 1]) * gsc,
                                        __uint_as_float(v[j + 2]) * gsc, __uint_as_float(v[j + 3]) * gsc);
                             if (P.dg) {
-#pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    gdot += __uint_as_float(v[j + q]) * __bfloat162float(wrow[c * 32 + j + q]);
+                                const uint4 w8 = wq[j / 8];
+                                const uint32_t w0 = (j & 4) ? w8.z : w8.x, w1 = (j & 4) ? w8.w : w8.y;
+                                gdot += __uint_as_float(v[j]) * bf_lo(w0) + __uint_as_float(v[j + 1]) * bf_hi(w0) +
+                                        __uint_as_float(v[j + 2]) * bf_lo(w1) + __uint_as_float(v[j + 3]) * bf_hi(w1);
                             }
                         }
                 }
@@ -1879,6 +1878,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty);
             tphase ^= 1;
+        }
+    } else if (P.db) {
+        // warps 6..9: the fused bias / beta gradient (delta column sums) on their own warps, so the
+        // epilogue warps never gate the pipeline stages of the next item
+        const int m = (warp & 3) * 32 + lane;
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int cot, ky, cit, split;
+            decode(item, cot, ky, cit, split);
+            const int co = cot * 128 + m;
+            if (P.db) {
+                const int nparts = P.k * P.ci_tiles, part = ky * P.ci_tiles + cit;
+                const bool want = part < 128;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float sum = 0.f;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    if (want) sum += db_col_sum(ptx::smem_u32(smem + stage * SB), col, part, nparts);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
+            }
         }
     }
     ptx::tc_fence_before();
@@ -1909,7 +1934,7 @@ struct WgPCfg {
 };
 
 template <int KW>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad_pair(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
     using Cfg = WgPCfg<KW>;
     constexpr int S = Cfg::kStages, SB = Cfg::kStageBytes, NP = Cfg::kPairs, TAPS = KW * KW;
@@ -2004,37 +2029,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tphase ^= 1;
             }
         }
-    } else {
+    } else if (warp < 6) {
         const int ew = warp & 3;
         const int m = ew * 32 + lane;             // accumulator row: (tap tA or tB, input channel m & 63)
         uint32_t tphase = 0;
-        int stage = 0;
-        uint32_t phase = 0;
-        const uint32_t col = (uint32_t)(((m & 63) >> 3) * 16 + (m & 7) * 2);   // delta column m (m < 64)
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
-            const int split = item % P.splits, cit = item / P.splits;
-            if (P.db) {
-                const bool want = cit == 0 && m < 64;
-                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
-                float sum = 0.f;
-                for (int pt = p0; pt < p1; ++pt) {
-                    ptx::mbar_wait(full + stage, phase);
-                    if (want) {
-                        const uint32_t base = ptx::smem_u32(smem + stage * SB);
-#pragma unroll 8
-                        for (int r = 0; r < 128; ++r) {
-                            const uint32_t a = base + r * 128 + (col ^ ((r & 7) << 4));
-                            unsigned short h;
-                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
-                            sum += __uint_as_float((uint32_t)h << 16);
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty + stage);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                if (want && m < P.c_out) atomicAdd(P.db + m, sum);
-            }
+            const int cit = item / P.splits;
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
             const int ci = cit * 64 + (m & 63);
@@ -2066,6 +2066,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty);
             tphase ^= 1;
+        }
+    } else if (P.db) {
+        // warps 6..9: the fused bias / beta gradient (delta column sums) on their own warps, so the
+        // epilogue warps never gate the pipeline stages of the next item
+        const int m = (warp & 3) * 32 + lane;
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t col = (uint32_t)(((m & 63) >> 3) * 16 + (m & 7) * 2);   // delta column m (m < 64)
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            const int split = item % P.splits, cit = item / P.splits;
+            if (P.db) {
+                const bool want = cit < 128 && m < 64;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float sum = 0.f;
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    if (want) sum += db_col_sum(ptx::smem_u32(smem + stage * SB), col, cit, P.ci_tiles);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                if (want && m < P.c_out) atomicAdd(P.db + m, sum);
+            }
         }
     }
     ptx::tc_fence_before();
@@ -2960,7 +2983,7 @@ static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorM
         attr = true;
     }
     int grid = P.items < num_sms() ? P.items : num_sms();
-    return launch_pdl(k_wgrad_tc<BN>, grid, kThreads, Cfg::kSmem, st, D, X, P);
+    return launch_pdl(k_wgrad_tc<BN>, grid, kWgThreads, Cfg::kSmem, st, D, X, P);
 }
 
 template <int BN, int KW>
@@ -2974,7 +2997,7 @@ static bool launch_wgrad_halo(const TcWgrad &P, const CUtensorMap &D, const CUte
         attr = true;
     }
     int grid = P.items < num_sms() ? P.items : num_sms();
-    return launch_pdl(k_wgrad_halo<BN, KW>, grid, kThreads, Cfg::kSmem, st, D, X, P);
+    return launch_pdl(k_wgrad_halo<BN, KW>, grid, kWgThreads, Cfg::kSmem, st, D, X, P);
 }
 
 // stride-1 k x k wgrad with c_out <= 64 (one 64-channel delta box) and 64-multiple input channels
@@ -3022,7 +3045,7 @@ static bool wgrad_pair(const WgradArgs &a, cudaStream_t st) {
         attr = true;
     }
     const int grid = P.items < num_sms() ? P.items : num_sms();
-    if (!launch_pdl(k_wgrad_pair<3>, grid, kThreads, Cfg::kSmem, st, D, X, P)) return false;
+    if (!launch_pdl(k_wgrad_pair<3>, grid, kWgThreads, Cfg::kSmem, st, D, X, P)) return false;
     if (P.db) a.db_done = true;
     return true;
 }
