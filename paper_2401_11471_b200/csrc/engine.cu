@@ -739,6 +739,47 @@ static lrcnn_status check_ws(Plan &P, void *ws, size_t ws_bytes) {
 
 using namespace lrcnn;
 
+// Replays a captured CUDA graph of `eager` while the call's key (its pointer arguments, stream, lr)
+// is unchanged: the first call runs eagerly (warms caches and function attributes), the second
+// captures and launches the graph, later ones only launch it.  Eager when graphs are off, on the
+// legacy stream, while profiling, or with a communicator that cannot be captured.
+template <typename F>
+static lrcnn_status graph_run(Plan &P, int slot, const uintptr_t (&key)[9], void *stream, F &&eager) {
+    static const int graphs = getenv("LRCNN_GRAPH") ? atoi(getenv("LRCNN_GRAPH")) : 1;
+    if (!graphs || stream == nullptr || P.profiling || (P.comm && !comm_graph_safe((Comm *)P.comm))) {
+        P.graph_calls[slot] = 0;
+        return eager();
+    }
+    const bool same = std::memcmp(key, P.graph_key[slot], sizeof(key)) == 0;
+    if (same && P.graph_exec[slot]) {
+        CK(cudaGraphLaunch((cudaGraphExec_t)P.graph_exec[slot], (cudaStream_t)stream));
+        P.launches = P.graph_launches[slot];
+        P.tc_launches = P.graph_tc_launches[slot];
+        P.fwd_done = false;
+        return LRCNN_OK;
+    }
+    P.graph_calls[slot] = same ? P.graph_calls[slot] + 1 : 1;
+    std::memcpy(P.graph_key[slot], key, sizeof(key));
+    if (P.graph_exec[slot]) { cudaGraphExecDestroy((cudaGraphExec_t)P.graph_exec[slot]); P.graph_exec[slot] = nullptr; }
+    if (P.graph_calls[slot] < 2) return eager();
+    cudaStream_t cs = (cudaStream_t)stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    lrcnn_status st = eager();
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    if (st != LRCNN_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (ce != cudaSuccess) return fail(LRCNN_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t ge = nullptr;
+    ce = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(LRCNN_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
+    P.graph_exec[slot] = ge;
+    P.graph_launches[slot] = P.launches;
+    P.graph_tc_launches[slot] = P.tc_launches;
+    CK(cudaGraphLaunch(ge, cs));
+    return LRCNN_OK;
+}
+
 extern "C" {
 
 const char *lrcnn_last_error(void) { return g_err.c_str(); }
@@ -812,7 +853,8 @@ lrcnn_status lrcnn_plan_turning_point(const lrcnn_net_desc *net, const lrcnn_pla
 
 lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
     if (plan) {
-        if (plan->P.graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)plan->P.graph_exec);
+        for (int g = 0; g < 2; ++g)
+            if (plan->P.graph_exec[g]) cudaGraphExecDestroy((cudaGraphExec_t)plan->P.graph_exec[g]);
         if (plan->P.side_stream) {
             cudaStreamSynchronize((cudaStream_t)plan->P.side_stream);
             cudaStreamDestroy((cudaStream_t)plan->P.side_stream);
@@ -980,9 +1022,8 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
     return st;
 }
 
-lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *grads, const void *x,
-                              const int32_t *labels, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
-    if (!plan || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
+static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, float *grads, const void *x,
+                                     const int32_t *labels, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
     Plan &P = plan->P;
     lrcnn_status st = check_ws(P, ws, ws_bytes);
     if (st != LRCNN_OK) return st;
@@ -1017,6 +1058,16 @@ lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *gra
     return st;
 }
 
+lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *grads, const void *x,
+                              const int32_t *labels, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!plan || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
+    const uintptr_t key[9] = {0, (uintptr_t)params, (uintptr_t)grads, (uintptr_t)x, (uintptr_t)labels,
+                              (uintptr_t)loss_dev, (uintptr_t)ws, (uintptr_t)stream, 0};
+    return graph_run(plan->P, 1, key, stream, [&]() {
+        return step_grads_eager(plan, params, grads, x, labels, loss_dev, ws, ws_bytes, stream);
+    });
+}
+
 lrcnn_status lrcnn_plan_set_comm(lrcnn_plan_t *plan, lrcnn_comm *comm) {
     if (!plan) return fail(LRCNN_E_ARG, "plan is NULL");
     if (comm && (comm_world((Comm *)comm) != plan->P.opts.world || comm_rank((Comm *)comm) != plan->P.opts.rank))
@@ -1036,7 +1087,7 @@ lrcnn_status lrcnn_sgd(lrcnn_plan_t *plan, float *master, void *params, float *g
 static lrcnn_status step_eager(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
                                const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes,
                                void *stream) {
-    lrcnn_status st = lrcnn_step_grads(plan, params, grads, x, labels, loss_dev, ws, ws_bytes, stream);
+    lrcnn_status st = step_grads_eager(plan, params, grads, x, labels, loss_dev, ws, ws_bytes, stream);
     if (st != LRCNN_OK) return st;
     return lrcnn_sgd(plan, master, params, grads, lr, stream);   // adds its own launch
 }
@@ -1047,46 +1098,14 @@ static lrcnn_status step_eager(lrcnn_plan_t *plan, float *master, void *params, 
 lrcnn_status lrcnn_step(lrcnn_plan_t *plan, float *master, void *params, float *grads, const void *x,
                         const int32_t *labels, float lr, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
     if (!plan || !master || !params || !grads || !x || !labels || !loss_dev) return fail(LRCNN_E_ARG, "NULL argument");
-    Plan &P = plan->P;
-    static const int graphs = getenv("LRCNN_GRAPH") ? atoi(getenv("LRCNN_GRAPH")) : 1;
     float lr_copy = lr;
     uint32_t lr_bits;
     std::memcpy(&lr_bits, &lr_copy, 4);
     const uintptr_t key[9] = {(uintptr_t)master, (uintptr_t)params, (uintptr_t)grads, (uintptr_t)x,
                               (uintptr_t)labels, (uintptr_t)loss_dev, (uintptr_t)ws, (uintptr_t)stream, lr_bits};
-    if (!graphs || stream == nullptr || P.profiling || (P.comm && !comm_graph_safe((Comm *)P.comm))) {
-        P.graph_calls = 0;
+    return graph_run(plan->P, 0, key, stream, [&]() {
         return step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
-    }
-    const bool same = std::memcmp(key, P.graph_key, sizeof(key)) == 0;
-    if (same && P.graph_exec) {
-        CK(cudaGraphLaunch((cudaGraphExec_t)P.graph_exec, (cudaStream_t)stream));
-        P.launches = P.graph_launches;
-        P.tc_launches = P.graph_tc_launches;
-        P.fwd_done = false;
-        return LRCNN_OK;
-    }
-    P.graph_calls = same ? P.graph_calls + 1 : 1;
-    std::memcpy(P.graph_key, key, sizeof(key));
-    if (P.graph_exec) { cudaGraphExecDestroy((cudaGraphExec_t)P.graph_exec); P.graph_exec = nullptr; }
-    if (P.graph_calls < 2)   // first call with these arguments: eager (warms caches, function attributes)
-        return step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
-    cudaStream_t cs = (cudaStream_t)stream;
-    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    lrcnn_status st = step_eager(plan, master, params, grads, x, labels, lr, loss_dev, ws, ws_bytes, stream);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(cs, &g);
-    if (st != LRCNN_OK) { if (g) cudaGraphDestroy(g); return st; }
-    if (ce != cudaSuccess) return fail(LRCNN_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
-    cudaGraphExec_t ge = nullptr;
-    ce = cudaGraphInstantiate(&ge, g, 0);
-    cudaGraphDestroy(g);
-    if (ce != cudaSuccess) return fail(LRCNN_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
-    P.graph_exec = ge;
-    P.graph_launches = P.launches;
-    P.graph_tc_launches = P.tc_launches;
-    CK(cudaGraphLaunch(ge, cs));
-    return LRCNN_OK;
+    });
 }
 
 

@@ -117,13 +117,14 @@ struct Plan {
     std::vector<std::string> pending_names[3];    // tcgen05 kernel launched inside the scope ("" = SIMT)
     std::vector<std::pair<std::string, ProfileSlot>> per_kernel[3];
     std::vector<std::pair<int, ProfileSlot>> per_tag;
-    // CUDA graph of one lrcnn_step, replayed while its arguments are unchanged
-    void *graph_exec = nullptr;                  // cudaGraphExec_t
+    // CUDA graphs of one lrcnn_step (slot 0) / lrcnn_step_grads (slot 1), replayed while the call's
+    // arguments are unchanged
+    void *graph_exec[2] = {nullptr, nullptr};    // cudaGraphExec_t
+    uintptr_t graph_key[2][9] = {};
+    int graph_calls[2] = {0, 0};                 // consecutive calls with the same key
+    long long graph_launches[2] = {0, 0}, graph_tc_launches[2] = {0, 0};
     // side stream for wgrad / parameter reductions (overlap with the dgrad chain) and its events
     void *side_stream = nullptr, *ev_fork = nullptr, *ev_join = nullptr;
-    uintptr_t graph_key[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    int graph_calls = 0;                         // consecutive calls with the same key
-    long long graph_launches = 0, graph_tc_launches = 0;
 };
 
 // Builds the plan; returns status and fills err on failure.

@@ -292,6 +292,35 @@ def test_step_graph_replay_matches_eager():
     assert rel(out[1][1], out[0][1]) <= 1e-4
 
 
+def test_step_grads_graph_replay_matches_step():
+    """lrcnn_step_grads (graph-replayed from its third call on a non-default stream; the data-parallel
+    path: caller all-reduce in between) followed by lrcnn_sgd == lrcnn_step, over 5 steps."""
+    net = WL.vgg16(H=32, W=32, width_div=4, cfg=[64, 64, "M", 128, "M"])
+    B = 2
+    params = WL.make_params(net, seed=2, bias_scale=0.05)
+    x = WL.make_input(net, B)
+    lab = WL.make_labels(net, B)
+    out = []
+    for split in (False, True):
+        plan = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=3)
+        ds = LB.DeviceState(plan)
+        ds.load(params=params, x=x, labels=lab)
+        st = torch.cuda.Stream()
+        losses = []
+        with torch.cuda.stream(st):
+            for _ in range(5):
+                if split:
+                    ds.step_grads(stream=st)
+                    plan.sgd(ds.master, ds.params, ds.grads, 0.05, st)
+                else:
+                    ds.step(0.05, stream=st)
+                torch.cuda.synchronize()
+                losses.append(float(ds.loss.cpu()))
+        out.append((losses, ds.master.cpu().numpy()))
+    assert np.allclose(out[0][0], out[1][0], rtol=1e-5)
+    assert rel(out[1][1], out[0][1]) <= 1e-4
+
+
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
 def test_fp_merge_identical(prec):
     """Decoupled FP bands (LRCNN_FLAG_FP_MERGE, N_FP < N_BP): the forward runs merged bands and
