@@ -1473,20 +1473,21 @@ __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, 
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
 }
 
-// Fused bias / beta gradient: column m (one output channel) of a 128-pixel delta tile in smem
-// (SWIZZLE_128B rows of 128 B), rows r0, r0 + step, ...: the items of one pixel split share the
-// rows of every tile (step = items per split that see the tile), so no item carries the whole
-// column sum (it gated the pipeline of the items that did: 2x slower 3x3 wgrad launches).
-__device__ __forceinline__ float db_col_sum(uint32_t base, uint32_t col, int r0, int step) {
-    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+// Bias-sum warps (128 threads): thread t sums output-channel PAIR cp = t % np (one 32-bit load per
+// row of the SWIZZLE_128B delta tile, 64-channel boxes kABytes apart) over the rows r0 + step * (g +
+// ngroups * j), g = t / np: half the loads of a column-per-thread sum and twice the parallelism.
+__device__ __forceinline__ float2 db_pair_sum(uint32_t base, int cp, int g, int ngroups, int r0, int step) {
+    const uint32_t box = (uint32_t)(cp >> 5) * kABytes, chunk = (uint32_t)((cp & 31) >> 2), cofs = (uint32_t)((cp & 3) * 4);
+    float a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f};
     int i = 0;
 #pragma unroll 4
-    for (int r = r0; r < 128; r += step, ++i) {
-        unsigned short h;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + r * 128 + (col ^ ((r & 7) << 4))));
-        s4[i & 3] += __uint_as_float((uint32_t)h << 16);
+    for (int r = r0 + step * g; r < 128; r += step * ngroups, ++i) {
+        uint32_t w;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(base + box + r * 128 + ((chunk ^ (r & 7)) << 4) + cofs));
+        a[i & 1] += bf_lo(w);
+        b[i & 1] += bf_hi(w);
     }
-    return (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    return make_float2(a[0] + a[1], b[0] + b[1]);
 }
 
 template <int BN>
@@ -1669,28 +1670,27 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     } else if (P.db) {
         // warps 6..9: the fused bias / beta gradient (delta column sums) on their own warps, so the
         // epilogue warps never gate the pipeline stages of the next item
-        const int m = (warp & 3) * 32 + lane;
+        const int t = (warp - 6) * 32 + lane, cp = t % 64, g = t / 64;
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             int cot, tap, cit, split;
             decode(item, cot, tap, cit, split);
-            const int co = cot * 128 + m;
-            if (P.db) {   // fused bias / beta gradient: sum the delta column m of every pixel tile
-                const int nparts = taps * P.ci_tiles, part = tap * P.ci_tiles + cit;
-                const bool want = part < 128;
-                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
-                float sum = 0.f;
-                for (int pt = p0; pt < p1; ++pt) {
-                    ptx::mbar_wait(full + stage, phase);
-                    if (want) sum += db_col_sum(ptx::smem_u32(smem + stage * SB), col, part, nparts);
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty + stage);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
+            const int nparts = taps * P.ci_tiles, part = tap * P.ci_tiles + cit;
+            const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+            float2 sum = make_float2(0.f, 0.f);
+            for (int pt = p0; pt < p1; ++pt) {
+                ptx::mbar_wait(full + stage, phase);
+                const float2 v = db_pair_sum(ptx::smem_u32(smem + stage * SB), cp, g, 2, part, nparts);
+                sum.x += v.x;
+                sum.y += v.y;
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(empty + stage);
+                if (++stage == S) { stage = 0; phase ^= 1; }
             }
+            const int co = cot * 128 + 2 * cp;
+            if (co < P.c_out) atomicAdd(P.db + co, sum.x);
+            if (co + 1 < P.c_out) atomicAdd(P.db + co + 1, sum.y);
         }
     }
     ptx::tc_fence_before();
@@ -1882,28 +1882,27 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     } else if (P.db) {
         // warps 6..9: the fused bias / beta gradient (delta column sums) on their own warps, so the
         // epilogue warps never gate the pipeline stages of the next item
-        const int m = (warp & 3) * 32 + lane;
+        const int t = (warp - 6) * 32 + lane, cp = t % 64, g = t / 64;
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t col = (uint32_t)((m >> 6) * kABytes + ((m & 63) >> 3) * 16 + (m & 7) * 2);
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             int cot, ky, cit, split;
             decode(item, cot, ky, cit, split);
-            const int co = cot * 128 + m;
-            if (P.db) {
-                const int nparts = P.k * P.ci_tiles, part = ky * P.ci_tiles + cit;
-                const bool want = part < 128;
-                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
-                float sum = 0.f;
-                for (int pt = p0; pt < p1; ++pt) {
-                    ptx::mbar_wait(full + stage, phase);
-                    if (want) sum += db_col_sum(ptx::smem_u32(smem + stage * SB), col, part, nparts);
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty + stage);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                if (want && co < P.c_out) atomicAdd(P.db + co, sum);
+            const int nparts = P.k * P.ci_tiles, part = ky * P.ci_tiles + cit;
+            const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+            float2 sum = make_float2(0.f, 0.f);
+            for (int pt = p0; pt < p1; ++pt) {
+                ptx::mbar_wait(full + stage, phase);
+                const float2 v = db_pair_sum(ptx::smem_u32(smem + stage * SB), cp, g, 2, part, nparts);
+                sum.x += v.x;
+                sum.y += v.y;
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(empty + stage);
+                if (++stage == S) { stage = 0; phase ^= 1; }
             }
+            const int co = cot * 128 + 2 * cp;
+            if (co < P.c_out) atomicAdd(P.db + co, sum.x);
+            if (co + 1 < P.c_out) atomicAdd(P.db + co + 1, sum.y);
         }
     }
     ptx::tc_fence_before();
@@ -2070,25 +2069,26 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     } else if (P.db) {
         // warps 6..9: the fused bias / beta gradient (delta column sums) on their own warps, so the
         // epilogue warps never gate the pipeline stages of the next item
-        const int m = (warp & 3) * 32 + lane;
+        const int t = (warp - 6) * 32 + lane, cp = t % 32, g = t / 32;
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t col = (uint32_t)(((m & 63) >> 3) * 16 + (m & 7) * 2);   // delta column m (m < 64)
         for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
             const int split = item % P.splits, cit = item / P.splits;
-            if (P.db) {
-                const bool want = cit < 128 && m < 64;
-                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
-                float sum = 0.f;
-                for (int pt = p0; pt < p1; ++pt) {
-                    ptx::mbar_wait(full + stage, phase);
-                    if (want) sum += db_col_sum(ptx::smem_u32(smem + stage * SB), col, cit, P.ci_tiles);
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty + stage);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                if (want && m < P.c_out) atomicAdd(P.db + m, sum);
+            const int nparts = P.ci_tiles, part = cit;
+            const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+            float2 sum = make_float2(0.f, 0.f);
+            for (int pt = p0; pt < p1; ++pt) {
+                ptx::mbar_wait(full + stage, phase);
+                const float2 v = db_pair_sum(ptx::smem_u32(smem + stage * SB), cp, g, 4, part, nparts);
+                sum.x += v.x;
+                sum.y += v.y;
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(empty + stage);
+                if (++stage == S) { stage = 0; phase ^= 1; }
             }
+            const int co = 2 * cp;
+            if (co < min(P.c_out, 64)) atomicAdd(P.db + co, sum.x);
+            if (co + 1 < min(P.c_out, 64)) atomicAdd(P.db + co + 1, sum.y);
         }
     }
     ptx::tc_fence_before();
@@ -2115,11 +2115,13 @@ struct TcWgI2c {
     int TW, TH, tw_log2, tiles_x, tiles_y, pix_tiles, per_split, splits, items;
     int out_a, out_b, Wo, dy_base;
     int pat_w, pat_h, pat_ox, pat_oy, in_base;
+    float *db;             // fused bias / beta gradient (two extra warps sum the delta tiles)
 };
 static constexpr int kWiStages = 4;
 static constexpr int kWiStage = 2 * 16384 + 16384;                 // A: 2 chunks x 16 KB, B: 16 KB
-static constexpr int kWiThreads = (kI2cGather + 1 + 4 + 1) * 32;   // gather, MMA, 4 epilogue, patch
+static constexpr int kWiThreads = (kI2cGather + 1 + 4 + 1 + 2) * 32;   // gather, MMA, 4 epilogue, patch, 2 bias
 static constexpr int kWiPatchWarp = kI2cGather + 5;
+static constexpr int kWiDbWarp = kI2cGather + 6;
 static constexpr int kWiSmem = kWiStages * kWiStage + 2 * kI2cPatch + 1024 + 256;
 
 template <int BN>
@@ -2139,7 +2141,7 @@ __global__ void __launch_bounds__(kWiThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kMma = kI2cGather;                  // warp 8; epilogue warps 9..12; patch warp 13
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kWiStages; ++i) { ptx::mbar_init(full + i, kI2cGather * 32 + 1); ptx::mbar_init(empty + i, 1); }
+        for (int i = 0; i < kWiStages; ++i) { ptx::mbar_init(full + i, kI2cGather * 32 + 1); ptx::mbar_init(empty + i, P.db ? 3 : 1); }
         ptx::mbar_init(tfull, 1);
         ptx::mbar_init(tempty, 4);
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(pfull + i, 1); ptx::mbar_init(pempty + i, kI2cGather * 32); }
@@ -2259,6 +2261,36 @@ __global__ void __launch_bounds__(kWiThreads, 1)
                 }
                 ptx::umma_commit(tfull);
                 tphase ^= 1;
+            }
+        }
+    } else if (warp >= kWiDbWarp) {
+        if (P.db) {   // lane = output-channel pair (32-bit loads), warp = row parity; rows shared by the m tiles
+            const int hw = warp - kWiDbWarp, nst = 2 * P.mtiles;
+            const uint32_t cofs = (uint32_t)((lane & 3) * 4), chunk = (uint32_t)(lane >> 2);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                const int split = item % P.splits, mt = item / P.splits;
+                const int p0 = split * P.per_split, p1 = min(p0 + P.per_split, P.pix_tiles);
+                float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f};
+                for (int pt = p0; pt < p1; ++pt) {
+                    ptx::mbar_wait(full + stage, phase);
+                    const uint32_t base = ptx::smem_u32(smem + stage * kWiStage + 2 * 16384);
+                    int i = 0;
+#pragma unroll 4
+                    for (int r = mt * 2 + hw; r < 128; r += nst, ++i) {
+                        uint32_t w;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(base + r * 128 + ((chunk ^ (r & 7)) << 4) + cofs));
+                        s0[i & 1] += bf_lo(w);
+                        s1[i & 1] += bf_hi(w);
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(empty + stage);
+                    if (++stage == kWiStages) { stage = 0; phase ^= 1; }
+                }
+                const int co = 2 * lane;
+                if (co < P.c_out) atomicAdd(P.db + co, s0[0] + s0[1]);
+                if (co + 1 < P.c_out) atomicAdd(P.db + co + 1, s1[0] + s1[1]);
             }
         }
     } else {
@@ -3115,6 +3147,8 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     const int rows = a.b - a.a;
     TcWgI2c P{};
     P.in = x; P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.ntaps = a.k * a.k; P.mtiles = (P.ntaps + 15) / 16;
+    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
+    P.db = fuse_db && !a.dg ? a.db : nullptr;   // bias / beta (dgamma: the param-grad kernel)
     P.a_mul = a.s; P.c_out = a.c_out;
     for (int ky = 0; ky < a.k; ++ky)
         for (int kx = 0; kx < a.k; ++kx) { P.tap_oy[ky * a.k + kx] = ky - a.p; P.tap_ox[ky * a.k + kx] = kx - a.p; }
@@ -3149,7 +3183,9 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     CUtensorMap D, Pm;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
     if (!encode_patch(&Pm, x, a.B, P.pat_w, P.pat_h)) return false;
-    return launch_wgrad_im2col<64>(P, D, Pm, st);
+    const bool ok = launch_wgrad_im2col<64>(P, D, Pm, st);
+    if (ok && P.db) a.db_done = true;
+    return ok;
 }
 
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
