@@ -27,7 +27,7 @@ python scripts/make_traffic.py gpurun_out/${tag}_traffic.json $caps > /dev/null
 cp gpurun_out/${tag}_traffic.json profiles/traffic.json
 timeout 900 python bench.py > gpurun_out/${tag}_bench_c2.json 2>gpurun_out/${tag}_bench_c2.err
 timeout 900 python bench.py --config c4 > gpurun_out/${tag}_bench_c4.json 2>gpurun_out/${tag}_bench_c4.err
-timeout 900 python bench.py --config c4 --n-bands 16 --no-baselines > gpurun_out/${tag}_bench_c4_16.json 2>gpurun_out/${tag}_bench_c4_16.err
+timeout 900 python bench.py --config c4 --n-bands 4 --no-baselines > gpurun_out/${tag}_bench_c4_4.json 2>gpurun_out/${tag}_bench_c4_4.err
 timeout 900 python bench.py --config c3 --no-baselines > gpurun_out/${tag}_bench_c3.json 2>gpurun_out/${tag}_bench_c3.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${tag}_bench_reference.json 2>&1
 tail -c 300 gpurun_out/${tag}_bench_c2.json; tail -c 300 gpurun_out/${tag}_bench_c4.json
