@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
     const int S = gridDim.x * PY;
     const int q0 = blockIdx.x * PY + py;
     int b = q0 / RW, p = q0 - b * RW;
+    // advance by S pixels: (b, p) += (S / RW, S % RW) with one carry (the stride can span many
+    // images when the band is thin: a repeated-subtraction loop cost S / RW iterations per step)
+    const int Sb = S / RW, Sp = S - Sb * RW;
+    auto advance = [&]() { p += Sp; b += Sb; if (p >= RW) { p -= RW; ++b; } };
     const T *dbase = (const T *)A.dy.p + voff(A.dy, 0, A.a, 0) + c0;
     const T *tbase = A.epi == 2 ? (const T *)A.t.p + voff(A.t, 0, A.a, 0) + c0 : nullptr;
     const T *rbase = A.epi == 2 && A.res.p ? (const T *)A.res.p + voff(A.res, 0, A.a, 0) + c0 : nullptr;
@@ -251,11 +255,10 @@ __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
         const uint4 z = make_uint4(0, 0, 0, 0);
         while (live && b < A.B) {
             const int b0 = b, p0 = p;
-            p += S;
-            while (p >= RW) { p -= RW; ++b; }
+            advance();
             const bool two = b < A.B;
             const int b1 = b, p1 = p;
-            if (two) { p += S; while (p >= RW) { p -= RW; ++b; } }
+            if (two) advance();
             const uint4 d0 = *reinterpret_cast<const uint4 *>(dbase + (long long)b0 * A.dy.bs + (long long)p0 * A.dy.Cp);
             const uint4 d1 = two ? *reinterpret_cast<const uint4 *>(dbase + (long long)b1 * A.dy.bs + (long long)p1 * A.dy.Cp) : z;
             if (A.epi == 2) {
@@ -282,8 +285,7 @@ __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
                 s0[j] += d[j];
                 if (A.epi == 2) s1[j] += d[j] * (t[j] - (rbase ? rr[j] : 0.f));
             }
-            p += S;
-            while (p >= RW) { p -= RW; ++b; }
+            advance();
         }
     }
     if (A.epi == 2) {
