@@ -270,8 +270,7 @@ def main():
         if world > 1 and not rows:
             plan.step_grads(ds.params, ds.grads, ds.x, ds.labels, ds.loss, ds.ws, stream)
             dist.all_reduce(ds.grads)          # wgrad all-reduce (NCCL, fp32, sum)
-            ds.grads.mul_(1.0 / world)
-            plan.sgd(ds.master, ds.params, ds.grads, lr, stream)
+            plan.sgd(ds.master, ds.params, ds.grads, lr / world, stream)   # mean over replicas folded into lr
         else:
             plan.step(ds.master, ds.params, ds.grads, ds.x, ds.labels, lr, ds.loss, ds.ws, stream)
 
