@@ -242,7 +242,22 @@ def main():
     if a.mode == "column":
         kw = {}
     rows = world > 1 and a.parallel == "rows"
-    if rows:
+    # data-parallel replicas over NCCL: the library all-reduces the gradient per segment on its own
+    # stream, overlapped with the backward (LRCNN_FLAG_DP); with gloo (N ranks sharing one GPU, to
+    # exercise the code path) the caller all-reduces after the step
+    lib_dp = world > 1 and not rows and a.backend == "nccl"
+    if lib_dp:
+        try:
+            plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags | LB.FLAG_DP, world=world, rank=rank, **kw)
+            uid = [LB.Comm.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = LB.Comm.nccl(uid[0], rank, world)
+            plan.set_comm(comm)
+        except Exception as e:   # the library's NCCL communicator could not be created: caller all-reduce
+            print("bench: library data-parallel path unavailable (%s); all-reduce after the step" % e, file=sys.stderr)
+            lib_dp = False
+            plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
+    elif rows:
         plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, world=world, rank=rank, **kw)
         uid = [LB.Comm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -267,14 +282,29 @@ def main():
     lr = 1e-3
 
     def one_step():
-        if world > 1 and not rows:
+        if lib_dp:   # sum over replicas inside the step; the mean folded into lr
+            plan.step(ds.master, ds.params, ds.grads, ds.x, ds.labels, lr / world, ds.loss, ds.ws, stream)
+        elif world > 1 and not rows:
             plan.step_grads(ds.params, ds.grads, ds.x, ds.labels, ds.loss, ds.ws, stream)
             dist.all_reduce(ds.grads)          # wgrad all-reduce (NCCL, fp32, sum)
             plan.sgd(ds.master, ds.params, ds.grads, lr / world, stream)   # mean over replicas folded into lr
         else:
             plan.step(ds.master, ds.params, ds.grads, ds.x, ds.labels, lr, ds.loss, ds.ws, stream)
 
-    for _ in range(a.warmup):
+    for i in range(a.warmup):
+        if i == 0 and lib_dp:
+            try:
+                one_step()
+                torch.cuda.synchronize()
+            except Exception as e:   # same workspace layout (DP plans the whole image): switch paths
+                print("bench: library data-parallel step failed (%s); all-reduce after the step" % e, file=sys.stderr)
+                plan.set_comm(None)
+                comm.free()
+                lib_dp = False
+                plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
+                ds.plan = plan
+                one_step()
+            continue
         one_step()
     torch.cuda.synchronize()
     peak = torch.cuda.max_memory_allocated(dev)
@@ -445,7 +475,9 @@ def main():
                "config": {"workload": "%s, batch %d per GPU, bf16" % (CONFIGS[a.config][4], B),
                           "global_batch": gb, "seq_len": None,
                           "parallelism": ("rows%d (row sharding, NCCL halo exchange + all-reduce)" % world if rows
-                                          else "dp%d (wgrad all-reduce)" % world if world > 1 else "single GPU"),
+                                          else "dp%d (per-segment NCCL wgrad all-reduce overlapped with the backward)" % world
+                                          if lib_dp else "dp%d (wgrad all-reduce after the step, %s)" % (world, a.backend)
+                                          if world > 1 else "single GPU"),
                           "mode": a.mode, "segments": a.segments, "bands": kw,
                           "bands_per_segment": [plan.seg(si)[2] for si in range(plan.nsegs())],
                           "fp_bands_per_segment": [plan.fp_bands(si)[0] for si in range(plan.nsegs())],
@@ -458,7 +490,7 @@ def main():
                "roofline": roofline, "memory": mem_rep, "cpu_baseline": cpu,
                "tensor_core_kernels": (not a.simt)}
         print(json.dumps(out), flush=True)
-    if rows:
+    if rows or lib_dp:
         plan.set_comm(None)
         comm.free()
     if world > 1:

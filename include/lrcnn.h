@@ -126,6 +126,13 @@ typedef struct {
  * merged band.  Peak memory is unchanged; results are identical (same kernels, same per-pixel
  * accumulation order).  lrcnn_plan_fp_bands reports N_FP per segment. */
 #define LRCNN_FLAG_FP_MERGE 16
+/* Data-parallel replicas (SURVEY 8(e) "across images"): opts.rank / opts.world name this replica,
+ * every replica plans the whole image (no row split) on its own batch, and lrcnn_step /
+ * lrcnn_step_grads sum the weight gradient over the replicas (the communicator set with
+ * lrcnn_plan_set_comm) in per-segment buckets on a communication stream, each as soon as that
+ * segment's backward is complete, overlapping the rest of the backward; the head gradient after
+ * the head.  The gradient is the SUM over replicas (pass lr / world for the mean). */
+#define LRCNN_FLAG_DP 32
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 

@@ -50,6 +50,7 @@ struct Run {
     cudaStream_t side = nullptr;   // wgrad / param-grad stream (nullptr: everything on st)
     bool side_busy = false;
     bool fp_merged = false;        // FP over merged bands: band tensors live in the FP buffers
+    bool dp_pending = false;       // gradient all-reduces enqueued on the communication stream
 };
 
 // Fork: side stream waits for everything enqueued so far on the main stream.
@@ -657,6 +658,40 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     return LRCNN_OK;
 }
 
+// Data-parallel replicas (LRCNN_FLAG_DP): sum the gradient range [lo, hi) over the replicas on the
+// communication stream once everything enqueued so far on the main stream (the range's last
+// writers) is done; the backward goes on meanwhile.  dp_join makes the main stream wait for the
+// reductions (before the SGD / the caller reads the gradient).
+static lrcnn_status dp_reduce(Run &R, size_t lo, size_t hi) {
+    Plan &P = R.P;
+    if (P.dp_world <= 1 || hi <= lo) return LRCNN_OK;
+    if (!P.comm) return fail(LRCNN_E_STATE, "LRCNN_FLAG_DP with world > 1 needs lrcnn_plan_set_comm");
+    if (!P.comm_stream) {   // created on the first (eager) call, before any graph capture
+        cudaStream_t cs;
+        cudaEvent_t e0, e1;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        P.comm_stream = cs; P.ev_comm = e0; P.ev_comm_done = e1;
+    }
+    cudaStream_t cs = (cudaStream_t)P.comm_stream;
+    CK(cudaEventRecord((cudaEvent_t)P.ev_comm, R.st));
+    CK(cudaStreamWaitEvent(cs, (cudaEvent_t)P.ev_comm, 0));
+    const char *err = nullptr;
+    if (comm_allreduce_f32((Comm *)P.comm, R.grads + lo, hi - lo, cs, &err))
+        return fail(LRCNN_E_NCCL, err ? err : "allreduce failed");
+    R.dp_pending = true;
+    return LRCNN_OK;
+}
+
+static lrcnn_status dp_join(Run &R) {
+    if (!R.dp_pending) return LRCNN_OK;
+    CK(cudaEventRecord((cudaEvent_t)R.P.ev_comm_done, (cudaStream_t)R.P.comm_stream));
+    CK(cudaStreamWaitEvent(R.st, (cudaEvent_t)R.P.ev_comm_done, 0));
+    R.dp_pending = false;
+    return LRCNN_OK;
+}
+
 static lrcnn_status run_backward(Run &R) {
     Plan &P = R.P;
     lrcnn_status st;
@@ -725,6 +760,8 @@ static lrcnn_status run_backward(Run &R) {
         if (P.opts.world > 1 && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, dfull_view(R.ws + P.dfull_off[(s + 1) & 1], P.t[S.in_t]), true)) != LRCNN_OK)
                 return st;
+        // this segment's weight gradient is final (its side-stream work joined at the band ends)
+        if (R.grads && (st = dp_reduce(R, P.seg_grad_lo[s], P.seg_grad_hi[s])) != LRCNN_OK) return st;
     }
     return LRCNN_OK;
 }
@@ -790,8 +827,33 @@ lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     *out = nullptr;
     lrcnn_plan_t *p = new lrcnn_plan_t();
     std::string err;
-    lrcnn_status st = build_plan(net, opts, p->P, err);
+    lrcnn_plan_opts o = opts ? *opts : lrcnn_plan_opts{};
+    const bool dp = opts && (opts->flags & LRCNN_FLAG_DP) && opts->world > 1;
+    if (dp) {   // replicas: every rank plans the whole image; the comm is used for the gradient only
+        if (opts->rank < 0 || opts->rank >= opts->world) { delete p; return fail(LRCNN_E_ARG, "rank out of range"); }
+        o.world = 1;
+        o.rank = 0;
+    }
+    lrcnn_status st = build_plan(net, opts ? &o : nullptr, p->P, err);
     if (st != LRCNN_OK) { delete p; return fail(st, err); }
+    if (dp) { p->P.dp_world = opts->world; p->P.dp_rank = opts->rank; }
+    {   // gradient bucket of every segment: its convolutions' parameters are contiguous (op order)
+        Plan &P = p->P;
+        P.seg_grad_lo.assign(P.seg.size(), 0);
+        P.seg_grad_hi.assign(P.seg.size(), 0);
+        for (size_t si = 0; si < P.seg.size(); ++si) {
+            size_t lo = (size_t)-1, hi = 0;
+            for (int i : P.seg[si].ops) {
+                const OpInfo &oi = P.op[i];
+                if (oi.d.kind != LRCNN_OP_CONV) continue;
+                lo = std::min(lo, oi.w_off);
+                hi = std::max(hi, oi.w_off + oi.w_cnt);
+                if (oi.b_cnt) hi = std::max(hi, oi.b_off + oi.b_cnt);
+                if (oi.beta_cnt) hi = std::max(hi, oi.beta_off + oi.beta_cnt);
+            }
+            if (lo != (size_t)-1) { P.seg_grad_lo[si] = lo; P.seg_grad_hi[si] = hi; }
+        }
+    }
     p->P.use_tc = p->P.opts.prec == LRCNN_BF16 && !(p->P.opts.flags & LRCNN_FLAG_NO_TCGEN05) && tc_available();
     *out = p;
     return LRCNN_OK;
@@ -855,6 +917,9 @@ lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan) {
     if (plan) {
         for (int g = 0; g < 2; ++g)
             if (plan->P.graph_exec[g]) cudaGraphExecDestroy((cudaGraphExec_t)plan->P.graph_exec[g]);
+        if (plan->P.comm_stream) cudaStreamDestroy((cudaStream_t)plan->P.comm_stream);
+        if (plan->P.ev_comm) cudaEventDestroy((cudaEvent_t)plan->P.ev_comm);
+        if (plan->P.ev_comm_done) cudaEventDestroy((cudaEvent_t)plan->P.ev_comm_done);
         if (plan->P.side_stream) {
             cudaStreamSynchronize((cudaStream_t)plan->P.side_stream);
             cudaStreamDestroy((cudaStream_t)plan->P.side_stream);
@@ -1013,6 +1078,7 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
     ++P.launches;
     if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     st = run_backward(R);
+    if (st == LRCNN_OK) st = dp_join(R);
     if (st == LRCNN_OK && P.opts.world > 1) {
         const char *err = nullptr;
         if (comm_allreduce_f32((Comm *)P.comm, grads, P.head_w_off, R.st, &err))
@@ -1048,7 +1114,9 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
                  R.params + P.head_w_off * R.E, R.params + P.head_b_off * R.E, labels, scratch, loss_dev,
                  grads + P.head_w_off, grads + P.head_b_off, w + P.dfull_off[slast & 1], z.relu, hw, R.st));
     P.launches += 3;
+    if ((st = dp_reduce(R, P.head_w_off, P.head_b_off + P.head_b_cnt)) != LRCNN_OK) return st;
     st = run_backward(R);
+    if (st == LRCNN_OK) st = dp_join(R);
     if (st == LRCNN_OK && P.opts.world > 1) {   // wgrad all-reduce (the conv parameters precede the head)
         const char *err = nullptr;
         if (comm_allreduce_f32((Comm *)P.comm, grads, P.head_w_off, R.st, &err))
@@ -1070,7 +1138,9 @@ lrcnn_status lrcnn_step_grads(lrcnn_plan_t *plan, const void *params, float *gra
 
 lrcnn_status lrcnn_plan_set_comm(lrcnn_plan_t *plan, lrcnn_comm *comm) {
     if (!plan) return fail(LRCNN_E_ARG, "plan is NULL");
-    if (comm && (comm_world((Comm *)comm) != plan->P.opts.world || comm_rank((Comm *)comm) != plan->P.opts.rank))
+    const Plan &P = plan->P;
+    const int world = P.dp_world > 1 ? P.dp_world : P.opts.world, rank = P.dp_world > 1 ? P.dp_rank : P.opts.rank;
+    if (comm && (comm_world((Comm *)comm) != world || comm_rank((Comm *)comm) != rank))
         return fail(LRCNN_E_ARG, "communicator rank/world differ from the plan's");
     plan->P.comm = comm;
     return LRCNN_OK;

@@ -125,6 +125,11 @@ struct Plan {
     long long graph_launches[2] = {0, 0}, graph_tc_launches[2] = {0, 0};
     // side stream for wgrad / parameter reductions (overlap with the dgrad chain) and its events
     void *side_stream = nullptr, *ev_fork = nullptr, *ev_join = nullptr;
+    // data-parallel replicas (LRCNN_FLAG_DP): replica count / index, per-segment gradient buckets
+    // [seg_grad_lo, seg_grad_hi) (flat parameter offsets), the communication stream and its events
+    int dp_world = 1, dp_rank = 0;
+    std::vector<size_t> seg_grad_lo, seg_grad_hi;
+    void *comm_stream = nullptr, *ev_comm = nullptr, *ev_comm_done = nullptr;
 };
 
 // Builds the plan; returns status and fills err on failure.

@@ -23,6 +23,7 @@ FLAG_NO_TCGEN05 = 2
 FLAG_BALANCED_BANDS = 4
 FLAG_NO_FUSE_RES = 8
 FLAG_FP_MERGE = 16
+FLAG_DP = 32
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 

@@ -114,3 +114,60 @@ def test_sharded_resnet_bf16_vs_single_rank():
                 continue
             for k in b:
                 assert rel(a[k], b[k]) <= 2e-2, (rank, i, k, rel(a[k], b[k]))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_dp_replicas_sum_gradients(prec):
+    """Data-parallel replicas (LRCNN_FLAG_DP): two replicas (loopback communicator, one host thread
+    and stream each) on different batches; the per-segment gradient buckets are all-reduced on the
+    communication stream while the backward goes on.  Every replica's gradient must equal the sum
+    of the two single-replica gradients, and its loss its own batch's loss."""
+    net = WL.resnet50(H=64, W=32, width_div=4, blocks=(2, 1, 1, 1)) if prec == "bf16" else \
+        WL.vgg16(H=32, W=32, width_div=8, segments="pool")
+    B = 2
+    bf = prec == "bf16"
+    params = WL.make_params(net, seed=3, bias_scale=0.05, bf16=bf)
+    xs = [WL.make_input(net, B, seed=10 + g, bf16=bf) for g in range(2)]
+    labs = [WL.make_labels(net, B, seed=20 + g) for g in range(2)]
+    single = []
+    for g in range(2):
+        p = LB.Plan(net, B, mode="2ps", prec=prec, n_bands=3)
+        ds = LB.DeviceState(p)
+        ds.load(params=params, x=xs[g], labels=labs[g])
+        ds.step_grads()
+        torch.cuda.synchronize()
+        single.append((float(ds.loss.cpu()), ds.grads.cpu().numpy().copy()))
+    comms = LB.Comm.loopback(2)
+    plans, states = [], []
+    for g in range(2):
+        p = LB.Plan(net, B, mode="2ps", prec=prec, n_bands=3, world=2, rank=g, flags=LB.FLAG_DP)
+        p.set_comm(comms[g])
+        ds = LB.DeviceState(p)
+        ds.load(params=params, x=xs[g], labels=labs[g])
+        plans.append(p)
+        states.append(ds)
+    torch.cuda.synchronize()
+    errs = [None] * 2
+
+    def body(g):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                states[g].step_grads(stream=st)
+            st.synchronize()
+        except Exception as e:   # surfaced below
+            errs[g] = e
+
+    th = [threading.Thread(target=body, args=(g,)) for g in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert all(e is None for e in errs), errs
+    ref = single[0][1] + single[1][1]
+    for g in range(2):
+        got = states[g].grads.cpu().numpy()
+        assert rel(got, ref) <= 1e-5, (g, rel(got, ref))
+        assert abs(float(states[g].loss.cpu()) - single[g][0]) <= 1e-6 * max(1.0, abs(single[g][0]))
+    for c in comms:
+        c.free()
