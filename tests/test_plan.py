@@ -350,3 +350,21 @@ def test_fp_merge_bands(which):
                 for t in range(t_in + 1, t_out + 1):
                     assert p0.rows(s, r, t) == p1.rows(s, r, t)
         assert merged > 0, nb
+
+
+def test_dp_replica_plan_is_the_single_gpu_plan():
+    """LRCNN_FLAG_DP: a replica plans the whole image (no row split): same bands, rows and workspace
+    as the single-GPU plan, for every rank; an out-of-range rank is rejected."""
+    net = WL.resnet50(H=96, W=64, width_div=8, blocks=(1, 1, 1, 1))
+    p0 = LB.Plan(net, 2, mode="2ps", prec="bf16", n_bands=3)
+    for rank in range(4):
+        p = LB.Plan(net, 2, mode="2ps", prec="bf16", n_bands=3, world=4, rank=rank, flags=LB.FLAG_DP)
+        assert p.ws_bytes == p0.ws_bytes and p.nsegs() == p0.nsegs()
+        for s in range(p.nsegs()):
+            assert p.seg(s) == p0.seg(s)
+            t_in, t_out, n = p.seg(s)
+            for r in range(n):
+                for t in range(t_in + 1, t_out + 1):
+                    assert p.rows(s, r, t) == p0.rows(s, r, t)
+    with pytest.raises(LB.LrcnnError):
+        LB.Plan(net, 2, mode="2ps", prec="bf16", n_bands=3, world=4, rank=4, flags=LB.FLAG_DP)
