@@ -35,7 +35,8 @@ def run(net, B, mode, params, x, dzl, flags=0, **kw):
 
 @pytest.mark.parametrize("cin,cout,H,W,k,p", [(64, 64, 20, 37, 3, 1), (64, 128, 9, 16, 3, 1),
                                               (128, 256, 7, 7, 3, 1), (256, 512, 5, 11, 3, 1),
-                                              (64, 64, 13, 29, 1, 0), (64, 192, 12, 40, 3, 0)])
+                                              (64, 64, 13, 29, 1, 0), (64, 192, 12, 40, 3, 0),
+                                              (256, 128, 9, 23, 1, 0), (512, 256, 6, 17, 1, 0)])
 def test_two_conv_layers_vs_oracle(cin, cout, H, W, k, p):
     """conv(8->cin) [SIMT] then conv(cin->cout) [tcgen05 FP, dgrad into the first layer's delta,
     wgrad]; bands of 3 rows (2PS) and one band (column)."""
