@@ -1113,7 +1113,7 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
     CK(head_tail(P.opts.prec, R.zl, P.net.B, z.ck_rows * z.W, z.Cp, z.C, P.net.n_classes,
                  R.params + P.head_w_off * R.E, R.params + P.head_b_off * R.E, labels, scratch, loss_dev,
                  grads + P.head_w_off, grads + P.head_b_off, w + P.dfull_off[slast & 1], z.relu, hw, R.st));
-    P.launches += 3;
+    P.launches += 4;   // gap, logits, FC grad, delta^L
     if ((st = dp_reduce(R, P.head_w_off, P.head_b_off + P.head_b_cnt)) != LRCNN_OK) return st;
     st = run_backward(R);
     if (st == LRCNN_OK) st = dp_join(R);

@@ -502,49 +502,61 @@ __global__ void k_gap(const T *zl, int HW, int Cp, float *gap, float hw_div) {
     gap[(long long)b * Cp + c] = s / hw_div;
 }
 
+// Head: FC -> softmax-CE (mean over B) -> d logits -> FC gradients.  k_fc_logits has one block per
+// image (warps over classes, lanes over channels) and writes that image's d logits and loss term;
+// k_fc_grad spreads the FC weight gradient over (class, channel) threads and sums the loss.
 template <typename T>
-__global__ void k_fc_ce(const float *gap, int B, int Cp, int C, int classes, const T *fw, const T *fb,
-                        const int32_t *labels, float *dlog, float *loss, float *gw, float *gb) {
+__global__ void k_fc_logits(const float *gap, int B, int Cp, int C, int classes, const T *fw, const T *fb,
+                            const int32_t *labels, float *dlog, float *lossb) {
     griddep_wait();   // PDL: previous kernel complete and visible
     griddep_launch();
-    extern __shared__ float sh[];   // logits [B*classes]
-    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int i = threadIdx.x >> 5; i < B * classes; i += nw) {   // one warp per (image, class)
-        const int b = i / classes, j = i % classes;
+    extern __shared__ float lg[];   // logits of this image [classes]
+    const int b = blockIdx.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int j = threadIdx.x >> 5; j < classes; j += nw) {
         float s = 0.f;
         for (int c = lane; c < C; c += 32) s += gap[(long long)b * Cp + c] * ldf(fw + (long long)j * Cp + c);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) sh[i] = s + ldf(fb + j);
+        if (lane == 0) lg[j] = s + ldf(fb + j);
     }
     __syncthreads();
-    __shared__ float lsum;
-    if (threadIdx.x == 0) lsum = 0.f;
-    __syncthreads();
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (threadIdx.x == 0) {
         float m = -INFINITY;
-        for (int j = 0; j < classes; ++j) m = fmaxf(m, sh[b * classes + j]);
+        for (int j = 0; j < classes; ++j) m = fmaxf(m, lg[j]);
         float se = 0.f;
-        for (int j = 0; j < classes; ++j) se += expf(sh[b * classes + j] - m);
-        int lab = labels[b];
-        atomicAdd(&lsum, (m + logf(se)) - sh[b * classes + lab]);
+        for (int j = 0; j < classes; ++j) se += expf(lg[j] - m);
+        const int lab = labels[b];
+        lossb[b] = (m + logf(se)) - lg[lab];
         for (int j = 0; j < classes; ++j)
-            dlog[b * classes + j] = (expf(sh[b * classes + j] - m) / se - (j == lab ? 1.f : 0.f)) / B;
+            dlog[b * classes + j] = (expf(lg[j] - m) / se - (j == lab ? 1.f : 0.f)) / B;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) *loss = lsum / B;
-    for (int i = threadIdx.x; i < classes * C; i += blockDim.x) {
-        int j = i / C, c = i % C;
+}
+template <typename T>
+__global__ void k_fc_grad(const float *gap, int B, int Cp, int C, int classes, const float *dlog, const float *lossb,
+                          float *loss, float *gw, float *gb) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < classes * C) {
+        const int j = i / C, c = i - j * C;
         float s = 0.f;
         for (int b = 0; b < B; ++b) s += dlog[b * classes + j] * gap[(long long)b * Cp + c];
         gw[(long long)j * Cp + c] += s;
     }
-    for (int j = threadIdx.x; j < classes; j += blockDim.x) {
-        float s = 0.f;
-        for (int b = 0; b < B; ++b) s += dlog[b * classes + j];
-        gb[j] += s;
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < classes) {
+            float s = 0.f;
+            for (int b = 0; b < B; ++b) s += dlog[b * classes + threadIdx.x];
+            gb[threadIdx.x] += s;
+        }
+        if (threadIdx.x == 0) {
+            float l = 0.f;
+            for (int b = 0; b < B; ++b) l += lossb[b];
+            *loss = l / B;
+        }
     }
 }
+
 
 template <typename T>
 __global__ void k_dzl(const T *zl, const float *dlog, const T *fw, int B, int HW, int Cp, int C, int classes,
@@ -1182,12 +1194,14 @@ cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_d
 cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, int classes, const void *fc_w,
                       const void *fc_b, const int32_t *labels, float *scratch, float *loss, float *g_fc_w,
                       float *g_fc_b, void *dzl, int gate, float hw_div, cudaStream_t st) {
-    float *gap = scratch, *dlog = scratch + (long long)B * Cp;
-    size_t shm = sizeof(float) * B * classes;
+    float *gap = scratch, *dlog = scratch + (long long)B * Cp, *lossb = dlog + (long long)B * classes;
     long long n = (long long)B * HW * Cp;
+    const unsigned gblocks = (unsigned)((classes * C + kT - 1) / kT);
     if (prec) {
-        launch_simt(k_fc_ce<bf16>, 1, 1024, shm, st, gap, B, Cp, C, classes, (const bf16 *)fc_w, (const bf16 *)fc_b, labels,
-                                            dlog, loss, g_fc_w, g_fc_b);
+        launch_simt(k_fc_logits<bf16>, B, 256, sizeof(float) * classes, st, gap, B, Cp, C, classes, (const bf16 *)fc_w,
+                    (const bf16 *)fc_b, labels, dlog, lossb);
+        launch_simt(k_fc_grad<bf16>, gblocks, kT, 0, st, gap, B, Cp, C, classes, (const float *)dlog,
+                    (const float *)lossb, loss, g_fc_w, g_fc_b);
         if (n > 0 && Cp % 8 == 0 && B <= 65535) {
             const long long nv = (long long)HW * Cp / 8;
             long long gx = (nv + kT * 4 - 1) / (kT * 4);
@@ -1199,8 +1213,10 @@ cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, in
             launch_simt(k_dzl<bf16>, grid_for(n), kT, 0, st, (const bf16 *)zl, dlog, (const bf16 *)fc_w, B, HW, Cp, C, classes,
                                                    (bf16 *)dzl, gate, hw_div);
     } else {
-        launch_simt(k_fc_ce<float>, 1, 1024, shm, st, gap, B, Cp, C, classes, (const float *)fc_w, (const float *)fc_b,
-                                             labels, dlog, loss, g_fc_w, g_fc_b);
+        launch_simt(k_fc_logits<float>, B, 256, sizeof(float) * classes, st, gap, B, Cp, C, classes,
+                    (const float *)fc_w, (const float *)fc_b, labels, dlog, lossb);
+        launch_simt(k_fc_grad<float>, gblocks, kT, 0, st, gap, B, Cp, C, classes, (const float *)dlog,
+                    (const float *)lossb, loss, g_fc_w, g_fc_b);
         if (n > 0)
             launch_simt(k_dzl<float>, grid_for(n), kT, 0, st, (const float *)zl, dlog, (const float *)fc_w, B, HW, Cp, C,
                                                     classes, (float *)dzl, gate, hw_div);

@@ -427,7 +427,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         P.xstage_off[1] = P.xstage_off[0] + 2 * xmax;
         M.other += 4 * xmax;
     }
-    P.head_off = alloc(sizeof(float) * (B * zl.Cp + B * net->n_classes + 64));
+    P.head_off = alloc(sizeof(float) * (B * zl.Cp + B * net->n_classes + B + 64));   // gap, d logits, loss terms
     P.flag_off = alloc(256);
     M.other += ws - (P.head_off);
     {
