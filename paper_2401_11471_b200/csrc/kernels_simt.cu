@@ -1067,9 +1067,10 @@ cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
     long long n = (long long)a.B * (a.b - a.a) * a.out.W * a.out.Cp;
     if (n <= 0) return cudaSuccess;
     if (pool2(a, a.out)) {
-        const int rowv = a.out.W * (a.out.Cp / 8);
-        dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
-        if (prec) launch_simt(k_pool2_fwd<bf16>, g, kT, 0, st, a); else launch_simt(k_pool2_fwd<float>, g, kT, 0, st, a);
+        // 128-thread blocks: a VGG output row is 896 channel vectors (7 x 128, no idle tail)
+        const int rowv = a.out.W * (a.out.Cp / 8), tb = 128;
+        dim3 g((rowv + tb - 1) / tb, a.B * (a.b - a.a));
+        if (prec) launch_simt(k_pool2_fwd<bf16>, g, tb, 0, st, a); else launch_simt(k_pool2_fwd<float>, g, tb, 0, st, a);
     } else if (a.out.Cp % 8 == 0) {
         n /= 8;
         if (prec) launch_simt(k_pool_fwd8<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_fwd8<float>, grid_for(n), kT, 0, st, a);
@@ -1096,9 +1097,9 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     if (pool2(a, a.dy)) {
         if (a.b <= a.a) return cudaSuccess;
-        const int rowv = a.dy.W * (a.dy.Cp / 8);
-        dim3 g((rowv + kT - 1) / kT, a.B * (a.b - a.a));
-        if (prec) launch_simt(k_pool2_bwd<bf16>, g, kT, 0, st, a); else launch_simt(k_pool2_bwd<float>, g, kT, 0, st, a);
+        const int rowv = a.dy.W * (a.dy.Cp / 8), tb = 128;
+        dim3 g((rowv + tb - 1) / tb, a.B * (a.b - a.a));
+        if (prec) launch_simt(k_pool2_bwd<bf16>, g, tb, 0, st, a); else launch_simt(k_pool2_bwd<float>, g, tb, 0, st, a);
     } else if (prec && a.k == 3 && a.s == 2 && a.p == 1 && a.dx.Cp % 8 == 0 && a.dx.Cp == a.dy.Cp && a.B <= 65535) {
         const size_t shm = (size_t)2 * (kP3TR / 2 + 2) * (kP3TP + 1) * (a.dy.Cp / 8) * 16;
         dim3 g((a.dx.W + 2 * kP3TP - 1) / (2 * kP3TP), (a.rb - a.ra + kP3TR - 1) / kP3TR, a.B);
