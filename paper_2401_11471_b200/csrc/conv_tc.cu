@@ -2116,6 +2116,8 @@ struct TcWgI2c {
     int out_a, out_b, Wo, dy_base;
     int pat_w, pat_h, pat_ox, pat_oy, in_base;
     float *db;             // fused bias / beta gradient (two extra warps sum the delta tiles)
+    float *dg;             // fused gamma gradient (epilogue: warp sums of W * dW_raw)
+    const bf16 *w;
 };
 static constexpr int kWiStages = 4;
 static constexpr int kWiStage = 2 * 16384 + 16384;                 // A: 2 chunks x 16 KB, B: 16 KB
@@ -2302,20 +2304,42 @@ __global__ void __launch_bounds__(kWiThreads, 1)
             const int tap = mt * 16 + (m >> 3), ci = m & 7;
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
+            float dgacc[BN / 32];   // fused dgamma: lane L keeps channel c * 32 + L's warp partial
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) dgacc[c] = 0.f;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
                 ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + c * 32, v);
                 ptx::tmem_ld_wait();
-                if (tap >= P.ntaps) continue;
+                if (tap < P.ntaps) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int co = c * 32 + j;
-                    if (co < P.c_out) {
-                        const float g = P.gamma ? __bfloat162float(P.gamma[co]) : 1.f;
-                        atomicAdd(P.dw + ((long long)co * P.ntaps + tap) * 8 + ci, __uint_as_float(v[j]) * g);
+                    for (int j = 0; j < 32; ++j) {
+                        const int co = c * 32 + j;
+                        if (co < P.c_out) {
+                            const float g = P.gamma ? __bfloat162float(P.gamma[co]) : 1.f;
+                            atomicAdd(P.dw + ((long long)co * P.ntaps + tap) * 8 + ci, __uint_as_float(v[j]) * g);
+                        }
                     }
                 }
+                if (P.dg) {   // dgamma[co] = sum_{tap,ci} W * (sum_p dy x): warp sum per co (all lanes shuffle)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int co = c * 32 + j;
+                        float pj = tap < P.ntaps && co < P.c_out
+                                       ? __uint_as_float(v[j]) *
+                                             __bfloat162float(P.w[((long long)co * P.ntaps + tap) * 8 + ci])
+                                       : 0.f;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) pj += __shfl_xor_sync(0xffffffffu, pj, o);
+                        if (lane == j) dgacc[c] += pj;
+                    }
+                }
+            }
+            if (P.dg) {
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c)
+                    if (c * 32 + lane < P.c_out) atomicAdd(P.dg + c * 32 + lane, dgacc[c]);
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -3148,7 +3172,10 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     TcWgI2c P{};
     P.in = x; P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.ntaps = a.k * a.k; P.mtiles = (P.ntaps + 15) / 16;
     static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
-    P.db = fuse_db && !a.dg ? a.db : nullptr;   // bias / beta (dgamma: the param-grad kernel)
+    P.db = fuse_db ? a.db : nullptr;            // bias / beta (dedicated warps), dgamma (epilogue)
+    P.dg = fuse_db && a.db ? a.dg : nullptr;
+    P.w = (const bf16 *)a.w;
+    if (P.dg && !P.w) P.db = P.dg = nullptr;
     P.a_mul = a.s; P.c_out = a.c_out;
     for (int ky = 0; ky < a.k; ++ky)
         for (int kx = 0; kx < a.k; ++kx) { P.tap_oy[ky * a.k + kx] = ky - a.p; P.tap_ox[ky * a.k + kx] = kx - a.p; }

@@ -103,13 +103,15 @@ def test_tc_matches_simt():
                 assert rel(a[key], b[key]) <= TOL, key
 
 
-@pytest.mark.parametrize("k,s,p,H,W", [(3, 1, 1, 37, 45), (7, 2, 3, 41, 53), (3, 2, 1, 30, 34), (5, 1, 2, 19, 70)])
-def test_image_layer_vs_oracle(k, s, p, H, W):
+@pytest.mark.parametrize("k,s,p,H,W,epi", [(3, 1, 1, 37, 45, "bias"), (7, 2, 3, 41, 53, "bias"), (3, 2, 1, 30, 34, "bias"),
+                                          (5, 1, 2, 19, 70, "bias"), (7, 2, 3, 41, 53, "affine")])
+def test_image_layer_vs_oracle(k, s, p, H, W, epi):
     """The RGB input layer (8 padded channels -> 64): FP through the tap-pair kernel (k_conv_pair,
     stride 1 and 2, descriptors straight into the TMA-loaded patch), wgrad through the patch-gather
-    im2col kernel; several bands, ragged rows and columns."""
+    im2col kernel with the bias / beta (dedicated warps) and gamma (epilogue warp sums) gradients
+    fused; several bands, ragged rows and columns."""
     net = {"C": 3, "H": H, "W": W, "classes": 10,
-           "ops": [WL.conv(0, 64, k, s, p), WL.conv(1, 64, 3, 1, 1)]}
+           "ops": [WL.conv(0, 64, k, s, p, epi=epi), WL.conv(1, 64, 3, 1, 1)]}
     B = 3
     params = WL.make_params(net, seed=11, bias_scale=0.1, bf16=True)
     x = WL.make_input(net, B, seed=6, bf16=True)
