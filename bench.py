@@ -1,15 +1,17 @@
 #!/usr/bin/env python
-"""bench.py -- row-centric VGG-16 training throughput on B200 (BASELINE.json configs[1]).
+"""bench.py -- row-centric ResNet-50 training on climate-scale images on B200 (the north star).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
 
 One step = one lrcnn_step (Alg. 1 l.5-24: row-centric FP, head, row-centric BP with
-recompute, SGD) over one batch of synthetic input; workload C2: VGG-16 conv stack,
-224x224x3, batch 32 per GPU, bf16, 2PS-H (2PS bands inside per-pool checkpoint
-segments).  N>1: one process per GPU (torchrun), each rank trains its own batch
-(weak scaling) and the fp32 gradients are all-reduced with NCCL before SGD.
-Prints ONE JSON line (rank 0).  --impl reference times the fp64 CPU oracle (the
-reference arm of this tier) on a bounded sample of the same workload.
+recompute, SGD) over one batch of synthetic input.  Default workload C4 (BASELINE.json
+configs[3], the north star): ResNet-50 v1.5 on 3600x2400x3 images, batch 8, bf16, 2PS-H
+(2PS bands inside per-stage checkpoint segments), tcgen05 kernels only.  N>1: one process
+per GPU (torchrun); the same batch's rows are split across the ranks (--parallel rows,
+default: NCCL halo exchange at every segment input + GAP / wgrad all-reduce, strong
+scaling); --parallel dp gives data-parallel replicas (weak scaling).  C2 / C3 / C5 are
+selectable with --config.  Prints ONE JSON line (rank 0).  --impl reference times the fp64
+CPU oracle (the reference arm of this tier) on a bounded sample of the same workload.
 """
 import argparse
 import json
@@ -26,7 +28,7 @@ sys.path.insert(0, ROOT)
 
 import workloads as WL  # noqa: E402
 
-METRIC = "train images/s (row-centric 2PS-H, bf16)"
+METRIC = "train images/s (row-centric 2PS-H, bf16) + peak feature-map HBM vs layer-wise"
 UNIT = "images/s"
 
 
@@ -36,9 +38,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
-                    help="BASELINE.json configs: c2 VGG-16 224^2 B32 (default), c3 ResNet-50 224^2 B256, "
-                         "c4 ResNet-50 3600x2400 B8, c5 VGG-16 2048^2 B16")
+    ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4", "c5"],
+                    help="BASELINE.json configs: c4 ResNet-50 3600x2400 B8 (default, the north star), c2 VGG-16 "
+                         "224^2 B32, c3 ResNet-50 224^2 B256, c5 VGG-16 2048^2 B16")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--hw", type=int, default=0)
     ap.add_argument("--mode", default="2ps", choices=["2ps", "overl", "column"])
@@ -49,7 +51,8 @@ def parse():
     ap.add_argument("--band-rows", type=int, default=0)
     ap.add_argument("--mem-budget-gb", type=float, default=0.0,
                     help="budget-driven planning: the smallest band count whose workspace fits (lrcnn_plan_budget)")
-    ap.add_argument("--no-baselines", action="store_true", help="skip column-mode memory and cpu baseline")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the layer-wise memory and cpu baselines")
+    ap.add_argument("--no-eager", action="store_true", help="skip the PyTorch-eager layer-wise context run")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
     ap.add_argument("--no-fp-merge", action="store_true",
                     help="forward pass on the BP bands (default: merged FP bands, LRCNN_FLAG_FP_MERGE)")
@@ -58,9 +61,9 @@ def parse():
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group backend; gloo only to exercise the N>1 code path on one GPU")
-    ap.add_argument("--parallel", default="dp", choices=["dp", "rows"],
-                    help="N>1: dp = each rank its own batch, wgrad all-reduce (weak scaling); rows = the "
-                         "same batch row-sharded across ranks with halo exchange (strong scaling, SURVEY 8(e))")
+    ap.add_argument("--parallel", default="rows", choices=["dp", "rows"],
+                    help="N>1: rows = the same batch row-sharded across ranks with NCCL halo exchange (default, "
+                         "the north star's split, SURVEY 8(e)); dp = each rank its own batch, wgrad all-reduce")
     return ap.parse_args()
 
 
@@ -143,37 +146,133 @@ def make_net(a):
 
 
 def cpu_baseline(a, steps=1):
-    """The fp64 oracle (column dataflow, as it stands) on a bounded sample: one image of the
-    workload at full 224x224, one training step (FP, head, BP, SGD), all host cores."""
+    """The fp64 oracle (column dataflow, as it stands) on a bounded sample of the workload: one
+    training step (FP, head, BP, SGD) on one image (C2 / C3) or on a full-width strip of one image
+    (C4 / C5, images/s extrapolated by strip / H), on all host cores and on 1 thread (a smaller
+    strip, so the default run stays within minutes)."""
     import oracle
     from oracle import column as C
     cores = os.cpu_count() or 1
+
+    def run(threads, strip):
+        oracle.set_threads(threads)
+        net, scale, what = oracle_sample(a, strip)
+        params = WL.make_params(net, seed=2)
+        x = WL.make_input(net, 1, seed=0)
+        lab = WL.make_labels(net, 1)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            params, loss, _, _, _ = C.step(net, params, x, lab, 0.01)
+            times.append(time.perf_counter() - t0)
+        return scale / statistics.mean(times), what
+    v, what = run(cores, 224)
+    v1, what1 = run(1, 32)
     oracle.set_threads(cores)
-    net, scale, what = oracle_sample(a)
-    params = WL.make_params(net, seed=2)
-    x = WL.make_input(net, 1, seed=0)
-    lab = WL.make_labels(net, 1)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        params, loss, _, _, _ = C.step(net, params, x, lab, 0.01)
-        times.append(time.perf_counter() - t0)
-    return {"value": scale / statistics.mean(times), "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": "%s, one fp64 column step (FP+head+BP+SGD), OpenMP over (b, c_out), mean of %d"
                       % (what, steps),
-            "s_per_image": statistics.mean(times) / scale}
+            "s_per_image": 1.0 / v,
+            "one_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": what1}}
 
 
-def oracle_sample(a):
+def oracle_sample(a, strip=224):
     """Bounded CPU sample of the workload: one full image for C2/C3; for the climate-scale
-    configs one full-width strip of 224 image rows (images/s extrapolated by strip/H)."""
+    configs one full-width strip of `strip` image rows (images/s extrapolated by strip/H)."""
     net = make_net(a)
     if net["H"] * net["W"] <= 512 * 512:
         return net, 1.0, "1 image of the %s batch" % a.config.upper()
-    strip = 224
     sub = dict(net, H=strip)
     return sub, strip / net["H"], ("1 image strip of %d rows x full width %d of %s (extrapolated x%d/%d)"
                                    % (strip, net["W"], a.config.upper(), strip, net["H"]))
+
+
+def eager_layerwise(net, B, params, x_np, lab_np, dev, steps=3):
+    """External layer-wise context: the same DAG trained layer by layer in PyTorch
+    eager mode -- bf16 channels_last cuDNN convolutions, frozen-BN affine, residual adds, max-pool,
+    GAP -> FC -> CE, autograd keeping whatever it keeps, plain SGD.  Returns its peak allocated HBM
+    and images/s (CUDA events), or {"error": ...} (e.g. out of memory).  Not our product path."""
+    import torch
+    import torch.nn.functional as F
+    try:
+        torch.cuda.empty_cache()
+        base = torch.cuda.memory_allocated(dev)
+        dt = torch.bfloat16
+        ws = []
+        for i, op in enumerate(net["ops"]):
+            if op["kind"] != "conv":
+                ws.append(None)
+                continue
+            p = params["convs"][i]
+            d = {"w": torch.tensor(p["w"], dtype=dt, device=dev).contiguous(memory_format=torch.channels_last)}
+            for k in ("b", "gamma", "beta"):
+                if k in p:
+                    d[k] = torch.tensor(p[k], dtype=dt, device=dev)
+            for v in d.values():
+                v.requires_grad_(True)
+            ws.append(d)
+        fw = torch.tensor(params["head"]["fc_w"], dtype=dt, device=dev, requires_grad=True)
+        fb = torch.tensor(params["head"]["fc_b"], dtype=dt, device=dev, requires_grad=True)
+        leaves = [v for d in ws if d for v in d.values()] + [fw, fb]
+        x = torch.tensor(x_np, dtype=dt, device=dev).contiguous(memory_format=torch.channels_last)
+        lab = torch.tensor(lab_np, dtype=torch.long, device=dev)
+
+        def step():
+            ts = [x]
+            for i, op in enumerate(net["ops"]):
+                src = ts[op["src"]]
+                if op["kind"] == "conv":
+                    y = F.conv2d(src, ws[i]["w"], None, op["s"], op["p"])
+                    if op["epi"] == "bias":
+                        y = y + ws[i]["b"].view(1, -1, 1, 1)
+                    elif op["epi"] == "affine":
+                        y = y * ws[i]["gamma"].view(1, -1, 1, 1) + ws[i]["beta"].view(1, -1, 1, 1)
+                    if op["res"] >= 0:
+                        y = y + ts[op["res"]]
+                    if op["relu"]:
+                        y = F.relu(y)
+                elif op["kind"] == "maxpool":
+                    y = F.max_pool2d(src, op["k"], op["s"], op["p"])
+                else:
+                    y = src + ts[op["res"]]
+                    if op["relu"]:
+                        y = F.relu(y)
+                ts.append(y)
+            logits = F.linear(ts[-1].float().mean(dim=(2, 3)), fw.float(), fb.float())
+            loss = F.cross_entropy(logits, lab)
+            loss.backward()
+            with torch.no_grad():
+                for v in leaves:
+                    v -= 1e-3 * v.grad
+                    v.grad = None
+            return loss
+
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
+        step()
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated(dev) - base
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        param_bytes = sum(v.numel() * v.element_size() for v in leaves)
+        x_bytes = x.numel() * x.element_size()
+        out = {"peak_allocated_bytes": peak, "feature_map_bytes": peak - param_bytes - x_bytes,
+               "images_per_s": B / (ms / 1000.0), "ms_per_step": ms,
+               "what": "PyTorch %s eager, bf16 channels_last cuDNN, autograd, same DAG (frozen-BN affine), "
+                       "SGD; feature maps = peak - params - input" % torch.__version__}
+    except torch.cuda.OutOfMemoryError as e:
+        out = {"error": "out of memory: %s" % str(e).split("\n")[0][:200]}
+    except Exception as e:   # context only: never fail the bench on it
+        out = {"error": repr(e)[:300]}
+    finally:
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_reference(a):
@@ -183,7 +282,7 @@ def run_reference(a):
     cb = cpu_baseline(a, steps=1)             # warm-up/first measurement
     import oracle
     from oracle import column as C
-    net, scale, what = oracle_sample(a)
+    net, scale, what = oracle_sample(a, 96)
     params = WL.make_params(net, seed=2)
     x = WL.make_input(net, 1, seed=0)
     lab = WL.make_labels(net, 1)
@@ -233,7 +332,7 @@ def main():
 
     net = make_net(a)
     B = a.batch or CONFIGS[a.config][3]
-    flags = (LB.FLAG_NO_TCGEN05 if a.simt else 0) | (0 if a.no_balanced else LB.FLAG_BALANCED_BANDS)
+    flags = (LB.FLAG_NO_TCGEN05 if a.simt else LB.FLAG_REQUIRE_TC) | (0 if a.no_balanced else LB.FLAG_BALANCED_BANDS)
     if not a.no_fp_merge:   # decoupled FP bands (N_FP < N_BP, same peak memory)
         flags |= LB.FLAG_FP_MERGE
     if a.n_bands is None:
@@ -402,7 +501,12 @@ def main():
     plan.profile(False)
     peaks, peak_src = measured_peaks()
     achieved = tc_fl / (tc_ms / 1000.0) / 1e12 if tc_ms > 0 else 0.0
-    peak_tf = peaks.get("bf16_tflops_sustained", 1385.7)
+    # the burst bf16 peak when the SM clock sat at its maximum during the timed steps, else the
+    # sustained (power-capped) one (B200_PROFILING: burst for a kernel at full clock)
+    at_max = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and
+                  clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
+    peak_kind = "bf16_tflops" if at_max else "bf16_tflops_sustained"
+    peak_tf = peaks.get(peak_kind, peaks.get("bf16_tflops_sustained", 1385.7))
     prof_steps = max(2, min(a.steps, 5))
     hbm_gbs = peaks.get("hbm_gbs", 6550.0)
     ridge = peak_tf * 1e12 / (hbm_gbs * 1e9)          # FLOP/B where the two rooflines meet
@@ -431,7 +535,11 @@ def main():
     drl = _rl(dom) if dom else _rl({"ms": 0, "flops": 0})
     roofline = dict(drl, kernel=dom["name"] if dom else None, traffic=traffic,
                     algorithmic_bytes_per_launch=dom["bytes"] / dom["launches"] if dom and dom["launches"] else None,
-                    peak_source="%s %s" % (peak_src, "bf16_tflops_sustained" if drl["bound"] == "tensor" else "hbm_gbs"),
+                    peak_source="%s %s" % (peak_src, peak_kind if drl["bound"] == "tensor" else "hbm_gbs"),
+                    frac_vs_sustained=(drl["achieved"] / peaks.get("bf16_tflops_sustained", 1385.7)
+                                       if drl["bound"] == "tensor" else None),
+                    frac_vs_burst=(drl["achieved"] / peaks.get("bf16_tflops", 1642.8)
+                                   if drl["bound"] == "tensor" else None),
                     ridge_flop_per_byte=ridge,
                     launches_per_step=dom["launches"] / prof_steps if dom else 0,
                     ms_per_step=dom["ms"] / prof_steps if dom else 0,
@@ -447,7 +555,13 @@ def main():
                                     for k in kern], key=lambda k: -k["ms_per_step"])[:10])
 
     # ---------------------------------------------------------------- memory vs layer-wise (COLUMN)
-    mem_rep = {"peak_allocated_bytes": peak, "xi_bytes": xi, "feature_map_bytes": peak - xi,
+    # feature-map HBM = allocator peak - xi (params, fp32 master, fp32 grads; the paper's xi),
+    # compared with three layer-wise references: Eq. (3) Omega (every op output stored once, bf16 --
+    # the analytical floor of layer-wise training), the same library in COLUMN mode (every map kept,
+    # same kernels) and PyTorch eager autograd on the same DAG (measured, external context)
+    fm = peak - xi
+    mem_rep = {"peak_allocated_bytes": peak, "xi_bytes": xi, "feature_map_bytes": fm,
+               "omega_eq3_bytes": mem["omega"], "reduction_vs_omega_x": mem["omega"] / max(1, fm),
                "plan": {k: mem[k] for k in ("omega", "band_act", "band_delta", "halo_cache", "carry",
                                             "checkpoints", "delta_full", "workspace")}}
     cpu = None
@@ -461,10 +575,17 @@ def main():
         cplan.step(cds.master, cds.params, cds.grads, cds.x, cds.labels, lr, cds.loss, cds.ws, stream)
         torch.cuda.synchronize()
         cpeak = torch.cuda.max_memory_allocated(dev)
-        mem_rep["layerwise_peak_allocated_bytes"] = cpeak
-        mem_rep["layerwise_feature_map_bytes"] = cpeak - xi
-        mem_rep["reduction_x"] = (cpeak - xi) / max(1, peak - xi)
-        del cds
+        mem_rep["layerwise_column_peak_allocated_bytes"] = cpeak
+        mem_rep["layerwise_column_feature_map_bytes"] = cpeak - xi
+        mem_rep["reduction_vs_column_x"] = (cpeak - xi) / max(1, fm)
+        del cds, cplan
+        torch.cuda.empty_cache()
+        if not a.no_eager:
+            with torch.cuda.stream(torch.cuda.Stream(device=dev)):
+                eg = eager_layerwise(net, B, params, x_np, lab_np, dev)
+            mem_rep["layerwise_pytorch_eager"] = eg
+            if "feature_map_bytes" in eg:
+                mem_rep["reduction_vs_pytorch_eager_x"] = eg["feature_map_bytes"] / max(1, fm)
         cpu = cpu_baseline(a)
 
     if rank == 0:
@@ -486,6 +607,7 @@ def main():
                "e2e": {"value": gb / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": xi_bytes + lab_bytes,
                        "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e},
                "gpu_launches": launches_per_step * a.steps,
+               "simt_fallbacks_per_step": plan.last_simt_fallbacks(),
                "host_enqueue_ms_per_step": 1000.0 * host_s / a.steps,
                "roofline": roofline, "memory": mem_rep, "cpu_baseline": cpu,
                "tensor_core_kernels": (not a.simt)}

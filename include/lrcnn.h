@@ -62,7 +62,7 @@ typedef enum {
     LRCNN_E_STATE = 5,        /* backward without forward, plan/buffer mismatch      */
     LRCNN_E_WORKSPACE = 6,    /* workspace NULL or too small                         */
     LRCNN_E_CUDA = 7,         /* a CUDA runtime/driver call failed                   */
-    LRCNN_E_NCCL = 8,         /* reserved for the multi-GPU exchange                 */
+    LRCNN_E_NCCL = 8,         /* a communicator call (halo exchange, all-reduce) failed */
     LRCNN_E_UNSUPPORTED = 9   /* valid request this build does not implement        */
 } lrcnn_status;
 
@@ -102,7 +102,8 @@ typedef struct {
     int band_rows;    /* >0: owned rows of each segment output per band, remainder to the
                          last band (reading R15) */
     int n_bands;      /* used when band_rows <= 0: near-equal split, earliest bands +1 row */
-    int rank, world;  /* row sharding across GPUs (world == 1 in this build) */
+    int rank, world;  /* row sharding across ranks (world > 1), or data-parallel
+                         replicas with LRCNN_FLAG_DP; world == 1: a single GPU */
     int flags;        /* LRCNN_FLAG_* */
 } lrcnn_plan_opts;
 
@@ -133,6 +134,11 @@ typedef struct {
  * segment's backward is complete, overlapping the rest of the backward; the head gradient after
  * the head.  The gradient is the SUM over replicas (pass lr / world for the mean). */
 #define LRCNN_FLAG_DP 32
+/* bf16 plans: a convolution whose shape no tensor-core kernel takes fails with LRCNN_E_UNSUPPORTED
+ * instead of running the SIMT kernel (bench.py sets it, so a timed step is tcgen05-only).  Without
+ * the flag such convolutions run on SIMT and are counted (lrcnn_last_simt_fallbacks).  A tensor-core
+ * launch that FAILS (launch or attribute error) is always LRCNN_E_CUDA, never a SIMT rerun. */
+#define LRCNN_FLAG_REQUIRE_TC 64
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 
@@ -284,6 +290,19 @@ LRCNN_API lrcnn_status lrcnn_profile_kernels(lrcnn_plan_t *plan, int cls, char *
 LRCNN_API lrcnn_status lrcnn_last_launch_count(const lrcnn_plan_t *plan, long long *launches);
 /* Of those, how many were tcgen05 tensor-core convolution kernels (FP, dgrad, wgrad). */
 LRCNN_API lrcnn_status lrcnn_last_tc_launch_count(const lrcnn_plan_t *plan, long long *launches);
+/* Convolution launches (FP, dgrad, wgrad) of a bf16 tensor-core plan that ran on the SIMT kernels
+ * because no tensor-core kernel takes the shape (0 for the benchmarked workloads; always 0 for
+ * fp32 / LRCNN_FLAG_NO_TCGEN05 plans, which are SIMT by request). */
+LRCNN_API lrcnn_status lrcnn_last_simt_fallbacks(const lrcnn_plan_t *plan, long long *n);
+
+/* Debug capture for parity tests (never on a timed path): register dst, a caller buffer holding
+ * the FULL map of tensor tid ([B][H][W][Cp] act_t, tid in 1..n_ops); every following forward pass
+ * (lrcnn_forward_rows, the FP and the BP recompute of lrcnn_step / lrcnn_step_grads) copies the
+ * rows each band computes of that tensor into it, so after a forward dst holds the map the
+ * row-centric sweep produced (every row is computed by exactly one band, R3).
+ * dst = NULL unregisters.  Disables CUDA-graph replay while any buffer is registered.  Row-sharded
+ * plans (world > 1) write the rows of their extended ranges (global row coordinates). */
+LRCNN_API lrcnn_status lrcnn_debug_capture(lrcnn_plan_t *plan, int tid, void *dst);
 
 LRCNN_API const char *lrcnn_last_error(void);
 LRCNN_API const char *lrcnn_version(void);

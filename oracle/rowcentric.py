@@ -17,6 +17,13 @@ the CUDA planner:
   Segments (checkpoints, 2PS-H / OverL-H): full-width maps
      at segment boundaries; BP walks segments in reverse.
 
+G-rank simulation: RankPlan / step_ranks split the rows of every segment
+output over G simulated ranks (enumerate_rank); rank g computes each tensor over the OverL hull of
+its owned output rows (the weak dependency across the rank cut, recomputed not
+exchanged) and runs 2PS bands inside it.  Ranks share nothing but explicit message buffers: the
+halo rows of each segment input (FP) and the delta of those rows sent back and added (BP), the
+partial GAP sums and the per-rank weight gradients (summed = the all-reduce).
+
 Negative controls (must NOT match the column oracle): share=False (cached rows
 replaced by zero rows -- the "padding redundancy" of Fig. 3(b)),
 carry=False (2PS BP drops the delta carry), overl_average=True (the averaging
@@ -100,8 +107,10 @@ def _band_range(plan, band, t):
     return band[t]
 
 
-def seg_forward(plan, s, params, x_in, share=True):
-    """FP of one segment.  Returns (full-width segment output, caches per boundary)."""
+def seg_forward(plan, s, params, x_in, share=True, in_lo=0):
+    """FP of one segment.  Returns (full-width segment output, caches per boundary).
+    x_in holds rows [in_lo, in_lo + rows) of the segment input (a rank's slab, else the full map);
+    the output has the full height, rows no band computes are zero."""
     net, shp = plan.net, plan.shp
     seg_in, ids, out = plan.segs[s]
     E, bands = plan.bands[s]
@@ -111,7 +120,7 @@ def seg_forward(plan, s, params, x_in, share=True):
     caches = []
     prev_cache = {}
     for r, band in enumerate(bands):
-        held = {seg_in: (0, x_in)}
+        held = {seg_in: (in_lo, x_in)}
         for i in ids:
             t = i + 1
             lo, a, b = _band_range(plan, band, t)
@@ -172,8 +181,9 @@ def _add_rows(d, t, r0, v):
     arr[:, :, r0 - lo:r0 - lo + v.shape[2]] += v
 
 
-def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_average=False):
-    """BP of one segment from the full-width delta of its output.  Returns (d_in, grads)."""
+def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_average=False, in_lo=0):
+    """BP of one segment from the full-width delta of its output.  Returns (d_in, grads);
+    d_in covers the same rows [in_lo, ..) as the input slab x_in."""
     net, shp = plan.net, plan.shp
     seg_in, ids, out = plan.segs[s]
     E, bands = plan.bands[s]
@@ -190,7 +200,7 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
                 m[lo:hi] += 1
     for r in range(len(bands) - 1, -1, -1):
         band = bands[r]
-        held = {seg_in: (0, x_in)}
+        held = {seg_in: (in_lo, x_in)}
         ranges = {}
         for i in ids:                                   # recompute (Alg. 1 l.17)
             t = i + 1
@@ -205,7 +215,7 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
                 clo, carr = caches[r - 1][t]
                 cached = carr[:, :, lo - clo:a - clo]
             held[t] = (lo, _concat(cached, new, lo, a))
-        d = {seg_in: (0, d_in)}
+        d = {seg_in: (in_lo, d_in)}
         for t, (lo, a, b) in ranges.items():
             if t == out:
                 d[t] = (a, dout[:, :, a:b].copy())
@@ -259,3 +269,153 @@ def step(plan, params, x, labels, lr, **kw):
     grads, _ = backward(plan, params, ckpts, allc, dzl, kw.get("carry_on", True),
                         kw.get("overl_average", False))
     return C.sgd(params, grads, hg, lr), loss, grads, hg, zl
+
+
+# ---------------------------------------------------------------- G-rank simulation (row sharding)
+class RankPlan:
+    """Rank g's band structure per segment, from enumerate_rank (not from the CUDA planner):
+    owned output rows own[s] = (ol, oh), extended ranges ext[s] = {t: (LO, HI)}, 2PS bands."""
+
+    def __init__(self, net, world, g, band_rows=None, n_bands=None):
+        from oracle.enumerate import enumerate_rank
+        self.net, self.mode, self.world, self.g = net, "2ps", world, g
+        self.shp = C.out_hw(net)
+        self.segs = segments(net)
+        self.bands, self.ext, self.own = [], [], []
+        for seg in self.segs:
+            ext, bands, own = enumerate_rank(net, seg, world, g, band_rows=band_rows,
+                                             n_bands=(n_bands or 1) if band_rows is None else None, shp=self.shp)
+            self.bands.append((None, bands))
+            self.ext.append(ext)
+            self.own.append(own)
+
+
+def _messages(plans, s, seg_in):
+    """Halo messages of segment s's input: (src rank, dst rank, r0, r1) for every row a rank needs
+    ([LO, HI) of the input) that another rank owns (the previous segment's owned rows)."""
+    msgs = []
+    for g, pg in enumerate(plans):
+        lo, hi = pg.ext[s][seg_in]
+        for q, pq in enumerate(plans):
+            if q == g:
+                continue
+            ol, oh = pq.own[s - 1]
+            r0, r1 = max(lo, ol), min(hi, oh)
+            if r1 > r0:
+                msgs.append((q, g, r0, r1))
+    return msgs
+
+
+def forward_ranks(plans, params, x):
+    """FP on G simulated ranks.  Each rank keeps only its OWNED rows of every segment output (plus
+    the input slabs it assembled); returns (per-rank state, z^L owned rows per rank, messages)."""
+    world = len(plans)
+    state = [{"slabs": [], "caches": [], "owned": []} for _ in range(world)]
+    log = []
+    for s, (seg_in, ids, out) in enumerate(plans[0].segs):
+        slabs = []
+        if s == 0:      # the image: every rank reads its extended rows of the input batch
+            for g, pg in enumerate(plans):
+                lo, hi = pg.ext[s][seg_in]
+                slabs.append((lo, np.asarray(x, dtype=np.float64)[:, :, lo:hi].copy()))
+        else:
+            msgs = _messages(plans, s, seg_in)
+            log.append(("fp", s, msgs))
+            for g, pg in enumerate(plans):
+                lo, hi = pg.ext[s][seg_in]
+                olo, own = state[g]["owned"][s - 1]
+                buf = np.zeros(own.shape[:2] + (hi - lo,) + own.shape[3:])
+                a, b = max(lo, olo), min(hi, olo + own.shape[2])
+                if b > a:
+                    buf[:, :, a - lo:b - lo] = own[:, :, a - olo:b - olo]
+                for (q, dst, r0, r1) in msgs:          # receive: a copy out of the sender's owned rows
+                    if dst != g:
+                        continue
+                    qlo, qown = state[q]["owned"][s - 1]
+                    buf[:, :, r0 - lo:r1 - lo] = qown[:, :, r0 - qlo:r1 - qlo].copy()
+                slabs.append((lo, buf))
+        for g, pg in enumerate(plans):
+            lo, slab = slabs[g]
+            y, caches = seg_forward(pg, s, params, slab, in_lo=lo)
+            ol, oh = pg.own[s]
+            state[g]["slabs"].append((lo, slab))
+            state[g]["caches"].append(caches)
+            state[g]["owned"].append((ol, y[:, :, ol:oh].copy()))
+    return state, [st["owned"][-1] for st in state], log
+
+
+def backward_ranks(plans, params, state, dzl):
+    """BP on G simulated ranks from delta^L (each rank takes its owned rows).  After each segment
+    the delta a rank produced on input rows another rank owns is sent there and added.  Returns
+    (per-rank grads, messages)."""
+    world = len(plans)
+    segs = plans[0].segs
+    dz = np.asarray(dzl, dtype=np.float64)
+    full_h = plans[0].shp[segs[-1][2]][1]
+    dout = []
+    for g, pg in enumerate(plans):     # full-height delta buffer, only owned rows set
+        ol, oh = pg.own[-1]
+        d = np.zeros(dz.shape[:2] + (full_h,) + dz.shape[3:])
+        d[:, :, ol:oh] = dz[:, :, ol:oh]
+        dout.append(d)
+    grads = [[None] * len(plans[0].net["ops"]) for _ in range(world)]
+    log = []
+    for s in range(len(segs) - 1, -1, -1):
+        seg_in, ids, out = segs[s]
+        dins = []
+        for g, pg in enumerate(plans):
+            lo, slab = state[g]["slabs"][s]
+            d_in, gr = seg_backward(pg, s, params, slab, dout[g], state[g]["caches"][s], in_lo=lo)
+            dins.append((lo, d_in))
+            for i, v in gr.items():
+                grads[g][i] = v
+        if s == 0:
+            break
+        msgs = _messages(plans, s, seg_in)        # FP schedule, run reversed: delta back to owners
+        log.append(("bp", s, msgs))
+        c, h, w = plans[0].shp[seg_in]
+        new = []
+        for g, pg in enumerate(plans):
+            ol, oh = pg.own[s - 1]
+            d = np.zeros(dz.shape[:1] + (c, h, w))
+            lo, d_in = dins[g]
+            a, b = max(lo, ol), min(lo + d_in.shape[2], oh)
+            if b > a:
+                d[:, :, a:b] += d_in[:, :, a - lo:b - lo]
+            for (src, q, r0, r1) in msgs:              # q held rows [r0, r1) that g owns
+                if src != g:
+                    continue
+                qlo, qd = dins[q]
+                d[:, :, r0:r1] += qd[:, :, r0 - qlo:r1 - qlo]
+            new.append(d)
+        dout = new
+    return grads, log
+
+
+def _sum_grads(per_rank):
+    """The weight-gradient all-reduce: elementwise sum over ranks."""
+    out = []
+    for i in range(len(per_rank[0])):
+        gs = [g[i] for g in per_rank if g[i] is not None]
+        if not gs:
+            out.append(None)
+            continue
+        out.append({k: sum(g[k] for g in gs) for k in gs[0]})
+    return out
+
+
+def step_ranks(net, params, x, labels, lr, world, band_rows=None, n_bands=None):
+    """One Alg. 1 iteration with the rows of every segment output split over `world` simulated
+    ranks.  Head: z^L is the concatenation of the ranks' owned rows (Alg. 1 l.11),
+    pooled as the sum of per-rank partial GAP sums.  Returns (new_params, loss, grads, head_grads,
+    z^L, message log)."""
+    plans = [RankPlan(net, world, g, band_rows, n_bands) for g in range(world)]
+    state, owned, flog = forward_ranks(plans, params, x)
+    c, h, w = plans[0].shp[plans[0].segs[-1][2]]
+    zl = np.zeros((np.shape(x)[0], c, h, w))
+    for (ol, rows) in owned:
+        zl[:, :, ol:ol + rows.shape[2]] = rows
+    loss, dzl, hg, _ = C.head_forward_backward(zl, params["head"], labels)
+    per_rank, blog = backward_ranks(plans, params, state, dzl)
+    grads = _sum_grads(per_rank)
+    return C.sgd(params, grads, hg, lr), loss, grads, hg, zl, flog + blog

@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <set>
 
 #include "tc.hpp"
 #include "tc_ptx.cuh"
@@ -2037,6 +2038,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
             const int ci = cit * 64 + (m & 63);
+            float dgacc[2] = {0.f, 0.f};   // fused dgamma: lane L keeps channel c * 32 + L's warp partial
 #pragma unroll 1
             for (int p = 0; p < NP; ++p) {
                 const int tA = p == NP - 1 && TAPS % 2 ? TAPS - 2 : 2 * p;
@@ -2048,6 +2050,19 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + p * 64 + c * 32, v);
                     ptx::tmem_ld_wait();
+                    if (P.dg) {   // dgamma[co] = sum_{tap,ci} W * (sum_p dy x): warp sum per co
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int co = c * 32 + j;
+                            float pj = keep && co < P.c_out
+                                           ? __uint_as_float(v[j]) *
+                                                 __bfloat162float(P.w[((long long)co * TAPS + t) * P.cin_p + ci])
+                                           : 0.f;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) pj += __shfl_xor_sync(0xffffffffu, pj, o);
+                            if (lane == j) dgacc[c] += pj;
+                        }
+                    }
                     if (!keep) continue;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -2061,6 +2076,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     }
                 }
             }
+            if (P.dg)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (c * 32 + lane < P.c_out) atomicAdd(P.dg + c * 32 + lane, dgacc[c]);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty);
@@ -2469,6 +2488,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 // step's CUDA graph as programmatic edges.  LRCNN_PDL=0 disables it.
 static int env_int(const char *name, int dflt);
 static thread_local const char *g_last_kernel = nullptr;
+// A failure that is not a shape decline (a launch or attribute error, or a strided dgrad whose later
+// parity class failed after earlier ones were enqueued): the engine turns it into LRCNN_E_CUDA
+// instead of running the SIMT kernel over the same rows.
+static thread_local bool g_tc_error = false;
+bool tc_take_error() { const bool e = g_tc_error; g_tc_error = false; return e; }
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device) -- thread safe
+static bool smem_attr(const void *kern, int bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { g_tc_error = true; return false; }
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({kern, dev})) return true;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+        g_tc_error = true;
+        return false;
+    }
+    done.insert({kern, dev});
+    return true;
+}
 static void note_kernel(const void *fn) {
     const char *nm = nullptr;
     if (cudaFuncGetName(&nm, fn) == cudaSuccess) g_last_kernel = nm;
@@ -2490,6 +2529,7 @@ static bool launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
     cfg.numAttrs = 1;
     const bool ok = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess;
     if (ok) note_kernel((const void *)kern);
+    else g_tc_error = true;
     return ok;
 }
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -2582,12 +2622,7 @@ template <int BN, int KC>
 static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
                         const CUtensorMap &G, const CUtensorMap &X, int tiles, cudaStream_t st) {
     using Cfg = ConvCfg<BN, KC>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_conv_tc<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_conv_tc<BN, KC>, Cfg::kSmem)) return false;
     int grid = tiles < num_sms() ? tiles : num_sms();
     return launch_pdl(k_conv_tc<BN, KC>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P, X);
 }
@@ -2596,13 +2631,7 @@ template <int BN>
 static bool launch_conv_halo(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
                              int tiles, cudaStream_t st) {
     using Cfg = HaloCfg<BN, 3>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_conv_tc_halo<BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-            cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_conv_tc_halo<BN, 3>, Cfg::kSmem)) return false;
     int grid = tiles < num_sms() ? tiles : num_sms();
     return launch_pdl(k_conv_tc_halo<BN, 3>, grid, kThreads, Cfg::kSmem, st, A, Bm, O, P);
 }
@@ -2636,12 +2665,7 @@ static bool conv_halo_rb(TcConv &P, const View &in, const void *w, int w_rows, i
     if (P.mode == 1 && P.gate && !encode_view(&G, P.act, P.B, 8, 16)) return false;
     P.tma_out = P.mode == 0;
     P.tma_dg = P.mode == 1;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_conv_halo_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, kRbSmem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_conv_halo_rb, kRbSmem)) return false;
     const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
     return launch_pdl(k_conv_halo_rb, grid, kThreads, kRbSmem, st, A, Bm, O, G, P);
 }
@@ -2761,22 +2785,10 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN / 2, KC)) return false;
         const int grid = tiles < num_sms() ? tiles : num_sms() & ~1;
         if (BN == 256) {
-            static bool attr = false;
-            if (!attr) {
-                if (cudaFuncSetAttribute(k_conv_tc2h<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Conv2HCfg<256>::kSmem) != cudaSuccess)
-                    return false;
-                attr = true;
-            }
+            if (!smem_attr((const void *)k_conv_tc2h<256>, Conv2HCfg<256>::kSmem)) return false;
             return launch_pdl(k_conv_tc2h<256>, grid, kConvThreads, Conv2HCfg<256>::kSmem, st, A, Bm, O, G, P);
         }
-        static bool attr = false;
-        if (!attr) {
-            if (cudaFuncSetAttribute(k_conv_tc2h<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Conv2HCfg<128>::kSmem) != cudaSuccess)
-                return false;
-            attr = true;
-        }
+        if (!smem_attr((const void *)k_conv_tc2h<128>, Conv2HCfg<128>::kSmem)) return false;
         return launch_pdl(k_conv_tc2h<128>, grid, kConvThreads, Conv2HCfg<128>::kSmem, st, A, Bm, O, G, P);
     }
     if (try2h) {   // no TMA epilogue for this shape: single-CTA halo kernel with the same box map
@@ -2791,22 +2803,10 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         if (!encode_w(&Bm, w, w_rows, w_taps, cin_p, BN / 2, KC)) return false;
         int grid = tiles < num_sms() ? tiles : num_sms() & ~1;
         if (BN == 256) {
-            static bool attr = false;
-            if (!attr) {
-                if (cudaFuncSetAttribute(k_conv_tc2<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Conv2Cfg<256>::kSmem) != cudaSuccess)
-                    return false;
-                attr = true;
-            }
+            if (!smem_attr((const void *)k_conv_tc2<256>, Conv2Cfg<256>::kSmem)) return false;
             return launch_pdl(k_conv_tc2<256>, grid, kConvThreads, Conv2Cfg<256>::kSmem, st, A, Bm, O, G, P, X);
         }
-        static bool attr = false;
-        if (!attr) {
-            if (cudaFuncSetAttribute(k_conv_tc2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Conv2Cfg<128>::kSmem) !=
-                cudaSuccess)
-                return false;
-            attr = true;
-        }
+        if (!smem_attr((const void *)k_conv_tc2<128>, Conv2Cfg<128>::kSmem)) return false;
         return launch_pdl(k_conv_tc2<128>, grid, kConvThreads, Conv2Cfg<128>::kSmem, st, A, Bm, O, G, P, X);
     }
     if (KC == 16) {
@@ -2836,13 +2836,7 @@ static bool encode_w2d(CUtensorMap *m, const void *w, int rows, int K, int BN) {
 template <int BN>
 static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensorMap &O, const CUtensorMap &Pm,
                           int tiles, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_conv_im2col<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI2cSmem) !=
-            cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_conv_im2col<BN>, kI2cSmem)) return false;
     int grid = tiles < num_sms() ? tiles : num_sms();
     return launch_pdl(k_conv_im2col<BN>, grid, kI2pThreads, kI2cSmem, st, Bm, O, Pm, P);
 }
@@ -2904,12 +2898,7 @@ static bool conv_pair(TcConv &P, const View &in, const void *w, int w_rows, cuda
     ov.rows = P.out_b - P.out.base;
     if (!encode_view(&O, ov, P.B, 8, 16)) return false;
     P.tma_out = 1;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_conv_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrSmem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_conv_pair, kPrSmem)) return false;
     const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
     return launch_pdl(k_conv_pair, grid, kConvThreads, kPrSmem, st, Pm, Wm, O, P);
 }
@@ -2994,6 +2983,7 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
     if (!a.wt || a.s < 1 || a.s > 2 || a.k * a.k > 49) return false;
     if (a.gate && (!aligned16(a.act.p) || a.act.Cp != a.dx.Cp)) return false;
     const int s = a.s, k = a.k, p = a.p;
+    int launched = 0;
     for (int ry = 0; ry < s; ++ry)
         for (int rx = 0; rx < s; ++rx) {
             TcConv P{};
@@ -3023,7 +3013,12 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
             if (n == 0 || P.out_b <= P.out_a || P.Wo <= 0) continue;
             P.k = k; P.pad = k - 1 - p; P.halo_ok = s == 1 && k == 3;
             if (a.add_on && s == 1) { P.add = a.add; P.add_req = 1; }
-            if (!conv_launch(P, a.dy, a.wt, a.dx.Cp, k * k, a.dy.Cp, st)) return false;
+            if (!conv_launch(P, a.dy, a.wt, a.dx.Cp, k * k, a.dy.Cp, st)) {
+                // earlier parity classes are already enqueued: a SIMT rerun would add them twice
+                if (launched) g_tc_error = true;
+                return false;
+            }
+            ++launched;
             if (P.dg_add) a.add_done = true;
         }
     return true;
@@ -3032,12 +3027,7 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
 template <int BN>
 static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorMap &X, cudaStream_t st) {
     using Cfg = WgCfg<BN>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_wgrad_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_wgrad_tc<BN>, Cfg::kSmem)) return false;
     int grid = P.items < num_sms() ? P.items : num_sms();
     return launch_pdl(k_wgrad_tc<BN>, grid, kWgThreads, Cfg::kSmem, st, D, X, P);
 }
@@ -3045,13 +3035,7 @@ static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorM
 template <int BN, int KW>
 static bool launch_wgrad_halo(const TcWgrad &P, const CUtensorMap &D, const CUtensorMap &X, cudaStream_t st) {
     using Cfg = WgHCfg<BN, KW>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_wgrad_halo<BN, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-            cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_wgrad_halo<BN, KW>, Cfg::kSmem)) return false;
     int grid = P.items < num_sms() ? P.items : num_sms();
     return launch_pdl(k_wgrad_halo<BN, KW>, grid, kWgThreads, Cfg::kSmem, st, D, X, P);
 }
@@ -3066,10 +3050,10 @@ static bool wgrad_pair(const WgradArgs &a, cudaStream_t st) {
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = 1;
-    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
-    P.db = fuse_db && !a.dg ? a.db : nullptr;   // (dgamma is not fused here: param-grad kernel)
-    P.dg = nullptr;
+    P.db = a.db;                                 // bias / beta (dedicated warps), dgamma (epilogue)
+    P.dg = a.db ? a.dg : nullptr;
     P.w = (const bf16 *)a.w;
+    if (P.dg && !P.w) P.db = P.dg = nullptr;
     long best = -1;
     for (int tw = 128; tw >= 16; tw >>= 1) {
         const int th = 128 / tw;
@@ -3094,15 +3078,11 @@ static bool wgrad_pair(const WgradArgs &a, cudaStream_t st) {
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
     if (!encode_view(&X, x, a.B, P.TW + a.k - 1, P.TH + a.k - 1)) return false;
     using Cfg = WgPCfg<3>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_wgrad_pair<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_wgrad_pair<3>, Cfg::kSmem)) return false;
     const int grid = P.items < num_sms() ? P.items : num_sms();
     if (!launch_pdl(k_wgrad_pair<3>, grid, kWgThreads, Cfg::kSmem, st, D, X, P)) return false;
     if (P.db) a.db_done = true;
+    if (P.dg) a.dg_done = true;
     return true;
 }
 
@@ -3115,9 +3095,8 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = 1;
-    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
-    P.db = fuse_db ? a.db : nullptr;
-    P.dg = fuse_db && a.db ? a.dg : nullptr;
+    P.db = a.db;
+    P.dg = a.db ? a.dg : nullptr;
     P.w = (const bf16 *)a.w;
     if (P.dg && !P.w) P.db = P.dg = nullptr;
     // 128-pixel tile, TW a multiple of 16 (one K-step = 16 pixels of one output row)
@@ -3148,17 +3127,13 @@ static bool wgrad_halo(const WgradArgs &a, cudaStream_t st) {
     if (!encode_view(&X, x, a.B, P.TW + a.k - 1, P.TH)) return false;
     const bool ok = BN == 64 ? launch_wgrad_halo<64, 3>(P, D, X, st) : launch_wgrad_halo<128, 3>(P, D, X, st);
     if (ok && P.db) a.db_done = true;
+    if (ok && P.dg) a.dg_done = true;
     return ok;
 }
 
 template <int BN>
 static bool launch_wgrad_im2col(const TcWgI2c &P, const CUtensorMap &D, const CUtensorMap &Pm, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_wgrad_im2col<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWiSmem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (!smem_attr((const void *)k_wgrad_im2col<BN>, kWiSmem)) return false;
     int grid = P.items < num_sms() ? P.items : num_sms();
     return launch_pdl(k_wgrad_im2col<BN>, grid, kWiThreads, kWiSmem, st, D, Pm, P);
 }
@@ -3171,9 +3146,8 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     const int rows = a.b - a.a;
     TcWgI2c P{};
     P.in = x; P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.ntaps = a.k * a.k; P.mtiles = (P.ntaps + 15) / 16;
-    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
-    P.db = fuse_db ? a.db : nullptr;            // bias / beta (dedicated warps), dgamma (epilogue)
-    P.dg = fuse_db && a.db ? a.dg : nullptr;
+    P.db = a.db;            // bias / beta (dedicated warps), dgamma (epilogue)
+    P.dg = a.db ? a.dg : nullptr;
     P.w = (const bf16 *)a.w;
     if (P.dg && !P.w) P.db = P.dg = nullptr;
     P.a_mul = a.s; P.c_out = a.c_out;
@@ -3212,6 +3186,7 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     if (!encode_patch(&Pm, x, a.B, P.pat_w, P.pat_h)) return false;
     const bool ok = launch_wgrad_im2col<64>(P, D, Pm, st);
     if (ok && P.db) a.db_done = true;
+    if (ok && P.dg) a.dg_done = true;
     return ok;
 }
 
@@ -3220,16 +3195,15 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     const View &dy = a.dy, &x = a.x;
     if (dy.Cp % 8 || x.Cp % 8 || !aligned16(dy.p) || !aligned16(x.p)) return false;
     const int rows = a.b - a.a;
-    if (rows <= 0) return true;
+    if (rows <= 0) { a.db_done = a.dg_done = true; return true; }
     if (wgrad_pair(a, st)) return true;
     if (wgrad_halo(a, st)) return true;
     if (wgrad_im2col(a, st)) return true;
     TcWgrad P{};
     P.dw = a.dw; P.gamma = (const bf16 *)a.gamma; P.k = a.k; P.pad = a.p; P.c_out = a.c_out; P.cin_p = x.Cp;
     P.s = a.s;
-    static const int fuse_db = env_int("LRCNN_FUSE_DB", 1);
-    P.db = fuse_db ? a.db : nullptr;
-    P.dg = fuse_db && a.db ? a.dg : nullptr;
+    P.db = a.db;
+    P.dg = a.db ? a.dg : nullptr;
     P.w = (const bf16 *)a.w;
     if (P.dg && !P.w) P.db = P.dg = nullptr;
     static const int fold = env_int("LRCNN_BATCH_FOLD", 1);
@@ -3258,6 +3232,7 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     const bool ok = BN == 16 ? launch_wgrad<16>(P, D, X, st)
                   : BN == 64 ? launch_wgrad<64>(P, D, X, st) : launch_wgrad<128>(P, D, X, st);
     if (ok && P.db) a.db_done = true;
+    if (ok && P.dg) a.dg_done = true;
     return ok;
 }
 

@@ -150,6 +150,19 @@ static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
 
 static const void *prm(Run &R, size_t off) { return off == (size_t)-1 ? nullptr : R.params + off * R.E; }
 
+// A tensor-core launcher returned false: a launch / attribute failure is an error (LRCNN_E_CUDA; the
+// SIMT kernel must not rerun rows a partial launch already produced); a declined shape runs the SIMT
+// kernel, is counted (lrcnn_last_simt_fallbacks) and is an error under LRCNN_FLAG_REQUIRE_TC.
+static lrcnn_status tc_declined(Plan &P, int op, const char *kind) {
+    if (tc_take_error())
+        return fail(LRCNN_E_CUDA, std::string("tensor-core ") + kind + " launch failed at op " + std::to_string(op));
+    ++P.simt_fallbacks;
+    if (P.opts.flags & LRCNN_FLAG_REQUIRE_TC)
+        return fail(LRCNN_E_UNSUPPORTED, std::string("no tensor-core kernel takes the ") + kind + " of op " +
+                                             std::to_string(op) + " (LRCNN_FLAG_REQUIRE_TC)");
+    return LRCNN_OK;
+}
+
 // ------------------------------------------------------------------ profiling
 struct ProfScope {
     Run &R;
@@ -200,7 +213,7 @@ static double conv_bytes(Plan &P, const OpInfo &o, int a, int b, int kind, int d
 }
 
 // ------------------------------------------------------------------ op forward on band rows [a, b)
-static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
+static lrcnn_status op_forward_impl(Run &R, const Segment &S, int r, int i) {
     Plan &P = R.P;
     const OpInfo &o = P.op[i];
     const int t = o.out_t;
@@ -219,7 +232,11 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
         A.a = a; A.b_ = b; A.B = P.net.B;
         ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 0, conv_bytes(P, o, a, b, 0));
         ++P.launches;
-        if (P.use_tc && tc_conv_fwd(A, R.st)) { ++P.tc_launches; CK(cudaGetLastError()); return LRCNN_OK; }
+        if (P.use_tc) {
+            if (tc_conv_fwd(A, R.st)) { ++P.tc_launches; CK(cudaGetLastError()); return LRCNN_OK; }
+            lrcnn_status st = tc_declined(P, i, "FP");
+            if (st != LRCNN_OK) return st;
+        }
         CK(simt_conv_fwd(R.prec, A, R.st));
     } else if (o.d.kind == LRCNN_OP_MAXPOOL) {
         PoolArgs A;
@@ -235,6 +252,30 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
         CK(simt_add_fwd(R.prec, A, R.st));
     }
     return LRCNN_OK;
+}
+
+// Debug capture (lrcnn_debug_capture): rows [a, b) of tensor t, just computed by a band, copied into
+// the caller's full-height buffer [B][H][W][Cp] -- every row of every tensor is produced by exactly
+// one band (interval rule), so after a forward the buffer holds the whole map the row-centric
+// sweep computed.  Parity tests only; never registered on a timed path.
+static lrcnn_status capture_rows(Run &R, int t, const View &out, int a, int b) {
+    Plan &P = R.P;
+    if ((size_t)t >= P.capture.size() || !P.capture[t] || b <= a) return LRCNN_OK;
+    const TensorInfo &ti = P.t[t];
+    const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+    const char *src = (const char *)out.p + (size_t)(a - out.base) * rb;
+    char *dst = (char *)P.capture[t] + (size_t)a * rb;
+    CK(cudaMemcpy2DAsync(dst, (size_t)ti.H * rb, src, (size_t)out.bs * R.E, (size_t)(b - a) * rb, P.net.B,
+                         cudaMemcpyDeviceToDevice, R.st));
+    return LRCNN_OK;
+}
+
+static lrcnn_status capture_rows(Run &R, int t, const View &out, int a, int b);
+static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
+    lrcnn_status st = op_forward_impl(R, S, r, i);
+    if (st != LRCNN_OK || R.P.capture.empty()) return st;
+    const int t = R.P.op[i].out_t;
+    return capture_rows(R, t, act_view(R, S, r, t), S.a[r][t], S.b[r][t]);
 }
 
 // copy rows between two views of the same tensor (B planes, pitched)
@@ -524,6 +565,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     const bool need_dx = o.in_t != 0;
     if (o.d.kind == LRCNN_OP_CONV) {
         float *g = R.grads;
+        lrcnn_status st0;
         // wgrad and the bias/affine reduction only read complete data of this band: run them on
         // the side stream so they overlap the dgrad chain (joined at the end of the band)
         cudaStream_t gst = R.st;
@@ -540,20 +582,23 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
             ++P.launches;
             ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2, conv_bytes(P, o, a, b, 2));
-            if (P.use_tc && tc_conv_wgrad(A, gst)) ++P.tc_launches;
-            else CK(simt_conv_wgrad(R.prec, A, gst));
+            bool tc = false;
+            if (P.use_tc) {
+                tc = tc_conv_wgrad(A, gst);
+                if (tc) ++P.tc_launches;
+                else if ((st0 = tc_declined(P, i, "wgrad")) != LRCNN_OK) return st0;
+            }
+            if (!tc) CK(simt_conv_wgrad(R.prec, A, gst));
             CK(cudaGetLastError());
             db_done = A.db_done;
+            // dgamma comes only from the wgrad (sum_{tap,ci} W * sum_p dy x, exact for gamma = 0)
+            if (A.dg && !A.dg_done) return fail(LRCNN_E_STATE, "wgrad of op " + std::to_string(i) + " did not take dgamma");
         }
-        if (o.d.epi != LRCNN_EPI_NONE && !db_done) {
+        if (o.d.epi != LRCNN_EPI_NONE && !db_done) {   // bias / beta: column sums of dy
             ParamGradArgs A;
-            A.dy = dy; A.t = act_view(R, S, r, t);
-            if (o.d.res >= 0) A.res = act_view(R, S, r, o.d.res);
-            A.gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
-            A.beta = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.beta_off) : nullptr;
-            A.db = g + o.b_off;
-            A.dbeta = o.d.epi == LRCNN_EPI_AFFINE ? g + o.beta_off : nullptr;
-            A.epi = o.d.epi; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
+            A.dy = dy;
+            A.db = g + (o.d.epi == LRCNN_EPI_AFFINE ? o.beta_off : o.b_off);
+            A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
             ++P.launches;
             ProfScope ps(R, 2, 0, i * 8 + 3);
             CK(simt_param_grad(R.prec, A, gst));
@@ -578,8 +623,13 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             {
                 ++P.launches;
                 ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0));
-                if (P.use_tc && tc_conv_dgrad(A, R.st)) ++P.tc_launches;
-                else CK(simt_conv_dgrad(R.prec, A, R.st));
+                bool tc = false;
+                if (P.use_tc) {
+                    tc = tc_conv_dgrad(A, R.st);
+                    if (tc) ++P.tc_launches;
+                    else if ((st0 = tc_declined(P, i, "dgrad")) != LRCNN_OK) return st0;
+                }
+                if (!tc) CK(simt_conv_dgrad(R.prec, A, R.st));
                 CK(cudaGetLastError());
             }
             if (fu >= 0) {   // residual rows the dgrad did not take
@@ -783,7 +833,8 @@ using namespace lrcnn;
 template <typename F>
 static lrcnn_status graph_run(Plan &P, int slot, const uintptr_t (&key)[9], void *stream, F &&eager) {
     static const int graphs = getenv("LRCNN_GRAPH") ? atoi(getenv("LRCNN_GRAPH")) : 1;
-    if (!graphs || stream == nullptr || P.profiling || (P.comm && !comm_graph_safe((Comm *)P.comm))) {
+    if (!graphs || stream == nullptr || P.profiling || !P.capture.empty() ||
+        (P.comm && !comm_graph_safe((Comm *)P.comm))) {
         P.graph_calls[slot] = 0;
         return eager();
     }
@@ -792,6 +843,7 @@ static lrcnn_status graph_run(Plan &P, int slot, const uintptr_t (&key)[9], void
         CK(cudaGraphLaunch((cudaGraphExec_t)P.graph_exec[slot], (cudaStream_t)stream));
         P.launches = P.graph_launches[slot];
         P.tc_launches = P.graph_tc_launches[slot];
+        P.simt_fallbacks = P.graph_simt_fallbacks[slot];
         P.fwd_done = false;
         return LRCNN_OK;
     }
@@ -813,6 +865,7 @@ static lrcnn_status graph_run(Plan &P, int slot, const uintptr_t (&key)[9], void
     P.graph_exec[slot] = ge;
     P.graph_launches[slot] = P.launches;
     P.graph_tc_launches[slot] = P.tc_launches;
+    P.graph_simt_fallbacks[slot] = P.simt_fallbacks;
     CK(cudaGraphLaunch(ge, cs));
     return LRCNN_OK;
 }
@@ -1049,7 +1102,7 @@ lrcnn_status lrcnn_forward_rows(lrcnn_plan_t *plan, const void *params, const vo
     Plan &P = plan->P;
     lrcnn_status st = check_ws(P, ws, ws_bytes);
     if (st != LRCNN_OK) return st;
-    P.launches = 0; P.tc_launches = 0;
+    P.launches = 0; P.tc_launches = 0; P.simt_fallbacks = 0;
     Run R{P, (char *)ws, (const char *)params, x, zl, nullptr, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     P.fwd_done = false;
     if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
@@ -1067,7 +1120,7 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
     if (st != LRCNN_OK) return st;
     if (!P.fwd_done || P.fwd_ws != ws || P.fwd_params != params || P.fwd_x != x)
         return fail(LRCNN_E_STATE, "backward_rows needs a matching forward_rows (same params, x, ws)");
-    P.launches = 0; P.tc_launches = 0;
+    P.launches = 0; P.tc_launches = 0; P.simt_fallbacks = 0;
     Run R{P, (char *)ws, (const char *)params, x, (void *)zl, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     const int L = P.net.n_ops;
     const TensorInfo &z = P.t[L];
@@ -1093,7 +1146,7 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
     Plan &P = plan->P;
     lrcnn_status st = check_ws(P, ws, ws_bytes);
     if (st != LRCNN_OK) return st;
-    P.launches = 0; P.tc_launches = 0;
+    P.launches = 0; P.tc_launches = 0; P.simt_fallbacks = 0;
     char *w = (char *)ws;
     Run R{P, w, (const char *)params, x, w + P.zl_off, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
     if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
@@ -1293,6 +1346,23 @@ lrcnn_status lrcnn_profile_dump(lrcnn_plan_t *plan, const char *path, void *stre
 lrcnn_status lrcnn_last_tc_launch_count(const lrcnn_plan_t *plan, long long *launches) {
     if (!plan || !launches) return fail(LRCNN_E_ARG, "bad args");
     *launches = plan->P.tc_launches;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_debug_capture(lrcnn_plan_t *plan, int tid, void *dst) {
+    if (!plan || tid < 1 || tid > plan->P.net.n_ops) return fail(LRCNN_E_ARG, "bad plan or tensor id");
+    Plan &P = plan->P;
+    if (P.capture.size() < P.t.size()) P.capture.resize(P.t.size(), nullptr);
+    P.capture[tid] = dst;
+    bool any = false;
+    for (void *c : P.capture) any = any || c;
+    if (!any) P.capture.clear();
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_last_simt_fallbacks(const lrcnn_plan_t *plan, long long *n) {
+    if (!plan || !n) return fail(LRCNN_E_ARG, "bad args");
+    *n = plan->P.simt_fallbacks;
     return LRCNN_OK;
 }
 

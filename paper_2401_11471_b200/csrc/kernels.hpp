@@ -53,16 +53,16 @@ struct WgradArgs {
     float *dg = nullptr;       // optional: affine gamma gradient, fused as sum_{tap,ci} W * (sum_p dy x)
     const void *w = nullptr;   // weights [Cout][k][k][Cin_p] (for dg)
     mutable bool db_done = false;   // set by a launcher that accumulated db (and dg when requested)
+    mutable bool dg_done = false;   // set by a launcher that accumulated dg (SIMT: always when dg is set)
     int k, s, p, c_out;
     int a, b;                  // output rows contributing
     int B;
 };
 
 struct ParamGradArgs {
-    View dy, t, res;
-    const void *gamma = nullptr, *beta = nullptr;
-    float *db = nullptr, *dbeta = nullptr;  // BIAS: db; AFFINE: db = dgamma, dbeta
-    int epi, c_out, a, b, B;
+    View dy;
+    float *db = nullptr;       // += column sums of dy: the bias (BIAS) or beta (AFFINE) gradient
+    int c_out, a, b, B;
 };
 
 struct PoolArgs {

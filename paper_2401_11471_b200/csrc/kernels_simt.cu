@@ -170,11 +170,21 @@ __global__ void k_conv_wgrad(WgradArgs A) {
     }
     red[lane_grp][threadIdx.x & 31] = acc;
     __syncthreads();
-    if (lane_grp == 0 && ci < Cin) {
+    if (lane_grp == 0) {
         float s = 0.f;
-        for (int j = 0; j < ngrp; ++j) s += red[j][threadIdx.x & 31];
-        if (A.gamma) s *= ldf((const T *)A.gamma + co);
-        A.dw[((long long)(co * A.k + ky) * A.k + kx) * Cin + ci] += s;
+        if (ci < Cin)
+            for (int j = 0; j < ngrp; ++j) s += red[j][threadIdx.x & 31];
+        const long long wi = ((long long)(co * A.k + ky) * A.k + kx) * Cin + ci;
+        if (A.dg) {   // dgamma[co] += sum_{tap,ci} W * (sum_p dy x): exact for any gamma (incl. 0)
+            float g = ci < Cin ? s * ldf((const T *)A.w + wi) : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+            if ((threadIdx.x & 31) == 0) atomicAdd(A.dg + co, g);
+        }
+        if (ci < Cin) {
+            if (A.gamma) s *= ldf((const T *)A.gamma + co);
+            A.dw[wi] += s;
+        }
     }
 }
 
@@ -202,28 +212,17 @@ __device__ __forceinline__ void st8(bf16 *p, const float (&v)[8]) {
     *reinterpret_cast<uint4 *>(p) = u;
 }
 
-// ------------------------------------------------------------------ bias / affine grads
-// db[c] += sum_pixels dy[p, c]  (BIAS);  AFFINE: dbeta[c] += sum dy, dgamma[c] += sum dy * c_raw
-// with c_raw = (t - beta - res)/gamma.  Block = (channel vectors of 8) x (pixel lanes);
-// coalesced 8-channel loads, per-thread partial sums, smem reduction over pixel lanes,
-// one fp32 atomicAdd per channel per block.
+// ------------------------------------------------------------------ bias / beta grads
+// db[c] += sum_pixels dy[p, c]: the bias (BIAS) or beta (AFFINE) gradient of a conv whose wgrad
+// kernel did not fuse it.  (dgamma is always taken by the wgrad as sum_{tap,ci} W * (sum_p dy x),
+// exact for any gamma -- never recovered from the stored output, which divides by gamma.)
+// Block = (channel vectors of 8) x (pixel lanes); coalesced 8-channel loads, per-thread partial
+// sums, smem reduction over pixel lanes, one fp32 atomicAdd per channel per block.
 template <typename T>
 __device__ __forceinline__ void acc8(const uint4 &u, float (&s)[8]) {
     const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
     for (int j = 0; j < 4; ++j) { float2 f = __bfloat1622float2(h[j]); s[2 * j] += f.x; s[2 * j + 1] += f.y; }
-}
-// s += d * (t - r)  (bf16 vectors of 8)
-__device__ __forceinline__ void accdot8(const uint4 &d, const uint4 &t, const uint4 &r, float (&s)[8]) {
-    const __nv_bfloat162 *dh = reinterpret_cast<const __nv_bfloat162 *>(&d);
-    const __nv_bfloat162 *th = reinterpret_cast<const __nv_bfloat162 *>(&t);
-    const __nv_bfloat162 *rh = reinterpret_cast<const __nv_bfloat162 *>(&r);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float2 fd = __bfloat1622float2(dh[j]), ft = __bfloat1622float2(th[j]), fr = __bfloat1622float2(rh[j]);
-        s[2 * j] += fd.x * (ft.x - fr.x);
-        s[2 * j + 1] += fd.y * (ft.y - fr.y);
-    }
 }
 
 template <typename T>
@@ -235,23 +234,20 @@ __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
     const int rows = A.b - A.a, W = A.dy.W, c0 = (blockIdx.y * CV + cv) * 8;
     const bool live = c0 < A.dy.Cp;
     const int RW = rows * W;                        // band pixels per image (contiguous rows)
-    float s0[8], s1[8];
+    float s0[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { s0[j] = 0.f; s1[j] = 0.f; }
+    for (int j = 0; j < 8; ++j) s0[j] = 0.f;
     // pixel q = b * RW + p walks with stride S; (b, p) updated without division
     const int S = gridDim.x * PY;
     const int q0 = blockIdx.x * PY + py;
     int b = q0 / RW, p = q0 - b * RW;
     // advance by S pixels: (b, p) += (S / RW, S % RW) with one carry (the stride can span many
-    // images when the band is thin: a repeated-subtraction loop cost S / RW iterations per step)
+    // images when the band is thin)
     const int Sb = S / RW, Sp = S - Sb * RW;
     auto advance = [&]() { p += Sp; b += Sb; if (p >= RW) { p -= RW; ++b; } };
     const T *dbase = (const T *)A.dy.p + voff(A.dy, 0, A.a, 0) + c0;
-    const T *tbase = A.epi == 2 ? (const T *)A.t.p + voff(A.t, 0, A.a, 0) + c0 : nullptr;
-    const T *rbase = A.epi == 2 && A.res.p ? (const T *)A.res.p + voff(A.res, 0, A.a, 0) + c0 : nullptr;
     if constexpr (sizeof(T) == 2) {
-        // bf16: raw 16-byte vectors, two pixels in flight per thread; AFFINE accumulates
-        // sum d (t - res) and dgamma = (sum d (t - res) - beta sum d) / gamma at the end
+        // bf16: raw 16-byte vectors, two pixels in flight per thread
         const uint4 z = make_uint4(0, 0, 0, 0);
         while (live && b < A.B) {
             const int b0 = b, p0 = p;
@@ -261,55 +257,27 @@ __global__ void __launch_bounds__(256, 4) k_param_grad(ParamGradArgs A) {
             if (two) advance();
             const uint4 d0 = *reinterpret_cast<const uint4 *>(dbase + (long long)b0 * A.dy.bs + (long long)p0 * A.dy.Cp);
             const uint4 d1 = two ? *reinterpret_cast<const uint4 *>(dbase + (long long)b1 * A.dy.bs + (long long)p1 * A.dy.Cp) : z;
-            if (A.epi == 2) {
-                const uint4 t0 = *reinterpret_cast<const uint4 *>(tbase + (long long)b0 * A.t.bs + (long long)p0 * A.t.Cp);
-                const uint4 t1 = two ? *reinterpret_cast<const uint4 *>(tbase + (long long)b1 * A.t.bs + (long long)p1 * A.t.Cp) : z;
-                const uint4 r0 = rbase ? *reinterpret_cast<const uint4 *>(rbase + (long long)b0 * A.res.bs + (long long)p0 * A.res.Cp) : z;
-                const uint4 r1 = rbase && two ? *reinterpret_cast<const uint4 *>(rbase + (long long)b1 * A.res.bs + (long long)p1 * A.res.Cp) : z;
-                accdot8(d0, t0, r0, s1);
-                accdot8(d1, t1, r1, s1);
-            }
             acc8<T>(d0, s0);
             acc8<T>(d1, s0);
         }
     } else {
         while (live && b < A.B) {
-            float d[8], t[8], rr[8];
+            float d[8];
             ld8(dbase + (long long)b * A.dy.bs + (long long)p * A.dy.Cp, d);
-            if (A.epi == 2) {
-                ld8(tbase + (long long)b * A.t.bs + (long long)p * A.t.Cp, t);
-                if (rbase) ld8(rbase + (long long)b * A.res.bs + (long long)p * A.res.Cp, rr);
-            }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                s0[j] += d[j];
-                if (A.epi == 2) s1[j] += d[j] * (t[j] - (rbase ? rr[j] : 0.f));
-            }
+            for (int j = 0; j < 8; ++j) s0[j] += d[j];
             advance();
         }
     }
-    if (A.epi == 2) {
+    extern __shared__ float red[];   // [PY][CV*8]
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const bool in = c0 + j < A.c_out;
-            const float g = in ? ldf((const T *)A.gamma + c0 + j) : 1.f;
-            const float be = in ? ldf((const T *)A.beta + c0 + j) : 0.f;
-            s1[j] = (s1[j] - be * s0[j]) / g;
-        }
-    }
-    extern __shared__ float red[];   // [PY][CV*8] x 2
-    float *r0 = red, *r1 = red + PY * CV * 8;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) { r0[py * CV * 8 + cv * 8 + j] = s0[j]; r1[py * CV * 8 + cv * 8 + j] = s1[j]; }
+    for (int j = 0; j < 8; ++j) red[py * CV * 8 + cv * 8 + j] = s0[j];
     __syncthreads();
     for (int c = py * CV + cv; c < CV * 8; c += PY * CV) {
-        float a0 = 0.f, a1 = 0.f;
-        for (int k = 0; k < PY; ++k) { a0 += r0[k * CV * 8 + c]; a1 += r1[k * CV * 8 + c]; }
+        float a0 = 0.f;
+        for (int k = 0; k < PY; ++k) a0 += red[k * CV * 8 + c];
         const int ch = blockIdx.y * CV * 8 + c;
-        if (ch < A.c_out) {
-            if (A.epi == 1) atomicAdd(A.db + ch, a0);
-            else { atomicAdd(A.db + ch, a1); atomicAdd(A.dbeta + ch, a0); }
-        }
+        if (ch < A.c_out) atomicAdd(A.db + ch, a0);
     }
 }
 
@@ -544,10 +512,10 @@ __global__ void k_fc_grad(const float *gap, int B, int Cp, int C, int classes, c
         gw[(long long)j * Cp + c] += s;
     }
     if (blockIdx.x == 0) {
-        if (threadIdx.x < classes) {
+        for (int j = threadIdx.x; j < classes; j += blockDim.x) {   // any class count
             float s = 0.f;
-            for (int b = 0; b < B; ++b) s += dlog[b * classes + threadIdx.x];
-            gb[threadIdx.x] += s;
+            for (int b = 0; b < B; ++b) s += dlog[b * classes + j];
+            gb[j] += s;
         }
         if (threadIdx.x == 0) {
             float l = 0.f;
@@ -1040,12 +1008,14 @@ cudaError_t simt_conv_dgrad(int prec, const DgradArgs &a, cudaStream_t st) {
 }
 cudaError_t simt_conv_wgrad(int prec, const WgradArgs &a, cudaStream_t st) {
     if (a.b <= a.a) return cudaSuccess;
+    if (a.dg && !a.w) return cudaErrorInvalidValue;
+    a.dg_done = a.dg != nullptr;
     dim3 g(a.c_out * a.k * a.k, (a.x.Cp + 31) / 32);
     if (prec) launch_simt(k_conv_wgrad<bf16>, g, 256, 0, st, a); else launch_simt(k_conv_wgrad<float>, g, 256, 0, st, a);
     return cudaGetLastError();
 }
 cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
-    if (a.b <= a.a || a.epi == 0) return cudaSuccess;
+    if (a.b <= a.a || !a.db) return cudaSuccess;
     const int CVall = a.dy.Cp / 8;
     if (CVall < 1 || a.dy.Cp % 8) return cudaErrorInvalidValue;
     const int CV = CVall < 64 ? CVall : 64, groups = (CVall + CV - 1) / CV;
@@ -1056,7 +1026,7 @@ cudaError_t simt_param_grad(int prec, const ParamGradArgs &a, cudaStream_t st) {
     if (g > cap) g = cap;
     if (g < 1) g = 1;
     dim3 grid((unsigned)g, groups);
-    size_t shm = 2 * sizeof(float) * blk.y * CV * 8;
+    size_t shm = sizeof(float) * blk.y * CV * 8;
     if (prec) launch_simt(k_param_grad<bf16>, grid, blk, shm, st, a); else launch_simt(k_param_grad<float>, grid, blk, shm, st, a);
     return cudaGetLastError();
 }

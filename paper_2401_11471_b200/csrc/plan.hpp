@@ -106,7 +106,9 @@ struct Plan {
     const void *fwd_params = nullptr, *fwd_x = nullptr;
     void *fwd_ws = nullptr;
     long long launches = 0, tc_launches = 0;
+    long long simt_fallbacks = 0;            // convs a bf16 tensor-core plan ran on SIMT (declined shapes)
     bool profiling = false;
+    std::vector<void *> capture;             // lrcnn_debug_capture buffers per tensor id (debug)
     ProfileSlot prof[3];
     void *ev_wt = nullptr;                   // transposed dgrad weights written (side stream, during FP)
     bool wt_pending = false;                 // FP launched the transposes; BP waits on ev_wt
@@ -122,7 +124,7 @@ struct Plan {
     void *graph_exec[2] = {nullptr, nullptr};    // cudaGraphExec_t
     uintptr_t graph_key[2][9] = {};
     int graph_calls[2] = {0, 0};                 // consecutive calls with the same key
-    long long graph_launches[2] = {0, 0}, graph_tc_launches[2] = {0, 0};
+    long long graph_launches[2] = {0, 0}, graph_tc_launches[2] = {0, 0}, graph_simt_fallbacks[2] = {0, 0};
     // side stream for wgrad / parameter reductions (overlap with the dgrad chain) and its events
     void *side_stream = nullptr, *ev_fork = nullptr, *ev_join = nullptr;
     // data-parallel replicas (LRCNN_FLAG_DP): replica count / index, per-segment gradient buckets

@@ -24,6 +24,7 @@ FLAG_BALANCED_BANDS = 4
 FLAG_NO_FUSE_RES = 8
 FLAG_FP_MERGE = 16
 FLAG_DP = 32
+FLAG_REQUIRE_TC = 64
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 
@@ -67,7 +68,8 @@ EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_turning_point", "lrcnn
            "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_profile_kernels", "lrcnn_plan_shard", "lrcnn_plan_xfers",
            "lrcnn_comm_nccl_unique_id", "lrcnn_comm_init_nccl", "lrcnn_comm_loopback_group",
            "lrcnn_comm_loopback_group_free", "lrcnn_comm_init_loopback", "lrcnn_comm_free", "lrcnn_plan_set_comm",
-           "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_error", "lrcnn_version"]
+           "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_simt_fallbacks", "lrcnn_debug_capture",
+           "lrcnn_last_error", "lrcnn_version"]
 
 _lib = None
 
@@ -116,6 +118,8 @@ def lib():
     L.lrcnn_comm_free.argtypes = [vp]
     L.lrcnn_plan_set_comm.argtypes = [vp, vp]
     L.lrcnn_last_tc_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+    L.lrcnn_last_simt_fallbacks.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+    L.lrcnn_debug_capture.argtypes = [vp, i, vp]
     L.lrcnn_last_error.restype = ctypes.c_char_p
     L.lrcnn_version.restype = ctypes.c_char_p
     for n in EXPORTS:
@@ -405,6 +409,17 @@ class Plan:
         n = ctypes.c_longlong()
         _check(lib().lrcnn_last_tc_launch_count(self.h, ctypes.byref(n)))
         return n.value
+
+    def last_simt_fallbacks(self):
+        """Convolution launches of a bf16 tensor-core plan that ran on SIMT (lrcnn_last_simt_fallbacks)."""
+        n = ctypes.c_longlong()
+        _check(lib().lrcnn_last_simt_fallbacks(self.h, ctypes.byref(n)))
+        return n.value
+
+    def debug_capture(self, tid, buf):
+        """lrcnn_debug_capture: the forward copies every band's rows of tensor tid into buf
+        ([B][H][W][Cp] tensor of the plan's dtype); buf=None unregisters (parity tests only)."""
+        _check(lib().lrcnn_debug_capture(self.h, tid, _ptr(buf)))
 
 
 class Comm:
