@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--hw", type=int, default=0)
     ap.add_argument("--mode", default="2ps", choices=["2ps", "overl", "column"])
-    ap.add_argument("--segments", default="pool", choices=["pool", "none"])
+    ap.add_argument("--segments", default="pool",
+                    help="checkpoint segments (2PS-H): pool = after every pool (VGG) / stage (ResNet); none = "
+                         "whole-net 2PS; ResNet cut string, e.g. 3 = one checkpoint after conv3_x, p234 = stage")
     ap.add_argument("--n-bands", type=int, default=None,
                     help="bands of the largest segment (default: 4; 8 for the climate-scale C4 / C5, where "
                          "it meets the north star's >= 5x feature-map reduction vs layer-wise)")
@@ -141,8 +143,8 @@ def make_net(a):
     if a.hw:
         H = W = a.hw
     if model == "vgg16":
-        return WL.vgg16(H=H, W=W, segments=a.segments)
-    return WL.resnet50(H=H, W=W, segments="stage" if a.segments == "pool" else "none")
+        return WL.vgg16(H=H, W=W, segments=a.segments if a.segments in ("pool", "none") else "pool")
+    return WL.resnet50(H=H, W=W, segments="stage" if a.segments == "pool" else a.segments)
 
 
 def cpu_baseline(a, steps=1):
@@ -562,6 +564,10 @@ def main():
     fm = peak - xi
     mem_rep = {"peak_allocated_bytes": peak, "xi_bytes": xi, "feature_map_bytes": fm,
                "omega_eq3_bytes": mem["omega"], "reduction_vs_omega_x": mem["omega"] / max(1, fm),
+               # Eq. (3) sums the op outputs l = 1..L; the input batch (bf16, channels padded 3 -> 8
+               # for 16-byte TMA pixels) is data, like xi: the same ratio without it
+               "input_batch_bytes": xi_bytes, "feature_map_excl_input_bytes": fm - xi_bytes,
+               "reduction_vs_omega_excl_input_x": mem["omega"] / max(1, fm - xi_bytes),
                "plan": {k: mem[k] for k in ("omega", "band_act", "band_delta", "halo_cache", "carry",
                                             "checkpoints", "delta_full", "workspace")}}
     cpu = None

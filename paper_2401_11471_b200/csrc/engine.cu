@@ -120,21 +120,6 @@ static View act_view(Run &R, const Segment &S, int r, int t) {
     return band_view(R.ws + ti.act_off, ti, S.lo[r][t], S.b[r][t]);
 }
 
-// A band-internal tensor without ReLU whose only reader is the residual input of a convolution u
-// (ResNet's projection shortcut) has delta(t) == delta(out_u) on the same rows: the residual add
-// passes the gradient through and there is no gate.  Its delta is that buffer (no memset, no copy
-// pass).  Returns u's output tensor, or -1.
-static int alias_delta(const Plan &P, const Segment &S, int t) {
-    if (t == 0 || t == S.in_t || t == S.out_t) return -1;
-    const TensorInfo &ti = P.t[t];
-    if (ti.relu || ti.cons.size() != 1 || ti.cons[0].role != 1) return -1;
-    const OpInfo &u = P.op[ti.cons[0].op];
-    if (u.d.kind != LRCNN_OP_CONV || u.d.res != t) return -1;
-    const TensorInfo &to = P.t[u.out_t];
-    if (to.Cp != ti.Cp || to.W != ti.W || to.H != ti.H) return -1;
-    return u.out_t;
-}
-
 static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
     {
         const int al = alias_delta(R.P, S, t);
@@ -778,34 +763,43 @@ static lrcnn_status run_backward(Run &R) {
         const int N = (int)S.E.size();
         for (int r = N - 1; r >= 0; --r) {
             if (recompute && (st = band_forward(R, S, r, false, true)) != LRCNN_OK) return st;
-            // band delta buffers: zero, then the carry of band r+1 (R6)
-            for (int t : S.tensors) {
-                if (t == S.out_t || delta_overwrite(P, S, t) || alias_delta(P, S, t) >= 0) continue;
-                const TensorInfo &ti = P.t[t];
-                size_t rb = (size_t)ti.W * ti.Cp * R.E;
-                int rows = S.b[r][t] - S.lo[r][t];
-                if (rows > 0)
-                    CK(cudaMemset2DAsync(R.ws + ti.dlt_off, ti.cap * rb, 0, rows * rb, P.net.B, R.st));
-                if (P.opts.mode == LRCNN_2PS && r + 1 < N) {
-                    int clo = S.lo[r + 1][t], chi = S.a[r + 1][t];
-                    if (chi > clo) {
-                        if ((st = copy_rows(R, ti, R.ws + ti.dlt_off + (size_t)(clo - S.lo[r][t]) * rb, ti.cap,
-                                            R.ws + ti.carry_off, ti.carry_cap, chi - clo)) != LRCNN_OK) return st;
+            for (auto it = S.ops.rbegin(); it != S.ops.rend(); ++it) {
+                const int i = *it;
+                // delta slots first written by op i's backward (plan: delta_slots).  A slot that held
+                // an earlier tensor's delta in this band may still be read by that tensor's wgrad on
+                // the side stream: join it first.  Then zero the slot and add the carry of band r+1
+                // (R6), unless the single writer overwrites it.
+                bool join = false;
+                for (int t : S.tensors)
+                    if (t != S.out_t && P.t[t].dfw == i && P.t[t].dreuse) join = true;
+                if (join) CK(join_side(R));
+                for (int t : S.tensors) {
+                    const TensorInfo &ti = P.t[t];
+                    if (t == S.out_t || ti.dfw != i || delta_overwrite(P, S, t)) continue;
+                    size_t rb = (size_t)ti.W * ti.Cp * R.E;
+                    int rows = S.b[r][t] - S.lo[r][t];
+                    if (rows > 0)
+                        CK(cudaMemset2DAsync(R.ws + ti.dlt_off, ti.cap * rb, 0, rows * rb, P.net.B, R.st));
+                    if (P.opts.mode == LRCNN_2PS && r + 1 < N) {
+                        int clo = S.lo[r + 1][t], chi = S.a[r + 1][t];
+                        if (chi > clo) {
+                            if ((st = copy_rows(R, ti, R.ws + ti.dlt_off + (size_t)(clo - S.lo[r][t]) * rb, ti.cap,
+                                                R.ws + ti.carry_off, ti.carry_cap, chi - clo)) != LRCNN_OK) return st;
+                        }
                     }
                 }
-            }
-            for (auto it = S.ops.rbegin(); it != S.ops.rend(); ++it)
-                if ((st = op_backward(R, S, s, r, *it)) != LRCNN_OK) return st;
-            CK(join_side(R));
-            if (P.opts.mode == LRCNN_2PS && r > 0) {
-                for (int t : S.tensors) {
-                    if (t == S.out_t) continue;
-                    const TensorInfo &ti = P.t[t];
-                    int rows = S.a[r][t] - S.lo[r][t];
+                // the 2PS carry out of op i's output: its cached rows [lo_r, a_r) are complete once
+                // every consumer has run (all later in op order); copy them before the slot is reused
+                const int to = P.op[i].out_t;
+                if (P.opts.mode == LRCNN_2PS && r > 0 && to != S.out_t && P.t[to].dfw >= 0) {
+                    const TensorInfo &ti = P.t[to];
+                    int rows = S.a[r][to] - S.lo[r][to];
                     if (rows > 0 && (st = copy_rows(R, ti, R.ws + ti.carry_off, ti.carry_cap, R.ws + ti.dlt_off, ti.cap,
                                                     rows)) != LRCNN_OK) return st;
                 }
+                if ((st = op_backward(R, S, s, r, i)) != LRCNN_OK) return st;
             }
+            CK(join_side(R));
         }
         if (P.opts.world > 1 && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, dfull_view(R.ws + P.dfull_off[(s + 1) & 1], P.t[S.in_t]), true)) != LRCNN_OK)

@@ -46,6 +46,75 @@ static bool window_role(const OpInfo &o, int role) {
     return role == 0 && o.d.kind != LRCNN_OP_ADD;
 }
 
+// BP delta buffers of one segment's band, overlaid by liveness.  In the BP's reverse op order the
+// delta of an internal tensor t is written first by the backward of its last consumer (dfw) and read
+// last by the backward of its producer (dy of wgrad / dgrad / parameter sums).  A conv u whose
+// residual input r is band-internal may read delta(out_u) again while another consumer of r runs its
+// dgrad (the fused residual gradient), so delta(out_u) stays live until the first consumer of r; a
+// projection output aliased to delta(out_u) (alias_delta) gets no slot of its own and keeps out_u's
+// alive until its producer.  Tensors whose live intervals do not overlap share a slot (greedy interval
+// colouring by first write, best fit).  assign: set dlt_off (relative to the slot area), dfw, dlr,
+// dreuse.  Returns the bytes of the slot area.
+static size_t delta_slots(Plan &P, const Segment &S, size_t B, size_t E, bool assign) {
+    const int N = (int)S.E.size();
+    std::vector<int> ts;
+    std::vector<int> fw(P.t.size(), -1), lr(P.t.size(), -1);
+    std::vector<size_t> bytes(P.t.size(), 0);
+    for (int t : S.tensors) {
+        if (t == S.out_t || alias_delta(P, S, t) >= 0) continue;
+        const TensorInfo &ti = P.t[t];
+        int f = ti.producer;
+        for (const Consumer &c : ti.cons) f = std::max(f, c.op);
+        fw[t] = f;
+        lr[t] = ti.producer;
+        int cap = 0;
+        for (int r = 0; r < N; ++r) cap = std::max(cap, S.b[r][t] - S.lo[r][t]);
+        bytes[t] = align_up(B * std::max(cap, 1) * (size_t)ti.W * ti.Cp * E);
+        ts.push_back(t);
+    }
+    for (int i : S.ops) {
+        const OpInfo &u = P.op[i];
+        if (u.d.kind != LRCNN_OP_CONV || u.d.res < 0 || fw[u.out_t] < 0) continue;
+        const int r = u.d.res;
+        if (r == S.in_t || r == 0) continue;
+        for (const Consumer &c : P.t[r].cons) lr[u.out_t] = std::min(lr[u.out_t], c.op);
+    }
+    for (int t : S.tensors) {
+        const int al = alias_delta(P, S, t);
+        if (al >= 0 && fw[al] >= 0) lr[al] = std::min(lr[al], P.t[t].producer);
+    }
+    std::sort(ts.begin(), ts.end(), [&](int x, int y) { return fw[x] != fw[y] ? fw[x] > fw[y] : x < y; });
+    struct Slot { size_t bytes; int last_lr; };
+    std::vector<Slot> slots;
+    std::vector<int> slot_of(P.t.size(), -1);
+    std::vector<bool> reuse(P.t.size(), false);
+    for (int t : ts) {
+        int best = -1;
+        for (int k = 0; k < (int)slots.size(); ++k) {
+            if (slots[k].last_lr <= fw[t]) continue;                     // still live at t's first write
+            if (best < 0) { best = k; continue; }
+            const bool fits = slots[k].bytes >= bytes[t], bfits = slots[best].bytes >= bytes[t];
+            if (fits != bfits ? fits : (fits ? slots[k].bytes < slots[best].bytes : slots[k].bytes > slots[best].bytes))
+                best = k;
+        }
+        if (best < 0) { slots.push_back({bytes[t], lr[t]}); best = (int)slots.size() - 1; }
+        else { slots[best].bytes = std::max(slots[best].bytes, bytes[t]); slots[best].last_lr = lr[t]; reuse[t] = true; }
+        slot_of[t] = best;
+    }
+    std::vector<size_t> off(slots.size(), 0);
+    size_t total = 0;
+    for (size_t k = 0; k < slots.size(); ++k) { off[k] = total; total += slots[k].bytes; }
+    if (assign) {
+        for (int t : S.tensors) {
+            if (t == S.out_t) continue;
+            TensorInfo &ti = P.t[t];
+            ti.dfw = fw[t]; ti.dlr = lr[t]; ti.dreuse = reuse[t];
+            ti.dlt_off = slot_of[t] >= 0 ? off[slot_of[t]] : 0;
+        }
+    }
+    return total;
+}
+
 lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, Plan &P, std::string &err) {
     if (!net || !opts || !net->ops || net->n_ops < 1) { err = "null net/opts or no ops"; return LRCNN_E_ARG; }
     if (net->B < 1 || net->C < 1 || net->H < 1 || net->W < 1 || net->n_classes < 1) {
@@ -318,10 +387,10 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
                 ccap = std::max(ccap, S.a[r][t] - S.lo[r][t]);
             }
             const size_t rb = (size_t)P.t[t].W * P.t[t].Cp * Esz;
-            a += 2 * align_up(Bsz * std::max(cap, 1) * rb);
+            a += align_up(Bsz * std::max(cap, 1) * rb);
             if (ccap > 0 && opts->mode == LRCNN_2PS) a += align_up(Bsz * ccap * rb);
         }
-        return a;
+        return a + delta_slots(P, S, Bsz, Esz, false);
     };
     for (Segment &S : P.seg) {
         lrcnn_status st = make_bands(S, 0);
@@ -452,9 +521,15 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             }
             ti.cap = std::max(cap, 1);
             ti.act_off = sub(B * ti.cap * rowbytes(t)); act += B * ti.cap * rowbytes(t);
-            ti.dlt_off = sub(B * ti.cap * rowbytes(t)); dl += B * ti.cap * rowbytes(t);
             ti.carry_cap = ccap;
             if (ccap > 0 && opts->mode == LRCNN_2PS) { ti.carry_off = sub(B * ccap * rowbytes(t)); car += B * ccap * rowbytes(t); }
+        }
+        {   // delta slots (liveness overlay), after the activation and carry buffers
+            dl = delta_slots(P, S, B, E, true);
+            const size_t d0 = a;
+            a = align_up(a + dl);
+            for (int t : S.tensors)
+                if (t != S.out_t && P.t[t].dfw >= 0) P.t[t].dlt_off += arena0 + d0;
         }
         if (a > arena_max) { arena_max = a; M.band_act = act; M.band_delta = dl; M.carry = car; }
     }

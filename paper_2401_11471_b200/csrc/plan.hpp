@@ -41,6 +41,10 @@ struct TensorInfo {
     // decoupled FP bands (LRCNN_FLAG_FP_MERGE): FP band buffer (aliases the band arena)
     size_t act_fp_off = 0;
     int cap_fp = 0;
+    // BP delta slot (delta_slots): live from the backward of op dfw (first writer) down to op dlr
+    // (last reader); dreuse = the slot held an earlier tensor's delta in the same band
+    int dfw = -1, dlr = -1;
+    bool dreuse = false;
 };
 
 struct OpInfo {
@@ -136,6 +140,21 @@ struct Plan {
 
 // Builds the plan; returns status and fills err on failure.
 lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, Plan &P, std::string &err);
+
+// A band-internal tensor without ReLU whose only reader is the residual input of a convolution u
+// (ResNet's projection shortcut) has delta(t) == delta(out_u) on the same rows: the residual add
+// passes the gradient through and there is no gate.  Its delta is that buffer (no memset, no copy
+// pass).  Returns u's output tensor, or -1.
+inline int alias_delta(const Plan &P, const Segment &S, int t) {
+    if (t == 0 || t == S.in_t || t == S.out_t) return -1;
+    const TensorInfo &ti = P.t[t];
+    if (ti.relu || ti.cons.size() != 1 || ti.cons[0].role != 1) return -1;
+    const OpInfo &u = P.op[ti.cons[0].op];
+    if (u.d.kind != LRCNN_OP_CONV || u.d.res != t) return -1;
+    const TensorInfo &to = P.t[u.out_t];
+    if (to.Cp != ti.Cp || to.W != ti.W || to.H != ti.H) return -1;
+    return u.out_t;
+}
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 inline int out_dim(int h, int k, int s, int p) {

@@ -1,12 +1,13 @@
 #!/bin/bash
 # One GPU session: pytest -m gpu, smoke, bench (default C4) -> gpurun_out/<tag>_*
-# usage: bash scripts/gpu_run.sh <tag> [pytest -k expr] [extra bench args]
+# usage: bash scripts/gpu_run.sh <tag> [pytest -k expr or ""] [extra bench args...]
 set -u
-TAG=${1:-run}; K=${2:-}; shift 2 2>/dev/null; EXTRA="$*"
+TAG=${1:-run}; K=${2:-}
+EXTRA="${@:3}"
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 if [ -n "$K" ]; then
-  timeout 2400 python -m pytest tests -m gpu -x -q -k "$K" > gpurun_out/${TAG}_pytest.txt 2>&1
+  timeout 2400 python -m pytest tests -m gpu -q -k "$K" > gpurun_out/${TAG}_pytest.txt 2>&1
 else
   timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest.txt 2>&1
 fi

@@ -75,15 +75,16 @@ def conditioned_grads(net, params, ts, aux, dzl):
 
 
 def compare_grads(g, g_ref, tol, tag=""):
-    worst = 0.0
+    """rel(T) <= tol for every gradient tensor; on failure the message lists the five worst."""
+    errs = []
     for i, (a, b) in enumerate(zip(g, g_ref)):
         if b is None:
             continue
         for k in b:
-            e = rel(a[k], b[k])
-            worst = max(worst, e)
-            assert e <= tol, (tag, "op", i, k, e)
-    return worst
+            errs.append((rel(a[k], b[k]), i, k))
+    errs.sort(reverse=True)
+    assert not errs or errs[0][0] <= tol, (tag, "worst (rel, op, param):", errs[:5])
+    return errs[0][0] if errs else 0.0
 
 
 def strip_rows(net, zl_rows):

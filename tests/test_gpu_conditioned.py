@@ -106,11 +106,11 @@ def test_c2_full_size_every_gradient_vs_oracle():
 
 def test_c4_full_size_every_gradient_vs_oracle():
     """C4 exactly as bench.py runs it (ResNet-50 3600x2400, B = 8, 2PS-H per stage, 8 balanced
-    bands, decoupled FP bands, tcgen05 only).  delta^L is non-zero on the top 2 rows of image 0's
+    bands, decoupled FP bands, tcgen05 only).  delta^L is non-zero on the top 6 rows of image 0's
     z^L only; their dependency cone (oracle.enumerate.need_sets) lies in the top rows of every
     tensor, so the oracle follows every gradient exactly on a strip of image 0 while the GPU runs
     the full-size step."""
-    H, W, B, j = 3600, 2400, 8, 2
+    H, W, B, j = 3600, 2400, 8, 6
     net = WL.resnet50(H=H, W=W, segments="stage")
     cone = strip_rows(net, j)
     Hs = cone[0][1]
@@ -167,16 +167,21 @@ def test_bench_step_bf16_vs_oracle_step():
     new_ref = C.sgd(params, g_ref, hg, lr)
     got, head = plan.unpack_grads(ds.master.cpu().numpy())
     assert np.all(ds.grads.cpu().numpy() == 0)
+
+    def upd_ok(old, new_gpu, new_oracle, tag):
+        # the update as the fp32 master stores it: lr * g to 2e-2 of its max, plus the fp32 rounding
+        # of theta - lr * g (a few ulp of |theta|)
+        d_ref, d_got = old - new_oracle, old - new_gpu
+        slack = TOL["bf16"] * np.max(np.abs(d_ref)) + 4 * np.finfo(np.float32).eps * np.abs(old)
+        assert np.all(np.abs(d_got - d_ref) <= slack), (tag, float(np.max(np.abs(d_got - d_ref) - slack)))
+
     for i, b in enumerate(new_ref["convs"]):
         if b is None:
             continue
         for k in b:
-            d_ref = params["convs"][i][k] - b[k]
-            d_got = params["convs"][i][k] - got[i][k]
-            assert rel(d_got, d_ref) <= TOL["bf16"], (i, k, rel(d_got, d_ref))
+            upd_ok(params["convs"][i][k], got[i][k], b[k], (i, k))
     for k in ("fc_w", "fc_b"):
-        d_ref = params["head"][k] - new_ref["head"][k]
-        assert rel(params["head"][k] - head[k], d_ref) <= TOL["bf16"], k
+        upd_ok(params["head"][k], head[k], new_ref["head"][k], k)
 
 
 def test_head_many_classes_fp32():

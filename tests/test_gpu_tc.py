@@ -33,17 +33,20 @@ def run(net, B, mode, params, x, dzl, flags=0, **kw):
     return zl, g
 
 
-@pytest.mark.parametrize("cin,cout,H,W,k,p", [(64, 64, 20, 37, 3, 1), (64, 128, 9, 16, 3, 1),
-                                              (128, 256, 7, 7, 3, 1), (256, 512, 5, 11, 3, 1),
-                                              (64, 64, 13, 29, 1, 0), (64, 192, 12, 40, 3, 0),
-                                              (256, 128, 9, 23, 1, 0), (512, 256, 6, 17, 1, 0)])
-def test_two_conv_layers_vs_oracle(cin, cout, H, W, k, p):
-    """conv(8->cin) [SIMT] then conv(cin->cout) [tcgen05 FP, dgrad into the first layer's delta,
-    wgrad]; bands of 3 rows (2PS) and one band (column)."""
+@pytest.mark.parametrize("cin,cout,H,W,k,p,epi", [(64, 64, 20, 37, 3, 1, "bias"), (64, 128, 9, 16, 3, 1, "bias"),
+                                                  (128, 256, 7, 7, 3, 1, "bias"), (256, 512, 5, 11, 3, 1, "bias"),
+                                                  (64, 64, 13, 29, 1, 0, "bias"), (64, 192, 12, 40, 3, 0, "bias"),
+                                                  (256, 128, 9, 23, 1, 0, "bias"), (512, 256, 6, 17, 1, 0, "bias"),
+                                                  (64, 64, 20, 37, 3, 1, "affine"), (64, 64, 13, 29, 1, 0, "affine"),
+                                                  (128, 256, 7, 19, 3, 1, "affine"), (256, 64, 9, 23, 1, 0, "affine")])
+def test_two_conv_layers_vs_oracle(cin, cout, H, W, k, p, epi):
+    """conv(8->cin) then conv(cin->cout) [tcgen05 FP, dgrad into the first layer's delta, wgrad with
+    the bias / beta and gamma gradients fused (dgamma = sum_{tap,ci} W * dW_raw)]; bands of 3 rows
+    (2PS) and one band (column)."""
     net = {"C": 3, "H": H, "W": W, "classes": 10,
-           "ops": [WL.conv(0, cin, 3, 1, 1), WL.conv(1, cout, k, 1, p), WL.conv(2, 64, 3, 1, 1)]}
+           "ops": [WL.conv(0, cin, 3, 1, 1), WL.conv(1, cout, k, 1, p, epi=epi), WL.conv(2, 64, 3, 1, 1)]}
     B = 2
-    params = WL.make_params(net, seed=5, bias_scale=0.1, bf16=True)
+    params = WL.make_params(net, seed=5, bias_scale=0.1, gamma_spread=0.3, bf16=True)
     x = WL.make_input(net, B, seed=3, bf16=True)
     ts, aux = C.forward(net, params, x, store=C.bf16_store)
     dzl = WL.make_dzl(ts[-1].shape, bf16=True)

@@ -218,9 +218,71 @@ def test_c1_cache_is_k_minus_s():
 
 
 # ---------------------------------------------------------------- balanced bands
+def _delta_slot_bytes(net, seg, bands, shp, B, E, cps):
+    """BP delta buffers under liveness overlay: in reverse op order the delta of an
+    internal tensor t lives from the backward of its last consumer to that of its producer (extended
+    to the first consumer of r for the output of a conv with internal residual input r; a projection
+    output read only as a residual shares its reader's delta); non-overlapping tensors share a slot
+    (greedy by first write, best fit).  Returns the slot bytes."""
+    seg_in, ids, out = seg
+    align = lambda v: (v + 255) // 256 * 256
+    ops = net["ops"]
+    cons = {}
+    for i in ids:
+        op = ops[i]
+        cons.setdefault(op["src"], []).append((i, 0))
+        if op.get("res", -1) is not None and op.get("res", -1) >= 0:
+            cons.setdefault(op["res"], []).append((i, 1))
+    internal = [i + 1 for i in ids if i + 1 != out]
+
+    def alias(t):
+        op_t = ops[t - 1]
+        c = cons.get(t, [])
+        if op_t.get("relu") or len(c) != 1 or c[0][1] != 1:
+            return -1
+        u = ops[c[0][0]]
+        if u["kind"] != "conv" or u["res"] != t or shp[c[0][0] + 1] != shp[t] or cps[c[0][0] + 1] != cps[t]:
+            return -1
+        return c[0][0] + 1
+    fw, lr, size = {}, {}, {}
+    for t in internal:
+        if alias(t) >= 0:
+            continue
+        fw[t] = max([t - 1] + [i for i, _ in cons.get(t, [])])
+        lr[t] = t - 1
+        cap = max(max(b[t][2] - b[t][0] for b in bands), 1)
+        size[t] = align(B * cap * shp[t][2] * cps[t] * E)
+    for i in ids:
+        op = ops[i]
+        if op["kind"] == "conv" and op["res"] >= 0 and (i + 1) in fw and op["res"] != seg_in and op["res"] != 0:
+            lr[i + 1] = min([lr[i + 1]] + [j for j, _ in cons.get(op["res"], [])])
+    for t in internal:
+        a = alias(t)
+        if a >= 0 and a in fw:
+            lr[a] = min(lr[a], t - 1)
+    slots = []   # [bytes, last_lr]
+    for t in sorted(fw, key=lambda t: (-fw[t], t)):
+        best = -1
+        for k, (by, last) in enumerate(slots):
+            if last <= fw[t]:
+                continue
+            if best < 0:
+                best = k
+                continue
+            fits, bfits = by >= size[t], slots[best][0] >= size[t]
+            if (fits != bfits and fits) or (fits == bfits and (by < slots[best][0] if fits else by > slots[best][0])):
+                best = k
+        if best < 0:
+            slots.append([size[t], lr[t]])
+        else:
+            slots[best] = [max(slots[best][0], size[t]), lr[t]]
+    return sum(s[0] for s in slots)
+
+
 def _arena_bytes(net, seg, bands, shp, B, E, cps):
-    """Band working set of one segment from the oracle enumerator's rows: act + delta buffers
-    (rows [lo, b) of every internal tensor, max over bands) plus the 2PS carry rows [lo, a)."""
+    """Band working set of one segment from the oracle enumerator's rows: activation buffers (rows
+    [lo, b) of every internal tensor, max over bands), the 2PS carry rows [lo, a) and the
+    liveness-overlaid delta slots."""
     seg_in, ids, out = seg
     align = lambda v: (v + 255) // 256 * 256
     tot = 0
@@ -230,10 +292,10 @@ def _arena_bytes(net, seg, bands, shp, B, E, cps):
         cap = max(max(b[t][2] - b[t][0] for b in bands), 1)
         ccap = max(b[t][1] - b[t][0] for b in bands)
         rb = shp[t][2] * cps[t] * E
-        tot += 2 * align(B * cap * rb)
+        tot += align(B * cap * rb)
         if ccap > 0:
             tot += align(B * ccap * rb)
-    return tot
+    return tot + _delta_slot_bytes(net, seg, bands, shp, B, E, cps)
 
 
 @pytest.mark.parametrize("which", ["vgg", "resnet", "random"])

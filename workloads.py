@@ -74,9 +74,12 @@ def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, block
         a = relu(aff(conv1x1(x)));  b = relu(aff(conv3x3/s(a)));  sc = aff(conv1x1/s(x)) or x
         out = relu(aff(conv1x1(b)) + sc)      (the residual add is fused into the last conv)
     segments: "stage" checkpoints after the stem max-pool and after every stage but the last
-    (2PS-H / OverL-H), "none" = whole-net row-centric."""
+    (2PS-H / OverL-H), "none" = whole-net row-centric, or a string naming the cut points: "p" the
+    stem max-pool, "2" / "3" / "4" the end of conv2_x / conv3_x / conv4_x (e.g. "3": one checkpoint
+    after conv3_x; "stage" == "p234")."""
     d = lambda c: max(8, c // width_div)
-    ops = [conv(0, d(64), 7, 2, 3, epi="affine"), maxpool(1, 3, 2, 1, seg_end=(segments == "stage"))]
+    cuts = {"stage": "p234", "none": ""}.get(segments, segments)
+    ops = [conv(0, d(64), 7, 2, 3, epi="affine"), maxpool(1, 3, 2, 1, seg_end=("p" in cuts))]
     t, cin = 2, d(64)
     for si, (nb, w) in enumerate(zip(blocks, (64, 128, 256, 512))):
         for bi in range(nb):
@@ -93,7 +96,7 @@ def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, block
                 sc = x
             ops.append(conv(b, d(4 * w), 1, 1, 0, epi="affine", relu=True, res=sc))
             t = len(ops)
-        if segments == "stage" and si < len(blocks) - 1:
+        if str(si + 2) in cuts and si < len(blocks) - 1:
             ops[-1]["seg_end"] = True
     ops[-1]["seg_end"] = False
     return {"C": C, "H": H, "W": W, "classes": classes, "ops": ops, "name": "resnet50"}
