@@ -105,6 +105,9 @@ typedef struct {
     int rank, world;  /* row sharding across ranks (world > 1), or data-parallel
                          replicas with LRCNN_FLAG_DP; world == 1: a single GPU */
     int flags;        /* LRCNN_FLAG_* */
+    int first_rows_pm;/* > 0 (with n_bands > 1): band 1 owns round(H * first_rows_pm / 1000) rows of each
+                         segment output, the other n_bands - 1 bands split the rest near-equally -- the
+                         greedy first band of Eq. (12), PAPER.md:297-310 (lrcnn_plan_greedy); 0 = off */
 } lrcnn_plan_opts;
 
 #define LRCNN_FLAG_ALLOW_OVERLAP_EXHAUSTION 1  /* OverL: do not reject N > H/o^0 */
@@ -139,6 +142,11 @@ typedef struct {
  * the flag such convolutions run on SIMT and are counted (lrcnn_last_simt_fallbacks).  A tensor-core
  * launch that FAILS (launch or attribute error) is always LRCNN_E_CUDA, never a SIMT rerun. */
 #define LRCNN_FLAG_REQUIRE_TC 64
+/* sqrt(n) checkpointing ("determine the optimal checkpoint locations ... Ref. [34]",
+ * PAPER.md:584 "a preferred checkpointing frequency is sqrt(n)"): the net's seg_end flags are
+ * replaced by ceil(sqrt(n_ops)) - 1 checkpoints, each at the valid cut (an op output that no other
+ * tensor is read past) nearest to an even spacing of the ops.  lrcnn_plan_seg reports them. */
+#define LRCNN_FLAG_AUTO_SEGMENTS 128
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 
@@ -174,6 +182,14 @@ LRCNN_API lrcnn_status lrcnn_plan_free(lrcnn_plan_t *plan);
  * Host only.  LRCNN_E_INFEASIBLE if no band count fits; LRCNN_E_ARG for COLUMN mode. */
 LRCNN_API lrcnn_status lrcnn_plan_budget(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, size_t budget_bytes,
                                          int max_bands, lrcnn_plan_t **out, int *n_bands);
+/* The 2PS greedy partitioning of Eq. (12): "max H_1^L and min N_BP" s.t. the
+ * memory fits.  For N = 1 .. max_bands (the smallest first), the largest first band (first_rows_pm
+ * on a grid of 1/64 of the segment outputs, from the whole height down to an equal split) whose
+ * exact workspace (lrcnn_plan_sizes, reading R9/R10 of DESIGN.md) is <= budget_bytes; the other
+ * N - 1 bands split the remaining rows.  Returns that plan in *out, N in *n_bands and the first band's
+ * share in *first_pm (0 when the equal split is taken).  LRCNN_E_INFEASIBLE if no (N, H_1) fits.  Host only. */
+LRCNN_API lrcnn_status lrcnn_plan_greedy(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, size_t budget_bytes,
+                                         int max_bands, lrcnn_plan_t **out, int *n_bands, int *first_pm);
 /* The turning point: the n_bands in 1 .. max_bands with the smallest
  * workspace -- past it the 2PS halo cache (growing with N) outweighs the shrinking band working
  * set.  Ties go to the smaller N.  Host only. */

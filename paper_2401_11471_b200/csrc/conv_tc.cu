@@ -139,14 +139,16 @@ static constexpr int kConvThreads = 320;      // k_conv_tc: producer, MMA, 8 epi
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
 static constexpr int kOutStage = 128 * 128;       // epilogue staging: 128 pixels x 64 channels bf16
-template <int BN, int KC = 64>
+template <int BN, int KC = 64, int NBUF = 4>
 struct ConvCfg {
     static constexpr int kA = 128 * KC * 2, kB = BN * KC * 2;
     static constexpr int kStageBytes = kA + kB;
-    // BN <= 128: two (delta, activation) staging pairs (double-buffered dgrad epilogue)
-    // four 16 KB staging buffers: FP stores / residual loads run up to three 64-channel groups
-    // ahead; dgrad: two (delta, activation) pairs (double-buffered epilogue)
-    static constexpr int kOutBufs = 4;
+    // NBUF 16 KB staging buffers: FP stores / residual loads run up to NBUF-1 64-channel groups
+    // ahead; dgrad: NBUF/2 (delta, activation) pairs, loads NBUF/2-1 items ahead.  NBUF = 8 (the
+    // small-K 1x1 convolutions: one or two K-steps per tile, bound by the epilogue's HBM traffic --
+    // residual / delta / activation tiles in, output tiles out -- not by the mainloop) keeps
+    // 112 KB of epilogue loads in flight per SM instead of 48 KB; it leaves two mainloop stages.
+    static constexpr int kOutBufs = NBUF;
     static constexpr int kBudget = 232448 - kOutBufs * kOutStage - 2048;
     static constexpr int kStages = kBudget / kStageBytes > 16 ? 16 : kBudget / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + kOutBufs * kOutStage + 1024 + 512;
@@ -474,7 +476,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
 // TMA loads of item k+1 are issued before item k's combine (once item k-1's store has read that
 // pair), so the HBM latency of the delta / activation tiles overlaps the current item instead of
 // being exposed once per tile (small-K layers: a 64-channel 3x3 dgrad tile is ~1200 MMA cycles).
-template <int BN, int NE = 4>
+template <int BN, int NE = 4, int NP = 2>
 __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
                                                       uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
                                                       uint8_t *stage_out, uint64_t *ebar, int warp, int lane,
@@ -503,9 +505,20 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         P.decode(tile, nt, tx, ty, b);
         return min(BN / 64, (P.n_out - nt * BN + 63) / 64);
     };
-    if (leader && (int)blockIdx.x < num_tiles) issue(blockIdx.x, 0, 0);
+    // item = (tile, group) of this CTA in order; item k uses pair k % NP; the first NP-1 are issued here
+    int it_tile = blockIdx.x, it_grp = 0;             // next item to issue
+    auto advance_issue = [&]() {
+        if (++it_grp == ngroups(it_tile)) { it_grp = 0; it_tile += gridDim.x; }
+    };
+    int ipair = 0;
+    if (leader)
+        for (int i = 0; i < NP - 1 && it_tile < num_tiles; ++i) {
+            issue(it_tile, it_grp, ipair);
+            ipair = ipair + 1 == NP ? 0 : ipair + 1;
+            advance_issue();
+        }
     int acc = 0, pi = 0;
-    uint32_t aphase = 0, ephase[2] = {0, 0};
+    uint32_t aphase = 0, ephase = 0;   // bit i: parity of the next completion of ebar[i]
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int nt, tx, ty, b;
         P.decode(tile, nt, tx, ty, b);
@@ -520,16 +533,15 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
 #pragma unroll
             for (int h = 0; h < CH / 32; ++h)
                 ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
-            if (leader) {   // prefetch the next item into the other pair (its last store has been read)
-                const int t2 = grp + 1 < ngrp ? tile : tile + (int)gridDim.x, g2 = grp + 1 < ngrp ? grp + 1 : 0;
-                if (t2 < num_tiles) {
-                    bulk_wait_read0();
-                    issue(t2, g2, pi ^ 1);
-                }
+            if (leader && it_tile < num_tiles) {   // prefetch NP-1 items ahead into the pair item k-1 used
+                bulk_wait_read0();                     // (its store, the latest committed, has read it)
+                issue(it_tile, it_grp, ipair);
+                ipair = ipair + 1 == NP ? 0 : ipair + 1;
+                advance_issue();
             }
             ptx::tmem_ld_wait();
-            ptx::mbar_wait(ebar + pi, ephase[pi]);
-            ephase[pi] ^= 1;
+            ptx::mbar_wait(ebar + pi, (ephase >> pi) & 1);
+            ephase ^= 1u << pi;
             const uint32_t rowD = ptx::smem_u32(stage_out + (2 * pi) * kOutStage) + m * 128;
             const uint32_t rowG = rowD + kOutStage;
 #pragma unroll
@@ -555,7 +567,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
                 tma_store_4d(tmO, stage_out + (2 * pi) * kOutStage, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
                 bulk_commit();
             }
-            pi ^= 1;
+            pi = pi + 1 == NP ? 0 : pi + 1;
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -656,12 +668,12 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
 // KC = input channels per pipeline stage: 64 (128-byte rows, SWIZZLE_128B, 4 MMAs of K=16) for
 // regular layers, 16 (32-byte rows, SWIZZLE_32B, 1 MMA) for small-channel layers (padded RGB
 // input of conv1_1 / the 7x7 stem), which would otherwise waste 8x tensor work on zero channels.
-template <int BN, int KC>
+template <int BN, int KC, int NBUF>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P,
               const __grid_constant__ CUtensorMap tmX) {
-    using Cfg = ConvCfg<BN, KC>;
+    using Cfg = ConvCfg<BN, KC, NBUF>;
     constexpr int S = Cfg::kStages;
     constexpr int ABYTES = Cfg::kA, BBYTES = Cfg::kB;
     constexpr uint32_t SBO = 8 * KC * 2;             // 8-row core-matrix groups
@@ -675,14 +687,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
-    uint64_t *ebar = tempty + 2;                     // 2 dgrad staging barriers
-    uint32_t *tslot = (uint32_t *)(ebar + 4);
+    uint64_t *ebar = tempty + 2;                     // NBUF staging barriers (dgrad pairs / residual ring)
+    uint32_t *tslot = (uint32_t *)(ebar + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
-        for (int i = 0; i < 4; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
+        for (int i = 0; i < NBUF; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -745,7 +757,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
     } else {
         if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
-        else if (P.tma_dg && Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
+        else if (P.tma_dg && Cfg::kOutBufs >= 4)
+            conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
     }
@@ -1914,6 +1927,23 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
 }
 
+// Warp transpose-sum: lane L holds p[0..31]; returns sum over the 32 lanes of p[L] (31 shuffles by
+// recursive halving: at width w a lane keeps the half of its remaining entries whose index bit w
+// matches its own lane bit and adds the partner's copy of that half).
+__device__ __forceinline__ float warp_tsum32(float (&p)[32], int lane) {
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const bool up = (lane & w) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const float send = up ? p[i] : p[i + w];
+            const float keep = up ? p[i + w] : p[i];
+            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+        }
+    }
+    return p[0];
+}
+
 // ------------------------------------------------------------------ wgrad, 64 output channels: tap pairs on M
 // For c_out <= 64 (VGG conv1_2, the ResNet stage-1 3x3) the M = 128 output-channel tile of
 // k_wgrad_halo is half empty.  Here the roles are swapped: M = 128 = two filter taps x 64 input
@@ -2050,18 +2080,17 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + p * 64 + c * 32, v);
                     ptx::tmem_ld_wait();
-                    if (P.dg) {   // dgamma[co] = sum_{tap,ci} W * (sum_p dy x): warp sum per co
+                    if (P.dg) {   // dgamma[co] = sum_{tap,ci} W * (sum_p dy x): warp transpose-sum, lane = co
+                        float pj[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const int co = c * 32 + j;
-                            float pj = keep && co < P.c_out
-                                           ? __uint_as_float(v[j]) *
-                                                 __bfloat162float(P.w[((long long)co * TAPS + t) * P.cin_p + ci])
-                                           : 0.f;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) pj += __shfl_xor_sync(0xffffffffu, pj, o);
-                            if (lane == j) dgacc[c] += pj;
+                            pj[j] = keep && co < P.c_out
+                                        ? __uint_as_float(v[j]) *
+                                              __bfloat162float(P.w[((long long)co * TAPS + t) * P.cin_p + ci])
+                                        : 0.f;
                         }
+                        dgacc[c] += warp_tsum32(pj, lane);
                     }
                     if (!keep) continue;
 #pragma unroll
@@ -2618,13 +2647,13 @@ static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 bool tc_available() { return true; }
 
-template <int BN, int KC>
+template <int BN, int KC, int NBUF = 4>
 static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
                         const CUtensorMap &G, const CUtensorMap &X, int tiles, cudaStream_t st) {
-    using Cfg = ConvCfg<BN, KC>;
-    if (!smem_attr((const void *)k_conv_tc<BN, KC>, Cfg::kSmem)) return false;
+    using Cfg = ConvCfg<BN, KC, NBUF>;
+    if (!smem_attr((const void *)k_conv_tc<BN, KC, NBUF>, Cfg::kSmem)) return false;
     int grid = tiles < num_sms() ? tiles : num_sms();
-    return launch_pdl(k_conv_tc<BN, KC>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P, X);
+    return launch_pdl(k_conv_tc<BN, KC, NBUF>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P, X);
 }
 
 template <int BN>
@@ -2813,6 +2842,13 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, G, X, tiles, st);
         if (BN == 128) return launch_conv<128, 16>(P, A, Bm, O, G, X, tiles, st);
         return launch_conv<256, 16>(P, A, Bm, O, G, X, tiles, st);
+    }
+    // small-K layers (one or two K-steps per tile: the 1x1 convolutions of ResNet's 64- / 128-wide
+    // bottleneck ends) are bound by the epilogue's tile traffic: the deep staging ring
+    static const int deep = env_int("LRCNN_DEEP_RING", 1);
+    if (deep && P.k_steps <= 2 && (P.tma_out || P.tma_dg)) {
+        if (BN == 256) return launch_conv<256, 64, 8>(P, A, Bm, O, G, X, tiles, st);
+        if (BN == 128) return launch_conv<128, 64, 8>(P, A, Bm, O, G, X, tiles, st);
     }
     if (BN == 64) return launch_conv<64, 64>(P, A, Bm, O, G, X, tiles, st);
     if (BN == 128) return launch_conv<128, 64>(P, A, Bm, O, G, X, tiles, st);

@@ -936,6 +936,44 @@ lrcnn_status lrcnn_plan_budget(const lrcnn_net_desc *net, const lrcnn_plan_opts 
                                         std::to_string(best_ws) + ")");
 }
 
+// The 2PS greedy of Eq. (12): min N_BP first, then the largest first band H_1^L
+// whose exact workspace fits; the first band is searched on a 1/64 grid of the segment outputs from
+// the whole height down to the equal split (first_pm = 0).
+lrcnn_status lrcnn_plan_greedy(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, size_t budget_bytes,
+                               int max_bands, lrcnn_plan_t **out, int *n_bands, int *first_pm) {
+    if (!out || !opts || !net) return fail(LRCNN_E_ARG, "net, opts or out is NULL");
+    *out = nullptr;
+    if (opts->mode != LRCNN_2PS) return fail(LRCNN_E_ARG, "the greedy first band is a 2PS plan");
+    if (max_bands < 1) return fail(LRCNN_E_ARG, "max_bands must be >= 1");
+    size_t best_ws = (size_t)-1;
+    for (int n = 1; n <= max_bands; ++n) {
+        const int grid = n == 1 ? 1 : 64;
+        for (int g = grid; g >= 1; --g) {
+            lrcnn_plan_opts o = *opts;
+            o.band_rows = 0;
+            o.n_bands = n;
+            o.first_rows_pm = n == 1 ? 0 : (int)((1000LL * g + grid / 2) / grid);
+            // below an equal first band the other bands would outgrow it: stop at the equal split
+            if (n > 1 && o.first_rows_pm * n < 1000) o.first_rows_pm = 0;
+            lrcnn_plan_t *p = nullptr;
+            if (lrcnn_plan(net, &o, &p) != LRCNN_OK) continue;
+            const size_t ws = p->P.ws_bytes;
+            if (ws <= budget_bytes) {
+                *out = p;
+                if (n_bands) *n_bands = n;
+                if (first_pm) *first_pm = o.first_rows_pm;
+                return LRCNN_OK;
+            }
+            best_ws = std::min(best_ws, ws);
+            lrcnn_plan_free(p);
+            if (o.first_rows_pm == 0) break;
+        }
+    }
+    return fail(LRCNN_E_INFEASIBLE, "no (N, H_1) with N <= " + std::to_string(max_bands) + " fits " +
+                                        std::to_string(budget_bytes) + " bytes (smallest workspace " +
+                                        std::to_string(best_ws) + ")");
+}
+
 // The paper's turning point: the band count whose workspace is the
 // smallest -- beyond it the 2PS halo cache, which grows with N, outweighs the shrinking band
 // working set.  Ties go to the smaller N (fewer, larger launches).

@@ -17,6 +17,7 @@
 //     lo = min_u max(0, lo_u*s - p),  hi = max_u min(H_t, (hi_u-1)*s - p + k).
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 
 #include "plan.hpp"
@@ -26,8 +27,25 @@ namespace lrcnn {
 static const size_t kAlign = 256;
 static size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-static std::vector<int> make_band_ends(int h_out, int band_rows, int n_bands) {
+// Band ends at a segment output of h_out rows: band_rows > 0 -> every band owns band_rows rows
+// (remainder to the last); else n_bands near-equal bands (earliest +1).  first_pm > 0 (the greedy
+// first band of Eq. (12)): band 1 owns round(h_out * first_pm / 1000) rows (at
+// least 1, leaving one row per other band) and the other n_bands - 1 bands split the rest.
+static std::vector<int> make_band_ends(int h_out, int band_rows, int n_bands, int first_pm = 0) {
     std::vector<int> E;
+    if (first_pm > 0 && band_rows <= 0 && n_bands > 1 && h_out >= 2) {
+        const int n = std::max(2, std::min(n_bands, h_out));
+        int h1 = (int)(((long long)h_out * first_pm + 500) / 1000);
+        h1 = std::max(1, std::min(h1, h_out - (n - 1)));
+        E.push_back(h1);
+        const int rest = h_out - h1, q = rest / (n - 1), rem = rest % (n - 1);
+        int acc = h1;
+        for (int r = 0; r < n - 1; ++r) {
+            acc += q + (r < rem ? 1 : 0);
+            E.push_back(acc);
+        }
+        return E;
+    }
     if (band_rows > 0) {
         for (int e = band_rows; e < h_out; e += band_rows) E.push_back(e);
         E.push_back(h_out);
@@ -177,6 +195,37 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     P.t[n_ops].is_zl = true;
 
     // ---------------------------------------------------------------- segments
+    if ((opts->flags & LRCNN_FLAG_AUTO_SEGMENTS) && opts->mode != LRCNN_COLUMN) {
+        // sqrt(n) checkpointing (PAPER.md:394 OverL-H / 2PS-H "determine the optimal checkpoint
+        // locations ... Ref. [34]", "a preferred checkpointing frequency is sqrt(n)"):
+        // the net's seg_end flags are replaced by ceil(sqrt(n)) - 1 checkpoints, n = number of ops,
+        // each at the valid cut (an op output no other tensor reaches past) nearest to j * n / sqrt(n)
+        std::vector<int> last_use(T, -1);
+        for (int i = 0; i < n_ops; ++i) {
+            last_use[P.ops_copy[i].src] = std::max(last_use[P.ops_copy[i].src], i);
+            if (P.ops_copy[i].res >= 0) last_use[P.ops_copy[i].res] = std::max(last_use[P.ops_copy[i].res], i);
+        }
+        std::vector<int> cuts;   // op i is a valid cut iff every tensor t <= i is last read at op <= i, except t = i + 1
+        int reach = -1;
+        for (int i = 0; i < n_ops - 1; ++i) {
+            reach = std::max(reach, last_use[i]);          // tensor i (produced by op i - 1, or the image)
+            if (reach <= i) cuts.push_back(i);
+        }
+        for (auto &o : P.ops_copy) o.seg_end = 0;
+        const int m = (int)std::ceil(std::sqrt((double)n_ops)) - 1;
+        int prev = -1;
+        for (int j = 1; j <= m && !cuts.empty(); ++j) {
+            const double target = (double)j * n_ops / (m + 1) - 1;
+            int best = -1;
+            for (int c : cuts)
+                if (c > prev && (best < 0 || std::fabs(c - target) < std::fabs(best - target))) best = c;
+            if (best < 0) break;
+            P.ops_copy[best].seg_end = 1;
+            prev = best;
+        }
+        P.net.ops = P.ops_copy.data();
+        for (int i = 0; i < n_ops; ++i) P.op[i].d.seg_end = P.ops_copy[i].seg_end;
+    }
     {
         Segment cur; cur.in_t = 0;
         for (int i = 0; i < n_ops; ++i) {
@@ -293,7 +342,8 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         const int own = S.own_hi - S.own_lo;
         if (opts->mode == LRCNN_COLUMN) S.E = {S.own_hi};
         else {
-            S.E = nb > 0 ? make_band_ends(own, 0, nb) : make_band_ends(own, opts->band_rows, opts->n_bands);
+            S.E = nb > 0 ? make_band_ends(own, 0, nb, opts->first_rows_pm)
+                         : make_band_ends(own, opts->band_rows, opts->n_bands, opts->first_rows_pm);
             for (int &e : S.E) e += S.own_lo;
         }
         for (size_t r = 1; r < S.E.size(); ++r)

@@ -25,6 +25,7 @@ FLAG_NO_FUSE_RES = 8
 FLAG_FP_MERGE = 16
 FLAG_DP = 32
 FLAG_REQUIRE_TC = 64
+FLAG_AUTO_SEGMENTS = 128
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 
@@ -50,7 +51,7 @@ class NetDesc(ctypes.Structure):
 class PlanOpts(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("prec", ctypes.c_int), ("band_rows", ctypes.c_int),
                 ("n_bands", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
-                ("flags", ctypes.c_int)]
+                ("flags", ctypes.c_int), ("first_rows_pm", ctypes.c_int)]
 
 
 class MemoryReport(ctypes.Structure):
@@ -62,7 +63,7 @@ class MemoryReport(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
-EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
+EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_greedy", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_fp_bands", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
            "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_profile_kernels", "lrcnn_plan_shard", "lrcnn_plan_xfers",
@@ -87,6 +88,8 @@ def lib():
     L.lrcnn_plan.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), ctypes.POINTER(vp)]
     L.lrcnn_plan_free.argtypes = [vp]
     L.lrcnn_plan_budget.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), sz, i, ctypes.POINTER(vp), ip]
+    L.lrcnn_plan_greedy.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), sz, i, ctypes.POINTER(vp), ip,
+                                    ip]
     L.lrcnn_plan_turning_point.argtypes = [ctypes.POINTER(NetDesc), ctypes.POINTER(PlanOpts), i, ip, szp]
     L.lrcnn_plan_sizes.argtypes = [vp, szp, szp, szp]
     L.lrcnn_plan_tensor.argtypes = [vp, i, ip, ip, ip, ip]
@@ -166,12 +169,14 @@ def net_ops(net):
 class Plan:
     """lrcnn_plan wrapper.  mode: column | 2ps | overl; prec: fp32 | bf16."""
 
-    def __init__(self, net, B, mode="2ps", prec="bf16", band_rows=None, n_bands=None, flags=0, rank=0, world=1):
+    def __init__(self, net, B, mode="2ps", prec="bf16", band_rows=None, n_bands=None, flags=0, rank=0, world=1,
+                 first_rows_pm=0):
         L = lib()
         self.net, self.B, self.mode, self.prec = net, B, mode, prec
         self._ops = net_ops(net)
         self._desc = NetDesc(len(net["ops"]), self._ops, B, net["C"], net["H"], net["W"], net["classes"])
-        self._opts = PlanOpts(MODES[mode], PRECS[prec], band_rows or 0, n_bands or 0, rank, world, flags)
+        self._opts = PlanOpts(MODES[mode], PRECS[prec], band_rows or 0, n_bands or 0, rank, world, flags,
+                              first_rows_pm)
         h = ctypes.c_void_p()
         _check(L.lrcnn_plan(ctypes.byref(self._desc), ctypes.byref(self._opts), ctypes.byref(h)))
         self.h = h
@@ -188,12 +193,32 @@ class Plan:
         self.net, self.B, self.mode, self.prec = net, B, mode, prec
         self._ops = net_ops(net)
         self._desc = NetDesc(len(net["ops"]), self._ops, B, net["C"], net["H"], net["W"], net["classes"])
-        self._opts = PlanOpts(MODES[mode], PRECS[prec], 0, 0, 0, 1, flags)
+        self._opts = PlanOpts(MODES[mode], PRECS[prec], 0, 0, 0, 1, flags, 0)
         h, nb = ctypes.c_void_p(), ctypes.c_int()
         _check(L.lrcnn_plan_budget(ctypes.byref(self._desc), ctypes.byref(self._opts), budget_bytes, max_bands,
                                    ctypes.byref(h), ctypes.byref(nb)))
         self.h = h
         self.n_bands = nb.value
+        ws, npar, zl = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        _check(L.lrcnn_plan_sizes(self.h, ctypes.byref(ws), ctypes.byref(npar), ctypes.byref(zl)))
+        self.ws_bytes, self.n_params, self.zl_elems = ws.value, npar.value, zl.value
+        self.elem = 2 if prec == "bf16" else 4
+        return self
+
+    @classmethod
+    def greedy(cls, net, B, budget_bytes, max_bands=64, prec="bf16", flags=0):
+        """lrcnn_plan_greedy (Eq. (12)): min N, then the largest first band, whose workspace fits."""
+        L = lib()
+        self = cls.__new__(cls)
+        self.net, self.B, self.mode, self.prec = net, B, "2ps", prec
+        self._ops = net_ops(net)
+        self._desc = NetDesc(len(net["ops"]), self._ops, B, net["C"], net["H"], net["W"], net["classes"])
+        self._opts = PlanOpts(MODES["2ps"], PRECS[prec], 0, 0, 0, 1, flags, 0)
+        h, nb, pm = ctypes.c_void_p(), ctypes.c_int(), ctypes.c_int()
+        _check(L.lrcnn_plan_greedy(ctypes.byref(self._desc), ctypes.byref(self._opts), budget_bytes, max_bands,
+                                   ctypes.byref(h), ctypes.byref(nb), ctypes.byref(pm)))
+        self.h = h
+        self.n_bands, self.first_rows_pm = nb.value, pm.value
         ws, npar, zl = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
         _check(L.lrcnn_plan_sizes(self.h, ctypes.byref(ws), ctypes.byref(npar), ctypes.byref(zl)))
         self.ws_bytes, self.n_params, self.zl_elems = ws.value, npar.value, zl.value
@@ -206,7 +231,7 @@ class Plan:
         L = lib()
         ops = net_ops(net)
         desc = NetDesc(len(net["ops"]), ops, B, net["C"], net["H"], net["W"], net["classes"])
-        opts = PlanOpts(MODES[mode], PRECS[prec], 0, 0, 0, 1, flags)
+        opts = PlanOpts(MODES[mode], PRECS[prec], 0, 0, 0, 1, flags, 0)
         n, ws = ctypes.c_int(), ctypes.c_size_t()
         _check(L.lrcnn_plan_turning_point(ctypes.byref(desc), ctypes.byref(opts), max_bands, ctypes.byref(n),
                                           ctypes.byref(ws)))

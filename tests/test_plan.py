@@ -430,3 +430,109 @@ def test_dp_replica_plan_is_the_single_gpu_plan():
                     assert p.rows(s, r, t) == p0.rows(s, r, t)
     with pytest.raises(LB.LrcnnError):
         LB.Plan(net, 2, mode="2ps", prec="bf16", n_bands=3, world=4, rank=4, flags=LB.FLAG_DP)
+
+
+# ---------------------------------------------------------------- Eq. (12) greedy, sqrt(n) checkpoints
+def _first_band_ends(h, n, pm):
+    """Band ends of the greedy first band (the lrcnn_plan_opts.first_rows_pm contract)."""
+    h1 = max(1, min(int((h * pm + 500) // 1000), h - (n - 1)))
+    rest = h - h1
+    q, rem = divmod(rest, n - 1)
+    E, acc = [h1], h1
+    for r in range(n - 1):
+        acc += q + (1 if r < rem else 0)
+        E.append(acc)
+    return E
+
+
+def test_first_band_rows_vs_enumerator():
+    """A large first band (first_rows_pm): every band's rows equal the enumerator's for those band ends."""
+    rng = np.random.default_rng(12)
+    for net in (WL.tiny3(p=1, H=40, W=8), WL.vgg16(H=96, W=32, width_div=16, segments="pool"),
+                WL.resnet50(H=128, W=32, width_div=8)):
+        shp = C.out_hw(net)
+        for _ in range(4):
+            n, pm = int(rng.integers(2, 5)), int(rng.integers(300, 900))
+            plan = LB.Plan(net, 2, mode="2ps", prec="bf16", n_bands=n, first_rows_pm=pm)
+            for s, seg in enumerate(EN.segments(net)):
+                h = shp[seg[2]][1]
+                if h < 2:
+                    continue
+                E = _first_band_ends(h, min(n, h), pm)
+                en = EN.enumerate_2ps(net, seg, E, shp)
+                assert plan.seg(s)[2] == len(E)
+                for r in range(len(E)):
+                    for t in [i + 1 for i in seg[1]]:
+                        assert plan.rows(s, r, t) == en[r][t], (net["name"], n, pm, s, r, t)
+
+
+@pytest.mark.parametrize("which", ["vgg", "resnet"])
+def test_greedy_eq12_is_lexicographic_optimum(which):
+    """lrcnn_plan_greedy: the smallest N for which some first band fits the budget, and at that N the
+    largest first band that fits (brute force over the same grid); the first band is the largest."""
+    net = WL.vgg16(H=160, W=64, width_div=4) if which == "vgg" else WL.resnet50(H=256, W=64, width_div=4, segments="none")
+    B = 2
+    ws1 = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=1).ws_bytes
+    for frac in (0.55, 0.7, 0.85):
+        budget = int(ws1 * frac)
+        try:
+            g = LB.Plan.greedy(net, B, budget, max_bands=12)
+        except LB.LrcnnError as e:
+            assert e.name == "E_INFEASIBLE"
+            continue
+        assert g.ws_bytes <= budget
+        n = g.n_bands
+
+        def feasible(nn, pm):
+            try:
+                return LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nn, first_rows_pm=pm).ws_bytes <= budget
+            except LB.LrcnnError:
+                return False
+        grid = [int((1000 * k + 32) // 64) for k in range(64, 0, -1)]
+        grid = [pm if pm * nn >= 1000 else 0 for nn in [n] for pm in grid]
+        for nn in range(1, n):
+            cand = [0] if nn == 1 else [pm if pm * nn >= 1000 else 0 for pm in
+                                        [int((1000 * k + 32) // 64) for k in range(64, 0, -1)]]
+            assert not any(feasible(nn, pm) for pm in cand), (frac, nn)
+        if n > 1 and g.first_rows_pm:
+            larger = [pm for pm in grid if pm > g.first_rows_pm]
+            assert not any(feasible(n, pm) for pm in larger), (frac, n, g.first_rows_pm)
+            E = [g.rows(g.nsegs() - 1, r, len(net["ops"]))[2] for r in range(n)]
+            sizes = [E[0]] + [E[r] - E[r - 1] for r in range(1, n)]
+            assert sizes[0] + 1 >= max(sizes[1:])      # (rounding of small outputs)
+
+
+def _valid_cuts(net):
+    """Ops whose output no other tensor is read past (a checkpoint there cuts the DAG)."""
+    last = {}
+    for i, op in enumerate(net["ops"]):
+        for t in (op["src"], op.get("res", -1)):
+            if t is not None and t >= 0:
+                last[t] = max(last.get(t, -1), i)
+    cuts = []
+    for i in range(len(net["ops"]) - 1):
+        if all(last.get(t, -1) <= i for t in range(0, i + 1)):
+            cuts.append(i)
+    return cuts
+
+
+def test_auto_segments_sqrt_n():
+    """LRCNN_FLAG_AUTO_SEGMENTS: ceil(sqrt(n)) - 1 checkpoints, all at valid cuts, spread
+    over the net (every segment between n / (2 sqrt(n)) and 2 n / sqrt(n) ops on a chain)."""
+    chain = {"C": 1, "H": 64, "W": 8, "classes": 3, "ops": [WL.conv(t, 4, 3, 1, 1) for t in range(25)]}
+    p = LB.Plan(chain, 1, mode="2ps", prec="fp32", n_bands=2, flags=LB.FLAG_AUTO_SEGMENTS)
+    assert p.nsegs() == 5
+    lens = [len([1 for t in range(p.seg(s)[0], p.seg(s)[1])]) for s in range(p.nsegs())]
+    assert all(2 <= L <= 10 for L in lens), lens
+    for net in (WL.resnet50(H=224, W=64, width_div=8, segments="none"), WL.vgg16(H=224, W=64, width_div=8)):
+        n = len(net["ops"])
+        p = LB.Plan(net, 1, mode="2ps", prec="bf16", n_bands=2, flags=LB.FLAG_AUTO_SEGMENTS)
+        want = int(np.ceil(np.sqrt(n))) - 1
+        assert p.nsegs() == want + 1, (net["name"], p.nsegs(), want)
+        cuts = set(_valid_cuts(net))
+        for s in range(p.nsegs() - 1):
+            assert p.seg(s)[1] - 1 in cuts
+        # the plan with these checkpoints equals the enumerator on the same segments
+        net2 = dict(net, ops=[dict(o, seg_end=(i + 1) in [p.seg(s)[1] for s in range(p.nsegs() - 1)])
+                              for i, o in enumerate(net["ops"])])
+        _check_plan_vs_enum(net2, "2ps", n_bands=2, B=1)
