@@ -18,7 +18,7 @@ elif cfg == "c3":
     net, B = WL.resnet50(H=224, W=224), 256
 else:
     net, B = WL.resnet50(H=3600, W=2400), 8
-plan = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb, flags=LB.FLAG_BALANCED_BANDS | LB.FLAG_FP_MERGE)   # = bench.py defaults
+plan = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb, flags=LB.FLAG_BALANCED_BANDS | LB.FLAG_FP_MERGE | LB.FLAG_REQUIRE_TC)   # = bench.py defaults
 ds = LB.DeviceState(plan)
 ds.load(params=WL.make_params(net, seed=2), x=WL.make_input(net, B, seed=1000), labels=WL.make_labels(net, B))
 st = torch.cuda.Stream()
