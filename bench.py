@@ -515,13 +515,33 @@ def main():
     # each kernel against the roofline its algorithmic intensity puts it under:
     # tensor-bound: algorithmic conv FLOPs / time vs the bf16 tensor peak; HBM-bound: algorithmic
     # bytes (every operand read once, every result written once) / time vs the measured copy bandwidth
+    # HBM writes alone sustain less than a copy on this GPU (measured here: a 1 GiB fill), so an
+    # HBM-bound kernel that writes more than it reads has a lower ceiling than the copy peak: its
+    # mixed roofline is bytes / max(bytes / copy_bw, written / write_bw) (reported beside `frac`)
+    wbuf = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    wbuf.fill_(1)
+    wts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        wbuf.fill_(0)
+        e1.record(stream)
+        e1.synchronize()
+        wts.append(e0.elapsed_time(e1))
+    write_gbs = wbuf.numel() / (min(wts) / 1000.0) / 1e9
+    del wbuf
+
     def _rl(k):
         sec = k["ms"] / 1000.0
         if sec <= 0:
             return {"bound": "tensor", "achieved": 0.0, "peak": peak_tf, "unit": "TFLOP/s", "frac": 0.0}
         if k.get("bytes", 0) > 0 and k["flops"] / k["bytes"] < ridge:
             gbs = k["bytes"] / sec / 1e9
-            return {"bound": "hbm", "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs}
+            t_min = max(k["bytes"] / (hbm_gbs * 1e9), k.get("wbytes", 0.0) / (write_gbs * 1e9))
+            mix = k["bytes"] / t_min / 1e9
+            return {"bound": "hbm", "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs,
+                    "write_share": k.get("wbytes", 0.0) / k["bytes"],
+                    "mixed_rw_roofline": {"peak": mix, "frac": gbs / mix, "write_gbs_measured": write_gbs}}
         tf = k["flops"] / sec / 1e12
         return {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": tf / peak_tf}
     # the dominant kernel: the tcgen05 kernel with the largest share of the step (CUDA events around

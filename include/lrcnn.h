@@ -297,8 +297,9 @@ LRCNN_API lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan);
  * (op, kind in fwd|dgrad|wgrad|param_grad|pool_fwd|pool_bwd|elt_fwd|elt_bwd): launches, ms, FLOPs. */
 LRCNN_API lrcnn_status lrcnn_profile_dump(lrcnn_plan_t *plan, const char *path, void *stream);
 /* Per-kernel profile of class cls (0 conv FP + dgrad, 1 wgrad, 2 other): one line per tcgen05
- * kernel ("simt" for SIMT launches) "name,launches,ms,flops,bytes\n" written NUL-terminated into buf
- * (bytes = algorithmic HBM bytes of the launches: each operand read once, each result written once)
+ * kernel ("simt" for SIMT launches) "name,launches,ms,flops,bytes,wbytes\n" written NUL-terminated into buf
+ * (bytes = algorithmic HBM bytes of the launches: each operand read once, each result written once;
+ * wbytes = the written part of bytes)
  * (len bytes; LRCNN_E_ARG if too small).  Synchronises `stream` (a cudaStream_t). */
 LRCNN_API lrcnn_status lrcnn_profile_kernels(lrcnn_plan_t *plan, int cls, char *buf, size_t len, void *stream);
 

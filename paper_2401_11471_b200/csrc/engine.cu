@@ -154,9 +154,10 @@ struct ProfScope {
     int cls;
     double flops;
     int tag;
-    double bytes;
+    double bytes, wbytes;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    ProfScope(Run &r, int c, double f, int t = -1, double by = 0) : R(r), cls(c), flops(f), tag(t), bytes(by) {
+    ProfScope(Run &r, int c, double f, int t = -1, double by = 0, double wb = 0)
+        : R(r), cls(c), flops(f), tag(t), bytes(by), wbytes(wb) {
         if (R.P.profiling) {
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
@@ -170,6 +171,7 @@ struct ProfScope {
             R.P.pending_events[cls].push_back({(void *)e0, (void *)e1});
             R.P.pending_flops[cls].push_back(flops);
             R.P.pending_bytes[cls].push_back(bytes);
+            R.P.pending_wbytes[cls].push_back(wbytes);
             R.P.pending_tags[cls].push_back(tag);
             const char *k = tc_last_kernel();
             R.P.pending_names[cls].push_back(k ? k : "");
@@ -185,13 +187,17 @@ static double conv_flops(Plan &P, const OpInfo &o, int rows) {
 // read once, every result written once.  kind 0 FP: input rows [a*s-p, (b-1)*s-p+k) clipped + weights
 // + output (+ residual); kind 1 dgrad: dy + weights + dx and the gating activation (+ dx read when
 // it accumulates); kind 2 wgrad: dy + input rows + the fp32 gradient read-modify-write.
-static double conv_bytes(Plan &P, const OpInfo &o, int a, int b, int kind, int dx_accum = 0, int gate = 0) {
+// write: only the bytes written (the output map, delta_in, the fp32 gradient's write half) --
+// HBM writes alone sustain less than a copy (bench.py's mixed read/write roofline)
+static double conv_bytes(Plan &P, const OpInfo &o, int a, int b, int kind, int dx_accum = 0, int gate = 0,
+                         bool write = false) {
     const TensorInfo &ti = P.t[o.in_t], &to = P.t[o.out_t];
     const double E = P.opts.prec == LRCNN_FP32 ? 4.0 : 2.0, B = P.net.B;
     const int ra = std::max(0, a * o.d.s - o.d.p), rb = std::min(ti.H, (b - 1) * o.d.s - o.d.p + o.d.k);
     const double in = B * (double)(rb - ra) * ti.W * ti.Cp * E;
     const double out = B * (double)(b - a) * to.W * to.Cp * E;
     const double w = (double)o.d.k * o.d.k * ti.Cp * o.d.c_out;
+    if (write) return kind == 0 ? out : kind == 1 ? in : w * 4.0;
     if (kind == 0) return in + out + w * E + (o.d.res >= 0 ? out : 0.0);
     if (kind == 1) return out + w * E + in * (1.0 + gate + dx_accum);
     return out + in + w * 8.0;
@@ -215,7 +221,8 @@ static lrcnn_status op_forward_impl(Run &R, const Segment &S, int r, int i) {
         A.beta = o.beta_cnt ? prm(R, o.beta_off) : nullptr;
         A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.epi = o.d.epi; A.relu = o.d.relu;
         A.a = a; A.b_ = b; A.B = P.net.B;
-        ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 0, conv_bytes(P, o, a, b, 0));
+        ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 0, conv_bytes(P, o, a, b, 0),
+                     conv_bytes(P, o, a, b, 0, 0, 0, true));
         ++P.launches;
         if (P.use_tc) {
             if (tc_conv_fwd(A, R.st)) { ++P.tc_launches; CK(cudaGetLastError()); return LRCNN_OK; }
@@ -566,7 +573,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
             if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
             ++P.launches;
-            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2, conv_bytes(P, o, a, b, 2));
+            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2, conv_bytes(P, o, a, b, 2),
+                         conv_bytes(P, o, a, b, 2, 0, 0, true));
             bool tc = false;
             if (P.use_tc) {
                 tc = tc_conv_wgrad(A, gst);
@@ -607,7 +615,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             }
             {
                 ++P.launches;
-                ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0));
+                ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0),
+                             conv_bytes(P, o, a, b, 1, 0, 0, true));
                 bool tc = false;
                 if (P.use_tc) {
                     tc = tc_conv_dgrad(A, R.st);
@@ -1280,6 +1289,7 @@ lrcnn_status lrcnn_profile_reset(lrcnn_plan_t *plan) {
         plan->P.pending_events[c].clear();
         plan->P.pending_flops[c].clear();
         plan->P.pending_bytes[c].clear();
+        plan->P.pending_wbytes[c].clear();
         plan->P.pending_tags[c].clear();
         plan->P.pending_names[c].clear();
         plan->P.per_kernel[c].clear();
@@ -1310,6 +1320,7 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
                 it->second.ms += t;
                 it->second.flops += P.pending_flops[c][i];
                 it->second.bytes += P.pending_bytes[c][i];
+                it->second.wbytes += P.pending_wbytes[c][i];
                 it->second.launches += 1;
             }
             const int tag = P.pending_tags[c][i];
@@ -1327,6 +1338,7 @@ lrcnn_status lrcnn_profile_read(lrcnn_plan_t *plan, int cls, double *ms, long lo
         P.pending_events[c].clear();
         P.pending_flops[c].clear();
         P.pending_bytes[c].clear();
+        P.pending_wbytes[c].clear();
         P.pending_tags[c].clear();
         P.pending_names[c].clear();
     }
@@ -1343,8 +1355,8 @@ lrcnn_status lrcnn_profile_kernels(lrcnn_plan_t *plan, int cls, char *buf, size_
     std::string out;
     char line[512];
     for (auto &e : plan->P.per_kernel[cls]) {
-        snprintf(line, sizeof line, "%s,%lld,%.6f,%.6e,%.6e\n", e.first.empty() ? "simt" : e.first.c_str(),
-                 e.second.launches, e.second.ms, e.second.flops, e.second.bytes);
+        snprintf(line, sizeof line, "%s,%lld,%.6f,%.6e,%.6e,%.6e\n", e.first.empty() ? "simt" : e.first.c_str(),
+                 e.second.launches, e.second.ms, e.second.flops, e.second.bytes, e.second.wbytes);
         out += line;
     }
     if (out.size() + 1 > len) return fail(LRCNN_E_ARG, "buffer too small");

@@ -83,6 +83,7 @@ struct Segment {
 
 struct ProfileSlot {
     double ms = 0, flops = 0, bytes = 0;   // bytes: algorithmic HBM bytes
+    double wbytes = 0;                     // of which written
     long long launches = 0;
 };
 
@@ -119,6 +120,7 @@ struct Plan {
     std::vector<std::pair<void *, void *>> pending_events[3];   // (start, stop) cudaEvent_t
     std::vector<double> pending_flops[3];
     std::vector<double> pending_bytes[3];
+    std::vector<double> pending_wbytes[3];
     std::vector<int> pending_tags[3];             // op*8 + kind (profile dump)
     std::vector<std::string> pending_names[3];    // tcgen05 kernel launched inside the scope ("" = SIMT)
     std::vector<std::pair<std::string, ProfileSlot>> per_kernel[3];

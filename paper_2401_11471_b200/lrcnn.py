@@ -412,14 +412,15 @@ class Plan:
         return ms.value, n.value, fl.value
 
     def profile_kernels(self, cls, stream=None):
-        """Per-kernel totals of profile class cls: [{name, launches, ms, flops, bytes}] (lrcnn_profile_kernels;
-        bytes = algorithmic HBM bytes of the launches)."""
+        """Per-kernel totals of profile class cls: [{name, launches, ms, flops, bytes, wbytes}]
+        (lrcnn_profile_kernels; bytes = algorithmic HBM bytes of the launches, wbytes = of which written)."""
         buf = ctypes.create_string_buffer(1 << 16)
         _check(lib().lrcnn_profile_kernels(self.h, cls, buf, len(buf), _stream(stream)))
         out = []
         for line in buf.value.decode().splitlines():
-            name, n, ms, fl, by = line.rsplit(",", 4)
-            out.append({"name": name, "launches": int(n), "ms": float(ms), "flops": float(fl), "bytes": float(by)})
+            name, n, ms, fl, by, wb = line.rsplit(",", 5)
+            out.append({"name": name, "launches": int(n), "ms": float(ms), "flops": float(fl), "bytes": float(by),
+                        "wbytes": float(wb)})
         return out
 
     def profile_dump(self, path, stream=None):
