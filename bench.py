@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true", help="skip the layer-wise memory and cpu baselines")
     ap.add_argument("--no-eager", action="store_true", help="skip the PyTorch-eager layer-wise context run")
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
+    ap.add_argument("--allow-overlap", action="store_true",
+                    help="OverL: accept N > H / o^0 at a segment input (LRCNN_FLAG_ALLOW_OVERLAP_EXHAUSTION)")
     ap.add_argument("--no-fp-merge", action="store_true",
                     help="forward pass on the BP bands (default: merged FP bands, LRCNN_FLAG_FP_MERGE)")
     ap.add_argument("--no-balanced", action="store_true",
@@ -337,6 +339,8 @@ def main():
     flags = (LB.FLAG_NO_TCGEN05 if a.simt else LB.FLAG_REQUIRE_TC) | (0 if a.no_balanced else LB.FLAG_BALANCED_BANDS)
     if not a.no_fp_merge:   # decoupled FP bands (N_FP < N_BP, same peak memory)
         flags |= LB.FLAG_FP_MERGE
+    if a.allow_overlap:
+        flags |= LB.FLAG_ALLOW_OVERLAP_EXHAUSTION
     if a.n_bands is None:
         a.n_bands = 8 if a.config in ("c4", "c5") else 4
     kw = {"band_rows": a.band_rows} if a.band_rows else {"n_bands": a.n_bands}

@@ -249,6 +249,22 @@ LRCNN_API lrcnn_status lrcnn_comm_init_nccl(const void *id128, int rank, int wor
 LRCNN_API lrcnn_status lrcnn_comm_loopback_group(int world, void **group);
 LRCNN_API lrcnn_status lrcnn_comm_loopback_group_free(void *group);
 LRCNN_API lrcnn_status lrcnn_comm_init_loopback(void *group, int rank, lrcnn_comm **out);
+/* Host-staged communicator (any process group the caller has, e.g. torch.distributed over gloo;
+ * used where NCCL is unavailable and by the multi-process tests): the library copies the device data
+ * of every halo transfer / all-reduce into pinned HOST staging buffers it owns (cudaMallocHost, grown
+ * on demand; no device memory), synchronises the stream and calls
+ *   exchange(user, n, peer[n], send[n], host_ptr[n], bytes[n]): send[i] = 1: send host_ptr[i][0, bytes[i])
+ *       to rank peer[i]; send[i] = 0: receive bytes[i] from peer[i] into host_ptr[i] (every rank posts
+ *       its sends and receives of one exchange together);
+ *   allreduce(user, host_buf, n): in-place sum of n floats over all ranks;
+ * each returning 0 on success, then copies the results back.  Synchronous on the host and not
+ * graph-capturable (lrcnn_step runs eagerly with it).  Callbacks run on the thread that called
+ * forward / backward / step. */
+typedef int (*lrcnn_host_exchange_fn)(void *user, int n, const int *peer, const int *send, void *const *host_ptr,
+                                      const size_t *bytes);
+typedef int (*lrcnn_host_allreduce_fn)(void *user, float *host_buf, size_t n);
+LRCNN_API lrcnn_status lrcnn_comm_init_host(int rank, int world, lrcnn_host_exchange_fn exchange,
+                                            lrcnn_host_allreduce_fn allreduce, void *user, lrcnn_comm **out);
 LRCNN_API lrcnn_status lrcnn_comm_free(lrcnn_comm *comm);
 LRCNN_API lrcnn_status lrcnn_plan_set_comm(lrcnn_plan_t *plan, lrcnn_comm *comm);
 

@@ -94,15 +94,69 @@ struct LoopGroup {
 };
 
 struct Comm {
-    int kind;       // 0 = NCCL, 1 = loopback
+    int kind;       // 0 = NCCL, 1 = loopback, 2 = host-staged callbacks
     int rank, world;
     ncclComm_t nccl = nullptr;
     LoopGroup *group = nullptr;
+    // host-staged backend: device data are copied to pinned host staging buffers (grown on demand;
+    // host memory, never device memory), the caller's callbacks move them between processes (e.g.
+    // torch.distributed over gloo), and the results are copied back; synchronous on the host
+    lrcnn_host_exchange_fn hx = nullptr;
+    lrcnn_host_allreduce_fn har = nullptr;
+    void *user = nullptr;
+    std::vector<void *> stage;
+    std::vector<size_t> stage_bytes;
+    ~Comm() { for (void *p : stage) cudaFreeHost(p); }
+    void *host_buf(size_t i, size_t bytes) {
+        if (stage.size() <= i) { stage.resize(i + 1, nullptr); stage_bytes.resize(i + 1, 0); }
+        if (stage_bytes[i] < bytes) {
+            if (stage[i]) cudaFreeHost(stage[i]);
+            stage[i] = nullptr;
+            stage_bytes[i] = 0;
+            if (cudaMallocHost(&stage[i], bytes) != cudaSuccess) return nullptr;
+            stage_bytes[i] = bytes;
+        }
+        return stage[i];
+    }
 };
 
 int comm_rank(const Comm *c) { return c->rank; }
 int comm_world(const Comm *c) { return c->world; }
 bool comm_graph_safe(const Comm *c) { return c->kind == 0; }
+
+static int host_exchange(Comm *c, const std::vector<XferBuf> &xs, cudaStream_t st, std::string &e) {
+    const size_t n = xs.size();
+    std::vector<int> peer(n), send(n);
+    std::vector<void *> hp(n);
+    std::vector<size_t> by(n);
+    for (size_t i = 0; i < n; ++i) {
+        peer[i] = xs[i].peer; send[i] = xs[i].send; by[i] = xs[i].bytes;
+        hp[i] = c->host_buf(i, xs[i].bytes);
+        if (!hp[i]) { e = "host staging: cudaMallocHost failed"; return 1; }
+        if (xs[i].send && cudaMemcpyAsync(hp[i], xs[i].ptr, xs[i].bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+            e = "host staging: D2H failed"; return 1;
+        }
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) { e = "host staging: stream sync failed"; return 1; }
+    if (c->hx(c->user, (int)n, peer.data(), send.data(), hp.data(), by.data())) { e = "host exchange callback failed"; return 1; }
+    for (size_t i = 0; i < n; ++i)
+        if (!xs[i].send && cudaMemcpyAsync(xs[i].ptr, hp[i], xs[i].bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            e = "host staging: H2D failed"; return 1;
+        }
+    if (cudaStreamSynchronize(st) != cudaSuccess) { e = "host staging: stream sync failed"; return 1; }
+    return 0;
+}
+
+static int host_allreduce(Comm *c, float *buf, size_t n, cudaStream_t st, std::string &e) {
+    float *h = (float *)c->host_buf(0, n * sizeof(float));
+    if (!h) { e = "host staging: cudaMallocHost failed"; return 1; }
+    if (cudaMemcpyAsync(h, buf, n * sizeof(float), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) { e = "host staging: D2H failed"; return 1; }
+    if (c->har(c->user, h, n)) { e = "host allreduce callback failed"; return 1; }
+    if (cudaMemcpyAsync(buf, h, n * sizeof(float), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) { e = "host staging: H2D failed"; return 1; }
+    return 0;
+}
 
 __global__ void k_add_f32(float *dst, const float *src, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -111,6 +165,11 @@ __global__ void k_add_f32(float *dst, const float *src, size_t n) {
 
 int comm_exchange(Comm *c, const std::vector<XferBuf> &xs, cudaStream_t st, const char **err) {
     static thread_local std::string e;
+    if (c->kind == 2) {
+        const int r = host_exchange(c, xs, st, e);
+        if (r) *err = e.c_str();
+        return r;
+    }
     if (c->kind == 0) {
         NcclApi *api = nccl_api(e);
         if (!api) { *err = e.c_str(); return 1; }
@@ -148,6 +207,11 @@ int comm_exchange(Comm *c, const std::vector<XferBuf> &xs, cudaStream_t st, cons
 int comm_allreduce_f32(Comm *c, float *buf, size_t n, cudaStream_t st, const char **err) {
     static thread_local std::string e;
     if (c->world == 1 || n == 0) return 0;
+    if (c->kind == 2) {
+        const int r = host_allreduce(c, buf, n, st, e);
+        if (r) *err = e.c_str();
+        return r;
+    }
     if (c->kind == 0) {
         NcclApi *api = nccl_api(e);
         if (!api) { *err = e.c_str(); return 1; }
@@ -233,6 +297,19 @@ lrcnn_status lrcnn_comm_init_loopback(void *group, int rank, lrcnn_comm **out) {
     if (!G || !out || rank < 0 || rank >= G->world) { set_last_error("bad args"); return LRCNN_E_ARG; }
     lrcnn_comm *c = new lrcnn_comm();
     c->kind = 1; c->rank = rank; c->world = G->world; c->group = G;
+    *out = c;
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_comm_init_host(int rank, int world, lrcnn_host_exchange_fn exchange, lrcnn_host_allreduce_fn allreduce,
+                                  void *user, lrcnn_comm **out) {
+    if (!out || !exchange || !allreduce || world < 1 || rank < 0 || rank >= world) {
+        set_last_error("bad args");
+        return LRCNN_E_ARG;
+    }
+    lrcnn_comm *c = new lrcnn_comm();
+    c->kind = 2; c->rank = rank; c->world = world;
+    c->hx = exchange; c->har = allreduce; c->user = user;
     *out = c;
     return LRCNN_OK;
 }

@@ -2787,9 +2787,15 @@ static void note_kernel(const void *fn) {
 }
 const char *tc_last_kernel() { return g_last_kernel; }
 void tc_clear_last_kernel() { g_last_kernel = nullptr; }
+// Per-launch profiling (lrcnn_profile_enable) turns PDL off: with programmatic launches a CUDA event
+// recorded between two kernels may complete when the first kernel TRIGGERS its dependents (right
+// after its setup) instead of when it finishes, which moves time from one kernel to the next.
+static thread_local bool g_pdl_off = false;
+void tc_set_pdl(bool on) { g_pdl_off = !on; }
 template <typename... KArgs, typename... Args>
 static bool launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args &&...args) {
-    static const int pdl = env_int("LRCNN_PDL", 1);
+    static const int pdl_env = env_int("LRCNN_PDL", 1);
+    const int pdl = pdl_env && !g_pdl_off;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);

@@ -706,10 +706,13 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
 // communication stream once everything enqueued so far on the main stream (the range's last
 // writers) is done; the backward goes on meanwhile.  dp_join makes the main stream wait for the
 // reductions (before the SGD / the caller reads the gradient).
+// Row sharding (opts.world > 1) uses the same per-segment buckets: a segment's weight gradient on
+// this rank is final once its band sweep is done, so it is summed over the ranks while the earlier
+// segments' backward runs.
 static lrcnn_status dp_reduce(Run &R, size_t lo, size_t hi) {
     Plan &P = R.P;
-    if (P.dp_world <= 1 || hi <= lo) return LRCNN_OK;
-    if (!P.comm) return fail(LRCNN_E_STATE, "LRCNN_FLAG_DP with world > 1 needs lrcnn_plan_set_comm");
+    if ((P.dp_world <= 1 && P.opts.world <= 1) || hi <= lo) return LRCNN_OK;
+    if (!P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     if (!P.comm_stream) {   // created on the first (eager) call, before any graph capture
         cudaStream_t cs;
         cudaEvent_t e0, e1;
@@ -1145,6 +1148,8 @@ lrcnn_status lrcnn_forward_rows(lrcnn_plan_t *plan, const void *params, const vo
     if (st != LRCNN_OK) return st;
     P.launches = 0; P.tc_launches = 0; P.simt_fallbacks = 0;
     Run R{P, (char *)ws, (const char *)params, x, zl, nullptr, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    tc_set_pdl(!P.profiling);
+    simt_set_pdl(!P.profiling);
     P.fwd_done = false;
     if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     st = run_forward(R);
@@ -1163,6 +1168,8 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
         return fail(LRCNN_E_STATE, "backward_rows needs a matching forward_rows (same params, x, ws)");
     P.launches = 0; P.tc_launches = 0; P.simt_fallbacks = 0;
     Run R{P, (char *)ws, (const char *)params, x, (void *)zl, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    tc_set_pdl(!P.profiling);
+    simt_set_pdl(!P.profiling);
     const int L = P.net.n_ops;
     const TensorInfo &z = P.t[L];
     // delta^L, gated by the last op's ReLU (gate on write), into the last segment's delta buffer
@@ -1171,13 +1178,8 @@ lrcnn_status lrcnn_backward_rows(lrcnn_plan_t *plan, const void *params, const v
                  z.relu, R.st));
     ++P.launches;
     if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
-    st = run_backward(R);
+    st = run_backward(R);   // (sharded: the per-segment wgrad buckets are summed over the ranks inside)
     if (st == LRCNN_OK) st = dp_join(R);
-    if (st == LRCNN_OK && P.opts.world > 1) {
-        const char *err = nullptr;
-        if (comm_allreduce_f32((Comm *)P.comm, grads, P.head_w_off, R.st, &err))
-            return fail(LRCNN_E_NCCL, err ? err : "allreduce failed");
-    }
     P.fwd_done = false;
     return st;
 }
@@ -1190,6 +1192,8 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
     P.launches = 0; P.tc_launches = 0; P.simt_fallbacks = 0;
     char *w = (char *)ws;
     Run R{P, w, (const char *)params, x, w + P.zl_off, grads, (cudaStream_t)stream, P.opts.prec, (size_t)P.elem};
+    tc_set_pdl(!P.profiling);
+    simt_set_pdl(!P.profiling);
     if (P.opts.world > 1 && !P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
     if ((st = run_forward(R)) != LRCNN_OK) return st;
     const int L = P.net.n_ops;
@@ -1208,14 +1212,9 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
                  R.params + P.head_w_off * R.E, R.params + P.head_b_off * R.E, labels, scratch, loss_dev,
                  grads + P.head_w_off, grads + P.head_b_off, w + P.dfull_off[slast & 1], z.relu, hw, R.st));
     P.launches += 4;   // gap, logits, FC grad, delta^L
-    if ((st = dp_reduce(R, P.head_w_off, P.head_b_off + P.head_b_cnt)) != LRCNN_OK) return st;
-    st = run_backward(R);
+    if (P.dp_world > 1 && (st = dp_reduce(R, P.head_w_off, P.head_b_off + P.head_b_cnt)) != LRCNN_OK) return st;
+    st = run_backward(R);   // (sharded: the per-segment wgrad buckets are summed over the ranks inside)
     if (st == LRCNN_OK) st = dp_join(R);
-    if (st == LRCNN_OK && P.opts.world > 1) {   // wgrad all-reduce (the conv parameters precede the head)
-        const char *err = nullptr;
-        if (comm_allreduce_f32((Comm *)P.comm, grads, P.head_w_off, R.st, &err))
-            return fail(LRCNN_E_NCCL, err ? err : "allreduce failed");
-    }
     P.fwd_done = false;
     return st;
 }

@@ -92,6 +92,8 @@ bool pool_tiled_shape(int k, int s, int Cp);      // overlapping max-pool backwa
 cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st);
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st);
 
+void simt_set_pdl(bool on);   // programmatic dependent launch on / off for this host thread (profiling)
+
 // head (Alg. 1 l.12-14) and update (l.24)
 cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int Cp, int C, int classes,
                                   const void *fc_w, const void *fc_b, const int32_t *labels, float *scratch,

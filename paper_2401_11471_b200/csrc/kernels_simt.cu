@@ -20,10 +20,12 @@ namespace lrcnn {
 // the preceding grid at its first statement, so it may be launched while that grid drains.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+static thread_local bool g_simt_pdl_off = false;   // per-launch profiling (see tc_set_pdl)
+void simt_set_pdl(bool on) { g_simt_pdl_off = !on; }
 static int simt_pdl() {
     static int v = -1;
     if (v < 0) { const char *e = getenv("LRCNN_PDL"); v = e && *e ? atoi(e) : 1; }
-    return v;
+    return v && !g_simt_pdl_off;
 }
 template <typename... KArgs, typename... Args>
 static void launch_simt(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {

@@ -16,4 +16,6 @@ void tc_clear_last_kernel();
 // true (and cleared) if a launcher failed for a reason other than declining the shape: the
 // engine reports LRCNN_E_CUDA instead of falling back to SIMT
 bool tc_take_error();
+// programmatic dependent launch on (default) / off (per-launch event profiling) for this host thread
+void tc_set_pdl(bool on);
 }  // namespace lrcnn

@@ -63,12 +63,18 @@ class MemoryReport(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+# host-staged communicator callbacks (lrcnn_comm_init_host)
+HOST_EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.POINTER(ctypes.c_size_t))
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float), ctypes.c_size_t)
+
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_greedy", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
            "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_fp_bands", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
            "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_profile_kernels", "lrcnn_plan_shard", "lrcnn_plan_xfers",
            "lrcnn_comm_nccl_unique_id", "lrcnn_comm_init_nccl", "lrcnn_comm_loopback_group",
-           "lrcnn_comm_loopback_group_free", "lrcnn_comm_init_loopback", "lrcnn_comm_free", "lrcnn_plan_set_comm",
+           "lrcnn_comm_loopback_group_free", "lrcnn_comm_init_loopback", "lrcnn_comm_init_host", "lrcnn_comm_free", "lrcnn_plan_set_comm",
            "lrcnn_last_launch_count", "lrcnn_last_tc_launch_count", "lrcnn_last_simt_fallbacks", "lrcnn_debug_capture",
            "lrcnn_last_error", "lrcnn_version"]
 
@@ -118,6 +124,7 @@ def lib():
     L.lrcnn_comm_loopback_group.argtypes = [i, ctypes.POINTER(vp)]
     L.lrcnn_comm_loopback_group_free.argtypes = [vp]
     L.lrcnn_comm_init_loopback.argtypes = [vp, i, ctypes.POINTER(vp)]
+    L.lrcnn_comm_init_host.argtypes = [i, i, HOST_EXCHANGE_FN, HOST_ALLREDUCE_FN, vp, ctypes.POINTER(vp)]
     L.lrcnn_comm_free.argtypes = [vp]
     L.lrcnn_plan_set_comm.argtypes = [vp, vp]
     L.lrcnn_last_tc_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
@@ -478,6 +485,46 @@ class Comm:
             _check(lib().lrcnn_comm_init_loopback(g, r, ctypes.byref(h)))
             out.append(Comm(h, g))
         return out
+
+    @staticmethod
+    def host(group=None):
+        """Host-staged communicator over a torch.distributed process group (e.g. gloo): the library
+        stages halo rows / gradients through pinned host buffers and these callbacks move them with
+        the group's send / recv / all_reduce (marshalling only; the library does every computation)."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def _arr(ptr, nbytes):
+            return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), shape=(nbytes,))
+
+        def exchange(_user, n, peer, send, host_ptr, nbytes):
+            try:
+                reqs = []
+                for i in range(n):
+                    t = torch.from_numpy(_arr(host_ptr[i], nbytes[i]))
+                    p = dist.get_global_rank(group, peer[i]) if group is not None else peer[i]
+                    reqs.append(dist.isend(t, p, group=group) if send[i] else dist.irecv(t, p, group=group))
+                for r in reqs:
+                    r.wait()
+                return 0
+            except Exception:   # reported by the library as LRCNN_E_NCCL
+                return 1
+
+        def allreduce(_user, buf, n):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(n,))
+                dist.all_reduce(torch.from_numpy(arr), group=group)
+                return 0
+            except Exception:
+                return 1
+
+        cb = (HOST_EXCHANGE_FN(exchange), HOST_ALLREDUCE_FN(allreduce))
+        h = ctypes.c_void_p()
+        _check(lib().lrcnn_comm_init_host(rank, world, cb[0], cb[1], None, ctypes.byref(h)))
+        c = Comm(h)
+        c._callbacks = cb   # keep the ctypes thunks alive as long as the communicator
+        return c
 
     def free(self):
         if self.h:

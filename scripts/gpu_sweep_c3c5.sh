@@ -5,7 +5,7 @@ TAG=${1:-sweep}
 mkdir -p gpurun_out
 for mode in 2ps overl; do
   for n in 2 4 7; do
-    timeout 600 python bench.py --config c3 --mode $mode --n-bands $n --no-balanced --no-baselines --steps 5 \
+    timeout 600 python bench.py --config c3 --mode $mode --n-bands $n --no-balanced --no-baselines --allow-overlap --steps 5 \
       > gpurun_out/${TAG}_c3_${mode}_${n}.json 2> gpurun_out/${TAG}_c3_${mode}_${n}.err
   done
 done
