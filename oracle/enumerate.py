@@ -236,3 +236,68 @@ def forward_split(chain, h0, in_ends):
         ends, h = new, h_out
         sizes.append([ends[0]] + [ends[i] - ends[i - 1] for i in range(1, len(ends))])
     return sizes
+
+
+def enumerate_rank_zr(net, seg, world, g, band_rows=None, n_bands=None, shp=None):
+    """Zero-redundancy row sharding, enumerated with explicit row sets.
+
+    The segment output is split into contiguous rank ranges [C_g, C_{g+1}) (rank_rows).  Every row of
+    every tensor t is computed by exactly ONE rank: the rank boundary of t at cut C is F_C(t) = the
+    lowest row of t needed by the output rows [C, H_out) (so a rank's rows depend only on its own rows
+    and on rows BELOW its range -- the weak dependency across the cut runs upward only); rank g owns
+    [F_{C_g}(t), F_{C_{g+1}}(t)) (rank 0 from row 0, the last rank to H_t).  Inside the rank, 2PS bands
+    over its owned output rows: band r computes [e_{r-1}(t), e_r(t)) with e_r(t) = max(F_{C_g}(t),
+    1 + max row of t needed by the outputs [C_g, E_r)) for r < N-1, the last band up to the rank's
+    end.  Buffers hold [lo, hi): lo = the first row the band's consumers read (2PS cache rows from the
+    band above inside the rank), hi = one past the last row they read; in the last band of a rank
+    rows [F_{C_{g+1}}(t), hi) belong to rank g+1 and arrive as the halo from below.
+
+    Returns (own, bands, (ol, oh)): own = {t: (F_g, F_{g+1})} for the segment input and every tensor,
+    bands = [{t: (lo, a, b, hi)} per band]."""
+    shp = shp or out_hw(net)
+    seg_in, ids, out = seg
+    h_out = shp[out][1]
+    tensors = [seg_in] + [i + 1 for i in ids]
+
+    def cut(C):
+        if C <= 0:
+            return {t: 0 for t in tensors}
+        if C >= h_out:
+            return {t: shp[t][1] for t in tensors}
+        need = need_sets(net, shp, seg, range(C, h_out))
+        return {t: (min(need[t]) if need.get(t) else shp[t][1]) for t in tensors}
+    ol, oh = rank_rows(h_out, world, g)
+    top, bot = cut(ol), cut(oh)
+    if g == world - 1:
+        bot = {t: shp[t][1] for t in tensors}
+    own = {t: (top[t], bot[t]) for t in tensors}
+    E = [ol + e for e in band_ends(oh - ol, band_rows=band_rows, n_bands=n_bands if band_rows is None else None)]
+    N = len(E)
+    ends = []
+    for r in range(N):
+        e = {}
+        if r == N - 1:
+            e = {t: own[t][1] for t in tensors}
+        else:
+            nd = need_sets(net, shp, seg, range(ol, E[r]))
+            for t in tensors:
+                nt = nd.get(t, set())
+                e[t] = max(own[t][0], (max(nt) + 1) if nt else own[t][0])
+        ends.append(e)
+    bands = []
+    for r in range(N):
+        band = {}
+        for t in tensors:
+            a = ends[r - 1][t] if r > 0 else own[t][0]
+            band[t] = [a, a, ends[r][t], ends[r][t]]
+        band[out] = [E[r - 1] if r else ol] * 2 + [E[r]] * 2
+        for i in reversed(ids):
+            op = net["ops"][i]
+            _, a, b, _ = band[i + 1]
+            for tin in set(_inputs(op)):
+                got = rf_of(op, tin, range(a, b), shp[tin][1])
+                if got:
+                    band[tin][0] = min(band[tin][0], min(got))
+                    band[tin][3] = max(band[tin][3], max(got) + 1)
+        bands.append({t: tuple(v) for t, v in band.items()})
+    return own, bands, (ol, oh)

@@ -16,6 +16,8 @@ if cfg == "c2":
     net, B = WL.vgg16(H=224, W=224, segments="pool"), 32
 elif cfg == "c3":
     net, B = WL.resnet50(H=224, W=224), 256
+elif cfg == "c5":
+    net, B = WL.vgg16(H=2048, W=2048, segments="pool"), 16
 else:
     net, B = WL.resnet50(H=3600, W=2400), 8
 plan = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=nb, flags=LB.FLAG_BALANCED_BANDS | LB.FLAG_FP_MERGE | LB.FLAG_REQUIRE_TC)   # = bench.py defaults
