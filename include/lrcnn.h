@@ -147,6 +147,15 @@ typedef struct {
  * replaced by ceil(sqrt(n_ops)) - 1 checkpoints, each at the valid cut (an op output that no other
  * tensor is read past) nearest to an even spacing of the ops.  lrcnn_plan_seg reports them. */
 #define LRCNN_FLAG_AUTO_SEGMENTS 128
+/* Zero-redundancy row sharding (world > 1, 2PS; the weak dependency across a rank
+ * cut, resolved by two-phase sharing instead of overlap): every row of every tensor is
+ * computed by exactly one rank -- rank g owns [F_{C_g}(t), F_{C_{g+1}}(t)), F_C(t) = the lowest row of
+ * t the outputs below the cut C need -- so a rank depends only on the FIRST rows of rank g+1: after
+ * every rank's first band the ranks exchange those rows of every band tensor (one grouped send/recv
+ * per segment), the last band of rank g reads them, and in the backward its delta for those rows
+ * goes back the same way and is added into rank g+1's first band.  No recomputation at the cuts.
+ * Needs >= 2 bands per rank (but the last); ignores BALANCED_BANDS / FP_MERGE. */
+#define LRCNN_FLAG_ZERO_REDUNDANCY 256
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 
@@ -220,6 +229,14 @@ LRCNN_API lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int ba
 
 LRCNN_API lrcnn_status lrcnn_plan_memory(const lrcnn_plan_t *plan, lrcnn_memory_report *rep);
 
+/* One past the last row of tensor `tid` that band `band`'s consumers read (== b of lrcnn_plan_rows,
+ * except in the last band of a zero-redundancy rank, which also reads rows of rank+1). */
+LRCNN_API lrcnn_status lrcnn_plan_read_end(const lrcnn_plan_t *plan, int seg, int band, int tid, int *hb);
+/* Zero-redundancy halo schedule of segment `seg` (LRCNN_FLAG_ZERO_REDUNDANCY): up to max entries
+ * (tensor, dir, rows [r0, r1)); dir 0 = rows of rank+1 my last band reads (received after the first
+ * band; their delta goes back in the BP), dir 1 = my rows rank-1's last band reads; *n the count. */
+LRCNN_API lrcnn_status lrcnn_plan_zr_halo(const lrcnn_plan_t *plan, int seg, int max, int *n, int *tid, int *dir,
+                                          int *r0, int *r1);
 /* Forward / backward band counts of segment `seg`: *n_bp = its bands; *n_fp = the bands the
  * forward pass runs (< *n_bp with LRCNN_FLAG_FP_MERGE when merged bands fit, else == *n_bp). */
 LRCNN_API lrcnn_status lrcnn_plan_fp_bands(const lrcnn_plan_t *plan, int seg, int *n_fp, int *n_bp);

@@ -267,6 +267,8 @@ def enumerate_rank_zr(net, seg, world, g, band_rows=None, n_bands=None, shp=None
         need = need_sets(net, shp, seg, range(C, h_out))
         return {t: (min(need[t]) if need.get(t) else shp[t][1]) for t in tensors}
     ol, oh = rank_rows(h_out, world, g)
+    if oh <= ol:
+        raise ValueError("infeasible: fewer segment-output rows than ranks")
     top, bot = cut(ol), cut(oh)
     if g == world - 1:
         bot = {t: shp[t][1] for t in tensors}
@@ -283,6 +285,8 @@ def enumerate_rank_zr(net, seg, world, g, band_rows=None, n_bands=None, shp=None
             for t in tensors:
                 nt = nd.get(t, set())
                 e[t] = max(own[t][0], (max(nt) + 1) if nt else own[t][0])
+                if e[t] > own[t][1] and t != seg_in:
+                    raise ValueError("infeasible: band %d of rank %d needs rows of tensor %d below its rank" % (r, g, t))
         ends.append(e)
     bands = []
     for r in range(N):

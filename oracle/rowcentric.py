@@ -419,3 +419,160 @@ def step_ranks(net, params, x, labels, lr, world, band_rows=None, n_bands=None):
     per_rank, blog = backward_ranks(plans, params, state, dzl)
     grads = _sum_grads(per_rank)
     return C.sgd(params, grads, hg, lr), loss, grads, hg, zl, flog + blog
+
+
+# ---------------------------------------------------------------- zero-redundancy G-rank simulation (f1)
+def _zr_band_fwd(net, shp, seg, band, held_in, cache, halo, params):
+    """One band of a zero-redundancy rank: band[t] = (lo, a, b, hi); rows [lo, a) come from the band
+    above (cache), [a, b) are computed, [b, hi) are the halo from rank g+1 (halo)."""
+    seg_in, ids, out = seg
+    held = dict(held_in)
+    B = held_in[seg_in][1].shape[0]
+    for i in ids:
+        t = i + 1
+        lo, a, b, hi = band[t]
+        new = _op_rows_fwd(net, i, held, params, a, b, shp)[0] if b > a else \
+            np.zeros((B, shp[t][0], 0, shp[t][2]))
+        parts = []
+        if lo < a:
+            clo, carr = cache[t]
+            parts.append(carr[:, :, lo - clo:a - clo])
+        parts.append(new)
+        if hi > b:
+            parts.append(halo[t])
+        held[t] = (lo, np.concatenate(parts, axis=2))
+    return held
+
+
+def step_ranks_zr(net, params, x, labels, lr, world, band_rows=None, n_bands=None):
+    """One Alg. 1 iteration with zero-redundancy row sharding over `world` simulated ranks (SURVEY
+    8(f) f1; oracle.enumerate.enumerate_rank_zr): every row of every tensor is computed by one rank;
+    rank g's last band reads the first rows of rank g+1 (a message after every rank's first band) and
+    sends their delta back (a message after its first BP band, added into rank g+1's first band).
+    Returns (new_params, loss, grads, head_grads, z^L, message log)."""
+    from oracle.enumerate import enumerate_rank_zr
+    shp = C.out_hw(net)
+    segs = segments(net)
+    x = np.asarray(x, dtype=np.float64)
+    B = x.shape[0]
+    log = []
+    plans = [[enumerate_rank_zr(net, seg, world, g, band_rows, (n_bands or 1) if band_rows is None else None, shp)
+              for g in range(world)] for seg in segs]
+    full_in = x                      # the segment input, assembled from the owners' rows (all ranks)
+    saved = []                       # per segment: per rank (input slab lo, slab, [held per band])
+    for s, seg in enumerate(segs):
+        seg_in, ids, out = seg
+        per = []
+        for g in range(world):
+            own, bands, _ = plans[s][g]
+            r0 = min(b[seg_in][0] for b in bands)
+            r1 = max(b[seg_in][3] for b in bands)
+            per.append((r0, full_in[:, :, r0:r1].copy()))
+        helds = [[None] * len(plans[s][g][1]) for g in range(world)]
+        # band 0 of every rank (bottom rank first: with one band a rank's only band is its last)
+        msgs = {}
+        order = list(range(world - 1, -1, -1))
+        for g in order:
+            own, bands, _ = plans[s][g]
+            N = len(bands)
+            halo = {}
+            if N == 1 and g + 1 < world:
+                halo = msgs[g + 1]
+            helds[g][0] = _zr_band_fwd(net, shp, seg, bands[0], {seg_in: per[g]}, {}, halo, params)
+            if g > 0:   # my first rows the rank above reads
+                own_up, bands_up, _ = plans[s][g - 1]
+                m = {}
+                for i in ids:
+                    t = i + 1
+                    if t == out:
+                        continue
+                    a0, a1 = own_up[t][1], bands_up[-1][t][3]
+                    if a1 > a0:
+                        lo, arr = helds[g][0][t]
+                        m[t] = arr[:, :, a0 - lo:a1 - lo].copy()
+                msgs[g] = m
+                log.append(("fp", s, g, g - 1, sorted((t, v.shape[2]) for t, v in m.items())))
+        for g in range(world):
+            own, bands, _ = plans[s][g]
+            for r in range(1, len(bands)):
+                halo = msgs.get(g + 1, {}) if r == len(bands) - 1 else {}
+                helds[g][r] = _zr_band_fwd(net, shp, seg, bands[r], {seg_in: per[g]}, helds[g][r - 1], halo, params)
+        c, h, w = shp[out]
+        y = np.zeros((B, c, h, w))
+        for g in range(world):
+            own, bands, (ol, oh) = plans[s][g]
+            for r, band in enumerate(bands):
+                lo, a, b, hi = band[out]
+                blo, arr = helds[g][r][out]
+                y[:, :, a:b] = arr[:, :, a - blo:b - blo]
+        saved.append((per, helds, msgs))
+        full_in = y
+    zl = full_in
+    loss, dzl, hg, _ = C.head_forward_backward(zl, params["head"], labels)
+    grads = [None] * len(net["ops"])
+    dout_full = np.asarray(dzl, dtype=np.float64)
+    for s in range(len(segs) - 1, -1, -1):
+        seg = segs[s]
+        seg_in, ids, out = seg
+        per, helds, fmsgs = saved[s]
+        d_ins = [np.zeros_like(per[g][1]) for g in range(world)]
+        seg_grads = [{i: {} for i in ids if net["ops"][i]["kind"] == "conv"} for _ in range(world)]
+        carry = [dict() for _ in range(world)]
+        dmsgs = {}
+
+        def bp_band(g, r):
+            own, bands, _ = plans[s][g]
+            band = bands[r]
+            held = helds[g][r]
+            d = {seg_in: (per[g][0], d_ins[g])}
+            for i in ids:
+                t = i + 1
+                lo, a, b, hi = band[t]
+                if t == out:
+                    d[t] = (a, dout_full[:, :, a:b].copy())
+                    continue
+                d[t] = (lo, np.zeros((B, shp[t][0], hi - lo, shp[t][2])))
+                if t in carry[g]:
+                    clo, carr = carry[g][t]
+                    _add_rows(d, t, clo, carr)
+                if r == 0 and g > 0 and t in dmsgs.get(g - 1, {}):
+                    _add_rows(d, t, own[t][0], dmsgs[g - 1][t])
+            for i in reversed(ids):
+                t = i + 1
+                lo, a, b, hi = band[t]
+                if b <= a:
+                    continue
+                _op_rows_bwd(net, i, held, params, a, b, shp, _rows(d, t, a, b), d, seg_grads[g])
+            carry[g] = {}
+            for i in ids:
+                t = i + 1
+                lo, a, b, hi = band[t]
+                if t != out and lo < a:
+                    carry[g][t] = (lo, _rows(d, t, lo, a).copy())
+            if r == len(bands) - 1 and g + 1 < world:   # the delta of rank g+1's rows goes back down
+                m = {}
+                for i in ids:
+                    t = i + 1
+                    lo, a, b, hi = band[t]
+                    if t != out and hi > b:
+                        m[t] = _rows(d, t, b, hi).copy()
+                dmsgs[g] = m
+                log.append(("bp", s, g, g + 1, sorted((t, v.shape[2]) for t, v in m.items())))
+        for g in range(world):                       # every rank's last band first (BP order)
+            N = len(plans[s][g][1])
+            for r in range(N - 1, 0, -1):
+                bp_band(g, r)
+        for g in range(world):                       # then every rank's first band (top rank first)
+            bp_band(g, 0)
+        for g in range(world):
+            for i, v in seg_grads[g].items():
+                if not v:
+                    continue
+                grads[i] = v if grads[i] is None else {k: grads[i][k] + v[k] for k in v}
+        c, h, w = shp[seg_in]
+        d_full = np.zeros((B, c, h, w))
+        for g in range(world):                       # the input delta back to its owners (added)
+            r0 = per[g][0]
+            d_full[:, :, r0:r0 + d_ins[g].shape[2]] += d_ins[g]
+        dout_full = d_full
+    return C.sgd(params, grads, hg, lr), loss, grads, hg, zl, log

@@ -12,6 +12,7 @@
 // allocated on the device.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -117,7 +118,7 @@ static View act_view(Run &R, const Segment &S, int r, int t) {
         v.bs = (long long)ti.cap_fp * ti.W * ti.Cp;
         return v;
     }
-    return band_view(R.ws + ti.act_off, ti, S.lo[r][t], S.b[r][t]);
+    return band_view(R.ws + ti.act_off, ti, S.lo[r][t], S.hb[r][t]);
 }
 
 static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
@@ -130,8 +131,10 @@ static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
     if (t == S.out_t) return dfull_view(R.ws + R.P.dfull_off[s & 1], ti);
     if (t == S.in_t) return dfull_view(t == 0 ? nullptr : R.ws + R.P.dfull_off[(s + 1) & 1], ti);
     (void)nseg;
-    return band_view(R.ws + ti.dlt_off, ti, S.lo[r][t], S.b[r][t]);
+    return band_view(R.ws + ti.dlt_off, ti, S.lo[r][t], S.hb[r][t]);
 }
+
+static bool zr_plan(const Plan &P) { return P.opts.world > 1 && (P.opts.flags & LRCNN_FLAG_ZERO_REDUNDANCY); }
 
 static const void *prm(Run &R, size_t off) { return off == (size_t)-1 ? nullptr : R.params + off * R.E; }
 
@@ -330,6 +333,15 @@ static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cach
                                 rows)) != LRCNN_OK) return st;
         }
     }
+    // zero-redundancy: the last band reads rows [HI, hb) of every band tensor that rank+1 computed in
+    // its first band (received after the first band, kept for the BP recompute)
+    if (r == (int)S.E.size() - 1)
+        for (const Segment::ZrRows &z : S.zr_from_below) {
+            const TensorInfo &ti = P.t[z.t];
+            const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+            if ((st = copy_rows(R, ti, R.ws + ti.act_off + (size_t)(z.r0 - S.lo[r][z.t]) * rb, ti.cap,
+                                R.ws + ti.zr_in_off, z.r1 - z.r0, z.r1 - z.r0)) != LRCNN_OK) return st;
+        }
     for (int i : S.ops) {
         if (skip_out && i + 1 == S.out_t) continue;
         if ((st = op_forward(R, S, r, i)) != LRCNN_OK) return st;
@@ -395,6 +407,30 @@ static lrcnn_status exchange(Run &R, const Segment &S, const View &v, bool bp) {
     return LRCNN_OK;
 }
 
+// Zero-redundancy halo exchange of one segment (one grouped send/recv, main stream, every rank at the
+// same point).  FP (after the first band): my first rows go up to rank-1 (zr_out), rank+1's first rows
+// come in (zr_in).  BP (after the last band's backward): the delta of rank+1's rows goes down
+// (zr_dout), the delta rank-1 computed for my first rows comes in (zr_din).
+static lrcnn_status zr_exchange(Run &R, const Segment &S, bool bp) {
+    Plan &P = R.P;
+    if (S.zr_from_below.empty() && S.zr_to_above.empty()) return LRCNN_OK;
+    const int rank = P.opts.rank;
+    std::vector<XferBuf> xs;
+    for (const Segment::ZrRows &z : S.zr_to_above) {
+        const TensorInfo &ti = P.t[z.t];
+        const size_t by = (size_t)P.net.B * (z.r1 - z.r0) * ti.W * ti.Cp * R.E;
+        xs.push_back({rank - 1, bp ? 0 : 1, R.ws + (bp ? ti.zr_din_off : ti.zr_out_off), by});
+    }
+    for (const Segment::ZrRows &z : S.zr_from_below) {
+        const TensorInfo &ti = P.t[z.t];
+        const size_t by = (size_t)P.net.B * (z.r1 - z.r0) * ti.W * ti.Cp * R.E;
+        xs.push_back({rank + 1, bp ? 1 : 0, R.ws + (bp ? ti.zr_dout_off : ti.zr_in_off), by});
+    }
+    const char *err = nullptr;
+    if (comm_exchange((Comm *)P.comm, xs, R.st, &err)) return fail(LRCNN_E_NCCL, err ? err : "zr exchange failed");
+    return LRCNN_OK;
+}
+
 // transposed weights for the tensor-core dgrad (gamma folded in), on stream st
 static lrcnn_status launch_transposes(Run &R, cudaStream_t st) {
     Plan &P = R.P;
@@ -435,8 +471,19 @@ static lrcnn_status run_forward(Run &R) {
                 if ((st = band_forward_merged(R, S, F, k)) != LRCNN_OK) return st;
             continue;
         }
-        for (int r = 0; r < (int)S.E.size(); ++r)
+        for (int r = 0; r < (int)S.E.size(); ++r) {
             if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) return st;
+            if (r == 0 && zr_plan(R.P)) {   // my first rows the rank above reads, then the exchange
+                for (const Segment::ZrRows &z : S.zr_to_above) {
+                    const TensorInfo &ti = R.P.t[z.t];
+                    const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+                    if ((st = copy_rows(R, ti, R.ws + ti.zr_out_off, z.r1 - z.r0,
+                                        R.ws + ti.act_off + (size_t)(z.r0 - S.lo[0][z.t]) * rb, ti.cap,
+                                        z.r1 - z.r0)) != LRCNN_OK) return st;
+                }
+                if ((st = zr_exchange(R, S, false)) != LRCNN_OK) return st;
+            }
+        }
     }
     return LRCNN_OK;
 }
@@ -456,6 +503,7 @@ static lrcnn_status run_forward(Run &R) {
 // row kernel.  Every band row of t must be covered by one of the two row ranges.  Returns u, or -1.
 static int fused_res(const Plan &P, const Segment &S, int t) {
     if (!P.use_tc || P.opts.mode == LRCNN_OVERL || t == 0 || t == S.in_t || t == S.out_t) return -1;
+    if (zr_plan(P)) return -1;   // (delta rows beyond the rank's own rows accumulate from several writers)
     if (P.opts.flags & LRCNN_FLAG_NO_FUSE_RES) return -1;
     const TensorInfo &ti = P.t[t];
     if (ti.cons.size() != 2) return -1;
@@ -484,7 +532,7 @@ static int fused_res(const Plan &P, const Segment &S, int t) {
 }
 
 static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
-    if (t == 0 || t == S.in_t || t == S.out_t) return false;
+    if (t == 0 || t == S.in_t || t == S.out_t || zr_plan(P)) return false;
     if (fused_res(P, S, t) >= 0) return true;
     const TensorInfo &ti = P.t[t];
     if (ti.cons.size() != 1 || ti.cons[0].role != 0) return false;
@@ -789,7 +837,7 @@ static lrcnn_status run_backward(Run &R) {
                     const TensorInfo &ti = P.t[t];
                     if (t == S.out_t || ti.dfw != i || delta_overwrite(P, S, t)) continue;
                     size_t rb = (size_t)ti.W * ti.Cp * R.E;
-                    int rows = S.b[r][t] - S.lo[r][t];
+                    int rows = S.hb[r][t] - S.lo[r][t];
                     if (rows > 0)
                         CK(cudaMemset2DAsync(R.ws + ti.dlt_off, ti.cap * rb, 0, rows * rb, P.net.B, R.st));
                     if (P.opts.mode == LRCNN_2PS && r + 1 < N) {
@@ -799,10 +847,21 @@ static lrcnn_status run_backward(Run &R) {
                                                 R.ws + ti.carry_off, ti.carry_cap, chi - clo)) != LRCNN_OK) return st;
                         }
                     }
+                    if (r == 0 && ti.zr_out_r1 > ti.zr_out_r0)   // + the delta rank-1 computed for my first rows
+                        CK(add_rows(R.prec, dlt_view(R, S, s, r, t), ti.zr_out_r0, ti.zr_out_r1, R.ws + ti.zr_din_off,
+                                    P.net.B, R.st));
+                }
+                const int to = P.op[i].out_t;
+                // zero-redundancy: the delta of rank+1's rows [HI, hb) of op i's output is complete too
+                if (r == N - 1 && to != S.out_t && P.t[to].zr_in_r1 > P.t[to].zr_in_r0) {
+                    const TensorInfo &ti = P.t[to];
+                    const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+                    if ((st = copy_rows(R, ti, R.ws + ti.zr_dout_off, ti.zr_in_r1 - ti.zr_in_r0,
+                                        R.ws + ti.dlt_off + (size_t)(ti.zr_in_r0 - S.lo[r][to]) * rb, ti.cap,
+                                        ti.zr_in_r1 - ti.zr_in_r0)) != LRCNN_OK) return st;
                 }
                 // the 2PS carry out of op i's output: its cached rows [lo_r, a_r) are complete once
                 // every consumer has run (all later in op order); copy them before the slot is reused
-                const int to = P.op[i].out_t;
                 if (P.opts.mode == LRCNN_2PS && r > 0 && to != S.out_t && P.t[to].dfw >= 0) {
                     const TensorInfo &ti = P.t[to];
                     int rows = S.a[r][to] - S.lo[r][to];
@@ -812,6 +871,7 @@ static lrcnn_status run_backward(Run &R) {
                 if ((st = op_backward(R, S, s, r, i)) != LRCNN_OK) return st;
             }
             CK(join_side(R));
+            if (r == N - 1 && zr_plan(P) && (st = zr_exchange(R, S, true)) != LRCNN_OK) return st;
         }
         if (P.opts.world > 1 && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, dfull_view(R.ws + P.dfull_off[(s + 1) & 1], P.t[S.in_t]), true)) != LRCNN_OK)
@@ -1097,6 +1157,34 @@ lrcnn_status lrcnn_plan_rows(const lrcnn_plan_t *plan, int seg, int band, int ti
     if (lo) *lo = S.lo[band][tid];
     if (a) *a = S.a[band][tid];
     if (b) *b = S.b[band][tid];
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_read_end(const lrcnn_plan_t *plan, int seg, int band, int tid, int *hb) {
+    if (!plan || !hb || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad segment");
+    const Segment &S = plan->P.seg[seg];
+    if (band < 0 || band >= (int)S.E.size()) return fail(LRCNN_E_ARG, "bad band");
+    bool in = false;
+    for (int t : S.tensors) in = in || t == tid;
+    if (!in) return fail(LRCNN_E_ARG, "tensor not in segment");
+    *hb = S.hb[band][tid];
+    return LRCNN_OK;
+}
+
+lrcnn_status lrcnn_plan_zr_halo(const lrcnn_plan_t *plan, int seg, int max, int *n, int *tid, int *dir, int *r0,
+                                int *r1) {
+    if (!plan || !n || seg < 0 || seg >= (int)plan->P.seg.size()) return fail(LRCNN_E_ARG, "bad args");
+    const Segment &S = plan->P.seg[seg];
+    std::vector<std::array<int, 4>> v;
+    for (auto &z : S.zr_from_below) v.push_back({z.t, 0, z.r0, z.r1});
+    for (auto &z : S.zr_to_above) v.push_back({z.t, 1, z.r0, z.r1});
+    *n = (int)v.size();
+    for (int i = 0; i < *n && i < max; ++i) {
+        if (tid) tid[i] = v[i][0];
+        if (dir) dir[i] = v[i][1];
+        if (r0) r0[i] = v[i][2];
+        if (r1) r1[i] = v[i][3];
+    }
     return LRCNN_OK;
 }
 

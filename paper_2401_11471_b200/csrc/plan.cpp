@@ -86,7 +86,7 @@ static size_t delta_slots(Plan &P, const Segment &S, size_t B, size_t E, bool as
         fw[t] = f;
         lr[t] = ti.producer;
         int cap = 0;
-        for (int r = 0; r < N; ++r) cap = std::max(cap, S.b[r][t] - S.lo[r][t]);
+        for (int r = 0; r < N; ++r) cap = std::max(cap, S.hb[r][t] - S.lo[r][t]);
         bytes[t] = align_up(B * std::max(cap, 1) * (size_t)ti.W * ti.Cp * E);
         ts.push_back(t);
     }
@@ -300,17 +300,76 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             LO[t] = lo; HI[t] = hi;
         }
     };
+    // Zero-redundancy sharding (LRCNN_FLAG_ZERO_REDUNDANCY): every row of every tensor
+    // is computed by ONE rank.  The rank boundary of tensor t at output cut C is F_C(t), the lowest row
+    // of t the outputs [C, H_out) need (the 2PS interval rule run from the bottom: F(out) = C,
+    // F(t) = min over consumers u of max(0, F(u) s - p)); rank g owns [F_{C_g}(t), F_{C_{g+1}}(t)).
+    // A rank's rows then depend only on its own rows and on rows BELOW its range (the weak dependency
+    // across the cut, runs upward only): its last band reads a few rows of every tensor
+    // that rank g+1 computes in its FIRST band -- no recomputation, one halo message per tensor per
+    // pass, and no rank waits for another's whole sweep.
+    const bool zr = world > 1 && (opts->flags & LRCNN_FLAG_ZERO_REDUNDANCY) && opts->mode == LRCNN_2PS;
+    auto cutF = [&](const Segment &S, int C, std::vector<int> &F) {
+        F.assign(T, 0);
+        std::vector<char> inside(T, 0);
+        for (int i : S.ops) inside[i + 1] = 1;
+        F[S.out_t] = std::min(C, P.t[S.out_t].H);
+        std::vector<int> order(S.tensors.rbegin(), S.tensors.rend());
+        order.push_back(S.in_t);
+        for (int t : order) {
+            if (t == S.out_t) continue;
+            int f = INT_MAX;
+            for (auto &c : P.t[t].cons) {
+                if (!inside[c.op + 1]) continue;
+                const OpInfo &o = P.op[c.op];
+                const int fu = F[c.op + 1];
+                if (fu >= P.t[c.op + 1].H) continue;   // that consumer needs no row at or below the cut
+                f = std::min(f, window_role(o, c.role) ? std::max(0, fu * o.d.s - o.d.p) : fu);
+            }
+            F[t] = f == INT_MAX ? P.t[t].H : std::min(f, P.t[t].H);
+        }
+    };
+    auto zr_ext = [&](const Segment &S, int g, std::vector<int> &LO, std::vector<int> &HI) {
+        int ol, oh;
+        split(P.t[S.out_t].H, g, ol, oh);
+        std::vector<int> Ft, Fb;
+        cutF(S, ol, Ft);
+        cutF(S, oh, Fb);
+        LO.assign(T, 0); HI.assign(T, 0);
+        for (int t : S.tensors) {
+            LO[t] = g == 0 ? 0 : Ft[t];
+            HI[t] = g == world - 1 ? P.t[t].H : Fb[t];
+        }
+        LO[S.out_t] = ol; HI[S.out_t] = oh;
+        int rl = INT_MAX, rb = 0;   // the segment input: the rows this rank's ops read
+        std::vector<char> inside(T, 0);
+        for (int i : S.ops) inside[i + 1] = 1;
+        for (auto &c : P.t[S.in_t].cons) {
+            if (!inside[c.op + 1]) continue;
+            const OpInfo &o = P.op[c.op];
+            const int lu = LO[c.op + 1], hu = HI[c.op + 1];
+            if (hu <= lu) continue;
+            const bool w = window_role(o, c.role);
+            rl = std::min(rl, w ? std::max(0, lu * o.d.s - o.d.p) : lu);
+            rb = std::max(rb, w ? std::min(P.t[S.in_t].H, (hu - 1) * o.d.s - o.d.p + o.d.k) : hu);
+        }
+        LO[S.in_t] = rl == INT_MAX ? 0 : rl;
+        HI[S.in_t] = rb;
+    };
     for (size_t si = 0; si < P.seg.size(); ++si) {
         Segment &S = P.seg[si];
         if (P.t[S.out_t].H < world) { err = "fewer segment-output rows than ranks"; return LRCNN_E_INFEASIBLE; }
         split(P.t[S.out_t].H, rank, S.own_lo, S.own_hi);
         split(P.t[S.in_t].H, rank, S.in_own_lo, S.in_own_hi);
         if (si > 0) { S.in_own_lo = P.seg[si - 1].own_lo; S.in_own_hi = P.seg[si - 1].own_hi; }
-        ext(S, S.own_lo, S.own_hi, S.LO, S.HI);
-        if (world > 1 && rank == world - 1)
-            for (int t : S.tensors) if (t != S.out_t) S.HI[t] = P.t[t].H;   // last rank: all trailing rows
-        if (world == 1)
-            for (int t : S.tensors) if (t != S.out_t) { S.LO[t] = 0; S.HI[t] = P.t[t].H; }
+        if (zr) zr_ext(S, rank, S.LO, S.HI);
+        else {
+            ext(S, S.own_lo, S.own_hi, S.LO, S.HI);
+            if (world > 1 && rank == world - 1)
+                for (int t : S.tensors) if (t != S.out_t) S.HI[t] = P.t[t].H;   // last rank: all trailing rows
+            if (world == 1)
+                for (int t : S.tensors) if (t != S.out_t) { S.LO[t] = 0; S.HI[t] = P.t[t].H; }
+        }
         if (world > 1 && S.in_t != 0) {
             // halo of the segment input from the neighbours; must come from adjacent ranks only
             for (int d = -1; d <= 1; d += 2) {
@@ -319,7 +378,8 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
                 int gol, goh;
                 split(P.t[S.out_t].H, g, gol, goh);
                 std::vector<int> LOg, HIg;
-                ext(S, gol, goh, LOg, HIg);
+                if (zr) zr_ext(S, g, LOg, HIg);
+                else ext(S, gol, goh, LOg, HIg);
                 int pl, ph;   // rows of the input tensor rank g owns (its previous-segment output split)
                 split(P.t[S.in_t].H, g, pl, ph);
                 // FP: what I need from g / what g needs from me
@@ -433,7 +493,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             if (t == S.out_t) continue;
             int cap = 0, ccap = 0;
             for (int r = 0; r < N; ++r) {
-                cap = std::max(cap, S.b[r][t] - S.lo[r][t]);
+                cap = std::max(cap, S.hb[r][t] - S.lo[r][t]);
                 ccap = std::max(ccap, S.a[r][t] - S.lo[r][t]);
             }
             const size_t rb = (size_t)P.t[t].W * P.t[t].Cp * Esz;
@@ -446,7 +506,80 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         lrcnn_status st = make_bands(S, 0);
         if (st != LRCNN_OK) return st;
     }
-    if ((opts->flags & LRCNN_FLAG_BALANCED_BANDS) && opts->mode != LRCNN_COLUMN) {
+    // buffer ends: one past the last row of t the consumers' computed rows read (== b except in the
+    // last band of a zero-redundancy rank, whose reads reach into rank g+1's first rows)
+    auto band_reads = [&](Segment &S) {
+        const int N = (int)S.E.size();
+        S.hb = S.b;
+        for (int r = 0; r < N; ++r)
+            for (int i : S.ops) {
+                const OpInfo &o = P.op[i];
+                const int u = o.out_t, au = S.a[r][u], bu = S.b[r][u];
+                if (bu <= au) continue;
+                for (int role = 0; role < 2; ++role) {
+                    const int tin = role == 0 ? o.d.src : o.d.res;
+                    if (tin < 0 || tin == S.in_t) continue;
+                    const bool w = window_role(o, role);
+                    const int h = w ? std::min(P.t[tin].H, (bu - 1) * o.d.s - o.d.p + o.d.k) : bu;
+                    S.hb[r][tin] = std::max(S.hb[r][tin], h);
+                }
+            }
+    };
+    if (zr) {
+        // bands inside each rank as planned (no balanced / merged variants: every rank must know its
+        // neighbours' band structure exactly), then the halo schedule with ranks g-1 and g+1
+        for (size_t si = 0; si < P.seg.size(); ++si) {
+            Segment &S = P.seg[si];
+            band_reads(S);
+            const int N = (int)S.E.size();
+            for (int r = 0; r + 1 < N; ++r)
+                for (int t : S.tensors)
+                    if (t != S.out_t && S.hb[r][t] > S.b[r][t]) {
+                        err = "zero-redundancy: band " + std::to_string(r) + " reads past its rank's rows (use fewer bands)";
+                        return LRCNN_E_INFEASIBLE;
+                    }
+            auto neighbour = [&](int g, Segment &Q) -> lrcnn_status {
+                Q = S;
+                split(P.t[S.out_t].H, g, Q.own_lo, Q.own_hi);
+                zr_ext(S, g, Q.LO, Q.HI);
+                lrcnn_status st2 = make_bands(Q, 0);
+                if (st2 != LRCNN_OK) return st2;
+                band_reads(Q);
+                return LRCNN_OK;
+            };
+            S.zr_from_below.clear(); S.zr_to_above.clear();
+            if (rank + 1 < world) {   // my last band's halo from below: computed by rank+1's band 0
+                if (N < 2) { err = "zero-redundancy needs >= 2 bands on every rank but the last"; return LRCNN_E_INFEASIBLE; }
+                Segment Q;
+                const lrcnn_status stq = neighbour(rank + 1, Q);
+                if (stq != LRCNN_OK) return stq;
+                for (int t : S.tensors) {
+                    if (t == S.out_t) continue;
+                    const int r0 = S.HI[t], r1 = S.hb[N - 1][t];
+                    if (r1 <= r0) continue;
+                    if (r1 > Q.b[0][t] || r1 > Q.HI[t]) {
+                        err = "zero-redundancy: halo deeper than rank " + std::to_string(rank + 1) + "'s first band";
+                        return LRCNN_E_INFEASIBLE;
+                    }
+                    S.zr_from_below.push_back({t, r0, r1});
+                }
+            }
+            if (rank > 0) {           // rank-1's last band reads my first rows
+                Segment Q;
+                const lrcnn_status stq = neighbour(rank - 1, Q);
+                if (stq != LRCNN_OK) return stq;
+                const int NQ = (int)Q.E.size();
+                for (int t : S.tensors) {
+                    if (t == S.out_t) continue;
+                    const int r0 = Q.HI[t], r1 = Q.hb[NQ - 1][t];
+                    if (r1 > r0) S.zr_to_above.push_back({t, r0, r1});
+                }
+            }
+        }
+    } else {
+        for (Segment &S : P.seg) band_reads(S);
+    }
+    if ((opts->flags & LRCNN_FLAG_BALANCED_BANDS) && opts->mode != LRCNN_COLUMN && !zr) {
         size_t budget = 0;
         for (const Segment &S : P.seg) budget = std::max(budget, seg_arena(S));
         for (Segment &S : P.seg) {
@@ -454,6 +587,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             for (int nb = 1; nb < n0; ++nb) {
                 Segment T2 = S;
                 if (make_bands(T2, nb) != LRCNN_OK) continue;
+                band_reads(T2);
                 if (seg_arena(T2) <= budget) { S = T2; break; }
             }
         }
@@ -525,6 +659,24 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             }
         }
     }
+    // zero-redundancy halo buffers (persistent from FP to BP): the rows from below (activations in,
+    // their delta out) and my first rows the rank above reads (activations out, their delta in)
+    for (Segment &S : P.seg) {
+        for (auto &z : S.zr_from_below) {
+            TensorInfo &ti = P.t[z.t];
+            const size_t by = B * (size_t)(z.r1 - z.r0) * rowbytes(z.t);
+            ti.zr_in_off = alloc(by); ti.zr_dout_off = alloc(by);
+            ti.zr_in_r0 = z.r0; ti.zr_in_r1 = z.r1;
+            M.halo_cache += 2 * by;
+        }
+        for (auto &z : S.zr_to_above) {
+            TensorInfo &ti = P.t[z.t];
+            const size_t by = B * (size_t)(z.r1 - z.r0) * rowbytes(z.t);
+            ti.zr_out_off = alloc(by); ti.zr_din_off = alloc(by);
+            ti.zr_out_r0 = z.r0; ti.zr_out_r1 = z.r1;
+            M.halo_cache += 2 * by;
+        }
+    }
     // full-width delta of segment outputs, ping-pong: buffer p holds the outputs of the segments
     // with index parity p (segment s reads its output delta from s & 1 and writes its input delta
     // into the other), so each buffer is sized for its own parity's largest map only
@@ -566,7 +718,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             TensorInfo &ti = P.t[t];
             int cap = 0, ccap = 0;
             for (int r = 0; r < N; ++r) {
-                cap = std::max(cap, S.b[r][t] - S.lo[r][t]);
+                cap = std::max(cap, S.hb[r][t] - S.lo[r][t]);
                 ccap = std::max(ccap, S.a[r][t] - S.lo[r][t]);
             }
             ti.cap = std::max(cap, 1);
@@ -589,7 +741,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     for (Segment &S : P.seg) {
         S.fp_r0.clear(); S.fp_lo.clear(); S.fp_a.clear(); S.fp_b.clear();
         const int N = (int)S.E.size();
-        if (!(opts->flags & LRCNN_FLAG_FP_MERGE) || opts->mode != LRCNN_2PS || N < 2) continue;
+        if (!(opts->flags & LRCNN_FLAG_FP_MERGE) || opts->mode != LRCNN_2PS || N < 2 || zr) continue;
         auto fp_arena = [&](int m, std::vector<int> *caps) {
             size_t a = 0;
             for (int t : S.tensors) {

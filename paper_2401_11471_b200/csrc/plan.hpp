@@ -45,6 +45,10 @@ struct TensorInfo {
     // (last reader); dreuse = the slot held an earlier tensor's delta in the same band
     int dfw = -1, dlr = -1;
     bool dreuse = false;
+    // zero-redundancy sharding: rows [zr_in_r0, zr_in_r1) come from rank+1 (activations in, their delta
+    // out); rows [zr_out_r0, zr_out_r1) of mine go to rank-1 (activations out, their delta in)
+    size_t zr_in_off = 0, zr_dout_off = 0, zr_out_off = 0, zr_din_off = 0;
+    int zr_in_r0 = 0, zr_in_r1 = 0, zr_out_r0 = 0, zr_out_r1 = 0;
 };
 
 struct OpInfo {
@@ -79,6 +83,12 @@ struct Segment {
     // merged per-band ranges live in fp_lo / fp_a / fp_b (empty: FP uses the BP bands)
     std::vector<int> fp_r0;
     std::vector<std::vector<int>> fp_lo, fp_a, fp_b;
+    // buffer end per band and tensor: one past the last row the band's consumers read (== b unless a
+    // zero-redundancy rank's last band reads rows of rank+1)
+    std::vector<std::vector<int>> hb;
+    // zero-redundancy halo schedule of the internal tensors (tensor, rows)
+    struct ZrRows { int t, r0, r1; };
+    std::vector<ZrRows> zr_from_below, zr_to_above;
 };
 
 struct ProfileSlot {

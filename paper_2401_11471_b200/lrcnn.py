@@ -26,6 +26,7 @@ FLAG_FP_MERGE = 16
 FLAG_DP = 32
 FLAG_REQUIRE_TC = 64
 FLAG_AUTO_SEGMENTS = 128
+FLAG_ZERO_REDUNDANCY = 256
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 
@@ -70,7 +71,7 @@ HOST_EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
 HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float), ctypes.c_size_t)
 
 EXPORTS = ["lrcnn_plan", "lrcnn_plan_budget", "lrcnn_plan_greedy", "lrcnn_plan_turning_point", "lrcnn_plan_free", "lrcnn_plan_sizes", "lrcnn_plan_tensor", "lrcnn_plan_param",
-           "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_fp_bands", "lrcnn_plan_memory", "lrcnn_forward_rows",
+           "lrcnn_plan_nsegs", "lrcnn_plan_seg", "lrcnn_plan_rows", "lrcnn_plan_read_end", "lrcnn_plan_zr_halo", "lrcnn_plan_fp_bands", "lrcnn_plan_memory", "lrcnn_forward_rows",
            "lrcnn_backward_rows", "lrcnn_step", "lrcnn_step_grads", "lrcnn_sgd", "lrcnn_profile_enable", "lrcnn_profile_read",
            "lrcnn_profile_reset", "lrcnn_profile_dump", "lrcnn_profile_kernels", "lrcnn_plan_shard", "lrcnn_plan_xfers",
            "lrcnn_comm_nccl_unique_id", "lrcnn_comm_init_nccl", "lrcnn_comm_loopback_group",
@@ -104,6 +105,8 @@ def lib():
     L.lrcnn_plan_seg.argtypes = [vp, i, ip, ip, ip]
     L.lrcnn_plan_fp_bands.argtypes = [vp, i, ip, ip]
     L.lrcnn_plan_rows.argtypes = [vp, i, i, i, ip, ip, ip]
+    L.lrcnn_plan_read_end.argtypes = [vp, i, i, i, ip]
+    L.lrcnn_plan_zr_halo.argtypes = [vp, i, i, ip, ip, ip, ip, ip]
     L.lrcnn_plan_memory.argtypes = [vp, ctypes.POINTER(MemoryReport)]
     L.lrcnn_forward_rows.argtypes = [vp, vp, vp, vp, vp, sz, vp]
     L.lrcnn_backward_rows.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
@@ -283,6 +286,19 @@ class Plan:
         lo, a, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _check(lib().lrcnn_plan_rows(self.h, seg, band, tid, ctypes.byref(lo), ctypes.byref(a), ctypes.byref(b)))
         return lo.value, a.value, b.value
+
+    def read_end(self, seg, band, tid):
+        """One past the last row of tid band `band` reads (lrcnn_plan_read_end)."""
+        hb = ctypes.c_int()
+        _check(lib().lrcnn_plan_read_end(self.h, seg, band, tid, ctypes.byref(hb)))
+        return hb.value
+
+    def zr_halo(self, seg):
+        """Zero-redundancy halo schedule of segment seg: [(tensor, dir, r0, r1)] (lrcnn_plan_zr_halo)."""
+        n = ctypes.c_int()
+        arrs = [(ctypes.c_int * 256)() for _ in range(4)]
+        _check(lib().lrcnn_plan_zr_halo(self.h, seg, 256, ctypes.byref(n), *arrs))
+        return [tuple(a[i] for a in arrs) for i in range(n.value)]
 
     def shard(self, seg, tid):
         """(own_lo, own_hi, lo, hi): owned segment-output rows and tensor tid's extended range."""

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 from paper_2401_11471_b200 import lrcnn as LB  # noqa: E402
 
 
-def run_sharded(net, B, prec, world, params, x, lab, capture=False, **kw):
+def run_sharded(net, B, prec, world, params, x, lab, capture=False, flags=0, **kw):
     """One lrcnn_step_grads per rank (loopback communicator, one host thread + stream per rank).
     capture: every rank records the rows it computes of every map (lrcnn_debug_capture into a
     NaN-filled full-height buffer); the merged maps (ranks compute identical values on overlapping
@@ -28,7 +28,7 @@ def run_sharded(net, B, prec, world, params, x, lab, capture=False, **kw):
     plans, states, bufs = [], [], []
     L = len(net["ops"])
     for g in range(world):
-        p = LB.Plan(net, B, mode="2ps", prec=prec, world=world, rank=g, **kw)
+        p = LB.Plan(net, B, mode="2ps", prec=prec, world=world, rank=g, flags=flags, **kw)
         p.set_comm(comms[g])
         ds = LB.DeviceState(p)
         ds.load(params=params, x=x, labels=lab)
@@ -195,3 +195,20 @@ def test_dp_replicas_sum_gradients(prec):
         assert abs(float(states[g].loss.cpu()) - single[g][0]) <= 1e-6 * max(1.0, abs(single[g][0]))
     for c in comms:
         c.free()
+
+
+@pytest.mark.parametrize("prec,world", [("fp32", 2), ("fp32", 3), ("bf16", 2), ("bf16", 3)])
+def test_zero_redundancy_sharding_vs_oracle(prec, world):
+    """LRCNN_FLAG_ZERO_REDUNDANCY: every row of every tensor on one rank, the halo
+    rows of rank g+1's first band received after the first band and their delta sent back; loss
+    vs the plain oracle, every rank's gradients vs the oracle conditioned on the merged maps (R17d;
+    the maps are captured per rank and must tile every tensor)."""
+    net = WL.resnet50(H=192, W=48, width_div=4, blocks=(2, 1, 1, 1))
+    B = 2
+    params, x, lab, loss_ref, _, _ = oracle_ref(net, B, 7, 0.1, bf16=(prec == "bf16"))
+    res, ts = run_sharded(net, B, prec, world, params, x, lab, capture=True, flags=LB.FLAG_ZERO_REDUNDANCY,
+                          n_bands=2)
+    tol = 2e-2 if prec == "bf16" else 1e-5
+    for rank, (loss, _) in enumerate(res):
+        assert abs(loss - loss_ref) <= tol * abs(loss_ref), (rank, loss, loss_ref)
+    check_conditioned(net, params, ts, lab, res, prec)
