@@ -187,11 +187,14 @@ int comm_exchange(Comm *c, const std::vector<XferBuf> &xs, cudaStream_t st, cons
     cudaEventRecord(G.ready[r], st);
     G.pub[r] = xs;
     G.barrier();
+    // the k-th receive from a peer matches that peer's k-th send to this rank (NCCL's ordering)
+    std::vector<int> seen(G.world, 0);
     for (const XferBuf &x : xs) {
         if (x.send) continue;
         const XferBuf *src = nullptr;
+        int k = seen[x.peer]++;
         for (const XferBuf &y : G.pub[x.peer])
-            if (y.send && y.peer == r) src = &y;
+            if (y.send && y.peer == r && k-- == 0) { src = &y; break; }
         if (!src || src->bytes != x.bytes) { e = "loopback: unmatched transfer"; *err = e.c_str(); return 1; }
         cudaStreamWaitEvent(st, G.ready[x.peer], 0);
         cudaMemcpyAsync(x.ptr, src->ptr, x.bytes, cudaMemcpyDeviceToDevice, st);
