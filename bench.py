@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group backend; gloo only to exercise the N>1 code path on one GPU")
+    ap.add_argument("--zero-redundancy", action="store_true",
+                    help="--parallel rows: zero-redundancy sharding (every row on one rank, halo from the rank "
+                         "below after the first band; LRCNN_FLAG_ZERO_REDUNDANCY) instead of OverL at the cuts")
     ap.add_argument("--parallel", default="rows", choices=["dp", "rows"],
                     help="N>1: rows = the same batch row-sharded across ranks with NCCL halo exchange (default, "
                          "the north star's split, SURVEY 8(e)); dp = each rank its own batch, wgrad all-reduce")
@@ -363,7 +366,8 @@ def main():
             lib_dp = False
             plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
     elif rows:
-        plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, world=world, rank=rank, **kw)
+        rflags = flags | (LB.FLAG_ZERO_REDUNDANCY if a.zero_redundancy else 0)
+        plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=rflags, world=world, rank=rank, **kw)
         uid = [LB.Comm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = LB.Comm.nccl(uid[0], rank, world)
@@ -625,7 +629,9 @@ def main():
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[0,1) images, U{0..9} labels)",
                "config": {"workload": "%s, batch %d per GPU, bf16" % (CONFIGS[a.config][4], B),
                           "global_batch": gb, "seq_len": None,
-                          "parallelism": ("rows%d (row sharding, NCCL halo exchange + all-reduce)" % world if rows
+                          "parallelism": ("rows%d (row sharding%s, NCCL halo exchange + per-segment wgrad all-reduce)"
+                                          % (world, ", zero redundancy" if a.zero_redundancy else ", OverL at the cuts")
+                                          if rows
                                           else "dp%d (per-segment NCCL wgrad all-reduce overlapped with the backward)" % world
                                           if lib_dp else "dp%d (wgrad all-reduce after the step, %s)" % (world, a.backend)
                                           if world > 1 else "single GPU"),
