@@ -11,6 +11,7 @@
 // Every device operation is enqueued on the caller's stream; nothing is
 // allocated on the device.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <array>
 #include <cstdio>
@@ -133,6 +134,17 @@ static View dlt_view(Run &R, const Segment &S, int s, int r, int t) {
     (void)nseg;
     return band_view(R.ws + ti.dlt_off, ti, S.lo[r][t], S.hb[r][t]);
 }
+
+// NVTX ranges (header-only nvtx3: a no-op unless a tool such as nsys / ncu --nvtx is attached):
+// one range per segment and band of the FP and the BP, the head and the exchanges
+struct Nvtx {
+    explicit Nvtx(const char *fmt, int a = 0, int b = 0) {
+        char buf[64];
+        snprintf(buf, sizeof buf, fmt, a, b);
+        nvtxRangePushA(buf);
+    }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 static bool zr_plan(const Plan &P) { return P.opts.world > 1 && (P.opts.flags & LRCNN_FLAG_ZERO_REDUNDANCY); }
 
@@ -467,11 +479,14 @@ static lrcnn_status run_forward(Run &R) {
             F.E.clear();
             for (size_t k = 0; k < S.fp_r0.size(); ++k)
                 F.E.push_back(S.E[k + 1 < S.fp_r0.size() ? S.fp_r0[k + 1] - 1 : S.E.size() - 1]);
-            for (int k = 0; k < (int)S.fp_r0.size(); ++k)
+            for (int k = 0; k < (int)S.fp_r0.size(); ++k) {
+                Nvtx nv("FP seg %d merged band %d", (int)(&S - R.P.seg.data()), k);
                 if ((st = band_forward_merged(R, S, F, k)) != LRCNN_OK) return st;
+            }
             continue;
         }
         for (int r = 0; r < (int)S.E.size(); ++r) {
+            Nvtx nv("FP seg %d band %d", (int)(&S - R.P.seg.data()), r);
             if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) return st;
             if (r == 0 && zr_plan(R.P)) {   // my first rows the rank above reads, then the exchange
                 for (const Segment::ZrRows &z : S.zr_to_above) {
@@ -822,6 +837,7 @@ static lrcnn_status run_backward(Run &R) {
         }
         const int N = (int)S.E.size();
         for (int r = N - 1; r >= 0; --r) {
+            Nvtx nv("BP seg %d band %d", s, r);
             if (recompute && (st = band_forward(R, S, r, false, true)) != LRCNN_OK) return st;
             for (auto it = S.ops.rbegin(); it != S.ops.rend(); ++it) {
                 const int i = *it;
@@ -1290,6 +1306,7 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
     // head on the pooled z^L: each rank pools its own rows, the partial sums are all-reduced
     const float hw = (float)z.H * z.W;
     float *scratch = (float *)(w + P.head_off);
+    Nvtx nv("head");
     CK(head_gap(P.opts.prec, R.zl, P.net.B, z.ck_rows * z.W, z.Cp, hw, scratch, R.st));
     if (P.opts.world > 1) {
         const char *err = nullptr;
