@@ -8,6 +8,8 @@
 // test on the GLOBAL row index, never on the band edge.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <mutex>
+#include <set>
 
 #include <cstdlib>
 #include <utility>
@@ -864,6 +866,12 @@ __global__ void __launch_bounds__(256) k_pool3s2_bwd(PoolArgs A) {
             if (have) {
                 code = make_uint4(cw[0], cw[1], cw[2], cw[3]);
                 dyv = *reinterpret_cast<const uint4 *>((const bf16 *)A.dy.p + voff(A.dy, b, y, x) + cv * 8);
+                if (A.gate) {   // the delta goes to the argmax, whose activation is the window max:
+                    dyv.x &= bf2_gt_mask(best[0], 0u);   // gate it here ([max > 0], ReLU'(0) = 0) and
+                    dyv.y &= bf2_gt_mask(best[1], 0u);   // phase 2 never re-reads the activation
+                    dyv.z &= bf2_gt_mask(best[2], 0u);
+                    dyv.w &= bf2_gt_mask(best[3], 0u);
+                }
             }
         }
         scode[pix * CV + cv] = code;
@@ -888,11 +896,11 @@ __global__ void __launch_bounds__(256) k_pool3s2_bwd(PoolArgs A) {
         if ((g & 1) == 0) window_row(g >> 1, 1);
         else { window_row(g >> 1, 2); window_row((g >> 1) + 1, 0); }
         bf16 *dp = (bf16 *)A.dx.p + voff(A.dx, b, g, xa) + cv * 8;
-        const bf16 *ap = (const bf16 *)A.act.p + voff(A.act, b, g, xa) + cv * 8;
+        // (gated in phase 1; an accumulated old delta was gated by its own writer: gate on write)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             if (e == 1 && xa + 1 >= Wi) break;
-            float o[8], a[8];
+            float o[8];
             const float (&acc)[8] = e ? accB : accA;
             if (A.acc) {
                 ld8(dp + e * A.dx.Cp, o);
@@ -901,12 +909,6 @@ __global__ void __launch_bounds__(256) k_pool3s2_bwd(PoolArgs A) {
             } else {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) o[j] = acc[j];
-            }
-            if (A.gate) {
-                ld8(ap + e * A.act.Cp, a);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (!(a[j] > 0.f)) o[j] = 0.f;
             }
             st8(dp + e * A.dx.Cp, o);
         }
@@ -1075,7 +1077,17 @@ cudaError_t simt_pool_bwd(int prec, const PoolArgs &a, cudaStream_t st) {
     } else if (prec && a.k == 3 && a.s == 2 && a.p == 1 && a.dx.Cp % 8 == 0 && a.dx.Cp == a.dy.Cp && a.B <= 65535) {
         const size_t shm = (size_t)2 * (kP3TR / 2 + 2) * (kP3TP + 1) * (a.dy.Cp / 8) * 16;
         dim3 g((a.dx.W + 2 * kP3TP - 1) / (2 * kP3TP), (a.rb - a.ra + kP3TR - 1) / kP3TR, a.B);
-        cudaFuncSetAttribute(k_pool3s2_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (shm > 48 * 1024) {   // once per (device, size): the attribute is per device
+            static std::mutex mu;
+            static std::set<std::pair<int, size_t>> done;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            std::lock_guard<std::mutex> lk(mu);
+            if (!done.count({dev, shm})) {
+                cudaFuncSetAttribute(k_pool3s2_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+                done.insert({dev, shm});
+            }
+        }
         launch_simt(k_pool3s2_bwd, g, kT, shm, st, a);
     } else if (pool_tiled(a)) {
         const int ny = pool_tile_rows(kPoolTR, a.k, a.s), nx = pool_tile_rows(kPoolTC, a.k, a.s);
