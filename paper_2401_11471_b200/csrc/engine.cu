@@ -146,6 +146,11 @@ struct Nvtx {
     ~Nvtx() { nvtxRangePop(); }
 };
 
+static int env_chunk_mb() {
+    const char *e = getenv("LRCNN_L2_CHUNK_MB");
+    return e && *e ? atoi(e) : 0;
+}
+
 static bool zr_plan(const Plan &P) { return P.opts.world > 1 && (P.opts.flags & LRCNN_FLAG_ZERO_REDUNDANCY); }
 
 static const void *prm(Run &R, size_t off) { return off == (size_t)-1 ? nullptr : R.params + off * R.E; }
@@ -621,65 +626,82 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     if (o.d.kind == LRCNN_OP_CONV) {
         float *g = R.grads;
         lrcnn_status st0;
-        // wgrad and the bias/affine reduction only read complete data of this band: run them on
-        // the side stream so they overlap the dgrad chain (joined at the end of the band)
-        cudaStream_t gst = R.st;
-        if (R.side) { CK(fork_side(R)); gst = R.side; }
-        bool db_done = false;
         const void *gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
+        // L2-sized row chunks (1x1 stride-1 convolutions, LRCNN_L2_CHUNK_MB > 0): the wgrad of a chunk
+        // (side stream) and its dgrad (main stream) run together over the same rows, so the second
+        // reader of delta(out) and of the input activation finds them in L2 instead of HBM
+        std::vector<int> cuts = {a, b};
         {
-            WgradArgs A;
-            A.dy = dy; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
-            A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
-            // bias (VGG) or affine (ResNet) parameter gradients fused into the tensor-core wgrad:
-            // db / dbeta = sum dy, dgamma = sum_{tap,ci} W * (sum_p dy x)
-            if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
-            if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
-            ++P.launches;
-            ProfScope ps(R, 1, conv_flops(P, o, b - a), i * 8 + 2, conv_bytes(P, o, a, b, 2),
-                         conv_bytes(P, o, a, b, 2, 0, 0, true));
-            bool tc = false;
-            if (P.use_tc) {
-                tc = tc_conv_wgrad(A, gst);
-                if (tc) ++P.tc_launches;
-                else if ((st0 = tc_declined(P, i, "wgrad")) != LRCNN_OK) return st0;
-            }
-            if (!tc) CK(simt_conv_wgrad(R.prec, A, gst));
-            CK(cudaGetLastError());
-            db_done = A.db_done;
-            // dgamma comes only from the wgrad (sum_{tap,ci} W * sum_p dy x, exact for gamma = 0)
-            if (A.dg && !A.dg_done) return fail(LRCNN_E_STATE, "wgrad of op " + std::to_string(i) + " did not take dgamma");
-        }
-        if (o.d.epi != LRCNN_EPI_NONE && !db_done) {   // bias / beta: column sums of dy
-            ParamGradArgs A;
-            A.dy = dy;
-            A.db = g + (o.d.epi == LRCNN_EPI_AFFINE ? o.beta_off : o.b_off);
-            A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
-            ++P.launches;
-            ProfScope ps(R, 2, 0, i * 8 + 3);
-            CK(simt_param_grad(R.prec, A, gst));
-        }
-
-        if (need_dx) {
-            DgradArgs A;
-            A.dy = dy; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);
-            A.gate = tin.relu; A.w = prm(R, o.w_off); A.wt = R.ws + o.wt_off; A.gamma = gamma;
-            A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.B = B;
-            A.ra = std::max(0, a * o.d.s - o.d.p);
-            A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
-            A.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
-            const int fu = fused_res(P, S, o.in_t);   // residual conv whose output delta is the addend
-            if (fu >= 0) {
-                const int tu = P.op[fu].out_t, oa = S.a[r][tu], ob = S.b[r][tu];
-                if (ob > oa) {
-                    A.add = sub_rows(dlt_view(R, S, s, r, tu), oa, ob, R.E);
-                    A.add_on = 1;
+            static const int chunk_mb = env_chunk_mb();
+            const bool pointwise = o.d.k == 1 && o.d.s == 1 && o.d.p == 0 && need_dx;
+            if (chunk_mb > 0 && pointwise) {
+                const double row_bytes = (double)B * P.t[t].W * (P.t[t].Cp + tin.Cp) * R.E;
+                const int per = std::max(1, (int)((double)chunk_mb * 1048576.0 / row_bytes));
+                if (b - a > per) {
+                    cuts.clear();
+                    const int n = (b - a + per - 1) / per;
+                    for (int c = 0; c <= n; ++c) cuts.push_back(a + (int)((long long)(b - a) * c / n));
                 }
             }
+        }
+        bool db_done = true, add_done_all = true, add_any = false;
+        int fu = -1, ra_all = 0, rb_all = 0, write_mode = 0;
+        DgradArgs D0;
+        for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+            const int ca = cuts[c], cb = cuts[c + 1];
+            const View dyc = sub_rows(dlt_view(R, S, s, r, t), ca, cb, R.E);
+            // wgrad and the bias/affine reduction only read complete data of this band: run them on
+            // the side stream so they overlap the dgrad chain (joined at the end of the band)
+            cudaStream_t gst = R.st;
+            if (R.side) { CK(fork_side(R)); gst = R.side; }
             {
+                WgradArgs A;
+                A.dy = dyc; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
+                A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.a = ca; A.b = cb; A.B = B;
+                // bias (VGG) or affine (ResNet) parameter gradients fused into the tensor-core wgrad:
+                // db / dbeta = sum dy, dgamma = sum_{tap,ci} W * (sum_p dy x)
+                if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
+                if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
                 ++P.launches;
-                ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0),
-                             conv_bytes(P, o, a, b, 1, 0, 0, true));
+                ProfScope ps(R, 1, conv_flops(P, o, cb - ca), i * 8 + 2, conv_bytes(P, o, ca, cb, 2),
+                             conv_bytes(P, o, ca, cb, 2, 0, 0, true));
+                bool tc = false;
+                if (P.use_tc) {
+                    tc = tc_conv_wgrad(A, gst);
+                    if (tc) ++P.tc_launches;
+                    else if ((st0 = tc_declined(P, i, "wgrad")) != LRCNN_OK) return st0;
+                }
+                if (!tc) CK(simt_conv_wgrad(R.prec, A, gst));
+                CK(cudaGetLastError());
+                db_done = db_done && A.db_done;
+                // dgamma comes only from the wgrad (sum_{tap,ci} W * sum_p dy x, exact for gamma = 0)
+                if (A.dg && !A.dg_done) return fail(LRCNN_E_STATE, "wgrad of op " + std::to_string(i) + " did not take dgamma");
+            }
+            if (o.d.epi != LRCNN_EPI_NONE && !db_done && cuts.size() > 2)
+                return fail(LRCNN_E_STATE, "chunked wgrad of op " + std::to_string(i) + " did not take the bias sums");
+            if (need_dx) {
+                DgradArgs A;
+                A.dy = dyc; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);
+                A.gate = tin.relu; A.w = prm(R, o.w_off); A.wt = R.ws + o.wt_off; A.gamma = gamma;
+                A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.B = B;
+                A.ra = std::max(0, ca * o.d.s - o.d.p);
+                A.rb = std::min(tin.H, (cb - 1) * o.d.s - o.d.p + o.d.k);
+                if (c == 0) ra_all = A.ra;
+                rb_all = A.rb;
+                A.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
+                write_mode = A.write;
+                fu = fused_res(P, S, o.in_t);   // residual conv whose output delta is the addend
+                if (fu >= 0) {
+                    const int tu = P.op[fu].out_t, oa = S.a[r][tu], ob = S.b[r][tu];
+                    if (ob > oa) {
+                        A.add = sub_rows(dlt_view(R, S, s, r, tu), oa, ob, R.E);
+                        A.add_on = 1;
+                    }
+                }
+                ++P.launches;
+                ProfScope ps(R, 0, conv_flops(P, o, cb - ca), i * 8 + 1,
+                             conv_bytes(P, o, ca, cb, 1, A.write ? 0 : 1, A.gate ? 1 : 0),
+                             conv_bytes(P, o, ca, cb, 1, 0, 0, true));
                 bool tc = false;
                 if (P.use_tc) {
                     tc = tc_conv_dgrad(A, R.st);
@@ -688,17 +710,32 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
                 }
                 if (!tc) CK(simt_conv_dgrad(R.prec, A, R.st));
                 CK(cudaGetLastError());
+                add_done_all = add_done_all && A.add_done;
+                add_any = add_any || A.add_done;
+                D0 = A;
             }
+        }
+        if (add_any && !add_done_all) return fail(LRCNN_E_STATE, "residual addend taken by some dgrad chunks only");
+        if (o.d.epi != LRCNN_EPI_NONE && !db_done) {   // bias / beta: column sums of dy
+            ParamGradArgs A;
+            A.dy = dy;
+            A.db = g + (o.d.epi == LRCNN_EPI_AFFINE ? o.beta_off : o.b_off);
+            A.c_out = o.d.c_out; A.a = a; A.b = b; A.B = B;
+            ++P.launches;
+            ProfScope ps(R, 2, 0, i * 8 + 3);
+            CK(simt_param_grad(R.prec, A, R.side ? R.side : R.st));
+        }
+        if (need_dx) {
             if (fu >= 0) {   // residual rows the dgrad did not take
-                lrcnn_status rs = fused_res_rows(R, S, s, r, i, A.ra, A.rb, A.add_done, false);
+                lrcnn_status rs = fused_res_rows(R, S, s, r, i, ra_all, rb_all, add_done_all && add_any, false);
                 if (rs != LRCNN_OK) return rs;
             }
             const int N = (int)S.E.size();
-            if (A.write && P.opts.mode == LRCNN_2PS && r + 1 < N) {   // + the carry of band r+1, gated
+            if (write_mode && P.opts.mode == LRCNN_2PS && r + 1 < N) {   // + the carry of band r+1, gated
                 const int t = o.in_t, clo = S.lo[r + 1][t], chi = S.a[r + 1][t];
                 if (chi > clo) {
                     EltArgs E;
-                    E.dx = A.dx; E.act = A.act; E.gate = tin.relu;
+                    E.dx = D0.dx; E.act = D0.act; E.gate = tin.relu;
                     E.dy = View{R.ws + tin.carry_off, clo, chi - clo, tin.H, tin.W, tin.Cp,
                                 (long long)tin.carry_cap * tin.W * tin.Cp};
                     E.a = clo; E.b = chi; E.B = B;
