@@ -1887,9 +1887,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 }
             } else {
                 // this thread's row co: 32 consecutive input channels per TMEM load, added with
-                // 16-byte vector reductions (cin_p % 8 == 0, so a 4-group is all in or all out)
+                // 16-byte vector reductions (cin_p % 8 == 0, so a 4-group is all in or all out).  The
+                // pixel splits of one (co, tap, ci) tile finish together and reduce into the same
+                // addresses: each split starts at a different 32-channel chunk so that their
+                // reductions do not queue on the same L2 lines
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int cc = 0; cc < BN / 32; ++cc) {
+                    const int c = (cc + split) % (BN / 32);
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, v);
                     const int ci0 = cit * BN + c * 32;
@@ -2100,11 +2104,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             ptx::tc_fence_after();
             float gdot = 0.f;
 #pragma unroll 1
-            for (int kx = 0; kx < KW; ++kx) {
+            for (int kk = 0; kk < KW; ++kk) {
+                const int kx = (kk + split) % KW;   // pixel splits of a tile start at different taps (see k_wgrad_tc)
                 float *dst = P.dw + ((long long)co * taps + ky * KW + kx) * P.cin_p + cit * BN;
                 const bf16 *wrow = P.w + ((long long)co * taps + ky * KW + kx) * P.cin_p + cit * BN;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int cc = 0; cc < BN / 32; ++cc) {
+                    const int c = (cc + split / KW) % (BN / 32);
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + kx * BN + c * 32, v);
                     const int ci0 = cit * BN + c * 32;
