@@ -1963,6 +1963,276 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ fused 1x1 dgrad + wgrad
+// The backward of a pointwise (1x1, stride 1) convolution in one pass over the band: every 128-pixel
+// tile of delta(out) [CO channels] and of the conv input x [CI channels] is TMA-loaded ONCE and
+// feeds two contractions from the same shared-memory bytes:
+//   dgrad   D1[px][ci] = sum_co delta[px][co] W'[ci][co]   (delta tile as the K-major A operand)
+//   wgrad   D2[co][ci] += sum_px delta[px][co] x[px][ci]   (delta / x tiles as MN-major A / B)
+// D1 goes through the dgrad epilogue (gate-on-write from the x tile already in shared memory, the
+// old delta or the fused residual addend TMA-loaded, TMA store); D2 stays in TMEM over the CTA's
+// contiguous run of tiles and is reduced into the fp32 gradient once at the end (scaled by gamma,
+// with dgamma = sum_ci W * D2 and the beta / bias column sums from dedicated warps).  Separately,
+// dgrad and wgrad each stream delta(out) and x from HBM; here the wgrad reads nothing extra.
+// (CI, CO) = (64, 256) -- the bottleneck's last 1x1 / the projection -- or (256, 64) -- its first 1x1.
+struct TcDw {
+    View dx, act, add;           // delta_in (output), gating activation (== x), fused residual addend
+    float *dw, *db, *dg;
+    const bf16 *gamma, *w;
+    int c_out, gate, write, dg_add;
+    int TW, TH, tiles_x, tiles_y, pix_tiles, per_cta;
+    int out_a, dy_base, x_base, B, tw_log2, th_log2;
+};
+
+template <int CI, int CO>
+struct DwCfg {
+    static constexpr int kDB = CO / 64, kXB = CI / 64;          // 64-channel boxes per tile
+    static constexpr int kStageBytes = (kDB + kXB) * kABytes;    // 80 KB
+    static constexpr int kStages = 2;
+    static constexpr int kWBytes = CI * CO * 2;                  // W' [CI][CO], resident
+    static constexpr int kSmem = kStages * kStageBytes + kWBytes + 2 * kOutStage + 1024 + 512;
+    static constexpr int kD1Bufs = CI <= 64 ? 2 : 1;
+    static constexpr int kMT = CO >= 128 ? CO / 128 : 1;         // wgrad M tiles (128 output channels)
+    static constexpr uint32_t kD2Col = kD1Bufs * CI;
+    static constexpr uint32_t kTmemCols = kD2Col + kMT * CI <= 256 ? 256 : 512;
+};
+static constexpr int kDwThreads = 448;   // producer, MMA, 8 epilogue warps, 4 bias-sum warps
+
+template <int CI, int CO>
+__global__ void __launch_bounds__(kDwThreads, 1)
+    k_dwgrad_pw(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
+                const __grid_constant__ CUtensorMap tmA, const TcDw P) {
+    using Cfg = DwCfg<CI, CO>;
+    constexpr int S = Cfg::kStages, SB = Cfg::kStageBytes, D1B = Cfg::kD1Bufs;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sW = smem + S * SB;
+    uint8_t *sO = sW + Cfg::kWBytes;                 // 2 x 16 KB epilogue staging
+    uint64_t *full = (uint64_t *)(sO + 2 * kOutStage);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *ebar = tempty + 2;                     // epilogue staging loads (2)
+    uint64_t *wbar = ebar + 2;
+    uint64_t *d2full = wbar + 1;
+    uint32_t *tslot = (uint32_t *)(d2full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool bias = P.db != nullptr;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1 + 8 + (bias ? 4 : 0)); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); ptx::mbar_init(ebar + i, 1); }
+        ptx::mbar_init(wbar, 1);
+        ptx::mbar_init(d2full, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmD);
+        ptx::prefetch_tmap(&tmX);
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, Cfg::kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    ptx::griddep_wait();
+    ptx::griddep_launch();
+    const int p0 = blockIdx.x * P.per_cta, p1 = min(p0 + P.per_cta, P.pix_tiles);
+    auto tile_xy = [&](int pt, int &x0, int &y0, int &b) {
+        const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y;
+        b = r / P.tiles_y;
+        x0 = tx * P.TW;
+        y0 = P.out_a + ty * P.TH;
+    };
+
+    if (warp == 0) {
+        if (lane == 0 && p0 < p1) {
+            ptx::mbar_arrive_expect_tx(wbar, Cfg::kWBytes);
+#pragma unroll
+            for (int kc = 0; kc < Cfg::kDB; ++kc) ptx::tma_load_3d(sW + kc * CI * 128, &tmW, wbar, kc * 64, 0, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = p0; pt < p1; ++pt) {
+                int x0, y0, b;
+                tile_xy(pt, x0, y0, b);
+                ptx::mbar_wait(empty + stage, phase ^ 1);
+                uint8_t *st = smem + stage * SB;
+                ptx::mbar_arrive_expect_tx(full + stage, SB);
+#pragma unroll
+                for (int kd = 0; kd < Cfg::kDB; ++kd)
+                    ptx::tma_load_4d(st + kd * kABytes, &tmD, full + stage, kd * 64, x0, y0 - P.dy_base, b);
+#pragma unroll
+                for (int kx = 0; kx < Cfg::kXB; ++kx)
+                    ptx::tma_load_4d(st + (Cfg::kDB + kx) * kABytes, &tmX, full + stage, kx * 64, x0, y0 - P.x_base, b);
+                if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (p0 < p1) {
+            constexpr uint32_t idg = ptx::idesc_bf16(128, CI, 0, 0), iwg = ptx::idesc_bf16(128, CI, 1, 1);
+            const uint64_t dK = ptx::smem_desc_sw128(ptx::smem_u32(smem), 16, 1024);        // K-major delta
+            const uint64_t dW = ptx::smem_desc_sw128(ptx::smem_u32(sW), 16, 1024);          // K-major W'
+            // MN-major: 64-element MN chunks 16 KB apart (delta: M = co; x: N = ci); CO = 64 has one
+            // chunk, so its second M chunk aliases the first (D2 rows 64..127 are never read)
+            const uint64_t dM = ptx::smem_desc_sw128(ptx::smem_u32(smem), CO >= 128 ? kABytes : 0, 1024);
+            const uint64_t dX = ptx::smem_desc_sw128(ptx::smem_u32(smem + Cfg::kDB * kABytes), kABytes, 1024);
+            const uint32_t hK = (uint32_t)(dK >> 32), hW = (uint32_t)(dW >> 32), hM = (uint32_t)(dM >> 32),
+                           hX = (uint32_t)(dX >> 32);
+            ptx::mbar_wait(wbar, 0);
+            ptx::tc_fence_after();
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int pt = p0; pt < p1; ++pt) {
+                ptx::mbar_wait(tempty + acc, aphase ^ 1);
+                ptx::mbar_wait(full + stage, phase);
+                ptx::tc_fence_after();
+                const uint32_t so = stage * (SB >> 4);
+                const uint32_t d1 = tmem + acc * CI;
+#pragma unroll
+                for (int kc = 0; kc < Cfg::kDB; ++kc)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        ptx::umma_bf16_lh(d1, (uint32_t)dK + so + kc * (kABytes >> 4) + 2 * kk, hK,
+                                          (uint32_t)dW + kc * (CI * 128 >> 4) + 2 * kk, hW, idg, (kc | kk) != 0);
+#pragma unroll
+                for (int mt = 0; mt < Cfg::kMT; ++mt)
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        ptx::umma_bf16_lh(tmem + Cfg::kD2Col + mt * CI, (uint32_t)dM + so + mt * 2 * (kABytes >> 4) + kk * 128,
+                                          hM, (uint32_t)dX + so + kk * 128, hX, iwg, (pt != p0 || kk != 0) ? 1u : 0u);
+                ptx::umma_commit(empty + stage);
+                ptx::umma_commit(tfull + acc);
+                if (++stage == S) { stage = 0; phase ^= 1; }
+                if (++acc == D1B) { acc = 0; aphase ^= 1; }
+            }
+            ptx::umma_commit(d2full);
+        }
+    } else if (warp < 10) {
+        // dgrad epilogue: 8 warps, warp (q, hh) = pixels 32q.. of the tile, channels hh*32 .. +32 of
+        // each 64-channel group; the gate is the x tile of the same stage (already in smem)
+        const int q = warp & 3, hh = (warp - 2) >> 2, m = q * 32 + lane;
+        const bool leader = warp == 2 && lane == 0;
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+        const bool dload = !P.write || P.dg_add;
+        const CUtensorMap *tmL = P.write ? &tmA : &tmO;
+        const int lbase = P.write ? P.add.base : P.dx.base;
+        int stage = 0, acc = 0, sb = 0;
+        uint32_t phase = 0, aphase = 0, ephase = 0;
+        for (int pt = p0; pt < p1; ++pt) {
+            int x0, y0, b;
+            tile_xy(pt, x0, y0, b);
+            ptx::mbar_wait(tfull + acc, aphase);
+            ptx::tc_fence_after();
+            const uint32_t xs = ptx::smem_u32(smem + stage * SB + Cfg::kDB * kABytes);
+#pragma unroll 1
+            for (int g = 0; g < Cfg::kXB; ++g) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tq + acc * CI + g * 64 + hh * 32, v);
+                if (leader) {   // this group's old delta / addend into staging buffer sb (its last store read)
+                    bulk_wait_read_n<1>();
+                    ptx::mbar_arrive_expect_tx(ebar + sb, dload ? (uint32_t)kOutStage : 0u);
+                    if (dload) ptx::tma_load_4d(sO + sb * kOutStage, tmL, ebar + sb, g * 64, x0, y0 - lbase, b);
+                }
+                ptx::tmem_ld_wait();
+                ptx::mbar_wait(ebar + sb, (ephase >> sb) & 1);
+                ephase ^= 1u << sb;
+                const uint32_t row = ptx::smem_u32(sO + sb * kOutStage) + m * 128;
+                const uint32_t grow = xs + g * kABytes + m * 128;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int c = hh * 4 + cc;
+                    const uint32_t off = (uint32_t)((c ^ (m & 7)) << 4);
+                    const uint4 dd = dload ? ld_shared_v4(row + off) : make_uint4(0, 0, 0, 0);
+                    const uint4 gg = P.gate ? ld_shared_v4(grow + off) : make_uint4(0, 0, 0, 0);
+                    const uint32_t dw4[4] = {dd.x, dd.y, dd.z, dd.w}, gw4[4] = {gg.x, gg.y, gg.z, gg.w};
+                    uint32_t o[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float f0 = hadd_lo(dw4[h], __uint_as_float(v[cc * 8 + 2 * h]));
+                        const float f1 = hadd_hi(dw4[h], __uint_as_float(v[cc * 8 + 2 * h + 1]));
+                        o[h] = pack2_act<false>(f0, f1);
+                        if (P.gate) o[h] &= relu_mask2(gw4[h]);
+                    }
+                    st_shared_v4(row + off, make_uint4(o[0], o[1], o[2], o[3]));
+                }
+                fence_async_smem();
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (leader) {
+                    tma_store_4d(&tmO, sO + sb * kOutStage, g * 64, x0, y0 - P.dx.base, b);
+                    bulk_commit();
+                }
+                sb ^= 1;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) { ptx::mbar_arrive(empty + stage); ptx::mbar_arrive(tempty + acc); }
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            if (++acc == D1B) { acc = 0; aphase ^= 1; }
+        }
+        if (leader) bulk_wait_all();
+        // the wgrad accumulator of this CTA's tiles: reduced once into the fp32 gradient
+        if (p0 < p1) {
+            ptx::mbar_wait(d2full, 0);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int mt = 0; mt < Cfg::kMT; ++mt) {
+                const int co = mt * 128 + m;
+                const bool live = co < P.c_out && (CO >= 128 || m < 64);
+                const float gsc = live && P.gamma ? __bfloat162float(P.gamma[co]) : 1.f;
+                float gdot = 0.f;
+#pragma unroll 1
+                for (int cc = 0; cc < CI / 64; ++cc) {
+                    const int c = (cc + blockIdx.x) % (CI / 64);   // rotated: CTAs do not queue on the same lines
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tq + Cfg::kD2Col + mt * CI + c * 64 + hh * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (!live) continue;
+                    const int ci0 = c * 64 + hh * 32;
+                    float *dst = P.dw + (long long)co * CI + ci0;
+                    const bf16 *wr = P.w + (long long)co * CI + ci0;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        red_add_v4(dst + j, __uint_as_float(v[j]) * gsc, __uint_as_float(v[j + 1]) * gsc,
+                                   __uint_as_float(v[j + 2]) * gsc, __uint_as_float(v[j + 3]) * gsc);
+                        if (P.dg)
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) gdot += __uint_as_float(v[j + h]) * __bfloat162float(wr[j + h]);
+                    }
+                }
+                if (P.dg && live) atomicAdd(P.dg + co, gdot);
+            }
+        }
+    } else if (bias) {
+        // bias / beta gradient: column sums of the delta tiles (channel pairs, SWIZZLE_128B boxes)
+        const int t = (warp - 10) * 32 + lane;
+        constexpr int NPAIR = CO / 2, NG = 128 / NPAIR > 0 ? 128 / NPAIR : 1;
+        const int cp = t % NPAIR, gi = t / NPAIR;
+        int stage = 0;
+        uint32_t phase = 0;
+        float2 sum = make_float2(0.f, 0.f);
+        for (int pt = p0; pt < p1; ++pt) {
+            ptx::mbar_wait(full + stage, phase);
+            if (gi < NG) {
+                const float2 vv = db_pair_sum(ptx::smem_u32(smem + stage * SB), cp, gi, NG, 0, 1);
+                sum.x += vv.x;
+                sum.y += vv.y;
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(empty + stage);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        const int co = 2 * cp;
+        if (gi < NG && p0 < p1) {
+            if (co < P.c_out) atomicAdd(P.db + co, sum.x);
+            if (co + 1 < P.c_out) atomicAdd(P.db + co + 1, sum.y);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
 // ------------------------------------------------------------------ wgrad, row halo (stride 1)
 // One work item = (co tile of 128, filter row ky, ci tile of BN, pixel split); its k taps
 // kx = 0..k-1 accumulate in k TMEM accumulators (k * BN columns).  Per pixel tile (TW x TH
@@ -3485,6 +3755,59 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     if (ok && P.db) a.db_done = true;
     if (ok && P.dg) a.dg_done = true;
     return ok;
+}
+
+// fused pointwise dgrad + wgrad (k_dwgrad_pw): 1x1 stride-1 convolutions with (Cp_in, Cp_out) =
+// (64, 256) or (256, 64); false = shape not taken (the caller launches wgrad and dgrad separately)
+bool tc_conv_dwgrad(const WgradArgs &wa, const DgradArgs &da, cudaStream_t st) {
+    static const int on = env_int("LRCNN_DWGRAD", 1);
+    if (!on || wa.k != 1 || wa.s != 1 || wa.p != 0 || da.k != 1 || da.s != 1 || da.p != 0 || !da.wt) return false;
+    const int CI = wa.x.Cp, CO = wa.dy.Cp;
+    if (!((CI == 64 && CO == 256) || (CI == 256 && CO == 64))) return false;
+    if (wa.c_out != CO || da.dx.Cp != CI || da.ra != wa.a || da.rb != wa.b) return false;
+    if (da.gate && (da.act.p != wa.x.p || da.act.base != wa.x.base || da.act.Cp != CI)) return false;
+    if (da.add_on && !da.write) return false;
+    if (wa.dg && !wa.w) return false;
+    if (!aligned16(wa.dy.p) || !aligned16(wa.x.p) || !aligned16(da.dx.p) || !aligned16(da.wt)) return false;
+    const int rows = wa.b - wa.a;
+    if (rows <= 0) return false;
+    TcDw P{};
+    P.dx = da.dx; P.act = da.act; P.add = da.add;
+    P.dw = wa.dw; P.db = wa.db; P.dg = wa.dg; P.gamma = (const bf16 *)wa.gamma; P.w = (const bf16 *)wa.w;
+    P.c_out = wa.c_out; P.gate = da.gate; P.write = da.write; P.dg_add = da.add_on ? 1 : 0;
+    pick_tile(rows, wa.dy.W, 1, P.TW, P.TH);
+    P.tiles_x = (wa.dy.W + P.TW - 1) / P.TW;
+    P.tiles_y = (rows + P.TH - 1) / P.TH;
+    P.pix_tiles = wa.B * P.tiles_x * P.tiles_y;
+    int grid = P.pix_tiles < num_sms() ? P.pix_tiles : num_sms();
+    P.per_cta = (P.pix_tiles + grid - 1) / grid;
+    grid = (P.pix_tiles + P.per_cta - 1) / P.per_cta;
+    P.out_a = wa.a; P.dy_base = wa.dy.base; P.x_base = wa.x.base; P.B = wa.B;
+    CUtensorMap D, X, Wm, O, A;
+    if (!encode_view(&D, wa.dy, wa.B, P.TW, P.TH) || !encode_view(&X, wa.x, wa.B, P.TW, P.TH)) return false;
+    if (!encode_w(&Wm, da.wt, CI, 1, CO, CI, 64)) return false;
+    View ov = da.dx;
+    ov.rows = da.rb - da.dx.base;
+    if (!encode_view(&O, ov, wa.B, P.TW, P.TH)) return false;
+    A = O;
+    if (P.dg_add && (da.add.Cp != CI || !aligned16(da.add.p) || da.add.rows <= 0 ||
+                     !encode_view(&A, da.add, wa.B, P.TW, P.TH)))
+        return false;
+    bool ok;
+    if (CI == 64) {
+        using Cfg = DwCfg<64, 256>;
+        if (!smem_attr((const void *)k_dwgrad_pw<64, 256>, Cfg::kSmem)) return false;
+        ok = launch_pdl(k_dwgrad_pw<64, 256>, grid, kDwThreads, Cfg::kSmem, st, D, X, Wm, O, A, P);
+    } else {
+        using Cfg = DwCfg<256, 64>;
+        if (!smem_attr((const void *)k_dwgrad_pw<256, 64>, Cfg::kSmem)) return false;
+        ok = launch_pdl(k_dwgrad_pw<256, 64>, grid, kDwThreads, Cfg::kSmem, st, D, X, Wm, O, A, P);
+    }
+    if (!ok) return false;
+    wa.db_done = wa.db != nullptr;
+    wa.dg_done = wa.dg != nullptr;
+    da.add_done = P.dg_add != 0;
+    return true;
 }
 
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {

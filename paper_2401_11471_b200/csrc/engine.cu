@@ -650,6 +650,47 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
         for (size_t c = 0; c + 1 < cuts.size(); ++c) {
             const int ca = cuts[c], cb = cuts[c + 1];
             const View dyc = sub_rows(dlt_view(R, S, s, r, t), ca, cb, R.E);
+            // fused pointwise dgrad + wgrad (one pass over delta(out) and x, tc_conv_dwgrad) when the
+            // shape has a kernel; else wgrad on the side stream and dgrad on the main stream
+            if (P.use_tc && need_dx && cuts.size() == 2 && o.d.k == 1 && o.d.s == 1 && o.d.p == 0) {
+                WgradArgs A;
+                A.dy = dyc; A.x = act_view(R, S, r, o.in_t); A.dw = g + o.w_off; A.gamma = gamma;
+                A.k = 1; A.s = 1; A.p = 0; A.c_out = o.d.c_out; A.a = ca; A.b = cb; A.B = B;
+                if (o.d.epi == LRCNN_EPI_BIAS) A.db = g + o.b_off;
+                if (o.d.epi == LRCNN_EPI_AFFINE) { A.db = g + o.beta_off; A.dg = g + o.b_off; A.w = prm(R, o.w_off); }
+                DgradArgs D;
+                D.dy = dyc; D.dx = dlt_view(R, S, s, r, o.in_t); D.act = act_view(R, S, r, o.in_t);
+                D.gate = tin.relu; D.w = prm(R, o.w_off); D.wt = R.ws + o.wt_off; D.gamma = gamma;
+                D.k = 1; D.s = 1; D.p = 0; D.c_out = o.d.c_out; D.B = B;
+                D.ra = ca; D.rb = std::min(tin.H, cb);
+                D.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
+                const int fu2 = fused_res(P, S, o.in_t);
+                if (fu2 >= 0) {
+                    const int tu = P.op[fu2].out_t, oa = S.a[r][tu], ob = S.b[r][tu];
+                    if (ob > oa) { D.add = sub_rows(dlt_view(R, S, s, r, tu), oa, ob, R.E); D.add_on = 1; }
+                }
+                bool fused;
+                {
+                    ProfScope ps(R, 0, 2.0 * conv_flops(P, o, cb - ca), i * 8 + 1,
+                                 conv_bytes(P, o, ca, cb, 1, D.write ? 0 : 1, D.gate ? 1 : 0) + conv_bytes(P, o, ca, cb, 2)
+                                     - conv_bytes(P, o, ca, cb, 2, 0, 0, false) + 8.0 * o.d.k * o.d.k * tin.Cp * o.d.c_out,
+                                 conv_bytes(P, o, ca, cb, 1, 0, 0, true) + conv_bytes(P, o, ca, cb, 2, 0, 0, true));
+                    fused = tc_conv_dwgrad(A, D, R.st);
+                    if (!fused && tc_take_error())
+                        return fail(LRCNN_E_CUDA, "fused dgrad + wgrad launch failed at op " + std::to_string(i));
+                }
+                if (fused) {
+                    P.launches += 1;
+                    ++P.tc_launches;
+                    CK(cudaGetLastError());
+                    db_done = db_done && A.db_done;
+                    if (A.dg && !A.dg_done) return fail(LRCNN_E_STATE, "fused dgrad+wgrad did not take dgamma");
+                    ra_all = D.ra; rb_all = D.rb; write_mode = D.write; fu = fu2;
+                    add_done_all = D.add_done; add_any = D.add_done;
+                    D0 = D;
+                    continue;
+                }
+            }
             // wgrad and the bias/affine reduction only read complete data of this band: run them on
             // the side stream so they overlap the dgrad chain (joined at the end of the band)
             cudaStream_t gst = R.st;

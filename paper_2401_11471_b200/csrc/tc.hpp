@@ -10,6 +10,8 @@ bool tc_available();
 bool tc_conv_fwd(const ConvFwdArgs &a, cudaStream_t st);
 bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st);
 bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st);
+// fused 1x1 stride-1 dgrad + wgrad (both results; sets a.db_done / dg_done, d.add_done) or false
+bool tc_conv_dwgrad(const WgradArgs &a, const DgradArgs &d, cudaStream_t st);
 // name of the last tcgen05 kernel this host thread launched (per-kernel profile), or nullptr
 const char *tc_last_kernel();
 void tc_clear_last_kernel();

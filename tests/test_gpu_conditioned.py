@@ -69,6 +69,22 @@ def test_resnet_identity_blocks_vs_oracle(prec):
                flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION | (LB.FLAG_REQUIRE_TC if bf else 0), tag="identity")
 
 
+def test_resnet_stage2_full_width_fused_pointwise_backward():
+    """ResNet-50's conv2_x at full width (64 / 256 channels): the pointwise convolutions' backward
+    runs as the fused dgrad + wgrad kernel (k_dwgrad_pw: 256 -> 64 with the fused residual addend,
+    64 -> 256 with the gate, the 64 -> 256 projection accumulating); bf16 vs the oracle (R17d),
+    COLUMN / 2PS / 1-row bands, some gammas 0."""
+    net = WL.resnet50(H=48, W=40, width_div=1, blocks=(3, 1, 1, 1))
+    B = 2
+    params = _gamma_zero(WL.make_params(net, seed=2, bias_scale=0.1, gamma_spread=0.2, bf16=True))
+    x = WL.make_input(net, B, seed=0, bf16=True)
+    ts, _ = C.forward(net, params, x, store=C.bf16_store)
+    _, dzl, _, _ = C.head_forward_backward(ts[-1], params["head"], WL.make_labels(net, B))
+    dzl = WL.round_bf16(dzl)
+    full_check(net, B, "bf16", [("column", {}), ("2ps", {"n_bands": 3}), ("2ps", {"band_rows": 1})], params, x, dzl,
+               flags=LB.FLAG_REQUIRE_TC, tag="stage2 full width")
+
+
 def test_vgg16_full_depth_bf16_all_modes():
     """All 13 convs and 5 pools of VGG-16 (reduced channels, 64x64) in bf16: whole-stack 2PS,
     per-pool 2PS-H, OverL-H, 1-row bands, COLUMN -- every gradient vs the oracle (R17d)."""

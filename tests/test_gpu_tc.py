@@ -38,7 +38,9 @@ def run(net, B, mode, params, x, dzl, flags=0, **kw):
                                                   (64, 64, 13, 29, 1, 0, "bias"), (64, 192, 12, 40, 3, 0, "bias"),
                                                   (256, 128, 9, 23, 1, 0, "bias"), (512, 256, 6, 17, 1, 0, "bias"),
                                                   (64, 64, 20, 37, 3, 1, "affine"), (64, 64, 13, 29, 1, 0, "affine"),
-                                                  (128, 256, 7, 19, 3, 1, "affine"), (256, 64, 9, 23, 1, 0, "affine")])
+                                                  (128, 256, 7, 19, 3, 1, "affine"), (256, 64, 9, 23, 1, 0, "affine"),
+                                                  (64, 256, 13, 29, 1, 0, "affine"), (64, 256, 17, 40, 1, 0, "bias"),
+                                                  (256, 64, 21, 37, 1, 0, "bias")])
 def test_two_conv_layers_vs_oracle(cin, cout, H, W, k, p, epi):
     """conv(8->cin) then conv(cin->cout) [tcgen05 FP, dgrad into the first layer's delta, wgrad with
     the bias / beta and gamma gradients fused (dgamma = sum_{tap,ci} W * dW_raw)]; bands of 3 rows
