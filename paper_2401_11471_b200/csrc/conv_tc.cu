@@ -2116,6 +2116,15 @@ __global__ void __launch_bounds__(kDwThreads, 1)
         const int lbase = P.write ? P.add.base : P.dx.base;
         int stage = 0, acc = 0, sb = 0;
         uint32_t phase = 0, aphase = 0, ephase = 0;
+        // item = (tile, 64-channel group); the old delta / addend of item j + 1 is TMA-loaded into the
+        // other staging buffer (once item j - 1's store has read it) while item j is combined
+        auto issue = [&](int pt2, int g2, int buf) {
+            int x2, y2, b2;
+            tile_xy(pt2, x2, y2, b2);
+            ptx::mbar_arrive_expect_tx(ebar + buf, dload ? (uint32_t)kOutStage : 0u);
+            if (dload) ptx::tma_load_4d(sO + buf * kOutStage, tmL, ebar + buf, g2 * 64, x2, y2 - lbase, b2);
+        };
+        if (leader && p0 < p1) issue(p0, 0, 0);
         for (int pt = p0; pt < p1; ++pt) {
             int x0, y0, b;
             tile_xy(pt, x0, y0, b);
@@ -2126,10 +2135,12 @@ __global__ void __launch_bounds__(kDwThreads, 1)
             for (int g = 0; g < Cfg::kXB; ++g) {
                 uint32_t v[32];
                 ptx::tmem_ld32(tq + acc * CI + g * 64 + hh * 32, v);
-                if (leader) {   // this group's old delta / addend into staging buffer sb (its last store read)
-                    bulk_wait_read_n<1>();
-                    ptx::mbar_arrive_expect_tx(ebar + sb, dload ? (uint32_t)kOutStage : 0u);
-                    if (dload) ptx::tma_load_4d(sO + sb * kOutStage, tmL, ebar + sb, g * 64, x0, y0 - lbase, b);
+                if (leader) {
+                    const int pn = g + 1 < Cfg::kXB ? pt : pt + 1, gn = g + 1 < Cfg::kXB ? g + 1 : 0;
+                    if (pn < p1) {
+                        bulk_wait_read_n<0>();   // the store of the previous item (buffer sb ^ 1) has read it
+                        issue(pn, gn, sb ^ 1);
+                    }
                 }
                 ptx::tmem_ld_wait();
                 ptx::mbar_wait(ebar + sb, (ephase >> sb) & 1);
