@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--simt", action="store_true", help="disable the tcgen05 kernels (debug)")
     ap.add_argument("--allow-overlap", action="store_true",
                     help="OverL: accept N > H / o^0 at a segment input (LRCNN_FLAG_ALLOW_OVERLAP_EXHAUSTION)")
+    ap.add_argument("--no-fuse-block", action="store_true",
+                    help="run the conv2_x identity bottlenecks unfused (default: one fused kernel per band, "
+                         "LRCNN_FLAG_NO_FUSE_BLOCK off)")
     ap.add_argument("--no-fp-merge", action="store_true",
                     help="forward pass on the BP bands (default: merged FP bands, LRCNN_FLAG_FP_MERGE)")
     ap.add_argument("--no-balanced", action="store_true",
@@ -340,6 +343,8 @@ def main():
     net = make_net(a)
     B = a.batch or CONFIGS[a.config][3]
     flags = (LB.FLAG_NO_TCGEN05 if a.simt else LB.FLAG_REQUIRE_TC) | (0 if a.no_balanced else LB.FLAG_BALANCED_BANDS)
+    if a.no_fuse_block:
+        flags |= LB.FLAG_NO_FUSE_BLOCK
     if not a.no_fp_merge:   # decoupled FP bands (N_FP < N_BP, same peak memory)
         flags |= LB.FLAG_FP_MERGE
     if a.allow_overlap:

@@ -156,6 +156,12 @@ typedef struct {
  * goes back the same way and is added into rank g+1's first band.  No recomputation at the cuts.
  * Needs >= 2 bands per rank (but the last); ignores BALANCED_BANDS / FP_MERGE. */
 #define LRCNN_FLAG_ZERO_REDUNDANCY 256
+/* Disable the fused bottleneck forward (bf16 tensor-core path): an identity ResNet
+ * bottleneck with a 64-channel middle (t[256] -> 1x1 -> 3x3 -> 1x1 + t) runs as ONE kernel per band
+ * that keeps the two 64-channel intermediate maps on chip (shared memory / TMEM) and writes them
+ * only where a later reader needs them (the 2PS cache rows in the FP pass, all rows in the BP
+ * recompute).  Same arithmetic as the unfused kernels.  Set only to compare (tests, bench A/B). */
+#define LRCNN_FLAG_NO_FUSE_BLOCK 512
 
 typedef struct lrcnn_plan_t lrcnn_plan_t;
 

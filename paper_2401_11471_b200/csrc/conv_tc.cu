@@ -3184,6 +3184,23 @@ static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 bool tc_available() { return true; }
 
+bool tc_smem_attr(const void *kern, int bytes) { return smem_attr(kern, bytes); }
+int tc_num_sms() { return num_sms(); }
+bool tc_encode_view(CUtensorMap *m, const View &v, int B, int TW, int TH, int es, int kc) {
+    return encode_view(m, v, B, TW, TH, es, kc);
+}
+bool tc_encode_w(CUtensorMap *m, const void *w, int rows, int taps, int cin_p, int BN, int kc) {
+    return encode_w(m, w, rows, taps, cin_p, BN, kc);
+}
+bool tc_pdl_on() {
+    static const int pdl_env = env_int("LRCNN_PDL", 1);
+    return pdl_env && !g_pdl_off;
+}
+void tc_note_launch(const void *fn, bool ok) {
+    if (ok) note_kernel(fn);
+    else g_tc_error = true;
+}
+
 template <int BN, int KC, int NBUF = 4>
 static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap &Bm, const CUtensorMap &O,
                         const CUtensorMap &G, const CUtensorMap &X, int tiles, cudaStream_t st) {

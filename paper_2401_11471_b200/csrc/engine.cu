@@ -290,6 +290,83 @@ static lrcnn_status op_forward(Run &R, const Segment &S, int r, int i) {
     return capture_rows(R, t, act_view(R, S, r, t), S.a[r][t], S.b[r][t]);
 }
 
+// ------------------------------------------------------------------ fused identity bottleneck (FP)
+// Ops i, i+1, i+2 of segment S form an identity bottleneck with a 64-channel middle (1x1 -> 3x3 ->
+// 1x1 + block input, frozen-BN affine + ReLU each; ResNet-50 conv2_x) whose two intermediate maps
+// nobody else reads: one k_bneck_fwd launch per band (bneck_tc.cu).
+static bool bneck_at(const Plan &P, const Segment &S, int i) {
+    if (!P.use_tc || (P.opts.flags & LRCNN_FLAG_NO_FUSE_BLOCK) || zr_plan(P)) return false;
+    if (i + 2 >= (int)P.op.size()) return false;
+    const OpInfo &c1 = P.op[i], &c2 = P.op[i + 1], &c3 = P.op[i + 2];
+    auto conv = [](const OpInfo &o, int k, int p, int c_out) {
+        return o.d.kind == LRCNN_OP_CONV && o.d.k == k && o.d.s == 1 && o.d.p == p && o.d.c_out == c_out &&
+               o.d.epi == LRCNN_EPI_AFFINE && o.d.relu;
+    };
+    if (!conv(c1, 1, 0, 64) || !conv(c2, 3, 1, 64) || !conv(c3, 1, 0, 256)) return false;
+    const int t = c1.in_t, t1 = c1.out_t, t2 = c2.out_t;
+    if (c1.d.res >= 0 || c2.d.res >= 0 || c3.d.res != t || c2.in_t != t1 || c3.in_t != t2) return false;
+    if (P.t[t].Cp != 256 || P.t[t1].Cp != 64 || P.t[t2].Cp != 64) return false;
+    if (P.t[t1].cons.size() != 1 || P.t[t2].cons.size() != 1) return false;
+    if (t1 == S.out_t || t2 == S.out_t || t1 == S.in_t || t2 == S.in_t) return false;
+    bool in1 = false, in2 = false;
+    for (int o : S.ops) { in1 = in1 || o == i + 1; in2 = in2 || o == i + 2; }
+    return in1 && in2;
+}
+
+static lrcnn_status capture_rows(Run &R, int t, const View &out, int a, int b);
+// One band (S may be the merged FP view, R.fp_merged) of the fused block at op i.  nwin / wlo / whi:
+// t1 rows to store (nwin < 0: all), write_t2: store t2 (BP recompute, capture).
+static lrcnn_status bneck_forward(Run &R, const Segment &S, int r, int i, int nwin, const int *wlo, const int *whi,
+                                  int write_t2) {
+    Plan &P = R.P;
+    const OpInfo &c1 = P.op[i], &c2 = P.op[i + 1], &c3 = P.op[i + 2];
+    const int t = c1.in_t, t1 = c1.out_t, t2 = c2.out_t, u = c3.out_t;
+    const bool cap = !P.capture.empty();
+    if (cap) { nwin = -1; write_t2 = 1; }
+    BneckArgs A;
+    A.t = act_view(R, S, r, t); A.t1 = act_view(R, S, r, t1); A.t2 = act_view(R, S, r, t2); A.u = act_view(R, S, r, u);
+    A.w1 = prm(R, c1.w_off); A.w2 = prm(R, c2.w_off); A.w3 = prm(R, c3.w_off);
+    A.g1 = prm(R, c1.b_off); A.e1 = prm(R, c1.beta_off);
+    A.g2 = prm(R, c2.b_off); A.e2 = prm(R, c2.beta_off);
+    A.g3 = prm(R, c3.b_off); A.e3 = prm(R, c3.beta_off);
+    A.a2 = S.a[r][t2]; A.b2 = S.b[r][t2]; A.a1 = S.a[r][t1]; A.b1 = S.b[r][t1]; A.B = P.net.B;
+    A.write_t2 = write_t2;
+    A.nwin = nwin;
+    for (int k = 0; k < nwin && k < 16; ++k) { A.wlo[k] = wlo[k]; A.whi[k] = whi[k]; }
+    if (S.a[r][u] != A.a2 || S.b[r][u] != A.b2) return fail(LRCNN_E_STATE, "fused bottleneck: t2 / u band rows differ");
+    if (A.b2 > A.a2) {
+        double fl = conv_flops(P, c1, A.b1 - A.a1) + conv_flops(P, c2, A.b2 - A.a2) + conv_flops(P, c3, A.b2 - A.a2);
+        const TensorInfo &T = P.t[t], &T1 = P.t[t1], &T2 = P.t[t2];
+        const double Bn = P.net.B, rbt = (double)T.W * T.Cp * R.E, rb1 = (double)T1.W * T1.Cp * R.E;
+        double w1rows = 0;
+        for (int y = A.a1; y < A.b1; ++y) {
+            bool st = nwin < 0;
+            for (int k = 0; k < nwin && !st; ++k) st = y >= wlo[k] && y < whi[k];
+            w1rows += st;
+        }
+        const double wr = Bn * ((A.b2 - A.a2) * rbt + w1rows * rb1 + (write_t2 ? (A.b2 - A.a2) * (double)T2.W * T2.Cp * R.E : 0));
+        const double rd = Bn * (A.b1 - A.a1) * rbt + (double)(c1.w_cnt + c2.w_cnt + c3.w_cnt) * R.E;
+        ProfScope ps(R, 0, fl, i * 8 + 0, rd + wr, wr);
+        ++P.launches;
+        if (!tc_bneck_fwd(A, R.st)) {
+            if (tc_take_error()) return fail(LRCNN_E_CUDA, "fused bottleneck launch failed at op " + std::to_string(i));
+            return fail(LRCNN_E_STATE, "fused bottleneck declined at op " + std::to_string(i));
+        }
+        ++P.tc_launches;
+        CK(cudaGetLastError());
+    }
+    if (cap) {
+        lrcnn_status st;
+        if ((st = capture_rows(R, t1, A.t1, A.a1, A.b1)) != LRCNN_OK) return st;
+        if ((st = capture_rows(R, t2, A.t2, A.a2, A.b2)) != LRCNN_OK) return st;
+        if ((st = capture_rows(R, u, A.u, A.a2, A.b2)) != LRCNN_OK) return st;
+    }
+    return LRCNN_OK;
+}
+
+// the BP recomputes every band from the FP's checkpoints and caches (else the FP's maps are final)
+static bool bp_recomputes(const Plan &P) { return !(P.seg.size() == 1 && P.seg[0].E.size() == 1); }
+
 // copy rows between two views of the same tensor (B planes, pitched)
 static lrcnn_status copy_rows(Run &R, const TensorInfo &ti, void *dst, size_t dst_pitch_rows, const void *src,
                               size_t src_pitch_rows, int rows) {
@@ -318,8 +395,25 @@ static lrcnn_status band_forward_merged(Run &R, const Segment &S, const Segment 
         }
     }
     R.fp_merged = true;
-    for (int i : S.ops)
+    for (size_t q = 0; q < S.ops.size(); ++q) {
+        const int i = S.ops[q];
+        if (q >= 2 && S.ops[q - 1] == i - 1 && bneck_at(P, S, i - 2) && S.ops[q - 2] == i - 2) continue;
+        if (q >= 1 && bneck_at(P, S, i - 1) && S.ops[q - 1] == i - 1) continue;
+        if (bneck_at(P, S, i) && q + 2 < S.ops.size() && S.ops[q + 1] == i + 1 && S.ops[q + 2] == i + 2) {
+            // t1 rows the BP bands [r0, r1) read from their 2PS cache
+            const TensorInfo &T1 = P.t[P.op[i].out_t];
+            int wlo[16], whi[16], nw = 0;
+            for (int rr = r0; rr < r1 && rr + 1 < N; ++rr)
+                if (T1.cache_rows[rr] > 0) {
+                    if (nw == 16) { nw = -1; break; }
+                    wlo[nw] = T1.cache_lo[rr]; whi[nw] = T1.cache_lo[rr] + T1.cache_rows[rr]; ++nw;
+                }
+            if (!bp_recomputes(P)) nw = -1;
+            if ((st = bneck_forward(R, F, k, i, nw, wlo, whi, !bp_recomputes(P))) != LRCNN_OK) { R.fp_merged = false; return st; }
+            continue;
+        }
         if ((st = op_forward(R, F, k, i)) != LRCNN_OK) { R.fp_merged = false; return st; }
+    }
     R.fp_merged = false;
     for (int r = r0; r < r1 && r + 1 < N; ++r) {
         for (int t : S.tensors) {
@@ -359,8 +453,27 @@ static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cach
             if ((st = copy_rows(R, ti, R.ws + ti.act_off + (size_t)(z.r0 - S.lo[r][z.t]) * rb, ti.cap,
                                 R.ws + ti.zr_in_off, z.r1 - z.r0, z.r1 - z.r0)) != LRCNN_OK) return st;
         }
-    for (int i : S.ops) {
+    for (size_t q = 0; q < S.ops.size(); ++q) {
+        const int i = S.ops[q];
         if (skip_out && i + 1 == S.out_t) continue;
+        // ops i+1, i+2 of a fused block ran with op i (unless the block output is skipped: BP recompute
+        // of the segment output, whose delta is known -- then ops i, i+1 run unfused)
+        const bool f2 = q >= 2 && S.ops[q - 1] == i - 1 && S.ops[q - 2] == i - 2 && bneck_at(P, S, i - 2) &&
+                        !(skip_out && i + 1 == S.out_t);
+        const bool f1 = q >= 1 && q + 1 < S.ops.size() && S.ops[q - 1] == i - 1 && S.ops[q + 1] == i + 1 &&
+                        bneck_at(P, S, i - 1) && !(skip_out && i + 2 == S.out_t);
+        if (f1 || f2) continue;
+        if (q + 2 < S.ops.size() && S.ops[q + 1] == i + 1 && S.ops[q + 2] == i + 2 && bneck_at(P, S, i) &&
+            !(skip_out && i + 3 == S.out_t)) {
+            const TensorInfo &T1 = P.t[P.op[i].out_t];
+            int wlo[1], whi[1], nw = 0;
+            if (save_cache && P.opts.mode == LRCNN_2PS && r + 1 < (int)S.E.size() && T1.cache_rows[r] > 0) {
+                wlo[0] = T1.cache_lo[r]; whi[0] = T1.cache_lo[r] + T1.cache_rows[r]; nw = 1;
+            }
+            const bool all = !save_cache || !bp_recomputes(P);   // BP recompute, or the FP's maps are final
+            if ((st = bneck_forward(R, S, r, i, all ? -1 : nw, wlo, whi, all)) != LRCNN_OK) return st;
+            continue;
+        }
         if ((st = op_forward(R, S, r, i)) != LRCNN_OK) return st;
     }
     if (save_cache && P.opts.mode == LRCNN_2PS && r + 1 < (int)S.E.size()) {

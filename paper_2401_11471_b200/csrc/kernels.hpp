@@ -72,6 +72,20 @@ struct PoolArgs {
     int acc = 1;               // bwd: 1 = dx += ..., 0 = dx rows [ra, rb) are written, not read (single writer)
 };
 
+// Fused identity bottleneck forward (bneck_tc.cu): t -> 1x1 (64) -> 3x3 (64) -> 1x1 (256) + t, frozen-BN
+// affine + ReLU after each conv, over the band's output rows [a2, b2) of t2 / u.  t1 rows [a1, b1) are
+// computed on chip, rows below a1 are read from the t1 view (2PS cache); t1 rows are stored in the
+// windows [wlo, whi) (nwin < 0: all of [a1, b1)), t2 rows [a2, b2) when write_t2.
+struct BneckArgs {
+    View t, t1, t2, u;
+    const void *w1 = nullptr, *w2 = nullptr, *w3 = nullptr;
+    const void *g1 = nullptr, *e1 = nullptr, *g2 = nullptr, *e2 = nullptr, *g3 = nullptr, *e3 = nullptr;
+    int a2 = 0, b2 = 0, a1 = 0, b1 = 0, B = 0;
+    int write_t2 = 0;
+    int nwin = -1;
+    int wlo[16] = {}, whi[16] = {};
+};
+
 struct EltArgs {
     View x0, x1, out;          // add fwd: out = relu?(x0 + x1) on rows [a, b)
     View dy, dx, act;          // res/add bwd: dx = gate(act) * (dx + dy) on rows [a, b)

@@ -27,6 +27,7 @@ FLAG_DP = 32
 FLAG_REQUIRE_TC = 64
 FLAG_AUTO_SEGMENTS = 128
 FLAG_ZERO_REDUNDANCY = 256
+FLAG_NO_FUSE_BLOCK = 512
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INFEASIBLE", 4: "E_DEGENERATE", 5: "E_STATE",
           6: "E_WORKSPACE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_UNSUPPORTED"}
 
