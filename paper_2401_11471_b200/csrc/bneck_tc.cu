@@ -60,7 +60,7 @@ struct TcBneck {
     int wlo[16], whi[16];
 };
 
-constexpr int kThreadsB = 352;   // producer, conv1 MMA, conv2/conv3 MMA, 4 + 4 epilogue warps
+constexpr int kThreadsB = 480;   // producer, conv1 MMA, conv2/conv3 MMA, 4 epilogue-A warps, 8 epilogue-B warps
 constexpr int kW2 = 9 * 8192;          // 9 taps x (64 rows x 64 ch), SWIZZLE_128B (resident)
 constexpr int kW3 = 256 * 128;         // 256 rows x 64 ch, SWIZZLE_128B (resident)
 constexpr int kTBox = 180 * 64;        // TMA bytes per 32-channel t chunk of the 10 x 18 box
@@ -71,7 +71,7 @@ constexpr int kTStage = 16384;         // 184 pixel rows x 64 B, then the W1 chu
 constexpr int kW1off = 12288;
 constexpr int kTStages = 3;
 constexpr int kT2 = 128 * 128;
-constexpr int kRB = 4;                 // epilogue B: per-warp residual / output ring of 32 px x 32 ch (2 KB, SWIZZLE_64B)
+constexpr int kRB = 4;                 // epilogue B: per-quarter residual / output ring of 32 px x 32 ch (2 KB, SWIZZLE_64B)
 constexpr int kStgB = 4 * kRB * 2048;
 constexpr int kPrm = 768 * 4;          // gamma / beta of the three convs (64 + 64 + 256 channels), fp32
 constexpr int oW2 = 0, oW3 = oW2 + kW2, oT = oW3 + kW3, oT2 = oT + kTStages * kTStage, oStg = oT2 + kT2,
@@ -174,12 +174,17 @@ __device__ __forceinline__ void decode(const TcBneck &P, int tile, int &tx, int 
     b = r / P.tiles_y;
 }
 
-__device__ __forceinline__ bool t1_store_row(const TcBneck &P, int y) {
-    if (y < P.a1 || y >= P.b1) return false;
-    if (P.nwin < 0) return true;
-    for (int i = 0; i < P.nwin; ++i)
-        if (y >= P.wlo[i] && y < P.whi[i]) return true;
-    return false;
+// bit r: t1 row y0 + r (r < n <= 17) is stored -- in [a1, b1) and in a window (nwin < 0: every row)
+__device__ __forceinline__ uint32_t t1_row_mask(const TcBneck &P, int y0, int n) {
+    auto span = [&](int lo, int hi) -> uint32_t {
+        lo = max(max(lo, P.a1), y0);
+        hi = min(min(hi, P.b1), y0 + n);
+        return hi > lo ? (((1u << (hi - lo)) - 1u) << (lo - y0)) : 0u;
+    };
+    if (P.nwin < 0) return span(P.a1, P.b1);
+    uint32_t m = 0;
+    for (int i = 0; i < P.nwin; ++i) m |= span(P.wlo[i], P.whi[i]);
+    return m;
 }
 
 }  // namespace
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(a1full + i, 1); ptx::mbar_init(a1empty + i, 4); }
         ptx::mbar_init(t1full, 4); ptx::mbar_init(t1empty, 1); ptx::mbar_init(a2full, 1);
         ptx::mbar_init(t2full, 4); ptx::mbar_init(t2empty, 1);
-        ptx::mbar_init(a3full, 1); ptx::mbar_init(a3empty, 4);
+        ptx::mbar_init(a3full, 1); ptx::mbar_init(a3empty, 8);
         for (int i = 0; i < 4 * kRB; ++i) ptx::mbar_init(rbar + i, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmT);
@@ -365,8 +370,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             // y0 .. y0+15 (+ y0+16 on the last tile row), coalesced: 16-byte items (row, pixel, chunk)
             {
                 const int nrows = last_row ? 17 : 16;
-                uint32_t rmask = 0;   // rows of this tile to store
-                for (int rr = 0; rr < nrows; ++rr) rmask |= (uint32_t)t1_store_row(P, y0 + rr) << rr;
+                const uint32_t rmask = t1_row_mask(P, y0, nrows);   // rows of this tile to store
 #pragma unroll 1
                 for (int it = ta; rmask && it < nrows * 64; it += 128) {
                     const int rr = it >> 6, px = (it >> 3) & 7, c = it & 7;
@@ -414,25 +418,32 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         }
     } else {
         // ---------------------------------------------------------------- epilogue B: u = relu(affine(conv3) + t)
-        // Four independent per-warp pipelines (no block barrier): warp q owns the tile's pixels 32q..32q+31
-        // (TMEM lane quarter q = tile rows 4q..4q+3) and moves them in 32-channel groups (8 per tile)
-        // through a private ring of kRB 2 KB buffers: the residual box (t at those pixels, 32 ch x 8 x 4,
-        // SWIZZLE_64B) is TMA-loaded kRB-1 groups ahead, each lane combines its pixel's row in place,
-        // lane 0 TMA-stores the group.  The next group's accumulator columns are loaded from TMEM while
+        // Eight warps, two per TMEM lane quarter q (the tile's pixels 32q..32q+31 = tile rows 4q..4q+3);
+        // warp half hf combines channels 16hf..16hf+15 of every 32-channel group.  Each quarter runs its
+        // own pipeline (no block barrier): the residual box (t at those pixels, 32 ch x 8 x 4, SWIZZLE_64B)
+        // is TMA-loaded kRB-1 groups ahead into the quarter's ring of kRB 2 KB buffers, both warps combine
+        // their halves of each pixel row in place, a 64-thread named barrier, lane 0 of half 0 TMA-stores
+        // the group and refills the ring.  The next group's accumulator columns are loaded from TMEM while
         // this group is combined.
-        const int q = warp & 3, m = q * 32 + lane;
-        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+        const int q = warp & 3, hf = (warp - 7) >> 2;
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + 256 + hf * 16;
         uint64_t *wb = rbar + q * kRB;
         uint8_t *ring = smem + oStg + q * kRB * 2048;
-        int lt = blockIdx.x, lg = 0;   // lane 0: next residual group to load
-        auto res_load = [&](int buf) {
+        const bool leader = hf == 0 && lane == 0;
+        int lt = blockIdx.x, lg = 0;   // leader: next residual group to load (tile lt, group lg)
+        int lx = 0, ly = 0, lb = 0;    // box coordinates of tile lt
+        auto set_lt = [&]() {
             int tx2, ty2, b2;
             decode(P, lt, tx2, ty2, b2);
-            ptx::mbar_arrive_expect_tx(wb + buf, 2048);
-            ptx::tma_load_4d(ring + buf * 2048, &tmR, wb + buf, lg * 32, tx2 * 8, P.a2 + ty2 * 16 + 4 * q - P.t.base, b2);
-            if (++lg == 8) { lg = 0; lt += gridDim.x; }
+            lx = tx2 * 8; ly = P.a2 + ty2 * 16 + 4 * q - P.t.base; lb = b2;
         };
-        if (lane == 0)
+        set_lt();
+        auto res_load = [&](int buf) {
+            ptx::mbar_arrive_expect_tx(wb + buf, 2048);
+            ptx::tma_load_4d(ring + buf * 2048, &tmR, wb + buf, lg * 32, lx, ly, lb);
+            if (++lg == 8) { lg = 0; lt += gridDim.x; if (lt < P.num_tiles) set_lt(); }
+        };
+        if (leader)
             for (int i = 0; i < kRB - 1 && lt < P.num_tiles; ++i) res_load(i);
         int sb = 0;
         uint32_t rph = 0;   // bit i: parity of wb[i]'s next completion
@@ -443,12 +454,12 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             const int y0 = P.a2 + ty * 16 + 4 * q, x0 = tx * 8;
             mbar_wait_sleep(a3full, j & 1);
             ptx::tc_fence_after();
-            uint32_t v[2][32];
-            ptx::tmem_ld32(tq + 256, v[0]);
+            uint32_t v[2][16];
+            ptx::tmem_ld16(tq, v[0]);
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
                 ptx::tmem_ld_wait();
-                if (g < 7) ptx::tmem_ld32(tq + 256 + (g + 1) * 32, v[(g + 1) & 1]);
+                if (g < 7) ptx::tmem_ld16(tq + (g + 1) * 32, v[(g + 1) & 1]);
                 if (g == 7) {
                     ptx::tc_fence_before();
                     __syncwarp();
@@ -458,26 +469,26 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 ptx::mbar_wait(wb + sb, (rph >> sb) & 1);
                 rph ^= 1u << sb;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    const int c = 2 * hf + c2;
                     const uint32_t a = row + ((c ^ ((lane >> 1) & 3)) << 4);
-                    st_shared_v4(a, affine_res_relu8(v[g & 1] + 8 * c, sprm + 1024 + 128 * g + 32 * c, sprm + 2048 + 128 * g + 32 * c, ld_shared_v4(a)));
+                    st_shared_v4(a, affine_res_relu8(v[g & 1] + 8 * c2, sprm + 1024 + 128 * g + 32 * c,
+                                                     sprm + 2048 + 128 * g + 32 * c, ld_shared_v4(a)));
                 }
                 fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
+                named_bar_sync(2 + q, 64);
+                if (leader) {
                     tma_store_4d(&tmU, ring + sb * 2048, g * 32, x0, y0 - P.u.base, b);
                     bulk_commit();
-                    if (lt < P.num_tiles) {   // the buffer stored kRB-1 groups ago... once its store has read it
+                    if (lt < P.num_tiles) {   // the buffer stored kRB-1 groups ago, once its store has read it
                         bulk_wait_read_n<kRB - 2>();
                         res_load(sb == 0 ? kRB - 1 : sb - 1);
                     }
                 }
-                __syncwarp();
                 sb = sb + 1 == kRB ? 0 : sb + 1;
             }
         }
-        (void)m;
-        if (lane == 0) bulk_wait_all();
+        if (leader) bulk_wait_all();
     }
     ptx::tc_fence_before();
     __syncthreads();
