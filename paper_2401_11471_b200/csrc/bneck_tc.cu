@@ -60,7 +60,8 @@ struct TcBneck {
     int wlo[16], whi[16];
 };
 
-constexpr int kThreadsB = 480;   // producer, conv1 MMA, conv2/conv3 MMA, 4 epilogue-A warps, 8 epilogue-B warps
+
+constexpr int kThreadsB = 512;   // producer, conv1 MMA, conv2/conv3 MMA, 4 epilogue-A warps, 8 epilogue-B warps, E3 DMA warp
 constexpr int kW2 = 9 * 8192;          // 9 taps x (64 rows x 64 ch), SWIZZLE_128B (resident)
 constexpr int kW3 = 256 * 128;         // 256 rows x 64 ch, SWIZZLE_128B (resident)
 constexpr int kTBox = 180 * 64;        // TMA bytes per 32-channel t chunk of the 10 x 18 box
@@ -102,8 +103,6 @@ __device__ __forceinline__ void bulk_wait_read_n() { asm volatile("cp.async.bulk
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 __device__ __forceinline__ float hadd_lo(uint32_t w, float x) {
     float r;
     asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(r) : "h"((unsigned short)(w & 0xffffu)), "f"(x));
@@ -200,8 +199,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     uint64_t *a1full = tempty + kTStages, *a1empty = a1full + 2;   // [2]: double-buffered conv1 accumulators
     uint64_t *t1full = a1full + 4, *t1empty = a1full + 5, *a2full = a1full + 6, *t2full = a1full + 7;
     uint64_t *t2empty = a1full + 8, *a3full = a1full + 9, *a3empty = a1full + 10;
-    uint64_t *rbar = a1full + 11;                                   // [4 warps][kRB] residual tiles landed
-    uint32_t *tslot = (uint32_t *)(rbar + 4 * kRB);
+    uint64_t *rbar = a1full + 11;                                   // [4 quarters][kRB] residual tiles landed
+    uint64_t *rdone = rbar + 4 * kRB;                               // [4 quarters][kRB] output rows combined
+    uint32_t *tslot = (uint32_t *)(rdone + 4 * kRB);
     // fp32 per-channel parameters: g1 @0, e1 @64, g2 @128, e2 @192, g3 @256, e3 @512 (floats)
     float *prm = reinterpret_cast<float *>(smem + oPrm);
     const uint32_t sprm = ptx::smem_u32(prm);
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         ptx::mbar_init(t1full, 4); ptx::mbar_init(t1empty, 1); ptx::mbar_init(a2full, 1);
         ptx::mbar_init(t2full, 4); ptx::mbar_init(t2empty, 1);
         ptx::mbar_init(a3full, 1); ptx::mbar_init(a3empty, 8);
-        for (int i = 0; i < 4 * kRB; ++i) ptx::mbar_init(rbar + i, 1);
+        for (int i = 0; i < 4 * kRB; ++i) { ptx::mbar_init(rbar + i, 1); ptx::mbar_init(rdone + i, 2); }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmT);
         ptx::prefetch_tmap(&tmW1);
@@ -270,17 +270,20 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             for (int c = 0; c < 8; ++c) {
                 ptx::mbar_wait(tfull + s, ph);
                 ptx::tc_fence_after();
-                const uint32_t a0 = (uint32_t)dT + s * (kTStage >> 4), b0 = a0 + (kW1off >> 4);
+                if (ptx::elect_one()) {
+                    const uint32_t a0 = (uint32_t)dT + s * (kTStage >> 4), b0 = a0 + (kW1off >> 4);
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+                    for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk)
-                        ptx::umma_bf16_lh(acc + h * 64, a0 + h * (kH1 * 64 >> 4) + 2 * kk, hT, b0 + 2 * kk, hT, id64,
-                                          (c | kk) != 0);
-                ptx::umma_commit(tempty + s);
+                        for (int kk = 0; kk < 2; ++kk)
+                            ptx::umma_bf16_1t(acc + h * 64, a0 + h * (kH1 * 64 >> 4) + 2 * kk, hT, b0 + 2 * kk, hT, id64,
+                                              (c | kk) != 0);
+                    ptx::umma_commit_1t(tempty + s);
+                    if (c == 7) ptx::umma_commit_1t(a1full + (j & 1));
+                }
+                __syncwarp();
                 if (++s == kTStages) { s = 0; ph ^= 1; }
             }
-            ptx::umma_commit(a1full + (j & 1));
         }
     } else if (warp == 2) {
         // conv2 (into the drained conv1 buffer j & 1, its columns 0..63) and conv3 (columns 256..511)
@@ -298,24 +301,30 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             mbar_wait_sleep(t1full, j & 1);   // epi1 wrote the t1 box and drained conv1 buffer j & 1
             ptx::tc_fence_after();
             const uint32_t acc2 = tmem + (j & 1) * 128;
+            if (ptx::elect_one()) {
 #pragma unroll 1
-            for (int tap = 0; tap < 9; ++tap) {
-                const int ky = tap / 3, kx = tap - 3 * ky;
-                const uint32_t a0 = (uint32_t)dT1 + (uint32_t)(ky * 10 + kx) * 8, b0 = (uint32_t)dW2 + tap * (8192 >> 4);
+                for (int tap = 0; tap < 9; ++tap) {
+                    const int ky = tap / 3, kx = tap - 3 * ky;
+                    const uint32_t a0 = (uint32_t)dT1 + (uint32_t)(ky * 10 + kx) * 8, b0 = (uint32_t)dW2 + tap * (8192 >> 4);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    ptx::umma_bf16_lh(acc2, a0 + 2 * kk, hT1, b0 + 2 * kk, hW2, id64, (tap | kk) != 0);
+                    for (int kk = 0; kk < 4; ++kk)
+                        ptx::umma_bf16_1t(acc2, a0 + 2 * kk, hT1, b0 + 2 * kk, hW2, id64, (tap | kk) != 0);
+                }
+                ptx::umma_commit_1t(t1empty);
+                ptx::umma_commit_1t(a2full);
             }
-            ptx::umma_commit(t1empty);
-            ptx::umma_commit(a2full);
+            __syncwarp();
             mbar_wait_sleep(t2full, j & 1);
             mbar_wait_sleep(a3empty, (j & 1) ^ 1);
             ptx::tc_fence_after();
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-                ptx::umma_bf16_lh(tmem + 256, (uint32_t)dT2 + 2 * kk, hT2, (uint32_t)dW3 + 2 * kk, hW3, id256, kk != 0);
-            ptx::umma_commit(t2empty);
-            ptx::umma_commit(a3full);
+                for (int kk = 0; kk < 4; ++kk)
+                    ptx::umma_bf16_1t(tmem + 256, (uint32_t)dT2 + 2 * kk, hT2, (uint32_t)dW3 + 2 * kk, hW3, id256, kk != 0);
+                ptx::umma_commit_1t(t2empty);
+                ptx::umma_commit_1t(a3full);
+            }
+            __syncwarp();
         }
     } else if (warp < 7) {
         // ---------------------------------------------------------------- epilogue A: t1 box, t2 tile
@@ -416,42 +425,22 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 }
             }
         }
-    } else {
+    } else if (warp < 15) {
         // ---------------------------------------------------------------- epilogue B: u = relu(affine(conv3) + t)
         // Eight warps, two per TMEM lane quarter q (the tile's pixels 32q..32q+31 = tile rows 4q..4q+3);
-        // warp half hf combines channels 16hf..16hf+15 of every 32-channel group.  Each quarter runs its
-        // own pipeline (no block barrier): the residual box (t at those pixels, 32 ch x 8 x 4, SWIZZLE_64B)
-        // is TMA-loaded kRB-1 groups ahead into the quarter's ring of kRB 2 KB buffers, both warps combine
-        // their halves of each pixel row in place, a 64-thread named barrier, lane 0 of half 0 TMA-stores
-        // the group and refills the ring.  The next group's accumulator columns are loaded from TMEM while
-        // this group is combined.
+        // warp half hf combines channels 16hf..16hf+15 of every 32-channel group in place in the quarter's
+        // ring buffer (the residual box: t at those pixels, 32 ch x 8 x 4, SWIZZLE_64B) and signals rdone;
+        // the DMA warp (15) TMA-stores the group and refills the buffer kRB groups ahead, so the combining
+        // warps never wait on a store.  The next group's accumulator columns are loaded from TMEM while this
+        // group is combined.
         const int q = warp & 3, hf = (warp - 7) >> 2;
         const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + 256 + hf * 16;
-        uint64_t *wb = rbar + q * kRB;
+        uint64_t *wb = rbar + q * kRB, *wd = rdone + q * kRB;
         uint8_t *ring = smem + oStg + q * kRB * 2048;
-        const bool leader = hf == 0 && lane == 0;
-        int lt = blockIdx.x, lg = 0;   // leader: next residual group to load (tile lt, group lg)
-        int lx = 0, ly = 0, lb = 0;    // box coordinates of tile lt
-        auto set_lt = [&]() {
-            int tx2, ty2, b2;
-            decode(P, lt, tx2, ty2, b2);
-            lx = tx2 * 8; ly = P.a2 + ty2 * 16 + 4 * q - P.t.base; lb = b2;
-        };
-        set_lt();
-        auto res_load = [&](int buf) {
-            ptx::mbar_arrive_expect_tx(wb + buf, 2048);
-            ptx::tma_load_4d(ring + buf * 2048, &tmR, wb + buf, lg * 32, lx, ly, lb);
-            if (++lg == 8) { lg = 0; lt += gridDim.x; if (lt < P.num_tiles) set_lt(); }
-        };
-        if (leader)
-            for (int i = 0; i < kRB - 1 && lt < P.num_tiles; ++i) res_load(i);
         int sb = 0;
         uint32_t rph = 0;   // bit i: parity of wb[i]'s next completion
         int j = 0;
         for (int tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x, ++j) {
-            int tx, ty, b;
-            decode(P, tile, tx, ty, b);
-            const int y0 = P.a2 + ty * 16 + 4 * q, x0 = tx * 8;
             mbar_wait_sleep(a3full, j & 1);
             ptx::tc_fence_after();
             uint32_t v[2][16];
@@ -476,19 +465,53 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                                                      sprm + 2048 + 128 * g + 32 * c, ld_shared_v4(a)));
                 }
                 fence_proxy_async();
-                named_bar_sync(2 + q, 64);
-                if (leader) {
-                    tma_store_4d(&tmU, ring + sb * 2048, g * 32, x0, y0 - P.u.base, b);
-                    bulk_commit();
-                    if (lt < P.num_tiles) {   // the buffer stored kRB-1 groups ago, once its store has read it
-                        bulk_wait_read_n<kRB - 2>();
-                        res_load(sb == 0 ? kRB - 1 : sb - 1);
-                    }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(wd + sb);
+                sb = sb + 1 == kRB ? 0 : sb + 1;
+            }
+        }
+    } else if (lane == 0) {
+        // ---------------------------------------------------------------- E3 DMA (warp 15): residual loads, u stores
+        // group sequence k = (tile, g): buffer k % kRB of every quarter; the residual of group k + kRB - 1 goes
+        // into buffer (k - 1) % kRB once group k - 1's stores have read it
+        auto coords = [&](int tile, int qq, int &x, int &yt, int &yu, int &bb) {
+            int tx, ty;
+            decode(P, tile, tx, ty, bb);
+            x = tx * 8;
+            yt = P.a2 + ty * 16 + 4 * qq - P.t.base;
+            yu = P.a2 + ty * 16 + 4 * qq - P.u.base;
+        };
+        int lt = blockIdx.x, lg = 0;   // next residual group to load
+        auto load_next = [&](int buf) {
+            for (int qq = 0; qq < 4; ++qq) {
+                int x, yt, yu, bb;
+                coords(lt, qq, x, yt, yu, bb);
+                ptx::mbar_arrive_expect_tx(rbar + qq * kRB + buf, 2048);
+                ptx::tma_load_4d(smem + oStg + (qq * kRB + buf) * 2048, &tmR, rbar + qq * kRB + buf, lg * 32, x, yt, bb);
+            }
+            if (++lg == 8) { lg = 0; lt += gridDim.x; }
+        };
+        for (int i = 0; i < kRB - 1 && lt < P.num_tiles; ++i) load_next(i);
+        int sb = 0;
+        uint32_t dph = 0;
+        for (int tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+            for (int g = 0; g < 8; ++g) {
+                for (int qq = 0; qq < 4; ++qq) {
+                    int x, yt, yu, bb;
+                    coords(tile, qq, x, yt, yu, bb);
+                    ptx::mbar_wait(rdone + qq * kRB + sb, (dph >> sb) & 1);
+                    tma_store_4d(&tmU, smem + oStg + (qq * kRB + sb) * 2048, g * 32, x, yu, bb);
+                }
+                dph ^= 1u << sb;
+                bulk_commit();
+                if (lt < P.num_tiles) {   // group k-1's stores have read buffer (k-1) % kRB
+                    bulk_wait_read_n<1>();
+                    load_next(sb == 0 ? kRB - 1 : sb - 1);
                 }
                 sb = sb + 1 == kRB ? 0 : sb + 1;
             }
         }
-        if (leader) bulk_wait_all();
+        bulk_wait_all();
     }
     ptx::tc_fence_before();
     __syncthreads();

@@ -60,7 +60,7 @@ struct TcConv {
     int tma_dg;            // dgrad: TMA-load delta (+ activation), combine in smem, TMA-store
     int tma_res;           // FP: the residual tile is TMA-loaded into the staging buffer
     int tap_oy[49], tap_ox[49], tap_w[49];
-    int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores, bit1 skip MMAs (microbenchmarks)
+    int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores (microbenchmarks)
     int tw_log2;           // TW = 1 << tw_log2
     int th_log2;           // TH = 1 << th_log2
     int NBt;               // images per tile (small maps: a 128-pixel tile spans NBt images; 0/1 = one)
@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     const uint32_t b0 = (uint32_t)dB + stage * (BBYTES >> 4);
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk)
-                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                        ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
                     ptx::umma_commit(empty + stage);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -1121,7 +1121,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
                     const uint32_t b0 = (uint32_t)dB + stage * (BBYTES >> 4);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        if (!(P.dbg & 2)) ptx::umma2_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                        ptx::umma2_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
                     ptx::umma2_commit_mc(empty + stage, 3);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -1288,7 +1288,7 @@ __global__ void __launch_bounds__(kI2pThreads, 1)
                     const uint32_t b0 = (uint32_t)dB + (nt * KS + ks) * (BN * 128 >> 4);
                     const int nk = min(8, P.ntaps - ks * 8);   // real taps in this stage
                     for (int kk = 0; kk < (nk + 1) / 2; ++kk)
-                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                        ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
                     ptx::umma_commit(empty + stage);
                     if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
                 }
@@ -1409,19 +1409,23 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 ptx::mbar_wait(full + st, ph);
                 ptx::tc_fence_after();
                 // descriptors advance incrementally: first K-half of pair (ky, j) is tap kx = 2j ->
-                // plane-A pixel i + (s == 1 ? 2j : j) of patch row ky; weights chunk pair (ky, j)
-                uint32_t aky = (uint32_t)dA + st * (kPrPatch >> 4), bt = (uint32_t)dB;
-                uint32_t acc_flag = 0;
-                for (int ky = 0; ky < KY; ++ky, aky += row16) {
-                    uint32_t at = aky;
-                    for (int j = 0; j < NPR; ++j, at += jstep, bt += 2048 >> 4) {
-                        if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, at, hiA, bt, hiB, idesc, acc_flag);
-                        acc_flag = 1;
+                // plane-A pixel i + (s == 1 ? 2j : j) of patch row ky; weights chunk pair (ky, j).
+                // One elected lane issues the tile's k * ceil(k/2) MMAs (N = 64: 32 tensor cycles each).
+                if (ptx::elect_one()) {
+                    uint32_t aky = (uint32_t)dA + st * (kPrPatch >> 4), bt = (uint32_t)dB;
+                    uint32_t acc_flag = 0;
+                    for (int ky = 0; ky < KY; ++ky, aky += row16) {
+                        uint32_t at = aky;
+                        for (int j = 0; j < NPR; ++j, at += jstep, bt += 2048 >> 4) {
+                            ptx::umma_bf16_1t(d, at, hiA, bt, hiB, idesc, acc_flag);
+                            acc_flag = 1;
+                        }
                     }
+                    ptx::umma_commit_1t(empty + st);
+                    ptx::umma_commit_1t(tfull + acc);
                 }
-                ptx::umma_commit(empty + st);
+                __syncwarp();
                 if (++st == kPrStages) { st = 0; ph ^= 1; }
-                ptx::umma_commit(tfull + acc);
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
@@ -1550,7 +1554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t b0 = (uint32_t)dB + sb * (Cfg::kBBytes >> 4);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            if (!(P.dbg & 2)) ptx::umma_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
+                            ptx::umma_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
                             first = 0;
                         }
                         ptx::umma_commit(emptyB + sb);
@@ -1693,7 +1697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
                         const uint32_t b0 = (uint32_t)dB + sb * (BB >> 4);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            if (!(P.dbg & 2)) ptx::umma2_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
+                            ptx::umma2_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
                             first = 0;
                         }
                         ptx::umma2_commit_mc(emptyB + sb, 3);
