@@ -985,13 +985,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t a0 = (uint32_t)dA + stage * (ABYTES >> 4);
                     const uint32_t b0 = (uint32_t)dB + stage * (BBYTES >> 4);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < KC / 16; ++kk)
-                        ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
-                    ptx::umma_commit(empty + stage);
+                        for (int kk = 0; kk < KC / 16; ++kk)
+                            ptx::umma_bf16_1t(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                        ptx::umma_commit_1t(empty + stage);
+                        if (ks + 1 == P.k_steps) ptx::umma_commit_1t(tfull + acc);
+                    }
+                    __syncwarp();
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
-                ptx::umma_commit(tfull + acc);
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
@@ -1119,13 +1122,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t a0 = (uint32_t)dA + stage * (ABYTES >> 4);
                     const uint32_t b0 = (uint32_t)dB + stage * (BBYTES >> 4);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        ptx::umma2_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
-                    ptx::umma2_commit_mc(empty + stage, 3);
+                        for (int kk = 0; kk < 4; ++kk)
+                            ptx::umma2_bf16_1t(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                        ptx::umma2_commit_mc_1t(empty + stage, 3);
+                        if (ks + 1 == P.k_steps) ptx::umma2_commit_mc_1t(tfull + acc, 3);
+                    }
+                    __syncwarp();
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
-                ptx::umma2_commit_mc(tfull + acc, 3);
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
@@ -1287,12 +1293,16 @@ __global__ void __launch_bounds__(kI2pThreads, 1)
                     const uint32_t a0 = (uint32_t)dA + stage * (kI2cStage >> 4);
                     const uint32_t b0 = (uint32_t)dB + (nt * KS + ks) * (BN * 128 >> 4);
                     const int nk = min(8, P.ntaps - ks * 8);   // real taps in this stage
-                    for (int kk = 0; kk < (nk + 1) / 2; ++kk)
-                        ptx::umma_bf16_lh(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
-                    ptx::umma_commit(empty + stage);
+                    if (ptx::elect_one()) {
+                        for (int kk = 0; kk < (nk + 1) / 2; ++kk)
+                            ptx::umma_bf16_1t(d, a0 + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (ks | kk) != 0);
+                        ptx::umma_commit_1t(empty + stage);
+                    }
+                    __syncwarp();
                     if (++stage == kI2cStages) { stage = 0; phase ^= 1; }
                 }
-                ptx::umma_commit(tfull + acc);
+                if (ptx::elect_one()) ptx::umma_commit_1t(tfull + acc);
+                __syncwarp();
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
@@ -1552,12 +1562,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tc_fence_after();
                         const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
                         const uint32_t b0 = (uint32_t)dB + sb * (Cfg::kBBytes >> 4);
+                        if (ptx::elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            ptx::umma_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
-                            first = 0;
+                            for (int kk = 0; kk < 4; ++kk)
+                                ptx::umma_bf16_1t(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (first && kk == 0) ? 0u : 1u);
+                            ptx::umma_commit_1t(emptyB + sb);
                         }
-                        ptx::umma_commit(emptyB + sb);
+                        __syncwarp();
+                        first = 0;
                         if (++sb == SB) { sb = 0; pb ^= 1; }
                     }
                     ptx::umma_commit(emptyA + sa);
@@ -1695,12 +1707,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
                         ptx::tc_fence_after();
                         const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
                         const uint32_t b0 = (uint32_t)dB + sb * (BB >> 4);
+                        if (ptx::elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            ptx::umma2_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, first ? 0u : 1u);
-                            first = 0;
+                            for (int kk = 0; kk < 4; ++kk)
+                                ptx::umma2_bf16_1t(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (first && kk == 0) ? 0u : 1u);
+                            ptx::umma2_commit_mc_1t(emptyB + sb, 3);
                         }
-                        ptx::umma2_commit_mc(emptyB + sb, 3);
+                        __syncwarp();
+                        first = 0;
                         if (++sb == SB) { sb = 0; pb ^= 1; }
                     }
                     ptx::umma2_commit_mc(emptyA + sa, 3);
@@ -1850,11 +1864,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     // MN-major SW128: 64-element MN chunks LBO = 16 KB apart, 8-row K groups SBO = 1 KB
                     const uint32_t a0 = (uint32_t)dA + stage * (SB >> 4);
                     const uint32_t b0 = (uint32_t)dB + stage * (SB >> 4);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        ptx::umma_bf16_lh(d, a0 + kk * 128, hiA, b0 + kk * (Cfg::KB == 64 ? 128 : 2 * Cfg::KB), hiB, idesc,
-                                          (pt != p0 || kk != 0) ? 1u : 0u);
-                    ptx::umma_commit(empty + stage);
+                        for (int kk = 0; kk < 8; ++kk)
+                            ptx::umma_bf16_1t(d, a0 + kk * 128, hiA, b0 + kk * (Cfg::KB == 64 ? 128 : 2 * Cfg::KB), hiB, idesc,
+                                              (pt != p0 || kk != 0) ? 1u : 0u);
+                        ptx::umma_commit_1t(empty + stage);
+                    }
+                    __syncwarp();
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
                 ptx::umma_commit(tfull + acc);
@@ -2090,20 +2107,23 @@ __global__ void __launch_bounds__(kDwThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t so = stage * (SB >> 4);
                 const uint32_t d1 = tmem + acc * CI;
+                if (ptx::elect_one()) {
 #pragma unroll
-                for (int kc = 0; kc < Cfg::kDB; ++kc)
+                    for (int kc = 0; kc < Cfg::kDB; ++kc)
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        ptx::umma_bf16_lh(d1, (uint32_t)dK + so + kc * (kABytes >> 4) + 2 * kk, hK,
-                                          (uint32_t)dW + kc * (CI * 128 >> 4) + 2 * kk, hW, idg, (kc | kk) != 0);
+                        for (int kk = 0; kk < 4; ++kk)
+                            ptx::umma_bf16_1t(d1, (uint32_t)dK + so + kc * (kABytes >> 4) + 2 * kk, hK,
+                                              (uint32_t)dW + kc * (CI * 128 >> 4) + 2 * kk, hW, idg, (kc | kk) != 0);
 #pragma unroll
-                for (int mt = 0; mt < Cfg::kMT; ++mt)
+                    for (int mt = 0; mt < Cfg::kMT; ++mt)
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        ptx::umma_bf16_lh(tmem + Cfg::kD2Col + mt * CI, (uint32_t)dM + so + mt * 2 * (kABytes >> 4) + kk * 128,
-                                          hM, (uint32_t)dX + so + kk * 128, hX, iwg, (pt != p0 || kk != 0) ? 1u : 0u);
-                ptx::umma_commit(empty + stage);
-                ptx::umma_commit(tfull + acc);
+                        for (int kk = 0; kk < 8; ++kk)
+                            ptx::umma_bf16_1t(tmem + Cfg::kD2Col + mt * CI, (uint32_t)dM + so + mt * 2 * (kABytes >> 4) + kk * 128,
+                                              hM, (uint32_t)dX + so + kk * 128, hX, iwg, (pt != p0 || kk != 0) ? 1u : 0u);
+                    ptx::umma_commit_1t(empty + stage);
+                    ptx::umma_commit_1t(tfull + acc);
+                }
+                __syncwarp();
                 if (++stage == S) { stage = 0; phase ^= 1; }
                 if (++acc == D1B) { acc = 0; aphase ^= 1; }
             }
@@ -2362,13 +2382,16 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t a0 = (uint32_t)dA + stage * (SB >> 4);
                     const uint32_t b0 = (uint32_t)dB + stage * (SB >> 4);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
+                        for (int j = 0; j < 8; ++j)
 #pragma unroll
-                        for (int kx = 0; kx < KW; ++kx)
-                            ptx::umma_bf16_lh(tmem + kx * BN, a0 + j * 128, hiA, b0 + joff[j] + kx * 8, hiB, idesc,
-                                              (pt != p0 || j != 0) ? 1u : 0u);
-                    ptx::umma_commit(empty + stage);
+                            for (int kx = 0; kx < KW; ++kx)
+                                ptx::umma_bf16_1t(tmem + kx * BN, a0 + j * 128, hiA, b0 + joff[j] + kx * 8, hiB, idesc,
+                                                  (pt != p0 || j != 0) ? 1u : 0u);
+                        ptx::umma_commit_1t(empty + stage);
+                    }
+                    __syncwarp();
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
                 ptx::umma_commit(tfull);
@@ -2581,13 +2604,16 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t so = stage * (SB >> 4);
                     const uint32_t b0 = lo0 + so;                      // delta box (B)
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
+                        for (int j = 0; j < 8; ++j)
 #pragma unroll
-                        for (int p = 0; p < NP; ++p)
-                            ptx::umma_bf16_lh(tmem + p * 64, loA[p] + so + joff[j], hi, b0 + j * 128, hi, idesc,
-                                              (pt != p0 || j != 0) ? 1u : 0u);
-                    ptx::umma_commit(empty + stage);
+                            for (int p = 0; p < NP; ++p)
+                                ptx::umma_bf16_1t(tmem + p * 64, loA[p] + so + joff[j], hi, b0 + j * 128, hi, idesc,
+                                                  (pt != p0 || j != 0) ? 1u : 0u);
+                        ptx::umma_commit_1t(empty + stage);
+                    }
+                    __syncwarp();
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
                 ptx::umma_commit(tfull);
@@ -2838,10 +2864,13 @@ __global__ void __launch_bounds__(kWiThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t a0 = (uint32_t)dA + stage * (kWiStage >> 4);
                     const uint32_t b0 = (uint32_t)dB + stage * (kWiStage >> 4);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        ptx::umma_bf16_lh(tmem, a0 + kk * 128, hiA, b0 + kk * 128, hiB, idesc, (pt != p0 || kk != 0) ? 1u : 0u);
-                    ptx::umma_commit(empty + stage);
+                        for (int kk = 0; kk < 8; ++kk)
+                            ptx::umma_bf16_1t(tmem, a0 + kk * 128, hiA, b0 + kk * 128, hiB, idesc, (pt != p0 || kk != 0) ? 1u : 0u);
+                        ptx::umma_commit_1t(empty + stage);
+                    }
+                    __syncwarp();
                     if (++stage == kWiStages) { stage = 0; phase ^= 1; }
                 }
                 ptx::umma_commit(tfull);
@@ -3017,18 +3046,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(fullA + sa, pa);
                 ptx::tc_fence_after();
                 const uint32_t a0 = (uint32_t)dA + sa * (AB >> 4);
+                if (ptx::elect_one()) {
+#pragma unroll 1
+                    for (int tap = 0; tap < taps; ++tap) {
+                        const int ky = tap / KH, kx = tap - ky * KH;
+                        const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
+                        const uint32_t b0 = (uint32_t)dB + tap * (BN * 128 >> 4);
 #pragma unroll
-                for (int tap = 0; tap < taps; ++tap) {
-                    const int ky = tap / KH, kx = tap - ky * KH;
-                    const uint32_t at = a0 + (uint32_t)(ky * HP + kx) * 8;
-                    const uint32_t b0 = (uint32_t)dB + tap * (BN * 128 >> 4);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        ptx::umma_bf16_lh(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (tap | kk) != 0);
+                        for (int kk = 0; kk < 4; ++kk)
+                            ptx::umma_bf16_1t(d, at + 2 * kk, hiA, b0 + 2 * kk, hiB, idesc, (tap | kk) != 0);
+                    }
+                    ptx::umma_commit_1t(emptyA + sa);
+                    ptx::umma_commit_1t(tfull + acc);
                 }
-                ptx::umma_commit(emptyA + sa);
+                __syncwarp();
                 if (++sa == SA) { sa = 0; pa ^= 1; }
-                ptx::umma_commit(tfull + acc);
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
