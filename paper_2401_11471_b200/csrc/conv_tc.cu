@@ -60,7 +60,7 @@ struct TcConv {
     int tma_dg;            // dgrad: TMA-load delta (+ activation), combine in smem, TMA-store
     int tma_res;           // FP: the residual tile is TMA-loaded into the staging buffer
     int tap_oy[49], tap_ox[49], tap_w[49];
-    int dbg;               // LRCNN_TC_DBG: bit0 skip epilogue stores (microbenchmarks)
+    int dbg;               // debug bits (bit0: skip epilogue stores); always 0 in the product
     int tw_log2;           // TW = 1 << tw_log2
     int th_log2;           // TH = 1 << th_log2
     int NBt;               // images per tile (small maps: a 128-pixel tile spans NBt images; 0/1 = one)
@@ -3299,17 +3299,9 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     const int rows = P.out_b - P.out_a;
     if (rows <= 0 || P.Wo <= 0) return true;
     if (P.halo_ok && conv_halo_rb(P, in, w, w_rows, cin_p, st)) return true;
-    {   // small launches (deep layers, thin bands): narrower N tiles so that every SM gets work
-        static const int adapt = env_int("LRCNN_BN_ADAPT", 0);
-        int tw = 8, th = 16;
-        if (!(env_int("LRCNN_HALO", 0) && P.halo_ok && cin_p % 64 == 0 && P.o_stride == 1)) pick_tile(rows, P.Wo, P.a_mul, tw, th);
-        const long mt = (long)P.B * ((P.Wo + tw - 1) / tw) * ((rows + th - 1) / th);
-        while (adapt && BN > 64 && mt * ((P.n_out + BN - 1) / BN) < num_sms()) BN >>= 1;
-    }
-    static const int dbg = env_int("LRCNN_TC_DBG", 0);
-    P.dbg = dbg;
+    P.dbg = 0;
     P.in_base = in.base;
-    static const int halo_on = env_int("LRCNN_HALO", 0), boff = env_int("LRCNN_HALO_BOFF", 0);
+    static const int halo_on = env_int("LRCNN_HALO", 0), boff = 0;
     const int KC = cin_p <= 16 ? 16 : 64;   // small-channel layers: 16-ch chunks
     P.cin_chunks = (cin_p + KC - 1) / KC;
     P.k_steps = P.ntaps * P.cin_chunks;
@@ -3500,7 +3492,7 @@ static bool conv_pair(TcConv &P, const View &in, const void *w, int w_rows, cuda
     const int npr = (k + 1) / 2;
     P.in = in;
     P.in_base = in.base;
-    P.dbg = env_int("LRCNN_TC_DBG", 0);
+    P.dbg = 0;
     P.pat_w = s == 1 ? 7 + 2 * npr : 7 + npr;
     P.pat_h = 15 * s + k;
     P.pat_ox = -P.pad; P.pat_oy = -P.pad;
@@ -3548,7 +3540,7 @@ static bool conv_im2col(TcConv &P, const View &in, const void *w, int w_rows, cu
     if (rows <= 0 || P.Wo <= 0) return true;
     P.in = in;
     P.in_base = in.base;
-    P.dbg = env_int("LRCNN_TC_DBG", 0);
+    P.dbg = 0;
     // tap offset hull -> patch geometry; tile = the 128-pixel rectangle with the fewest padded
     // pixels whose patch fits one 16 KB buffer
     int oy0 = 1 << 20, oy1 = -(1 << 20), ox0 = 1 << 20, ox1 = -(1 << 20);

@@ -15,7 +15,7 @@ done
 # DRAM traffic of every launch of the top kernels in one C4 step
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active \
     --clock-control none --profile-from-start off --kernel-name-base demangled \
-    -k "regex:k_conv_tc|k_wgrad_tc|k_dwgrad_pw|k_conv_halo_rb|k_conv_pair" -o gpurun_out/${tag}_traffic_c4 \
+    -k "regex:k_conv_tc|k_wgrad_tc|k_dwgrad_pw|k_conv_halo_rb|k_conv_pair|k_bneck_fwd|k_wgrad_im2col|k_wgrad_halo|k_pool3s2_bwd" -o gpurun_out/${tag}_traffic_c4 \
     python scripts/one_step.py c4 8 > gpurun_out/${tag}_traffic_c4.log 2>&1
 ncu -i gpurun_out/${tag}_traffic_c4.ncu-rep --page raw --csv > gpurun_out/${tag}_traffic_c4.raw.csv 2>/dev/null
 rm -f gpurun_out/${tag}_traffic_c4.ncu-rep
