@@ -3890,7 +3890,11 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
     P.pix_tiles = (a.B + NB - 1) / NB * P.tiles_x * P.tiles_y;
-    const int BN = x.Cp >= 128 ? 128 : (x.Cp <= 16 ? 16 : 64);
+    // N = 256 input channels per item where the input has them: per 128-pixel K-step the tensor pipe then
+    // reads 12 KB of operands per 128 cycles instead of 8 KB per 64 (N = 128), which with the TMA writes
+    // of the same bytes keeps the shared-memory port at ~190 B/clk instead of ~250 (A re-read per N tile)
+    static const int wide = env_int("LRCNN_WG_256", 1);
+    const int BN = wide && x.Cp >= 256 && x.Cp % 256 == 0 ? 256 : x.Cp >= 128 ? 128 : (x.Cp <= 16 ? 16 : 64);
     P.co_tiles = (dy.Cp + 127) / 128;
     P.ci_tiles = (x.Cp + BN - 1) / BN;
     const int base_items = P.co_tiles * a.k * a.k * P.ci_tiles;
@@ -3906,7 +3910,8 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     if (!encode_view(&D, dy, a.B, P.TW, P.TH, 1, 64, NB)) return false;
     if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s, BN < 64 ? BN : 64, NB)) return false;
     const bool ok = BN == 16 ? launch_wgrad<16>(P, D, X, st)
-                  : BN == 64 ? launch_wgrad<64>(P, D, X, st) : launch_wgrad<128>(P, D, X, st);
+                  : BN == 64 ? launch_wgrad<64>(P, D, X, st)
+                  : BN == 128 ? launch_wgrad<128>(P, D, X, st) : launch_wgrad<256>(P, D, X, st);
     if (ok && P.db) a.db_done = true;
     if (ok && P.dg) a.dg_done = true;
     return ok;
