@@ -2724,6 +2724,7 @@ struct TcWgI2c {
     int TW, TH, tw_log2, tiles_x, tiles_y, pix_tiles, per_split, splits, items;
     int out_a, out_b, Wo, dy_base;
     int pat_w, pat_h, pat_ox, pat_oy, in_base;
+    int pat_flat;          // patch map over (W*Cp, rows, B): one box row = pat_w pixels x 16 B contiguous
     float *db;             // fused bias / beta gradient (two extra warps sum the delta tiles)
     float *dg;             // fused gamma gradient (epilogue: warp sums of W * dW_raw)
     const bf16 *w;
@@ -2840,8 +2841,9 @@ __global__ void __launch_bounds__(kWiThreads, 1)
                     const int tx = pt % P.tiles_x, r = pt / P.tiles_x, ty = r % P.tiles_y, b = r / P.tiles_y;
                     ptx::mbar_wait(pempty + pb, pphase ^ 1);
                     ptx::mbar_arrive_expect_tx(pfull + pb, pbytes);
-                    ptx::tma_load_4d(sP + pb * kI2cPatch, &tmP, pfull + pb, 0, tx * P.TW * P.a_mul + P.pat_ox,
-                                     (P.out_a + ty * P.TH) * P.a_mul + P.pat_oy - P.in_base, b);
+                    const int px = tx * P.TW * P.a_mul + P.pat_ox, py = (P.out_a + ty * P.TH) * P.a_mul + P.pat_oy - P.in_base;
+                    if (P.pat_flat) ptx::tma_load_3d(sP + pb * kI2cPatch, &tmP, pfull + pb, px * 8, py, b);
+                    else ptx::tma_load_4d(sP + pb * kI2cPatch, &tmP, pfull + pb, 0, px, py, b);
                     if (++pb == 2) { pb = 0; pphase ^= 1; }
                 }
             }
@@ -3466,6 +3468,20 @@ static bool launch_im2col(const TcConv &P, const CUtensorMap &Bm, const CUtensor
 
 // 4D map over an 8-channel band View with a (8, pw, ph, 1) box, no swizzle (16-byte pixels packed
 // densely in smem); rows outside the band's valid range [base, min(base+rows, H)) read as zero.
+// the same patch with the pixel row flattened: dims (W*Cp, rows, B), box (pw*Cp, ph, 1) -- the TMA moves
+// rows of pw*16 contiguous bytes instead of pw separate 16-byte elements (8-channel inputs, stride-1 box)
+static bool encode_patch_flat(CUtensorMap *m, const View &v, int B, int pw, int ph) {
+    auto fn = encode_fn();
+    const int rows = v.rows < v.H - v.base ? v.rows : v.H - v.base;
+    if (!fn || rows <= 0 || pw * v.Cp > 256 || ph > 256) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)v.W * v.Cp, (cuuint64_t)rows, (cuuint64_t)B};
+    cuuint64_t strides[2] = {(cuuint64_t)v.W * v.Cp * 2, (cuuint64_t)v.bs * 2};
+    cuuint32_t box[3] = {(cuuint32_t)(pw * v.Cp), (cuuint32_t)ph, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, v.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 static bool encode_patch(CUtensorMap *m, const View &v, int B, int pw, int ph, int es_w = 1) {
     auto fn = encode_fn();
     const int rows = v.rows < v.H - v.base ? v.rows : v.H - v.base;
@@ -3806,7 +3822,8 @@ static bool wgrad_im2col(const WgradArgs &a, cudaStream_t st) {
     P.out_a = a.a; P.out_b = a.b; P.Wo = dy.W; P.dy_base = dy.base;
     CUtensorMap D, Pm;
     if (!encode_view(&D, dy, a.B, P.TW, P.TH)) return false;
-    if (!encode_patch(&Pm, x, a.B, P.pat_w, P.pat_h)) return false;
+    P.pat_flat = encode_patch_flat(&Pm, x, a.B, P.pat_w, P.pat_h) ? 1 : 0;
+    if (!P.pat_flat && !encode_patch(&Pm, x, a.B, P.pat_w, P.pat_h)) return false;
     const bool ok = launch_wgrad_im2col<64>(P, D, Pm, st);
     if (ok && P.db) a.db_done = true;
     if (ok && P.dg) a.dg_done = true;
