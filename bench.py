@@ -316,6 +316,26 @@ def run_reference(a):
           flush=True)
 
 
+def coordination_counters(plan):
+    """The paper's two coordination counters (Sec. V-D, Fig. 9): Computation Interruptions
+    (2PS-H: one per band boundary and band tensor whose next band reads shared rows computed by the
+    band before it) and Overlapped Dimensions (OverL-H: rows of a band tensor that consecutive bands both
+    compute), counted from the plan's exact per-band row ranges (lrcnn_plan_rows); plus the sharing
+    data the 2PS cache holds (bytes)."""
+    ci = od = 0
+    for s in range(plan.nsegs()):
+        tin, tout, nb = plan.seg(s)
+        for r in range(1, nb):
+            for t in range(tin + 1, tout + 1):
+                lo, a_, _ = plan.rows(s, r, t)
+                _, _, b_prev = plan.rows(s, r - 1, t)
+                if lo < a_:
+                    ci += 1
+                od += max(0, b_prev - a_)
+    return {"computation_interruptions": ci, "overlapped_rows": od,
+            "sharing_data_bytes": plan.memory()["halo_cache"]}
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -603,6 +623,7 @@ def main():
                "reduction_vs_omega_excl_input_x": mem["omega"] / max(1, fm - xi_bytes),
                "plan": {k: mem[k] for k in ("omega", "band_act", "band_delta", "halo_cache", "carry",
                                             "checkpoints", "delta_full", "workspace")}}
+    mem_rep["coordination"] = coordination_counters(plan)
     cpu = None
     if not a.no_baselines and world == 1 and a.mode != "column":   # layer-wise memory + cpu_baseline: N=1 only
         del ds, flush

@@ -536,3 +536,21 @@ def test_auto_segments_sqrt_n():
         net2 = dict(net, ops=[dict(o, seg_end=(i + 1) in [p.seg(s)[1] for s in range(p.nsegs() - 1)])
                               for i, o in enumerate(net["ops"])])
         _check_plan_vs_enum(net2, "2ps", n_bands=2, B=1)
+
+
+@pytest.mark.parametrize("nb", [2, 4, 8])
+def test_coordination_counters_closed_form(nb):
+    """The paper's coordination counters (Sec. V-D): on the C1 chain (three 3x3/s1/p1
+    convs, H = 32) OverL-H overlaps 2d rows of a tensor d layers below the output at every band
+    boundary (Eq. (15) with k = 3, s = 1: o = 2 + 2 ... per side 1 row per layer) -> (2*2 + 2*1)(N-1) rows,
+    and 2PS-H interrupts the computation once per boundary for each of the two internal tensors (both
+    read c = k - s = 2 shared rows, Eq. (11)-(14)) and holds (N-1) * 2 tensors * 2 rows * W * C * 4 B
+    of sharing data (reading R9)."""
+    import bench
+    net = WL.tiny3(p=1)
+    ov = bench.coordination_counters(LB.Plan(net, 1, mode="overl", prec="fp32", n_bands=nb,
+                                             flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION))
+    assert ov == {"computation_interruptions": 0, "overlapped_rows": 6 * (nb - 1), "sharing_data_bytes": 0}
+    tp = bench.coordination_counters(LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=nb))
+    assert tp == {"computation_interruptions": 2 * (nb - 1), "overlapped_rows": 0,
+                  "sharing_data_bytes": (nb - 1) * 2 * 2 * 32 * 8 * 4}
