@@ -136,7 +136,8 @@ struct TcWgrad {
 
 static constexpr int kThreads = 192;
 static constexpr int kWgThreads = 320;        // wgrad kernels: producer, MMA, 4 epilogue, 4 bias-sum warps
-static constexpr int kConvThreads = 320;      // k_conv_tc: producer, MMA, 8 epilogue warps
+static constexpr int kConvThreads = 320;      // producer, MMA, 8 epilogue warps
+static constexpr int kConvTcThreads = 352;    // k_conv_tc: + the epilogue's store warp (conv_store_dma)
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
 static constexpr int kOutStage = 128 * 128;       // epilogue staging: 128 pixels x 64 channels bf16
@@ -260,11 +261,14 @@ __device__ __forceinline__ void epi_fast_r(bool relu, const uint32_t (&v)[CH], c
     else epi_fast<CH, EPI, RES, false>(v, pb, pe, pr, buf, chunk0, m);
 }
 
-template <int BN, int NE = 4, int NB = 2>
+// DMA = true (k_conv_tc): a dedicated store warp (conv_store_dma) issues every TMA store and every
+// residual load; the epilogue warps wait only for their buffer (rbar: residual landed / previous store
+// read) and signal gdone[buf] (count NE) -- no block barrier and no leader round trip per group.
+template <int BN, int NE = 4, int NB = 2, bool DMA = false>
 __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
                                                   uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
                                                   int lane, int lead_warp = 2, const CUtensorMap *tmR = nullptr,
-                                                  uint64_t *rbar = nullptr) {
+                                                  uint64_t *rbar = nullptr, uint64_t *gdone = nullptr) {
     constexpr int CH = 64 * 4 / NE;   // channels of a 64-channel group handled per thread
     const int num_tiles = P.m_tiles * P.n_tiles;
     const int q = warp & 3, hh = (warp - lead_warp) >> 2;
@@ -294,7 +298,7 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                          P.out_a + ty2 * P.TH - P.res.base, b2);
         if (++lg == ngrp(lt)) { lg = 0; lt += gridDim.x; }
     };
-    if (rt && leader)
+    if (!DMA && rt && leader)
         for (int i = 0; i < NB - 1 && lt < num_tiles; ++i) res_load(i);
     int acc = 0, sbuf = 0;
     uint32_t aphase = 0, rphases = 0;   // bit i: parity of the next completion of rbar[i]
@@ -334,9 +338,11 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             ptx::tmem_ld_wait();
             const uint32_t buf = ptx::smem_u32(stage_out + sbuf * kOutStage + m * 128);
             const int chunk0 = hh * (CH / 8);
-            if (rt) {
-                ptx::mbar_wait(rbar + sbuf, (rphases >> sbuf) & 1);   // residual tile of this group in buf
+            if (rt || DMA) {
+                ptx::mbar_wait(rbar + sbuf, (rphases >> sbuf) & 1);   // residual in buf / buf free (DMA)
                 rphases ^= 1u << sbuf;
+            }
+            if (rt) {
                 // each thread reads, then overwrites, only its own row's chunks: no barrier needed
 #pragma unroll
                 for (int c = 0; c < CH / 8; ++c) pr[c] = ld_shared_v4(buf + (((chunk0 + c) ^ (m & 7)) << 4));
@@ -369,6 +375,12 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
                 }
             }
             fence_async_smem();
+            if (DMA) {   // the store warp takes it from here
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(gdone + sbuf);
+                sbuf = sbuf + 1 == NB ? 0 : sbuf + 1;
+                continue;
+            }
             // without a residual: before this barrier the leader makes sure the NEXT group's buffer
             // (last stored NB groups before it) has been read by its store
             if (!rt && leader) bulk_wait_read_n<NB - 2>();
@@ -389,6 +401,57 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
         if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     if (leader) bulk_wait_all();
+}
+
+// The store warp of conv_epilogue_tma<..., DMA = true>: walks the CTA's (tile, 64-channel group) sequence;
+// group k uses staging buffer k % NB.  It fills every buffer first (the residual tile, or just "free"),
+// then per group waits for the NE epilogue warps (gdone), TMA-stores the buffer and, once the store has
+// read it, refills the buffer for group k + NB.
+template <int BN, int NB>
+__device__ __forceinline__ void conv_store_dma(const TcConv &P, const CUtensorMap *tmO, uint8_t *stage_out,
+                                               const CUtensorMap *tmR, uint64_t *rbar, uint64_t *gdone) {
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    const bool rt = P.has_res && P.tma_res && tmR;
+    auto ngrp = [&](int tile2) {
+        int nt2, tx2, ty2, b2;
+        P.decode(tile2, nt2, tx2, ty2, b2);
+        const int left = P.n_out - nt2 * BN;
+        return left >= BN ? BN / 64 : (left + 63) / 64;
+    };
+    int lt = blockIdx.x, lg = 0;   // next group to make ready
+    auto fill = [&](int buf) {
+        if (lt >= num_tiles) return;
+        if (rt) {
+            int nt2, tx2, ty2, b2;
+            P.decode(lt, nt2, tx2, ty2, b2);
+            ptx::mbar_arrive_expect_tx(rbar + buf, kOutStage);
+            ptx::tma_load_4d(stage_out + buf * kOutStage, tmR, rbar + buf, nt2 * BN + lg * 64, tx2 * P.TW,
+                             P.out_a + ty2 * P.TH - P.res.base, b2);
+        } else {
+            ptx::mbar_arrive(rbar + buf);
+        }
+        if (++lg == ngrp(lt)) { lg = 0; lt += gridDim.x; }
+    };
+    for (int i = 0; i < NB; ++i) fill(i);
+    int sbuf = 0;
+    uint32_t gph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
+        const int ng = ngrp(tile);
+        for (int grp = 0; grp < ng; ++grp) {
+            ptx::mbar_wait(gdone + sbuf, (gph >> sbuf) & 1);
+            gph ^= 1u << sbuf;
+            tma_store_4d(tmO, stage_out + sbuf * kOutStage, n0 + grp * 64, P.o_col0 + P.o_stride * xg0,
+                         P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+            bulk_commit();
+            bulk_wait_read0();   // the store has read the buffer: refill it for group k + NB
+            fill(sbuf);
+            sbuf = sbuf + 1 == NB ? 0 : sbuf + 1;
+        }
+    }
+    bulk_wait_all();
 }
 
 // Per-warp FP epilogue (small-K 1x1 convolutions, P.warp_epi): no block-wide barrier.  Warp
@@ -909,7 +972,7 @@ __device__ __forceinline__ void conv_epilogue(const TcConv &P, uint32_t tmem, ui
 // regular layers, 16 (32-byte rows, SWIZZLE_32B, 1 MMA) for small-channel layers (padded RGB
 // input of conv1_1 / the 7x7 stem), which would otherwise waste 8x tensor work on zero channels.
 template <int BN, int KC, int NBUF>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kConvTcThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P,
               const __grid_constant__ CUtensorMap tmX) {
@@ -934,7 +997,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
-        for (int i = 0; i < (NBUF >= 8 ? 32 : NBUF); ++i) ptx::mbar_init(ebar + i, 1);   // staging rings
+        const bool dma = P.tma_out && !(NBUF >= 8 && BN >= 128 && P.warp_epi);   // conv_store_dma runs
+        for (int i = 0; i < (NBUF >= 8 ? 32 : 2 * NBUF); ++i)                       // staging rings;
+            ptx::mbar_init(ebar + i, dma && i >= NBUF && i < 2 * NBUF ? 8 : 1);    // gdone: 8 warps
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -998,12 +1063,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
+    } else if (warp == 10) {
+        if (P.tma_out && !(NBUF >= 8 && BN >= 128 && P.warp_epi) && lane == 0)
+            conv_store_dma<BN, Cfg::kOutBufs>(P, &tmO, sO, &tmG, ebar, ebar + NBUF);
     } else {
         if (NBUF >= 8 && BN >= 128 && P.warp_epi && P.tma_out)
             conv_epilogue_tma_w<BN, NBUF / 2>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, &tmG, ebar);
         else if (NBUF >= 8 && BN >= 128 && P.warp_epi && P.tma_dg)
             conv_epilogue_tma_dg_w<BN, NBUF / 4>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, &tmX);
-        else if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
+        else if (P.tma_out)
+            conv_epilogue_tma<BN, 8, Cfg::kOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar,
+                                                          ebar + NBUF);
         else if (P.tma_dg && Cfg::kOutBufs >= 4)
             conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
@@ -3245,7 +3315,7 @@ static bool launch_conv(const TcConv &P, const CUtensorMap &A, const CUtensorMap
     using Cfg = ConvCfg<BN, KC, NBUF>;
     if (!smem_attr((const void *)k_conv_tc<BN, KC, NBUF>, Cfg::kSmem)) return false;
     int grid = tiles < num_sms() ? tiles : num_sms();
-    return launch_pdl(k_conv_tc<BN, KC, NBUF>, grid, kConvThreads, Cfg::kSmem, st, A, Bm, O, G, P, X);
+    return launch_pdl(k_conv_tc<BN, KC, NBUF>, grid, kConvTcThreads, Cfg::kSmem, st, A, Bm, O, G, P, X);
 }
 
 template <int BN>
