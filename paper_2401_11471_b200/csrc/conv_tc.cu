@@ -673,11 +673,14 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
 // TMA loads of item k+1 are issued before item k's combine (once item k-1's store has read that
 // pair), so the HBM latency of the delta / activation tiles overlaps the current item instead of
 // being exposed once per tile (small-K layers: a 64-channel 3x3 dgrad tile is ~1200 MMA cycles).
-template <int BN, int NE = 4, int NP = 2>
+// DMA = true (k_conv_tc): conv_store_dma_dg issues all loads and stores; the epilogue warps signal
+// gdone[pair] (count NE) after combining an item instead of a block barrier + leader store.
+template <int BN, int NE = 4, int NP = 2, bool DMA = false>
 __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
                                                       uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
                                                       uint8_t *stage_out, uint64_t *ebar, int warp, int lane,
-                                                      int lead_warp = 2, const CUtensorMap *tmX = nullptr) {
+                                                      int lead_warp = 2, const CUtensorMap *tmX = nullptr,
+                                                      uint64_t *gdone = nullptr) {
     constexpr int CH = 64 * 4 / NE;           // channels of a 64-channel group per thread
     const int num_tiles = P.m_tiles * P.n_tiles;
     const int q = warp & 3, m = q * 32 + lane, hh = (warp - lead_warp) >> 2;
@@ -708,7 +711,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         if (++it_grp == ngroups(it_tile)) { it_grp = 0; it_tile += gridDim.x; }
     };
     int ipair = 0;
-    if (leader)
+    if (leader && !DMA)
         for (int i = 0; i < NP - 1 && it_tile < num_tiles; ++i) {
             issue(it_tile, it_grp, ipair);
             ipair = ipair + 1 == NP ? 0 : ipair + 1;
@@ -730,7 +733,7 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
 #pragma unroll
             for (int h = 0; h < CH / 32; ++h)
                 ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
-            if (leader && it_tile < num_tiles) {   // prefetch NP-1 items ahead into the pair item k-1 used
+            if (!DMA && leader && it_tile < num_tiles) {   // prefetch NP-1 items ahead into the pair item k-1 used
                 bulk_wait_read0();                     // (its store, the latest committed, has read it)
                 issue(it_tile, it_grp, ipair);
                 ipair = ipair + 1 == NP ? 0 : ipair + 1;
@@ -759,6 +762,12 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
                 st_shared_v4(rowD + off, make_uint4(o[0], o[1], o[2], o[3]));
             }
             fence_async_smem();
+            if (DMA) {
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(gdone + pi);
+                pi = pi + 1 == NP ? 0 : pi + 1;
+                continue;
+            }
             epi_bar_n<NE>();
             if (leader) {
                 tma_store_4d(tmO, stage_out + (2 * pi) * kOutStage, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.out.base, b);
@@ -772,6 +781,57 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
     if (leader) bulk_wait_all();
+}
+
+// The store warp of conv_epilogue_tma_dg2<..., DMA = true>: item k = (tile, 64-channel group) of this CTA
+// uses staging pair k % NP (delta buffer, activation buffer).  All pairs are loaded first; per item it
+// waits for the epilogue warps (gdone), TMA-stores the combined delta and, once the store has read the
+// pair, loads item k + NP into it.
+template <int BN, int NP>
+__device__ __forceinline__ void conv_store_dma_dg(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
+                                                  const CUtensorMap *tmX, uint8_t *stage_out, uint64_t *ebar,
+                                                  uint64_t *gdone) {
+    const int num_tiles = P.m_tiles * P.n_tiles;
+    const bool dload = !P.dg_write || (P.dg_add && tmX);
+    const CUtensorMap *tmD = P.dg_write ? tmX : tmO;
+    const uint32_t ebytes = (dload ? (uint32_t)kOutStage : 0u) + (P.gate ? (uint32_t)kOutStage : 0u);
+    auto ngroups = [&](int tile) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        return min(BN / 64, (P.n_out - nt * BN + 63) / 64);
+    };
+    int it_tile = blockIdx.x, it_grp = 0;   // next item to load
+    auto issue = [&](int pi) {
+        if (it_tile >= num_tiles) return;
+        int nt, tx, ty, b;
+        P.decode(it_tile, nt, tx, ty, b);
+        const int nb = nt * BN + it_grp * 64, xg0 = tx * P.TW, yg0 = P.out_a + ty * P.TH;
+        uint8_t *bd = stage_out + (2 * pi) * kOutStage;
+        ptx::mbar_arrive_expect_tx(ebar + pi, ebytes);
+        if (dload) ptx::tma_load_4d(bd, tmD, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - (P.dg_write ? P.add.base : P.out.base), b);
+        if (P.gate) ptx::tma_load_4d(bd + kOutStage, tmG, ebar + pi, nb, P.o_col0 + P.o_stride * xg0, P.o_row0 + P.o_stride * yg0 - P.act.base, b);
+        if (++it_grp == ngroups(it_tile)) { it_grp = 0; it_tile += gridDim.x; }
+    };
+    for (int i = 0; i < NP; ++i) issue(i);
+    int pi = 0;
+    uint32_t gph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int nt, tx, ty, b;
+        P.decode(tile, nt, tx, ty, b);
+        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
+        const int ng = ngroups(tile);
+        for (int grp = 0; grp < ng; ++grp) {
+            ptx::mbar_wait(gdone + pi, (gph >> pi) & 1);
+            gph ^= 1u << pi;
+            tma_store_4d(tmO, stage_out + (2 * pi) * kOutStage, n0 + grp * 64, P.o_col0 + P.o_stride * xg0,
+                         P.o_row0 + P.o_stride * yg0 - P.out.base, b);
+            bulk_commit();
+            bulk_wait_read0();
+            issue(pi);
+            pi = pi + 1 == NP ? 0 : pi + 1;
+        }
+    }
+    bulk_wait_all();
 }
 
 // Per-warp dgrad epilogue (small-K 1x1 convolutions, P.warp_epi): as conv_epilogue_tma_w, each warp
@@ -997,7 +1057,8 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
-        const bool dma = P.tma_out && !(NBUF >= 8 && BN >= 128 && P.warp_epi);   // conv_store_dma runs
+        const bool dma = (P.tma_out || (P.tma_dg && Cfg::kOutBufs >= 4)) &&
+                         !(NBUF >= 8 && BN >= 128 && P.warp_epi);   // conv_store_dma(_dg) runs
         for (int i = 0; i < (NBUF >= 8 ? 32 : 2 * NBUF); ++i)                       // staging rings;
             ptx::mbar_init(ebar + i, dma && i >= NBUF && i < 2 * NBUF ? 8 : 1);    // gdone: 8 warps
         ptx::fence_barrier_init();
@@ -1064,8 +1125,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
             }
         }
     } else if (warp == 10) {
-        if (P.tma_out && !(NBUF >= 8 && BN >= 128 && P.warp_epi) && lane == 0)
-            conv_store_dma<BN, Cfg::kOutBufs>(P, &tmO, sO, &tmG, ebar, ebar + NBUF);
+        if (lane == 0 && !(NBUF >= 8 && BN >= 128 && P.warp_epi)) {
+            if (P.tma_out) conv_store_dma<BN, Cfg::kOutBufs>(P, &tmO, sO, &tmG, ebar, ebar + NBUF);
+            else if (P.tma_dg && Cfg::kOutBufs >= 4)
+                conv_store_dma_dg<BN, Cfg::kOutBufs / 2>(P, &tmO, &tmG, &tmX, sO, ebar, ebar + NBUF);
+        }
     } else {
         if (NBUF >= 8 && BN >= 128 && P.warp_epi && P.tma_out)
             conv_epilogue_tma_w<BN, NBUF / 2>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, &tmG, ebar);
@@ -1075,7 +1139,8 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
             conv_epilogue_tma<BN, 8, Cfg::kOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar,
                                                           ebar + NBUF);
         else if (P.tma_dg && Cfg::kOutBufs >= 4)
-            conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
+            conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2, true>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2,
+                                                                  &tmX, ebar + NBUF);
         else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
         else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
     }
