@@ -137,7 +137,8 @@ struct TcWgrad {
 static constexpr int kThreads = 192;
 static constexpr int kWgThreads = 320;        // wgrad kernels: producer, MMA, 4 epilogue, 4 bias-sum warps
 static constexpr int kConvThreads = 320;      // producer, MMA, 8 epilogue warps
-static constexpr int kConvTcThreads = 352;    // k_conv_tc: + the epilogue's store warp (conv_store_dma)
+static constexpr int kConvTcEpi = 16;         // k_conv_tc: epilogue warps of the store-warp (DMA) epilogues
+static constexpr int kConvTcThreads = (2 + kConvTcEpi + 1) * 32;   // producer, MMA, 16 epilogue warps, store warp
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
 static constexpr int kOutStage = 128 * 128;       // epilogue staging: 128 pixels x 64 channels bf16
@@ -321,9 +322,13 @@ __device__ __forceinline__ void conv_epilogue_tma(const TcConv &P, const CUtenso
             if (nb >= P.n_out) break;
             const int cb = nb + hh * CH;              // this thread's first channel
             uint32_t v[CH];
+            if constexpr (CH == 16) {
+                ptx::tmem_ld16(tq + acc * BN + grp * 64 + hh * CH, *reinterpret_cast<uint32_t(*)[16]>(v));
+            } else {
 #pragma unroll
-            for (int h = 0; h < CH / 32; ++h)
-                ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+                for (int h = 0; h < CH / 32; ++h)
+                    ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+            }
             // per-channel epilogue parameters (identical for every pixel) and the residual
             uint4 pb[CH / 8], pe[CH / 8], pr[CH / 8];
 #pragma unroll
@@ -624,9 +629,13 @@ __device__ __forceinline__ void conv_epilogue_tma_dg(const TcConv &P, const CUte
         for (int grp = 0; grp < ngrp; ++grp) {
             const int nb = n0 + grp * 64;
             uint32_t v[CH];
+            if constexpr (CH == 16) {
+                ptx::tmem_ld16(tq + acc * BN + grp * 64 + hh * CH, *reinterpret_cast<uint32_t(*)[16]>(v));
+            } else {
 #pragma unroll
-            for (int h = 0; h < CH / 32; ++h)
-                ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+                for (int h = 0; h < CH / 32; ++h)
+                    ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+            }
             ptx::tmem_ld_wait();
             ptx::mbar_wait(ebar, ephase);
             ephase ^= 1;
@@ -730,9 +739,13 @@ __device__ __forceinline__ void conv_epilogue_tma_dg2(const TcConv &P, const CUt
         for (int grp = 0; grp < ngrp; ++grp) {
             const int nb = n0 + grp * 64;
             uint32_t v[CH];
+            if constexpr (CH == 16) {
+                ptx::tmem_ld16(tq + acc * BN + grp * 64 + hh * CH, *reinterpret_cast<uint32_t(*)[16]>(v));
+            } else {
 #pragma unroll
-            for (int h = 0; h < CH / 32; ++h)
-                ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+                for (int h = 0; h < CH / 32; ++h)
+                    ptx::tmem_ld32(tq + acc * BN + grp * 64 + hh * CH + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + h * 32));
+            }
             if (!DMA && leader && it_tile < num_tiles) {   // prefetch NP-1 items ahead into the pair item k-1 used
                 bulk_wait_read0();                     // (its store, the latest committed, has read it)
                 issue(it_tile, it_grp, ipair);
@@ -1056,11 +1069,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
-        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
-        const bool dma = (P.tma_out || (P.tma_dg && Cfg::kOutBufs >= 4)) &&
-                         !(NBUF >= 8 && BN >= 128 && P.warp_epi);   // conv_store_dma(_dg) runs
-        for (int i = 0; i < (NBUF >= 8 ? 32 : 2 * NBUF); ++i)                       // staging rings;
-            ptx::mbar_init(ebar + i, dma && i >= NBUF && i < 2 * NBUF ? 8 : 1);    // gdone: 8 warps
+        // store-warp epilogues: 16 epilogue warps + conv_store_dma(_dg); otherwise warps 2..9 only
+        const bool dma = P.tma_out || (P.tma_dg && Cfg::kOutBufs >= 4);
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, dma ? kConvTcEpi : 8); }
+        for (int i = 0; i < 2 * NBUF; ++i)                                       // staging rings; gdone[NBUF]
+            ptx::mbar_init(ebar + i, dma && i >= NBUF ? kConvTcEpi : 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -1124,25 +1137,23 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
-    } else if (warp == 10) {
-        if (lane == 0 && !(NBUF >= 8 && BN >= 128 && P.warp_epi)) {
+    } else if (warp == 2 + kConvTcEpi) {
+        if (lane == 0) {
             if (P.tma_out) conv_store_dma<BN, Cfg::kOutBufs>(P, &tmO, sO, &tmG, ebar, ebar + NBUF);
             else if (P.tma_dg && Cfg::kOutBufs >= 4)
                 conv_store_dma_dg<BN, Cfg::kOutBufs / 2>(P, &tmO, &tmG, &tmX, sO, ebar, ebar + NBUF);
         }
     } else {
-        if (NBUF >= 8 && BN >= 128 && P.warp_epi && P.tma_out)
-            conv_epilogue_tma_w<BN, NBUF / 2>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, &tmG, ebar);
-        else if (NBUF >= 8 && BN >= 128 && P.warp_epi && P.tma_dg)
-            conv_epilogue_tma_dg_w<BN, NBUF / 4>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, &tmX);
-        else if (P.tma_out)
-            conv_epilogue_tma<BN, 8, Cfg::kOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar,
-                                                          ebar + NBUF);
+        if (P.tma_out)
+            conv_epilogue_tma<BN, kConvTcEpi, Cfg::kOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG,
+                                                                   ebar, ebar + NBUF);
         else if (P.tma_dg && Cfg::kOutBufs >= 4)
-            conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2, true>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2,
-                                                                  &tmX, ebar + NBUF);
-        else if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
-        else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
+            conv_epilogue_tma_dg2<BN, kConvTcEpi, Cfg::kOutBufs / 2, true>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp,
+                                                                           lane, 2, &tmX, ebar + NBUF);
+        else if (warp < 10) {   // the other epilogues run on warps 2..9
+            if (P.tma_dg) conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+            else conv_epilogue<BN, 8>(P, tmem, tfull, tempty, warp, lane);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -3490,9 +3501,11 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     tile_div_init(P);
     // small-K layers (one or two K-steps per tile: the 1x1 convolutions of ResNet's bottleneck ends)
     // are bound by the epilogue's tile traffic: the deep staging ring and per-warp epilogue boxes
-    static const int deep = env_int("LRCNN_DEEP_RING", 1), wepi = env_int("LRCNN_WARP_EPI", 1);
+    static const int deep = env_int("LRCNN_DEEP_RING", 1);
     const bool deep_ring = deep && !try2h && P.k_steps <= 2 && BN >= 128 && KC == 64;
-    P.warp_epi = deep_ring && wepi && NB == 1 && P.TW * P.TH == 128 ? 1 : 0;
+    // the per-warp epilogues (conv_epilogue_tma_w / _dg_w) measured slower than the store-warp ring
+    // (profiles/r02/r02e_epilogue_w_timeline_cycles.txt): k_conv_tc always takes the latter
+    P.warp_epi = 0;
     if (P.mode == 0 && P.has_res && !(P.res.Cp == P.out.Cp && P.n_out % 64 == 0 && aligned16(P.res.p)))
         P.warp_epi = 0;   // the per-warp epilogue takes the residual through TMA only
     const int EW = P.warp_epi ? std::min(P.TW, 32) : P.TW, EH = P.warp_epi ? 32 / EW : P.TH;   // epilogue box
