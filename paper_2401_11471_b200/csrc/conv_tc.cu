@@ -139,6 +139,7 @@ static constexpr int kWgThreads = 320;        // wgrad kernels: producer, MMA, 4
 static constexpr int kConvThreads = 320;      // producer, MMA, 8 epilogue warps
 static constexpr int kConvTcEpi = 16;         // k_conv_tc: epilogue warps of the store-warp (DMA) epilogues
 static constexpr int kConvTcThreads = (2 + kConvTcEpi + 1) * 32;   // producer, MMA, 16 epilogue warps, store warp
+static constexpr int kConv2Threads = 352;     // k_conv_tc2: producer, MMA, 8 epilogue warps, store warp
 static constexpr int kABytes = 128 * 128;   // 128 pixels x 64 bf16
 
 static constexpr int kOutStage = 128 * 128;       // epilogue staging: 128 pixels x 64 channels bf16
@@ -1185,7 +1186,7 @@ struct Conv2Cfg {
 };
 
 template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConv2Threads, 1)
     k_conv_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P,
                const __grid_constant__ CUtensorMap tmX) {
@@ -1201,15 +1202,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
-    uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 4);
+    uint64_t *ebar = tempty + 2;                     // staging ring [4] + gdone [4] (store warp)
+    uint32_t *tslot = (uint32_t *)(ebar + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 16); }
-        for (int i = 0; i < 4; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
+        for (int i = 0; i < 8; ++i) ptx::mbar_init(ebar + i, i < 4 ? 1 : 8);   // ring / gdone (8 epilogue warps)
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -1281,10 +1282,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
+    } else if (warp == 10) {   // store warp: every TMA store and staging load of this CTA's epilogue
+        if (lane == 0) {
+            if (P.tma_out) conv_store_dma<BN, Cfg::kOutBufs>(P, &tmO, sO, &tmG, ebar, ebar + 4);
+            else conv_store_dma_dg<BN, Cfg::kOutBufs / 2>(P, &tmO, &tmG, &tmX, sO, ebar, ebar + 4);
+        }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
-        else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, &tmX);
-        else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        static_assert(Conv2Cfg<BN>::kOutBufs == 4, "k_conv_tc2 store-warp epilogues: 4 staging buffers");
+        if (P.tma_out)
+            conv_epilogue_tma<BN, 8, Cfg::kOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar, ebar + 4);
+        else
+            conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2, true>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2,
+                                                                  &tmX, ebar + 4);
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();     // no CTA leaves while its peer may still signal its barriers
@@ -3573,10 +3582,10 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         int grid = tiles < num_sms() ? tiles : num_sms() & ~1;
         if (BN == 256) {
             if (!smem_attr((const void *)k_conv_tc2<256>, Conv2Cfg<256>::kSmem)) return false;
-            return launch_pdl(k_conv_tc2<256>, grid, kConvThreads, Conv2Cfg<256>::kSmem, st, A, Bm, O, G, P, X);
+            return launch_pdl(k_conv_tc2<256>, grid, kConv2Threads, Conv2Cfg<256>::kSmem, st, A, Bm, O, G, P, X);
         }
         if (!smem_attr((const void *)k_conv_tc2<128>, Conv2Cfg<128>::kSmem)) return false;
-        return launch_pdl(k_conv_tc2<128>, grid, kConvThreads, Conv2Cfg<128>::kSmem, st, A, Bm, O, G, P, X);
+        return launch_pdl(k_conv_tc2<128>, grid, kConv2Threads, Conv2Cfg<128>::kSmem, st, A, Bm, O, G, P, X);
     }
     if (KC == 16) {
         if (BN == 64) return launch_conv<64, 16>(P, A, Bm, O, G, X, tiles, st);
