@@ -1498,7 +1498,8 @@ static lrcnn_status step_grads_eager(lrcnn_plan_t *plan, const void *params, flo
     const float hw = (float)z.H * z.W;
     float *scratch = (float *)(w + P.head_off);
     Nvtx nv("head");
-    CK(head_gap(P.opts.prec, R.zl, P.net.B, z.ck_rows * z.W, z.Cp, hw, scratch, R.st));
+    CK(head_gap(P.opts.prec, R.zl, P.net.B, z.ck_rows * z.W, z.Cp, hw, scratch, R.st,
+                scratch + (size_t)P.net.B * z.Cp + (size_t)P.net.B * P.net.n_classes + P.net.B + 64));
     if (P.opts.world > 1) {
         const char *err = nullptr;
         if (comm_allreduce_f32((Comm *)P.comm, scratch, (size_t)P.net.B * z.Cp, R.st, &err))

@@ -113,7 +113,9 @@ cudaError_t head_forward_backward(int prec, const void *zl, int B, int HW, int C
                                   const void *fc_w, const void *fc_b, const int32_t *labels, float *scratch,
                                   float *loss, float *g_fc_w, float *g_fc_b, void *dzl, int gate,
                                   cudaStream_t st);
-cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st);
+// partial: B * kGapChunks(64) * Cp floats for the two-pass bf16 GAP (nullptr: one-pass kernel)
+cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st,
+                     float *partial = nullptr);
 cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, int classes, const void *fc_w,
                       const void *fc_b, const int32_t *labels, float *scratch, float *loss, float *g_fc_w,
                       float *g_fc_b, void *dzl, int gate, float hw_div, cudaStream_t st);

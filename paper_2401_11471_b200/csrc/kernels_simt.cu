@@ -474,6 +474,49 @@ __global__ void k_gap(const T *zl, int HW, int Cp, float *gap, float hw_div) {
     gap[(long long)b * Cp + c] = s / hw_div;
 }
 
+// GAP in two deterministic passes (z^L is the largest head input: 278 MB at C4).  Pass 1: block
+// (chunk, b) sums the pixels [chunk * per, ...) of image b with 16-byte loads (a thread = 8 channels of
+// one pixel slot; ppi pixel slots per block iteration), reduces its slots in shared memory and writes
+// partial[b][chunk][c].  Pass 2: one thread per (b, c) adds the chunks in order.
+constexpr int kGapChunks = 64;
+template <typename T>
+__global__ void __launch_bounds__(256) k_gap_partial(const T *zl, int HW, int Cp, float *partial) {
+    griddep_wait();
+    griddep_launch();
+    extern __shared__ float gsum[];   // [ppi][Cp]
+    const int chunk = blockIdx.x, b = blockIdx.y;
+    const int tpp = Cp / 8, ppi = blockDim.x / tpp;   // threads per pixel, pixel slots per iteration
+    const int slot = threadIdx.x / tpp, cv = threadIdx.x - slot * tpp;
+    const int per = (HW + kGapChunks - 1) / kGapChunks, p0 = chunk * per, p1 = min(HW, p0 + per);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (slot < ppi) {
+        const T *z = zl + (long long)b * HW * Cp + cv * 8;
+        for (int p = p0 + slot; p < p1; p += ppi) {
+            float v[8];
+            ld8(z + (long long)p * Cp, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += v[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) gsum[slot * Cp + cv * 8 + j] = acc[j];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < Cp; c += blockDim.x) {
+        float t = 0.f;
+        for (int s2 = 0; s2 < ppi; ++s2) t += gsum[s2 * Cp + c];
+        partial[((long long)b * kGapChunks + chunk) * Cp + c] = t;
+    }
+}
+__global__ void k_gap_final(const float *partial, int Cp, float *gap, float hw_div) {
+    griddep_wait();
+    griddep_launch();
+    const int b = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= Cp) return;
+    float t = 0.f;
+    for (int k = 0; k < kGapChunks; ++k) t += partial[((long long)b * kGapChunks + k) * Cp + c];
+    gap[(long long)b * Cp + c] = t / hw_div;
+}
+
 // Head: FC -> softmax-CE (mean over B) -> d logits -> FC gradients.  k_fc_logits has one block per
 // image (warps over classes, lanes over channels) and writes that image's d logits and loss term;
 // k_fc_grad spreads the FC weight gradient over (class, channel) threads and sums the loss.
@@ -1168,12 +1211,21 @@ __global__ void k_dzl8(const bf16 *zl, const float *dlog, const bf16 *fw, int HW
 }
 
 // GAP over the z^L rows this rank holds (HW pixels per image), divided by the global H_L*W_L
-cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st) {
+cudaError_t head_gap(int prec, const void *zl, int B, int HW, int Cp, float hw_div, float *scratch, cudaStream_t st,
+                     float *partial) {
+    if (prec && partial && Cp % 8 == 0 && Cp / 8 <= 256 && B <= 65535) {   // bf16: two-pass, 16-byte loads
+        const int ppi = 256 / (Cp / 8);
+        launch_simt(k_gap_partial<bf16>, dim3(kGapChunks, B), 256, sizeof(float) * ppi * Cp, st, (const bf16 *)zl, HW, Cp,
+                    partial);
+        launch_simt(k_gap_final, dim3((Cp + 127) / 128, B), 128, 0, st, (const float *)partial, Cp, scratch, hw_div);
+        return cudaGetLastError();
+    }
     dim3 g1(B, (Cp + 127) / 128);
     if (prec) launch_simt(k_gap<bf16>, g1, 128, 0, st, (const bf16 *)zl, HW, Cp, scratch, hw_div);
     else launch_simt(k_gap<float>, g1, 128, 0, st, (const float *)zl, HW, Cp, scratch, hw_div);
     return cudaGetLastError();
 }
+size_t head_gap_partial_floats(int B, int Cp) { return (size_t)B * kGapChunks * Cp; }
 
 // FC -> softmax-CE -> d logits -> FC grads -> delta^L (gated by the last op's ReLU) on this rank's rows
 cudaError_t head_tail(int prec, const void *zl, int B, int HW, int Cp, int C, int classes, const void *fc_w,

@@ -698,7 +698,8 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         P.xstage_off[1] = P.xstage_off[0] + 2 * xmax;
         M.other += 4 * xmax;
     }
-    P.head_off = alloc(sizeof(float) * (B * zl.Cp + B * net->n_classes + B + 64));   // gap, d logits, loss terms
+    // gap, d logits, loss terms, then the two-pass GAP partial sums [B][64 chunks][Cp] (head_gap)
+    P.head_off = alloc(sizeof(float) * (B * zl.Cp + B * net->n_classes + B + 64 + (size_t)B * 64 * zl.Cp));
     P.flag_off = alloc(256);
     M.other += ws - (P.head_off);
     {
