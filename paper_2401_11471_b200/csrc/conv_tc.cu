@@ -1765,7 +1765,7 @@ struct Conv2HCfg {
 };
 
 template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConv2Threads, 1)
     k_conv_tc2h(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
     using Cfg = Conv2HCfg<BN>;
@@ -1782,8 +1782,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
     uint64_t *emptyB = fullB + SB;
     uint64_t *tfull = emptyB + SB;
     uint64_t *tempty = tfull + 2;
-    uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 4);
+    uint64_t *ebar = tempty + 2;                     // staging ring [4] + gdone [4] (store warp)
+    uint32_t *tslot = (uint32_t *)(ebar + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -1791,7 +1791,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
         for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
         for (int i = 0; i < SB; ++i) { ptx::mbar_init(fullB + i, 1); ptx::mbar_init(emptyB + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 16); }
-        for (int i = 0; i < 4; ++i) ptx::mbar_init(ebar + i, 1);   // dgrad pairs / residual ring
+        for (int i = 0; i < 8; ++i) ptx::mbar_init(ebar + i, i < 4 ? 1 : 8);   // ring / gdone (8 epilogue warps)
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -1880,9 +1880,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kConvThreads, 1)
             }
         }
     } else {
-        if (P.tma_out) conv_epilogue_tma<BN, 8, Cfg::kOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar);
-        else if (Cfg::kOutBufs >= 4) conv_epilogue_tma_dg2<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
-        else conv_epilogue_tma_dg<BN, 8>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        if (warp == 10) {   // store warp: every TMA store and staging load of this CTA's epilogue
+            if (lane == 0) {
+                if (P.tma_out) conv_store_dma<BN, Cfg::kOutBufs>(P, &tmO, sO, &tmG, ebar, ebar + 4);
+                else conv_store_dma_dg<BN, Cfg::kOutBufs / 2>(P, &tmO, &tmG, nullptr, sO, ebar, ebar + 4);
+            }
+        } else if (P.tma_out) {
+            conv_epilogue_tma<BN, 8, Cfg::kOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, &tmG, ebar, ebar + 4);
+        } else {
+            conv_epilogue_tma_dg2<BN, 8, Cfg::kOutBufs / 2, true>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2,
+                                                                  nullptr, ebar + 4);
+        }
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -3564,10 +3572,10 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
         const int grid = tiles < num_sms() ? tiles : num_sms() & ~1;
         if (BN == 256) {
             if (!smem_attr((const void *)k_conv_tc2h<256>, Conv2HCfg<256>::kSmem)) return false;
-            return launch_pdl(k_conv_tc2h<256>, grid, kConvThreads, Conv2HCfg<256>::kSmem, st, A, Bm, O, G, P);
+            return launch_pdl(k_conv_tc2h<256>, grid, kConv2Threads, Conv2HCfg<256>::kSmem, st, A, Bm, O, G, P);
         }
         if (!smem_attr((const void *)k_conv_tc2h<128>, Conv2HCfg<128>::kSmem)) return false;
-        return launch_pdl(k_conv_tc2h<128>, grid, kConvThreads, Conv2HCfg<128>::kSmem, st, A, Bm, O, G, P);
+        return launch_pdl(k_conv_tc2h<128>, grid, kConv2Threads, Conv2HCfg<128>::kSmem, st, A, Bm, O, G, P);
     }
     if (try2h) {   // no TMA epilogue for this shape: single-CTA halo kernel with the same box map
         if (BN == 128) return launch_conv_halo<128>(P, A, Bm, O, tiles, st);
