@@ -136,7 +136,7 @@ struct TcWgrad {
 
 static constexpr int kThreads = 192;
 static constexpr int kWgThreads = 320;        // wgrad kernels: producer, MMA, 4 epilogue, 4 bias-sum warps
-static constexpr int kConvThreads = 320;      // producer, MMA, 8 epilogue warps
+
 static constexpr int kConvTcEpi = 16;         // k_conv_tc: epilogue warps of the store-warp (DMA) epilogues
 static constexpr int kConvTcThreads = (2 + kConvTcEpi + 1) * 32;   // producer, MMA, 16 epilogue warps, store warp
 static constexpr int kConv2Threads = 352;     // k_conv_tc2: producer, MMA, 8 epilogue warps, store warp
@@ -1495,7 +1495,7 @@ static constexpr int kPrBMax = 7 * 4 * 2048;          // 7 rows x 4 pairs x 2 ch
 static constexpr int kPrOutBufs = 6;
 static constexpr int kPrSmem = kPrStages * kPrPatch + kPrBMax + kPrOutBufs * kOutStage + 1024 + 256;
 
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kConv2Threads, 1)
     k_conv_pair(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmO, const TcConv P) {
     constexpr int BN = 64;
@@ -1509,13 +1509,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint64_t *tfull = empty + kPrStages;
     uint64_t *tempty = tfull + 2;
     uint64_t *bfull = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(bfull + 1);
+    uint64_t *rbar = bfull + 1, *gdone = rbar + kPrOutBufs;   // store-warp ring: buffer free / combined
+    uint32_t *tslot = (uint32_t *)(gdone + kPrOutBufs);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KY = P.k, NPR = (P.k + 1) / 2, s = P.a_mul;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPrStages; ++i) { ptx::mbar_init(full + i, 1); ptx::mbar_init(empty + i, 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); }
         ptx::mbar_init(bfull, 1);
+        for (int i = 0; i < kPrOutBufs; ++i) { ptx::mbar_init(rbar + i, 1); ptx::mbar_init(gdone + i, 8); }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmP);
         ptx::prefetch_tmap(&tmW);
@@ -1595,7 +1597,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
         }
     } else {
-        conv_epilogue_tma<BN, 8, kPrOutBufs>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2);
+        if (warp == 10) {   // store warp
+            if (lane == 0) conv_store_dma<BN, kPrOutBufs>(P, &tmO, sO, nullptr, rbar, gdone);
+        } else {
+            conv_epilogue_tma<BN, 8, kPrOutBufs, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, nullptr, rbar, gdone);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -3704,7 +3710,7 @@ static bool conv_pair(TcConv &P, const View &in, const void *w, int w_rows, cuda
     P.tma_out = 1;
     if (!smem_attr((const void *)k_conv_pair, kPrSmem)) return false;
     const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
-    return launch_pdl(k_conv_pair, grid, kConvThreads, kPrSmem, st, Pm, Wm, O, P);
+    return launch_pdl(k_conv_pair, grid, kConv2Threads, kPrSmem, st, Pm, Wm, O, P);
 }
 
 // FP of an 8-channel-input conv through the im2col kernel; false = shape not taken.
