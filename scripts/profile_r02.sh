@@ -21,7 +21,7 @@ ncu -i gpurun_out/${tag}_traffic_c4.ncu-rep --page raw --csv > gpurun_out/${tag}
 rm -f gpurun_out/${tag}_traffic_c4.ncu-rep
 python scripts/make_traffic.py gpurun_out/${tag}_traffic.json gpurun_out/${tag}_traffic_c4.raw.csv > /dev/null
 # --set full of a few launches of the top kernels
-for k in "k_conv_tc<.int.256, .int.64, .int.8>:20:3" "k_conv_tc2<.int.256>:20:3" "k_wgrad_tc<.int.128>:20:3" \
+for k in "k_conv_tc<.int.256, .int.64, .int.8>:20:3" "k_conv_tc2<.int.256>:20:3" "k_wgrad_tc<.int.256>:20:3" "k_bneck_fwd:2:2" \
          "k_dwgrad_pw<.int.256, .int.64>:4:2" "k_dwgrad_pw<.int.64, .int.256>:4:2" "k_conv_pair:1:1"; do
   IFS=: read kre skip cnt <<< "$k"
   name=$(echo "$kre" | tr -dc 'a-z0-9_')
