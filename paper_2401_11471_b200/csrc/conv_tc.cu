@@ -70,7 +70,7 @@ struct TcConv {
     int pat_w, pat_h, pat_ox, pat_oy;   // im2col kernel: input patch per tile (pixels) and its offset
     uint32_t fd_nt[2], fd_tx[2], fd_ty[2];   // fast division by n_tiles, tiles_x, tiles_y (mul, shift)
     int cta2;              // 1: CTA-pair kernel (k_conv_tc2): tile = 2 * pair + CTA rank, m_tiles rounded up to even
-    int warp_epi;          // per-warp epilogue boxes (k_conv_tc deep ring): maps O / G / X have box (64, bw, bh)
+    int warp_epi;          // unused (round-1 per-warp epilogue boxes), always 0
     // tile index -> (n tile, tile column, tile row, image); n tiles vary fastest.  CTA pairs: the two
     // CTAs of a pair take consecutive pixel tiles of the same n tile (an odd last tile decodes to
     // image B: fully out of bounds for every TMA load / store).
@@ -460,138 +460,6 @@ __device__ __forceinline__ void conv_store_dma(const TcConv &P, const CUtensorMa
     bulk_wait_all();
 }
 
-// Per-warp FP epilogue (small-K 1x1 convolutions, P.warp_epi): no block-wide barrier.  Warp
-// (q, hh) owns the tile's pixels 32q .. 32q+31 (TMEM lane quarter q) and the 64-channel groups
-// g == hh (mod 2) of every tile; each group it loads (residual), combines and stores as ONE box of
-// its own 32 pixels x 64 channels (4 KB, tensor maps with box (64, bw, bh) = (64, min(TW, 32),
-// max(1, 32 / TW))), in a private ring of NBW 4 KB buffers with its own mbarriers: eight independent
-// load -> combine -> store pipelines per SM instead of one pipeline that synchronises eight warps
-// per 64-channel group.  Batch-folded tiles (NBt > 1) do not take this path.
-template <int BN, int NBW>
-__device__ __forceinline__ void conv_epilogue_tma_w(const TcConv &P, const CUtensorMap *tmO, uint32_t tmem,
-                                                    uint64_t *tfull, uint64_t *tempty, uint8_t *stage_out, int warp,
-                                                    int lane, const CUtensorMap *tmR, uint64_t *rbar) {
-    constexpr int G = BN / 64;                        // 64-channel groups per tile
-    const int num_tiles = P.m_tiles * P.n_tiles;
-    const int q = warp & 3, hh = (warp - 2) >> 2, wi = warp - 2;
-    const bool l0 = lane == 0;
-    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-    const int m0 = q * 32, my0 = m0 >> P.tw_log2, mx0 = m0 & ((1 << P.tw_log2) - 1);
-    uint8_t *ring = stage_out + wi * NBW * 4096;
-    uint64_t *bars = rbar + wi * NBW;
-    const bool rt = P.has_res && P.tma_res && tmR;
-    // this warp's items: (tile, group g) for the CTA's tiles, g = hh, hh + 2, ... < the tile's groups
-    auto ngrp = [&](int tile2) {
-        int nt2, tx2, ty2, b2;
-        P.decode(tile2, nt2, tx2, ty2, b2);
-        const int left = P.n_out - nt2 * BN;
-        return left >= BN ? G : (left + 63) / 64;
-    };
-    int lt = blockIdx.x, lg = hh;                     // next residual item to load (lane 0)
-    auto skip_empty = [&]() {
-        while (lt < num_tiles && lg >= ngrp(lt)) { lg = hh; lt += gridDim.x; }
-    };
-    auto res_load = [&](int slot) {
-        int nt2, tx2, ty2, b2;
-        P.decode(lt, nt2, tx2, ty2, b2);
-        ptx::mbar_arrive_expect_tx(bars + slot, 4096);
-        ptx::tma_load_4d(ring + slot * 4096, tmR, bars + slot, nt2 * BN + lg * 64, tx2 * P.TW + mx0,
-                         P.out_a + ty2 * P.TH + my0 - P.res.base, b2);
-        lg += 2;
-        skip_empty();
-    };
-    int lslot = 0;
-    if (rt && l0) {
-        skip_empty();
-        for (int i = 0; i < NBW - 1 && lt < num_tiles; ++i) { res_load(lslot); lslot = lslot + 1 == NBW ? 0 : lslot + 1; }
-    }
-    int acc = 0, sbuf = 0;
-    uint32_t aphase = 0, rphases = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int nt, tx, ty, b;
-        P.decode(tile, nt, tx, ty, b);
-        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
-        const int ng = ngrp(tile);
-        ptx::mbar_wait(tfull + acc, aphase);
-        ptx::tc_fence_after();
-#pragma unroll 1
-        for (int grp = hh; grp < ng; grp += 2) {
-            const int nb = n0 + grp * 64;
-            uint32_t v[64];
-            ptx::tmem_ld32(tq + acc * BN + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-            ptx::tmem_ld32(tq + acc * BN + grp * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-            uint4 pb[8], pe[8], pr[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int n = nb + c * 8;
-                const bool in = n < P.n_out;
-                pb[c] = P.epi != 0 && in ? *reinterpret_cast<const uint4 *>(P.bias + n) : make_uint4(0, 0, 0, 0);
-                pe[c] = P.epi == 2 && in ? *reinterpret_cast<const uint4 *>(P.beta + n) : make_uint4(0, 0, 0, 0);
-                pr[c] = make_uint4(0, 0, 0, 0);
-            }
-            const bool ragged = nb + 64 > P.c_real;
-            const uint32_t buf = ptx::smem_u32(ring + sbuf * 4096 + lane * 128);
-            if (!rt && l0) bulk_wait_read_n<NBW - 1>();   // this buffer's previous store has read it
-            __syncwarp();
-            ptx::tmem_ld_wait();
-            if (rt) {
-                ptx::mbar_wait(bars + sbuf, (rphases >> sbuf) & 1);
-                rphases ^= 1u << sbuf;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) pr[c] = ld_shared_v4(buf + ((c ^ (lane & 7)) << 4));
-            }
-            if (!ragged && P.epi == 1 && !P.has_res) epi_fast_r<64, 1, false>(P.relu, v, pb, pe, pr, buf, 0, lane);
-            else if (!ragged && P.epi == 2 && !P.has_res) epi_fast_r<64, 2, false>(P.relu, v, pb, pe, pr, buf, 0, lane);
-            else if (!ragged && P.epi == 2 && P.has_res) epi_fast_r<64, 2, true>(P.relu, v, pb, pe, pr, buf, 0, lane);
-            else if (!ragged && P.epi == 1 && P.has_res) epi_fast_r<64, 1, true>(P.relu, v, pb, pe, pr, buf, 0, lane);
-            else if (!ragged && P.epi == 0 && !P.has_res) epi_fast_r<64, 0, false>(P.relu, v, pb, pe, pr, buf, 0, lane);
-            else {
-                const float lo = P.relu ? 0.f : -INFINITY;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const int n = nb + c * 8;
-                    const uint16_t *bh = reinterpret_cast<const uint16_t *>(&pb[c]);
-                    const uint16_t *eh = reinterpret_cast<const uint16_t *>(&pe[c]);
-                    const uint16_t *rh = reinterpret_cast<const uint16_t *>(&pr[c]);
-                    float f[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float x = __uint_as_float(v[c * 8 + j]);
-                        const bool live = !ragged || n + j < P.c_real;
-                        if (P.epi == 1) x += live ? bf2f(bh[j]) : 0.f;
-                        else if (P.epi == 2) x = live ? bf2f(bh[j]) * x + bf2f(eh[j]) : 0.f;
-                        x += bf2f(rh[j]);
-                        f[j] = fmaxf(x, lo);
-                    }
-                    uint4 o;
-                    o.x = pack2(f[0], f[1]); o.y = pack2(f[2], f[3]); o.z = pack2(f[4], f[5]); o.w = pack2(f[6], f[7]);
-                    st_shared_v4(buf + ((c ^ (lane & 7)) << 4), o);
-                }
-            }
-            fence_async_smem();
-            __syncwarp();
-            if (l0) {
-                if (!(P.dbg & 1)) {
-                    tma_store_4d(tmO, ring + sbuf * 4096, nb, P.o_col0 + P.o_stride * (xg0 + mx0),
-                                 P.o_row0 + P.o_stride * (yg0 + my0) - P.out.base, b);
-                    bulk_commit();
-                }
-                if (rt && lt < num_tiles) {   // next residual into the buffer of the previous item
-                    bulk_wait_read_n<1>();       // (its store, the one before this item's, has read it)
-                    res_load(lslot);
-                    lslot = lslot + 1 == NBW ? 0 : lslot + 1;
-                }
-            }
-            __syncwarp();
-            sbuf = sbuf + 1 == NBW ? 0 : sbuf + 1;
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (l0) P.tempty_arrive(tempty + acc);
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
-    }
-    if (l0) bulk_wait_all();
-}
 
 // dgrad epilogue through TMA (unit output stride): per 64-channel group the delta tile of the
 // conv input (and, when its producer applies ReLU, the activation tile) is TMA-loaded into
@@ -848,111 +716,6 @@ __device__ __forceinline__ void conv_store_dma_dg(const TcConv &P, const CUtenso
     bulk_wait_all();
 }
 
-// Per-warp dgrad epilogue (small-K 1x1 convolutions, P.warp_epi): as conv_epilogue_tma_w, each warp
-// combines its own 32 pixels x 64 channels per group: the old delta / the fused residual addend
-// and the gating activation are TMA-loaded as 4 KB boxes into a private ring of NS 8 KB slots
-// (NS-1 items ahead), delta = gate(act) * (old + acc) is written in place and TMA-stored.
-template <int BN, int NS>
-__device__ __forceinline__ void conv_epilogue_tma_dg_w(const TcConv &P, const CUtensorMap *tmO, const CUtensorMap *tmG,
-                                                       uint32_t tmem, uint64_t *tfull, uint64_t *tempty,
-                                                       uint8_t *stage_out, uint64_t *ebar, int warp, int lane,
-                                                       const CUtensorMap *tmX) {
-    constexpr int G = BN / 64;
-    const int num_tiles = P.m_tiles * P.n_tiles;
-    const int q = warp & 3, hh = (warp - 2) >> 2, wi = warp - 2;
-    const bool l0 = lane == 0;
-    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-    const int m0 = q * 32, my0 = m0 >> P.tw_log2, mx0 = m0 & ((1 << P.tw_log2) - 1);
-    uint8_t *ring = stage_out + wi * NS * 8192;
-    uint64_t *bars = ebar + wi * NS;
-    const bool dload = !P.dg_write || (P.dg_add && tmX);
-    const CUtensorMap *tmD = P.dg_write ? tmX : tmO;
-    const uint32_t ebytes = (dload ? 4096u : 0u) + (P.gate ? 4096u : 0u);
-    auto ngrp = [&](int tile2) {
-        int nt2, tx2, ty2, b2;
-        P.decode(tile2, nt2, tx2, ty2, b2);
-        return min(G, (P.n_out - nt2 * BN + 63) / 64);
-    };
-    int it = blockIdx.x, ig = hh;                     // next item to issue (lane 0)
-    auto skip_empty = [&]() {
-        while (it < num_tiles && ig >= ngrp(it)) { ig = hh; it += gridDim.x; }
-    };
-    auto issue = [&](int slot) {
-        int nt2, tx2, ty2, b2;
-        P.decode(it, nt2, tx2, ty2, b2);
-        const int nb = nt2 * BN + ig * 64;
-        const int cx = P.o_col0 + P.o_stride * (tx2 * P.TW + mx0);
-        const int cy = P.o_row0 + P.o_stride * (P.out_a + ty2 * P.TH + my0);
-        uint8_t *bd = ring + slot * 8192;
-        ptx::mbar_arrive_expect_tx(bars + slot, ebytes);
-        if (dload) ptx::tma_load_4d(bd, tmD, bars + slot, nb, cx, cy - (P.dg_write ? P.add.base : P.out.base), b2);
-        if (P.gate) ptx::tma_load_4d(bd + 4096, tmG, bars + slot, nb, cx, cy - P.act.base, b2);
-        ig += 2;
-        skip_empty();
-    };
-    int islot = 0;
-    if (l0) {
-        skip_empty();
-        for (int i = 0; i < NS - 1 && it < num_tiles; ++i) { issue(islot); islot = islot + 1 == NS ? 0 : islot + 1; }
-    }
-    int acc = 0, pi = 0;
-    uint32_t aphase = 0, ephase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int nt, tx, ty, b;
-        P.decode(tile, nt, tx, ty, b);
-        const int yg0 = P.out_a + ty * P.TH, xg0 = tx * P.TW, n0 = nt * BN;
-        const int ng = ngrp(tile);
-        ptx::mbar_wait(tfull + acc, aphase);
-        ptx::tc_fence_after();
-#pragma unroll 1
-        for (int grp = hh; grp < ng; grp += 2) {
-            const int nb = n0 + grp * 64;
-            uint32_t v[64];
-            ptx::tmem_ld32(tq + acc * BN + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-            ptx::tmem_ld32(tq + acc * BN + grp * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-            if (l0 && it < num_tiles) {        // NS-1 items ahead, into the slot the previous item used
-                bulk_wait_read_n<0>();         // (its store, the latest committed, has read it)
-                issue(islot);
-                islot = islot + 1 == NS ? 0 : islot + 1;
-            }
-            __syncwarp();
-            ptx::tmem_ld_wait();
-            ptx::mbar_wait(bars + pi, (ephase >> pi) & 1);
-            ephase ^= 1u << pi;
-            const uint32_t rowD = ptx::smem_u32(ring + pi * 8192) + lane * 128, rowG = rowD + 4096;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const uint32_t off = (uint32_t)((c ^ (lane & 7)) << 4);
-                const uint4 dd = dload ? ld_shared_v4(rowD + off) : make_uint4(0, 0, 0, 0);
-                const uint4 gg = P.gate ? ld_shared_v4(rowG + off) : make_uint4(0, 0, 0, 0);
-                const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
-                uint32_t o[4];
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const float x0 = hadd_lo(dw[h], __uint_as_float(v[c * 8 + 2 * h]));
-                    const float x1 = hadd_hi(dw[h], __uint_as_float(v[c * 8 + 2 * h + 1]));
-                    o[h] = pack2_act<false>(x0, x1);
-                    if (P.gate) o[h] &= relu_mask2(gw[h]);   // gate-on-write: delta = [act > 0] (delta + acc)
-                }
-                st_shared_v4(rowD + off, make_uint4(o[0], o[1], o[2], o[3]));
-            }
-            fence_async_smem();
-            __syncwarp();
-            if (l0) {
-                tma_store_4d(tmO, ring + pi * 8192, nb, P.o_col0 + P.o_stride * (xg0 + mx0),
-                             P.o_row0 + P.o_stride * (yg0 + my0) - P.out.base, b);
-                bulk_commit();
-            }
-            __syncwarp();
-            pi = pi + 1 == NS ? 0 : pi + 1;
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (l0) P.tempty_arrive(tempty + acc);
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
-    }
-    if (l0) bulk_wait_all();
-}
 
 // Epilogue warps (4 warps = 128 TMEM lanes = 128 pixels of the tile): tcgen05.ld the
 // accumulator in 32-column chunks, apply the fused epilogue, 16-byte bf16 stores.
@@ -3523,15 +3286,13 @@ static bool conv_launch(TcConv &P, const View &in, const void *w, int w_rows, in
     P.m_tiles = (P.B + NB - 1) / NB * P.tiles_x * P.tiles_y;
     tile_div_init(P);
     // small-K layers (one or two K-steps per tile: the 1x1 convolutions of ResNet's bottleneck ends)
-    // are bound by the epilogue's tile traffic: the deep staging ring and per-warp epilogue boxes
+    // are bound by the epilogue's tile traffic: the deep (8-buffer) staging ring.  (Per-warp TMA epilogue
+    // boxes, round 1, measured slower than the store-warp ring -- profiles/r02/r02e_epilogue_w_timeline_
+    // cycles.txt -- and were removed.)
     static const int deep = env_int("LRCNN_DEEP_RING", 1);
     const bool deep_ring = deep && !try2h && P.k_steps <= 2 && BN >= 128 && KC == 64;
-    // the per-warp epilogues (conv_epilogue_tma_w / _dg_w) measured slower than the store-warp ring
-    // (profiles/r02/r02e_epilogue_w_timeline_cycles.txt): k_conv_tc always takes the latter
     P.warp_epi = 0;
-    if (P.mode == 0 && P.has_res && !(P.res.Cp == P.out.Cp && P.n_out % 64 == 0 && aligned16(P.res.p)))
-        P.warp_epi = 0;   // the per-warp epilogue takes the residual through TMA only
-    const int EW = P.warp_epi ? std::min(P.TW, 32) : P.TW, EH = P.warp_epi ? 32 / EW : P.TH;   // epilogue box
+    const int EW = P.TW, EH = P.TH;   // epilogue box
     if (try2h ? !encode_view(&A, in, P.B, HaloGeom<3>::kPitch, HaloGeom<3>::kRows)
               : !encode_view(&A, in, P.B, P.TW, P.TH, P.a_mul, KC, NB))
         return false;
