@@ -1949,7 +1949,7 @@ struct DwCfg {
     static constexpr uint32_t kD2Col = kD1Bufs * CI;
     static constexpr uint32_t kTmemCols = kD2Col + kMT * CI <= 256 ? 256 : 512;
 };
-static constexpr int kDwThreads = 448;   // producer, MMA, 8 epilogue warps, 4 bias-sum warps
+static constexpr int kDwThreads = 480;   // producer, MMA, 8 epilogue warps, 4 bias-sum warps, store warp
 
 template <int CI, int CO>
 __global__ void __launch_bounds__(kDwThreads, 1)
@@ -1969,7 +1969,8 @@ __global__ void __launch_bounds__(kDwThreads, 1)
     uint64_t *ebar = tempty + 2;                     // epilogue staging loads (2)
     uint64_t *wbar = ebar + 2;
     uint64_t *d2full = wbar + 1;
-    uint32_t *tslot = (uint32_t *)(d2full + 1);
+    uint64_t *gdone = d2full + 1;                    // staging buffer combined (8 epilogue warps) -> store warp
+    uint32_t *tslot = (uint32_t *)(gdone + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool bias = P.db != nullptr;
     if (threadIdx.x == 0) {
@@ -1977,6 +1978,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 8); ptx::mbar_init(ebar + i, 1); }
         ptx::mbar_init(wbar, 1);
         ptx::mbar_init(d2full, 1);
+        for (int i = 0; i < 2; ++i) ptx::mbar_init(gdone + i, 8);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmD);
         ptx::prefetch_tmap(&tmX);
@@ -2080,7 +2082,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
             ptx::mbar_arrive_expect_tx(ebar + buf, dload ? (uint32_t)kOutStage : 0u);
             if (dload) ptx::tma_load_4d(sO + buf * kOutStage, tmL, ebar + buf, g2 * 64, x2, y2 - lbase, b2);
         };
-        if (leader && p0 < p1) issue(p0, 0, 0);
+        (void)leader;
         for (int pt = p0; pt < p1; ++pt) {
             int x0, y0, b;
             tile_xy(pt, x0, y0, b);
@@ -2091,13 +2093,6 @@ __global__ void __launch_bounds__(kDwThreads, 1)
             for (int g = 0; g < Cfg::kXB; ++g) {
                 uint32_t v[32];
                 ptx::tmem_ld32(tq + acc * CI + g * 64 + hh * 32, v);
-                if (leader) {
-                    const int pn = g + 1 < Cfg::kXB ? pt : pt + 1, gn = g + 1 < Cfg::kXB ? g + 1 : 0;
-                    if (pn < p1) {
-                        bulk_wait_read_n<0>();   // the store of the previous item (buffer sb ^ 1) has read it
-                        issue(pn, gn, sb ^ 1);
-                    }
-                }
                 ptx::tmem_ld_wait();
                 ptx::mbar_wait(ebar + sb, (ephase >> sb) & 1);
                 ephase ^= 1u << sb;
@@ -2121,11 +2116,8 @@ __global__ void __launch_bounds__(kDwThreads, 1)
                     st_shared_v4(row + off, make_uint4(o[0], o[1], o[2], o[3]));
                 }
                 fence_async_smem();
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                if (leader) {
-                    tma_store_4d(&tmO, sO + sb * kOutStage, g * 64, x0, y0 - P.dx.base, b);
-                    bulk_commit();
-                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(gdone + sb);   // the store warp takes the buffer from here
                 sb ^= 1;
             }
             ptx::tc_fence_before();
@@ -2134,7 +2126,6 @@ __global__ void __launch_bounds__(kDwThreads, 1)
             if (++stage == S) { stage = 0; phase ^= 1; }
             if (++acc == D1B) { acc = 0; aphase ^= 1; }
         }
-        if (leader) bulk_wait_all();
         // the wgrad accumulator of this CTA's tiles: reduced once into the fp32 gradient
         if (p0 < p1) {
             ptx::mbar_wait(d2full, 0);
@@ -2166,6 +2157,42 @@ __global__ void __launch_bounds__(kDwThreads, 1)
                 }
                 if (P.dg && live) atomicAdd(P.dg + co, gdot);
             }
+        }
+    } else if (warp == 14) {
+        // store warp: item k = (tile, 64-channel group) of this CTA's run uses staging buffer k % 2; the
+        // old delta / the residual addend of item k is TMA-loaded into it, the 8 epilogue warps combine it
+        // (gdone), the TMA store follows and, once it has read the buffer, item k + 2 is loaded
+        if (lane == 0) {
+            const bool dload = !P.write || P.dg_add;
+            const CUtensorMap *tmL = P.write ? &tmA : &tmO;
+            const int lbase = P.write ? P.add.base : P.dx.base;
+            int lpt = p0, lg = 0;   // next item to load
+            auto issue = [&](int buf) {
+                if (lpt >= p1) return;
+                int x2, y2, b2;
+                tile_xy(lpt, x2, y2, b2);
+                ptx::mbar_arrive_expect_tx(ebar + buf, dload ? (uint32_t)kOutStage : 0u);
+                if (dload) ptx::tma_load_4d(sO + buf * kOutStage, tmL, ebar + buf, lg * 64, x2, y2 - lbase, b2);
+                if (++lg == Cfg::kXB) { lg = 0; ++lpt; }
+            };
+            issue(0);
+            issue(1);
+            int sb = 0;
+            uint32_t gph = 0;
+            for (int pt = p0; pt < p1; ++pt) {
+                int x0, y0, b;
+                tile_xy(pt, x0, y0, b);
+                for (int g = 0; g < Cfg::kXB; ++g) {
+                    ptx::mbar_wait(gdone + sb, (gph >> sb) & 1);
+                    gph ^= 1u << sb;
+                    tma_store_4d(&tmO, sO + sb * kOutStage, g * 64, x0, y0 - P.dx.base, b);
+                    bulk_commit();
+                    bulk_wait_read0();
+                    issue(sb);
+                    sb ^= 1;
+                }
+            }
+            bulk_wait_all();
         }
     } else if (bias) {
         // bias / beta gradient: column sums of the delta tiles (channel pairs, SWIZZLE_128B boxes)
