@@ -2937,8 +2937,9 @@ __global__ void __launch_bounds__(kWiThreads, 1)
 static constexpr int kRbSA = 3;
 static constexpr int kRbB = 9 * 64 * 128;                                    // 72 KB
 static constexpr int kRbSmem = kRbSA * HaloGeom<3>::kABytes + kRbB + 4 * kOutStage + 1024 + 512;
+static constexpr int kRbThreads = 224;   // producer, MMA, 4 epilogue warps, store warp
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kRbThreads, 1)
     k_conv_halo_rb(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG, const TcConv P) {
     constexpr int BN = 64, KH = 3, taps = 9, SA = kRbSA;
@@ -2953,15 +2954,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *bfull = emptyA + SA;
     uint64_t *tfull = bfull + 1;
     uint64_t *tempty = tfull + 2;
-    uint64_t *ebar = tempty + 2;
-    uint32_t *tslot = (uint32_t *)(ebar + 2);
+    uint64_t *ebar = tempty + 2;                     // staging ring [4] (FP) / pairs [2] (dgrad), gdone [4]
+    uint32_t *tslot = (uint32_t *)(ebar + 8);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < SA; ++i) { ptx::mbar_init(fullA + i, 1); ptx::mbar_init(emptyA + i, 1); }
         ptx::mbar_init(bfull, 1);
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(tfull + i, 1); ptx::mbar_init(tempty + i, 4); }
-        ptx::mbar_init(ebar, 1);
-        ptx::mbar_init(ebar + 1, 1);
+        for (int i = 0; i < 8; ++i) ptx::mbar_init(ebar + i, i < 4 ? 1 : 4);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -3025,10 +3025,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
+    } else if (warp == 6) {   // store warp
+        if (lane == 0) {
+            if (P.mode == 0) conv_store_dma<BN, 4>(P, &tmO, sO, nullptr, ebar, ebar + 4);
+            else conv_store_dma_dg<BN, 2>(P, &tmO, &tmG, nullptr, sO, ebar, ebar + 4);
+        }
     } else if (P.mode == 0) {
-        conv_epilogue_tma<BN>(P, &tmO, tmem, tfull, tempty, sO, warp, lane);
+        conv_epilogue_tma<BN, 4, 4, true>(P, &tmO, tmem, tfull, tempty, sO, warp, lane, 2, nullptr, ebar, ebar + 4);
     } else {
-        conv_epilogue_tma_dg2<BN>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane);
+        conv_epilogue_tma_dg2<BN, 4, 2, true>(P, &tmO, &tmG, tmem, tfull, tempty, sO, ebar, warp, lane, 2, nullptr, ebar + 4);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -3247,7 +3252,7 @@ static bool conv_halo_rb(TcConv &P, const View &in, const void *w, int w_rows, i
     P.tma_dg = P.mode == 1;
     if (!smem_attr((const void *)k_conv_halo_rb, kRbSmem)) return false;
     const int grid = P.m_tiles < num_sms() ? P.m_tiles : num_sms();
-    return launch_pdl(k_conv_halo_rb, grid, kThreads, kRbSmem, st, A, Bm, O, G, P);
+    return launch_pdl(k_conv_halo_rb, grid, kRbThreads, kRbSmem, st, A, Bm, O, G, P);
 }
 
 // Launch one implicit-GEMM conv over the output grid rows [P.out_a, P.out_b) x cols [0, P.Wo).
