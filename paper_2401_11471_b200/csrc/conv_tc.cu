@@ -1684,12 +1684,12 @@ __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, 
 // Bias-sum warps (128 threads): thread t sums output-channel PAIR cp = t % np (one 32-bit load per
 // row of the SWIZZLE_128B delta tile, 64-channel boxes kABytes apart) over the rows r0 + step * (g +
 // ngroups * j), g = t / np: half the loads of a column-per-thread sum and twice the parallelism.
-__device__ __forceinline__ float2 db_pair_sum(uint32_t base, int cp, int g, int ngroups, int r0, int step) {
-    const uint32_t box = (uint32_t)(cp >> 5) * kABytes, chunk = (uint32_t)((cp & 31) >> 2), cofs = (uint32_t)((cp & 3) * 4);
+__device__ __forceinline__ float2 db_pair_sum(uint32_t base, int cp, int g, int ngroups, int r0, int step, int rows = 128) {
+    const uint32_t box = (uint32_t)(cp >> 5) * (uint32_t)(rows * 128), chunk = (uint32_t)((cp & 31) >> 2), cofs = (uint32_t)((cp & 3) * 4);
     float a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f};
     int i = 0;
 #pragma unroll 4
-    for (int r = r0 + step * g; r < 128; r += step * ngroups, ++i) {
+    for (int r = r0 + step * g; r < rows; r += step * ngroups, ++i) {
         uint32_t w;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(base + box + r * 128 + ((chunk ^ (r & 7)) << 4) + cofs));
         a[i & 1] += bf_lo(w);
@@ -1698,22 +1698,26 @@ __device__ __forceinline__ float2 db_pair_sum(uint32_t base, int cp, int g, int 
     return make_float2(a[0] + a[1], b[0] + b[1]);
 }
 
-template <int BN>
+// KP = pixels per pipeline stage (the K of one stage): 128, or 64 for N = 256 items, whose 96 KB
+// stages would leave only two in the ring (one load in flight while the other is consumed: the
+// tensor pipe starved at ~35 %); 64-pixel stages keep three loads in flight.
+template <int BN, int KP = 128>
 struct WgCfg {
     // B operand (shifted band input): BN/KB boxes of KB channels (KB = 64, SWIZZLE_128B; or
     // KB = BN = 16, SWIZZLE_32B for small-channel inputs)
     static constexpr int KB = BN < 64 ? BN : 64;
-    static constexpr int kBBox = 128 * KB * 2;
-    static constexpr int kStageBytes = kWgA + (BN / KB) * kBBox;
+    static constexpr int kA = 2 * KP * 128;                  // delta: two 64-channel MN chunks
+    static constexpr int kBBox = KP * KB * 2;
+    static constexpr int kStageBytes = kA + (BN / KB) * kBBox;
     static constexpr int kStages = (192 * 1024) / kStageBytes > 12 ? 12 : (192 * 1024) / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
     static constexpr uint32_t kTmemCols = 2 * BN;
 };
 
-template <int BN>
+template <int BN, int KP = 128>
 __global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad_tc(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, const TcWgrad P) {
-    using Cfg = WgCfg<BN>;
+    using Cfg = WgCfg<BN, KP>;
     constexpr int S = Cfg::kStages;
     constexpr int SB = Cfg::kStageBytes;
     extern __shared__ uint8_t smem_raw[];
@@ -1765,10 +1769,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     uint8_t *st = smem + stage * SB;
                     ptx::mbar_arrive_expect_tx(full + stage, SB);
                     ptx::tma_load_4d(st, &tmD, full + stage, cot * 128, x0, y0 - P.dy_base, b);
-                    ptx::tma_load_4d(st + kABytes, &tmD, full + stage, cot * 128 + 64, x0, y0 - P.dy_base, b);
+                    ptx::tma_load_4d(st + Cfg::kA / 2, &tmD, full + stage, cot * 128 + 64, x0, y0 - P.dy_base, b);
 #pragma unroll
                     for (int h = 0; h < BN / Cfg::KB; ++h)
-                        ptx::tma_load_4d(st + kWgA + h * Cfg::kBBox, &tmX, full + stage, cit * BN + h * Cfg::KB,
+                        ptx::tma_load_4d(st + Cfg::kA + h * Cfg::kBBox, &tmX, full + stage, cit * BN + h * Cfg::KB,
                                          x0 * P.s - P.pad + kx, y0 * P.s - P.pad + ky - P.x_base, b);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -1777,9 +1781,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     } else if (warp == 1) {
         {   // whole warp: tcgen05.mma / commit are elect.sync-issued once per warp
             constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
-            const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), kABytes, 1024);
-            const uint64_t dB = Cfg::KB == 64 ? ptx::smem_desc_sw128(ptx::smem_u32(smem + kWgA), kABytes, 1024)
-                                              : ptx::smem_desc(ptx::smem_u32(smem + kWgA), 4096, 8 * Cfg::KB * 2, 6);
+            const uint64_t dA = ptx::smem_desc_sw128(ptx::smem_u32(smem), Cfg::kA / 2, 1024);
+            const uint64_t dB = Cfg::KB == 64 ? ptx::smem_desc_sw128(ptx::smem_u32(smem + Cfg::kA), Cfg::kBBox, 1024)
+                                              : ptx::smem_desc(ptx::smem_u32(smem + Cfg::kA), 4096, 8 * Cfg::KB * 2, 6);
             const uint32_t hiA = (uint32_t)(dA >> 32), hiB = (uint32_t)(dB >> 32);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
@@ -1798,7 +1802,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     const uint32_t b0 = (uint32_t)dB + stage * (SB >> 4);
                     if (ptx::elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)
+                        for (int kk = 0; kk < KP / 16; ++kk)
                             ptx::umma_bf16_1t(d, a0 + kk * 128, hiA, b0 + kk * (Cfg::KB == 64 ? 128 : 2 * Cfg::KB), hiB, idesc,
                                               (pt != p0 || kk != 0) ? 1u : 0u);
                         ptx::umma_commit_1t(empty + stage);
@@ -1896,7 +1900,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             float2 sum = make_float2(0.f, 0.f);
             for (int pt = p0; pt < p1; ++pt) {
                 ptx::mbar_wait(full + stage, phase);
-                const float2 v = db_pair_sum(ptx::smem_u32(smem + stage * SB), cp, g, 2, part, nparts);
+                const float2 v = db_pair_sum(ptx::smem_u32(smem + stage * SB), cp, g, 2, part, nparts, KP);
                 sum.x += v.x;
                 sum.y += v.y;
                 __syncwarp();
@@ -3169,13 +3173,24 @@ static void pick_tile(int rows, int W, int s, int &TW, int &TH) {
     }
 }
 
+// a 64-pixel rectangle TW x TH (TW*TH = 64, TW*s <= 256) minimising padded pixels
+static void pick_tile64(int rows, int W, int s, int &TW, int &TH) {
+    long best = -1;
+    for (int tw = 64; tw >= 4; tw >>= 1) {
+        int th = 64 / tw;
+        if (tw * s > 256 || th * s > 256) continue;
+        long cost = (long)((W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
+        if (best < 0 || cost < best) { best = cost; TW = tw; TH = th; }
+    }
+}
+
 // the same with batch folding: a 128-pixel tile of TW x TH x NB (NB images of a small map), the
 // shape with the fewest padded pixel slots (small maps: 7x7 -> 8x8x2 instead of 8x16x1)
-static void pick_tile_nb(int rows, int W, int s, int B, int &TW, int &TH, int &NB) {
+static void pick_tile_nb(int rows, int W, int s, int B, int &TW, int &TH, int &NB, int px = 128) {
     long best = -1;
-    for (int nb = 1; nb <= 16; nb <<= 1)
-        for (int tw = 128 / nb; tw >= 4; tw >>= 1) {
-            const int th = 128 / nb / tw;
+    for (int nb = 1; nb <= 16 && nb <= px / 4; nb <<= 1)
+        for (int tw = px / nb; tw >= 4; tw >>= 1) {
+            const int th = px / nb / tw;
             if (th < 1 || tw * s > 256 || th * s > 256) continue;
             const long cost = (long)((B + nb - 1) / nb) * nb * ((W + tw - 1) / tw) * tw * (long)((rows + th - 1) / th) * th;
             if (best < 0 || cost < best) { best = cost; TW = tw; TH = th; NB = nb; }
@@ -3627,12 +3642,12 @@ bool tc_conv_dgrad(const DgradArgs &a, cudaStream_t st) {
     return true;
 }
 
-template <int BN>
+template <int BN, int KP = 128>
 static bool launch_wgrad(const TcWgrad &P, const CUtensorMap &D, const CUtensorMap &X, cudaStream_t st) {
-    using Cfg = WgCfg<BN>;
-    if (!smem_attr((const void *)k_wgrad_tc<BN>, Cfg::kSmem)) return false;
+    using Cfg = WgCfg<BN, KP>;
+    if (!smem_attr((const void *)k_wgrad_tc<BN, KP>, Cfg::kSmem)) return false;
     int grid = P.items < num_sms() ? P.items : num_sms();
-    return launch_pdl(k_wgrad_tc<BN>, grid, kWgThreads, Cfg::kSmem, st, D, X, P);
+    return launch_pdl(k_wgrad_tc<BN, KP>, grid, kWgThreads, Cfg::kSmem, st, D, X, P);
 }
 
 template <int BN, int KW>
@@ -3867,6 +3882,14 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     int NB = 1;
     if (fold) pick_tile_nb(rows, dy.W, a.s, a.B, P.TW, P.TH, NB);
     else pick_tile(rows, dy.W, a.s, P.TW, P.TH);
+    // N = 256 items: 64-pixel stages (WgCfg KP) -- single-image 64-pixel tiles
+    static const int kp64_on = env_int("LRCNN_WG_KP64", 1);
+    const bool kp64 = kp64_on && env_int("LRCNN_WG_256", 1) && x.Cp >= 256 && x.Cp % 256 == 0;   // == BN 256
+    if (kp64) {
+        NB = 1;
+        if (fold) pick_tile_nb(rows, dy.W, a.s, a.B, P.TW, P.TH, NB, 64);
+        else pick_tile64(rows, dy.W, a.s, P.TW, P.TH);
+    }
     P.NB = NB;
     P.tiles_x = (dy.W + P.TW - 1) / P.TW;
     P.tiles_y = (rows + P.TH - 1) / P.TH;
@@ -3892,7 +3915,8 @@ bool tc_conv_wgrad(const WgradArgs &a, cudaStream_t st) {
     if (!encode_view(&X, x, a.B, P.TW, P.TH, a.s, BN < 64 ? BN : 64, NB)) return false;
     const bool ok = BN == 16 ? launch_wgrad<16>(P, D, X, st)
                   : BN == 64 ? launch_wgrad<64>(P, D, X, st)
-                  : BN == 128 ? launch_wgrad<128>(P, D, X, st) : launch_wgrad<256>(P, D, X, st);
+                  : BN == 128 ? launch_wgrad<128>(P, D, X, st)
+                  : kp64 ? launch_wgrad<256, 64>(P, D, X, st) : launch_wgrad<256>(P, D, X, st);
     if (ok && P.db) a.db_done = true;
     if (ok && P.dg) a.dg_done = true;
     return ok;
