@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(256) k_pool_bwd_tile8(PoolArgs A, int ny_max, 
 // 16-bit codes + dy in shared memory (invalid windows: code 0xffff); phase 2 gives a thread one
 // input row x column pair x 8 channels and masks dy with packed compares (vcmpeq2), no branches
 // on window validity.  A warp covers one input row, so the row-parity branch is warp-uniform.
-constexpr int kP3TR = 8, kP3TP = 16;   // input rows x column pairs per CTA
+constexpr int kP3TR = 16, kP3TP = 16;   // input rows x column pairs per CTA
 __device__ __forceinline__ uint32_t bf2_gt_mask(uint32_t a, uint32_t b) {
     uint32_t m;
     asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(a), "r"(b));
