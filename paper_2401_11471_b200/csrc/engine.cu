@@ -346,14 +346,25 @@ static lrcnn_status bneck_forward(Run &R, const Segment &S, int r, int i, int nw
         }
         const double wr = Bn * ((A.b2 - A.a2) * rbt + w1rows * rb1 + (write_t2 ? (A.b2 - A.a2) * (double)T2.W * T2.Cp * R.E : 0));
         const double rd = Bn * (A.b1 - A.a1) * rbt + (double)(c1.w_cnt + c2.w_cnt + c3.w_cnt) * R.E;
-        ProfScope ps(R, 0, fl, i * 8 + 0, rd + wr, wr);
-        ++P.launches;
-        if (!tc_bneck_fwd(A, R.st)) {
-            if (tc_take_error()) return fail(LRCNN_E_CUDA, "fused bottleneck launch failed at op " + std::to_string(i));
-            return fail(LRCNN_E_STATE, "fused bottleneck declined at op " + std::to_string(i));
+        bool declined = false;
+        {
+            ProfScope ps(R, 0, fl, i * 8 + 0, rd + wr, wr);
+            if (tc_bneck_fwd(A, R.st)) {
+                ++P.launches;
+                ++P.tc_launches;
+                CK(cudaGetLastError());
+            } else if (tc_take_error()) {
+                return fail(LRCNN_E_CUDA, "fused bottleneck launch failed at op " + std::to_string(i));
+            } else {
+                declined = true;
+            }
         }
-        ++P.tc_launches;
-        CK(cudaGetLastError());
+        if (declined) {   // a shape / alignment the fused kernel does not take: the three ops unfused
+            lrcnn_status st;
+            for (int k = 0; k < 3; ++k)
+                if ((st = op_forward(R, S, r, i + k)) != LRCNN_OK) return st;
+            return LRCNN_OK;
+        }
     }
     if (cap) {
         lrcnn_status st;
