@@ -13,6 +13,15 @@ full height and kept (Fig. 1; SPEC column-oracle S:204-261).
 Op semantics: a conv op computes
   t = relu?( epi(Conv(src)) + res ),  epi in {bias: +b, affine: gamma*c+beta, none}
 ReLU'(0) = 0 (SPEC.md:115).  Everything is fp64, NCHW.
+
+Training-mode BatchNorm (the paper names BN in FP, but excludes it
+from its analysis -- DESIGN.md reading R24): a "bn" op computes, per channel over the whole batch
+and map (M = B*H*W values; biased variance, eps = BN_EPS),
+  mean = sum(c)/M,  var = sum((c-mean)^2)/M,  xh = (c-mean)/sqrt(var+eps),
+  t = relu?( gamma*xh + beta + res )
+and its backward the textbook batch-statistics adjoint (da = gated dt):
+  dbeta = sum(da),  dgamma = sum(da*xh),
+  dc = gamma/sqrt(var+eps) * (da - dbeta/M - xh*dgamma/M),  dres = da.
 """
 import numpy as np
 
@@ -30,8 +39,9 @@ def out_hw(net):
         elif op["kind"] == "maxpool":
             shp.append((c, O.out_dim(h, op["p"], op["p"], op["k"], op["s"]),
                         O.out_dim(w, op["p"], op["p"], op["k"], op["s"])))
-        elif op["kind"] == "add":
-            assert shp[op["res"]] == (c, h, w)
+        elif op["kind"] == "add" or op["kind"] == "bn":
+            if op["kind"] == "add" or op.get("res", -1) >= 0:
+                assert shp[op["res"]] == (c, h, w)
             shp.append((c, h, w))
         else:
             raise ValueError(op["kind"])
@@ -75,6 +85,37 @@ def conv_op_bwd(op, prm, x, c, t, dt, pads, in_hw):
     return dx, dres, g
 
 
+BN_EPS = 1e-5   # DESIGN.md R24
+
+
+def bn_stats(c):
+    """Batch statistics of a full map c [B, C, H, W]: (mean, biased var) per channel."""
+    mean = c.mean(axis=(0, 2, 3))
+    var = ((c - mean[None, :, None, None]) ** 2).mean(axis=(0, 2, 3))
+    return mean, var
+
+
+def bn_apply(prm, c, mean, var, res, relu):
+    """t = relu?(gamma * (c - mean)/sqrt(var + eps) + beta + res) on any rows of c."""
+    xh = (c - mean[None, :, None, None]) / np.sqrt(var + BN_EPS)[None, :, None, None]
+    a = prm["gamma"][None, :, None, None] * xh + prm["beta"][None, :, None, None]
+    if res is not None:
+        a = a + res
+    return np.maximum(a, 0.0) if relu else a
+
+
+def bn_bwd_full(prm, c, t, dt, mean, var, relu, M):
+    """Backward of a bn op on the full map: returns (dc, da, {gamma, beta})."""
+    da = dt * (t > 0) if relu else dt
+    sig = np.sqrt(var + BN_EPS)[None, :, None, None]
+    xh = (c - mean[None, :, None, None]) / sig
+    dbeta = da.sum(axis=(0, 2, 3))
+    dgamma = (da * xh).sum(axis=(0, 2, 3))
+    dc = prm["gamma"][None, :, None, None] / sig * (
+        da - dbeta[None, :, None, None] / M - xh * dgamma[None, :, None, None] / M)
+    return dc, da, {"gamma": dgamma, "beta": dbeta}
+
+
 def bf16_store(a):
     """Round to the nearest bfloat16 (round-to-nearest-even), kept as float64.
 
@@ -112,6 +153,11 @@ def forward(net, params, x, store=None):
         elif op["kind"] == "maxpool":
             t, am = O.maxpool_fwd(src, op["k"], op["s"], pads)
             aux.append(am)
+        elif op["kind"] == "bn":
+            mean, var = bn_stats(src)
+            res = ts[op["res"]] if op["res"] >= 0 else None
+            t = bn_apply(params["convs"][i], src, mean, var, res, op["relu"])
+            aux.append((mean, var))
         else:
             a = src + ts[op["res"]]
             t = np.maximum(a, 0.0) if op["relu"] else a
@@ -147,6 +193,15 @@ def backward(net, params, ts, aux, dzl, need_dx=True):
                 acc(op["res"], dres)
         elif op["kind"] == "maxpool":
             acc(op["src"], O.maxpool_bwd(aux[i], dt, src.shape[2:]))
+        elif op["kind"] == "bn":
+            mean, var = aux[i]
+            M = src.shape[0] * src.shape[2] * src.shape[3]
+            dc, da, g = bn_bwd_full(params["convs"][i], src, ts[i + 1], dt, mean, var, op["relu"], M)
+            grads[i] = g
+            if op["src"] > 0 or need_dx:
+                acc(op["src"], dc)
+            if op["res"] >= 0:
+                acc(op["res"], da)
         else:
             da = dt * (ts[i + 1] > 0) if op["relu"] else dt
             acc(op["src"], da)

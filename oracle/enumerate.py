@@ -66,7 +66,7 @@ def _inputs(op):
 
 def rf(op, rows_out, h_in):
     """Rows of an input read by the given output rows (explicit set enumeration)."""
-    if op["kind"] == "add":
+    if op["kind"] in ("add", "bn"):   # pointwise (bn: its statistics are a separate sweep)
         return {y for y in rows_out if 0 <= y < h_in}
     k, s, p = op["k"], op["s"], op["p"]
     got = set()

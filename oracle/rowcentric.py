@@ -24,6 +24,19 @@ exchanged) and runs 2PS bands inside it.  Ranks share nothing but explicit messa
 halo rows of each segment input (FP) and the delta of those rows sent back and added (BP), the
 partial GAP sums and the per-rank weight gradients (summed = the all-reduce).
 
+Training-mode BatchNorm (R24): a bn op's batch statistics cover every row
+of its input, a strong dependency across all bands.  Exactly, in the order the dependencies force:
+  FP statistics sweeps -- for every bn op j of a segment in op order, one band sweep computes the ops
+     before j (their bn statistics are already known) and sums the rows each band computes of j's
+     input (the interval rule gives every row to exactly one band): mean_j, var_j.  Then the
+     ordinary FP sweep.
+  BP sums sweeps -- for every bn op j in reverse op order, one reverse band sweep recomputes the band
+     and back-propagates through the ops after j (their sums are known) down to the complete delta
+     of j's output, summing dbeta_j = sum(da) and dgamma_j = sum(da*xh) over the band's rows of j's
+     output.  Then the ordinary BP sweep, whose bn backward uses them (the textbook adjoint).
+2PS and column only (OverL's overlapping bands would count rows twice).  Negative control:
+per_band_stats=True normalises every band by its own rows' statistics.
+
 Negative controls (must NOT match the column oracle): share=False (cached rows
 replaced by zero rows -- the "padding redundancy" of Fig. 3(b)),
 carry=False (2PS BP drops the delta carry), overl_average=True (the averaging
@@ -57,10 +70,15 @@ def _slab(op, held, src, a, b, h_in, share=True):
     return _rows(held, src, g0, g1), (pt, pb, p, p), g0
 
 
-def _op_rows_fwd(net, i, held, params, a, b, shp, share=True):
+def _op_rows_fwd(net, i, held, params, a, b, shp, share=True, bn=None):
     """Rows [a, b) of op i's output from held slabs.  Returns (t_rows, aux)."""
     op = net["ops"][i]
     src = op["src"]
+    if op["kind"] == "bn":
+        c = _rows(held, src, a, b)
+        mean, var = bn[i] if bn is not None and i in bn else C.bn_stats(c)   # (no stats: per band)
+        res = _rows(held, op["res"], a, b) if op["res"] >= 0 else None
+        return C.bn_apply(params["convs"][i], c, mean, var, res, op["relu"]), None
     if op["kind"] == "add":
         t = _rows(held, src, a, b) + _rows(held, op["res"], a, b)
         return (np.maximum(t, 0.0) if op["relu"] else t), None
@@ -107,10 +125,12 @@ def _band_range(plan, band, t):
     return band[t]
 
 
-def seg_forward(plan, s, params, x_in, share=True, in_lo=0):
+def seg_forward(plan, s, params, x_in, share=True, in_lo=0, bn=None, stop_at=None, on_rows=None):
     """FP of one segment.  Returns (full-width segment output, caches per boundary).
     x_in holds rows [in_lo, in_lo + rows) of the segment input (a rank's slab, else the full map);
-    the output has the full height, rows no band computes are zero."""
+    the output has the full height, rows no band computes are zero.
+    bn: {op: (mean, var)} of the segment's bn ops; stop_at: compute only ops < stop_at (a bn
+    statistics sweep); on_rows(t, a, rows): called with the rows [a, b) each band computes."""
     net, shp = plan.net, plan.shp
     seg_in, ids, out = plan.segs[s]
     E, bands = plan.bands[s]
@@ -122,12 +142,16 @@ def seg_forward(plan, s, params, x_in, share=True, in_lo=0):
     for r, band in enumerate(bands):
         held = {seg_in: (in_lo, x_in)}
         for i in ids:
+            if stop_at is not None and i >= stop_at:
+                continue
             t = i + 1
             lo, a, b = _band_range(plan, band, t)
             if plan.mode == "overl" and t == out:
                 lo, a, b = (E[r - 1] if r else 0), (E[r - 1] if r else 0), E[r]
-            new, _ = _op_rows_fwd(net, i, held, params, a, b, shp, share) if b > a else \
+            new, _ = _op_rows_fwd(net, i, held, params, a, b, shp, share, bn) if b > a else \
                 (np.zeros((B, shp[t][0], 0, shp[t][2])), None)
+            if on_rows is not None:
+                on_rows(t, a, new)
             cached = None
             if lo < a:
                 clo, carr = prev_cache[t]
@@ -139,7 +163,7 @@ def seg_forward(plan, s, params, x_in, share=True, in_lo=0):
         if plan.mode == "2ps" and r + 1 < len(bands):
             for i in ids:
                 t = i + 1
-                if t == out:
+                if t == out or t not in held:
                     continue
                 nlo = bands[r + 1][t][0]
                 lo, arr = held[t]
@@ -150,10 +174,26 @@ def seg_forward(plan, s, params, x_in, share=True, in_lo=0):
     return y, caches
 
 
-def _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads):
-    """Backward of op i over its output rows [a, b) given complete delta dt; adds into d[...]."""
+def _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn=None, bns=None):
+    """Backward of op i over its output rows [a, b) given complete delta dt; adds into d[...].
+    bn / bns: {op: (mean, var)} and {op: (dbeta, dgamma)} of the segment's bn ops (full-map sums)."""
     op = net["ops"][i]
     src = op["src"]
+    if op["kind"] == "bn":
+        mean, var = bn[i]
+        dbeta, dgamma = bns[i]
+        t = _rows(held, i + 1, a, b)
+        c = _rows(held, src, a, b)
+        M = dt.shape[0] * shp[src][1] * shp[src][2]
+        da = dt * (t > 0) if op["relu"] else dt
+        sig = np.sqrt(var + C.BN_EPS)[None, :, None, None]
+        xh = (c - mean[None, :, None, None]) / sig
+        dc = params["convs"][i]["gamma"][None, :, None, None] / sig * (
+            da - dbeta[None, :, None, None] / M - xh * dgamma[None, :, None, None] / M)
+        _add_rows(d, src, a, dc)
+        if op["res"] >= 0:
+            _add_rows(d, op["res"], a, da)
+        return
     if op["kind"] == "add":
         t = _rows(held, i + 1, a, b)
         da = dt * (t > 0) if op["relu"] else dt
@@ -181,14 +221,20 @@ def _add_rows(d, t, r0, v):
     arr[:, :, r0 - lo:r0 - lo + v.shape[2]] += v
 
 
-def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_average=False, in_lo=0):
+def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_average=False, in_lo=0,
+                 bn=None, bns=None, stop_at=None, on_delta=None):
     """BP of one segment from the full-width delta of its output.  Returns (d_in, grads);
-    d_in covers the same rows [in_lo, ..) as the input slab x_in."""
+    d_in covers the same rows [in_lo, ..) as the input slab x_in.
+    stop_at / on_delta: a bn sums sweep -- back-propagate through the ops after bn op stop_at and
+    call on_delta(held, a, b, dt) with the complete delta rows of its output in every band."""
     net, shp = plan.net, plan.shp
     seg_in, ids, out = plan.segs[s]
     E, bands = plan.bands[s]
     B = x_in.shape[0]
     grads = {i: {} for i in ids if net["ops"][i]["kind"] == "conv"}
+    for i in ids:
+        if net["ops"][i]["kind"] == "bn" and bns is not None and i in bns:
+            grads[i] = {"beta": bns[i][0].copy(), "gamma": bns[i][1].copy()}
     d_in = np.zeros_like(x_in)
     carry = {}
     mult = None
@@ -208,7 +254,7 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
             if plan.mode == "overl" and t == out:
                 lo, a, b = (E[r - 1] if r else 0), (E[r - 1] if r else 0), E[r]
             ranges[t] = (lo, a, b)
-            new, _ = _op_rows_fwd(net, i, held, params, a, b, shp) if b > a else \
+            new, _ = _op_rows_fwd(net, i, held, params, a, b, shp, True, bn) if b > a else \
                 (np.zeros((B, shp[t][0], 0, shp[t][2])), None)
             cached = None
             if lo < a:
@@ -225,6 +271,8 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
                     clo, carr = carry[t]
                     _add_rows(d, t, clo, carr)
         for i in reversed(ids):
+            if stop_at is not None and i < stop_at:
+                break
             t = i + 1
             lo, a, b = ranges[t]
             if b <= a:
@@ -232,7 +280,10 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
             dt = _rows(d, t, a, b)
             if mult is not None and t != out:
                 dt = dt / mult[t][None, None, a:b, None]
-            _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads)
+            if stop_at is not None and i == stop_at:
+                on_delta(held, a, b, dt)
+                break
+            _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn, bns)
         carry = {}
         for t, (lo, a, b) in ranges.items():
             if t != out and lo < a:
@@ -240,12 +291,68 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
     return d_in, grads
 
 
-def forward(plan, params, x, share=True):
-    """Row-centric FP over all segments: returns (z^L, checkpoints, caches)."""
+def _bn_ops(plan, s):
+    return [i for i in plan.segs[s][1] if plan.net["ops"][i]["kind"] == "bn"]
+
+
+def seg_bn_stats(plan, s, params, x_in):
+    """FP statistics sweeps of segment s (module docstring): {bn op: (mean, var)}."""
+    net, shp = plan.net, plan.shp
+    bn = {}
+    for j in _bn_ops(plan, s):
+        assert plan.mode != "overl", "training-mode BN: 2PS / column only"
+        src = net["ops"][j]["src"]
+        if src == plan.segs[s][0]:
+            bn[j] = C.bn_stats(x_in)
+            continue
+        B, c, h, w = x_in.shape[0], shp[src][0], shp[src][1], shp[src][2]
+        acc = {"s1": np.zeros(c), "n": 0, "rows": []}
+
+        def on_rows(t, a, rows, src=src, acc=acc):
+            if t == src:
+                acc["s1"] += rows.sum(axis=(0, 2, 3))
+                acc["n"] += rows.shape[2]
+                acc["rows"].append(rows)
+        seg_forward(plan, s, params, x_in, bn=bn, stop_at=j, on_rows=on_rows)
+        assert acc["n"] == h, ("every row of the bn input exactly once", acc["n"], h)
+        M = B * h * w
+        mean = acc["s1"] / M
+        var = sum(((r_ - mean[None, :, None, None]) ** 2).sum(axis=(0, 2, 3)) for r_ in acc["rows"]) / M
+        bn[j] = (mean, var)
+    return bn
+
+
+def seg_bn_sums(plan, s, params, x_in, dout, caches, bn):
+    """BP sums sweeps of segment s: {bn op: (dbeta, dgamma)} (full-map sums of da, da*xh)."""
+    net = plan.net
+    bns = {}
+    for j in reversed(_bn_ops(plan, s)):
+        op = net["ops"][j]
+        mean, var = bn[j]
+        acc = {"s1": np.zeros(len(mean)), "s2": np.zeros(len(mean))}
+
+        def on_delta(held, a, b, dt, j=j, op=op, mean=mean, var=var, acc=acc):
+            t = _rows(held, j + 1, a, b)
+            c = _rows(held, op["src"], a, b)
+            da = dt * (t > 0) if op["relu"] else dt
+            xh = (c - mean[None, :, None, None]) / np.sqrt(var + C.BN_EPS)[None, :, None, None]
+            acc["s1"] += da.sum(axis=(0, 2, 3))
+            acc["s2"] += (da * xh).sum(axis=(0, 2, 3))
+        seg_backward(plan, s, params, x_in, dout, caches, bn=bn, bns=bns, stop_at=j, on_delta=on_delta)
+        bns[j] = (acc["s1"], acc["s2"])
+    return bns
+
+
+def forward(plan, params, x, share=True, per_band_stats=False):
+    """Row-centric FP over all segments: returns (z^L, checkpoints, caches); plan.bn_stats[s]
+    holds the bn statistics of segment s (statistics sweeps; per_band_stats: negative control)."""
     ckpts = [np.asarray(x, dtype=np.float64)]
     allc = []
+    plan.bn_stats = []
     for s in range(len(plan.segs)):
-        y, caches = seg_forward(plan, s, params, ckpts[-1], share)
+        bn = {} if per_band_stats or not _bn_ops(plan, s) else seg_bn_stats(plan, s, params, ckpts[-1])
+        plan.bn_stats.append(bn)
+        y, caches = seg_forward(plan, s, params, ckpts[-1], share, bn=None if per_band_stats else bn)
         ckpts.append(y)
         allc.append(caches)
     return ckpts[-1], ckpts, allc
@@ -256,7 +363,10 @@ def backward(plan, params, ckpts, allc, dzl, carry_on=True, overl_average=False)
     grads = [None] * len(plan.net["ops"])
     dout = np.asarray(dzl, dtype=np.float64)
     for s in range(len(plan.segs) - 1, -1, -1):
-        dout, g = seg_backward(plan, s, params, ckpts[s], dout, allc[s], carry_on, overl_average)
+        bn = plan.bn_stats[s] if getattr(plan, "bn_stats", None) else {}
+        bns = seg_bn_sums(plan, s, params, ckpts[s], dout, allc[s], bn) if bn else None
+        dout, g = seg_backward(plan, s, params, ckpts[s], dout, allc[s], carry_on, overl_average,
+                               bn=bn, bns=bns)
         for i, v in g.items():
             grads[i] = v
     return grads, dout
@@ -264,7 +374,8 @@ def backward(plan, params, ckpts, allc, dzl, carry_on=True, overl_average=False)
 
 def step(plan, params, x, labels, lr, **kw):
     """One Alg. 1 iteration, row-centric: returns (new_params, loss, grads, head_grads, z^L)."""
-    zl, ckpts, allc = forward(plan, params, x, share=kw.get("share", True))
+    zl, ckpts, allc = forward(plan, params, x, share=kw.get("share", True),
+                              per_band_stats=kw.get("per_band_stats", False))
     loss, dzl, hg, _ = C.head_forward_backward(zl, params["head"], labels)
     grads, _ = backward(plan, params, ckpts, allc, dzl, kw.get("carry_on", True),
                         kw.get("overl_average", False))

@@ -14,6 +14,9 @@ Tensor ids: 0 = the image; op i produces tensor i+1.  An op is a dict:
            t_out = relu?( epi(Conv(t_src)) + t_res )
   maxpool: {"kind":"maxpool","src":t,"k":k,"s":s,"p":p,"seg_end":bool}
   add:     {"kind":"add","src":t,"res":t2,"relu":bool,"seg_end":bool}
+  bn:      {"kind":"bn","src":t,"res":t or -1,"relu":bool,"seg_end":bool}
+           training-mode batch normalisation: statistics of t_src over the whole
+           batch and map, t_out = relu?( gamma*(t_src-mean)/sqrt(var+eps) + beta + t_res )
 "seg_end" marks a checkpoint boundary after the op (2PS-H / OverL-H).
 
 Input recipe:
@@ -36,6 +39,10 @@ def maxpool(src, k=2, s=2, p=0, seg_end=False):
 
 def add(src, res, relu=True, seg_end=False):
     return {"kind": "add", "src": src, "res": res, "relu": relu, "seg_end": seg_end}
+
+
+def bn(src, res=-1, relu=True, seg_end=False):
+    return {"kind": "bn", "src": src, "res": res, "relu": relu, "seg_end": seg_end}
 
 
 # ---------------------------------------------------------------- presets
@@ -67,7 +74,7 @@ def vgg16(H=224, W=224, C=3, classes=10, segments="none", width_div=1, cfg=None)
     return {"C": C, "H": H, "W": W, "classes": classes, "ops": ops, "name": "vgg16"}
 
 
-def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, blocks=(3, 4, 6, 3)):
+def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, blocks=(3, 4, 6, 3), bn_train=False):
     """ResNet-50 v1.5 (torchvision topology: stride on the 3x3 of the first block of stages 2-4,
     1x1 projection shortcut on every stage's first block), frozen-statistics BN folded into
     per-channel affine convs (R11, R14).  Bottleneck:
@@ -76,10 +83,14 @@ def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, block
     segments: "stage" checkpoints after the stem max-pool and after every stage but the last
     (2PS-H / OverL-H), "none" = whole-net row-centric, or a string naming the cut points: "p" the
     stem max-pool, "2" / "3" / "4" the end of conv2_x / conv3_x / conv4_x (e.g. "3": one checkpoint
-    after conv3_x; "stage" == "p234")."""
+    after conv3_x; "stage" == "p234"; "block" checkpoints after every bottleneck).
+    bn_train: training-mode BatchNorm -- every affine conv becomes a plain conv
+    (epi "none", no ReLU) followed by a "bn" op that carries the ReLU and the residual."""
+    if bn_train:
+        return _bn_train(resnet50(H, W, C, classes, segments, width_div, blocks))
     d = lambda c: max(8, c // width_div)
     cuts = {"stage": "p234", "none": ""}.get(segments, segments)
-    ops = [conv(0, d(64), 7, 2, 3, epi="affine"), maxpool(1, 3, 2, 1, seg_end=("p" in cuts))]
+    ops = [conv(0, d(64), 7, 2, 3, epi="affine"), maxpool(1, 3, 2, 1, seg_end=("p" in cuts or cuts == "block"))]
     t, cin = 2, d(64)
     for si, (nb, w) in enumerate(zip(blocks, (64, 128, 256, 512))):
         for bi in range(nb):
@@ -96,10 +107,47 @@ def resnet50(H=224, W=224, C=3, classes=10, segments="stage", width_div=1, block
                 sc = x
             ops.append(conv(b, d(4 * w), 1, 1, 0, epi="affine", relu=True, res=sc))
             t = len(ops)
+            if cuts == "block" and not (si == len(blocks) - 1 and bi == nb - 1):
+                ops[-1]["seg_end"] = True
         if str(si + 2) in cuts and si < len(blocks) - 1:
             ops[-1]["seg_end"] = True
     ops[-1]["seg_end"] = False
     return {"C": C, "H": H, "W": W, "classes": classes, "ops": ops, "name": "resnet50"}
+
+
+def _bn_train(net):
+    """Rewrite every affine conv op as conv (epi none, no ReLU, no residual) + bn op (ReLU,
+    residual), renumbering tensor ids (topology bookkeeping only)."""
+    ops, new_id = [], {0: 0}
+    for i, op in enumerate(net["ops"]):
+        o = dict(op)
+        o["src"] = new_id[op["src"]]
+        if op.get("res", -1) >= 0:
+            o["res"] = new_id[op["res"]]
+        if op["kind"] == "conv" and op["epi"] == "affine":
+            c = dict(o, epi="none", relu=False, res=-1, seg_end=False)
+            ops.append(c)
+            ops.append(bn(len(ops), res=o["res"], relu=op["relu"], seg_end=op["seg_end"]))
+        else:
+            ops.append(o)
+        new_id[i + 1] = len(ops)
+    out = dict(net, ops=ops)
+    out["name"] = net.get("name", "net") + "_bn"
+    return out
+
+
+def bn_chain(H=16, W=8, C=2, ch=4, n=3, p=1, res_every=0, classes=10):
+    """Tiny BN test net: n x [conv3x3 (no bias) -> bn (ReLU)], optionally with a residual every
+    res_every layers (the bn of layer j adds the output of layer j - res_every)."""
+    ops, outs = [], [0]
+    t = 0
+    for j in range(n):
+        ops.append(conv(t, ch, 3, 1, p, epi="none", relu=False))
+        res = outs[j + 1 - res_every] if res_every and (j + 1) % res_every == 0 and j + 1 - res_every >= 1 else -1
+        ops.append(bn(len(ops), res=res, relu=True))
+        t = len(ops)
+        outs.append(t)
+    return {"C": C, "H": H, "W": W, "classes": classes, "ops": ops, "name": "bn_chain"}
 
 
 # ---------------------------------------------------------------- inputs
@@ -143,6 +191,13 @@ def make_params(net, seed=2, bias_scale=0.0, gamma_spread=0.0, bf16=False):
     rnd = round_bf16 if bf16 else (lambda a: a)
     convs = []
     for op in net["ops"]:
+        if op["kind"] == "bn":
+            co = ch[op["src"]]
+            convs.append({
+                "gamma": rnd(r.uniform(1 - gamma_spread, 1 + gamma_spread, size=co)) if gamma_spread
+                else np.ones(co),
+                "beta": rnd(r.uniform(-bias_scale, bias_scale, size=co)) if bias_scale else np.zeros(co)})
+            continue
         if op["kind"] != "conv":
             convs.append(None)
             continue
