@@ -33,7 +33,7 @@
  *   - Element type: float (LRCNN_FP32) or bfloat16 (LRCNN_BF16) -- "act_t".
  *   - Parameters: one flat array laid out by the plan (lrcnn_plan_param):
  *     per conv op w[C_out][k][k][Cp_in] (OHWI), then bias[C_out] (EPI_BIAS) or
- *     gamma[C_out], beta[C_out] (EPI_AFFINE); then the head fc_w[classes][C_L],
+ *     gamma[C_out], beta[C_out] (EPI_AFFINE); per BN op gamma[C], beta[C]; then the head fc_w[classes][C_L],
  *     fc_b[classes].  Device copies in act_t ("params"), an fp32 master copy
  *     ("master") and fp32 gradients ("grads") share these offsets.
  */
@@ -68,7 +68,7 @@ typedef enum {
 
 typedef enum { LRCNN_COLUMN = 0, LRCNN_2PS = 1, LRCNN_OVERL = 2 } lrcnn_mode;
 typedef enum { LRCNN_FP32 = 0, LRCNN_BF16 = 1 } lrcnn_precision;
-enum { LRCNN_OP_CONV = 0, LRCNN_OP_MAXPOOL = 1, LRCNN_OP_ADD = 2 };
+enum { LRCNN_OP_CONV = 0, LRCNN_OP_MAXPOOL = 1, LRCNN_OP_ADD = 2, LRCNN_OP_BN = 3 };
 enum { LRCNN_EPI_NONE = 0, LRCNN_EPI_BIAS = 1, LRCNN_EPI_AFFINE = 2 };
 
 /* One op of the DAG.  Tensor ids: 0 = the image, op i produces tensor i+1.
@@ -76,6 +76,15 @@ enum { LRCNN_EPI_NONE = 0, LRCNN_EPI_BIAS = 1, LRCNN_EPI_AFFINE = 2 };
  *            epi: BIAS  -> + b[co];  AFFINE -> gamma[co]*c + beta[co] (frozen-statistics BN)
  *   MAXPOOL: t = max over k x k windows, stride s, pad p (pads never win, ties -> lowest index)
  *   ADD:     t = relu?( t_src + t_res )
+ *   BN:      t = relu?( gamma[c]*(t_src - mean[c])/sqrt(var[c] + 1e-5) + beta[c] + t_res )   (t_res optional)
+ *            training-mode BatchNorm (BN in the FP: PAPER.md:112; R24): mean and
+ *            biased var of t_src over the whole batch and map, recomputed every step; the backward is the
+ *            batch-statistics adjoint.  Parameters gamma[C], beta[C] (plan layout).  The statistics are
+ *            a dependency on EVERY row of t_src: lrcnn_forward_rows runs one statistics sweep per
+ *            dependency level of a segment's BN ops before its FP sweep, lrcnn_backward_rows one sums
+ *            sweep per level (reverse) before its BP sweep.  Modes COLUMN and 2PS on
+ *            one GPU or data-parallel replicas (per-replica statistics); OverL, row sharding and zero
+ *            redundancy return LRCNN_E_UNSUPPORTED.
  * seg_end != 0 stores the op's output as a full-width checkpoint (segment boundary). */
 typedef struct {
     int kind;

@@ -166,8 +166,10 @@ def forward(net, params, x, store=None):
     return ts, aux
 
 
-def backward(net, params, ts, aux, dzl, need_dx=True):
-    """Column BP from delta^L (= dz^L); returns (grads per op, dx)."""
+def backward(net, params, ts, aux, dzl, need_dx=True, trace=None):
+    """Column BP from delta^L (= dz^L); returns (grads per op, dx).
+    trace: optional dict, filled per bn op with the summation magnitudes of its parameter gradients
+    {"beta": sum|da|, "gamma": sum|da*xh|} per channel (the condition of those full-map sums)."""
     ds = [None] * len(ts)
     ds[-1] = np.asarray(dzl, dtype=np.float64).copy()
     grads = [None] * len(net["ops"])
@@ -198,6 +200,9 @@ def backward(net, params, ts, aux, dzl, need_dx=True):
             M = src.shape[0] * src.shape[2] * src.shape[3]
             dc, da, g = bn_bwd_full(params["convs"][i], src, ts[i + 1], dt, mean, var, op["relu"], M)
             grads[i] = g
+            if trace is not None:
+                xh = (src - mean[None, :, None, None]) / np.sqrt(var + BN_EPS)[None, :, None, None]
+                trace[i] = {"beta": np.abs(da).sum(axis=(0, 2, 3)), "gamma": np.abs(da * xh).sum(axis=(0, 2, 3))}
             if op["src"] > 0 or need_dx:
                 acc(op["src"], dc)
             if op["res"] >= 0:

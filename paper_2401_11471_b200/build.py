@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["plan.cpp", "kernels_simt.cu", "conv_tc.cu", "bneck_tc.cu", "comm.cu", "engine.cu"]
+SOURCES = ["plan.cpp", "kernels_simt.cu", "conv_tc.cu", "bneck_tc.cu", "bn.cu", "comm.cu", "engine.cu"]
 HEADERS = ["plan.hpp", "kernels.hpp", "tc.hpp", "tc_ptx.cuh", "comm.hpp"]
 
 

@@ -1,0 +1,272 @@
+// bn.cu -- training-mode BatchNorm on band rows (reading R24).
+//
+// The paper names BatchNorm in the FP and leaves it out of its analysis; with
+// batch statistics a bn op's normalisation depends on EVERY row of its input -- a strong dependency
+// across all bands.  The engine resolves it with statistics sweeps (FP) and sums sweeps (BP), see
+// engine.cu; these kernels are the per-band pieces:
+//   k_bn_stats        sum c, sum c^2 per channel over band rows [a, b) (fp64 partials + atomics)
+//   k_bn_finalize_fwd mean, biased var -> coef: a = gamma*invstd, b = beta - a*mean (and mean, invstd)
+//   k_bn_fwd          t = relu?(a*c + b + res) on band rows
+//   k_bn_sums         S1 = sum da, S2 = sum da*(c-mean)*invstd over band rows (da: the gated delta)
+//   k_bn_finalize_bwd p, q of  dc = a*da + p + q*c  (the batch-statistics adjoint
+//                     dc = a*(da - S1/M - xh*S2/M)); dgamma += S2, dbeta += S1
+//   k_bn_bwd          delta(src) += gate * (a*da + p + q*c) on band rows
+// All arithmetic fp32, sums fp64; activations act_t (fp32 or bf16), NHWC rows of a View, channels
+// processed as 8-element vectors (Cp is a multiple of 8).  coef layout: [6][Cp] floats
+// (a, b, p, q, mean, invstd); channels >= C get a = b = p = q = 0 (padded channels stay zero).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.hpp"
+
+namespace lrcnn {
+
+namespace {
+
+typedef __nv_bfloat16 bf16;
+constexpr double kBnEps = 1e-5;   // DESIGN.md R24 (the oracle states its own copy)
+constexpr int kBnThreads = 256;
+
+__device__ __forceinline__ long long bn_off(const View &v, int b, int g, int x) {
+    return (long long)b * v.bs + ((long long)(g - v.base) * v.W + x) * v.Cp;
+}
+__device__ __forceinline__ void load8(const float *p, float *v) {
+    const float4 a = *(const float4 *)p, b = *(const float4 *)(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const bf16 *p, float *v) {
+    const uint4 u = *(const uint4 *)p;
+    const __nv_bfloat162 *h = (const __nv_bfloat162 *)&u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        v[2 * k] = f.x; v[2 * k + 1] = f.y;
+    }
+}
+__device__ __forceinline__ void store8(float *p, const float *v) {
+    *(float4 *)p = make_float4(v[0], v[1], v[2], v[3]);
+    *(float4 *)(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(bf16 *p, const float *v) {
+    uint4 u;
+    __nv_bfloat162 *h = (__nv_bfloat162 *)&u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+    *(uint4 *)p = u;
+}
+
+// pixel p of the band rows [a, b) -> (image, row, column)
+__device__ __forceinline__ void pix(long long p, int rows, int W, int a, int &b_, int &y, int &x) {
+    x = (int)(p % W);
+    const long long r = p / W;
+    y = a + (int)(r % rows);
+    b_ = (int)(r / rows);
+}
+
+// Per-channel sums of two per-element quantities over the band's pixels: thread (lane, g) owns the
+// 8 channels of group g for pixels lane, lane + lanes, ...; fp64 partials, a block reduction over
+// the lanes, one fp64 atomic per channel and quantity.  mode 0: (c, c^2); mode 1: (da, da*xh).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kBnThreads) k_bn_reduce(View x, View dy, const float *coef, int a, int b, int B,
+                                                          double *out) {
+    extern __shared__ double red[];   // [lanes * G][16]
+    const int Cp = x.Cp, G = Cp / 8, lanes = kBnThreads / G;
+    const int lane = threadIdx.x / G, g = threadIdx.x % G;
+    const int rows = b - a, W = x.W;
+    const long long n = (long long)B * rows * W;
+    double s[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s[k] = 0.0;
+    float mean[8], inv[8];
+    if (MODE == 1) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { mean[k] = coef[4 * Cp + g * 8 + k]; inv[k] = coef[5 * Cp + g * 8 + k]; }
+    }
+    if (lane < lanes) {
+        for (long long p = (long long)blockIdx.x * lanes + lane; p < n; p += (long long)gridDim.x * lanes) {
+            int bi, y, xx;
+            pix(p, rows, W, a, bi, y, xx);
+            float v[8];
+            load8((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, v);
+            if (MODE == 0) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) { s[k] += v[k]; s[8 + k] += (double)v[k] * v[k]; }
+            } else {
+                float d[8];
+                load8((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, d);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    s[k] += d[k];
+                    s[8 + k] += (double)d[k] * ((v[k] - mean[k]) * inv[k]);
+                }
+            }
+        }
+    }
+    if (lane < lanes) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) red[(size_t)threadIdx.x * 16 + k] = s[k];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < G * 16; j += blockDim.x) {
+        const int gg = j / 16, k = j % 16;
+        double acc = 0.0;
+        for (int l = 0; l < lanes; ++l) acc += red[(size_t)(l * G + gg) * 16 + k];
+        const int c = gg * 8 + (k & 7);
+        atomicAdd(out + (k < 8 ? 0 : Cp) + c, acc);
+    }
+}
+
+template <typename T>
+__global__ void k_bn_finalize_fwd(const double *sums, const T *gamma, const T *beta, int C, int Cp, double M,
+                                  float *coef) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= Cp) return;
+    float a = 0.f, bb = 0.f, mean = 0.f, inv = 0.f;
+    if (c < C) {
+        const double m = sums[c] / M;
+        const double var = fmax(sums[Cp + c] / M - m * m, 0.0);
+        const double is = 1.0 / sqrt(var + kBnEps);
+        const double ga = (double)(float)gamma[c], be = (double)(float)beta[c];
+        a = (float)(ga * is);
+        bb = (float)(be - ga * is * m);
+        mean = (float)m;
+        inv = (float)is;
+    }
+    coef[c] = a; coef[Cp + c] = bb; coef[4 * Cp + c] = mean; coef[5 * Cp + c] = inv;
+}
+
+__global__ void k_bn_finalize_bwd(const double *S, float *coef, int C, int Cp, double M, float *dgamma,
+                                  float *dbeta) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= Cp) return;
+    float p = 0.f, q = 0.f;
+    if (c < C) {
+        const double a = coef[c], mean = coef[4 * Cp + c], inv = coef[5 * Cp + c];
+        const double s1 = S[c], s2 = S[Cp + c];
+        const double qq = -a * s2 * inv / M;
+        q = (float)qq;
+        p = (float)(-a * s1 / M - qq * mean);
+        if (dgamma) dgamma[c] += (float)s2;
+        if (dbeta) dbeta[c] += (float)s1;
+    }
+    coef[2 * Cp + c] = p; coef[3 * Cp + c] = q;
+}
+
+template <typename T>
+__global__ void k_bn_fwd(View in, View res, View out, const float *coef, int relu, int has_res, int a, int b,
+                         int B) {
+    const int Cp = out.Cp, G = Cp / 8, W = out.W, rows = b - a;
+    const long long n = (long long)B * rows * W * G;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int g = (int)(i % G);
+        int bi, y, x;
+        pix(i / G, rows, W, a, bi, y, x);
+        float v[8], r[8];
+        load8((const T *)in.p + bn_off(in, bi, y, x) + g * 8, v);
+        if (has_res) load8((const T *)res.p + bn_off(res, bi, y, x) + g * 8, r);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int c = g * 8 + k;
+            float t = fmaf(coef[c], v[k], coef[Cp + c]);
+            if (has_res) t += r[k];
+            v[k] = relu ? fmaxf(t, 0.f) : t;
+        }
+        store8((T *)out.p + bn_off(out, bi, y, x) + g * 8, v);
+    }
+}
+
+template <typename T>
+__global__ void k_bn_bwd(View dy, View x, View dx, View act, int gate, const float *coef, int a, int b, int B) {
+    const int Cp = dx.Cp, G = Cp / 8, W = dx.W, rows = b - a;
+    const long long n = (long long)B * rows * W * G;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int g = (int)(i % G);
+        int bi, y, xx;
+        pix(i / G, rows, W, a, bi, y, xx);
+        float d[8], v[8], o[8], m[8];
+        load8((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, d);
+        load8((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, v);
+        T *dst = (T *)dx.p + bn_off(dx, bi, y, xx) + g * 8;
+        load8(dst, o);
+        if (gate) load8((const T *)act.p + bn_off(act, bi, y, xx) + g * 8, m);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int c = g * 8 + k;
+            const float dc = fmaf(coef[c], d[k], fmaf(coef[3 * Cp + c], v[k], coef[2 * Cp + c]));
+            o[k] = (gate && m[k] <= 0.f) ? 0.f : o[k] + dc;
+        }
+        store8(dst, o);
+    }
+}
+
+unsigned grid_elem(long long n) {
+    long long g = (n + kBnThreads - 1) / kBnThreads;
+    return (unsigned)std::max(1LL, std::min(g, 148LL * 16));
+}
+
+template <int MODE>
+cudaError_t bn_reduce(int prec, const View &x, const View &dy, const float *coef, int a, int b, int B, double *out,
+                      cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    const int G = x.Cp / 8;
+    if (x.Cp % 8 || G > kBnThreads) return cudaErrorInvalidValue;
+    const int lanes = kBnThreads / G;
+    const long long n = (long long)B * (b - a) * x.W;
+    const unsigned grid = (unsigned)std::max(1LL, std::min((n + lanes - 1) / lanes, 148LL * 4));
+    const size_t smem = (size_t)kBnThreads * 16 * sizeof(double);
+    if (prec) k_bn_reduce<bf16, MODE><<<grid, kBnThreads, smem, st>>>(x, dy, coef, a, b, B, out);
+    else k_bn_reduce<float, MODE><<<grid, kBnThreads, smem, st>>>(x, dy, coef, a, b, B, out);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t bn_stats(int prec, const View &x, int a, int b, int B, double *sums, cudaStream_t st) {
+    return bn_reduce<0>(prec, x, x, nullptr, a, b, B, sums, st);
+}
+
+cudaError_t bn_sums(int prec, const View &dy, const View &x, const float *coef, int a, int b, int B, double *S,
+                    cudaStream_t st) {
+    return bn_reduce<1>(prec, x, dy, coef, a, b, B, S, st);
+}
+
+cudaError_t bn_finalize_fwd(int prec, const double *sums, const void *gamma, const void *beta, int C, int Cp,
+                            double M, float *coef, cudaStream_t st) {
+    const unsigned g = (unsigned)((Cp + 127) / 128);
+    if (prec) k_bn_finalize_fwd<bf16><<<g, 128, 0, st>>>(sums, (const bf16 *)gamma, (const bf16 *)beta, C, Cp, M, coef);
+    else k_bn_finalize_fwd<float><<<g, 128, 0, st>>>(sums, (const float *)gamma, (const float *)beta, C, Cp, M, coef);
+    return cudaGetLastError();
+}
+
+cudaError_t bn_finalize_bwd(const double *S, float *coef, int C, int Cp, double M, float *dgamma, float *dbeta,
+                            cudaStream_t st) {
+    k_bn_finalize_bwd<<<(unsigned)((Cp + 127) / 128), 128, 0, st>>>(S, coef, C, Cp, M, dgamma, dbeta);
+    return cudaGetLastError();
+}
+
+cudaError_t bn_fwd(int prec, const View &in, const View &res, const View &out, const float *coef, int relu, int a,
+                   int b, int B, cudaStream_t st) {
+    const long long n = (long long)B * (b - a) * out.W * (out.Cp / 8);
+    if (n <= 0) return cudaSuccess;
+    if (out.Cp % 8) return cudaErrorInvalidValue;
+    const int hr = res.p != nullptr;
+    if (prec) k_bn_fwd<bf16><<<grid_elem(n), kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
+    else k_bn_fwd<float><<<grid_elem(n), kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
+    return cudaGetLastError();
+}
+
+cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, const View &act, int gate,
+                   const float *coef, int a, int b, int B, cudaStream_t st) {
+    const long long n = (long long)B * (b - a) * dx.W * (dx.Cp / 8);
+    if (n <= 0) return cudaSuccess;
+    if (dx.Cp % 8) return cudaErrorInvalidValue;
+    if (prec) k_bn_bwd<bf16><<<grid_elem(n), kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
+    else k_bn_bwd<float><<<grid_elem(n), kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
+    return cudaGetLastError();
+}
+
+}  // namespace lrcnn

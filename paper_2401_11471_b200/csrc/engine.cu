@@ -53,6 +53,11 @@ struct Run {
     bool side_busy = false;
     bool fp_merged = false;        // FP over merged bands: band tensors live in the FP buffers
     bool dp_pending = false;       // gradient all-reduces enqueued on the communication stream
+    // training-mode BN sweeps: FP statistics sweep -- compute only the ops in fmask;
+    // BP sums sweep -- run the backward of the ops in bops only, write the delta of the tensors in
+    // bneed only, no weight / parameter gradients; bn_level: the BN ops whose sums the sweep takes
+    const std::vector<char> *fmask = nullptr, *bops = nullptr, *bneed = nullptr;
+    const std::vector<int> *bn_level = nullptr;
 };
 
 // Fork: side stream waits for everything enqueued so far on the main stream.
@@ -256,6 +261,12 @@ static lrcnn_status op_forward_impl(Run &R, const Segment &S, int r, int i) {
         ++P.launches;
         ProfScope ps(R, 2, 0, i * 8 + 4);
         CK(simt_pool_fwd(R.prec, A, R.st));
+    } else if (o.d.kind == LRCNN_OP_BN) {   // t = relu?(a*c + b + res), a / b from this step's statistics
+        View res;
+        if (o.d.res >= 0) res = act_view(R, S, r, o.d.res);
+        ++P.launches;
+        ProfScope ps(R, 2, 0, i * 8 + 6);
+        CK(bn_fwd(R.prec, in, res, out, (const float *)(R.ws + o.bn_coef_off), o.d.relu, a, b, P.net.B, R.st));
     } else {
         EltArgs A;
         A.x0 = in; A.x1 = act_view(R, S, r, o.d.res); A.out = out; A.relu = o.d.relu; A.a = a; A.b = b; A.B = P.net.B;
@@ -467,6 +478,7 @@ static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cach
     for (size_t q = 0; q < S.ops.size(); ++q) {
         const int i = S.ops[q];
         if (skip_out && i + 1 == S.out_t) continue;
+        if (R.fmask && !(*R.fmask)[i]) continue;   // BN statistics sweep: only the ops it needs
         // ops i+1, i+2 of a fused block ran with op i (unless the block output is skipped: BP recompute
         // of the segment output, whose delta is known -- then ops i, i+1 run unfused)
         const bool f2 = q >= 2 && S.ops[q - 1] == i - 1 && S.ops[q - 2] == i - 2 && bneck_at(P, S, i - 2) &&
@@ -584,6 +596,54 @@ static lrcnn_status launch_transposes(Run &R, cudaStream_t st) {
     return LRCNN_OK;
 }
 
+// Training-mode BN statistics: per FP level of the segment's BN ops,
+// one band sweep computes the ops their inputs need (the lower levels' statistics are final) and sums
+// c, c^2 over the rows each band computes of every BN input (the interval rule gives each row to one
+// band); then mean / var -> the affine coefficients the FP sweep applies.
+static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
+    Plan &P = R.P;
+    lrcnn_status st;
+    const int B = P.net.B;
+    for (size_t l = 0; l < S.bn_fp_levels.size(); ++l) {
+        bool banded = false;
+        for (int j : S.bn_fp_levels[l]) {
+            const OpInfo &o = P.op[j];
+            CK(cudaMemsetAsync(R.ws + o.bn_sums_off, 0, 2 * (size_t)P.t[o.in_t].Cp * sizeof(double), R.st));
+            if (o.in_t == S.in_t) {   // BN of the segment input: its full map is the checkpoint
+                const TensorInfo &ti = P.t[o.in_t];
+                ++P.launches;
+                CK(bn_stats(R.prec, full_view(ckpt_ptr(R, o.in_t), ti), ti.ck_lo, ti.ck_lo + ti.ck_rows, B,
+                            (double *)(R.ws + o.bn_sums_off), R.st));
+            } else {
+                banded = true;
+            }
+        }
+        if (banded) {
+            R.fmask = &S.bn_fp_ops[l];
+            for (int r = 0; r < (int)S.E.size(); ++r) {
+                Nvtx nv("FP BN statistics level %d band %d", (int)l, r);
+                if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) { R.fmask = nullptr; return st; }
+                for (int j : S.bn_fp_levels[l]) {
+                    const OpInfo &o = P.op[j];
+                    if (o.in_t == S.in_t) continue;
+                    const int a = S.a[r][o.in_t], b = S.b[r][o.in_t];
+                    if (b <= a) continue;
+                    ++P.launches;
+                    CK(bn_stats(R.prec, act_view(R, S, r, o.in_t), a, b, B, (double *)(R.ws + o.bn_sums_off), R.st));
+                }
+            }
+            R.fmask = nullptr;
+        }
+        for (int j : S.bn_fp_levels[l]) {
+            const OpInfo &o = P.op[j];
+            const TensorInfo &ti = P.t[o.in_t];
+            CK(bn_finalize_fwd(R.prec, (const double *)(R.ws + o.bn_sums_off), prm(R, o.b_off), prm(R, o.beta_off), ti.C,
+                               ti.Cp, (double)B * ti.H * ti.W, (float *)(R.ws + o.bn_coef_off), R.st));
+        }
+    }
+    return LRCNN_OK;
+}
+
 static lrcnn_status run_forward(Run &R) {
     lrcnn_status st;
     {   // the dgrad weight transposes depend only on this step's weights: overlap them with the FP
@@ -602,6 +662,7 @@ static lrcnn_status run_forward(Run &R) {
     for (const Segment &S : R.P.seg) {
         if (sharded && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, full_view(ckpt_ptr(R, S.in_t), R.P.t[S.in_t]), false)) != LRCNN_OK) return st;
+        if (!S.bn_fp_levels.empty() && (st = bn_stat_sweeps(R, S)) != LRCNN_OK) return st;
         if (!S.fp_r0.empty()) {   // decoupled FP bands (N_FP < N_BP)
             Segment F = S;
             F.lo = S.fp_lo; F.a = S.fp_a; F.b = S.fp_b;
@@ -739,6 +800,67 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     const OpInfo &o = P.op[i];
     const int t = o.out_t;
     const int a = S.a[r][t], b = S.b[r][t];
+    // BN sums sweep (R.bneed): only the deltas the sweep needs, no weight / parameter gradients
+    auto need = [&](int tid) { return !R.bneed || (*R.bneed)[tid]; };
+    if (R.bneed && o.d.kind == LRCNN_OP_CONV) {
+        if (b <= a || o.in_t == 0 || !need(o.in_t)) return LRCNN_OK;
+        View dy = sub_rows(dlt_view(R, S, s, r, t), a, b, R.E);
+        const TensorInfo &tin = P.t[o.in_t];
+        DgradArgs A;
+        A.dy = dy; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);
+        A.gate = tin.relu; A.w = prm(R, o.w_off); A.wt = R.ws + o.wt_off;
+        A.gamma = o.d.epi == LRCNN_EPI_AFFINE ? prm(R, o.b_off) : nullptr;
+        A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.c_out = o.d.c_out; A.B = P.net.B;
+        A.ra = std::max(0, a * o.d.s - o.d.p);
+        A.rb = std::min(tin.H, (b - 1) * o.d.s - o.d.p + o.d.k);
+        A.write = delta_overwrite(P, S, o.in_t) ? 1 : 0;
+        ++P.launches;
+        ProfScope ps(R, 0, conv_flops(P, o, b - a), i * 8 + 1, conv_bytes(P, o, a, b, 1, A.write ? 0 : 1, A.gate ? 1 : 0),
+                     conv_bytes(P, o, a, b, 1, 0, 0, true));
+        bool tc = false;
+        if (P.use_tc) {
+            tc = tc_conv_dgrad(A, R.st);
+            lrcnn_status st0;
+            if (tc) ++P.tc_launches;
+            else if ((st0 = tc_declined(P, i, "dgrad")) != LRCNN_OK) return st0;
+        }
+        if (!tc) CK(simt_conv_dgrad(R.prec, A, R.st));
+        CK(cudaGetLastError());
+        const int N = (int)S.E.size();
+        if (A.write && P.opts.mode == LRCNN_2PS && r + 1 < N) {   // + the carry of band r+1, gated
+            const int ti_ = o.in_t, clo = S.lo[r + 1][ti_], chi = S.a[r + 1][ti_];
+            if (chi > clo) {
+                EltArgs E;
+                E.dx = A.dx; E.act = A.act; E.gate = tin.relu;
+                E.dy = View{R.ws + tin.carry_off, clo, chi - clo, tin.H, tin.W, tin.Cp,
+                            (long long)tin.carry_cap * tin.W * tin.Cp};
+                E.a = clo; E.b = chi; E.B = P.net.B;
+                ++P.launches;
+                CK(simt_acc_gate(R.prec, E, R.st));
+            }
+        }
+        return LRCNN_OK;
+    }
+    if (o.d.kind == LRCNN_OP_BN) {   // delta(src) += gate * (a*da + p + q*c); delta(res) += gate * da
+        if (b <= a) return LRCNN_OK;
+        View dy = sub_rows(dlt_view(R, S, s, r, t), a, b, R.E);
+        const float *coef = (const float *)(R.ws + o.bn_coef_off);
+        if (o.in_t != 0 && need(o.in_t)) {
+            const View x = act_view(R, S, r, o.in_t);
+            ++P.launches;
+            ProfScope ps(R, 2, 0, i * 8 + 7);
+            CK(bn_bwd(R.prec, dy, x, dlt_view(R, S, s, r, o.in_t), x, P.t[o.in_t].relu, coef, a, b, P.net.B, R.st));
+        }
+        if (o.d.res > 0 && need(o.d.res)) {
+            EltArgs A;
+            A.dy = dy; A.dx = dlt_view(R, S, s, r, o.d.res); A.act = act_view(R, S, r, o.d.res);
+            A.gate = P.t[o.d.res].relu; A.a = a; A.b = b; A.B = P.net.B;
+            ++P.launches;
+            ProfScope ps(R, 2, 0, i * 8 + 7);
+            CK(simt_acc_gate(R.prec, A, R.st));
+        }
+        return LRCNN_OK;
+    }
     if (b <= a) {   // no rows of this op in band r; a fused block input still gets its residual rows
         if (o.d.kind == LRCNN_OP_CONV && o.in_t != 0) return fused_res_rows(R, S, s, r, i, 0, 0, false, true);
         return LRCNN_OK;
@@ -923,7 +1045,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             }
         }
     } else if (o.d.kind == LRCNN_OP_MAXPOOL) {
-        if (need_dx) {
+        if (need_dx && need(o.in_t)) {
             PoolArgs A;
             A.dy = dy; A.dx = dlt_view(R, S, s, r, o.in_t); A.act = act_view(R, S, r, o.in_t);
             A.gate = tin.relu; A.k = o.d.k; A.s = o.d.s; A.p = o.d.p; A.a = a; A.b = b; A.B = B;
@@ -955,7 +1077,7 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
     } else {
         for (int which = 0; which < 2; ++which) {
             int tid = which ? o.d.res : o.in_t;
-            if (tid == 0) continue;
+            if (tid == 0 || !need(tid)) continue;
             EltArgs A;
             A.dy = dy; A.dx = dlt_view(R, S, s, r, tid); A.act = act_view(R, S, r, tid);
             A.gate = P.t[tid].relu; A.a = a; A.b = b; A.B = B;
@@ -1038,8 +1160,8 @@ static lrcnn_status run_backward(Run &R) {
                                R.st));
         }
         const int N = (int)S.E.size();
-        for (int r = N - 1; r >= 0; --r) {
-            Nvtx nv("BP seg %d band %d", s, r);
+        auto band_bp = [&](int r) -> lrcnn_status {
+            lrcnn_status st;
             if (recompute && (st = band_forward(R, S, r, false, true)) != LRCNN_OK) return st;
             for (auto it = S.ops.rbegin(); it != S.ops.rend(); ++it) {
                 const int i = *it;
@@ -1086,10 +1208,46 @@ static lrcnn_status run_backward(Run &R) {
                     if (rows > 0 && (st = copy_rows(R, ti, R.ws + ti.carry_off, ti.carry_cap, R.ws + ti.dlt_off, ti.cap,
                                                     rows)) != LRCNN_OK) return st;
                 }
+                if (R.bn_level && std::find(R.bn_level->begin(), R.bn_level->end(), i) != R.bn_level->end()) {
+                    // BN sums sweep: the delta of op i's output is complete -- sum da, da*xh over its rows
+                    const OpInfo &o = P.op[i];
+                    const int a = S.a[r][to], b = S.b[r][to];
+                    if (b > a) {
+                        ++P.launches;
+                        CK(bn_sums(R.prec, sub_rows(dlt_view(R, S, s, r, to), a, b, R.E), act_view(R, S, r, o.in_t),
+                                   (const float *)(R.ws + o.bn_coef_off), a, b, P.net.B,
+                                   (double *)(R.ws + o.bn_S_off), R.st));
+                    }
+                    continue;
+                }
+                if (R.bops && !(*R.bops)[i]) continue;
                 if ((st = op_backward(R, S, s, r, i)) != LRCNN_OK) return st;
             }
             CK(join_side(R));
             if (r == N - 1 && zr_plan(P) && (st = zr_exchange(R, S, true)) != LRCNN_OK) return st;
+            return LRCNN_OK;
+        };
+        // training-mode BN: one sums sweep per BP level, deepest BN ops first
+        for (size_t l = 0; l < S.bn_bp_levels.size(); ++l) {
+            for (int j : S.bn_bp_levels[l])
+                CK(cudaMemsetAsync(R.ws + P.op[j].bn_S_off, 0, 2 * (size_t)P.t[P.op[j].out_t].Cp * sizeof(double), R.st));
+            R.bops = &S.bn_bp_ops[l]; R.bneed = &S.bn_bp_need[l]; R.bn_level = &S.bn_bp_levels[l];
+            for (int r = N - 1; r >= 0; --r) {
+                Nvtx nv("BP BN sums level %d band %d", (int)l, r);
+                if ((st = band_bp(r)) != LRCNN_OK) return st;
+            }
+            R.bops = nullptr; R.bneed = nullptr; R.bn_level = nullptr;
+            for (int j : S.bn_bp_levels[l]) {
+                const OpInfo &o = P.op[j];
+                const TensorInfo &ts = P.t[o.in_t];
+                CK(bn_finalize_bwd((const double *)(R.ws + o.bn_S_off), (float *)(R.ws + o.bn_coef_off), ts.C, ts.Cp,
+                                   (double)P.net.B * ts.H * ts.W, R.grads ? R.grads + o.b_off : nullptr,
+                                   R.grads ? R.grads + o.beta_off : nullptr, R.st));
+            }
+        }
+        for (int r = N - 1; r >= 0; --r) {
+            Nvtx nv("BP seg %d band %d", s, r);
+            if ((st = band_bp(r)) != LRCNN_OK) return st;
         }
         if (P.opts.world > 1 && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, dfull_view(R.ws + P.dfull_off[(s + 1) & 1], P.t[S.in_t]), true)) != LRCNN_OK)
@@ -1182,8 +1340,8 @@ lrcnn_status lrcnn_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             size_t lo = (size_t)-1, hi = 0;
             for (int i : P.seg[si].ops) {
                 const OpInfo &oi = P.op[i];
-                if (oi.d.kind != LRCNN_OP_CONV) continue;
-                lo = std::min(lo, oi.w_off);
+                if (oi.d.kind != LRCNN_OP_CONV && oi.d.kind != LRCNN_OP_BN) continue;
+                lo = std::min(lo, oi.d.kind == LRCNN_OP_BN ? oi.b_off : oi.w_off);
                 hi = std::max(hi, oi.w_off + oi.w_cnt);
                 if (oi.b_cnt) hi = std::max(hi, oi.b_off + oi.b_cnt);
                 if (oi.beta_cnt) hi = std::max(hi, oi.beta_off + oi.beta_cnt);

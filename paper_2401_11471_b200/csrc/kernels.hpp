@@ -106,6 +106,20 @@ bool pool_tiled_shape(int k, int s, int Cp);      // overlapping max-pool backwa
 cudaError_t simt_add_fwd(int prec, const EltArgs &a, cudaStream_t st);
 cudaError_t simt_acc_gate(int prec, const EltArgs &a, cudaStream_t st);
 
+// training-mode BatchNorm (bn.cu): coef = [6][Cp] floats (a, b, p, q, mean, invstd),
+// sums / S = [2][Cp] doubles (accumulated; the caller zeroes them)
+cudaError_t bn_stats(int prec, const View &x, int a, int b, int B, double *sums, cudaStream_t st);
+cudaError_t bn_finalize_fwd(int prec, const double *sums, const void *gamma, const void *beta, int C, int Cp,
+                            double M, float *coef, cudaStream_t st);
+cudaError_t bn_fwd(int prec, const View &in, const View &res, const View &out, const float *coef, int relu, int a,
+                   int b, int B, cudaStream_t st);
+cudaError_t bn_sums(int prec, const View &dy, const View &x, const float *coef, int a, int b, int B, double *S,
+                    cudaStream_t st);
+cudaError_t bn_finalize_bwd(const double *S, float *coef, int C, int Cp, double M, float *dgamma, float *dbeta,
+                            cudaStream_t st);
+cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, const View &act, int gate,
+                   const float *coef, int a, int b, int B, cudaStream_t st);
+
 void simt_set_pdl(bool on);   // programmatic dependent launch on / off for this host thread (profiling)
 
 // head (Alg. 1 l.12-14) and update (l.24)

@@ -61,7 +61,7 @@ static std::vector<int> make_band_ends(int h_out, int band_rows, int n_bands, in
 }
 
 static bool window_role(const OpInfo &o, int role) {
-    return role == 0 && o.d.kind != LRCNN_OP_ADD;
+    return role == 0 && o.d.kind != LRCNN_OP_ADD && o.d.kind != LRCNN_OP_BN;
 }
 
 // BP delta buffers of one segment's band, overlaid by liveness.  In the BP's reverse op order the
@@ -182,11 +182,19 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
                 if (d.res >= 0) { err = "maxpool has no residual"; return LRCNN_E_ARG; }
                 out.C = in.C; out.relu = 0;
             }
-        } else if (d.kind == LRCNN_OP_ADD) {
-            if (d.res < 0) { err = "add needs res"; return LRCNN_E_ARG; }
-            const TensorInfo &r = P.t[d.res];
-            if (r.C != in.C || r.H != in.H || r.W != in.W) { err = "add shape mismatch"; return LRCNN_E_SHAPE; }
+        } else if (d.kind == LRCNN_OP_ADD || d.kind == LRCNN_OP_BN) {
+            if (d.kind == LRCNN_OP_ADD && d.res < 0) { err = "add needs res"; return LRCNN_E_ARG; }
+            if (d.res >= 0) {
+                const TensorInfo &r = P.t[d.res];
+                if (r.C != in.C || r.H != in.H || r.W != in.W) { err = "add / bn residual shape mismatch"; return LRCNN_E_SHAPE; }
+            }
             out.C = in.C; out.H = in.H; out.W = in.W; out.relu = d.relu ? 1 : 0;
+            if (d.kind == LRCNN_OP_BN) {
+                // training-mode BN (f4): the statistics sweeps need disjoint band rows on one full map
+                if (opts->mode == LRCNN_OVERL) { err = "training-mode BN: OverL bands overlap (use 2PS or COLUMN)"; return LRCNN_E_UNSUPPORTED; }
+                if (opts->world > 1 && !(opts->flags & LRCNN_FLAG_DP)) { err = "training-mode BN with row sharding is not supported (use data-parallel replicas)"; return LRCNN_E_UNSUPPORTED; }
+                if (opts->flags & LRCNN_FLAG_ZERO_REDUNDANCY) { err = "training-mode BN with zero-redundancy sharding is not supported"; return LRCNN_E_UNSUPPORTED; }
+            }
         } else { err = "bad op kind"; return LRCNN_E_ARG; }
         out.Cp = round_up(out.C, 8);
         P.t[d.src].cons.push_back({i, 0});
@@ -598,6 +606,11 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
     auto take = [&](size_t n) { size_t o = off; off += (n + 7) / 8 * 8; return o; };
     for (int i = 0; i < n_ops; ++i) {
         OpInfo &o = P.op[i];
+        if (o.d.kind == LRCNN_OP_BN) {   // gamma, beta (b_off / beta_off as for an affine conv)
+            o.b_cnt = P.t[o.out_t].C; o.b_off = take(o.b_cnt);
+            o.beta_cnt = P.t[o.out_t].C; o.beta_off = take(o.beta_cnt);
+            continue;
+        }
         if (o.d.kind != LRCNN_OP_CONV) continue;
         o.w_cnt = (size_t)o.d.c_out * o.d.k * o.d.k * P.t[o.in_t].Cp;
         o.w_off = take(o.w_cnt);
@@ -706,7 +719,87 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         size_t o0 = ws;
         for (OpInfo &o : P.op)
             if (o.d.kind == LRCNN_OP_CONV) o.wt_off = alloc(o.w_cnt * E);
+        for (OpInfo &o : P.op)
+            if (o.d.kind == LRCNN_OP_BN) {
+                const size_t Cp = P.t[o.out_t].Cp;
+                o.bn_sums_off = alloc(2 * Cp * sizeof(double));
+                o.bn_S_off = alloc(2 * Cp * sizeof(double));
+                o.bn_coef_off = alloc(6 * Cp * sizeof(float));
+            }
         M.other += ws - o0;
+    }
+    // training-mode BN levels per segment (Segment::bn_*)
+    for (Segment &S : P.seg) {
+        std::vector<int> bns;
+        for (int i : S.ops)
+            if (P.op[i].d.kind == LRCNN_OP_BN) bns.push_back(i);
+        if (bns.empty()) continue;
+        std::vector<char> inside(T, 0);
+        for (int i : S.ops) inside[i + 1] = 1;
+        auto ins = [&](int i) {
+            std::vector<int> v = {P.op[i].d.src};
+            if (P.op[i].d.res >= 0) v.push_back(P.op[i].d.res);
+            return v;
+        };
+        // ancestors of tensor t inside the segment (ops), by a reverse walk
+        auto anc_ops = [&](const std::vector<int> &roots) {
+            std::vector<char> op_in(n_ops, 0), seen(T, 0);
+            std::vector<int> st = roots;
+            while (!st.empty()) {
+                const int t = st.back(); st.pop_back();
+                if (seen[t] || !inside[t]) continue;
+                seen[t] = 1;
+                const int i = P.t[t].producer;
+                op_in[i] = 1;
+                for (int u : ins(i)) st.push_back(u);
+            }
+            return op_in;
+        };
+        std::vector<int> lvl(n_ops, -1), rlvl(n_ops, -1);
+        for (int j : bns) {   // op order is topological: ancestors first
+            int l = 0;
+            std::vector<char> a = anc_ops({P.op[j].d.src});
+            for (int k : bns)
+                if (k != j && a[k]) l = std::max(l, lvl[k] + 1);
+            lvl[j] = l;
+        }
+        // descendants of op j's output inside the segment (tensors), by a forward walk in op order
+        auto desc_t = [&](const std::vector<int> &roots) {
+            std::vector<char> d(T, 0);
+            for (int t : roots) d[t] = 1;
+            for (int i : S.ops)
+                for (int u : ins(i))
+                    if (d[u]) d[i + 1] = 1;
+            return d;
+        };
+        for (auto it = bns.rbegin(); it != bns.rend(); ++it) {
+            const int j = *it;
+            std::vector<char> d = desc_t({P.op[j].out_t});
+            int l = 0;
+            for (int k : bns)
+                if (k != j && d[P.op[k].out_t]) l = std::max(l, rlvl[k] + 1);
+            rlvl[j] = l;
+        }
+        int nf = 0, nb = 0;
+        for (int j : bns) { nf = std::max(nf, lvl[j] + 1); nb = std::max(nb, rlvl[j] + 1); }
+        S.bn_fp_levels.assign(nf, {});
+        S.bn_bp_levels.assign(nb, {});
+        for (int j : bns) { S.bn_fp_levels[lvl[j]].push_back(j); S.bn_bp_levels[rlvl[j]].push_back(j); }
+        for (int l = 0; l < nf; ++l) {
+            std::vector<int> roots;
+            for (int j : S.bn_fp_levels[l]) roots.push_back(P.op[j].d.src);
+            S.bn_fp_ops.push_back(anc_ops(roots));
+        }
+        for (int l = 0; l < nb; ++l) {
+            std::vector<int> roots;
+            for (int j : S.bn_bp_levels[l]) roots.push_back(P.op[j].out_t);
+            std::vector<char> need = desc_t(roots), ops(n_ops, 0);
+            for (int i : S.ops)
+                if (need[i + 1]) ops[i] = 1;
+            for (int j : S.bn_bp_levels[l]) ops[j] = 0;
+            S.bn_bp_need.push_back(need);
+            S.bn_bp_ops.push_back(ops);
+        }
     }
     // per-segment arena (band act/delta/carry), overlaid across segments
     size_t arena0 = ws, arena_max = 0;

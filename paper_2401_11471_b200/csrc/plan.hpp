@@ -56,6 +56,9 @@ struct OpInfo {
     int in_t, out_t;
     size_t w_off = 0, w_cnt = 0, b_off = 0, b_cnt = 0, beta_off = 0, beta_cnt = 0;
     size_t wt_off = 0;        // transposed (dgrad) weights in workspace (bf16 tensor-core path)
+    // training-mode BN (LRCNN_OP_BN): workspace scratch -- sums [2][Cp] fp64 (sum c, sum c^2), S [2][Cp] fp64
+    // (sum da, sum da*xh), coef [6][Cp] fp32 (a, b, p, q, mean, invstd); see bn.cu
+    size_t bn_sums_off = 0, bn_S_off = 0, bn_coef_off = 0;
 };
 
 // One halo transfer of a boundary tensor between this rank and a neighbour (rows [r0, r1)).
@@ -89,6 +92,13 @@ struct Segment {
     // zero-redundancy halo schedule of the internal tensors (tensor, rows)
     struct ZrRows { int t, r0, r1; };
     std::vector<ZrRows> zr_from_below, zr_to_above;
+    // training-mode BN: the segment's BN ops grouped by dependency
+    // level -- FP level k = BN ops whose input depends on BN ops of levels < k only (one statistics
+    // sweep per level computes the ops in bn_fp_ops[k]); BP level k (reverse) = BN ops whose output
+    // feeds BN ops of levels < k only (one sums sweep per level runs the backward of the ops in
+    // bn_bp_ops[k] and writes the delta of the tensors in bn_bp_need[k] only).  Per op / tensor id.
+    std::vector<std::vector<int>> bn_fp_levels, bn_bp_levels;
+    std::vector<std::vector<char>> bn_fp_ops, bn_bp_ops, bn_bp_need;
 };
 
 struct ProfileSlot {

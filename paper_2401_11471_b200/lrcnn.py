@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblrcnn.so")
 
-OP_CONV, OP_MAXPOOL, OP_ADD = 0, 1, 2
+OP_CONV, OP_MAXPOOL, OP_ADD, OP_BN = 0, 1, 2, 3
 EPI = {"none": 0, "bias": 1, "affine": 2}
 MODES = {"column": 0, "2ps": 1, "overl": 2}
 PRECS = {"fp32": 0, "bf16": 1}
@@ -170,7 +170,7 @@ def net_ops(net):
     """Marshal a workloads-style net dict into the C op array."""
     ops = (Op * len(net["ops"]))()
     for i, o in enumerate(net["ops"]):
-        kind = {"conv": OP_CONV, "maxpool": OP_MAXPOOL, "add": OP_ADD}[o["kind"]]
+        kind = {"conv": OP_CONV, "maxpool": OP_MAXPOOL, "add": OP_ADD, "bn": OP_BN}[o["kind"]]
         ops[i] = Op(kind, o["src"], o.get("res", -1) if o.get("res", -1) is not None else -1, o.get("cout", 0),
                     o.get("k", 1), o.get("s", 1), o.get("p", 0), EPI[o.get("epi", "none")] if kind == OP_CONV else 0,
                     1 if o.get("relu", False) else 0, 1 if o.get("seg_end", False) else 0)
@@ -331,6 +331,12 @@ class Plan:
             p = params["convs"][i]
             if p is None:
                 continue
+            if op["kind"] == "bn":   # gamma, beta (lrcnn.h: per BN op gamma[C], beta[C])
+                off, n = self.param(i, 1)
+                flat[off:off + n] = p["gamma"]
+                off, n = self.param(i, 2)
+                flat[off:off + n] = p["beta"]
+                continue
             off, n = self.param(i, 0)
             w = np.asarray(p["w"], dtype=np.float64)
             co, ci, k, _ = w.shape
@@ -362,6 +368,14 @@ class Plan:
         flat = np.asarray(flat, dtype=np.float64)
         out = []
         for i, op in enumerate(self.net["ops"]):
+            if op["kind"] == "bn":
+                g = {}
+                off, n = self.param(i, 1)
+                g["gamma"] = flat[off:off + n]
+                off, n = self.param(i, 2)
+                g["beta"] = flat[off:off + n]
+                out.append(g)
+                continue
             if op["kind"] != "conv":
                 out.append(None)
                 continue

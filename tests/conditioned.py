@@ -50,6 +50,11 @@ def validate_forward(net, params, ts, store, tol, rows=None):
         elif op["kind"] == "maxpool":
             ref, am = O.maxpool_fwd(src, op["k"], op["s"], _pads(op))
             aux.append(am)
+        elif op["kind"] == "bn":   # batch statistics of the GPU's stored full input map
+            mean, var = C.bn_stats(src)
+            res = ts[op["res"]] if op["res"] >= 0 else None
+            ref = C.bn_apply(params["convs"][i], src, mean, var, res, op["relu"])
+            aux.append((mean, var))
         else:
             a = src + ts[op["res"]]
             ref = np.maximum(a, 0.0) if op["relu"] else a

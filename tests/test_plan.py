@@ -554,3 +554,23 @@ def test_coordination_counters_closed_form(nb):
     tp = bench.coordination_counters(LB.Plan(net, 1, mode="2ps", prec="fp32", n_bands=nb))
     assert tp == {"computation_interruptions": 2 * (nb - 1), "overlapped_rows": 0,
                   "sharing_data_bytes": (nb - 1) * 2 * 2 * 32 * 8 * 4}
+
+
+def test_bn_plans_vs_enumerator_and_errors():
+    """Training-mode BN ops (f4) read their input 1:1: the interval rule of a BN net equals the
+    brute-force enumeration; OverL, row sharding and zero redundancy are refused (R24)."""
+    nets = [WL.bn_chain(H=19, W=7, C=3, ch=8, n=4, res_every=2),
+            WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True),
+            WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True, segments="block")]
+    for net in nets:
+        for kw in ({"band_rows": 1}, {"n_bands": 3}, {"n_bands": 1}):
+            _check_plan_vs_enum(net, "2ps", **kw)
+    net = nets[0]
+    for mode, kw in (("overl", {}), ("2ps", {"world": 2, "rank": 0})):
+        with pytest.raises(RuntimeError, match="UNSUPPORTED|not supported|overlap"):
+            LB.Plan(net, 2, mode=mode, prec="fp32", n_bands=2, **kw)
+    # parameters: gamma / beta per BN op in the flat layout
+    plan = LB.Plan(net, 2, mode="2ps", prec="fp32", n_bands=2)
+    for i, op in enumerate(net["ops"]):
+        if op["kind"] == "bn":
+            assert plan.param(i, 1)[1] == plan.param(i, 2)[1] == 8
