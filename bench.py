@@ -65,6 +65,9 @@ def parse():
                     help="forward pass on the BP bands (default: merged FP bands, LRCNN_FLAG_FP_MERGE)")
     ap.add_argument("--no-balanced", action="store_true",
                     help="same band count in every segment (default: balanced bands, LRCNN_FLAG_BALANCED_BANDS)")
+    ap.add_argument("--bn-train", action="store_true",
+                    help="ResNet with training-mode BatchNorm after every conv (SURVEY 8(f) f4: statistics / sums "
+                         "sweeps per dependency level, DESIGN.md §5.2) instead of frozen-statistics affine")
     ap.add_argument("--per-op-csv", default="", help="write the per-op kernel profile (CSV) here")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group backend; gloo only to exercise the N>1 code path on one GPU")
@@ -152,7 +155,8 @@ def make_net(a):
         H = W = a.hw
     if model == "vgg16":
         return WL.vgg16(H=H, W=W, segments=a.segments if a.segments in ("pool", "none") else "pool")
-    return WL.resnet50(H=H, W=W, segments="stage" if a.segments == "pool" else a.segments)
+    return WL.resnet50(H=H, W=W, segments="stage" if a.segments == "pool" else a.segments,
+                       bn_train=getattr(a, "bn_train", False))
 
 
 def cpu_baseline(a, steps=1):
@@ -210,6 +214,11 @@ def eager_layerwise(net, B, params, x_np, lab_np, dev, steps=3):
         dt = torch.bfloat16
         ws = []
         for i, op in enumerate(net["ops"]):
+            if op["kind"] == "bn":   # fp32 gamma / beta (torch's batch_norm parameters under autocast)
+                p = params["convs"][i]
+                ws.append({k: torch.tensor(p[k], dtype=torch.float32, device=dev).requires_grad_(True)
+                           for k in ("gamma", "beta")})
+                continue
             if op["kind"] != "conv":
                 ws.append(None)
                 continue
@@ -243,6 +252,13 @@ def eager_layerwise(net, B, params, x_np, lab_np, dev, steps=3):
                         y = F.relu(y)
                 elif op["kind"] == "maxpool":
                     y = F.max_pool2d(src, op["k"], op["s"], op["p"])
+                elif op["kind"] == "bn":   # training-mode batch statistics (cuDNN / native BN kernel)
+                    y = F.batch_norm(src, None, None, ws[i]["gamma"].to(dt), ws[i]["beta"].to(dt), training=True,
+                                     eps=1e-5)
+                    if op["res"] >= 0:
+                        y = y + ts[op["res"]]
+                    if op["relu"]:
+                        y = F.relu(y)
                 else:
                     y = src + ts[op["res"]]
                     if op["relu"]:
@@ -274,8 +290,10 @@ def eager_layerwise(net, B, params, x_np, lab_np, dev, steps=3):
         x_bytes = x.numel() * x.element_size()
         out = {"peak_allocated_bytes": peak, "feature_map_bytes": peak - param_bytes - x_bytes,
                "images_per_s": B / (ms / 1000.0), "ms_per_step": ms,
-               "what": "PyTorch %s eager, bf16 channels_last cuDNN, autograd, same DAG (frozen-BN affine), "
-                       "SGD; feature maps = peak - params - input" % torch.__version__}
+               "what": "PyTorch %s eager, bf16 channels_last cuDNN, autograd, same DAG (%s), "
+                       "SGD; feature maps = peak - params - input"
+                       % (torch.__version__, "training-mode BN" if any(o["kind"] == "bn" for o in net["ops"])
+                          else "frozen-BN affine")}
     except torch.cuda.OutOfMemoryError as e:
         out = {"error": "out of memory: %s" % str(e).split("\n")[0][:200]}
     except Exception as e:   # context only: never fail the bench on it
@@ -653,7 +671,8 @@ def main():
                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                "scaling": "strong" if rows else "weak",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[0,1) images, U{0..9} labels)",
-               "config": {"workload": "%s, batch %d per GPU, bf16" % (CONFIGS[a.config][4], B),
+               "config": {"workload": "%s, batch %d per GPU, bf16%s" % (CONFIGS[a.config][4], B,
+                                                                       ", training-mode BatchNorm" if a.bn_train else ""),
                           "global_batch": gb, "seq_len": None,
                           "parallelism": ("rows%d (row sharding%s, NCCL halo exchange + per-segment wgrad all-reduce)"
                                           % (world, ", zero redundancy" if a.zero_redundancy else ", OverL at the cuts")

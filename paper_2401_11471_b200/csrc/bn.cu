@@ -57,25 +57,18 @@ __device__ __forceinline__ void store8(bf16 *p, const float *v) {
     *(uint4 *)p = u;
 }
 
-// pixel p of the band rows [a, b) -> (image, row, column)
-__device__ __forceinline__ void pix(long long p, int rows, int W, int a, int &b_, int &y, int &x) {
-    x = (int)(p % W);
-    const long long r = p / W;
-    y = a + (int)(r % rows);
-    b_ = (int)(r / rows);
-}
-
-// Per-channel sums of two per-element quantities over the band's pixels: thread (lane, g) owns the
-// 8 channels of group g for pixels lane, lane + lanes, ...; fp64 partials, a block reduction over
-// the lanes, one fp64 atomic per channel and quantity.  mode 0: (c, c^2); mode 1: (da, da*xh).
+// Per-channel sums of two per-element quantities over the band's pixels.  Block j takes the image
+// rows j, j + gridDim.x, ... of the B * (b - a) band rows; thread (lane, g) owns the 8 channels of group
+// g for the columns lane, lane + lanes, ... of a row (no per-element index division); fp64 partials,
+// a block reduction over the lanes, one fp64 atomic per channel and quantity.
+// mode 0: (c, c^2); mode 1: (da, da*xh).
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(View x, View dy, const float *coef, int a, int b, int B,
                                                           double *out) {
     extern __shared__ double red[];   // [lanes * G][16]
     const int Cp = x.Cp, G = Cp / 8, lanes = kBnThreads / G;
     const int lane = threadIdx.x / G, g = threadIdx.x % G;
-    const int rows = b - a, W = x.W;
-    const long long n = (long long)B * rows * W;
+    const int rows = b - a, W = x.W, nrows = B * rows;
     double s[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) s[k] = 0.0;
@@ -85,21 +78,24 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(View x, View dy, const
         for (int k = 0; k < 8; ++k) { mean[k] = coef[4 * Cp + g * 8 + k]; inv[k] = coef[5 * Cp + g * 8 + k]; }
     }
     if (lane < lanes) {
-        for (long long p = (long long)blockIdx.x * lanes + lane; p < n; p += (long long)gridDim.x * lanes) {
-            int bi, y, xx;
-            pix(p, rows, W, a, bi, y, xx);
-            float v[8];
-            load8((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, v);
-            if (MODE == 0) {
+        for (int ry = blockIdx.x; ry < nrows; ry += gridDim.x) {
+            const int bi = ry / rows, y = a + ry % rows;
+            const T *xr = (const T *)x.p + bn_off(x, bi, y, 0) + g * 8;
+            const T *dr = MODE == 1 ? (const T *)dy.p + bn_off(dy, bi, y, 0) + g * 8 : nullptr;
+            for (int xx = lane; xx < W; xx += lanes) {
+                float v[8];
+                load8(xr + (size_t)xx * Cp, v);
+                if (MODE == 0) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) { s[k] += v[k]; s[8 + k] += (double)v[k] * v[k]; }
-            } else {
-                float d[8];
-                load8((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, d);
+                    for (int k = 0; k < 8; ++k) { s[k] += v[k]; s[8 + k] += (double)v[k] * v[k]; }
+                } else {
+                    float d[8];
+                    load8(dr + (size_t)xx * Cp, d);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    s[k] += d[k];
-                    s[8 + k] += (double)d[k] * ((v[k] - mean[k]) * inv[k]);
+                    for (int k = 0; k < 8; ++k) {
+                        s[k] += d[k];
+                        s[8 + k] += (double)d[k] * ((v[k] - mean[k]) * inv[k]);
+                    }
                 }
             }
         }
@@ -154,39 +150,46 @@ __global__ void k_bn_finalize_bwd(const double *S, float *coef, int C, int Cp, d
     coef[2 * Cp + c] = p; coef[3 * Cp + c] = q;
 }
 
+// Elementwise kernels: grid.y strides over the B * (b - a) image rows, grid.x * blockDim.x over the
+// W * Cp / 8 channel vectors of a row (32-bit index math, no per-element division by W or rows).
 template <typename T>
 __global__ void k_bn_fwd(View in, View res, View out, const float *coef, int relu, int has_res, int a, int b,
                          int B) {
-    const int Cp = out.Cp, G = Cp / 8, W = out.W, rows = b - a;
-    const long long n = (long long)B * rows * W * G;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int g = (int)(i % G);
-        int bi, y, x;
-        pix(i / G, rows, W, a, bi, y, x);
+    const int Cp = out.Cp, G = Cp / 8, rows = b - a, nv = out.W * G, nrows = B * rows;
+    const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v0 >= nv) return;
+    const int g = v0 % G, xx = v0 / G;
+    float ca[8], cb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { ca[k] = coef[g * 8 + k]; cb[k] = coef[Cp + g * 8 + k]; }
+    for (int ry = blockIdx.y; ry < nrows; ry += gridDim.y) {
+        const int bi = ry / rows, y = a + ry % rows;
         float v[8], r[8];
-        load8((const T *)in.p + bn_off(in, bi, y, x) + g * 8, v);
-        if (has_res) load8((const T *)res.p + bn_off(res, bi, y, x) + g * 8, r);
+        load8((const T *)in.p + bn_off(in, bi, y, xx) + g * 8, v);
+        if (has_res) load8((const T *)res.p + bn_off(res, bi, y, xx) + g * 8, r);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const int c = g * 8 + k;
-            float t = fmaf(coef[c], v[k], coef[Cp + c]);
+            float t = fmaf(ca[k], v[k], cb[k]);
             if (has_res) t += r[k];
             v[k] = relu ? fmaxf(t, 0.f) : t;
         }
-        store8((T *)out.p + bn_off(out, bi, y, x) + g * 8, v);
+        store8((T *)out.p + bn_off(out, bi, y, xx) + g * 8, v);
     }
 }
 
 template <typename T>
 __global__ void k_bn_bwd(View dy, View x, View dx, View act, int gate, const float *coef, int a, int b, int B) {
-    const int Cp = dx.Cp, G = Cp / 8, W = dx.W, rows = b - a;
-    const long long n = (long long)B * rows * W * G;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int g = (int)(i % G);
-        int bi, y, xx;
-        pix(i / G, rows, W, a, bi, y, xx);
+    const int Cp = dx.Cp, G = Cp / 8, rows = b - a, nv = dx.W * G, nrows = B * rows;
+    const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v0 >= nv) return;
+    const int g = v0 % G, xx = v0 / G;
+    float ca[8], cp[8], cq[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        ca[k] = coef[g * 8 + k]; cp[k] = coef[2 * Cp + g * 8 + k]; cq[k] = coef[3 * Cp + g * 8 + k];
+    }
+    for (int ry = blockIdx.y; ry < nrows; ry += gridDim.y) {
+        const int bi = ry / rows, y = a + ry % rows;
         float d[8], v[8], o[8], m[8];
         load8((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, d);
         load8((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, v);
@@ -195,18 +198,19 @@ __global__ void k_bn_bwd(View dy, View x, View dx, View act, int gate, const flo
         if (gate) load8((const T *)act.p + bn_off(act, bi, y, xx) + g * 8, m);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const int c = g * 8 + k;
-            const float dc = fmaf(coef[c], d[k], fmaf(coef[3 * Cp + c], v[k], coef[2 * Cp + c]));
+            const float dc = fmaf(ca[k], d[k], fmaf(cq[k], v[k], cp[k]));
             o[k] = (gate && m[k] <= 0.f) ? 0.f : o[k] + dc;
         }
         store8(dst, o);
     }
 }
 
-unsigned grid_elem(long long n) {
-    long long g = (n + kBnThreads - 1) / kBnThreads;
-    return (unsigned)std::max(1LL, std::min(g, 148LL * 16));
+dim3 grid_rows(int nv, int nrows) {
+    const unsigned gx = (unsigned)((nv + kBnThreads - 1) / kBnThreads);
+    // one image row per block row (a block strides over rows only beyond 65535)
+    return dim3(gx, (unsigned)std::max(1, std::min(nrows, 65535)));
 }
+
 
 template <int MODE>
 cudaError_t bn_reduce(int prec, const View &x, const View &dy, const float *coef, int a, int b, int B, double *out,
@@ -215,8 +219,8 @@ cudaError_t bn_reduce(int prec, const View &x, const View &dy, const float *coef
     const int G = x.Cp / 8;
     if (x.Cp % 8 || G > kBnThreads) return cudaErrorInvalidValue;
     const int lanes = kBnThreads / G;
-    const long long n = (long long)B * (b - a) * x.W;
-    const unsigned grid = (unsigned)std::max(1LL, std::min((n + lanes - 1) / lanes, 148LL * 4));
+    (void)lanes;
+    const unsigned grid = (unsigned)std::max(1, std::min(B * (b - a), 148 * 4));
     const size_t smem = (size_t)kBnThreads * 16 * sizeof(double);
     if (prec) k_bn_reduce<bf16, MODE><<<grid, kBnThreads, smem, st>>>(x, dy, coef, a, b, B, out);
     else k_bn_reduce<float, MODE><<<grid, kBnThreads, smem, st>>>(x, dy, coef, a, b, B, out);
@@ -254,8 +258,9 @@ cudaError_t bn_fwd(int prec, const View &in, const View &res, const View &out, c
     if (n <= 0) return cudaSuccess;
     if (out.Cp % 8) return cudaErrorInvalidValue;
     const int hr = res.p != nullptr;
-    if (prec) k_bn_fwd<bf16><<<grid_elem(n), kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
-    else k_bn_fwd<float><<<grid_elem(n), kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
+    const dim3 grid = grid_rows(out.W * (out.Cp / 8), B * (b - a));
+    if (prec) k_bn_fwd<bf16><<<grid, kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
+    else k_bn_fwd<float><<<grid, kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
     return cudaGetLastError();
 }
 
@@ -264,8 +269,9 @@ cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, cons
     const long long n = (long long)B * (b - a) * dx.W * (dx.Cp / 8);
     if (n <= 0) return cudaSuccess;
     if (dx.Cp % 8) return cudaErrorInvalidValue;
-    if (prec) k_bn_bwd<bf16><<<grid_elem(n), kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
-    else k_bn_bwd<float><<<grid_elem(n), kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
+    const dim3 grid = grid_rows(dx.W * (dx.Cp / 8), B * (b - a));
+    if (prec) k_bn_bwd<bf16><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
+    else k_bn_bwd<float><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
     return cudaGetLastError();
 }
 

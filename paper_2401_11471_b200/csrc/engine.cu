@@ -629,6 +629,7 @@ static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
                     const int a = S.a[r][o.in_t], b = S.b[r][o.in_t];
                     if (b <= a) continue;
                     ++P.launches;
+                    ProfScope ps(R, 2, 0, j * 8 + 6);
                     CK(bn_stats(R.prec, act_view(R, S, r, o.in_t), a, b, B, (double *)(R.ws + o.bn_sums_off), R.st));
                 }
             }
@@ -1214,6 +1215,7 @@ static lrcnn_status run_backward(Run &R) {
                     const int a = S.a[r][to], b = S.b[r][to];
                     if (b > a) {
                         ++P.launches;
+                        ProfScope ps(R, 2, 0, i * 8 + 7);
                         CK(bn_sums(R.prec, sub_rows(dlt_view(R, S, s, r, to), a, b, R.E), act_view(R, S, r, o.in_t),
                                    (const float *)(R.ws + o.bn_coef_off), a, b, P.net.B,
                                    (double *)(R.ws + o.bn_S_off), R.st));
