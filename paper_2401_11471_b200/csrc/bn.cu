@@ -10,7 +10,8 @@
 //   k_bn_sums         S1 = sum da, S2 = sum da*(c-mean)*invstd over band rows (da: the gated delta)
 //   k_bn_finalize_bwd p, q of  dc = a*da + p + q*c  (the batch-statistics adjoint
 //                     dc = a*(da - S1/M - xh*S2/M)); dgamma += S2, dbeta += S1
-//   k_bn_bwd          delta(src) += gate * (a*da + p + q*c) on band rows
+//   k_bn_bwd          delta(src) (+)= gate * (a*da + p + q*c) on band rows (written, not accumulated,
+//                     when the BN op is the only writer of those rows)
 // All arithmetic fp32, sums fp64; activations act_t (fp32 or bf16), NHWC rows of a View, channels
 // processed as 8-element vectors (Cp is a multiple of 8).  coef layout: [6][Cp] floats
 // (a, b, p, q, mean, invstd); channels >= C get a = b = p = q = 0 (padded channels stay zero).
@@ -57,6 +58,22 @@ __device__ __forceinline__ void store8(bf16 *p, const float *v) {
     *(uint4 *)p = u;
 }
 
+constexpr int kRowsPer = 2;
+
+__device__ __forceinline__ void coef8(const float *c, float *v) {
+    const float4 a = *(const float4 *)c, b = *(const float4 *)(c + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <typename T> struct Raw8;
+template <> struct Raw8<bf16> { uint4 u; };
+template <> struct Raw8<float> { float4 a, b; };
+__device__ __forceinline__ void ldraw(const bf16 *p, Raw8<bf16> &r) { r.u = *(const uint4 *)p; }
+__device__ __forceinline__ void ldraw(const float *p, Raw8<float> &r) { r.a = *(const float4 *)p; r.b = *(const float4 *)(p + 4); }
+__device__ __forceinline__ void unraw(const Raw8<bf16> &r, float *v) { load8((const bf16 *)&r.u, v); }
+__device__ __forceinline__ void unraw(const Raw8<float> &r, float *v) {
+    v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w; v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
+}
+
 // Per-channel sums of two per-element quantities over the band's pixels.  Block j takes the image
 // rows j, j + gridDim.x, ... of the B * (b - a) band rows; thread (lane, g) owns the 8 channels of group
 // g for the columns lane, lane + lanes, ... of a row (no per-element index division); fp64 partials,
@@ -65,44 +82,55 @@ __device__ __forceinline__ void store8(bf16 *p, const float *v) {
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kBnThreads) k_bn_reduce(View x, View dy, const float *coef, int a, int b, int B,
                                                           double *out) {
-    extern __shared__ double red[];   // [lanes * G][16]
+    extern __shared__ double red[];   // [kBnThreads][16]: per-thread fp64 sums (folded once per row)
     const int Cp = x.Cp, G = Cp / 8, lanes = kBnThreads / G;
     const int lane = threadIdx.x / G, g = threadIdx.x % G;
     const int rows = b - a, W = x.W, nrows = B * rows;
-    double s[16];
+    double *my = red + (size_t)threadIdx.x * 16;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) s[k] = 0.0;
-    float mean[8], inv[8];
-    if (MODE == 1) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) { mean[k] = coef[4 * Cp + g * 8 + k]; inv[k] = coef[5 * Cp + g * 8 + k]; }
-    }
+    for (int k = 0; k < 16; ++k) my[k] = 0.0;
     if (lane < lanes) {
+        float mean[8], inv[8];
+        if (MODE == 1) {
+            coef8(coef + 4 * Cp + g * 8, mean);
+            coef8(coef + 5 * Cp + g * 8, inv);
+        }
         for (int ry = blockIdx.x; ry < nrows; ry += gridDim.x) {
             const int bi = ry / rows, y = a + ry % rows;
             const T *xr = (const T *)x.p + bn_off(x, bi, y, 0) + g * 8;
             const T *dr = MODE == 1 ? (const T *)dy.p + bn_off(dy, bi, y, 0) + g * 8 : nullptr;
-            for (int xx = lane; xx < W; xx += lanes) {
-                float v[8];
-                load8(xr + (size_t)xx * Cp, v);
-                if (MODE == 0) {
+            float f[16];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) { s[k] += v[k]; s[8 + k] += (double)v[k] * v[k]; }
-                } else {
-                    float d[8];
-                    load8(dr + (size_t)xx * Cp, d);
+            for (int k = 0; k < 16; ++k) f[k] = 0.f;
+            for (int x0 = lane; x0 < W; x0 += 2 * lanes) {
+                Raw8<T> rv[2], rd[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int xx = min(x0 + u * lanes, W - 1);
+                    ldraw(xr + (size_t)xx * Cp, rv[u]);
+                    if (MODE == 1) ldraw(dr + (size_t)xx * Cp, rd[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (x0 + u * lanes >= W) continue;
+                    float v[8], d[8];
+                    unraw(rv[u], v);
+                    if (MODE == 1) unraw(rd[u], d);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        s[k] += d[k];
-                        s[8 + k] += (double)d[k] * ((v[k] - mean[k]) * inv[k]);
+                        if (MODE == 0) {
+                            f[k] += v[k];
+                            f[8 + k] = fmaf(v[k], v[k], f[8 + k]);
+                        } else {
+                            f[k] += d[k];
+                            f[8 + k] = fmaf(d[k], (v[k] - mean[k]) * inv[k], f[8 + k]);
+                        }
                     }
                 }
             }
-        }
-    }
-    if (lane < lanes) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) red[(size_t)threadIdx.x * 16 + k] = s[k];
+            for (int k = 0; k < 16; ++k) my[k] += f[k];
+        }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < G * 16; j += blockDim.x) {
@@ -150,67 +178,97 @@ __global__ void k_bn_finalize_bwd(const double *S, float *coef, int C, int Cp, d
     coef[2 * Cp + c] = p; coef[3 * Cp + c] = q;
 }
 
-// Elementwise kernels: grid.y strides over the B * (b - a) image rows, grid.x * blockDim.x over the
-// W * Cp / 8 channel vectors of a row (32-bit index math, no per-element division by W or rows).
+// Elementwise kernels: thread (g, x) = channel vector g of column x (grid.x * blockDim.x over the W * Cp / 8
+// vectors of a row); grid.y strides over the B * (b - a) image rows, kRowsPer rows per iteration with all
+// loads issued first (memory-level parallelism), held as raw 16-byte vectors until used (few registers:
+// four resident blocks per SM).  The per-channel coefficients are loaded once per thread as float4
+// vectors (loading them per element made the kernels L1-bound: ncu l1tex 97 %).
 template <typename T>
-__global__ void k_bn_fwd(View in, View res, View out, const float *coef, int relu, int has_res, int a, int b,
-                         int B) {
+__global__ void __launch_bounds__(kBnThreads) k_bn_fwd(View in, View res, View out, const float *coef, int relu,
+                                                        int has_res, int a, int b, int B) {
     const int Cp = out.Cp, G = Cp / 8, rows = b - a, nv = out.W * G, nrows = B * rows;
     const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (v0 >= nv) return;
     const int g = v0 % G, xx = v0 / G;
-    float ca[8], cb[8];
+    for (int r0 = blockIdx.y * kRowsPer; r0 < nrows; r0 += gridDim.y * kRowsPer) {
+        Raw8<T> rv[kRowsPer], rr[kRowsPer];
+        long long off[kRowsPer];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { ca[k] = coef[g * 8 + k]; cb[k] = coef[Cp + g * 8 + k]; }
-    for (int ry = blockIdx.y; ry < nrows; ry += gridDim.y) {
-        const int bi = ry / rows, y = a + ry % rows;
-        float v[8], r[8];
-        load8((const T *)in.p + bn_off(in, bi, y, xx) + g * 8, v);
-        if (has_res) load8((const T *)res.p + bn_off(res, bi, y, xx) + g * 8, r);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            float t = fmaf(ca[k], v[k], cb[k]);
-            if (has_res) t += r[k];
-            v[k] = relu ? fmaxf(t, 0.f) : t;
+        for (int u = 0; u < kRowsPer; ++u) {
+            const int ry = min(r0 + u, nrows - 1);   // (a duplicate of the last row is recomputed, not stored)
+            const int bi = ry / rows, y = a + ry % rows;
+            off[u] = bn_off(out, bi, y, xx) + g * 8;
+            ldraw((const T *)in.p + bn_off(in, bi, y, xx) + g * 8, rv[u]);
+            if (has_res) ldraw((const T *)res.p + bn_off(res, bi, y, xx) + g * 8, rr[u]);
         }
-        store8((T *)out.p + bn_off(out, bi, y, xx) + g * 8, v);
+        float ca[8], cb[8];
+        coef8(coef + g * 8, ca);
+        coef8(coef + Cp + g * 8, cb);
+#pragma unroll
+        for (int u = 0; u < kRowsPer; ++u) {
+            float v[8], r[8];
+            unraw(rv[u], v);
+            if (has_res) unraw(rr[u], r);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                float t = fmaf(ca[k], v[k], cb[k]);
+                if (has_res) t += r[k];
+                v[k] = relu ? fmaxf(t, 0.f) : t;
+            }
+            if (r0 + u < nrows) store8((T *)out.p + off[u], v);
+        }
     }
 }
 
+// write != 0: delta(src) rows are produced by this kernel alone (single writer) -- not read
 template <typename T>
-__global__ void k_bn_bwd(View dy, View x, View dx, View act, int gate, const float *coef, int a, int b, int B) {
+__global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx, View act, int gate, int write,
+                                                        const float *coef, int a, int b, int B) {
     const int Cp = dx.Cp, G = Cp / 8, rows = b - a, nv = dx.W * G, nrows = B * rows;
     const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (v0 >= nv) return;
     const int g = v0 % G, xx = v0 / G;
-    float ca[8], cp[8], cq[8];
+    for (int r0 = blockIdx.y * kRowsPer; r0 < nrows; r0 += gridDim.y * kRowsPer) {
+        Raw8<T> rd[kRowsPer], rv[kRowsPer], ro[kRowsPer], rm[kRowsPer];
+        long long off[kRowsPer];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        ca[k] = coef[g * 8 + k]; cp[k] = coef[2 * Cp + g * 8 + k]; cq[k] = coef[3 * Cp + g * 8 + k];
-    }
-    for (int ry = blockIdx.y; ry < nrows; ry += gridDim.y) {
-        const int bi = ry / rows, y = a + ry % rows;
-        float d[8], v[8], o[8], m[8];
-        load8((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, d);
-        load8((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, v);
-        T *dst = (T *)dx.p + bn_off(dx, bi, y, xx) + g * 8;
-        load8(dst, o);
-        if (gate) load8((const T *)act.p + bn_off(act, bi, y, xx) + g * 8, m);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float dc = fmaf(ca[k], d[k], fmaf(cq[k], v[k], cp[k]));
-            o[k] = (gate && m[k] <= 0.f) ? 0.f : o[k] + dc;
+        for (int u = 0; u < kRowsPer; ++u) {
+            const int ry = min(r0 + u, nrows - 1);
+            const int bi = ry / rows, y = a + ry % rows;
+            off[u] = bn_off(dx, bi, y, xx) + g * 8;
+            ldraw((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, rd[u]);
+            ldraw((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, rv[u]);
+            if (!write) ldraw((const T *)dx.p + off[u], ro[u]);
+            if (gate) ldraw((const T *)act.p + bn_off(act, bi, y, xx) + g * 8, rm[u]);
         }
-        store8(dst, o);
+        float ca[8], cp[8], cq[8];
+        coef8(coef + g * 8, ca);
+        coef8(coef + 2 * Cp + g * 8, cp);
+        coef8(coef + 3 * Cp + g * 8, cq);
+#pragma unroll
+        for (int u = 0; u < kRowsPer; ++u) {
+            float d[8], v[8], o[8], m[8];
+            unraw(rd[u], d);
+            unraw(rv[u], v);
+            if (!write) unraw(ro[u], o);
+            if (gate) unraw(rm[u], m);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float dc = fmaf(ca[k], d[k], fmaf(cq[k], v[k], cp[k]));
+                o[k] = (gate && m[k] <= 0.f) ? 0.f : (write ? dc : o[k] + dc);
+            }
+            if (r0 + u < nrows) store8((T *)dx.p + off[u], o);
+        }
     }
 }
 
 dim3 grid_rows(int nv, int nrows) {
-    const unsigned gx = (unsigned)((nv + kBnThreads - 1) / kBnThreads);
-    // one image row per block row (a block strides over rows only beyond 65535)
-    return dim3(gx, (unsigned)std::max(1, std::min(nrows, 65535)));
+    const int gx = (nv + kBnThreads - 1) / kBnThreads;
+    // about 8 blocks of 256 threads per SM in total, each striding over groups of kRowsPer rows
+    const int groups = (nrows + kRowsPer - 1) / kRowsPer;
+    const int gy = std::max(1, std::min(std::min(groups, 65535), (148 * 8 + gx - 1) / gx));
+    return dim3((unsigned)gx, (unsigned)gy);
 }
-
 
 template <int MODE>
 cudaError_t bn_reduce(int prec, const View &x, const View &dy, const float *coef, int a, int b, int B, double *out,
@@ -220,7 +278,7 @@ cudaError_t bn_reduce(int prec, const View &x, const View &dy, const float *coef
     if (x.Cp % 8 || G > kBnThreads) return cudaErrorInvalidValue;
     const int lanes = kBnThreads / G;
     (void)lanes;
-    const unsigned grid = (unsigned)std::max(1, std::min(B * (b - a), 148 * 4));
+    const unsigned grid = (unsigned)std::max(1, std::min(B * (b - a), 148 * 8));
     const size_t smem = (size_t)kBnThreads * 16 * sizeof(double);
     if (prec) k_bn_reduce<bf16, MODE><<<grid, kBnThreads, smem, st>>>(x, dy, coef, a, b, B, out);
     else k_bn_reduce<float, MODE><<<grid, kBnThreads, smem, st>>>(x, dy, coef, a, b, B, out);
@@ -264,14 +322,14 @@ cudaError_t bn_fwd(int prec, const View &in, const View &res, const View &out, c
     return cudaGetLastError();
 }
 
-cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, const View &act, int gate,
+cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, const View &act, int gate, int write,
                    const float *coef, int a, int b, int B, cudaStream_t st) {
     const long long n = (long long)B * (b - a) * dx.W * (dx.Cp / 8);
     if (n <= 0) return cudaSuccess;
     if (dx.Cp % 8) return cudaErrorInvalidValue;
     const dim3 grid = grid_rows(dx.W * (dx.Cp / 8), B * (b - a));
-    if (prec) k_bn_bwd<bf16><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
-    else k_bn_bwd<float><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, coef, a, b, B);
+    if (prec) k_bn_bwd<bf16><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B);
+    else k_bn_bwd<float><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B);
     return cudaGetLastError();
 }
 

@@ -744,6 +744,11 @@ static bool delta_overwrite(const Plan &P, const Segment &S, int t) {
     if (ti.cons.size() != 1 || ti.cons[0].role != 0) return false;
     const OpInfo &u = P.op[ti.cons[0].op];
     if (u.d.kind == LRCNN_OP_CONV) return u.d.s == 1;
+    if (u.d.kind == LRCNN_OP_BN) {   // 1:1 reader: its band rows are exactly the tensor's rows (no cache, no carry)
+        for (size_t r = 0; r < S.E.size(); ++r)
+            if (S.lo[r][t] != S.a[r][t] || S.a[r][t] != S.a[r][u.out_t] || S.b[r][t] != S.b[r][u.out_t]) return false;
+        return true;
+    }
     // a non-overlapping max-pool that tiles the map exactly writes every input position once
     const TensorInfo &to = P.t[u.out_t];
     if (u.d.kind != LRCNN_OP_MAXPOOL) return false;
@@ -850,7 +855,8 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             const View x = act_view(R, S, r, o.in_t);
             ++P.launches;
             ProfScope ps(R, 2, 0, i * 8 + 7);
-            CK(bn_bwd(R.prec, dy, x, dlt_view(R, S, s, r, o.in_t), x, P.t[o.in_t].relu, coef, a, b, P.net.B, R.st));
+            CK(bn_bwd(R.prec, dy, x, dlt_view(R, S, s, r, o.in_t), x, P.t[o.in_t].relu,
+                      delta_overwrite(P, S, o.in_t) ? 1 : 0, coef, a, b, P.net.B, R.st));
         }
         if (o.d.res > 0 && need(o.d.res)) {
             EltArgs A;

@@ -16,6 +16,10 @@ if cfg == "c2":
     net, B = WL.vgg16(H=224, W=224, segments="pool"), 32
 elif cfg == "c3":
     net, B = WL.resnet50(H=224, W=224), 256
+elif cfg == "c3bn":   # training-mode BN, per-block checkpoints (bench --bn-train --segments block)
+    net, B = WL.resnet50(H=224, W=224, bn_train=True, segments="block"), 256
+elif cfg == "c4bn":
+    net, B = WL.resnet50(H=3600, W=2400, bn_train=True, segments="block"), 8
 elif cfg == "c5":
     net, B = WL.vgg16(H=2048, W=2048, segments="pool"), 16
 else:
