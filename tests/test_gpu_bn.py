@@ -26,7 +26,7 @@ def test_bn_chain_fp32_bands_and_segments():
     check(net, 2, "fp32", ["2ps"], [{"n_bands": 2}, {"band_rows": 3}], bias=0.3, gspread=0.4, plain_grads=True)
 
 
-def check_bn_bf16(net, B, modes, kws, dzl_kind):
+def check_bn_bf16(net, B, modes, kws, dzl_kind, flags=0):
     """bf16 BN parity (R25): z^L vs the plain oracle, every stored map validated, every
     weight gradient vs the decision-conditioned oracle <= 2e-2 of its max-abs (R18), and every BN
     gamma / beta gradient -- a full-map sum of a delta whose channel mean the downstream BN removes
@@ -43,7 +43,7 @@ def check_bn_bf16(net, B, modes, kws, dzl_kind):
         dzl = WL.round_bf16(dzl)
     for mode in modes:
         for kw in (kws if mode != "column" else [{}]):
-            _, zl, g, tsg = run_capture(net, B, "bf16", mode, params, x, dzl, **kw)
+            _, zl, g, tsg = run_capture(net, B, "bf16", mode, params, x, dzl, flags=flags, **kw)
             assert rel(zl, ts[-1]) <= TOL["bf16"], (mode, kw, "zL", rel(zl, ts[-1]))
             _, aux_g = validate_forward(net, params, tsg, C.bf16_store, TOL["bf16"])
             trace = {}
@@ -114,3 +114,63 @@ def test_bn_step_graph_replay_bf16():
     assert max(losses) - min(losses) <= 1e-6 * abs(losses[0]), losses   # lr = 0: identical steps
     _, loss_ref, _, _, _ = C.step(net, params, x, lab, 0.0)
     assert abs(losses[0] - loss_ref) <= 2e-2 * abs(loss_ref)
+
+
+def test_bn_bench_flags_bf16():
+    """The BN path with bench.py's flags (balanced bands, decoupled FP bands, tensor cores required)
+    and per-block checkpoints, bf16, vs the oracle (R17d / R25)."""
+    net = WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True, segments="block")
+    flags = LB.FLAG_BALANCED_BANDS | LB.FLAG_FP_MERGE | LB.FLAG_REQUIRE_TC
+    check_bn_bf16(net, 2, ["2ps"], [{"n_bands": 4}], "head", flags=flags)
+
+
+def test_bn_data_parallel_replicas_fp32():
+    """Training-mode BN under data-parallel replicas (LRCNN_FLAG_DP, loopback communicator): every
+    replica normalises by its own batch's statistics, and the all-reduced gradient equals the sum of
+    the oracle's per-replica column gradients (fp32, 1e-5)."""
+    import threading
+    net = WL.bn_chain(H=20, W=12, C=3, ch=8, n=4, res_every=2)
+    net["ops"][3]["seg_end"] = True
+    B = 2
+    params = WL.make_params(net, seed=3, bias_scale=0.2, gamma_spread=0.3)
+    xs = [WL.make_input(net, B, seed=10 + g) for g in range(2)]
+    labs = [WL.make_labels(net, B, seed=20 + g) for g in range(2)]
+    ref = [C.step(net, params, xs[g], labs[g], 0.0) for g in range(2)]
+    comms = LB.Comm.loopback(2)
+    plans, states = [], []
+    for g in range(2):
+        p = LB.Plan(net, B, mode="2ps", prec="fp32", n_bands=3, world=2, rank=g, flags=LB.FLAG_DP)
+        p.set_comm(comms[g])
+        ds = LB.DeviceState(p)
+        ds.load(params=params, x=xs[g], labels=labs[g])
+        plans.append(p)
+        states.append(ds)
+    torch.cuda.synchronize()
+    errs = [None] * 2
+
+    def body(g):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                states[g].step_grads(stream=st)
+            st.synchronize()
+        except Exception as e:   # surfaced below
+            errs[g] = e
+
+    th = [threading.Thread(target=body, args=(g,)) for g in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert all(e is None for e in errs), errs
+    for g in range(2):
+        got, head = plans[g].unpack_grads(states[g].grads.cpu().numpy())
+        assert abs(float(states[g].loss.cpu()) - ref[g][1]) <= 1e-5 * abs(ref[g][1])
+        for i, gi in enumerate(got):
+            if gi is None:
+                continue
+            for k in gi:
+                want = ref[0][2][i][k] + ref[1][2][i][k]
+                assert rel(gi[k], want) <= 1e-5, (g, i, k, rel(gi[k], want))
+    for c in comms:
+        c.free()
