@@ -34,9 +34,11 @@ BENCH_FLAGS = LB.FLAG_BALANCED_BANDS | LB.FLAG_FP_MERGE | LB.FLAG_REQUIRE_TC
 def full_check(net, B, prec, modes, params, x, dzl, flags=0, tag=""):
     store = C.bf16_store if prec == "bf16" else C.fp32_store
     ts_ref, _ = C.forward(net, params, x, store=store)
+    zl_fp64 = C.forward(net, params, x)[0][-1]   # true fp64 training, no storage rounding at all
     for mode, kw in modes:
         _, zl, g, ts = run_capture(net, B, prec, mode, params, x, dzl, flags=flags, **kw)
         assert rel(zl, ts_ref[-1]) <= TOL[prec], (tag, mode, kw, "zL vs plain oracle", rel(zl, ts_ref[-1]))
+        assert rel(zl, zl_fp64) <= TOL[prec], (tag, mode, kw, "zL vs fp64 oracle", rel(zl, zl_fp64))
         _, aux = validate_forward(net, params, ts, store, TOL[prec])
         g_ref = conditioned_grads(net, params, ts, aux, dzl)
         compare_grads(g, g_ref, TOL[prec], (tag, mode, str(kw)))
