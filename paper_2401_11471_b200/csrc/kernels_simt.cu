@@ -11,6 +11,7 @@
 #include <mutex>
 #include <set>
 
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -690,6 +691,43 @@ __global__ void k_pool_fwd8(PoolArgs A) {
     }
 }
 
+// Row-structured max-pool forward (any k / s / p, Cp % 8 == 0): grid.y = image rows of the band, one
+// 8-channel vector per thread with 32-bit index math (the flat grid-stride k_pool_fwd8 spent its issue
+// slots on 64-bit index division), max only (the forward needs no argmax; the backward recomputes it).
+template <typename T>
+__global__ void k_pool_fwd_rows8(PoolArgs A) {
+    griddep_wait();   // PDL: previous kernel complete and visible
+    griddep_launch();
+    const int CV = A.out.Cp / 8, Wo = A.out.W, rows = A.b - A.a;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= Wo * CV) return;
+    const int cv = v % CV, x = v / CV;
+    for (int ry = blockIdx.y; ry < A.B * rows; ry += gridDim.y) {
+        const int y = A.a + ry % rows, b = ry / rows;
+        float best[8];
+        bool first = true;
+        for (int ky = 0; ky < A.k; ++ky) {
+            const int g = y * A.s - A.p + ky;
+            if (!vhas(A.in, g)) continue;
+            const T *row = (const T *)A.in.p + voff(A.in, b, g, 0) + cv * 8;
+            for (int kx = 0; kx < A.k; ++kx) {
+                const int xi = x * A.s - A.p + kx;
+                if (xi < 0 || xi >= A.in.W) continue;
+                float w[8];
+                ld8(row + (size_t)xi * A.in.Cp, w);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) best[j] = first ? w[j] : fmaxf(best[j], w[j]);
+                first = false;
+            }
+        }
+        if (first) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) best[j] = 0.f;
+        }
+        st8((T *)A.out.p + voff(A.out, b, y, x) + cv * 8, best);
+    }
+}
+
 // gather: every input pixel checks the (at most ceil(k/s)^2) windows that contain it
 template <typename T>
 __global__ void k_pool_bwd8(PoolArgs A) {
@@ -1089,8 +1127,9 @@ cudaError_t simt_pool_fwd(int prec, const PoolArgs &a, cudaStream_t st) {
         dim3 g((rowv + tb - 1) / tb, a.B * (a.b - a.a));
         if (prec) launch_simt(k_pool2_fwd<bf16>, g, tb, 0, st, a); else launch_simt(k_pool2_fwd<float>, g, tb, 0, st, a);
     } else if (a.out.Cp % 8 == 0) {
-        n /= 8;
-        if (prec) launch_simt(k_pool_fwd8<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_fwd8<float>, grid_for(n), kT, 0, st, a);
+        const int rowv = a.out.W * (a.out.Cp / 8), tb = 128;
+        dim3 g((rowv + tb - 1) / tb, std::min(65535, a.B * (a.b - a.a)));
+        if (prec) launch_simt(k_pool_fwd_rows8<bf16>, g, tb, 0, st, a); else launch_simt(k_pool_fwd_rows8<float>, g, tb, 0, st, a);
     } else {
         if (prec) launch_simt(k_pool_fwd<bf16>, grid_for(n), kT, 0, st, a); else launch_simt(k_pool_fwd<float>, grid_for(n), kT, 0, st, a);
     }
