@@ -58,6 +58,9 @@ struct Run {
     // bneed only, no weight / parameter gradients; bn_level: the BN ops whose sums the sweep takes
     const std::vector<char> *fmask = nullptr, *bops = nullptr, *bneed = nullptr;
     const std::vector<int> *bn_level = nullptr;
+    // BN tail statistics sweep: tensor `redirect` (the tail BN's input) is written straight into the
+    // segment output's full-width checkpoint instead of its band buffer (-1: none)
+    int redirect = -1;
 };
 
 // Fork: side stream waits for everything enqueued so far on the main stream.
@@ -119,6 +122,7 @@ static void *ckpt_ptr(Run &R, int t) {
 static View act_view(Run &R, const Segment &S, int r, int t) {
     const TensorInfo &ti = R.P.t[t];
     if (t == S.in_t || t == S.out_t) return full_view(ckpt_ptr(R, t), ti);
+    if (t == R.redirect) return full_view(ckpt_ptr(R, S.out_t), R.P.t[S.out_t]);
     if (R.fp_merged) {   // S is the merged FP view of the segment (fp_lo / fp_b as lo / b)
         View v = band_view(R.ws + ti.act_fp_off, ti, S.lo[r][t], S.b[r][t]);
         v.bs = (long long)ti.cap_fp * ti.W * ti.Cp;
@@ -618,14 +622,16 @@ static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
                 banded = true;
             }
         }
+        const bool tail = S.bn_tail >= 0 && l + 1 == S.bn_fp_levels.size();
+        if (tail) R.redirect = P.op[S.bn_tail].in_t;
         if (banded) {
             R.fmask = &S.bn_fp_ops[l];
             for (int r = 0; r < (int)S.E.size(); ++r) {
                 Nvtx nv("FP BN statistics level %d band %d", (int)l, r);
-                if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) { R.fmask = nullptr; return st; }
+                if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) { R.fmask = nullptr; R.redirect = -1; return st; }
                 for (int j : S.bn_fp_levels[l]) {
                     const OpInfo &o = P.op[j];
-                    if (o.in_t == S.in_t) continue;
+                    if (o.in_t == S.in_t || tail) continue;
                     const int a = S.a[r][o.in_t], b = S.b[r][o.in_t];
                     if (b <= a) continue;
                     ++P.launches;
@@ -635,11 +641,35 @@ static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
             }
             R.fmask = nullptr;
         }
+        R.redirect = -1;
+        if (tail) {   // statistics of the tail BN's input over the full checkpoint it was written into
+            const OpInfo &o = P.op[S.bn_tail];
+            const TensorInfo &to = P.t[S.out_t];
+            ++P.launches;
+            ProfScope ps(R, 2, 0, S.bn_tail * 8 + 6);
+            CK(bn_stats(R.prec, full_view(ckpt_ptr(R, S.out_t), to), to.ck_lo, to.ck_lo + to.ck_rows, B,
+                        (double *)(R.ws + o.bn_sums_off), R.st));
+        }
         for (int j : S.bn_fp_levels[l]) {
             const OpInfo &o = P.op[j];
             const TensorInfo &ti = P.t[o.in_t];
             CK(bn_finalize_fwd(R.prec, (const double *)(R.ws + o.bn_sums_off), prm(R, o.b_off), prm(R, o.beta_off), ti.C,
                                ti.Cp, (double)B * ti.H * ti.W, (float *)(R.ws + o.bn_coef_off), R.st));
+        }
+        if (tail) {   // t = relu?(a*c + b + res) in place over the checkpoint (every element read, then written)
+            const OpInfo &o = P.op[S.bn_tail];
+            const TensorInfo &to = P.t[S.out_t];
+            const View v = full_view(ckpt_ptr(R, S.out_t), to);
+            View res;
+            if (o.d.res >= 0) res = full_view(ckpt_ptr(R, o.d.res), P.t[o.d.res]);
+            ++P.launches;
+            ProfScope ps(R, 2, 0, S.bn_tail * 8 + 6);
+            CK(bn_fwd(R.prec, v, res, v, (const float *)(R.ws + o.bn_coef_off), o.d.relu, to.ck_lo,
+                      to.ck_lo + to.ck_rows, B, R.st));
+            if (!P.capture.empty()) {
+                lrcnn_status cs = capture_rows(R, S.out_t, v, to.ck_lo, to.ck_lo + to.ck_rows);
+                if (cs != LRCNN_OK) return cs;
+            }
         }
     }
     return LRCNN_OK;
@@ -664,6 +694,7 @@ static lrcnn_status run_forward(Run &R) {
         if (sharded && S.in_t != 0 && !S.in_xfers.empty())
             if ((st = exchange(R, S, full_view(ckpt_ptr(R, S.in_t), R.P.t[S.in_t]), false)) != LRCNN_OK) return st;
         if (!S.bn_fp_levels.empty() && (st = bn_stat_sweeps(R, S)) != LRCNN_OK) return st;
+        if (S.bn_tail >= 0) continue;   // the last statistics sweep + the in-place BN produced the segment
         if (!S.fp_r0.empty()) {   // decoupled FP bands (N_FP < N_BP)
             Segment F = S;
             F.lo = S.fp_lo; F.a = S.fp_a; F.b = S.fp_b;

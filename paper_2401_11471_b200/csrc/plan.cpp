@@ -800,6 +800,15 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             S.bn_bp_need.push_back(need);
             S.bn_bp_ops.push_back(ops);
         }
+        {   // BN tail
+            const int jl = P.t[S.out_t].producer;
+            const OpInfo &o = P.op[jl];
+            const bool recomputes = !(P.seg.size() == 1 && S.E.size() == 1);
+            if (o.d.kind == LRCNN_OP_BN && recomputes && S.bn_fp_levels.back().size() == 1 &&
+                S.bn_fp_levels.back()[0] == jl && (o.d.res < 0 || o.d.res == S.in_t) && inside[o.in_t] &&
+                o.in_t != S.out_t && P.t[o.in_t].cons.size() == 1 && P.t[o.in_t].C == P.t[S.out_t].C)
+                S.bn_tail = jl;
+        }
     }
     // per-segment arena (band act/delta/carry), overlaid across segments
     size_t arena0 = ws, arena_max = 0;

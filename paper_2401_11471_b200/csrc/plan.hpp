@@ -99,6 +99,11 @@ struct Segment {
     // bn_bp_ops[k] and writes the delta of the tensors in bn_bp_need[k] only).  Per op / tensor id.
     std::vector<std::vector<int>> bn_fp_levels, bn_bp_levels;
     std::vector<std::vector<char>> bn_fp_ops, bn_bp_ops, bn_bp_need;
+    // BN tail: the segment output is produced by BN op bn_tail (alone in the last FP
+    // level, residual = none or the segment input, its input a band tensor only it reads): the last
+    // statistics sweep writes that input straight into the output checkpoint, the BN is then applied
+    // in place over the full map, and the FP sweep of the segment is skipped.  -1: none.
+    int bn_tail = -1;
 };
 
 struct ProfileSlot {
