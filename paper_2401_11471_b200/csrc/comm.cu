@@ -17,7 +17,7 @@
 typedef struct ncclComm *ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
-enum { kNcclUint8 = 1, kNcclFloat32 = 7 };
+enum { kNcclUint8 = 1, kNcclFloat32 = 7, kNcclFloat64 = 8 };
 enum { kNcclSum = 0 };
 
 namespace lrcnn {
@@ -159,6 +159,11 @@ static int host_allreduce(Comm *c, float *buf, size_t n, cudaStream_t st, std::s
 }
 
 __global__ void k_add_f32(float *dst, const float *src, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+
+__global__ void k_add_f64(double *dst, const double *src, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         dst[i] += src[i];
 }
@@ -328,3 +333,50 @@ lrcnn_status lrcnn_comm_free(lrcnn_comm *c) {
 }
 
 }  // extern "C"
+
+namespace lrcnn {
+
+// Batch statistics of training-mode BN under row sharding (engine.cu): small per-channel fp64 sums.
+int comm_allreduce_f64(Comm *c, double *buf, size_t n, cudaStream_t st, const char **err) {
+    static thread_local std::string e;
+    if (c->world == 1 || n == 0) return 0;
+    if (c->kind == 2) {
+        e = "the host-staged communicator has no fp64 all-reduce (training-mode BN with row sharding needs NCCL "
+            "or the loopback communicator)";
+        *err = e.c_str();
+        return 1;
+    }
+    if (c->kind == 0) {
+        NcclApi *api = nccl_api(e);
+        if (!api) { *err = e.c_str(); return 1; }
+        if (api->AllReduce(buf, buf, n, kNcclFloat64, kNcclSum, c->nccl, st)) {
+            e = "ncclAllReduce (fp64) failed"; *err = e.c_str(); return 1;
+        }
+        return 0;
+    }
+    LoopGroup &G = *c->group;
+    const int r = c->rank;
+    cudaEventRecord(G.ready[r], st);
+    G.ar[r] = (float *)buf;
+    G.barrier();
+    if (r == 0) {
+        for (int p = 1; p < G.world; ++p) {
+            cudaStreamWaitEvent(st, G.ready[p], 0);
+            k_add_f64<<<64, 256, 0, st>>>(buf, (const double *)G.ar[p], n);
+        }
+        cudaEventRecord(G.done[0], st);
+    }
+    G.barrier();
+    if (r != 0) {
+        cudaStreamWaitEvent(st, G.done[0], 0);
+        cudaMemcpyAsync(buf, G.ar[0], n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+        cudaEventRecord(G.done[r], st);
+    }
+    G.barrier();
+    if (r == 0)
+        for (int p = 1; p < G.world; ++p) cudaStreamWaitEvent(st, G.done[p], 0);
+    G.barrier();
+    return cudaGetLastError() == cudaSuccess ? 0 : (e = "loopback allreduce failed", *err = e.c_str(), 1);
+}
+
+}  // namespace lrcnn

@@ -600,6 +600,30 @@ static lrcnn_status launch_transposes(Run &R, cudaStream_t st) {
     return LRCNN_OK;
 }
 
+// zero-redundancy sharding, after every rank's first FP band: my first rows the rank above reads go out,
+// rank+1's first rows come in (one grouped exchange, every rank at the same point)
+static lrcnn_status zr_first_band(Run &R, const Segment &S) {
+    lrcnn_status st;
+    for (const Segment::ZrRows &z : S.zr_to_above) {
+        const TensorInfo &ti = R.P.t[z.t];
+        const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+        if ((st = copy_rows(R, ti, R.ws + ti.zr_out_off, z.r1 - z.r0,
+                            R.ws + ti.act_off + (size_t)(z.r0 - S.lo[0][z.t]) * rb, ti.cap,
+                            z.r1 - z.r0)) != LRCNN_OK) return st;
+    }
+    return zr_exchange(R, S, false);
+}
+
+// row sharding: a BN op's per-rank sums over the rows the rank computes -> sums over the whole map
+static lrcnn_status bn_allreduce(Run &R, double *buf, size_t n) {
+    if (R.P.opts.world <= 1) return LRCNN_OK;
+    if (!R.P.comm) return fail(LRCNN_E_STATE, "world > 1 needs lrcnn_plan_set_comm");
+    const char *err = nullptr;
+    if (comm_allreduce_f64((Comm *)R.P.comm, buf, n, R.st, &err))
+        return fail(LRCNN_E_NCCL, err ? err : "fp64 allreduce failed");
+    return LRCNN_OK;
+}
+
 // Training-mode BN statistics: per FP level of the segment's BN ops,
 // one band sweep computes the ops their inputs need (the lower levels' statistics are final) and sums
 // c, c^2 over the rows each band computes of every BN input (the interval rule gives each row to one
@@ -629,6 +653,7 @@ static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
             for (int r = 0; r < (int)S.E.size(); ++r) {
                 Nvtx nv("FP BN statistics level %d band %d", (int)l, r);
                 if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) { R.fmask = nullptr; R.redirect = -1; return st; }
+                if (r == 0 && zr_plan(P) && (st = zr_first_band(R, S)) != LRCNN_OK) { R.fmask = nullptr; return st; }
                 for (int j : S.bn_fp_levels[l]) {
                     const OpInfo &o = P.op[j];
                     if (o.in_t == S.in_t || tail) continue;
@@ -653,6 +678,7 @@ static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
         for (int j : S.bn_fp_levels[l]) {
             const OpInfo &o = P.op[j];
             const TensorInfo &ti = P.t[o.in_t];
+            if ((st = bn_allreduce(R, (double *)(R.ws + o.bn_sums_off), 2 * (size_t)ti.Cp)) != LRCNN_OK) return st;
             CK(bn_finalize_fwd(R.prec, (const double *)(R.ws + o.bn_sums_off), prm(R, o.b_off), prm(R, o.beta_off), ti.C,
                                ti.Cp, (double)B * ti.H * ti.W, (float *)(R.ws + o.bn_coef_off), R.st));
         }
@@ -710,16 +736,7 @@ static lrcnn_status run_forward(Run &R) {
         for (int r = 0; r < (int)S.E.size(); ++r) {
             Nvtx nv("FP seg %d band %d", (int)(&S - R.P.seg.data()), r);
             if ((st = band_forward(R, S, r, true, false)) != LRCNN_OK) return st;
-            if (r == 0 && zr_plan(R.P)) {   // my first rows the rank above reads, then the exchange
-                for (const Segment::ZrRows &z : S.zr_to_above) {
-                    const TensorInfo &ti = R.P.t[z.t];
-                    const size_t rb = (size_t)ti.W * ti.Cp * R.E;
-                    if ((st = copy_rows(R, ti, R.ws + ti.zr_out_off, z.r1 - z.r0,
-                                        R.ws + ti.act_off + (size_t)(z.r0 - S.lo[0][z.t]) * rb, ti.cap,
-                                        z.r1 - z.r0)) != LRCNN_OK) return st;
-                }
-                if ((st = zr_exchange(R, S, false)) != LRCNN_OK) return st;
-            }
+            if (r == 0 && zr_plan(R.P) && (st = zr_first_band(R, S)) != LRCNN_OK) return st;
         }
     }
     return LRCNN_OK;
@@ -1279,9 +1296,16 @@ static lrcnn_status run_backward(Run &R) {
             for (int j : S.bn_bp_levels[l]) {
                 const OpInfo &o = P.op[j];
                 const TensorInfo &ts = P.t[o.in_t];
+                // dgamma, dbeta += this rank's sums (the per-segment gradient buckets sum them over the
+                // ranks); p, q from the sums over every rank (recomputed after the all-reduce)
                 CK(bn_finalize_bwd((const double *)(R.ws + o.bn_S_off), (float *)(R.ws + o.bn_coef_off), ts.C, ts.Cp,
                                    (double)P.net.B * ts.H * ts.W, R.grads ? R.grads + o.b_off : nullptr,
                                    R.grads ? R.grads + o.beta_off : nullptr, R.st));
+                if (P.opts.world > 1) {
+                    if ((st = bn_allreduce(R, (double *)(R.ws + o.bn_S_off), 2 * (size_t)ts.Cp)) != LRCNN_OK) return st;
+                    CK(bn_finalize_bwd((const double *)(R.ws + o.bn_S_off), (float *)(R.ws + o.bn_coef_off), ts.C,
+                                       ts.Cp, (double)P.net.B * ts.H * ts.W, nullptr, nullptr, R.st));
+                }
             }
         }
         for (int r = N - 1; r >= 0; --r) {

@@ -192,8 +192,12 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             if (d.kind == LRCNN_OP_BN) {
                 // training-mode BN (f4): the statistics sweeps need disjoint band rows on one full map
                 if (opts->mode == LRCNN_OVERL) { err = "training-mode BN: OverL bands overlap (use 2PS or COLUMN)"; return LRCNN_E_UNSUPPORTED; }
-                if (opts->world > 1 && !(opts->flags & LRCNN_FLAG_DP)) { err = "training-mode BN with row sharding is not supported (use data-parallel replicas)"; return LRCNN_E_UNSUPPORTED; }
-                if (opts->flags & LRCNN_FLAG_ZERO_REDUNDANCY) { err = "training-mode BN with zero-redundancy sharding is not supported"; return LRCNN_E_UNSUPPORTED; }
+                // row sharding: the batch statistics are all-reduced over the ranks, so every row must be
+                // computed by exactly one rank -- zero-redundancy cuts only (OverL cuts recompute rows)
+                if (opts->world > 1 && !(opts->flags & (LRCNN_FLAG_DP | LRCNN_FLAG_ZERO_REDUNDANCY))) {
+                    err = "training-mode BN with row sharding needs LRCNN_FLAG_ZERO_REDUNDANCY (OverL cuts recompute rows)";
+                    return LRCNN_E_UNSUPPORTED;
+                }
             }
         } else { err = "bad op kind"; return LRCNN_E_ARG; }
         out.Cp = round_up(out.C, 8);
@@ -734,6 +738,11 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         for (int i : S.ops)
             if (P.op[i].d.kind == LRCNN_OP_BN) bns.push_back(i);
         if (bns.empty()) continue;
+        for (int j : bns)
+            if (world > 1 && P.op[j].in_t == S.in_t) {
+                err = "training-mode BN of a segment input with row sharding is not supported";
+                return LRCNN_E_UNSUPPORTED;
+            }
         std::vector<char> inside(T, 0);
         for (int i : S.ops) inside[i + 1] = 1;
         auto ins = [&](int i) {
@@ -804,7 +813,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             const int jl = P.t[S.out_t].producer;
             const OpInfo &o = P.op[jl];
             const bool recomputes = !(P.seg.size() == 1 && S.E.size() == 1);
-            if (o.d.kind == LRCNN_OP_BN && recomputes && S.bn_fp_levels.back().size() == 1 &&
+            if (o.d.kind == LRCNN_OP_BN && recomputes && world <= 1 && S.bn_fp_levels.back().size() == 1 &&
                 S.bn_fp_levels.back()[0] == jl && (o.d.res < 0 || o.d.res == S.in_t) && inside[o.in_t] &&
                 o.in_t != S.out_t && P.t[o.in_t].cons.size() == 1 && P.t[o.in_t].C == P.t[S.out_t].C)
                 S.bn_tail = jl;

@@ -174,3 +174,40 @@ def test_bn_data_parallel_replicas_fp32():
                 assert rel(gi[k], want) <= 1e-5, (g, i, k, rel(gi[k], want))
     for c in comms:
         c.free()
+
+
+@pytest.mark.parametrize("prec,world", [("fp32", 2), ("fp32", 3), ("bf16", 2)])
+def test_bn_zero_redundancy_row_sharding(prec, world):
+    """Training-mode BN with rows of every image split over ranks (LRCNN_FLAG_ZERO_REDUNDANCY,
+    loopback communicator): every rank sums its own rows, the fp64 sums are all-reduced before the
+    statistics and the backward sums are final, the ZR halo exchange runs in every statistics / sums
+    sweep.  Loss vs the oracle, every rank's all-reduced gradient vs the oracle conditioned on the
+    merged maps (fp32 1e-5; bf16 2e-2, BN parameters against their summation magnitude, R25)."""
+    from test_gpu_shard import run_sharded
+    net = WL.resnet50(H=192, W=48, width_div=4, blocks=(2, 1, 1, 1), bn_train=True)
+    B = 2
+    bf = prec == "bf16"
+    params = WL.make_params(net, seed=7, bias_scale=0.1, gamma_spread=0.2, bf16=bf)
+    x = WL.make_input(net, B, seed=7, bf16=bf)
+    lab = WL.make_labels(net, B)
+    _, loss_ref, _, _, _ = C.step(net, params, x, lab, 0.0)
+    res, ts = run_sharded(net, B, prec, world, params, x, lab, capture=True, flags=LB.FLAG_ZERO_REDUNDANCY,
+                          n_bands=2)
+    tol = TOL[prec]
+    store = C.bf16_store if bf else C.fp32_store
+    _, aux = validate_forward(net, params, ts, store, tol)
+    loss_c, dzl, hg, _ = C.head_forward_backward(ts[-1], params["head"], lab)
+    trace = {}
+    g_ref, _ = C.backward(net, params, ts, aux, dzl, need_dx=False, trace=trace)
+    for rank, (loss, (g, head)) in enumerate(res):
+        assert abs(loss - loss_ref) <= tol * abs(loss_ref), (rank, loss, loss_ref)
+        if not bf:
+            compare_grads(g, g_ref, tol, ("rank", rank))
+            continue
+        wg = [None if net["ops"][i]["kind"] == "bn" else gi for i, gi in enumerate(g)]
+        wr = [None if net["ops"][i]["kind"] == "bn" else gi for i, gi in enumerate(g_ref)]
+        compare_grads(wg, wr, tol, ("rank", rank))
+        for i, tr in trace.items():
+            for k in ("gamma", "beta"):
+                e = float(np.max(np.abs(g[i][k] - g_ref[i][k]) / np.maximum(tr[k], 1e-30)))
+                assert e <= tol, (rank, i, k, e)

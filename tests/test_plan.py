@@ -574,3 +574,11 @@ def test_bn_plans_vs_enumerator_and_errors():
     for i, op in enumerate(net["ops"]):
         if op["kind"] == "bn":
             assert plan.param(i, 1)[1] == plan.param(i, 2)[1] == 8
+
+
+def test_bn_row_sharding_needs_zero_redundancy():
+    net = WL.bn_chain(H=19, W=7, C=3, ch=8, n=4, res_every=2)
+    with pytest.raises(RuntimeError, match="ZERO_REDUNDANCY|not supported"):
+        LB.Plan(net, 2, mode="2ps", prec="fp32", n_bands=2, world=2, rank=0)
+    net = WL.bn_chain(H=64, W=7, C=3, ch=8, n=4, res_every=2)
+    LB.Plan(net, 2, mode="2ps", prec="fp32", n_bands=2, world=2, rank=0, flags=LB.FLAG_ZERO_REDUNDANCY)
