@@ -409,6 +409,10 @@ def main():
             lib_dp = False
             plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=flags, **kw)
     elif rows:
+        if a.bn_train and not a.zero_redundancy:   # batch statistics need every row on exactly one rank
+            a.zero_redundancy = True
+            if rank == 0:
+                print("bench: --bn-train with row sharding uses the zero-redundancy cuts", file=sys.stderr)
         rflags = flags | (LB.FLAG_ZERO_REDUNDANCY if a.zero_redundancy else 0)
         plan = LB.Plan(net, B, mode=a.mode, prec="bf16", flags=rflags, world=world, rank=rank, **kw)
         uid = [LB.Comm.nccl_unique_id() if rank == 0 else None]
