@@ -34,8 +34,11 @@ of its input, a strong dependency across all bands.  Exactly, in the order the d
      and back-propagates through the ops after j (their sums are known) down to the complete delta
      of j's output, summing dbeta_j = sum(da) and dgamma_j = sum(da*xh) over the band's rows of j's
      output.  Then the ordinary BP sweep, whose bn backward uses them (the textbook adjoint).
-2PS and column only (OverL's overlapping bands would count rows twice).  Negative control:
-per_band_stats=True normalises every band by its own rows' statistics.
+OverL (bands overlap): the statistics count each row once, in the first band that computes it; the
+backward sums add every band's partial delta (linear); the bn backward's batch-statistics terms
+(-gamma/sigma*(dbeta/M + xh*dgamma/M), a function of the row, not of the band's partial delta) are added
+once per row, in that same first band.  Negative control: per_band_stats=True normalises every band by
+its own rows' statistics.
 
 Negative controls (must NOT match the column oracle): share=False (cached rows
 replaced by zero rows -- the "padding redundancy" of Fig. 3(b)),
@@ -174,7 +177,7 @@ def seg_forward(plan, s, params, x_in, share=True, in_lo=0, bn=None, stop_at=Non
     return y, caches
 
 
-def _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn=None, bns=None):
+def _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn=None, bns=None, own=None):
     """Backward of op i over its output rows [a, b) given complete delta dt; adds into d[...].
     bn / bns: {op: (mean, var)} and {op: (dbeta, dgamma)} of the segment's bn ops (full-map sums)."""
     op = net["ops"][i]
@@ -188,8 +191,11 @@ def _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn=None, bns=Non
         da = dt * (t > 0) if op["relu"] else dt
         sig = np.sqrt(var + C.BN_EPS)[None, :, None, None]
         xh = (c - mean[None, :, None, None]) / sig
-        dc = params["convs"][i]["gamma"][None, :, None, None] / sig * (
-            da - dbeta[None, :, None, None] / M - xh * dgamma[None, :, None, None] / M)
+        g_s = params["convs"][i]["gamma"][None, :, None, None] / sig
+        stat = -g_s * (dbeta[None, :, None, None] / M + xh * dgamma[None, :, None, None] / M)
+        if own is not None:   # OverL: the statistics terms once per row (rows [own0, b) of this band)
+            stat[:, :, :max(0, own - a)] = 0.0
+        dc = g_s * da + stat
         _add_rows(d, src, a, dc)
         if op["res"] >= 0:
             _add_rows(d, op["res"], a, da)
@@ -283,7 +289,10 @@ def seg_backward(plan, s, params, x_in, dout, caches, carry_on=True, overl_avera
             if stop_at is not None and i == stop_at:
                 on_delta(held, a, b, dt)
                 break
-            _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn, bns)
+            own = None
+            if plan.mode == "overl" and net["ops"][i]["kind"] == "bn" and r > 0:
+                own = bands[r - 1][t][1]   # rows below the previous band's end belong to an earlier band
+            _op_rows_bwd(net, i, held, params, a, b, shp, dt, d, grads, bn, bns, own)
         carry = {}
         for t, (lo, a, b) in ranges.items():
             if t != out and lo < a:
@@ -300,16 +309,18 @@ def seg_bn_stats(plan, s, params, x_in):
     net, shp = plan.net, plan.shp
     bn = {}
     for j in _bn_ops(plan, s):
-        assert plan.mode != "overl", "training-mode BN: 2PS / column only"
         src = net["ops"][j]["src"]
         if src == plan.segs[s][0]:
             bn[j] = C.bn_stats(x_in)
             continue
         B, c, h, w = x_in.shape[0], shp[src][0], shp[src][1], shp[src][2]
-        acc = {"s1": np.zeros(c), "n": 0, "rows": []}
+        acc = {"s1": np.zeros(c), "n": 0, "rows": [], "end": 0}
 
         def on_rows(t, a, rows, src=src, acc=acc):
-            if t == src:
+            if t == src:   # rows [a, a + n): count those no earlier band computed (OverL overlap)
+                n_all = rows.shape[2]
+                rows = rows[:, :, max(0, acc["end"] - a):]
+                acc["end"] = max(acc["end"], a + n_all)
                 acc["s1"] += rows.sum(axis=(0, 2, 3))
                 acc["n"] += rows.shape[2]
                 acc["rows"].append(rows)

@@ -9,8 +9,9 @@ The bn op is pinned against things other than itself:
     sum(dc*xh) = gamma/sigma * dgamma * eps/(var+eps) per channel (a dropped term breaks one);
   * central finite differences of the whole step's loss;
   * the method's invariant: the row-centric executor with statistics / sums sweeps equals the column
-    oracle in fp64 for any band count and segmentation, and the per-band-statistics negative control
-    does not.
+    oracle in fp64 for any band count and segmentation, in 2PS and OverL (overlapping bands: each row
+    counted once, the statistics terms of the backward added once), and the per-band-statistics
+    negative control does not.
 CPU only."""
 import numpy as np
 import pytest
@@ -130,15 +131,16 @@ def test_bn_step_finite_differences():
             assert abs(fd - grads[i][k][idx]) <= 1e-6 * max(1.0, abs(fd)), (i, k, idx, fd, grads[i][k][idx])
 
 
+@pytest.mark.parametrize("mode", ["2ps", "overl"])
 @pytest.mark.parametrize("n_bands,seg", [(1, None), (2, None), (3, 3), (5, 1), (12, 3)])
-def test_rowcentric_bn_equals_column(n_bands, seg):
+def test_rowcentric_bn_equals_column(n_bands, seg, mode):
     net = _net(n=4, res_every=2, H=12, seg=seg)
     B = 2
     x = WL.make_input(net, B)
     lab = WL.make_labels(net, B)
     prm = WL.make_params(net, bias_scale=0.3, gamma_spread=0.3)
     _, loss0, g0, hg0, ts = C.step(net, prm, x, lab, 0.1)
-    plan = RC.Plan(net, "2ps", n_bands=n_bands)
+    plan = RC.Plan(net, mode, n_bands=n_bands)
     _, loss1, g1, hg1, zl = RC.step(plan, prm, x, lab, 0.1)
     assert abs(loss1 - loss0) <= 1e-12 * abs(loss0)
     np.testing.assert_allclose(zl, ts[-1], rtol=0, atol=1e-12)
@@ -149,14 +151,15 @@ def test_rowcentric_bn_equals_column(n_bands, seg):
             np.testing.assert_allclose(g1[i][k], g[k], rtol=1e-10, atol=1e-12 * np.abs(g[k]).max())
 
 
-def test_rowcentric_bn_resnet_blocks():
+@pytest.mark.parametrize("mode", ["2ps", "overl"])
+def test_rowcentric_bn_resnet_blocks(mode):
     net = WL.resnet50(H=40, W=16, width_div=16, blocks=(2, 1, 1, 1), bn_train=True, segments="p3")
     B = 2
     x = WL.make_input(net, B)
     lab = WL.make_labels(net, B)
     prm = WL.make_params(net, bias_scale=0.2, gamma_spread=0.3)
     _, loss0, g0, _, ts = C.step(net, prm, x, lab, 0.1)
-    plan = RC.Plan(net, "2ps", n_bands=3)
+    plan = RC.Plan(net, mode, n_bands=3)
     _, loss1, g1, _, zl = RC.step(plan, prm, x, lab, 0.1)
     assert abs(loss1 - loss0) <= 1e-11 * abs(loss0)
     for i, g in enumerate(g0):
