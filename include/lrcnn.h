@@ -82,11 +82,12 @@ enum { LRCNN_EPI_NONE = 0, LRCNN_EPI_BIAS = 1, LRCNN_EPI_AFFINE = 2 };
  *            batch-statistics adjoint.  Parameters gamma[C], beta[C] (plan layout).  The statistics are
  *            a dependency on EVERY row of t_src: lrcnn_forward_rows runs one statistics sweep per
  *            dependency level of a segment's BN ops before its FP sweep, lrcnn_backward_rows one sums
- *            sweep per level (reverse) before its BP sweep.  Modes COLUMN and 2PS: one
- *            GPU, data-parallel replicas (per-replica statistics), or rows sharded with
+ *            sweep per level (reverse) before its BP sweep.  One GPU, data-parallel replicas (per-replica statistics), or rows sharded with
  *            LRCNN_FLAG_ZERO_REDUNDANCY (statistics over the whole map: fp64 sums all-reduced over the
- *            ranks; NCCL or loopback communicator).  OverL bands or OverL rank cuts (rows computed twice)
- *            and a BN of a segment input under sharding return LRCNN_E_UNSUPPORTED.
+ *            ranks; NCCL or loopback communicator).  Modes COLUMN, 2PS and OverL (overlapping bands:
+ *            each row counted once, the backward's statistics terms added once per row).  OverL rank
+ *            cuts (rows computed by two ranks) and a BN of a segment input under sharding return
+ *            LRCNN_E_UNSUPPORTED.
  * seg_end != 0 stores the op's output as a full-width checkpoint (segment boundary). */
 typedef struct {
     int kind;

@@ -11,7 +11,8 @@
 //   k_bn_finalize_bwd p, q of  dc = a*da + p + q*c  (the batch-statistics adjoint
 //                     dc = a*(da - S1/M - xh*S2/M)); dgamma += S2, dbeta += S1
 //   k_bn_bwd          delta(src) (+)= gate * (a*da + p + q*c) on band rows (written, not accumulated,
-//                     when the BN op is the only writer of those rows)
+//                     when the BN op is the only writer of those rows); rows below cs get a*da only
+//                     (OverL: the statistics terms p + q*c once per row, in the first band computing it)
 // All arithmetic fp32, sums fp64; activations act_t (fp32 or bf16), NHWC rows of a View, channels
 // processed as 8-element vectors (Cp is a multiple of 8).  coef layout: [6][Cp] floats
 // (a, b, p, q, mean, invstd); channels >= C get a = b = p = q = 0 (padded channels stay zero).
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd(View in, View res, View o
 // write != 0: delta(src) rows are produced by this kernel alone (single writer) -- not read
 template <typename T>
 __global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx, View act, int gate, int write,
-                                                        const float *coef, int a, int b, int B) {
+                                                        const float *coef, int a, int b, int B, int cs) {
     const int Cp = dx.Cp, G = Cp / 8, rows = b - a, nv = dx.W * G, nrows = B * rows;
     const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (v0 >= nv) return;
@@ -231,11 +232,13 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx,
     for (int r0 = blockIdx.y * kRowsPer; r0 < nrows; r0 += gridDim.y * kRowsPer) {
         Raw8<T> rd[kRowsPer], rv[kRowsPer], ro[kRowsPer], rm[kRowsPer];
         long long off[kRowsPer];
+        bool stat[kRowsPer];
 #pragma unroll
         for (int u = 0; u < kRowsPer; ++u) {
             const int ry = min(r0 + u, nrows - 1);
             const int bi = ry / rows, y = a + ry % rows;
             off[u] = bn_off(dx, bi, y, xx) + g * 8;
+            stat[u] = y >= cs;
             ldraw((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, rd[u]);
             ldraw((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, rv[u]);
             if (!write) ldraw((const T *)dx.p + off[u], ro[u]);
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx,
             if (gate) unraw(rm[u], m);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const float dc = fmaf(ca[k], d[k], fmaf(cq[k], v[k], cp[k]));
+                const float dc = stat[u] ? fmaf(ca[k], d[k], fmaf(cq[k], v[k], cp[k])) : ca[k] * d[k];
                 o[k] = (gate && m[k] <= 0.f) ? 0.f : (write ? dc : o[k] + dc);
             }
             if (r0 + u < nrows) store8((T *)dx.p + off[u], o);
@@ -323,13 +326,13 @@ cudaError_t bn_fwd(int prec, const View &in, const View &res, const View &out, c
 }
 
 cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, const View &act, int gate, int write,
-                   const float *coef, int a, int b, int B, cudaStream_t st) {
+                   const float *coef, int a, int b, int B, int cs, cudaStream_t st) {
     const long long n = (long long)B * (b - a) * dx.W * (dx.Cp / 8);
     if (n <= 0) return cudaSuccess;
     if (dx.Cp % 8) return cudaErrorInvalidValue;
     const dim3 grid = grid_rows(dx.W * (dx.Cp / 8), B * (b - a));
-    if (prec) k_bn_bwd<bf16><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B);
-    else k_bn_bwd<float><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B);
+    if (prec) k_bn_bwd<bf16><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B, cs);
+    else k_bn_bwd<float><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B, cs);
     return cudaGetLastError();
 }
 

@@ -657,7 +657,9 @@ static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
                 for (int j : S.bn_fp_levels[l]) {
                     const OpInfo &o = P.op[j];
                     if (o.in_t == S.in_t || tail) continue;
-                    const int a = S.a[r][o.in_t], b = S.b[r][o.in_t];
+                    // rows no earlier band computed (OverL bands overlap; 2PS bands are disjoint)
+                    const int a = r > 0 ? std::max(S.a[r][o.in_t], S.b[r - 1][o.in_t]) : S.a[r][o.in_t];
+                    const int b = S.b[r][o.in_t];
                     if (b <= a) continue;
                     ++P.launches;
                     ProfScope ps(R, 2, 0, j * 8 + 6);
@@ -903,8 +905,11 @@ static lrcnn_status op_backward(Run &R, const Segment &S, int s, int r, int i) {
             const View x = act_view(R, S, r, o.in_t);
             ++P.launches;
             ProfScope ps(R, 2, 0, i * 8 + 7);
+            // OverL: rows an earlier band also computed get only the linear term (the statistics terms
+            // once per row); 2PS bands are disjoint (a == the previous band's end)
+            const int cs = r > 0 ? std::max(a, S.b[r - 1][t]) : a;
             CK(bn_bwd(R.prec, dy, x, dlt_view(R, S, s, r, o.in_t), x, P.t[o.in_t].relu,
-                      delta_overwrite(P, S, o.in_t) ? 1 : 0, coef, a, b, P.net.B, R.st));
+                      delta_overwrite(P, S, o.in_t) ? 1 : 0, coef, a, b, P.net.B, cs, R.st));
         }
         if (o.d.res > 0 && need(o.d.res)) {
             EltArgs A;

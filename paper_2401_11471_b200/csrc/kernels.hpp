@@ -118,7 +118,7 @@ cudaError_t bn_sums(int prec, const View &dy, const View &x, const float *coef, 
 cudaError_t bn_finalize_bwd(const double *S, float *coef, int C, int Cp, double M, float *dgamma, float *dbeta,
                             cudaStream_t st);
 cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, const View &act, int gate, int write,
-                   const float *coef, int a, int b, int B, cudaStream_t st);
+                   const float *coef, int a, int b, int B, int cs, cudaStream_t st);
 
 void simt_set_pdl(bool on);   // programmatic dependent launch on / off for this host thread (profiling)
 

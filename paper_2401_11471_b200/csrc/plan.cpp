@@ -191,7 +191,6 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             out.C = in.C; out.H = in.H; out.W = in.W; out.relu = d.relu ? 1 : 0;
             if (d.kind == LRCNN_OP_BN) {
                 // training-mode BN (f4): the statistics sweeps need disjoint band rows on one full map
-                if (opts->mode == LRCNN_OVERL) { err = "training-mode BN: OverL bands overlap (use 2PS or COLUMN)"; return LRCNN_E_UNSUPPORTED; }
                 // row sharding: the batch statistics are all-reduced over the ranks, so every row must be
                 // computed by exactly one rank -- zero-redundancy cuts only (OverL cuts recompute rows)
                 if (opts->world > 1 && !(opts->flags & (LRCNN_FLAG_DP | LRCNN_FLAG_ZERO_REDUNDANCY))) {

@@ -20,10 +20,11 @@ from paper_2401_11471_b200 import lrcnn as LB  # noqa: E402
 def test_bn_chain_fp32_bands_and_segments():
     """conv3x3 -> bn(+residual every 2 layers) x4, ragged bands incl. 1-row bands, a checkpoint."""
     net = WL.bn_chain(H=19, W=11, C=3, ch=8, n=4, res_every=2)
-    check(net, 2, "fp32", ["column", "2ps"], [{"band_rows": 1}, {"band_rows": 4}, {"n_bands": 3}],
-          bias=0.3, gspread=0.4, plain_grads=True)
+    check(net, 2, "fp32", ["column", "2ps", "overl"], [{"band_rows": 1}, {"band_rows": 4}, {"n_bands": 3}],
+          bias=0.3, gspread=0.4, plain_grads=True, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
     net["ops"][3]["seg_end"] = True
-    check(net, 2, "fp32", ["2ps"], [{"n_bands": 2}, {"band_rows": 3}], bias=0.3, gspread=0.4, plain_grads=True)
+    check(net, 2, "fp32", ["2ps", "overl"], [{"n_bands": 2}, {"band_rows": 3}], bias=0.3, gspread=0.4,
+          plain_grads=True, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
 
 
 def check_bn_bf16(net, B, modes, kws, dzl_kind, flags=0):
@@ -64,10 +65,12 @@ def test_bn_resnet_reduced_fp32_and_bf16():
     blocks, stem BN before the 3x3/s2 max-pool), per-stage and per-block checkpoints."""
     for segs in ("stage", "block"):
         net = WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True, segments=segs)
-        check(net, 2, "fp32", ["column", "2ps"], [{"n_bands": 3}], bias=0.1, gspread=0.2)
+        check(net, 2, "fp32", ["column", "2ps", "overl"], [{"n_bands": 3}], bias=0.1, gspread=0.2,
+              flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
         check(net, 2, "fp32", ["2ps"], [{"n_bands": 3}], bias=0.1, gspread=0.2, dzl_kind="head")
         for kind in ("head", "random"):
-            check_bn_bf16(net, 2, ["column", "2ps"], [{"n_bands": 3}, {"band_rows": 2}], kind)
+            check_bn_bf16(net, 2, ["column", "2ps", "overl"], [{"n_bands": 3}, {"band_rows": 2}], kind,
+                          flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
 
 
 def test_bn_step_matches_oracle_fp32():

@@ -558,7 +558,7 @@ def test_coordination_counters_closed_form(nb):
 
 def test_bn_plans_vs_enumerator_and_errors():
     """Training-mode BN ops (f4) read their input 1:1: the interval rule of a BN net equals the
-    brute-force enumeration; OverL, row sharding and zero redundancy are refused (R24)."""
+    brute-force enumeration (2PS and OverL); row sharding with OverL cuts is refused (R23)."""
     nets = [WL.bn_chain(H=19, W=7, C=3, ch=8, n=4, res_every=2),
             WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True),
             WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True, segments="block")]
@@ -566,9 +566,10 @@ def test_bn_plans_vs_enumerator_and_errors():
         for kw in ({"band_rows": 1}, {"n_bands": 3}, {"n_bands": 1}):
             _check_plan_vs_enum(net, "2ps", **kw)
     net = nets[0]
-    for mode, kw in (("overl", {}), ("2ps", {"world": 2, "rank": 0})):
-        with pytest.raises(RuntimeError, match="UNSUPPORTED|not supported|overlap"):
-            LB.Plan(net, 2, mode=mode, prec="fp32", n_bands=2, **kw)
+    for kw in ({"n_bands": 3}, {"band_rows": 2}):
+        _check_plan_vs_enum(net, "overl", **kw)
+    with pytest.raises(RuntimeError, match="UNSUPPORTED|not supported|ZERO_REDUNDANCY"):
+        LB.Plan(net, 2, mode="overl", prec="fp32", n_bands=2, world=2, rank=0)
     # parameters: gamma / beta per BN op in the flat layout
     plan = LB.Plan(net, 2, mode="2ps", prec="fp32", n_bands=2)
     for i, op in enumerate(net["ops"]):
