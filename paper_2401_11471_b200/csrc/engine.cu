@@ -61,6 +61,9 @@ struct Run {
     // BN tail statistics sweep: tensor `redirect` (the tail BN's input) is written straight into the
     // segment output's full-width checkpoint instead of its band buffer (-1: none)
     int redirect = -1;
+    // FP of a segment with training-mode BN: tensors with a stash slot (Segment::stash_off) live full-width
+    // there instead of in their band buffers
+    bool stash = false;
 };
 
 // Fork: side stream waits for everything enqueued so far on the main stream.
@@ -123,6 +126,10 @@ static View act_view(Run &R, const Segment &S, int r, int t) {
     const TensorInfo &ti = R.P.t[t];
     if (t == S.in_t || t == S.out_t) return full_view(ckpt_ptr(R, t), ti);
     if (t == R.redirect) return full_view(ckpt_ptr(R, S.out_t), R.P.t[S.out_t]);
+    if (R.stash && (size_t)t < S.stash_off.size() && S.stash_off[t] != (size_t)-1) {
+        View v{R.ws + S.stash_off[t], 0, ti.H, ti.H, ti.W, ti.Cp, (long long)ti.H * ti.W * ti.Cp};
+        return v;
+    }
     if (R.fp_merged) {   // S is the merged FP view of the segment (fp_lo / fp_b as lo / b)
         View v = band_view(R.ws + ti.act_fp_off, ti, S.lo[r][t], S.b[r][t]);
         v.bs = (long long)ti.cap_fp * ti.W * ti.Cp;
@@ -423,6 +430,7 @@ static lrcnn_status band_forward_merged(Run &R, const Segment &S, const Segment 
     R.fp_merged = true;
     for (size_t q = 0; q < S.ops.size(); ++q) {
         const int i = S.ops[q];
+        if (R.fmask && !(*R.fmask)[i]) continue;   // BN input stash: its producers ran in a statistics sweep
         if (q >= 2 && S.ops[q - 1] == i - 1 && bneck_at(P, S, i - 2) && S.ops[q - 2] == i - 2) continue;
         if (q >= 1 && bneck_at(P, S, i - 1) && S.ops[q - 1] == i - 1) continue;
         if (bneck_at(P, S, i) && q + 2 < S.ops.size() && S.ops[q + 1] == i + 1 && S.ops[q + 2] == i + 2) {
@@ -444,6 +452,7 @@ static lrcnn_status band_forward_merged(Run &R, const Segment &S, const Segment 
     for (int r = r0; r < r1 && r + 1 < N; ++r) {
         for (int t : S.tensors) {
             if (t == S.out_t) continue;
+            if (R.fmask && !(*R.fmask)[P.t[t].producer]) continue;
             const TensorInfo &ti = P.t[t];
             const int rows = ti.cache_rows[r];
             if (rows <= 0) continue;
@@ -506,6 +515,7 @@ static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cach
     if (save_cache && P.opts.mode == LRCNN_2PS && r + 1 < (int)S.E.size()) {
         for (int t : S.tensors) {
             if (t == S.out_t) continue;
+            if (R.fmask && !(*R.fmask)[P.t[t].producer]) continue;   // not computed in this sweep
             const TensorInfo &ti = P.t[t];
             int rows = ti.cache_rows[r];
             if (rows <= 0) continue;
@@ -628,7 +638,15 @@ static lrcnn_status bn_allreduce(Run &R, double *buf, size_t n) {
 // one band sweep computes the ops their inputs need (the lower levels' statistics are final) and sums
 // c, c^2 over the rows each band computes of every BN input (the interval rule gives each row to one
 // band); then mean / var -> the affine coefficients the FP sweep applies.
+static lrcnn_status bn_stat_sweeps_impl(Run &R, const Segment &S);
 static lrcnn_status bn_stat_sweeps(Run &R, const Segment &S) {
+    R.stash = true;
+    const lrcnn_status st = bn_stat_sweeps_impl(R, S);
+    R.stash = false; R.fmask = nullptr; R.redirect = -1;
+    return st;
+}
+
+static lrcnn_status bn_stat_sweeps_impl(Run &R, const Segment &S) {
     Plan &P = R.P;
     lrcnn_status st;
     const int B = P.net.B;
@@ -723,6 +741,13 @@ static lrcnn_status run_forward(Run &R) {
             if ((st = exchange(R, S, full_view(ckpt_ptr(R, S.in_t), R.P.t[S.in_t]), false)) != LRCNN_OK) return st;
         if (!S.bn_fp_levels.empty() && (st = bn_stat_sweeps(R, S)) != LRCNN_OK) return st;
         if (S.bn_tail >= 0) continue;   // the last statistics sweep + the in-place BN produced the segment
+        struct StashScope {   // BN segments: the FP sweep reads the stashed BN inputs
+            Run &R; bool on;
+            StashScope(Run &r_, const Segment &S) : R(r_), on(!S.bn_fp_levels.empty()) {
+                if (on) { R.stash = true; R.fmask = &S.bn_fp_final; }
+            }
+            ~StashScope() { if (on) { R.stash = false; R.fmask = nullptr; } }
+        } stash_scope(R, S);
         if (!S.fp_r0.empty()) {   // decoupled FP bands (N_FP < N_BP)
             Segment F = S;
             F.lo = S.fp_lo; F.a = S.fp_a; F.b = S.fp_b;

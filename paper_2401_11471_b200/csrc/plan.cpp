@@ -749,14 +749,17 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             if (P.op[i].d.res >= 0) v.push_back(P.op[i].d.res);
             return v;
         };
-        // ancestors of tensor t inside the segment (ops), by a reverse walk
-        auto anc_ops = [&](const std::vector<int> &roots) {
+        // ancestors of tensor t inside the segment (ops), by a reverse walk; tensors with cut[t] != 0 are
+        // available (stashed by an earlier sweep): their producers are not needed
+        std::vector<char> nocut(T, 0);
+        auto anc_ops = [&](const std::vector<int> &roots, const std::vector<char> &cut) {
             std::vector<char> op_in(n_ops, 0), seen(T, 0);
             std::vector<int> st = roots;
             while (!st.empty()) {
                 const int t = st.back(); st.pop_back();
                 if (seen[t] || !inside[t]) continue;
                 seen[t] = 1;
+                if (cut[t]) continue;
                 const int i = P.t[t].producer;
                 op_in[i] = 1;
                 for (int u : ins(i)) st.push_back(u);
@@ -766,7 +769,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         std::vector<int> lvl(n_ops, -1), rlvl(n_ops, -1);
         for (int j : bns) {   // op order is topological: ancestors first
             int l = 0;
-            std::vector<char> a = anc_ops({P.op[j].d.src});
+            std::vector<char> a = anc_ops({P.op[j].d.src}, nocut);
             for (int k : bns)
                 if (k != j && a[k]) l = std::max(l, lvl[k] + 1);
             lvl[j] = l;
@@ -793,10 +796,45 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         S.bn_fp_levels.assign(nf, {});
         S.bn_bp_levels.assign(nb, {});
         for (int j : bns) { S.bn_fp_levels[lvl[j]].push_back(j); S.bn_bp_levels[rlvl[j]].push_back(j); }
+        // BN tail (below) and input stash: the inputs of the other BN ops, full-width, overlaying the delta
+        // buffers (BP only) while they fit; one GPU (a rank's rows would need the halo rows too)
+        const bool recomputes = !(P.seg.size() == 1 && S.E.size() == 1);
+        {
+            const int jl = P.t[S.out_t].producer;
+            const OpInfo &o = P.op[jl];
+            if (o.d.kind == LRCNN_OP_BN && recomputes && world <= 1 && S.bn_fp_levels.back().size() == 1 &&
+                S.bn_fp_levels.back()[0] == jl && (o.d.res < 0 || o.d.res == S.in_t) && inside[o.in_t] &&
+                o.in_t != S.out_t && P.t[o.in_t].cons.size() == 1 && P.t[o.in_t].C == P.t[S.out_t].C)
+                S.bn_tail = jl;
+        }
+        S.stash_off.assign(T, (size_t)-1);
+        std::vector<int> stash_level(T, -1);
+        if (recomputes && world <= 1) {
+            const size_t r0 = P.dfull_off[0];
+            const size_t r1 = P.seg.size() > 1 ? P.dfull_off[1] + dmax[1] : P.dfull_off[0] + dmax[0];
+            size_t used = 0;
+            for (int j : bns) {
+                const int c = P.op[j].in_t;
+                if (j == S.bn_tail || !inside[c] || c == S.out_t || P.t[c].cons.size() != 1) continue;
+                const size_t bytes = align_up(B * (size_t)P.t[c].H * rowbytes(c));
+                if (r0 + used + bytes > r1) continue;
+                S.stash_off[c] = r0 + used;
+                stash_level[c] = lvl[j];
+                used += bytes;
+            }
+        }
         for (int l = 0; l < nf; ++l) {
             std::vector<int> roots;
             for (int j : S.bn_fp_levels[l]) roots.push_back(P.op[j].d.src);
-            S.bn_fp_ops.push_back(anc_ops(roots));
+            std::vector<char> cut(T, 0);   // stashed by an earlier level's sweep
+            for (int t = 0; t < T; ++t) cut[t] = stash_level[t] >= 0 && stash_level[t] < l;
+            S.bn_fp_ops.push_back(anc_ops(roots, cut));
+        }
+        {   // the FP sweep: every op but the producers of stashed tensors
+            S.bn_fp_final.assign(n_ops, 0);
+            for (int i : S.ops) S.bn_fp_final[i] = 1;
+            for (int t = 0; t < T; ++t)
+                if (stash_level[t] >= 0) S.bn_fp_final[P.t[t].producer] = 0;
         }
         for (int l = 0; l < nb; ++l) {
             std::vector<int> roots;
@@ -807,15 +845,6 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             for (int j : S.bn_bp_levels[l]) ops[j] = 0;
             S.bn_bp_need.push_back(need);
             S.bn_bp_ops.push_back(ops);
-        }
-        {   // BN tail
-            const int jl = P.t[S.out_t].producer;
-            const OpInfo &o = P.op[jl];
-            const bool recomputes = !(P.seg.size() == 1 && S.E.size() == 1);
-            if (o.d.kind == LRCNN_OP_BN && recomputes && world <= 1 && S.bn_fp_levels.back().size() == 1 &&
-                S.bn_fp_levels.back()[0] == jl && (o.d.res < 0 || o.d.res == S.in_t) && inside[o.in_t] &&
-                o.in_t != S.out_t && P.t[o.in_t].cons.size() == 1 && P.t[o.in_t].C == P.t[S.out_t].C)
-                S.bn_tail = jl;
         }
     }
     // per-segment arena (band act/delta/carry), overlaid across segments

@@ -104,6 +104,13 @@ struct Segment {
     // statistics sweep writes that input straight into the output checkpoint, the BN is then applied
     // in place over the full map, and the FP sweep of the segment is skipped.  -1: none.
     int bn_tail = -1;
+    // BN input stash: in the FP of this segment, the input c of a BN op is written once,
+    // full-width, at workspace offset stash_off[c] (overlaying the full-width delta buffers, which only
+    // the BP uses), and later statistics sweeps and the FP sweep read it instead of recomputing its
+    // producers; bn_fp_ops are cut at the stashed tensors, bn_fp_final = the FP sweep's ops.  Per tensor
+    // id, (size_t)-1 = not stashed.
+    std::vector<size_t> stash_off;
+    std::vector<char> bn_fp_final;
 };
 
 struct ProfileSlot {
