@@ -64,6 +64,8 @@ struct Run {
     // FP of a segment with training-mode BN: tensors with a stash slot (Segment::stash_off) live full-width
     // there instead of in their band buffers
     bool stash = false;
+    // BP of a segment with a BN stash: tensors with a slot in bp_stash (absolute offsets) live there
+    const std::vector<size_t> *bp_stash = nullptr;
 };
 
 // Fork: side stream waits for everything enqueued so far on the main stream.
@@ -128,6 +130,10 @@ static View act_view(Run &R, const Segment &S, int r, int t) {
     if (t == R.redirect) return full_view(ckpt_ptr(R, S.out_t), R.P.t[S.out_t]);
     if (R.stash && (size_t)t < S.stash_off.size() && S.stash_off[t] != (size_t)-1) {
         View v{R.ws + S.stash_off[t], 0, ti.H, ti.H, ti.W, ti.Cp, (long long)ti.H * ti.W * ti.Cp};
+        return v;
+    }
+    if (R.bp_stash && (size_t)t < R.bp_stash->size() && (*R.bp_stash)[t] != (size_t)-1) {
+        View v{R.ws + (*R.bp_stash)[t], 0, ti.H, ti.H, ti.W, ti.Cp, (long long)ti.H * ti.W * ti.Cp};
         return v;
     }
     if (R.fp_merged) {   // S is the merged FP view of the segment (fp_lo / fp_b as lo / b)
@@ -1313,8 +1319,21 @@ static lrcnn_status run_backward(Run &R) {
             if (r == N - 1 && zr_plan(P) && (st = zr_exchange(R, S, true)) != LRCNN_OK) return st;
             return LRCNN_OK;
         };
+        // BN BP stash: the first sweep of the segment writes the stashed BN inputs, the later ones
+        // recompute only the other ops (R.fmask in band_forward)
+        struct BpStash {
+            Run &R;
+            BpStash(Run &r_, const Segment &S) : R(r_) { if (!S.bp_stash_off.empty()) R.bp_stash = &S.bp_stash_off; }
+            ~BpStash() { R.bp_stash = nullptr; R.fmask = nullptr; }
+        } bp_stash_scope(R, S);
+        bool first_sweep = true;
+        auto next_sweep = [&]() {
+            if (!first_sweep && !S.bn_bp_recompute.empty()) R.fmask = &S.bn_bp_recompute;
+            first_sweep = false;
+        };
         // training-mode BN: one sums sweep per BP level, deepest BN ops first
         for (size_t l = 0; l < S.bn_bp_levels.size(); ++l) {
+            next_sweep();
             for (int j : S.bn_bp_levels[l])
                 CK(cudaMemsetAsync(R.ws + P.op[j].bn_S_off, 0, 2 * (size_t)P.t[P.op[j].out_t].Cp * sizeof(double), R.st));
             R.bops = &S.bn_bp_ops[l]; R.bneed = &S.bn_bp_need[l]; R.bn_level = &S.bn_bp_levels[l];
@@ -1338,6 +1357,7 @@ static lrcnn_status run_backward(Run &R) {
                 }
             }
         }
+        next_sweep();
         for (int r = N - 1; r >= 0; --r) {
             Nvtx nv("BP seg %d band %d", s, r);
             if ((st = band_bp(r)) != LRCNN_OK) return st;

@@ -732,6 +732,7 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
         M.other += ws - o0;
     }
     // training-mode BN levels per segment (Segment::bn_*)
+    size_t bp_stash_need = 0;
     for (Segment &S : P.seg) {
         std::vector<int> bns;
         for (int i : S.ops)
@@ -836,6 +837,28 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             for (int t = 0; t < T; ++t)
                 if (stash_level[t] >= 0) S.bn_fp_final[P.t[t].producer] = 0;
         }
+        if (recomputes && world <= 1 && S.bn_bp_levels.size() > 0) {
+            // BP stash: BN inputs (not the tail's) while they fit in one boundary map's bytes; offsets
+            // relative to the BP stash region, allocated below (the largest segment's need)
+            const size_t budget = std::max(dmax[0], dmax[1]);
+            size_t used = 0;
+            S.bp_stash_off.assign(T, (size_t)-1);
+            S.bn_bp_recompute.assign(n_ops, 0);
+            for (int i : S.ops) S.bn_bp_recompute[i] = 1;
+            bool any = false;
+            for (int j : bns) {
+                const int c = P.op[j].in_t;
+                if (j == S.bn_tail || !inside[c] || c == S.out_t || P.t[c].cons.size() != 1) continue;
+                const size_t bytes = align_up(B * (size_t)P.t[c].H * rowbytes(c));
+                if (used + bytes > budget) continue;
+                S.bp_stash_off[c] = used;
+                S.bn_bp_recompute[P.t[c].producer] = 0;
+                used += bytes;
+                any = true;
+            }
+            if (!any) { S.bp_stash_off.clear(); S.bn_bp_recompute.clear(); }
+            bp_stash_need = std::max(bp_stash_need, used);
+        }
         for (int l = 0; l < nb; ++l) {
             std::vector<int> roots;
             for (int j : S.bn_bp_levels[l]) roots.push_back(P.op[j].out_t);
@@ -846,6 +869,13 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             S.bn_bp_need.push_back(need);
             S.bn_bp_ops.push_back(ops);
         }
+    }
+    if (bp_stash_need) {   // BN BP stash region (shared by the segments: one segment's BP at a time)
+        const size_t base = alloc(bp_stash_need);
+        M.other += bp_stash_need;
+        for (Segment &S : P.seg)
+            for (size_t &o : S.bp_stash_off)
+                if (o != (size_t)-1) o += base;
     }
     // per-segment arena (band act/delta/carry), overlaid across segments
     size_t arena0 = ws, arena_max = 0;

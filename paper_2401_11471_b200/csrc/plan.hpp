@@ -111,6 +111,11 @@ struct Segment {
     // id, (size_t)-1 = not stashed.
     std::vector<size_t> stash_off;
     std::vector<char> bn_fp_final;
+    // BP stash: the segment's first backward sweep writes these BN inputs full-width into a region of
+    // their own (bp_stash_off, absolute workspace offsets), the later sweeps recompute only the ops in
+    // bn_bp_recompute (not their producers).  Empty: none.
+    std::vector<size_t> bp_stash_off;
+    std::vector<char> bn_bp_recompute;
 };
 
 struct ProfileSlot {
