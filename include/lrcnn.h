@@ -84,7 +84,7 @@ enum { LRCNN_EPI_NONE = 0, LRCNN_EPI_BIAS = 1, LRCNN_EPI_AFFINE = 2 };
  *            dependency level of a segment's BN ops before its FP sweep, lrcnn_backward_rows one sums
  *            sweep per level (reverse) before its BP sweep.  One GPU, data-parallel replicas (per-replica statistics), or rows sharded with
  *            LRCNN_FLAG_ZERO_REDUNDANCY (statistics over the whole map: fp64 sums all-reduced over the
- *            ranks; NCCL or loopback communicator).  Modes COLUMN, 2PS and OverL (overlapping bands:
+ *            ranks -- NCCL, loopback, or host-staged as an all-gather through the exchange callback).  Modes COLUMN, 2PS and OverL (overlapping bands:
  *            each row counted once, the backward's statistics terms added once per row).  OverL rank
  *            cuts (rows computed by two ranks) and a BN of a segment input under sharding return
  *            LRCNN_E_UNSUPPORTED.
@@ -292,6 +292,8 @@ LRCNN_API lrcnn_status lrcnn_comm_init_loopback(void *group, int rank, lrcnn_com
  *       to rank peer[i]; send[i] = 0: receive bytes[i] from peer[i] into host_ptr[i] (every rank posts
  *       its sends and receives of one exchange together);
  *   allreduce(user, host_buf, n): in-place sum of n floats over all ranks;
+ * (fp64 sums -- training-mode BN statistics -- go through exchange as an all-gather and are summed on
+ * the host in rank order, identically on every rank);
  * each returning 0 on success, then copies the results back.  Synchronous on the host and not
  * graph-capturable (lrcnn_step runs eagerly with it).  Callbacks run on the thread that called
  * forward / backward / step. */

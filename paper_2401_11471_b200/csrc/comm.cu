@@ -341,10 +341,38 @@ int comm_allreduce_f64(Comm *c, double *buf, size_t n, cudaStream_t st, const ch
     static thread_local std::string e;
     if (c->world == 1 || n == 0) return 0;
     if (c->kind == 2) {
-        e = "the host-staged communicator has no fp64 all-reduce (training-mode BN with row sharding needs NCCL "
-            "or the loopback communicator)";
-        *err = e.c_str();
-        return 1;
+        // host-staged: an all-gather through the exchange callback (my sums to every peer, theirs from
+        // every peer), then the sum in rank order on the host (the same order on every rank)
+        const size_t bytes = n * sizeof(double);
+        const int W = c->world, me = c->rank;
+        std::vector<double *> slot(W, nullptr);
+        for (int p = 0; p < W; ++p) {
+            slot[p] = (double *)c->host_buf(1 + p, bytes);
+            if (!slot[p]) { e = "host staging: cudaMallocHost failed"; *err = e.c_str(); return 1; }
+        }
+        if (cudaMemcpyAsync(slot[me], buf, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) { e = "host staging: D2H failed"; *err = e.c_str(); return 1; }
+        std::vector<int> peer, send;
+        std::vector<void *> hp;
+        std::vector<size_t> by;
+        for (int p = 0; p < W; ++p) {
+            if (p == me) continue;
+            peer.push_back(p); send.push_back(1); hp.push_back(slot[me]); by.push_back(bytes);
+            peer.push_back(p); send.push_back(0); hp.push_back(slot[p]); by.push_back(bytes);
+        }
+        if (c->hx(c->user, (int)peer.size(), peer.data(), send.data(), hp.data(), by.data())) {
+            e = "host exchange callback failed (fp64 all-reduce)"; *err = e.c_str(); return 1;
+        }
+        double *acc = (double *)c->host_buf(0, bytes);
+        if (!acc) { e = "host staging: cudaMallocHost failed"; *err = e.c_str(); return 1; }
+        for (size_t i = 0; i < n; ++i) {
+            double v = 0.0;
+            for (int p = 0; p < W; ++p) v += slot[p][i];
+            acc[i] = v;
+        }
+        if (cudaMemcpyAsync(buf, acc, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) { e = "host staging: H2D failed"; *err = e.c_str(); return 1; }
+        return 0;
     }
     if (c->kind == 0) {
         NcclApi *api = nccl_api(e);

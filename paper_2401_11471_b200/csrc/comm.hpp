@@ -28,7 +28,8 @@ bool comm_graph_safe(const Comm *c);   // may the calls be captured into a CUDA 
 int comm_exchange(Comm *c, const std::vector<XferBuf> &xs, cudaStream_t st, const char **err);
 // in-place sum over ranks of n floats, ordered on `st`
 int comm_allreduce_f32(Comm *c, float *buf, size_t n, cudaStream_t st, const char **err);
-// in-place sum over ranks of n doubles (NCCL, loopback; the host-staged transport has none)
+// in-place sum over ranks of n doubles (NCCL, loopback; host-staged: an all-gather through the exchange
+// callback and a rank-ordered sum on the host)
 int comm_allreduce_f64(Comm *c, double *buf, size_t n, cudaStream_t st, const char **err);
 
 }  // namespace lrcnn

@@ -40,7 +40,8 @@ def _worker(rank, world, port, out_dir, case):
     x = WL.make_input(net, B, seed=xseed, bf16=bf)
     lab = WL.make_labels(net, B, seed=1 + (rank if kind == "dp" else 0))
     if kind == "rows":
-        plan = LB.Plan(net, B, mode="2ps", prec=prec, world=world, rank=rank, n_bands=2)
+        plan = LB.Plan(net, B, mode="2ps", prec=prec, world=world, rank=rank, n_bands=2,
+                       flags=case.get("flags", 0))
     else:
         plan = LB.Plan(net, B, mode="2ps", prec=prec, world=world, rank=rank, n_bands=2, flags=LB.FLAG_DP)
     comm = LB.Comm.host()
@@ -135,3 +136,28 @@ def test_dp_two_processes_host_comm_sum():
         compare_grads(g, g_sum, 1e-5, ("replica", r))
         for k in ("fc_w", "fc_b"):
             assert float(np.max(np.abs(head[k] - h_sum[k])) / np.max(np.abs(h_sum[k]))) <= 1e-5
+
+
+def test_bn_rows_two_processes_host_comm_vs_oracle():
+    """Training-mode BN with rows split over two real processes (zero-redundancy cuts, host-staged
+    communicator over gloo: the fp64 statistics sums gathered through the exchange callback and summed
+    in rank order): loss and every rank's gradients vs the fp64 oracle conditioned on the merged maps
+    (fp32, 1e-5)."""
+    from paper_2401_11471_b200 import lrcnn as LB
+    net = WL.resnet50(H=192, W=48, width_div=4, blocks=(2, 1, 1, 1), bn_train=True)
+    B = 2
+    case = {"net": net, "B": B, "prec": "fp32", "kind": "rows", "seed": 3, "flags": LB.FLAG_ZERO_REDUNDANCY}
+    res = _run(case)
+    params = WL.make_params(net, seed=3, bias_scale=0.1, gamma_spread=0.2)
+    x = WL.make_input(net, B, seed=3)
+    lab = WL.make_labels(net, B, seed=1)
+    _, loss_ref, _, _, _ = C.step(net, params, x, lab, 0.0)
+    plan_like = LB.Plan(net, B, mode="2ps", prec="fp32", n_bands=2)
+    ts = [x] + _merge(res, net, plan_like)
+    _, aux = validate_forward(net, params, ts, C.fp32_store, 1e-5)
+    loss_c, dzl, hg, _ = C.head_forward_backward(ts[-1], params["head"], lab)
+    g_ref = conditioned_grads(net, params, ts, aux, dzl)
+    for r, out in enumerate(res):
+        assert abs(out["loss"] - loss_ref) <= 1e-5 * abs(loss_ref), (r, out["loss"], loss_ref)
+        g, head = plan_like.unpack_grads(out["grads"])
+        compare_grads(g, g_ref, 1e-5, ("rank", r))
