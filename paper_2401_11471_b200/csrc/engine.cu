@@ -480,9 +480,14 @@ static lrcnn_status band_forward(Run &R, const Segment &S, int r, bool save_cach
             const TensorInfo &ti = P.t[t];
             int rows = S.a[r][t] - S.lo[r][t];
             if (rows <= 0) continue;
-            // cache[r-1] holds rows [lo_r, b_{r-1}) == [lo_r, a_r)
-            if ((st = copy_rows(R, ti, R.ws + ti.act_off, ti.cap, R.ws + ti.cache_off[r - 1], ti.cache_rows[r - 1],
-                                rows)) != LRCNN_OK) return st;
+            // cache[r-1] holds rows [lo_r, b_{r-1}) == [lo_r, a_r); a stashed tensor (full-width slot, BN)
+            // gets them at their rows of the slot (the BP walks the bands upward: band r-1 comes later)
+            const View dv = act_view(R, S, r, t);
+            const size_t rb = (size_t)ti.W * ti.Cp * R.E;
+            char *dst = (char *)dv.p + (size_t)(S.lo[r][t] - dv.base) * rb;
+            const size_t pitch = (size_t)dv.bs / ((size_t)ti.W * ti.Cp);
+            if ((st = copy_rows(R, ti, dst, pitch, R.ws + ti.cache_off[r - 1], ti.cache_rows[r - 1], rows)) != LRCNN_OK)
+                return st;
         }
     }
     // zero-redundancy: the last band reads rows [HI, hb) of every band tensor that rank+1 computed in

@@ -847,14 +847,19 @@ lrcnn_status build_plan(const lrcnn_net_desc *net, const lrcnn_plan_opts *opts, 
             for (int i : S.ops) S.bn_bp_recompute[i] = 1;
             bool any = false;
             for (int j : bns) {
-                const int c = P.op[j].in_t;
-                if (j == S.bn_tail || !inside[c] || c == S.out_t || P.t[c].cons.size() != 1) continue;
-                const size_t bytes = align_up(B * (size_t)P.t[c].H * rowbytes(c));
-                if (used + bytes > budget) continue;
-                S.bp_stash_off[c] = used;
-                S.bn_bp_recompute[P.t[c].producer] = 0;
-                used += bytes;
-                any = true;
+                if (j == S.bn_tail) continue;
+                // the BN input c (its sums / backward read it) and the BN output t (the next conv's input
+                // and the ReLU gate): with both stashed, the later sweeps recompute neither
+                for (int c : {P.op[j].in_t, P.op[j].out_t}) {
+                    if (!inside[c] || c == S.out_t) continue;
+                    if (c == P.op[j].in_t && P.t[c].cons.size() != 1) continue;
+                    const size_t bytes = align_up(B * (size_t)P.t[c].H * rowbytes(c));
+                    if (used + bytes > budget) continue;
+                    S.bp_stash_off[c] = used;
+                    S.bn_bp_recompute[P.t[c].producer] = 0;
+                    used += bytes;
+                    any = true;
+                }
             }
             if (!any) { S.bp_stash_off.clear(); S.bn_bp_recompute.clear(); }
             bp_stash_need = std::max(bp_stash_need, used);
