@@ -44,9 +44,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--hw", type=int, default=0)
     ap.add_argument("--mode", default="2ps", choices=["2ps", "overl", "column"])
-    ap.add_argument("--segments", default="pool",
-                    help="checkpoint segments (2PS-H): pool = after every pool (VGG) / stage (ResNet); none = "
-                         "whole-net 2PS; ResNet cut string, e.g. 3 = one checkpoint after conv3_x, p234 = stage")
+    ap.add_argument("--segments", default=None,
+                    help="checkpoint segments (2PS-H): pool = after every pool (VGG) / stage (ResNet, the default); "
+                         "none = whole-net 2PS; ResNet cut string, e.g. 3 = one checkpoint after conv3_x, p234 = "
+                         "stage; block = after every bottleneck (the --bn-train default: 3 BN levels per segment)")
     ap.add_argument("--n-bands", type=int, default=None,
                     help="bands of the largest segment (default: 4; 8 for the climate-scale C4 / C5, where "
                          "it meets the north star's >= 5x feature-map reduction vs layer-wise)")
@@ -150,6 +151,8 @@ CONFIGS = {   # (model, H, W, batch, description)
 
 
 def make_net(a):
+    if a.segments is None:
+        a.segments = "block" if getattr(a, "bn_train", False) and CONFIGS[a.config][0] == "resnet50" else "pool"
     model, H, W, _, _ = CONFIGS[a.config]
     if a.hw:
         H = W = a.hw
