@@ -25,6 +25,9 @@ def test_bn_chain_fp32_bands_and_segments():
     net["ops"][3]["seg_end"] = True
     check(net, 2, "fp32", ["2ps", "overl"], [{"n_bands": 2}, {"band_rows": 3}], bias=0.3, gspread=0.4,
           plain_grads=True, flags=LB.FLAG_ALLOW_OVERLAP_EXHAUSTION)
+    # 12 channels: padded to 16 on the device (padded channels must stay zero through the BN)
+    net = WL.bn_chain(H=13, W=9, C=3, ch=12, n=3, res_every=2)
+    check(net, 3, "fp32", ["column", "2ps"], [{"n_bands": 3}], bias=0.3, gspread=0.4, plain_grads=True)
 
 
 def check_bn_bf16(net, B, modes, kws, dzl_kind, flags=0):
