@@ -60,6 +60,7 @@ __device__ __forceinline__ void store8(bf16 *p, const float *v) {
 }
 
 constexpr int kRowsPer = 2;
+constexpr int kFwdRowsPer = 4;   // k_bn_fwd (two raw loads per row): more rows in flight
 
 __device__ __forceinline__ void coef8(const float *c, float *v) {
     const float4 a = *(const float4 *)c, b = *(const float4 *)(c + 4);
@@ -191,11 +192,11 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd(View in, View res, View o
     const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (v0 >= nv) return;
     const int g = v0 % G, xx = v0 / G;
-    for (int r0 = blockIdx.y * kRowsPer; r0 < nrows; r0 += gridDim.y * kRowsPer) {
-        Raw8<T> rv[kRowsPer], rr[kRowsPer];
-        long long off[kRowsPer];
+    for (int r0 = blockIdx.y * kFwdRowsPer; r0 < nrows; r0 += gridDim.y * kFwdRowsPer) {
+        Raw8<T> rv[kFwdRowsPer], rr[kFwdRowsPer];
+        long long off[kFwdRowsPer];
 #pragma unroll
-        for (int u = 0; u < kRowsPer; ++u) {
+        for (int u = 0; u < kFwdRowsPer; ++u) {
             const int ry = min(r0 + u, nrows - 1);   // (a duplicate of the last row is recomputed, not stored)
             const int bi = ry / rows, y = a + ry % rows;
             off[u] = bn_off(out, bi, y, xx) + g * 8;
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd(View in, View res, View o
         coef8(coef + g * 8, ca);
         coef8(coef + Cp + g * 8, cb);
 #pragma unroll
-        for (int u = 0; u < kRowsPer; ++u) {
+        for (int u = 0; u < kFwdRowsPer; ++u) {
             float v[8], r[8];
             unraw(rv[u], v);
             if (has_res) unraw(rr[u], r);
@@ -265,10 +266,10 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx,
     }
 }
 
-dim3 grid_rows(int nv, int nrows) {
+dim3 grid_rows(int nv, int nrows, int per = kRowsPer) {
     const int gx = (nv + kBnThreads - 1) / kBnThreads;
-    // about 8 blocks of 256 threads per SM in total, each striding over groups of kRowsPer rows
-    const int groups = (nrows + kRowsPer - 1) / kRowsPer;
+    // about 8 blocks of 256 threads per SM in total, each striding over groups of `per` rows
+    const int groups = (nrows + per - 1) / per;
     const int gy = std::max(1, std::min(std::min(groups, 65535), (148 * 8 + gx - 1) / gx));
     return dim3((unsigned)gx, (unsigned)gy);
 }
@@ -319,7 +320,7 @@ cudaError_t bn_fwd(int prec, const View &in, const View &res, const View &out, c
     if (n <= 0) return cudaSuccess;
     if (out.Cp % 8) return cudaErrorInvalidValue;
     const int hr = res.p != nullptr;
-    const dim3 grid = grid_rows(out.W * (out.Cp / 8), B * (b - a));
+    const dim3 grid = grid_rows(out.W * (out.Cp / 8), B * (b - a), kFwdRowsPer);
     if (prec) k_bn_fwd<bf16><<<grid, kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
     else k_bn_fwd<float><<<grid, kBnThreads, 0, st>>>(in, res, out, coef, relu, hr, a, b, B);
     return cudaGetLastError();
