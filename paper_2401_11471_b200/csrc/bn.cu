@@ -222,44 +222,46 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd(View in, View res, View o
     }
 }
 
-// write != 0: delta(src) rows are produced by this kernel alone (single writer) -- not read
-template <typename T>
-__global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx, View act, int gate, int write,
-                                                        const float *coef, int a, int b, int B, int cs) {
+// WRITE: delta(src) rows are produced by this kernel alone (single writer) -- not read; GATE: the input
+// has a ReLU (gate on write).  Specialised so the common case (a conv output: no gate, single writer)
+// holds two raw loads per row and keeps four rows in flight.
+template <typename T, bool GATE, bool WRITE, int RP>
+__global__ void __launch_bounds__(kBnThreads) k_bn_bwd(View dy, View x, View dx, View act, const float *coef, int a,
+                                                        int b, int B, int cs) {
     const int Cp = dx.Cp, G = Cp / 8, rows = b - a, nv = dx.W * G, nrows = B * rows;
     const int v0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (v0 >= nv) return;
     const int g = v0 % G, xx = v0 / G;
-    for (int r0 = blockIdx.y * kRowsPer; r0 < nrows; r0 += gridDim.y * kRowsPer) {
-        Raw8<T> rd[kRowsPer], rv[kRowsPer], ro[kRowsPer], rm[kRowsPer];
-        long long off[kRowsPer];
-        bool stat[kRowsPer];
+    for (int r0 = blockIdx.y * RP; r0 < nrows; r0 += gridDim.y * RP) {
+        Raw8<T> rd[RP], rv[RP], ro[RP], rm[RP];
+        long long off[RP];
+        bool stat[RP];
 #pragma unroll
-        for (int u = 0; u < kRowsPer; ++u) {
+        for (int u = 0; u < RP; ++u) {
             const int ry = min(r0 + u, nrows - 1);
             const int bi = ry / rows, y = a + ry % rows;
             off[u] = bn_off(dx, bi, y, xx) + g * 8;
             stat[u] = y >= cs;
             ldraw((const T *)dy.p + bn_off(dy, bi, y, xx) + g * 8, rd[u]);
             ldraw((const T *)x.p + bn_off(x, bi, y, xx) + g * 8, rv[u]);
-            if (!write) ldraw((const T *)dx.p + off[u], ro[u]);
-            if (gate) ldraw((const T *)act.p + bn_off(act, bi, y, xx) + g * 8, rm[u]);
+            if (!WRITE) ldraw((const T *)dx.p + off[u], ro[u]);
+            if (GATE) ldraw((const T *)act.p + bn_off(act, bi, y, xx) + g * 8, rm[u]);
         }
         float ca[8], cp[8], cq[8];
         coef8(coef + g * 8, ca);
         coef8(coef + 2 * Cp + g * 8, cp);
         coef8(coef + 3 * Cp + g * 8, cq);
 #pragma unroll
-        for (int u = 0; u < kRowsPer; ++u) {
+        for (int u = 0; u < RP; ++u) {
             float d[8], v[8], o[8], m[8];
             unraw(rd[u], d);
             unraw(rv[u], v);
-            if (!write) unraw(ro[u], o);
-            if (gate) unraw(rm[u], m);
+            if (!WRITE) unraw(ro[u], o);
+            if (GATE) unraw(rm[u], m);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const float dc = stat[u] ? fmaf(ca[k], d[k], fmaf(cq[k], v[k], cp[k])) : ca[k] * d[k];
-                o[k] = (gate && m[k] <= 0.f) ? 0.f : (write ? dc : o[k] + dc);
+                o[k] = (GATE && m[k] <= 0.f) ? 0.f : (WRITE ? dc : o[k] + dc);
             }
             if (r0 + u < nrows) store8((T *)dx.p + off[u], o);
         }
@@ -331,9 +333,18 @@ cudaError_t bn_bwd(int prec, const View &dy, const View &x, const View &dx, cons
     const long long n = (long long)B * (b - a) * dx.W * (dx.Cp / 8);
     if (n <= 0) return cudaSuccess;
     if (dx.Cp % 8) return cudaErrorInvalidValue;
-    const dim3 grid = grid_rows(dx.W * (dx.Cp / 8), B * (b - a));
-    if (prec) k_bn_bwd<bf16><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B, cs);
-    else k_bn_bwd<float><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, gate, write, coef, a, b, B, cs);
+    const int nv = dx.W * (dx.Cp / 8), nr = B * (b - a);
+#define LRCNN_BN_BWD(G_, W_, RP_)                                                                             \
+    do {                                                                                                      \
+        const dim3 grid = grid_rows(nv, nr, RP_);                                                             \
+        if (prec) k_bn_bwd<bf16, G_, W_, RP_><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, coef, a, b, B, cs); \
+        else k_bn_bwd<float, G_, W_, RP_><<<grid, kBnThreads, 0, st>>>(dy, x, dx, act, coef, a, b, B, cs);   \
+    } while (0)
+    if (!gate && write) LRCNN_BN_BWD(false, true, 4);
+    else if (!gate) LRCNN_BN_BWD(false, false, 2);
+    else if (write) LRCNN_BN_BWD(true, true, 2);
+    else LRCNN_BN_BWD(true, false, 2);
+#undef LRCNN_BN_BWD
     return cudaGetLastError();
 }
 
