@@ -544,17 +544,22 @@ def step_ranks(net, params, x, labels, lr, world, band_rows=None, n_bands=None):
 
 
 # ---------------------------------------------------------------- zero-redundancy G-rank simulation (f1)
-def _zr_band_fwd(net, shp, seg, band, held_in, cache, halo, params):
+def _zr_band_fwd(net, shp, seg, band, held_in, cache, halo, params, bn=None, stop_at=None, on_rows=None):
     """One band of a zero-redundancy rank: band[t] = (lo, a, b, hi); rows [lo, a) come from the band
-    above (cache), [a, b) are computed, [b, hi) are the halo from rank g+1 (halo)."""
+    above (cache), [a, b) are computed, [b, hi) are the halo from rank g+1 (halo).  bn / stop_at /
+    on_rows: as seg_forward (training-mode BN statistics sweeps)."""
     seg_in, ids, out = seg
     held = dict(held_in)
     B = held_in[seg_in][1].shape[0]
     for i in ids:
+        if stop_at is not None and i >= stop_at:
+            continue
         t = i + 1
         lo, a, b, hi = band[t]
-        new = _op_rows_fwd(net, i, held, params, a, b, shp)[0] if b > a else \
+        new = _op_rows_fwd(net, i, held, params, a, b, shp, True, bn)[0] if b > a else \
             np.zeros((B, shp[t][0], 0, shp[t][2]))
+        if on_rows is not None:
+            on_rows(t, a, new)
         parts = []
         if lo < a:
             clo, carr = cache[t]
@@ -571,7 +576,9 @@ def step_ranks_zr(net, params, x, labels, lr, world, band_rows=None, n_bands=Non
     8(f) f1; oracle.enumerate.enumerate_rank_zr): every row of every tensor is computed by one rank;
     rank g's last band reads the first rows of rank g+1 (a message after every rank's first band) and
     sends their delta back (a message after its first BP band, added into rank g+1's first band).
-    Returns (new_params, loss, grads, head_grads, z^L, message log)."""
+    Training-mode BN: every statistics / sums sweep is a whole sharded sweep (with its messages) and
+    the per-rank sums over the rows each rank computes are added over the ranks (the all-reduce).
+    Returns (new_params, loss, grads, head_grads, z^L, message log of the final sweeps)."""
     from oracle.enumerate import enumerate_rank_zr
     shp = C.out_hw(net)
     segs = segments(net)
@@ -580,9 +587,9 @@ def step_ranks_zr(net, params, x, labels, lr, world, band_rows=None, n_bands=Non
     log = []
     plans = [[enumerate_rank_zr(net, seg, world, g, band_rows, (n_bands or 1) if band_rows is None else None, shp)
               for g in range(world)] for seg in segs]
-    full_in = x                      # the segment input, assembled from the owners' rows (all ranks)
-    saved = []                       # per segment: per rank (input slab lo, slab, [held per band])
-    for s, seg in enumerate(segs):
+
+    def seg_fp(s, full_in, bn, stop_at=None, on_rows=None, log_on=True):
+        seg = segs[s]
         seg_in, ids, out = seg
         per = []
         for g in range(world):
@@ -593,50 +600,49 @@ def step_ranks_zr(net, params, x, labels, lr, world, band_rows=None, n_bands=Non
         helds = [[None] * len(plans[s][g][1]) for g in range(world)]
         # band 0 of every rank (bottom rank first: with one band a rank's only band is its last)
         msgs = {}
-        order = list(range(world - 1, -1, -1))
-        for g in order:
+        for g in range(world - 1, -1, -1):
             own, bands, _ = plans[s][g]
             N = len(bands)
             halo = {}
             if N == 1 and g + 1 < world:
                 halo = msgs[g + 1]
-            helds[g][0] = _zr_band_fwd(net, shp, seg, bands[0], {seg_in: per[g]}, {}, halo, params)
+            helds[g][0] = _zr_band_fwd(net, shp, seg, bands[0], {seg_in: per[g]}, {}, halo, params, bn, stop_at,
+                                       on_rows)
             if g > 0:   # my first rows the rank above reads
                 own_up, bands_up, _ = plans[s][g - 1]
                 m = {}
                 for i in ids:
                     t = i + 1
-                    if t == out:
+                    if t == out or t not in helds[g][0]:
                         continue
                     a0, a1 = own_up[t][1], bands_up[-1][t][3]
                     if a1 > a0:
                         lo, arr = helds[g][0][t]
                         m[t] = arr[:, :, a0 - lo:a1 - lo].copy()
                 msgs[g] = m
-                log.append(("fp", s, g, g - 1, sorted((t, v.shape[2]) for t, v in m.items())))
+                if log_on:
+                    log.append(("fp", s, g, g - 1, sorted((t, v.shape[2]) for t, v in m.items())))
         for g in range(world):
             own, bands, _ = plans[s][g]
             for r in range(1, len(bands)):
                 halo = msgs.get(g + 1, {}) if r == len(bands) - 1 else {}
-                helds[g][r] = _zr_band_fwd(net, shp, seg, bands[r], {seg_in: per[g]}, helds[g][r - 1], halo, params)
+                helds[g][r] = _zr_band_fwd(net, shp, seg, bands[r], {seg_in: per[g]}, helds[g][r - 1], halo, params,
+                                           bn, stop_at, on_rows)
         c, h, w = shp[out]
         y = np.zeros((B, c, h, w))
-        for g in range(world):
-            own, bands, (ol, oh) = plans[s][g]
-            for r, band in enumerate(bands):
-                lo, a, b, hi = band[out]
-                blo, arr = helds[g][r][out]
-                y[:, :, a:b] = arr[:, :, a - blo:b - blo]
-        saved.append((per, helds, msgs))
-        full_in = y
-    zl = full_in
-    loss, dzl, hg, _ = C.head_forward_backward(zl, params["head"], labels)
-    grads = [None] * len(net["ops"])
-    dout_full = np.asarray(dzl, dtype=np.float64)
-    for s in range(len(segs) - 1, -1, -1):
+        if stop_at is None:
+            for g in range(world):
+                own, bands, (ol, oh) = plans[s][g]
+                for r, band in enumerate(bands):
+                    lo, a, b, hi = band[out]
+                    blo, arr = helds[g][r][out]
+                    y[:, :, a:b] = arr[:, :, a - blo:b - blo]
+        return y, (per, helds, msgs)
+
+    def seg_bp(s, saved_s, dout_full, bn, bns, stop_at=None, on_delta=None, log_on=True):
         seg = segs[s]
         seg_in, ids, out = seg
-        per, helds, fmsgs = saved[s]
+        per, helds, fmsgs = saved_s
         d_ins = [np.zeros_like(per[g][1]) for g in range(world)]
         seg_grads = [{i: {} for i in ids if net["ops"][i]["kind"] == "conv"} for _ in range(world)]
         carry = [dict() for _ in range(world)]
@@ -660,11 +666,16 @@ def step_ranks_zr(net, params, x, labels, lr, world, band_rows=None, n_bands=Non
                 if r == 0 and g > 0 and t in dmsgs.get(g - 1, {}):
                     _add_rows(d, t, own[t][0], dmsgs[g - 1][t])
             for i in reversed(ids):
+                if stop_at is not None and i < stop_at:
+                    break
                 t = i + 1
                 lo, a, b, hi = band[t]
                 if b <= a:
                     continue
-                _op_rows_bwd(net, i, held, params, a, b, shp, _rows(d, t, a, b), d, seg_grads[g])
+                if stop_at is not None and i == stop_at:
+                    on_delta(held, a, b, _rows(d, t, a, b))
+                    break
+                _op_rows_bwd(net, i, held, params, a, b, shp, _rows(d, t, a, b), d, seg_grads[g], bn, bns)
             carry[g] = {}
             for i in ids:
                 t = i + 1
@@ -679,22 +690,73 @@ def step_ranks_zr(net, params, x, labels, lr, world, band_rows=None, n_bands=Non
                     if t != out and hi > b:
                         m[t] = _rows(d, t, b, hi).copy()
                 dmsgs[g] = m
-                log.append(("bp", s, g, g + 1, sorted((t, v.shape[2]) for t, v in m.items())))
+                if log_on:
+                    log.append(("bp", s, g, g + 1, sorted((t, v.shape[2]) for t, v in m.items())))
         for g in range(world):                       # every rank's last band first (BP order)
             N = len(plans[s][g][1])
             for r in range(N - 1, 0, -1):
                 bp_band(g, r)
         for g in range(world):                       # then every rank's first band (top rank first)
             bp_band(g, 0)
-        for g in range(world):
-            for i, v in seg_grads[g].items():
-                if not v:
-                    continue
-                grads[i] = v if grads[i] is None else {k: grads[i][k] + v[k] for k in v}
         c, h, w = shp[seg_in]
         d_full = np.zeros((B, c, h, w))
         for g in range(world):                       # the input delta back to its owners (added)
             r0 = per[g][0]
             d_full[:, :, r0:r0 + d_ins[g].shape[2]] += d_ins[g]
+        return d_full, seg_grads
+
+    def bn_ops(s):
+        return [i for i in segs[s][1] if net["ops"][i]["kind"] == "bn"]
+
+    full_in = x                      # the segment input, assembled from the owners' rows (all ranks)
+    saved, bn_all = [], []
+    for s in range(len(segs)):
+        bn = {}
+        for j in bn_ops(s):          # statistics sweeps (module docstring), summed over every rank's rows
+            src = net["ops"][j]["src"]
+            assert src != segs[s][0], "BN of a segment input under row sharding"
+            acc = {"rows": []}
+
+            def on_rows(t, a, rows, src=src, acc=acc):
+                if t == src:
+                    acc["rows"].append(rows)
+            seg_fp(s, full_in, bn, stop_at=j, on_rows=on_rows, log_on=False)
+            assert sum(r_.shape[2] for r_ in acc["rows"]) == shp[src][1], "every row on exactly one rank"
+            M = B * shp[src][1] * shp[src][2]
+            mean = sum(r_.sum(axis=(0, 2, 3)) for r_ in acc["rows"]) / M
+            var = sum(((r_ - mean[None, :, None, None]) ** 2).sum(axis=(0, 2, 3)) for r_ in acc["rows"]) / M
+            bn[j] = (mean, var)
+        y, saved_s = seg_fp(s, full_in, bn)
+        saved.append(saved_s)
+        bn_all.append(bn)
+        full_in = y
+    zl = full_in
+    loss, dzl, hg, _ = C.head_forward_backward(zl, params["head"], labels)
+    grads = [None] * len(net["ops"])
+    dout_full = np.asarray(dzl, dtype=np.float64)
+    for s in range(len(segs) - 1, -1, -1):
+        bn, bns = bn_all[s], {}
+        for j in reversed(bn_ops(s)):   # sums sweeps, summed over the ranks
+            op = net["ops"][j]
+            mean, var = bn[j]
+            acc = {"s1": np.zeros(len(mean)), "s2": np.zeros(len(mean))}
+
+            def on_delta(held, a, b, dt, j=j, op=op, mean=mean, var=var, acc=acc):
+                t = _rows(held, j + 1, a, b)
+                c = _rows(held, op["src"], a, b)
+                da = dt * (t > 0) if op["relu"] else dt
+                xh = (c - mean[None, :, None, None]) / np.sqrt(var + C.BN_EPS)[None, :, None, None]
+                acc["s1"] += da.sum(axis=(0, 2, 3))
+                acc["s2"] += (da * xh).sum(axis=(0, 2, 3))
+            seg_bp(s, saved[s], dout_full, bn, bns, stop_at=j, on_delta=on_delta, log_on=False)
+            bns[j] = (acc["s1"], acc["s2"])
+        d_full, seg_grads = seg_bp(s, saved[s], dout_full, bn, bns)
+        for g in range(world):
+            for i, v in seg_grads[g].items():
+                if not v:
+                    continue
+                grads[i] = v if grads[i] is None else {k: grads[i][k] + v[k] for k in v}
+        for j, (s1, s2) in bns.items():
+            grads[j] = {"beta": s1.copy(), "gamma": s2.copy()}
         dout_full = d_full
     return C.sgd(params, grads, hg, lr), loss, grads, hg, zl, log

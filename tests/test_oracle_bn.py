@@ -178,3 +178,23 @@ def test_per_band_statistics_is_not_batch_norm():
     plan = RC.Plan(net, "2ps", n_bands=3)
     zl, _, _ = RC.forward(plan, prm, x, per_band_stats=True)
     assert np.abs(zl - ts[-1]).max() > 1e-2 * np.abs(ts[-1]).max()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_zr_ranks_bn_equal_column(world):
+    """The oracle's zero-redundancy G-rank executor with training-mode BN: every statistics / sums sweep
+    is a whole sharded sweep and the per-rank sums over the rows each rank computes are added over the
+    ranks (the all-reduce of the CUDA path): loss and every gradient equal the column oracle (fp64)."""
+    net = WL.resnet50(H=96, W=16, width_div=16, blocks=(2, 1, 1, 1), bn_train=True)
+    B = 2
+    x = WL.make_input(net, B)
+    lab = WL.make_labels(net, B)
+    prm = WL.make_params(net, bias_scale=0.2, gamma_spread=0.3)
+    _, loss0, g0, _, _ = C.step(net, prm, x, lab, 0.1)
+    _, loss1, g1, _, _, log = RC.step_ranks_zr(net, prm, x, lab, 0.1, world, n_bands=2)
+    assert abs(loss1 - loss0) <= 1e-12 * abs(loss0)
+    for i, g in enumerate(g0):
+        if g is None:
+            continue
+        for k in g:
+            np.testing.assert_allclose(g1[i][k], g[k], rtol=1e-9, atol=1e-11 * np.abs(g[k]).max())
