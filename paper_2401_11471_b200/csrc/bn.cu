@@ -34,10 +34,6 @@ constexpr int kBnThreads = 256;
 __device__ __forceinline__ long long bn_off(const View &v, int b, int g, int x) {
     return (long long)b * v.bs + ((long long)(g - v.base) * v.W + x) * v.Cp;
 }
-__device__ __forceinline__ void load8(const float *p, float *v) {
-    const float4 a = *(const float4 *)p, b = *(const float4 *)(p + 4);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
 __device__ __forceinline__ void load8(const bf16 *p, float *v) {
     const uint4 u = *(const uint4 *)p;
     const __nv_bfloat162 *h = (const __nv_bfloat162 *)&u;
