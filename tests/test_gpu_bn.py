@@ -217,3 +217,10 @@ def test_bn_zero_redundancy_row_sharding(prec, world):
             for k in ("gamma", "beta"):
                 e = float(np.max(np.abs(g[i][k] - g_ref[i][k]) / np.maximum(tr[k], 1e-30)))
                 assert e <= tol, (rank, i, k, e)
+
+
+def test_bn_auto_segments_fp32():
+    """Training-mode BN with the sqrt(n) automatic checkpoints (LRCNN_FLAG_AUTO_SEGMENTS, f2): the plan's
+    own cuts, FP / BP stashes and tails, fp32 vs the plain oracle (segmentation never changes the result)."""
+    net = WL.resnet50(H=64, W=48, width_div=8, blocks=(2, 1, 1, 1), bn_train=True, segments="none")
+    check(net, 2, "fp32", ["2ps"], [{"n_bands": 3}], bias=0.1, gspread=0.2, flags=LB.FLAG_AUTO_SEGMENTS)

@@ -583,3 +583,23 @@ def test_bn_row_sharding_needs_zero_redundancy():
         LB.Plan(net, 2, mode="2ps", prec="fp32", n_bands=2, world=2, rank=0)
     net = WL.bn_chain(H=64, W=7, C=3, ch=8, n=4, res_every=2)
     LB.Plan(net, 2, mode="2ps", prec="fp32", n_bands=2, world=2, rank=0, flags=LB.FLAG_ZERO_REDUNDANCY)
+
+
+def test_bn_budget_planner_and_auto_segments():
+    """The budget-driven planner (f2) and sqrt(n) checkpoints plan training-mode BN nets (f4): the
+    smallest fitting band count is returned, and the automatic cuts are valid segment boundaries whose
+    plans equal the enumerator (BN ops read 1:1)."""
+    net = WL.resnet50(H=320, W=160, width_div=4, blocks=(2, 2, 2, 1), bn_train=True, segments="none")
+    B = 2
+    ws = {n: _ws(net, B, n) for n in range(1, 13)}
+    lo, hi = min(ws.values()), ws[1]
+    for budget in (hi, (lo + hi) // 2, lo):
+        p = LB.Plan.for_budget(net, B, budget, max_bands=12)
+        assert p.ws_bytes == ws[p.n_bands] <= budget
+        assert all(ws[m] > budget for m in range(1, p.n_bands))
+    p = LB.Plan(net, B, mode="2ps", prec="bf16", n_bands=3, flags=LB.FLAG_AUTO_SEGMENTS)
+    assert p.nsegs() > 1
+    cut = [dict(o) for o in net["ops"]]
+    for s in range(p.nsegs() - 1):
+        cut[p.seg(s)[1] - 1]["seg_end"] = True
+    _check_plan_vs_enum(dict(net, ops=cut), "2ps", n_bands=3)
