@@ -620,6 +620,14 @@ def main():
                                        if drl["bound"] == "tensor" else None),
                     frac_vs_burst=(drl["achieved"] / peaks.get("bf16_tflops", 1642.8)
                                    if drl["bound"] == "tensor" else None),
+                    # NVIDIA's nominal dense bf16 2.25 PFLOP/s (B200_PROFILING) scaled to the median SM clock of
+                    # the timed steps: the hardware ceiling at the clock the power cap left (the measured cuBLAS
+                    # peaks were taken at other clocks -- the sustained one at ~1357 MHz -- so a kernel at a
+                    # higher clock can exceed them)
+                    nominal_tflops_at_clock=(2250.0 * clocks["sm_mhz"] / 1965.0 if clocks.get("sm_mhz") else None),
+                    frac_vs_nominal_at_clock=(drl["achieved"] / (2250.0 * clocks["sm_mhz"] / 1965.0)
+                                              if drl["bound"] == "tensor" and clocks.get("sm_mhz") else None),
+                    exceeds_measured_peak=bool(drl["frac"] > 1.0),
                     ridge_flop_per_byte=ridge,
                     launches_per_step=dom["launches"] / prof_steps if dom else 0,
                     ms_per_step=dom["ms"] / prof_steps if dom else 0,
